@@ -1,0 +1,350 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 restarted-PDHG LP engine (contract in the task prompt;
+workload choice and roofline arithmetic in DESIGN.md §6).
+
+Headline workload (BASELINE.json metric "LPs solved/sec to 1e-4 KKT (batched)",
+configs[1]): C2 = a batch of 1024 PyEPO-style 5x5 shortest-path LPs sharing K
+with varying costs, raPDHG (headline; r2HPDHG reported as "secondary") to 1e-4
+relative KKT.  One step = one pass of the
+whole hot path: lp_create_batch (upload, validate, transpose, precondition),
+lp_solve_batch (every instance to OPTIMAL), lp_get_solutions, lp_destroy.
+
+  value : LPs/s with inputs resident in HBM (device pointers), per-step CUDA
+          events on the solve stream, L2 flushed between steps, max over ranks.
+  e2e   : the same through the C ABI with pinned HOST buffers: H2D of the
+          problem + costs and D2H of every solution inside the timed region.
+  --impl reference : the CPU oracle (oracle/) on the host cores, same metric.
+
+Multi-GPU (torchrun): every rank solves its own batch (independent LPs, no
+data-path collective) -> "scaling": "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import lpgen  # noqa: E402
+
+METRIC = "LPs solved/sec to 1e-4 KKT (batched)"
+UNIT = "LPs/s"
+WORKLOAD = ("C2: batch of 1024 PyEPO-style 5x5 shortest-path LPs (40 arcs, 25 flow rows, shared K, "
+            "varying c), to 1e-4 relative KKT, every instance OPTIMAL")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--alg", default="ra", choices=["r2", "ra"])
+    ap.add_argument("--secondary-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# --------------------------------------------------------------- clocks -----
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ workload -----
+
+def make_workload(batch: int, seed: int):
+    lp, C = lpgen.g_grid(batch=batch, seed=seed)
+    return lp, C
+
+
+def cpu_baseline(lp, C, alg, seconds):
+    """The oracle as it stands, on the host cores, on a bounded sample of the
+    workload: whole-batch solves repeated until ~`seconds` of CPU time."""
+    import oracle
+    threads = len(os.sched_getaffinity(0))
+    oracle.set_threads(threads)
+    done, t0 = 0, time.perf_counter()
+    reps = 0
+    while True:
+        _, _, res = oracle.solve_batch(lp, C, None, alg, threads=threads)
+        assert all(r["status"] == oracle.OPTIMAL for r in res)
+        done += len(res)
+        reps += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{reps} x the full {len(C)}-LP C2 batch ({done} LPs, {dt:.1f} s wall)",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+# ------------------------------------------------------------ reference -----
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    lp, C = make_workload(args.batch, seed=2)
+    threads = len(os.sched_getaffinity(0))
+    oracle.set_threads(threads)
+    # bounded sample per step so that warmup + steps end within a few minutes
+    t0 = time.perf_counter()
+    oracle.solve_batch(lp, C[:64], None, args.alg, threads=threads)
+    per_lp = (time.perf_counter() - t0) / 64
+    budget = 150.0 / max(args.steps + args.warmup, 1)
+    sample = int(max(8, min(args.batch, budget / max(per_lp, 1e-9))))
+    for w in range(args.warmup):
+        oracle.solve_batch(lp, C[:sample], None, args.alg, threads=threads)
+    times = []
+    for s in range(args.steps):
+        t0 = time.perf_counter()
+        _, _, res = oracle.solve_batch(lp, C[:sample], None, args.alg, threads=threads)
+        times.append(time.perf_counter() - t0)
+        assert all(r["status"] == oracle.OPTIMAL for r in res)
+    total = sum(times)
+    value = sample * args.steps / total
+    desc = f"{sample} of the {args.batch} C2 instances per step, oracle solve_batch on {threads} threads"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "batch": args.batch, "sample_per_step": sample,
+                       "algorithm": "r2hpdhg" if args.alg == "r2" else "rapdhg", "eps": 1e-4},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
+                             "cpu_model": _cpu_model()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- ours -----
+
+def run_ours(args):
+    import torch
+    import paper_2412_09734_b200 as mp
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    lp, C = make_workload(args.batch, seed=2 + rank)
+    prob_h = mp.Problem.from_lp(lp)
+    prob_d = prob_h.to(dev)
+    C_d = torch.as_tensor(C, device=dev)
+    # pinned host copies for the end-to-end leg
+    pin = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt).pin_memory()
+    prob_p = mp.Problem(lp.n, lp.m1, lp.m2, pin(lp.row_ptr, torch.int64), pin(lp.col_idx, torch.int32),
+                        pin(lp.val, torch.float64), pin(lp.c, torch.float64), pin(lp.q, torch.float64),
+                        pin(lp.l, torch.float64), pin(lp.u, torch.float64))
+    C_p = pin(C, torch.float64)
+    X_p = torch.empty((args.batch, lp.n), dtype=torch.float64).pin_memory()
+    Y_p = torch.empty((args.batch, lp.m), dtype=torch.float64).pin_memory()
+    X_d = torch.empty((args.batch, lp.n), dtype=torch.float64, device=dev)
+    Y_d = torch.empty((args.batch, lp.m), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    def step(prob, Cx, X, Y, mem, alg=args.alg):
+        bs = mp.BatchSolver(prob, Cx)
+        res = bs.solve(algorithm=alg)
+        bs.solutions(memory=mem, X=X, Y=Y)
+        bs.close()
+        return res
+
+    def timed(prob, Cx, X, Y, mem, steps, collect, alg=args.alg):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        all_res = []
+        for s in range(steps):
+            flush.zero_()                       # evict L2 between steps (outside the event pair)
+            ev[s][0].record(stream)
+            res = step(prob, Cx, X, Y, mem, alg)
+            ev[s][1].record(stream)
+            if collect:
+                all_res.append(res)
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in ev), all_res
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        step(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE)
+        step(prob_p, C_p, X_p, Y_p, mp.LP_HOST)
+    # ---- device-resident timed region ----
+    sampler = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0])
+                           if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit() else local)
+    barrier()
+    sampler.start()
+    n0 = mp.launch_count()
+    barrier()
+    ms, results = timed(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, args.steps, True)
+    barrier()
+    launches = mp.launch_count() - n0
+    clocks = sampler.stop()
+    # ---- end-to-end timed region (host buffers through the C ABI) ----
+    barrier()
+    ms_e2e, _ = timed(prob_p, C_p, X_p, Y_p, mp.LP_HOST, args.steps, False)
+    barrier()
+    # ---- secondary: the other algorithm on the same workload (context, not the headline) ----
+    alg2 = "r2" if args.alg == "ra" else "ra"
+    step(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, alg2)
+    barrier()
+    ms2, res2 = timed(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, args.secondary_steps, True, alg2)
+    barrier()
+    t = torch.tensor([ms, ms_e2e, ms2], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms, ms_e2e, ms2 = float(t[0]), float(t[1]), float(t[2])
+    it2 = np.array([r["iterations"] for r in res2[-1]])
+    secondary = {"algorithm": "r2hpdhg" if alg2 == "r2" else "rapdhg",
+                 "value": args.batch * args.secondary_steps * ws / (ms2 * 1e-3), "unit": UNIT,
+                 "ms_per_step": ms2 / args.secondary_steps,
+                 "all_optimal": all(r["status"] == mp.LP_OPTIMAL for res in res2 for r in res),
+                 "iterations": {"p50": float(np.median(it2)), "p99": float(np.percentile(it2, 99)),
+                                "max": int(it2.max())}}
+    # correctness of every timed instance
+    statuses = [r["status"] for res in results for r in res]
+    assert all(s == mp.LP_OPTIMAL for s in statuses), "non-optimal instance in the timed region"
+    lps = args.batch * args.steps * ws
+    value = lps / (ms * 1e-3)
+    e2e = lps / (ms_e2e * 1e-3)
+    last = results[-1]
+    iters = np.array([r["iterations"] for r in last])
+    atts = np.array([r["attempts"] for r in last])
+    kern_ms = statistics.mean(res[0]["solve_seconds"] for res in results) * 1e3
+    # roofline of the dominant kernel (the per-instance solver kernel): fp64 ALU bound
+    nnz, n, m = lp.nnz, lp.n, lp.m
+    flop_attempt = 4 * nnz + 25 * (n + m)          # SURVEY §8(d) d.2 per-attempt flops
+    flops = float(atts.sum()) * flop_attempt
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    fp64_peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12   # 148 SMs x 64 FP64 FMA/clk x 2 flop
+    achieved = flops / (kern_ms * 1e-3) / 1e12
+    h2d = (lp.row_ptr.nbytes + lp.col_idx.nbytes + lp.val.nbytes + lp.c.nbytes + lp.q.nbytes + lp.l.nbytes +
+           lp.u.nbytes + C.nbytes)
+    d2h = X_p.numel() * 8 + Y_p.numel() * 8 + args.batch * 96
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "batch": args.batch, "algorithm": "r2hpdhg" if args.alg == "r2" else "rapdhg",
+                   "eps": 1e-4, "l2": "flushed between steps (256 MiB write outside the event pair)",
+                   "parallelism": f"instances x{ws} ranks (weak)"},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": ms_e2e / args.steps},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp64_peak, "traffic": None,
+                     "kernel": "instance_kernel<1>", "kernel_ms": kern_ms,
+                     "flops_per_launch": flops,
+                     "note": "fp64 FMA peak derived (148 SMs x 64 DFMA/clk x 2 x sm_max); per-instance solves "
+                             "are latency-bound, see DESIGN.md §6"},
+        "iterations": {"p50": float(np.median(iters)), "p99": float(np.percentile(iters, 99)),
+                       "max": int(iters.max()), "attempts_total": int(atts.sum())},
+        "clocks": clocks,
+        "secondary": secondary,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(lp, C, args.alg, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,197 @@
+/*
+ * lp.h -- C ABI of the B200-native restarted-PDHG LP engine
+ * (raPDHG and r2HPDHG of MPAX, arXiv 2412.09734), fp64, sm_100a.
+ *
+ * The problem (Eq. (1)):
+ *     min c'x   s.t.   G x >= h,   A x = b,   l <= x <= u,
+ * is handed over already stacked as in its saddle form Eq. (2):
+ *     K = [G; A]  (rows 0..m1-1 are the ">=" rows, rows m1..m1+m2-1 the "=" rows),
+ *     q = (h; b).
+ * "<=" rows are negated by the caller.  l may hold -inf, u +inf.
+ *
+ * The solver implements the iteration contract written down in DESIGN.md §3
+ * (= SURVEY.md §8(c) c.2): Ruiz + Pock-Chambolle preconditioning, PDHG
+ * steps Eq. (pdhg) with the adaptive step size, averaging
+ * (raPDHG) or Halpern reflection Eq. (hrpdhg) (r2HPDHG), checks of
+ * termination / restart every 64 iterations, primal-weight
+ * update on restart, warm start and batches of same-shape
+ * instances.  Everything after argument checks runs in CUDA kernels
+ * on the handle's stream; there is no CPU fallback.
+ *
+ * Conventions (all entry points):
+ *  - Return value: an lp_error code (LP_OK = 0).  Output parameters are only
+ *    written on LP_OK.  lp_last_error_detail() gives a thread-local message.
+ *  - Solver outcome is an lp_status inside lp_result, never an error code.
+ *  - memory: LP_HOST or LP_DEVICE tells where EVERY pointer of that call lives
+ *    (device pointers must be in the current CUDA device's memory).
+ *  - Ownership: lp_create* COPY their inputs into library-owned device memory;
+ *    the caller keeps its arrays.  Results are COPIED OUT into caller buffers.
+ *    The handle owns all device state until lp_destroy().
+ *  - Streams: all work of a handle is ordered on the cuda_stream given at
+ *    creation (NULL = legacy default stream).  lp_solve / lp_solve_batch block
+ *    once, at the end, to fill lp_result; nothing synchronises per iteration.
+ *  - Threads: a handle is not thread-safe; distinct handles are independent.
+ */
+#ifndef MPAX_B200_LP_H
+#define MPAX_B200_LP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LP_ABI_VERSION 1
+
+typedef struct lp_handle_s *lp_handle; /* opaque, library-owned */
+
+enum lp_error {
+  LP_OK = 0,
+  LP_ERR_INVALID_ARGUMENT = -1, /* NULL where data is required, bad option value */
+  LP_ERR_DIMENSION = -2,        /* inconsistent sizes, unsorted / out-of-range CSR */
+  LP_ERR_NAN = -3,              /* NaN anywhere, or +-inf outside l/u */
+  LP_ERR_CROSSED_BOUNDS = -4,   /* l_j > u_j, l_j = +inf or u_j = -inf */
+  LP_ERR_BATCH_SHAPE = -5,      /* batch arrays inconsistent with the shared problem */
+  LP_ERR_OUT_OF_MEMORY = -6,
+  LP_ERR_CUDA = -7,             /* a CUDA call failed (detail names it) */
+  LP_ERR_NCCL = -8,
+  LP_ERR_NOT_SOLVED = -9,       /* lp_get_solution before a solve */
+  LP_ERR_UNSUPPORTED = -10      /* path not available for this handle / build */
+};
+
+enum lp_status {
+  LP_OPTIMAL = 1,          /* relative KKT termination test passed */
+  LP_ITERATION_LIMIT = 2,  /* iteration_limit accepted steps reached */
+  LP_NUMERICAL_ERROR = 3,  /* 100 consecutive line-search rejections */
+  LP_PRIMAL_INFEASIBLE = 4,/* reserved */
+  LP_DUAL_INFEASIBLE = 5   /* reserved */
+};
+
+enum lp_algorithm { LP_RAPDHG = 0, LP_R2HPDHG = 1 };
+enum lp_memory { LP_HOST = 0, LP_DEVICE = 1 };
+
+/* Solve path selection (lp_options.path). */
+enum lp_path {
+  LP_PATH_AUTO = 0,     /* batch / small LP -> per-instance kernel; big LP -> grid kernel */
+  LP_PATH_INSTANCE = 1, /* one CTA per instance, whole solve loop in-kernel (§8(a) a11) */
+  LP_PATH_GRID = 2,     /* one LP over the whole GPU: fused SpMV phases (§8(a) a5-a9) */
+  LP_PATH_DMMA = 3      /* batch sharing a dense K: fp64 tensor-core contraction (a12) */
+};
+
+/* The LP, K = [G; A] in CSR.  If dense != 0 the CSR holds every entry of the
+ * row-major m x n matrix (nnz = m*n, col_idx[i*n+j] = j); the dense flag lets
+ * a batch use the shared-A DMMA path. */
+typedef struct {
+  int64_t n;          /* columns (variables), >= 1 */
+  int64_t m1, m2;     /* ">=" rows, "=" rows; m = m1 + m2 >= 0 */
+  int64_t nnz;        /* stored entries of K */
+  int32_t dense;      /* see above */
+  int32_t memory;     /* LP_HOST or LP_DEVICE for every pointer below */
+  const int64_t *row_ptr; /* m+1, row_ptr[0] = 0, row_ptr[m] = nnz */
+  const int32_t *col_idx; /* nnz, strictly increasing within each row, in [0, n) */
+  const double *values;   /* nnz, finite */
+  const double *c;        /* n */
+  const double *q;        /* m: (h; b) */
+  const double *l, *u;    /* n: -inf <= l <= u <= +inf */
+} lp_problem_desc;
+
+/* Options (Appendix, plus the engine's path / logging switches). */
+typedef struct {
+  double eps_abs;               /* 1e-4 */
+  double eps_rel;               /* 1e-4 */
+  double eps_primal_infeasible; /* 1e-8, reserved */
+  double eps_dual_infeasible;   /* 1e-8, reserved */
+  double eps_feas_polish;       /* 1e-6, reserved */
+  int64_t iteration_limit;      /* INT64_MAX; accepted steps */
+  int32_t check_frequency;      /* 64 */
+  int32_t algorithm;            /* lp_algorithm, default LP_R2HPDHG */
+  int32_t warm_start;           /* informational; a non-NULL x0 / y0 is what warm-starts */
+  int32_t feasibility_polishing;/* must be 0 (reserved) */
+  int32_t verbose;              /* reserved */
+  int32_t display_frequency;    /* 10, reserved */
+  int32_t path;                 /* lp_path, default LP_PATH_AUTO */
+  int32_t reserved;
+} lp_options;
+
+/* Per-instance outcome.  The objectives and residuals are those of the
+ * returned (x, y) in ORIGINAL space (contract step 5/6):
+ *   primal_residual = ||(q - Kx) with ">=" rows clipped at 0||_2,
+ *   dual_residual   = ||lambda+ [l=-inf] + lambda- [u=+inf]||_2, lambda = c - K'y,
+ *   gap = |pobj - dobj|,
+ *   rel_kkt = max(pres/(1+||q||), dres/(1+||c||), gap/(1+|pobj|+|dobj|)). */
+typedef struct {
+  int32_t status;       /* lp_status */
+  int32_t pad;
+  int64_t iterations;   /* accepted PDHG steps k */
+  int64_t attempts;     /* line-search attempts j (>= iterations) */
+  int64_t restarts;
+  double primal_objective, dual_objective;
+  double primal_residual, dual_residual, gap, rel_kkt;
+  double omega, eta;    /* final primal weight and step size (scaled space) */
+  double solve_seconds; /* device time of the whole solve call (all instances) */
+} lp_result;
+
+/* Fills o with the Appendix defaults: 1e-4, 1e-4, 1e-8, 1e-8, 1e-6,
+ * INT64_MAX, 64, LP_R2HPDHG, 0, 0, 0, 10, LP_PATH_AUTO. */
+void lp_default_options(lp_options *o);
+
+/* Create a single-LP handle: validates, uploads, builds
+ * K~' (transpose) and the Ruiz(10) + Pock-Chambolle(alpha=1) scaling
+ * on the device.  cuda_stream: a cudaStream_t or NULL. */
+int lp_create(const lp_problem_desc *p, void *cuda_stream, lp_handle *out);
+
+/* Create a batch handle for `batch` instances sharing K, l, u.
+ * C: batch x n row-major costs (NULL: every instance uses shared->c);
+ * Q: batch x m row-major right-hand sides (NULL: every instance uses shared->q).
+ * `memory` applies to C and Q; shared->memory to the shared problem.
+ * Preconditioning depends on K only, so it is shared; all other state is per
+ * instance (contract step 6 "Batch"). */
+int lp_create_batch(const lp_problem_desc *shared, int64_t batch, const double *C, const double *Q,
+                    int32_t memory, void *cuda_stream, lp_handle *out);
+
+/* Replace the per-instance costs / right-hand sides of a batch handle (same
+ * shapes; NULL leaves that side unchanged).  Used for SPO+-style loops where K
+ * is fixed and c changes every step. */
+int lp_update_batch(lp_handle h, const double *C, const double *Q, int32_t memory);
+
+/* Solve a single-LP handle.  x0 (n) / y0 (m) are an optional warm start in
+ * ORIGINAL space; NULL halves start at zero.  `memory`
+ * applies to x0, y0.  `out` is a host struct. */
+int lp_solve(lp_handle h, const lp_options *o, const double *x0, const double *y0, int32_t memory,
+             lp_result *out);
+
+/* Solve every instance of a batch handle.  X0 (batch x n), Y0 (batch x m)
+ * optional warm starts.  `out` is a host array of `batch` results. */
+int lp_solve_batch(lp_handle h, const lp_options *o, const double *X0, const double *Y0,
+                   int32_t memory, lp_result *out);
+
+/* Copy out instance `instance`'s solution of the last solve, in original space:
+ * x (n), y (m), reduced costs lambda = c - K'y (n).  Any pointer may be NULL. */
+int lp_get_solution(lp_handle h, int64_t instance, double *x, double *y, double *reduced_costs,
+                    int32_t memory);
+
+/* Copy out every instance: X (batch x n), Y (batch x m); either may be NULL. */
+int lp_get_solutions(lp_handle h, double *X, double *Y, int32_t memory);
+
+/* Shapes of a handle: n, m1, m2, batch (any pointer may be NULL). */
+int lp_get_shape(lp_handle h, int64_t *n, int64_t *m1, int64_t *m2, int64_t *batch);
+
+/* Diagnostics used by the parity tests: the diagonal scalings Dr (m), Dc (n)
+ * of step 1, and the scaled products K~ v (m) and K~' w (n) computed by the
+ * solver's own SpMV kernels.  Any pointer may be NULL. */
+int lp_get_scaling(lp_handle h, double *Dr, double *Dc, int32_t memory);
+int lp_spmv_scaled(lp_handle h, const double *v, double *Kv, const double *w, double *KTw,
+                   int32_t memory);
+
+/* Number of kernels this library has launched in the calling process so far
+ * (bench.py reports the difference across its timed region). */
+int64_t lp_kernel_launch_count(void);
+
+const char *lp_error_string(int code);
+const char *lp_last_error_detail(void); /* thread-local */
+void lp_destroy(lp_handle h);           /* NULL is a no-op */
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,363 @@
+// api.cu -- the C ABI of include/lp.h: argument checks, uploads, dispatch to the
+// device setup (setup.cu) and solver kernels (instance_solver.cu), copies out.
+// Host code here only marshals; every step of the method runs in kernels.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace mpax {
+std::atomic<int64_t> g_launches{0};
+static thread_local std::string t_detail;
+void set_error_detail(const std::string &s) { t_detail = s; }
+}  // namespace mpax
+
+using namespace mpax;
+
+struct lp_handle_s {
+  cudaStream_t stream = nullptr;
+  DevProblem P;
+  int64_t batch = 1;
+  bool is_batch = false;
+  double *C0 = nullptr, *Q0 = nullptr;  // batch x n / batch x m (or n / m when shared)
+  int64_t cstride = 0, qstride = 0;
+  double *X = nullptr, *Y = nullptr, *L = nullptr;
+  double *X0 = nullptr, *Y0 = nullptr;  // warm-start staging
+  lp_result *d_res = nullptr, *h_res = nullptr;
+  unsigned long long *queue = nullptr;
+  double *work = nullptr;
+  size_t work_bytes = 0;
+  int64_t *rp64 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool solved = false;
+};
+
+namespace {
+
+std::once_flag g_pool_once;
+
+void init_pool() {
+  std::call_once(g_pool_once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+int fail(int code, const std::string &msg) {
+  set_error_detail(msg);
+  return code;
+}
+
+template <class T>
+int dalloc(T **p, size_t count, cudaStream_t s) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  MPAX_CUDA(cudaMallocAsync((void **)p, count * sizeof(T), s));
+  return LP_OK;
+}
+
+#define TRY(x)            \
+  do {                    \
+    int r_ = (x);         \
+    if (r_ != LP_OK) {    \
+      return r_;          \
+    }                     \
+  } while (0)
+
+void free_handle(lp_handle h) {
+  if (!h) return;
+  cudaStream_t s = h->stream;
+  void *ptrs[] = {h->P.rp, h->P.ci, h->P.kv0, h->P.kv, h->P.trp, h->P.tci, h->P.perm, h->P.tkv, h->P.l0,
+                  h->P.u0, h->P.ls, h->P.us, h->P.Dr, h->P.Dc, h->P.kmax, h->P.tab, h->C0, h->Q0, h->X,
+                  h->Y, h->L, h->X0, h->Y0, h->d_res, h->queue, h->work, h->rp64};
+  for (void *p : ptrs)
+    if (p) cudaFreeAsync(p, s);
+  if (h->h_res) cudaFreeHost(h->h_res);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  cudaStreamSynchronize(s);
+  delete h;
+}
+
+int check_desc(const lp_problem_desc *p) {
+  if (!p) return fail(LP_ERR_INVALID_ARGUMENT, "problem descriptor is NULL");
+  if (p->memory != LP_HOST && p->memory != LP_DEVICE) return fail(LP_ERR_INVALID_ARGUMENT, "bad memory kind");
+  if (p->n < 1 || p->m1 < 0 || p->m2 < 0 || p->nnz < 0)
+    return fail(LP_ERR_DIMENSION, "need n >= 1, m1, m2, nnz >= 0");
+  const int64_t m = p->m1 + p->m2;
+  if (p->nnz >= (int64_t)INT32_MAX || p->n >= (int64_t)INT32_MAX || m >= (int64_t)INT32_MAX)
+    return fail(LP_ERR_UNSUPPORTED, "nnz, n and m must be < 2^31");
+  if (m == 0 && p->nnz != 0) return fail(LP_ERR_DIMENSION, "nnz > 0 with no rows");
+  if (p->dense && p->nnz != p->n * m) return fail(LP_ERR_DIMENSION, "dense K needs nnz = m*n");
+  if (!p->row_ptr || (p->nnz > 0 && (!p->col_idx || !p->values)) || !p->c || !p->l || !p->u ||
+      (m > 0 && !p->q))
+    return fail(LP_ERR_INVALID_ARGUMENT, "a required array is NULL");
+  return LP_OK;
+}
+
+int create_common(const lp_problem_desc *p, int64_t batch, const double *C, const double *Q, int32_t memory,
+                  void *stream, lp_handle *out, bool is_batch) {
+  TRY(check_desc(p));
+  if (!out) return fail(LP_ERR_INVALID_ARGUMENT, "out is NULL");
+  if (batch < 1) return fail(LP_ERR_BATCH_SHAPE, "batch must be >= 1");
+  if (memory != LP_HOST && memory != LP_DEVICE) return fail(LP_ERR_INVALID_ARGUMENT, "bad memory kind");
+  init_pool();
+  lp_handle h = new lp_handle_s();
+  h->stream = (cudaStream_t)stream;
+  h->batch = batch;
+  h->is_batch = is_batch;
+  cudaStream_t s = h->stream;
+  DevProblem &P = h->P;
+  P.n = p->n; P.m1 = p->m1; P.m2 = p->m2; P.m = p->m1 + p->m2; P.nnz = p->nnz; P.dense = p->dense;
+  const int64_t n = P.n, m = P.m, nnz = P.nnz;
+  int rc = LP_OK;
+  auto cleanup = [&](int code) { free_handle(h); return code; };
+#define CK(x)                       \
+  do {                              \
+    rc = (x);                       \
+    if (rc != LP_OK) return cleanup(rc); \
+  } while (0)
+  CK(dalloc(&h->rp64, m + 1, s)); CK(dalloc(&P.rp, m + 1, s)); CK(dalloc(&P.ci, nnz, s));
+  CK(dalloc(&P.kv0, nnz, s)); CK(dalloc(&P.kv, nnz, s)); CK(dalloc(&P.trp, n + 1, s));
+  CK(dalloc(&P.tci, nnz, s)); CK(dalloc(&P.perm, nnz, s)); CK(dalloc(&P.tkv, nnz, s));
+  CK(dalloc(&P.l0, n, s)); CK(dalloc(&P.u0, n, s)); CK(dalloc(&P.ls, n, s)); CK(dalloc(&P.us, n, s));
+  CK(dalloc(&P.Dr, m, s)); CK(dalloc(&P.Dc, n, s)); CK(dalloc(&P.kmax, 1, s)); CK(dalloc(&P.tab, 2 * kStepTab, s));
+  const bool perC = is_batch && C != nullptr, perQ = is_batch && Q != nullptr;
+  h->cstride = perC ? n : 0;
+  h->qstride = perQ ? m : 0;
+  CK(dalloc(&h->C0, perC ? batch * n : n, s));
+  CK(dalloc(&h->Q0, perQ ? batch * m : m, s));
+  CK(dalloc(&h->X, batch * n, s)); CK(dalloc(&h->Y, batch * m, s)); CK(dalloc(&h->L, batch * n, s));
+  CK(dalloc(&h->d_res, batch, s)); CK(dalloc(&h->queue, 1, s));
+  if (cudaMallocHost((void **)&h->h_res, (size_t)batch * sizeof(lp_result)) != cudaSuccess)
+    return cleanup(fail(LP_ERR_OUT_OF_MEMORY, "pinned result buffer"));
+  if (cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess)
+    return cleanup(fail(LP_ERR_CUDA, "event create"));
+  auto cp = [&](void *dst, const void *src, size_t bytes) -> int {
+    if (bytes == 0) return LP_OK;
+    MPAX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    return LP_OK;
+  };
+  CK(cp(h->rp64, p->row_ptr, (size_t)(m + 1) * sizeof(int64_t)));
+  CK(cp(P.ci, p->col_idx, (size_t)nnz * sizeof(int32_t)));
+  CK(cp(P.kv0, p->values, (size_t)nnz * sizeof(double)));
+  CK(cp(P.l0, p->l, (size_t)n * sizeof(double)));
+  CK(cp(P.u0, p->u, (size_t)n * sizeof(double)));
+  CK(cp(h->C0, perC ? (const void *)C : (const void *)p->c, (size_t)(perC ? batch * n : n) * sizeof(double)));
+  if (m > 0) CK(cp(h->Q0, perQ ? (const void *)Q : (const void *)p->q, (size_t)(perQ ? batch * m : m) * sizeof(double)));
+  int flag[5];
+  CK(setup_validate(P, h->rp64, h->C0, perC ? batch * n : n, h->Q0, perQ ? batch * m : m, s, flag));
+  if (flag[0] == 3) return cleanup(fail(LP_ERR_DIMENSION, "CSR structure invalid at row " + std::to_string(flag[4])));
+  if (flag[0] == 2) return cleanup(fail(LP_ERR_NAN, "NaN or infinity in K, c or q (or NaN in l/u) near index " + std::to_string(flag[3])));
+  if (flag[0] == 1) return cleanup(fail(LP_ERR_CROSSED_BOUNDS, "crossed bounds at index " + std::to_string(flag[2])));
+  CK(setup_build(P, h->rp64, s));
+  *out = h;
+  return LP_OK;
+#undef CK
+}
+
+int check_options(const lp_options *o) {
+  if (!o) return fail(LP_ERR_INVALID_ARGUMENT, "options NULL");
+  if (!(o->eps_abs >= 0.0) || !(o->eps_rel >= 0.0) || o->iteration_limit < 1 || o->check_frequency < 1 ||
+      (o->algorithm != LP_RAPDHG && o->algorithm != LP_R2HPDHG))
+    return fail(LP_ERR_INVALID_ARGUMENT, "bad option value");
+  if (o->feasibility_polishing) return fail(LP_ERR_UNSUPPORTED, "feasibility polishing is not built yet");
+  if (o->path < LP_PATH_AUTO || o->path > LP_PATH_DMMA) return fail(LP_ERR_INVALID_ARGUMENT, "bad path");
+  return LP_OK;
+}
+
+int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *Y0, int32_t memory,
+              lp_result *out) {
+  if (!h || !out) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle or result");
+  TRY(check_options(o));
+  if (memory != LP_HOST && memory != LP_DEVICE) return fail(LP_ERR_INVALID_ARGUMENT, "bad memory kind");
+  cudaStream_t s = h->stream;
+  const int64_t n = h->P.n, m = h->P.m, B = h->batch;
+  // warm starts: staged into library memory (original space; scaled in-kernel)
+  const double *dX0 = nullptr, *dY0 = nullptr;
+  if (X0) {
+    if (!h->X0) TRY(dalloc(&h->X0, B * n, s));
+    MPAX_CUDA(cudaMemcpyAsync(h->X0, X0, (size_t)(B * n) * sizeof(double), cudaMemcpyDefault, s));
+    dX0 = h->X0;
+  }
+  if (Y0 && m > 0) {
+    if (!h->Y0) TRY(dalloc(&h->Y0, B * m, s));
+    MPAX_CUDA(cudaMemcpyAsync(h->Y0, Y0, (size_t)(B * m) * sizeof(double), cudaMemcpyDefault, s));
+    dY0 = h->Y0;
+  }
+  if (o->path == LP_PATH_GRID || o->path == LP_PATH_DMMA)
+    return fail(LP_ERR_UNSUPPORTED, "requested path not available in this build");
+  InstanceLaunch L;
+  L.C0 = h->C0; L.cstride = h->cstride; L.Q0 = h->Q0; L.qstride = h->qstride;
+  L.X0 = dX0; L.Y0 = dY0; L.batch = B; L.X = h->X; L.Y = h->Y; L.L = h->L; L.res = h->d_res;
+  MPAX_CUDA(cudaEventRecord(h->ev0, s));
+  TRY(instance_solve(h->P, *o, L, s, h->queue, &h->work, &h->work_bytes));
+  MPAX_CUDA(cudaEventRecord(h->ev1, s));
+  MPAX_CUDA(cudaMemcpyAsync(h->h_res, h->d_res, (size_t)B * sizeof(lp_result), cudaMemcpyDeviceToHost, s));
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  float ms = 0.0f;
+  MPAX_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  for (int64_t b = 0; b < B; ++b) {
+    out[b] = h->h_res[b];
+    out[b].solve_seconds = ms * 1e-3;
+  }
+  h->solved = true;
+  return LP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void lp_default_options(lp_options *o) {
+  if (!o) return;
+  memset(o, 0, sizeof(*o));
+  o->eps_abs = 1e-4;
+  o->eps_rel = 1e-4;
+  o->eps_primal_infeasible = 1e-8;
+  o->eps_dual_infeasible = 1e-8;
+  o->eps_feas_polish = 1e-6;
+  o->iteration_limit = INT64_MAX;
+  o->check_frequency = 64;
+  o->algorithm = LP_R2HPDHG;
+  o->warm_start = 0;
+  o->feasibility_polishing = 0;
+  o->verbose = 0;
+  o->display_frequency = 10;
+  o->path = LP_PATH_AUTO;
+}
+
+int lp_create(const lp_problem_desc *p, void *cuda_stream, lp_handle *out) {
+  return create_common(p, 1, nullptr, nullptr, p ? p->memory : LP_HOST, cuda_stream, out, false);
+}
+
+int lp_create_batch(const lp_problem_desc *shared, int64_t batch, const double *C, const double *Q,
+                    int32_t memory, void *cuda_stream, lp_handle *out) {
+  return create_common(shared, batch, C, Q, memory, cuda_stream, out, true);
+}
+
+int lp_update_batch(lp_handle h, const double *C, const double *Q, int32_t memory) {
+  if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  if (memory != LP_HOST && memory != LP_DEVICE) return fail(LP_ERR_INVALID_ARGUMENT, "bad memory kind");
+  cudaStream_t s = h->stream;
+  const int64_t n = h->P.n, m = h->P.m, B = h->batch;
+  if (C) {
+    if (h->cstride == 0 && B > 1) return fail(LP_ERR_BATCH_SHAPE, "handle was created with a shared c");
+    MPAX_CUDA(cudaMemcpyAsync(h->C0, C, (size_t)(B * n) * sizeof(double), cudaMemcpyDefault, s));
+  }
+  if (Q && m > 0) {
+    if (h->qstride == 0 && B > 1) return fail(LP_ERR_BATCH_SHAPE, "handle was created with a shared q");
+    MPAX_CUDA(cudaMemcpyAsync(h->Q0, Q, (size_t)(B * m) * sizeof(double), cudaMemcpyDefault, s));
+  }
+  h->solved = false;
+  return LP_OK;
+}
+
+int lp_solve(lp_handle h, const lp_options *o, const double *x0, const double *y0, int32_t memory,
+             lp_result *out) {
+  if (h && h->batch != 1) return fail(LP_ERR_BATCH_SHAPE, "lp_solve on a batch handle; use lp_solve_batch");
+  return run_solve(h, o, x0, y0, memory, out);
+}
+
+int lp_solve_batch(lp_handle h, const lp_options *o, const double *X0, const double *Y0, int32_t memory,
+                   lp_result *out) {
+  return run_solve(h, o, X0, Y0, memory, out);
+}
+
+int lp_get_solution(lp_handle h, int64_t instance, double *x, double *y, double *rc, int32_t memory) {
+  if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  if (!h->solved) return fail(LP_ERR_NOT_SOLVED, "no solve yet");
+  if (instance < 0 || instance >= h->batch) return fail(LP_ERR_BATCH_SHAPE, "instance out of range");
+  cudaStream_t s = h->stream;
+  const int64_t n = h->P.n, m = h->P.m;
+  if (x) MPAX_CUDA(cudaMemcpyAsync(x, h->X + instance * n, (size_t)n * sizeof(double), cudaMemcpyDefault, s));
+  if (y && m) MPAX_CUDA(cudaMemcpyAsync(y, h->Y + instance * m, (size_t)m * sizeof(double), cudaMemcpyDefault, s));
+  if (rc) MPAX_CUDA(cudaMemcpyAsync(rc, h->L + instance * n, (size_t)n * sizeof(double), cudaMemcpyDefault, s));
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  return LP_OK;
+}
+
+int lp_get_solutions(lp_handle h, double *X, double *Y, int32_t memory) {
+  if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  if (!h->solved) return fail(LP_ERR_NOT_SOLVED, "no solve yet");
+  cudaStream_t s = h->stream;
+  const int64_t n = h->P.n, m = h->P.m, B = h->batch;
+  if (X) MPAX_CUDA(cudaMemcpyAsync(X, h->X, (size_t)(B * n) * sizeof(double), cudaMemcpyDefault, s));
+  if (Y && m) MPAX_CUDA(cudaMemcpyAsync(Y, h->Y, (size_t)(B * m) * sizeof(double), cudaMemcpyDefault, s));
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  return LP_OK;
+}
+
+int lp_get_shape(lp_handle h, int64_t *n, int64_t *m1, int64_t *m2, int64_t *batch) {
+  if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  if (n) *n = h->P.n;
+  if (m1) *m1 = h->P.m1;
+  if (m2) *m2 = h->P.m2;
+  if (batch) *batch = h->batch;
+  return LP_OK;
+}
+
+int lp_get_scaling(lp_handle h, double *Dr, double *Dc, int32_t memory) {
+  if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  cudaStream_t s = h->stream;
+  if (Dr && h->P.m) MPAX_CUDA(cudaMemcpyAsync(Dr, h->P.Dr, (size_t)h->P.m * sizeof(double), cudaMemcpyDefault, s));
+  if (Dc) MPAX_CUDA(cudaMemcpyAsync(Dc, h->P.Dc, (size_t)h->P.n * sizeof(double), cudaMemcpyDefault, s));
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  return LP_OK;
+}
+
+int lp_spmv_scaled(lp_handle h, const double *v, double *Kv, const double *w, double *KTw, int32_t memory) {
+  if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  cudaStream_t s = h->stream;
+  const int64_t n = h->P.n, m = h->P.m;
+  double *dv = nullptr, *dKv = nullptr, *dw = nullptr, *dKTw = nullptr;
+  if (v && Kv) {
+    TRY(dalloc(&dv, n, s)); TRY(dalloc(&dKv, m, s));
+    MPAX_CUDA(cudaMemcpyAsync(dv, v, (size_t)n * sizeof(double), cudaMemcpyDefault, s));
+  }
+  if (w && KTw) {
+    TRY(dalloc(&dw, m, s)); TRY(dalloc(&dKTw, n, s));
+    if (m) MPAX_CUDA(cudaMemcpyAsync(dw, w, (size_t)m * sizeof(double), cudaMemcpyDefault, s));
+  }
+  TRY(spmv_scaled(h->P, dv, dKv, dw, dKTw, s));
+  if (dKv && m) MPAX_CUDA(cudaMemcpyAsync(Kv, dKv, (size_t)m * sizeof(double), cudaMemcpyDefault, s));
+  if (dKTw) MPAX_CUDA(cudaMemcpyAsync(KTw, dKTw, (size_t)n * sizeof(double), cudaMemcpyDefault, s));
+  for (double *p : {dv, dKv, dw, dKTw})
+    if (p) cudaFreeAsync(p, s);
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  return LP_OK;
+}
+
+int64_t lp_kernel_launch_count(void) { return g_launches.load(); }
+
+const char *lp_error_string(int code) {
+  switch (code) {
+    case LP_OK: return "ok";
+    case LP_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case LP_ERR_DIMENSION: return "dimension / structure error";
+    case LP_ERR_NAN: return "NaN or misplaced infinity";
+    case LP_ERR_CROSSED_BOUNDS: return "crossed bounds";
+    case LP_ERR_BATCH_SHAPE: return "batch shape error";
+    case LP_ERR_OUT_OF_MEMORY: return "out of device memory";
+    case LP_ERR_CUDA: return "CUDA error";
+    case LP_ERR_NCCL: return "NCCL error";
+    case LP_ERR_NOT_SOLVED: return "not solved";
+    case LP_ERR_UNSUPPORTED: return "unsupported";
+    default: return "unknown error";
+  }
+}
+
+const char *lp_last_error_detail(void) { return t_detail.c_str(); }
+
+void lp_destroy(lp_handle h) { free_handle(h); }
+
+}  // extern "C"

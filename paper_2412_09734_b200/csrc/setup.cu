@@ -1,0 +1,265 @@
+// setup.cu -- one-time device setup of an LP handle:
+//   validate, CSR of K' by a stable radix sort on the
+//   column index, Ruiz (10 rounds, inf-norm) + Pock-Chambolle (alpha = 1)
+//   diagonal scaling (contract step 1 in DESIGN.md §3), the
+//   scaled matrix / bounds, max|K~| for eta0, and the line-search factor table.
+//
+// Determinism: every reduction here is a per-row / per-column sequential loop
+// in stored order (K' rows are in increasing row order, so column sums run in
+// the same order as a row-major scan) or an order-free max, so the scalings are
+// bitwise reproducible run to run.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace mpax {
+
+namespace {
+
+// ---- validation -------------------------------------------------------------
+// flag[0] = worst severity (3 dimension, 2 NaN/inf, 1 crossed bounds), flag[1] = an index.
+__device__ __forceinline__ void report(int *flag, int sev, int idx) {
+  atomicMax(flag, sev);
+  atomicMin(flag + 1 + sev, idx);
+}
+
+__global__ void validate_kernel(int64_t m, int64_t n, int64_t nnz, const int64_t *__restrict__ rp,
+                                const int32_t *__restrict__ ci, const double *__restrict__ v,
+                                const double *__restrict__ c, int64_t nc, const double *__restrict__ q,
+                                int64_t nq, const double *__restrict__ l, const double *__restrict__ u,
+                                int *flag) {
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < m; i += stride) {  // rows: offsets, ranges, sorted columns
+    int64_t a = rp[i], b = rp[i + 1];
+    if ((i == 0 && a != 0) || (i == m - 1 && b != nnz) || b < a || a < 0 || b > nnz) {
+      report(flag, 3, (int)i);
+      continue;
+    }
+    for (int64_t p = a; p < b; ++p) {
+      int32_t j = ci[p];
+      if (j < 0 || j >= n || (p > a && j <= ci[p - 1])) { report(flag, 3, (int)i); break; }
+    }
+  }
+  for (int64_t p = tid; p < nnz; p += stride)
+    if (!isfinite(v[p])) report(flag, 2, (int)p);
+  for (int64_t j = tid; j < nc; j += stride)
+    if (!isfinite(c[j])) report(flag, 2, (int)j);
+  for (int64_t i = tid; i < nq; i += stride)
+    if (!isfinite(q[i])) report(flag, 2, (int)i);
+  for (int64_t j = tid; j < n; j += stride) {
+    double lj = l[j], uj = u[j];
+    if (isnan(lj) || isnan(uj)) report(flag, 2, (int)j);
+    else if (lj == INFINITY || uj == -INFINITY || lj > uj) report(flag, 1, (int)j);
+  }
+}
+
+// ---- transpose --------------------------------------------------------------
+__global__ void rows_to_int32(int64_t m, const int64_t *__restrict__ rp64, int32_t *__restrict__ rp32,
+                              int32_t *__restrict__ row_of) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= m; i += (int64_t)gridDim.x * blockDim.x) {
+    rp32[i] = (int32_t)rp64[i];
+    if (i < m)
+      for (int64_t p = rp64[i]; p < rp64[i + 1]; ++p) row_of[p] = (int32_t)i;
+  }
+}
+
+__global__ void iota_kernel(int64_t nnz, int32_t *__restrict__ a) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+    a[p] = (int32_t)p;
+}
+
+// K' row pointer: trp[j] = first position of column j in the sorted keys (lower bound).
+__global__ void transpose_finish(int64_t n, int64_t nnz, const int32_t *__restrict__ skeys,
+                                 const int32_t *__restrict__ perm, const int32_t *__restrict__ row_of,
+                                 int32_t *__restrict__ trp, int32_t *__restrict__ tci) {
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = tid; j <= n; j += st) {
+    int64_t lo = 0, hi = nnz;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (skeys[mid] < j) lo = mid + 1; else hi = mid;
+    }
+    trp[j] = (int32_t)lo;
+  }
+  for (int64_t d = tid; d < nnz; d += st) tci[d] = row_of[perm[d]];
+}
+
+// ---- preconditioning (contract step 1) ---------------------------------------
+// a_ij = (|K_ij| Dr_i) Dc_j.  use_sum = 0: inf-norm (Ruiz), 1: 1-norm (Pock-Chambolle alpha=1).
+__global__ void precond_norms(int64_t m, int64_t n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                              const int32_t *__restrict__ trp, const int32_t *__restrict__ tci,
+                              const int32_t *__restrict__ perm, const double *__restrict__ kv0,
+                              const double *__restrict__ Dr, const double *__restrict__ Dc,
+                              double *__restrict__ rho, double *__restrict__ gam, int use_sum) {
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = tid; t < m + n; t += st) {
+    double acc = 0.0;
+    if (t < m) {
+      int64_t i = t;
+      double dr = Dr[i];
+      for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+        double a = (fabs(kv0[p]) * dr) * Dc[ci[p]];
+        acc = use_sum ? acc + a : fmax(acc, a);
+      }
+      rho[i] = acc;
+    } else {
+      int64_t j = t - m;
+      double dc = Dc[j];
+      for (int32_t d = trp[j]; d < trp[j + 1]; ++d) {
+        double a = (fabs(kv0[perm[d]]) * Dr[tci[d]]) * dc;
+        acc = use_sum ? acc + a : fmax(acc, a);
+      }
+      gam[j] = acc;
+    }
+  }
+}
+
+__global__ void precond_update(int64_t m, int64_t n, const double *__restrict__ rho, const double *__restrict__ gam,
+                               double *__restrict__ Dr, double *__restrict__ Dc) {
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = tid; t < m + n; t += st) {
+    if (t < m) { double r = rho[t]; Dr[t] *= (r > 0.0 ? 1.0 / sqrt(r) : 1.0); }
+    else { double g = gam[t - m]; Dc[t - m] *= (g > 0.0 ? 1.0 / sqrt(g) : 1.0); }
+  }
+}
+
+__global__ void set_ones(int64_t len, double *__restrict__ a) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < len; t += (int64_t)gridDim.x * blockDim.x)
+    a[t] = 1.0;
+}
+
+// K~_ij = (K_ij Dr_i) Dc_j into both copies; l~ = l / Dc, u~ = u / Dc; max |K~| (order-free max on the bits).
+__global__ void scale_kernel(int64_t m, int64_t n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                             const int32_t *__restrict__ trp, const int32_t *__restrict__ tci,
+                             const int32_t *__restrict__ perm, const double *__restrict__ kv0,
+                             const double *__restrict__ Dr, const double *__restrict__ Dc, double *__restrict__ kv,
+                             double *__restrict__ tkv, const double *__restrict__ l0, const double *__restrict__ u0,
+                             double *__restrict__ ls, double *__restrict__ us, unsigned long long *kmax_bits) {
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+  double mx = 0.0;
+  for (int64_t t = tid; t < m + n; t += st) {
+    if (t < m) {
+      double dr = Dr[t];
+      for (int32_t p = rp[t]; p < rp[t + 1]; ++p) {
+        double s = (kv0[p] * dr) * Dc[ci[p]];
+        kv[p] = s;
+        mx = fmax(mx, fabs(s));
+      }
+    } else {
+      int64_t j = t - m;
+      double dc = Dc[j];
+      for (int32_t d = trp[j]; d < trp[j + 1]; ++d) tkv[d] = (kv0[perm[d]] * Dr[tci[d]]) * dc;
+      ls[j] = l0[j] / dc;
+      us[j] = u0[j] / dc;
+    }
+  }
+  if (mx > 0.0) atomicMax(kmax_bits, (unsigned long long)__double_as_longlong(mx));
+}
+
+__global__ void step_table_kernel(double *tab) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < kStepTab; j += gridDim.x * blockDim.x) {
+    double jp1 = (double)(j + 1);
+    tab[2 * j] = 1.0 - pow(jp1, -0.3);
+    tab[2 * j + 1] = 1.0 + pow(jp1, -0.6);
+  }
+}
+
+// Plain SpMV with the solver's scaled matrices (diagnostics / tests).
+__global__ void spmv_kernel(int64_t rows, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                            const double *__restrict__ v, const double *__restrict__ x, double *__restrict__ y) {
+  // one warp per row, lanes stride the row, butterfly sum
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < rows; r += nw) {
+    double s = 0.0;
+    for (int32_t p = rp[r] + lane; p < rp[r + 1]; p += 32) s += v[p] * x[ci[p]];
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    if (lane == 0) y[r] = s;
+  }
+}
+
+inline int grid_for(int64_t work, int block = 256) {
+  int64_t g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)g;
+}
+
+}  // namespace
+
+int setup_validate(DevProblem &P, const int64_t *row_ptr64, const double *c, int64_t nc, const double *q, int64_t nq,
+                   cudaStream_t s, int *h_flag) {
+  int *d_flag = nullptr;
+  MPAX_CUDA(cudaMallocAsync(&d_flag, 5 * sizeof(int), s));
+  int init[5] = {0, INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
+  MPAX_CUDA(cudaMemcpyAsync(d_flag, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  int64_t work = P.m + P.nnz + nc + nq + P.n;
+  MPAX_LAUNCH(validate_kernel, grid_for(work), 256, 0, s, P.m, P.n, P.nnz, row_ptr64, P.ci, P.kv0, c, nc, q, nq,
+              P.l0, P.u0, d_flag);
+  MPAX_CHECK_LAUNCH();
+  MPAX_CUDA(cudaMemcpyAsync(h_flag, d_flag, 5 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  MPAX_CUDA(cudaFreeAsync(d_flag, s));
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  return LP_OK;
+}
+
+int setup_build(DevProblem &P, const int64_t *row_ptr64, cudaStream_t s) {
+  const int64_t m = P.m, n = P.n, nnz = P.nnz;
+  int32_t *row_of = nullptr, *keys_out = nullptr, *idx_in = nullptr;
+  size_t nz = (size_t)(nnz > 0 ? nnz : 1);
+  MPAX_CUDA(cudaMallocAsync(&row_of, nz * sizeof(int32_t), s));
+  MPAX_CUDA(cudaMallocAsync(&keys_out, nz * sizeof(int32_t), s));
+  MPAX_CUDA(cudaMallocAsync(&idx_in, nz * sizeof(int32_t), s));
+  MPAX_LAUNCH(rows_to_int32, grid_for(m + 1), 256, 0, s, m, row_ptr64, P.rp, row_of);
+  MPAX_LAUNCH(iota_kernel, grid_for(nnz), 256, 0, s, nnz, idx_in);
+  // stable LSD radix sort of (col, position) pairs: rows stay in increasing order within a column
+  if (nnz > 0) {
+    int end_bit = 1;
+    while (end_bit < 31 && (1ll << end_bit) <= n) ++end_bit;
+    size_t temp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, P.ci, keys_out, idx_in, P.perm, (int)nnz, 0, end_bit, s);
+    void *temp = nullptr;
+    MPAX_CUDA(cudaMallocAsync(&temp, temp_bytes, s));
+    MPAX_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, P.ci, keys_out, idx_in, P.perm, (int)nnz, 0,
+                                              end_bit, s));
+    g_launches.fetch_add(4, std::memory_order_relaxed);  // CUB's onesweep/histogram kernels (approx.)
+    MPAX_CUDA(cudaFreeAsync(temp, s));
+  }
+  MPAX_LAUNCH(transpose_finish, grid_for(n + 1 + nnz), 256, 0, s, n, nnz, keys_out, P.perm, row_of, P.trp, P.tci);
+  // Ruiz x10 then Pock-Chambolle alpha=1 (contract step 1)
+  double *rho = nullptr, *gam = nullptr;
+  MPAX_CUDA(cudaMallocAsync(&rho, (size_t)(m > 0 ? m : 1) * sizeof(double), s));
+  MPAX_CUDA(cudaMallocAsync(&gam, (size_t)n * sizeof(double), s));
+  MPAX_LAUNCH(set_ones, grid_for(m), 256, 0, s, m, P.Dr);
+  MPAX_LAUNCH(set_ones, grid_for(n), 256, 0, s, n, P.Dc);
+  for (int r = 0; r < 11; ++r) {
+    int use_sum = (r == 10);
+    MPAX_LAUNCH(precond_norms, grid_for(m + n, 128), 128, 0, s, m, n, P.rp, P.ci, P.trp, P.tci, P.perm, P.kv0,
+                P.Dr, P.Dc, rho, gam, use_sum);
+    MPAX_LAUNCH(precond_update, grid_for(m + n), 256, 0, s, m, n, rho, gam, P.Dr, P.Dc);
+  }
+  MPAX_CUDA(cudaMemsetAsync(P.kmax, 0, sizeof(double), s));
+  MPAX_LAUNCH(scale_kernel, grid_for(m + n, 128), 128, 0, s, m, n, P.rp, P.ci, P.trp, P.tci, P.perm, P.kv0, P.Dr,
+              P.Dc, P.kv, P.tkv, P.l0, P.u0, P.ls, P.us, (unsigned long long *)P.kmax);
+  MPAX_LAUNCH(step_table_kernel, 64, 256, 0, s, P.tab);
+  MPAX_CHECK_LAUNCH();
+  MPAX_CUDA(cudaFreeAsync(rho, s));
+  MPAX_CUDA(cudaFreeAsync(gam, s));
+  MPAX_CUDA(cudaFreeAsync(row_of, s));
+  MPAX_CUDA(cudaFreeAsync(keys_out, s));
+  MPAX_CUDA(cudaFreeAsync(idx_in, s));
+  P.avg_row = m > 0 ? (double)nnz / (double)m : 0.0;
+  P.avg_col = (double)nnz / (double)n;
+  return LP_OK;
+}
+
+int spmv_scaled(const DevProblem &P, const double *v, double *Kv, const double *w, double *KTw, cudaStream_t s) {
+  if (v && Kv && P.m > 0) MPAX_LAUNCH(spmv_kernel, grid_for(P.m * 32), 256, 0, s, P.m, P.rp, P.ci, P.kv, v, Kv);
+  if (w && KTw) MPAX_LAUNCH(spmv_kernel, grid_for(P.n * 32), 256, 0, s, P.n, P.trp, P.tci, P.tkv, w, KTw);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+}  // namespace mpax

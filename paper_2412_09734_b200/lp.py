@@ -1,0 +1,372 @@
+"""ctypes binding of include/lp.h.  Argument marshalling only."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIBPATH = os.path.join(_HERE, "libmpax_b200.so")
+_lock = threading.Lock()
+_lib = None
+
+LP_HOST, LP_DEVICE = 0, 1
+LP_OPTIMAL, LP_ITERATION_LIMIT, LP_NUMERICAL_ERROR = 1, 2, 3
+RAPDHG, R2HPDHG = 0, 1
+PATH_AUTO, PATH_INSTANCE, PATH_GRID, PATH_DMMA = 0, 1, 2, 3
+
+EXPORTED_SYMBOLS = [
+    "lp_default_options", "lp_create", "lp_create_batch", "lp_update_batch", "lp_solve", "lp_solve_batch",
+    "lp_get_solution", "lp_get_solutions", "lp_get_shape", "lp_get_scaling", "lp_spmv_scaled",
+    "lp_kernel_launch_count", "lp_error_string", "lp_last_error_detail", "lp_destroy",
+]
+
+
+class LpError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        L = lib()
+        msg = L.lp_error_string(code).decode()
+        detail = L.lp_last_error_detail().decode()
+        super().__init__(f"{where}: {msg} ({code}){': ' + detail if detail else ''}")
+        self.code = code
+
+
+class ProblemDesc(C.Structure):
+    _fields_ = [("n", C.c_int64), ("m1", C.c_int64), ("m2", C.c_int64), ("nnz", C.c_int64),
+                ("dense", C.c_int32), ("memory", C.c_int32),
+                ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p),
+                ("c", C.c_void_p), ("q", C.c_void_p), ("l", C.c_void_p), ("u", C.c_void_p)]
+
+
+class Options(C.Structure):
+    _fields_ = [("eps_abs", C.c_double), ("eps_rel", C.c_double), ("eps_primal_infeasible", C.c_double),
+                ("eps_dual_infeasible", C.c_double), ("eps_feas_polish", C.c_double),
+                ("iteration_limit", C.c_int64), ("check_frequency", C.c_int32), ("algorithm", C.c_int32),
+                ("warm_start", C.c_int32), ("feasibility_polishing", C.c_int32), ("verbose", C.c_int32),
+                ("display_frequency", C.c_int32), ("path", C.c_int32), ("reserved", C.c_int32)]
+
+
+class Result(C.Structure):
+    _fields_ = [("status", C.c_int32), ("pad", C.c_int32), ("iterations", C.c_int64),
+                ("attempts", C.c_int64), ("restarts", C.c_int64),
+                ("primal_objective", C.c_double), ("dual_objective", C.c_double),
+                ("primal_residual", C.c_double), ("dual_residual", C.c_double), ("gap", C.c_double),
+                ("rel_kkt", C.c_double), ("omega", C.c_double), ("eta", C.c_double),
+                ("solve_seconds", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad"}
+
+
+def library_path() -> str:
+    return _LIBPATH
+
+
+def lib():
+    """Load libmpax_b200.so.  Raises if it has not been built (no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(_LIBPATH):
+                raise ImportError(f"{_LIBPATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+            L = C.CDLL(_LIBPATH)
+            P, V = C.POINTER, C.c_void_p
+            L.lp_default_options.argtypes = [P(Options)]
+            L.lp_create.argtypes = [P(ProblemDesc), V, P(V)]
+            L.lp_create_batch.argtypes = [P(ProblemDesc), C.c_int64, V, V, C.c_int32, V, P(V)]
+            L.lp_update_batch.argtypes = [V, V, V, C.c_int32]
+            L.lp_solve.argtypes = [V, P(Options), V, V, C.c_int32, P(Result)]
+            L.lp_solve_batch.argtypes = [V, P(Options), V, V, C.c_int32, V]
+            L.lp_get_solution.argtypes = [V, C.c_int64, V, V, V, C.c_int32]
+            L.lp_get_solutions.argtypes = [V, V, V, C.c_int32]
+            L.lp_get_shape.argtypes = [V, P(C.c_int64), P(C.c_int64), P(C.c_int64), P(C.c_int64)]
+            L.lp_get_scaling.argtypes = [V, V, V, C.c_int32]
+            L.lp_spmv_scaled.argtypes = [V, V, V, V, V, C.c_int32]
+            L.lp_kernel_launch_count.restype = C.c_int64
+            L.lp_error_string.argtypes = [C.c_int]
+            L.lp_error_string.restype = C.c_char_p
+            L.lp_last_error_detail.restype = C.c_char_p
+            L.lp_destroy.argtypes = [V]
+            _lib = L
+    return _lib
+
+
+def launch_count() -> int:
+    return int(lib().lp_kernel_launch_count())
+
+
+def _check(code, where):
+    if code != 0:
+        raise LpError(code, where)
+
+
+# ------------------------------------------------------------ arrays --------
+
+def _is_torch(a):
+    return type(a).__module__.startswith("torch")
+
+
+def _mem_of(a):
+    if a is None:
+        return None
+    if _is_torch(a):
+        return LP_DEVICE if a.is_cuda else LP_HOST
+    return LP_HOST
+
+
+class _Arr:
+    """A contiguous array of a given dtype on host (numpy) or device (torch)."""
+
+    def __init__(self, a, dtype):
+        self.src = a
+        if a is None:
+            self.obj, self.ptr = None, None
+        elif _is_torch(a):
+            import torch
+            tdt = {np.float64: torch.float64, np.int64: torch.int64, np.int32: torch.int32}[dtype]
+            t = a.to(dtype=tdt).contiguous()
+            self.obj, self.ptr = t, t.data_ptr()
+        else:
+            arr = np.ascontiguousarray(a, dtype=dtype)
+            self.obj, self.ptr = arr, (arr.ctypes.data if arr.size else None)
+
+
+def _same_mem(arrs):
+    kinds = {_mem_of(a) for a in arrs if a is not None}
+    if len(kinds) > 1:
+        raise ValueError("mix of host and device arrays in one call")
+    return kinds.pop() if kinds else LP_HOST
+
+
+def _stream_handle(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            pass
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+# ------------------------------------------------------------ problem -------
+
+class Problem:
+    """The LP of PAPER.md Eq. (1) stacked as K = [G; A] (CSR), q = (h; b)."""
+
+    def __init__(self, n, m1, m2, row_ptr, col_idx, values, c, q, l, u, dense=False):
+        self.n, self.m1, self.m2 = int(n), int(m1), int(m2)
+        self.row_ptr, self.col_idx, self.values = row_ptr, col_idx, values
+        self.c, self.q, self.l, self.u = c, q, l, u
+        self.dense = bool(dense)
+
+    @property
+    def m(self):
+        return self.m1 + self.m2
+
+    @classmethod
+    def from_lp(cls, lp):
+        """From any object with n, m1, m2, row_ptr, col_idx, val, c, q, l, u (e.g. lpgen.LP)."""
+        values = lp.val if hasattr(lp, "val") else lp.values
+        return cls(lp.n, lp.m1, lp.m2, lp.row_ptr, lp.col_idx, values, lp.c, lp.q, lp.l, lp.u,
+                   getattr(lp, "dense", False))
+
+    def to(self, device):
+        import torch
+        f = lambda a, dt: None if a is None else torch.as_tensor(np.asarray(a) if not _is_torch(a) else a,
+                                                                 dtype=dt, device=device)
+        return Problem(self.n, self.m1, self.m2, f(self.row_ptr, torch.int64), f(self.col_idx, torch.int32),
+                       f(self.values, torch.float64), f(self.c, torch.float64), f(self.q, torch.float64),
+                       f(self.l, torch.float64), f(self.u, torch.float64), self.dense)
+
+    def _desc(self):
+        arrs = [_Arr(self.row_ptr, np.int64), _Arr(self.col_idx, np.int32), _Arr(self.values, np.float64),
+                _Arr(self.c, np.float64), _Arr(self.q, np.float64), _Arr(self.l, np.float64),
+                _Arr(self.u, np.float64)]
+        mem = _same_mem([a.src for a in arrs])
+        nnz = int(arrs[2].obj.numel() if _is_torch(arrs[2].obj) else arrs[2].obj.size)
+        d = ProblemDesc(self.n, self.m1, self.m2, nnz, int(self.dense), mem, *[a.ptr for a in arrs])
+        return d, arrs
+
+
+def create_lp(c, A=None, b=None, G=None, h=None, l=None, u=None, use_sparse_matrix=True) -> Problem:
+    """PAPER.md P:121 `create_lp(c, A, b, G, h, l, u)`: stacks K = [G; A], q = (h; b).
+    A and G may be dense arrays or scipy sparse matrices; l/u default to -inf/+inf."""
+    c = np.asarray(c, np.float64)
+    n = c.size
+    try:
+        import scipy.sparse as sp
+    except Exception:  # pragma: no cover
+        sp = None
+
+    def as_csr(M):
+        if M is None:
+            return sp.csr_matrix((0, n)) if sp else None
+        if sp is not None and sp.issparse(M):
+            return sp.csr_matrix(M)
+        return sp.csr_matrix(np.atleast_2d(np.asarray(M, np.float64)))
+
+    Gm, Am = as_csr(G), as_csr(A)
+    K = sp.vstack([Gm, Am]).tocsr()
+    K.sum_duplicates()
+    K.sort_indices()
+    if use_sparse_matrix:
+        K.eliminate_zeros()
+        rp, ci, v = K.indptr.astype(np.int64), K.indices.astype(np.int32), K.data.astype(np.float64)
+        dense = False
+    else:
+        Kd = K.toarray()
+        m = Kd.shape[0]
+        rp = (np.arange(m + 1) * n).astype(np.int64)
+        ci = np.tile(np.arange(n, dtype=np.int32), m)
+        v = Kd.ravel().astype(np.float64)
+        dense = True
+    hq = np.zeros(0) if h is None else np.atleast_1d(np.asarray(h, np.float64))
+    bq = np.zeros(0) if b is None else np.atleast_1d(np.asarray(b, np.float64))
+    if hq.size != Gm.shape[0] or bq.size != Am.shape[0] or Gm.shape[1] != n or Am.shape[1] != n:
+        raise ValueError("dimension mismatch between c, G, h, A, b")
+    l = np.full(n, -np.inf) if l is None else np.asarray(l, np.float64)
+    u = np.full(n, np.inf) if u is None else np.asarray(u, np.float64)
+    return Problem(n, Gm.shape[0], Am.shape[0], rp, ci, v, c, np.concatenate([hq, bq]), l, u, dense)
+
+
+def default_options(**kw) -> Options:
+    o = Options()
+    lib().lp_default_options(C.byref(o))
+    alg = kw.pop("algorithm", None)
+    if alg is not None:
+        o.algorithm = R2HPDHG if alg in ("r2", "r2hpdhg", "r2HPDHG", R2HPDHG) else RAPDHG
+    for k, v in kw.items():
+        if v is None:
+            continue
+        if not hasattr(o, k):
+            raise TypeError(f"unknown option {k}")
+        setattr(o, k, v)
+    return o
+
+
+def _new_out(shape, like_mem, device):
+    if like_mem == LP_DEVICE:
+        import torch
+        return torch.empty(shape, dtype=torch.float64, device=device)
+    return np.zeros(shape)
+
+
+class Solver:
+    """One LP handle: lp_create / lp_solve / lp_get_solution / lp_destroy."""
+
+    def __init__(self, problem: Problem, stream=None):
+        self.problem = problem
+        d, keep = problem._desc()
+        self._mem = d.memory
+        self._device = problem.c.device if _is_torch(problem.c) else None
+        h = C.c_void_p()
+        _check(lib().lp_create(C.byref(d), _stream_handle(stream), C.byref(h)), "lp_create")
+        self._h = h
+        del keep
+
+    def solve(self, x0=None, y0=None, **opts):
+        o = default_options(**opts)
+        a, b = _Arr(x0, np.float64), _Arr(y0, np.float64)
+        mem = _same_mem([x0, y0])
+        r = Result()
+        _check(lib().lp_solve(self._h, C.byref(o), a.ptr, b.ptr, mem, C.byref(r)), "lp_solve")
+        return r.as_dict()
+
+    def solution(self, memory=LP_HOST):
+        n, m = self.problem.n, self.problem.m
+        x, y, lam = (_new_out(n, memory, self._device), _new_out(m, memory, self._device),
+                     _new_out(n, memory, self._device))
+        p = lambda t: t.data_ptr() if _is_torch(t) else (t.ctypes.data if t.size else None)
+        _check(lib().lp_get_solution(self._h, 0, p(x), p(y) if m else None, p(lam), memory), "lp_get_solution")
+        return x, y, lam
+
+    def scaling(self):
+        Dr, Dc = np.zeros(max(self.problem.m, 1)), np.zeros(self.problem.n)
+        _check(lib().lp_get_scaling(self._h, Dr.ctypes.data, Dc.ctypes.data, LP_HOST), "lp_get_scaling")
+        return Dr[: self.problem.m], Dc
+
+    def spmv_scaled(self, v=None, w=None):
+        n, m = self.problem.n, self.problem.m
+        va, wa = _Arr(v, np.float64), _Arr(w, np.float64)
+        Kv = np.zeros(max(m, 1)) if v is not None else None
+        KTw = np.zeros(n) if w is not None else None
+        _check(lib().lp_spmv_scaled(self._h, va.ptr, None if Kv is None else Kv.ctypes.data, wa.ptr,
+                                    None if KTw is None else KTw.ctypes.data, LP_HOST), "lp_spmv_scaled")
+        return (None if Kv is None else Kv[:m]), KTw
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().lp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class BatchSolver:
+    """A batch sharing K, l, u: lp_create_batch / lp_solve_batch."""
+
+    def __init__(self, problem: Problem, C_=None, Q=None, stream=None):
+        self.problem = problem
+        d, keep = problem._desc()
+        ca, qa = _Arr(C_, np.float64), _Arr(Q, np.float64)
+        mem = _same_mem([C_, Q])
+        if C_ is not None:
+            self.batch = int(C_.shape[0])
+        elif Q is not None:
+            self.batch = int(Q.shape[0])
+        else:
+            raise ValueError("a batch needs C or Q")
+        self._device = problem.c.device if _is_torch(problem.c) else (C_.device if _is_torch(C_) else None)
+        h = C.c_void_p()
+        _check(lib().lp_create_batch(C.byref(d), self.batch, ca.ptr, qa.ptr, mem, _stream_handle(stream),
+                                     C.byref(h)), "lp_create_batch")
+        self._h = h
+        del keep
+
+    def update(self, C_=None, Q=None):
+        ca, qa = _Arr(C_, np.float64), _Arr(Q, np.float64)
+        _check(lib().lp_update_batch(self._h, ca.ptr, qa.ptr, _same_mem([C_, Q])), "lp_update_batch")
+
+    def solve(self, X0=None, Y0=None, **opts):
+        o = default_options(**opts)
+        a, b = _Arr(X0, np.float64), _Arr(Y0, np.float64)
+        res = (Result * self.batch)()
+        _check(lib().lp_solve_batch(self._h, C.byref(o), a.ptr, b.ptr, _same_mem([X0, Y0]), res),
+               "lp_solve_batch")
+        return [r.as_dict() for r in res]
+
+    def solutions(self, memory=LP_HOST, X=None, Y=None):
+        n, m, B = self.problem.n, self.problem.m, self.batch
+        X = _new_out((B, n), memory, self._device) if X is None else X
+        Y = _new_out((B, m), memory, self._device) if Y is None else Y
+        p = lambda t: t.data_ptr() if _is_torch(t) else (t.ctypes.data if t.size else None)
+        _check(lib().lp_get_solutions(self._h, p(X), p(Y) if m else None, memory), "lp_get_solutions")
+        return X, Y
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().lp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

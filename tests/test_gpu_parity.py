@@ -1,0 +1,287 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs (SURVEY.md §8(c) c.5 parity budget):
+  * scalings Dr, Dc bitwise equal (same correctly rounded ops, same order);
+  * iterates after a fixed number K of accepted steps within 1e-9 relative;
+  * status, iteration, attempt and restart counts identical wherever they are
+    well-posed: the oracle's own counts must not move under 1-ulp
+    perturbations of c and no logged decision may be a near-tie (margin < 1e-9);
+    the contract's trajectories are chaotic on some instances;
+  * final objective within 1e-6 relative, KKT residuals <= 1e-4 relative.
+"""
+import numpy as np
+import pytest
+
+import lpgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_2412_09734_b200 as mp  # noqa: E402
+
+ALGS = ["ra", "r2"]
+MARGIN = 1e-9
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    den = max(np.linalg.norm(b), 1e-300)
+    return np.linalg.norm(a - b) / den
+
+
+def min_margin(r):
+    """Smallest relative margin of any discontinuous decision the oracle took."""
+    mm = np.inf
+    att = r.get("att_log")
+    if att is not None and len(att):
+        eta, eb = att[:, 2], att[:, 3]
+        fin = np.isfinite(eb)
+        if fin.any():
+            mm = min(mm, np.min(np.abs(eta[fin] - eb[fin]) / np.maximum(eta[fin], 1e-300)))
+    chk = r.get("chk_log")
+    if chk is not None and len(chk):
+        for k, metric, ref, last, rs, ps in chk:
+            if ref > 0 and np.isfinite(ref):
+                mm = min(mm, abs(metric - 0.2 * ref) / ref, abs(metric - 0.8 * ref) / ref)
+            if np.isfinite(last) and metric > 0:
+                mm = min(mm, abs(metric - last) / metric)
+    return mm
+
+
+def perturbed(lp, sign):
+    """The same LP with c scaled by (1 +- 2^-52): a 1-ulp input perturbation."""
+    return lp.with_costs(c=lp.c * (1.0 + sign * 2.0 ** -52))
+
+
+def oracle_stability(lp, alg, **kw):
+    """Sensitivity guard: run the oracle on the LP and on two
+    1-ulp perturbations of c.  Returns (result, counts_stable, drift): the
+    counts are stable when the oracle's own status / iteration / attempt /
+    restart counts do not move under the perturbations (and no logged decision
+    is a near-tie), and `drift` is how far its own iterate moves (relative).  A
+    GPU run with a different, equally valid summation order can only be held to
+    identical counts when they are stable, and to max(1e-9, 100 drift)."""
+    r = oracle.solve(lp, alg, log_capacity=1 << 16, **kw)
+    stable = min_margin(r) >= MARGIN
+    drift = 0.0
+    for sgn in (1, -1):
+        p = oracle.solve(perturbed(lp, sgn), alg, **kw)
+        stable &= all(p[k] == r[k] for k in ("status", "iterations", "attempts", "restarts"))
+        drift = max(drift, rel(p["x"], r["x"]), rel(p["y"], r["y"]) if lp.m else 0.0)
+    return r, bool(stable), drift
+
+
+def gpu_solve(lp, alg, device=False, **kw):
+    prob = mp.Problem.from_lp(lp)
+    if device:
+        prob = prob.to("cuda:0")
+    with mp.Solver(prob) as s:
+        r = s.solve(algorithm=alg, **kw)
+        x, y, lam = s.solution()
+    r.update(x=x, y=y, lam=lam)
+    return r
+
+
+def small_lps():
+    yield "tiny", lpgen.tiny_spec()
+    yield "C1", lpgen.g_rand(50, 100, 10, seed=1)
+    yield "ragged", lpgen.g_rand(37, 61, 5, seed=7)
+    yield "grid", lpgen.g_grid(batch=1)[0]
+    yield "dense", lpgen.g_dense(30, 50, batch=1, seed=5)[0]
+
+
+# ------------------------------------------------------------------ setup ----
+
+@pytest.mark.parametrize("name,lp", list(small_lps()))
+def test_scaling_bitwise(name, lp):
+    with mp.Solver(mp.Problem.from_lp(lp)) as s:
+        Dr, Dc = s.scaling()
+    Dro, Dco = oracle.precondition(lp)
+    assert np.array_equal(Dr, Dro) and np.array_equal(Dc, Dco)
+
+
+@pytest.mark.parametrize("name,lp", list(small_lps()) + [("mid", lpgen.g_rand(3000, 5000, 12, seed=3))])
+def test_spmv_scaled_vs_oracle(name, lp):
+    s_or = oracle.scaled_problem(lp)
+    rng = np.random.default_rng(0)
+    v, w = rng.normal(size=lp.n), rng.normal(size=lp.m)
+    with mp.Solver(mp.Problem.from_lp(lp)) as s:
+        Kv, KTw = s.spmv_scaled(v, w)
+    scaled = lpgen.LP(lp.n, lp.m1, lp.m2, lp.row_ptr, lp.col_idx, s_or["Kv"], lp.c, lp.q, lp.l, lp.u)
+    Kv_o, KTw_o = oracle.spmv_pair(scaled, x=v, w=w)
+    assert rel(Kv, Kv_o) <= 1e-14 and rel(KTw, KTw_o) <= 1e-14
+    assert abs(Kv @ w - v @ KTw) <= 1e-12 * (abs(Kv @ w) + 1e-300)
+
+
+def test_validation_errors():
+    bad = lpgen.tiny_spec()
+    bad.l = np.array([1.0, 0.0]); bad.u = np.array([0.0, 1.0])
+    with pytest.raises(mp.LpError) as e:
+        mp.Solver(mp.Problem.from_lp(bad))
+    assert e.value.code == -4
+    bad = lpgen.tiny_spec()
+    bad.q = np.array([np.nan])
+    with pytest.raises(mp.LpError) as e:
+        mp.Solver(mp.Problem.from_lp(bad))
+    assert e.value.code == -3
+    bad = lpgen.tiny_spec()
+    bad.col_idx = np.array([1, 0], np.int32)                    # unsorted row
+    with pytest.raises(mp.LpError) as e:
+        mp.Solver(mp.Problem.from_lp(bad))
+    assert e.value.code == -2
+    bad = lpgen.tiny_spec()
+    bad.u = np.array([-np.inf, 1.0])
+    with pytest.raises(mp.LpError) as e:
+        mp.Solver(mp.Problem.from_lp(bad))
+    assert e.value.code == -4
+
+
+# ------------------------------------------------------- fixed-K parity ----
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("K", [1, 2, 64, 256])
+@pytest.mark.parametrize("name,lp", list(small_lps()))
+def test_fixed_K_iterates(alg, K, name, lp):
+    ro, stable, drift = oracle_stability(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=K)
+    rg = gpu_solve(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=K)
+    if not stable:
+        pytest.skip("ill-conditioned at this K: the oracle's own counts move under a 1-ulp perturbation of c")
+    tol = max(1e-9, 100 * drift)
+    for key in ("status", "iterations", "attempts", "restarts"):
+        assert rg[key] == ro[key], (key, rg[key], ro[key])
+    assert rel(rg["x"], ro["x"]) <= tol
+    if lp.m:
+        assert rel(rg["y"], ro["y"]) <= tol
+    assert abs(rg["primal_objective"] - ro["primal_objective"]) <= tol * (1 + abs(ro["primal_objective"]))
+
+
+# --------------------------------------------------------- full solves -----
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("name,lp", list(small_lps()))
+def test_full_solve(alg, name, lp):
+    ro, stable, drift = oracle_stability(lp, alg)
+    rg = gpu_solve(lp, alg)
+    assert rg["status"] == mp.LP_OPTIMAL and ro["status"] == oracle.OPTIMAL
+    if stable:
+        for key in ("iterations", "attempts", "restarts"):
+            assert rg[key] == ro[key], (key, rg[key], ro[key])
+        assert abs(rg["primal_objective"] - ro["primal_objective"]) <= 1e-6 * (1 + abs(ro["primal_objective"]))
+    assert rg["rel_kkt"] <= 1e-4
+    # self-certification on original data with the oracle's independent KKT routine
+    k = oracle.kkt_original(lp, rg["x"], rg["y"])
+    nq, nc = np.linalg.norm(lp.q), np.linalg.norm(lp.c)
+    assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * nq)
+    assert k["dres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * nc)
+    assert np.all(rg["x"] >= lp.l) and np.all(rg["x"] <= lp.u) and np.all(rg["y"][: lp.m1] >= 0)
+    if lp.obj_star is not None:
+        assert abs(rg["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_tiny_tight_tolerance_and_warm_start(alg):
+    lp = lpgen.tiny_spec()
+    rg = gpu_solve(lp, alg, eps_abs=1e-8, eps_rel=1e-8)
+    assert rg["status"] == mp.LP_OPTIMAL and abs(rg["primal_objective"] - 1.0) <= 1e-6
+    with mp.Solver(mp.Problem.from_lp(lp)) as s:
+        r = s.solve(np.array([0.0, 1.0]), np.array([1.0]), algorithm=alg)
+    assert r["status"] == mp.LP_OPTIMAL and r["iterations"] == 64
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_warm_start_parity(alg):
+    lp = lpgen.g_rand(50, 100, 10, seed=1)
+    rng = np.random.default_rng(3)
+    x0, y0 = rng.normal(size=lp.n), rng.normal(size=lp.m)
+    ro = oracle.solve(lp, alg, x0=x0, y0=y0, iteration_limit=128, eps_abs=0, eps_rel=0)
+    with mp.Solver(mp.Problem.from_lp(lp)) as s:
+        rg = s.solve(x0, y0, algorithm=alg, iteration_limit=128, eps_abs=0.0, eps_rel=0.0)
+        x, y, _ = s.solution()
+    assert rg["attempts"] == ro["attempts"] and rel(x, ro["x"]) <= 1e-9 and rel(y, ro["y"]) <= 1e-9
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_degenerate_cases(alg):
+    lp0 = lpgen.stack([1.0, -2.0, 0.5], l=[-1, -1, 0], u=[1, 3, 2])        # no rows
+    rg = gpu_solve(lp0, alg, eps_abs=1e-9, eps_rel=1e-9)
+    assert rg["status"] == mp.LP_OPTIMAL and np.allclose(rg["x"], [-1, 3, 0], atol=1e-8)
+    lpz = lpgen.stack([1.0, 1.0], G=[[1.0, 0.0], [0.0, 0.0]], h=[1.0, -1.0], l=[0, 0], u=[5, 5])
+    ro = oracle.solve(lpz, alg, eps_abs=1e-9, eps_rel=1e-9)
+    rg = gpu_solve(lpz, alg, eps_abs=1e-9, eps_rel=1e-9)
+    assert rg["status"] == mp.LP_OPTIMAL and rg["iterations"] == ro["iterations"]
+    assert abs(rg["primal_objective"] - 1.0) <= 1e-7
+    lp = lpgen.g_rand(50, 100, 10, seed=1)
+    rg = gpu_solve(lp, alg, eps_abs=1e-12, eps_rel=1e-12, iteration_limit=100)
+    assert rg["status"] == mp.LP_ITERATION_LIMIT and rg["iterations"] == 100
+
+
+def test_device_memory_path_equals_host_path():
+    lp = lpgen.g_rand(50, 100, 10, seed=1)
+    a = gpu_solve(lp, "r2")
+    b = gpu_solve(lp, "r2", device=True)
+    assert np.array_equal(a["x"], b["x"]) and a["attempts"] == b["attempts"]
+
+
+# ------------------------------------------------------------- batches -----
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_grid_batch_c2(alg):
+    """C2: 1024 PyEPO-style 5x5 shortest-path LPs sharing K."""
+    lp, C = lpgen.g_grid(batch=1024)
+    bs = mp.BatchSolver(mp.Problem.from_lp(lp), C)
+    res = bs.solve(algorithm=alg)
+    X, Y = bs.solutions()
+    bs.close()
+    Xo, Yo, ro = oracle.solve_batch(lp, C, None, alg)
+    # sensitivity guard: instances whose oracle counts move under 1-ulp perturbations of c
+    _, _, rp = oracle.solve_batch(lp, C * (1 + 2.0 ** -52), None, alg)
+    _, _, rm = oracle.solve_batch(lp, C * (1 - 2.0 ** -52), None, alg)
+    keys = ("status", "iterations", "attempts", "restarts")
+    stable = [all(ro[b][k] == rp[b][k] == rm[b][k] for k in keys) for b in range(1024)]
+    n_stable = sum(stable)
+    assert n_stable >= 700, n_stable
+    for b in range(1024):
+        assert res[b]["status"] == mp.LP_OPTIMAL
+        assert res[b]["rel_kkt"] <= 1e-4
+        dp = lpgen.grid_dp_optimum(5, C[b])
+        assert abs(res[b]["primal_objective"] - dp) <= 1e-3 * (1 + dp)
+        if stable[b]:
+            assert all(res[b][k] == ro[b][k] for k in keys), (b, res[b], ro[b])
+            assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= 1e-6 * (1 + dp)
+            assert rel(X[b], Xo[b]) <= 1e-7
+
+
+def test_batch_equals_single_and_determinism():
+    lp, C = lpgen.g_grid(batch=40)
+    C[7] = C[3]
+    bs = mp.BatchSolver(mp.Problem.from_lp(lp), C)
+    r1 = bs.solve(algorithm="r2")
+    X1, Y1 = bs.solutions()
+    r2 = bs.solve(algorithm="r2")
+    X2, Y2 = bs.solutions()
+    bs.close()
+    assert np.array_equal(X1, X2) and np.array_equal(Y1, Y2)              # bitwise deterministic
+    assert np.array_equal(X1[7], X1[3])                                    # identical instances
+    for b in (0, 3, 39):
+        r = gpu_solve(lp.with_costs(c=C[b]), "r2")
+        assert np.array_equal(r["x"], X1[b]) and r["attempts"] == r1[b]["attempts"]
+
+
+def test_dense_batch_per_instance_c3_sample():
+    lp, C, Q, obj = lpgen.g_dense(200, 400, batch=256, seed=3)
+    Cs, Qs = C[:8], Q[:8]
+    bs = mp.BatchSolver(mp.Problem.from_lp(lp), Cs, Qs)
+    res = bs.solve(algorithm="r2", path=mp.PATH_INSTANCE)
+    X, _ = bs.solutions()
+    bs.close()
+    Xo, _, ro = oracle.solve_batch(lp, Cs, Qs, "r2")
+    _, _, rp = oracle.solve_batch(lp, Cs * (1 + 2.0 ** -52), Qs, "r2")
+    for b in range(8):
+        assert res[b]["status"] == mp.LP_OPTIMAL and res[b]["rel_kkt"] <= 1e-4
+        assert abs(res[b]["primal_objective"] - obj[b]) <= 1e-3 * (1 + abs(obj[b]))
+        if ro[b]["attempts"] == rp[b]["attempts"] and ro[b]["iterations"] == rp[b]["iterations"]:
+            assert res[b]["attempts"] == ro[b]["attempts"]
+            assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= 1e-6 * (1 + abs(obj[b]))
