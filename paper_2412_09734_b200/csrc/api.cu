@@ -194,8 +194,27 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
     MPAX_CUDA(cudaMemcpyAsync(h->Y0, Y0, (size_t)(B * m) * sizeof(double), cudaMemcpyDefault, s));
     dY0 = h->Y0;
   }
-  if (o->path == LP_PATH_GRID || o->path == LP_PATH_DMMA)
-    return fail(LP_ERR_UNSUPPORTED, "requested path not available in this build");
+  if (o->path == LP_PATH_DMMA) return fail(LP_ERR_UNSUPPORTED, "requested path not available in this build");
+  const bool big = h->P.nnz >= 32768 || h->P.n + h->P.m >= 4096;
+  const bool use_grid = (B == 1) && (o->path == LP_PATH_GRID || (o->path == LP_PATH_AUTO && big));
+  if (o->path == LP_PATH_GRID && B != 1) return fail(LP_ERR_UNSUPPORTED, "the grid path solves one LP");
+  if (use_grid) {
+    GridLaunch G;
+    G.c0 = h->C0; G.q0 = h->Q0; G.X0 = dX0; G.Y0 = dY0; G.X = h->X; G.Y = h->Y; G.L = h->L; G.res = h->d_res;
+    MPAX_CUDA(cudaEventRecord(h->ev0, s));
+    int rc = grid_solve(h->P, *o, G, s, &h->work, &h->work_bytes);
+    if (rc == LP_ERR_UNSUPPORTED) return fail(rc, "cooperative launch unavailable");
+    TRY(rc);
+    MPAX_CUDA(cudaEventRecord(h->ev1, s));
+    MPAX_CUDA(cudaMemcpyAsync(h->h_res, h->d_res, sizeof(lp_result), cudaMemcpyDeviceToHost, s));
+    MPAX_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.0f;
+    MPAX_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    out[0] = h->h_res[0];
+    out[0].solve_seconds = ms * 1e-3;
+    h->solved = true;
+    return LP_OK;
+  }
   InstanceLaunch L;
   L.C0 = h->C0; L.cstride = h->cstride; L.Q0 = h->Q0; L.qstride = h->qstride;
   L.X0 = dX0; L.Y0 = dY0; L.batch = B; L.X = h->X; L.Y = h->Y; L.L = h->L; L.res = h->d_res;

@@ -1,0 +1,570 @@
+// grid_solver.cu -- one LP spread over the whole GPU (SURVEY §8(a) rows a4-a10,
+// configs C4/C5): a persistent cooperative kernel whose CTAs stay resident for
+// the entire solve and meet at grid barriers, so no host round trip and no
+// kernel launch happens per iteration ("the loop stays on device").
+//
+// One attempt = two fused phases and two grid barriers:
+//   phase A (columns j of K~'):  [accepted last attempt]  K~'_j y'  (SpMV #2) and the
+//       n-side commit (raPDHG: average + swap; r2HPDHG: Halpern reflection on x and
+//       K~'y, Eq. (hrpdhg)), then the next primal step
+//       x'_j = proj(x_j - tau (c~_j - (K~'y)_j)) (Eq. (pdhg)) and ||dx||^2.
+//   phase B (rows i of K~):  [accepted] m-side commit, then K~_i x' (SpMV #1), the
+//       dual step y'_i = proj(y_i + sigma (q~_i - 2 K~_i x' + (K~x)_i)), ||dy||^2 and
+//       <dy, K~x' - K~x>.
+//   Every CTA then sums the per-CTA partials in a fixed order and takes the
+//   line-search decision redundantly: no extra barrier, no float atomics.
+// Every check_frequency accepted steps a commit-only phase, the
+// average's two SpMVs (raPDHG) fused with the original-space KKT partials, the
+// restart test and primal-weight update, and an optional restart copy.
+//
+// Data layout: CSR of K~ and of K~' (int32 offsets/indices, fp64 values), all
+// vectors fp64 SoA.  The matrices are streamed with evict-first loads; the
+// gathered vector (x' in phase B, y' in phase A) uses the default policy so it
+// can stay L2-resident.  Each row is summed by G lanes (butterfly), G from the
+// mean row length.  Results are bitwise deterministic.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mpax {
+
+namespace {
+
+constexpr int kNP = 20;      // max partial sums per phase
+constexpr int kBS = 512;     // threads per CTA
+
+struct GridParams {
+  int64_t n, m, m1;
+  const int32_t *rp, *ci, *trp, *tci;
+  const double *kv, *tkv, *Dr, *Dc, *ls, *us, *l0, *u0, *c0, *q0, *X0, *Y0, *kmax, *tab;
+  double *cs, *qs;
+  double *x, *KTy, *xp, *KTyp, *xa, *KTya, *xr;   // n-side
+  double *y, *Kx, *yp, *Kxp, *ya, *Kxa, *yr;      // m-side
+  double *part;                                   // gridDim.x x kNP
+  double eps_abs, eps_rel;
+  int64_t iter_limit;
+  int32_t check_freq, alg, gk, gkt;
+  double *X, *Y, *L;
+  lp_result *res;
+};
+
+struct KktT {
+  double pres, dres, pobj, dobj, gap;
+};
+__device__ __forceinline__ KktT mk(const double *v) {
+  KktT k;
+  k.pres = sqrt(v[0]); k.dres = sqrt(v[1]); k.pobj = v[2]; k.dobj = v[3]; k.gap = fabs(v[2] - v[3]);
+  return k;
+}
+__device__ __forceinline__ bool pass(const KktT &k, double nq, double nc, double ea, double er) {
+  return k.pres <= ea + er * nq && k.dres <= ea + er * nc && k.gap <= ea + er * (fabs(k.pobj) + fabs(k.dobj));
+}
+__device__ __forceinline__ double relk(const KktT &k, double nq, double nc) {
+  return fmax(k.pres / (1.0 + nq), fmax(k.dres / (1.0 + nc), k.gap / (1.0 + fabs(k.pobj) + fabs(k.dobj))));
+}
+
+// KKT contributions of one row / one column (contract step 5), original or scaled space.
+__device__ __forceinline__ void kkt_row(double *v, bool orig, int64_t i, int64_t m1, double dr, double ys, double Kxs,
+                                        double q0, double qs) {
+  const double Kx = orig ? Kxs / dr : Kxs, q = orig ? q0 : qs, y = orig ? dr * ys : ys;
+  double r = q - Kx;
+  if (i < m1) r = fmax(r, 0.0);
+  v[0] += r * r;
+  v[3] += q * y;
+}
+__device__ __forceinline__ void kkt_col(double *v, bool orig, double dc, double xs, double KTys, double c0, double cs,
+                                        double l0, double ls, double u0, double us) {
+  const double x = orig ? dc * xs : xs, KTy = orig ? KTys / dc : KTys;
+  const double c = orig ? c0 : cs, l = orig ? l0 : ls, u = orig ? u0 : us;
+  const double lam = c - KTy, lp = fmax(lam, 0.0), lm = fmax(-lam, 0.0);
+  double d = 0.0;
+  if (l == -INFINITY) d += lp;
+  if (u == INFINITY) d += lm;
+  v[1] += d * d;
+  v[2] += c * x;
+  if (l > -INFINITY) v[3] += l * lp;
+  if (u < INFINITY) v[3] -= u * lm;
+}
+
+// streamed (evict-first) loads of the matrices
+__device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
+__device__ __forceinline__ int32_t ld_stream(const int32_t *p) { return __ldcs(p); }
+
+// Sum of row r of a CSR matrix times x, G lanes per row (all lanes get the sum).
+__device__ __forceinline__ double row_dot(int64_t r, bool valid, int G, int gl, const int32_t *__restrict__ rp,
+                                          const int32_t *__restrict__ ci, const double *__restrict__ v,
+                                          const double *x) {
+  double s = 0.0;
+  if (valid) {
+    const int32_t e = __ldg(rp + r + 1);
+    int32_t p = __ldg(rp + r) + gl;
+#pragma unroll 4
+    for (; p < e; p += G) s += ld_stream(v + p) * x[ld_stream(ci + p)];
+  }
+  for (int off = G >> 1; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+  return s;
+}
+
+template <int V>
+__device__ __forceinline__ void block_partials(double (&v)[V], double *part, double (*s_red)[kNP]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    double s = v[k];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    if (lane == 0) s_red[wid][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < V) {
+    double s = 0.0;
+    for (int w = 0; w < kBS / 32; ++w) s += s_red[w][threadIdx.x];
+    part[(int64_t)blockIdx.x * kNP + threadIdx.x] = s;
+  }
+}
+
+// After a grid barrier: every CTA sums the per-CTA partials in the same fixed order.
+template <int V>
+__device__ __forceinline__ void grid_totals(double (&t)[V], const double *part, double *s_tot) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      double s = 0.0;
+      for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(part + (int64_t)b * kNP + k);
+#pragma unroll
+      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+      if (lane == 0) s_tot[k] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < V; ++k) t[k] = s_tot[k];
+}
+
+__global__ void __launch_bounds__(kBS) grid_kernel(GridParams P) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double s_red[kBS / 32][kNP];
+  __shared__ double s_tot[kNP];
+  const int64_t n = P.n, m = P.m, m1 = P.m1;
+  const int64_t gtid = (int64_t)blockIdx.x * kBS + threadIdx.x, gthreads = (int64_t)gridDim.x * kBS;
+  const bool r2 = (P.alg == LP_R2HPDHG);
+  // SpMV group mapping (fixed for the whole solve, so every row / column has one owner group)
+  const int G = P.gk, Gt = P.gkt;
+  const int64_t grp = gtid / G, ngrp = gthreads / G;
+  const int gl = (int)(gtid % G);
+  const int64_t grpt = gtid / Gt, ngrpt = gthreads / Gt;
+  const int glt = (int)(gtid % Gt);
+  const int64_t row_iters = (m + ngrp - 1) / ngrp, col_iters = (n + ngrpt - 1) / ngrpt;
+  double *x = P.x, *KTy = P.KTy, *xp = P.xp, *KTyp = P.KTyp, *xa = P.xa, *KTya = P.KTya, *xr = P.xr;
+  double *y = P.y, *Kx = P.Kx, *yp = P.yp, *Kxp = P.Kxp, *ya = P.ya, *Kxa = P.Kxa, *yr = P.yr;
+  const double *cs = P.cs, *qs = P.qs;
+
+  // ---------------- step 2: initialise ----------------
+  {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t j = gtid; j < n; j += gthreads) {
+      const double dc = P.Dc[j], c = P.c0[j], cj = c * dc;
+      P.cs[j] = cj;
+      v[0] += cj * cj;
+      v[2] += c * c;
+      x[j] = median3(P.ls[j], P.X0 ? P.X0[j] / dc : 0.0, P.us[j]);
+    }
+    for (int64_t i = gtid; i < m; i += gthreads) {
+      const double dr = P.Dr[i], q = P.q0[i], qi = q * dr;
+      P.qs[i] = qi;
+      v[1] += qi * qi;
+      v[3] += q * q;
+      double yv = P.Y0 ? P.Y0[i] / dr : 0.0;
+      if (i < m1) yv = fmax(yv, 0.0);
+      y[i] = yv;
+    }
+    block_partials<4>(v, P.part, s_red);
+  }
+  grid.sync();
+  double tot4[4];
+  grid_totals<4>(tot4, P.part, s_tot);
+  const double nc0 = sqrt(tot4[2]), nq0 = sqrt(tot4[3]);
+  double omega = 1.0;
+  if (sqrt(tot4[0]) > 1e-10 && sqrt(tot4[1]) > 1e-10) omega = sqrt(tot4[0]) / sqrt(tot4[1]);
+  const double kmx = *P.kmax;
+  double eta = kmx > 0.0 ? 1.0 / kmx : 1.0;
+  {
+    // K~x0, K~'y0; anchors / restart point; KKT_omega(z0) partials (scaled space)
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t it = 0; it < row_iters; ++it) {
+      const int64_t i = it * ngrp + grp;
+      const bool ok = i < m;
+      const double s = row_dot(i, ok, G, gl, P.rp, P.ci, P.kv, x);
+      if (ok && gl == 0) {
+        Kx[i] = s; Kxa[i] = s;
+        const double yv = y[i];
+        ya[i] = yv; yr[i] = yv;
+        kkt_row(v, false, i, m1, 1.0, yv, s, 0.0, qs[i]);
+      }
+    }
+    for (int64_t it = 0; it < col_iters; ++it) {
+      const int64_t j = it * ngrpt + grpt;
+      const bool ok = j < n;
+      const double s = row_dot(j, ok, Gt, glt, P.trp, P.tci, P.tkv, y);
+      if (ok && glt == 0) {
+        KTy[j] = s; KTya[j] = s;
+        const double xv = x[j];
+        xa[j] = xv; xr[j] = xv;
+        kkt_col(v, false, 1.0, xv, s, 0.0, cs[j], 0.0, P.ls[j], 0.0, P.us[j]);
+      }
+    }
+    block_partials<4>(v, P.part, s_red);
+  }
+  grid.sync();
+  int64_t k = 0, jatt = 0, k_in = 0, restarts = 0;
+  double W = 0.0, last = INFINITY, ref = 0.0;
+  {
+    double t[4];
+    grid_totals<4>(t, P.part, s_tot);
+    if (!r2) {
+      const KktT ks = mk(t);
+      ref = sqrt(omega * ks.pres * ks.pres + ks.dres * ks.dres / omega + ks.gap * ks.gap);
+    }
+  }
+
+  int status = 0;
+  bool pending = false;        // an accepted attempt whose commit is fused into the next phases
+  double theta = 0.0, ha = 0.0, hb = 0.0;  // raPDHG average weight / r2HPDHG Halpern coefficients
+  int rejects = 0;
+  // returned candidate (pointers)
+  const double *ox = x, *oy = y, *oKx = Kx, *oKTy = KTy;
+  bool done = false;
+
+  while (!done) {
+    // ================= phase A: [commit n-side] + primal step =================
+    const double tau = eta / omega, sigma = eta * omega;
+    double v3[3] = {0.0, 0.0, 0.0};
+    if (pending) {
+      for (int64_t it = 0; it < col_iters; ++it) {
+        const int64_t j = it * ngrpt + grpt;
+        const bool ok = j < n;
+        const double s = row_dot(j, ok, Gt, glt, P.trp, P.tci, P.tkv, yp);
+        if (ok && glt == 0) {
+          double xn, kt;
+          if (!r2) {
+            const double xv = xp[j];
+            xa[j] += theta * (xv - xa[j]);
+            xn = xv; kt = s;
+            KTyp[j] = s;           // becomes KTy after the pointer swap
+          } else {
+            xn = ha * (2.0 * xp[j] - x[j]) + hb * xa[j];
+            kt = ha * (2.0 * s - KTy[j]) + hb * KTya[j];
+            x[j] = xn; KTy[j] = kt;
+          }
+          const double xnew = median3(P.ls[j], xn - tau * (cs[j] - kt), P.us[j]);
+          if (!r2) x[j] = xnew;    // x (old-x buffer) becomes x' after the swap
+          else xp[j] = xnew;
+          const double d = xnew - xn;
+          v3[0] += d * d;
+        }
+      }
+      if (!r2) {  // swap: x <-> x', K~'y <-> K~'y'
+        double *t = x; x = xp; xp = t;
+        t = KTy; KTy = KTyp; KTyp = t;
+      }
+    } else {
+      for (int64_t j = gtid; j < n; j += gthreads) {
+        const double xo = x[j];
+        const double xn = median3(P.ls[j], xo - tau * (cs[j] - KTy[j]), P.us[j]);
+        xp[j] = xn;
+        const double d = xn - xo;
+        v3[0] += d * d;
+      }
+    }
+    grid.sync();
+    // ================= phase B: [commit m-side] + SpMV #1 + dual step =================
+    {
+      for (int64_t it = 0; it < row_iters; ++it) {
+        const int64_t i = it * ngrp + grp;
+        const bool ok = i < m;
+        const double s = row_dot(i, ok, G, gl, P.rp, P.ci, P.kv, xp);
+        if (ok && gl == 0) {
+          double yv, kxv;
+          if (pending) {
+            if (!r2) {
+              yv = yp[i];
+              ya[i] += theta * (yv - ya[i]);
+              kxv = Kxp[i];
+            } else {
+              yv = ha * (2.0 * yp[i] - y[i]) + hb * ya[i];
+              kxv = ha * (2.0 * Kxp[i] - Kx[i]) + hb * Kxa[i];
+              y[i] = yv; Kx[i] = kxv;
+            }
+          } else {
+            yv = y[i]; kxv = Kx[i];
+          }
+          double yn = yv + sigma * (qs[i] - 2.0 * s + kxv);
+          if (i < m1) yn = fmax(yn, 0.0);
+          if (pending && !r2) { y[i] = yn; Kx[i] = s; }   // old buffers become y', K~x' after the swap
+          else { yp[i] = yn; Kxp[i] = s; }
+          const double d = yn - yv;
+          v3[1] += d * d;
+          v3[2] += d * (s - kxv);
+        }
+      }
+      if (pending && !r2) {
+        double *t = y; y = yp; yp = t;
+        t = Kx; Kx = Kxp; Kxp = t;
+      }
+      pending = false;
+      block_partials<3>(v3, P.part, s_red);
+    }
+    grid.sync();
+    double t3[3];
+    grid_totals<3>(t3, P.part, s_tot);
+    ++jatt;
+    const double I = t3[2];
+    const double M = omega * t3[0] + t3[1] / omega;
+    const double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : INFINITY;
+    const bool acc = (eta <= eb);
+    const double eta_used = eta;
+    double f1, f2;
+    step_factors(P.tab, jatt, f1, f2);
+    eta = fmin(f1 * eb, f2 * eta);
+    if (!acc) {
+      if (++rejects >= 100) { status = LP_NUMERICAL_ERROR; ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
+      continue;
+    }
+    rejects = 0;
+    // accepted: prepare the commit (step 4)
+    double rP = 0.0;
+    if (!r2) {
+      const double W1 = W + eta_used;
+      theta = eta_used / W1;
+      W = W1;
+    } else {
+      rP = sqrt(fmax(0.0, M / eta_used - 2.0 * I));
+      if (k_in == 0) ref = rP;
+      ha = (double)(k_in + 1) / (double)(k_in + 2);
+      hb = 1.0 / (double)(k_in + 2);
+    }
+    ++k;
+    ++k_in;
+    if (k % P.check_freq != 0 && k != P.iter_limit) { pending = true; continue; }
+
+    // ================= check: commit-only phase (both sides) =================
+    {
+      double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int64_t it = 0; it < col_iters; ++it) {
+        const int64_t j = it * ngrpt + grpt;
+        const bool ok = j < n;
+        const double s = row_dot(j, ok, Gt, glt, P.trp, P.tci, P.tkv, yp);
+        if (ok && glt == 0) {
+          KTyp[j] = s;
+          if (!r2) {
+            xa[j] += theta * (xp[j] - xa[j]);
+          } else {
+            x[j] = ha * (2.0 * xp[j] - x[j]) + hb * xa[j];
+            KTy[j] = ha * (2.0 * s - KTy[j]) + hb * KTya[j];
+            const double dc = P.Dc[j];
+            kkt_col(v, true, dc, xp[j], s, P.c0[j], cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+            const double d = xp[j] - xr[j];
+            v[4] += d * d;
+          }
+        }
+      }
+      for (int64_t i = gtid; i < m; i += gthreads) {
+        if (!r2) {
+          ya[i] += theta * (yp[i] - ya[i]);
+        } else {
+          const double ypi = yp[i], kxp = Kxp[i];
+          y[i] = ha * (2.0 * ypi - y[i]) + hb * ya[i];
+          Kx[i] = ha * (2.0 * kxp - Kx[i]) + hb * Kxa[i];
+          kkt_row(v, true, i, m1, P.Dr[i], ypi, kxp, P.q0[i], qs[i]);
+          const double d = ypi - yr[i];
+          v[5] += d * d;
+        }
+      }
+      if (!r2) {
+        double *t = x; x = xp; xp = t;
+        t = KTy; KTy = KTyp; KTyp = t;
+        t = y; y = yp; yp = t;
+        t = Kx; Kx = Kxp; Kxp = t;
+      }
+      if (r2) block_partials<6>(v, P.part, s_red);
+    }
+    grid.sync();
+    const double *cx, *cy, *cKx, *cKTy;
+    double metric, dx2, dy2;
+    if (!r2) {
+      // average's products (2 SpMVs) fused with all KKT / distance partials
+      double v[kNP];
+#pragma unroll
+      for (int q = 0; q < kNP; ++q) v[q] = 0.0;
+      for (int64_t it = 0; it < row_iters; ++it) {
+        const int64_t i = it * ngrp + grp;
+        const bool ok = i < m;
+        const double s = row_dot(i, ok, G, gl, P.rp, P.ci, P.kv, xa);
+        if (ok && gl == 0) {
+          Kxa[i] = s;
+          const double dr = P.Dr[i], yai = ya[i], yi = y[i], kxi = Kx[i], q0 = P.q0[i], qsi = qs[i];
+          kkt_row(v + 0, true, i, m1, dr, yai, s, q0, qsi);
+          kkt_row(v + 4, true, i, m1, dr, yi, kxi, q0, qsi);
+          kkt_row(v + 8, false, i, m1, dr, yai, s, q0, qsi);
+          kkt_row(v + 12, false, i, m1, dr, yi, kxi, q0, qsi);
+          const double da = yai - yr[i], dcur = yi - yr[i];
+          v[17] += da * da;
+          v[19] += dcur * dcur;
+        }
+      }
+      for (int64_t it = 0; it < col_iters; ++it) {
+        const int64_t j = it * ngrpt + grpt;
+        const bool ok = j < n;
+        const double s = row_dot(j, ok, Gt, glt, P.trp, P.tci, P.tkv, ya);
+        if (ok && glt == 0) {
+          KTya[j] = s;
+          const double dc = P.Dc[j], xaj = xa[j], xj = x[j], ktj = KTy[j];
+          const double c0 = P.c0[j], csj = cs[j], l0 = P.l0[j], lsj = P.ls[j], u0 = P.u0[j], usj = P.us[j];
+          kkt_col(v + 0, true, dc, xaj, s, c0, csj, l0, lsj, u0, usj);
+          kkt_col(v + 4, true, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+          kkt_col(v + 8, false, dc, xaj, s, c0, csj, l0, lsj, u0, usj);
+          kkt_col(v + 12, false, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+          const double da = xaj - xr[j], dcur = xj - xr[j];
+          v[16] += da * da;
+          v[18] += dcur * dcur;
+        }
+      }
+      block_partials<kNP>(v, P.part, s_red);
+      grid.sync();
+      double t[kNP];
+      grid_totals<kNP>(t, P.part, s_tot);
+      const KktT ka = mk(t + 0), kc = mk(t + 4);
+      if (pass(ka, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; break; }
+      if (pass(kc, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
+      if (k == P.iter_limit) {
+        status = LP_ITERATION_LIMIT;
+        if (relk(ka, nq0, nc0) < relk(kc, nq0, nc0)) { ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; }
+        else { ox = x; oy = y; oKx = Kx; oKTy = KTy; }
+        break;
+      }
+      const KktT sa = mk(t + 8), sc = mk(t + 12);
+      const double e_a = sqrt(omega * sa.pres * sa.pres + sa.dres * sa.dres / omega + sa.gap * sa.gap);
+      const double e_c = sqrt(omega * sc.pres * sc.pres + sc.dres * sc.dres / omega + sc.gap * sc.gap);
+      if (e_a < e_c) { cx = xa; cy = ya; cKx = Kxa; cKTy = KTya; metric = e_a; dx2 = t[16]; dy2 = t[17]; }
+      else { cx = x; cy = y; cKx = Kx; cKTy = KTy; metric = e_c; dx2 = t[18]; dy2 = t[19]; }
+    } else {
+      double t[6];
+      grid_totals<6>(t, P.part, s_tot);
+      const KktT kw = mk(t);
+      if (pass(kw, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
+      if (k == P.iter_limit) { status = LP_ITERATION_LIMIT; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
+      cx = xp; cy = yp; cKx = Kxp; cKTy = KTyp; metric = rP; dx2 = t[4]; dy2 = t[5];
+    }
+    const bool restart = ((double)k_in >= 0.36 * (double)k) || (metric <= 0.2 * ref) ||
+                         (metric <= 0.8 * ref && metric > last);
+    last = metric;
+    if (restart) {
+      ++restarts;
+      const double dxn = sqrt(dx2), dyn = sqrt(dy2);
+      if (dxn > 1e-10 && dyn > 1e-10) omega = sqrt(omega * (dyn / dxn));
+      for (int64_t j = gtid; j < n; j += gthreads) {
+        const double xv = cx[j], kt = cKTy[j];
+        x[j] = xv; xr[j] = xv; xa[j] = xv; KTy[j] = kt; KTya[j] = kt;
+      }
+      for (int64_t i = gtid; i < m; i += gthreads) {
+        const double yv = cy[i], kx = cKx[i];
+        y[i] = yv; yr[i] = yv; ya[i] = yv; Kx[i] = kx; Kxa[i] = kx;
+      }
+      k_in = 0;
+      if (!r2) { W = 0.0; ref = metric; }
+      grid.sync();
+    }
+  }
+
+  // ================= step 6: output the candidate =================
+  {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t j = gtid; j < n; j += gthreads) {
+      const double dc = P.Dc[j], xs = ox[j], kt = oKTy[j];
+      kkt_col(v, true, dc, xs, kt, P.c0[j], cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+      P.X[j] = dc * xs;
+      P.L[j] = P.c0[j] - kt / dc;
+    }
+    for (int64_t i = gtid; i < m; i += gthreads) {
+      const double dr = P.Dr[i];
+      kkt_row(v, true, i, m1, dr, oy[i], oKx[i], P.q0[i], qs[i]);
+      P.Y[i] = dr * oy[i];
+    }
+    block_partials<4>(v, P.part, s_red);
+  }
+  grid.sync();
+  double t[4];
+  grid_totals<4>(t, P.part, s_tot);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const KktT ko = mk(t);
+    lp_result r;
+    r.status = status; r.pad = 0;
+    r.iterations = k; r.attempts = jatt; r.restarts = restarts;
+    r.primal_objective = ko.pobj; r.dual_objective = ko.dobj;
+    r.primal_residual = ko.pres; r.dual_residual = ko.dres; r.gap = ko.gap;
+    r.rel_kkt = relk(ko, nq0, nc0);
+    r.omega = omega; r.eta = eta; r.solve_seconds = 0.0;
+    *P.res = r;
+  }
+}
+
+inline int pow2_floor(double v) {
+  int g = 1;
+  while (g * 2 <= v && g < 32) g *= 2;
+  return g;
+}
+
+}  // namespace
+
+int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cudaStream_t s, double **work,
+               size_t *work_bytes) {
+  int dev = 0, sms = 0, coop = 0;
+  MPAX_CUDA(cudaGetDevice(&dev));
+  MPAX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  MPAX_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  if (!coop) return LP_ERR_UNSUPPORTED;
+  int per_sm = 0;
+  MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_kernel, kBS, 0));
+  if (per_sm < 1) return LP_ERR_UNSUPPORTED;
+  const int64_t n = D.n, m = D.m;
+  int blocks = per_sm * sms;
+  // small problems do not need the whole GPU
+  const int64_t work_items = (D.nnz + n + m);
+  while (blocks > sms && (int64_t)blocks * kBS > 4 * work_items) blocks -= sms;
+  const size_t vec = (size_t)(8 * n + 8 * m) + (size_t)blocks * kNP;
+  const size_t need = vec * sizeof(double);
+  if (*work_bytes < need) {
+    if (*work) MPAX_CUDA(cudaFreeAsync(*work, s));
+    *work = nullptr;
+    MPAX_CUDA(cudaMallocAsync((void **)work, need, s));
+    *work_bytes = need;
+  }
+  double *w = *work;
+  GridParams P;
+  P.n = n; P.m = m; P.m1 = D.m1;
+  P.rp = D.rp; P.ci = D.ci; P.trp = D.trp; P.tci = D.tci;
+  P.kv = D.kv; P.tkv = D.tkv; P.Dr = D.Dr; P.Dc = D.Dc; P.ls = D.ls; P.us = D.us; P.l0 = D.l0; P.u0 = D.u0;
+  P.c0 = L.c0; P.q0 = L.q0; P.X0 = L.X0; P.Y0 = L.Y0; P.kmax = D.kmax; P.tab = D.tab;
+  P.cs = w; w += n;
+  P.x = w; w += n; P.KTy = w; w += n; P.xp = w; w += n; P.KTyp = w; w += n; P.xa = w; w += n; P.KTya = w; w += n;
+  P.xr = w; w += n;
+  P.qs = w; w += m;
+  P.y = w; w += m; P.Kx = w; w += m; P.yp = w; w += m; P.Kxp = w; w += m; P.ya = w; w += m; P.Kxa = w; w += m;
+  P.yr = w; w += m;
+  P.part = w;
+  P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
+  P.check_freq = o.check_frequency; P.alg = o.algorithm;
+  P.gk = pow2_floor(D.avg_row / 4.0);
+  P.gkt = pow2_floor(D.avg_col / 4.0);
+  P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
+  void *args[] = {&P};
+  MPAX_CUDA(cudaLaunchCooperativeKernel((void *)grid_kernel, dim3(blocks), dim3(kBS), args, 0, s));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+}  // namespace mpax

@@ -1,0 +1,103 @@
+"""GPU parity of the whole-GPU grid path (one LP across all SMs; configs C4/C5)
+against the CPU oracle, through the C ABI.  Same guards as test_gpu_parity.py."""
+import numpy as np
+import pytest
+
+import lpgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_2412_09734_b200 as mp  # noqa: E402
+from tests.test_gpu_parity import oracle_stability, rel  # noqa: E402
+
+ALGS = ["ra", "r2"]
+
+
+def grid_solve(lp, alg, path=mp.PATH_GRID, x0=None, y0=None, **kw):
+    with mp.Solver(mp.Problem.from_lp(lp)) as s:
+        r = s.solve(x0, y0, algorithm=alg, path=path, **kw)
+        x, y, lam = s.solution()
+    r.update(x=x, y=y, lam=lam)
+    return r
+
+
+CASES = [("tiny", lpgen.tiny_spec()), ("C1", lpgen.g_rand(50, 100, 10, seed=1)),
+         ("ragged", lpgen.g_rand(37, 61, 5, seed=7)), ("mid", lpgen.g_rand(3000, 5000, 12, seed=3)),
+         ("wide", lpgen.g_rand(700, 9000, 30, seed=8)), ("dense", lpgen.g_dense(60, 90, batch=1, seed=5)[0])]
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("K", [1, 2, 64, 200])
+@pytest.mark.parametrize("name,lp", CASES)
+def test_grid_fixed_K(alg, K, name, lp):
+    ro, stable, drift = oracle_stability(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=K)
+    rg = grid_solve(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=K)
+    if not stable:
+        pytest.skip("ill-conditioned at this K: the oracle's own counts move under a 1-ulp perturbation of c")
+    tol = max(1e-9, 100 * drift)
+    for key in ("status", "iterations", "attempts", "restarts"):
+        assert rg[key] == ro[key], (key, rg[key], ro[key])
+    assert rel(rg["x"], ro["x"]) <= tol
+    if lp.m:
+        assert rel(rg["y"], ro["y"]) <= tol
+    assert rel(rg["lam"], ro["lam"]) <= max(1e-8, 1e3 * drift)
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("name,lp", CASES)
+def test_grid_full_solve(alg, name, lp):
+    ro, stable, drift = oracle_stability(lp, alg)
+    rg = grid_solve(lp, alg)
+    assert rg["status"] == mp.LP_OPTIMAL and rg["rel_kkt"] <= 1e-4
+    if stable:
+        for key in ("iterations", "attempts", "restarts"):
+            assert rg[key] == ro[key], (key, rg[key], ro[key])
+        assert abs(rg["primal_objective"] - ro["primal_objective"]) <= 1e-6 * (1 + abs(ro["primal_objective"]))
+    k = oracle.kkt_original(lp, rg["x"], rg["y"])
+    assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.q))
+    assert k["dres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.c))
+    if lp.obj_star is not None:
+        assert abs(rg["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
+
+
+def test_grid_determinism_and_warm_start():
+    lp = lpgen.g_rand(3000, 5000, 12, seed=3)
+    a = grid_solve(lp, "r2", iteration_limit=300, eps_abs=0.0, eps_rel=0.0)
+    b = grid_solve(lp, "r2", iteration_limit=300, eps_abs=0.0, eps_rel=0.0)
+    assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["y"], b["y"]) and a["attempts"] == b["attempts"]
+    rng = np.random.default_rng(2)
+    x0, y0 = rng.normal(size=lp.n), rng.normal(size=lp.m)
+    ro = oracle.solve(lp, "ra", x0=x0, y0=y0, iteration_limit=64, eps_abs=0, eps_rel=0)
+    rg = grid_solve(lp, "ra", x0=x0, y0=y0, iteration_limit=64, eps_abs=0.0, eps_rel=0.0)
+    assert rg["attempts"] == ro["attempts"] and rel(rg["x"], ro["x"]) <= 1e-9
+
+
+def test_grid_matches_instance_path():
+    lp = lpgen.g_rand(50, 100, 10, seed=1)
+    a = grid_solve(lp, "ra", path=mp.PATH_GRID, iteration_limit=64, eps_abs=0.0, eps_rel=0.0)
+    b = grid_solve(lp, "ra", path=mp.PATH_INSTANCE, iteration_limit=64, eps_abs=0.0, eps_rel=0.0)
+    assert a["attempts"] == b["attempts"] and rel(a["x"], b["x"]) <= 1e-12
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_c4_full_size(alg):
+    """C4 = G-RAND(1e5, 2e5, 20, seed 4) at its BASELINE size: parity after one
+    check interval (K = 64) and a full solve to 1e-4 against the known optimum."""
+    lp = lpgen.g_rand(100_000, 200_000, 20, seed=4)
+    ro, stable, drift = oracle_stability(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=64)
+    rg = grid_solve(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=64)
+    if stable:
+        assert rg["attempts"] == ro["attempts"] and rg["restarts"] == ro["restarts"]
+        assert rel(rg["x"], ro["x"]) <= max(1e-9, 100 * drift)
+        assert rel(rg["y"], ro["y"]) <= max(1e-9, 100 * drift)
+    r = grid_solve(lp, alg)
+    assert r["status"] == mp.LP_OPTIMAL and r["rel_kkt"] <= 1e-4
+    assert abs(r["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
+    k = oracle.kkt_original(lp, r["x"], r["y"])
+    assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.q))
+    assert np.all(r["x"] >= lp.l) and np.all(r["x"] <= lp.u) and np.all(r["y"][: lp.m1] >= 0)
