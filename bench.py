@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--alg", default="ra", choices=["r2", "ra"])
     ap.add_argument("--secondary-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-large", action="store_true", help="skip the C4 whole-GPU leg")
+    ap.add_argument("--large-m", type=int, default=100_000)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -330,6 +332,8 @@ def run_ours(args):
         "clocks": clocks,
         "secondary": secondary,
     }
+    if not args.no_large:
+        line["large_lp"] = large_lp_leg(mp, torch, dev, stream, peaks, args)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(lp, C, args.alg, args.cpu_seconds)
     if rank == 0:
@@ -337,6 +341,48 @@ def run_ours(args):
     if ws > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def attempt_bytes(n, m, nnz, alg):
+    """Algorithmic bytes of one accepted attempt of the grid path (DESIGN.md §6,
+    SURVEY §8(d) d.2): the SpMV pair streams K~ and K~' once (12 B per entry each)
+    plus their int32 row pointers and gathers x' and y' once; the fused updates
+    move 64n + 56m (raPDHG) or 88n + 88m (r2HPDHG) bytes."""
+    pair = 24 * nnz + 4 * (m + 1) + 4 * (n + 1) + 8 * n + 8 * m
+    upd = 64 * n + 56 * m if alg == "ra" else 88 * n + 88 * m
+    return pair, pair + upd
+
+
+def large_lp_leg(mp, torch, dev, stream, peaks, args):
+    """C4 = G-RAND(1e5, 2e5, 20, seed 4) solved to 1e-4 on the whole-GPU grid path:
+    time to tolerance and achieved HBM GB/s of the fused SpMV-pair + update loop."""
+    m = args.large_m
+    lp = lpgen.g_rand(m, 2 * m, 20, seed=4)
+    prob = mp.Problem.from_lp(lp).to(dev)
+    out = {"workload": f"C4: G-RAND({m}, {2 * m}, 20, seed 4), one LP on the whole GPU (grid path), to 1e-4",
+           "nnz": lp.nnz}
+    hbm = peaks.get("hbm_gbs", 6546.6)
+    for alg in ("ra", "r2"):
+        with mp.Solver(prob) as s:
+            s.solve(algorithm=alg, path=mp.PATH_GRID)                       # warm-up
+            best = None
+            for _ in range(3):
+                r = s.solve(algorithm=alg, path=mp.PATH_GRID)
+                best = r if best is None or r["solve_seconds"] < best["solve_seconds"] else best
+        pair, acc = attempt_bytes(lp.n, lp.m, lp.nnz, alg)
+        rej = best["attempts"] - best["iterations"]
+        byts = best["iterations"] * acc + rej * (pair // 2)
+        t = best["solve_seconds"]
+        gbs = byts / t / 1e9
+        out[alg] = {"status_optimal": best["status"] == mp.LP_OPTIMAL, "time_ms": t * 1e3,
+                    "iterations": best["iterations"], "attempts": best["attempts"], "restarts": best["restarts"],
+                    "rel_kkt": best["rel_kkt"], "objective_rel_err": abs(best["primal_objective"] - lp.obj_star)
+                    / (1 + abs(lp.obj_star)), "us_per_attempt": t * 1e6 / best["attempts"],
+                    "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                                 "traffic": None, "kernel": "grid_kernel",
+                                 "algorithmic_bytes_per_accepted_attempt": acc,
+                                 "note": "working set (~70 MB) is L2-resident at C4; achieved may exceed HBM"}}
+    return out
 
 
 def main():

@@ -32,6 +32,8 @@ struct lp_handle_s {
   double *work = nullptr;
   size_t work_bytes = 0;
   int64_t *rp64 = nullptr;
+  int *d_flag = nullptr, *h_flag = nullptr;
+  void *arena = nullptr;  // one allocation holding every per-handle array
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool solved = false;
 };
@@ -76,17 +78,28 @@ int dalloc(T **p, size_t count, cudaStream_t s) {
 void free_handle(lp_handle h) {
   if (!h) return;
   cudaStream_t s = h->stream;
-  void *ptrs[] = {h->P.rp, h->P.ci, h->P.kv0, h->P.kv, h->P.trp, h->P.tci, h->P.perm, h->P.tkv, h->P.l0,
-                  h->P.u0, h->P.ls, h->P.us, h->P.Dr, h->P.Dc, h->P.kmax, h->P.tab, h->C0, h->Q0, h->X,
-                  h->Y, h->L, h->X0, h->Y0, h->d_res, h->queue, h->work, h->rp64};
-  for (void *p : ptrs)
+  for (void *p : {(void *)h->arena, (void *)h->X0, (void *)h->Y0, (void *)h->work})
     if (p) cudaFreeAsync(p, s);
   if (h->h_res) cudaFreeHost(h->h_res);
+  if (h->h_flag) cudaFreeHost(h->h_flag);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   cudaStreamSynchronize(s);
   delete h;
 }
+
+// Carves typed, 256-byte aligned arrays out of one device allocation.
+struct Arena {
+  size_t off = 0;
+  char *base = nullptr;
+  template <class T>
+  void take(T **p, size_t count) {
+    if (count == 0) count = 1;
+    off = (off + 255) & ~(size_t)255;
+    *p = base ? (T *)(base + off) : nullptr;
+    off += count * sizeof(T);
+  }
+};
 
 int check_desc(const lp_problem_desc *p) {
   if (!p) return fail(LP_ERR_INVALID_ARGUMENT, "problem descriptor is NULL");
@@ -126,20 +139,30 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
     rc = (x);                       \
     if (rc != LP_OK) return cleanup(rc); \
   } while (0)
-  CK(dalloc(&h->rp64, m + 1, s)); CK(dalloc(&P.rp, m + 1, s)); CK(dalloc(&P.ci, nnz, s));
-  CK(dalloc(&P.kv0, nnz, s)); CK(dalloc(&P.kv, nnz, s)); CK(dalloc(&P.trp, n + 1, s));
-  CK(dalloc(&P.tci, nnz, s)); CK(dalloc(&P.perm, nnz, s)); CK(dalloc(&P.tkv, nnz, s));
-  CK(dalloc(&P.l0, n, s)); CK(dalloc(&P.u0, n, s)); CK(dalloc(&P.ls, n, s)); CK(dalloc(&P.us, n, s));
-  CK(dalloc(&P.Dr, m, s)); CK(dalloc(&P.Dc, n, s)); CK(dalloc(&P.kmax, 1, s)); CK(dalloc(&P.tab, 2 * kStepTab, s));
   const bool perC = is_batch && C != nullptr, perQ = is_batch && Q != nullptr;
   h->cstride = perC ? n : 0;
   h->qstride = perQ ? m : 0;
-  CK(dalloc(&h->C0, perC ? batch * n : n, s));
-  CK(dalloc(&h->Q0, perQ ? batch * m : m, s));
-  CK(dalloc(&h->X, batch * n, s)); CK(dalloc(&h->Y, batch * m, s)); CK(dalloc(&h->L, batch * n, s));
-  CK(dalloc(&h->d_res, batch, s)); CK(dalloc(&h->queue, 1, s));
-  if (cudaMallocHost((void **)&h->h_res, (size_t)batch * sizeof(lp_result)) != cudaSuccess)
-    return cleanup(fail(LP_ERR_OUT_OF_MEMORY, "pinned result buffer"));
+  auto carve = [&](Arena &A) {
+    A.take(&h->rp64, m + 1); A.take(&P.rp, m + 1); A.take(&P.ci, nnz); A.take(&P.kv0, nnz); A.take(&P.kv, nnz);
+    A.take(&P.trp, n + 1); A.take(&P.tci, nnz); A.take(&P.perm, nnz); A.take(&P.tkv, nnz);
+    A.take(&P.l0, n); A.take(&P.u0, n); A.take(&P.ls, n); A.take(&P.us, n); A.take(&P.Dr, m); A.take(&P.Dc, n);
+    A.take(&P.kmax, 1); A.take(&h->C0, perC ? batch * n : n); A.take(&h->Q0, perQ ? batch * m : m);
+    A.take(&h->X, batch * n); A.take(&h->Y, batch * m); A.take(&h->L, batch * n);
+    A.take(&h->d_res, batch); A.take(&h->queue, 1); A.take(&h->d_flag, 8);
+  };
+  {
+    Arena sizing;
+    carve(sizing);
+    CK(dalloc((char **)&h->arena, sizing.off, s));
+    Arena real;
+    real.base = (char *)h->arena;
+    carve(real);
+  }
+  P.tab = const_cast<double *>(step_table(s));
+  if (!P.tab) return cleanup(fail(LP_ERR_CUDA, "line-search table"));
+  if (cudaMallocHost((void **)&h->h_res, (size_t)batch * sizeof(lp_result)) != cudaSuccess ||
+      cudaMallocHost((void **)&h->h_flag, 8 * sizeof(int)) != cudaSuccess)
+    return cleanup(fail(LP_ERR_OUT_OF_MEMORY, "pinned host buffers"));
   if (cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess)
     return cleanup(fail(LP_ERR_CUDA, "event create"));
   auto cp = [&](void *dst, const void *src, size_t bytes) -> int {
@@ -154,12 +177,21 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
   CK(cp(P.u0, p->u, (size_t)n * sizeof(double)));
   CK(cp(h->C0, perC ? (const void *)C : (const void *)p->c, (size_t)(perC ? batch * n : n) * sizeof(double)));
   if (m > 0) CK(cp(h->Q0, perQ ? (const void *)Q : (const void *)p->q, (size_t)(perQ ? batch * m : m) * sizeof(double)));
-  int flag[5];
-  CK(setup_validate(P, h->rp64, h->C0, perC ? batch * n : n, h->Q0, perQ ? batch * m : m, s, flag));
+  {
+    const int init[8] = {0, INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX, 0, 0, 0};
+    memcpy(h->h_flag, init, sizeof(init));
+    CK(cp(h->d_flag, h->h_flag, sizeof(init)));
+  }
+  CK(setup_validate(P, h->rp64, h->C0, perC ? batch * n : n, h->Q0, perQ ? batch * m : m, s, h->d_flag));
+  CK(setup_build(P, h->rp64, s, h->d_flag));
+  CK(cp(h->h_flag, h->d_flag, 8 * sizeof(int)));
+  if (cudaStreamSynchronize(s) != cudaSuccess) return cleanup(fail(LP_ERR_CUDA, "setup"));
+  const int *flag = h->h_flag;
   if (flag[0] == 3) return cleanup(fail(LP_ERR_DIMENSION, "CSR structure invalid at row " + std::to_string(flag[4])));
   if (flag[0] == 2) return cleanup(fail(LP_ERR_NAN, "NaN or infinity in K, c or q (or NaN in l/u) near index " + std::to_string(flag[3])));
   if (flag[0] == 1) return cleanup(fail(LP_ERR_CROSSED_BOUNDS, "crossed bounds at index " + std::to_string(flag[2])));
-  CK(setup_build(P, h->rp64, s));
+  P.max_row = flag[5];
+  P.max_col = flag[6];
   *out = h;
   return LP_OK;
 #undef CK
@@ -219,7 +251,9 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
   L.C0 = h->C0; L.cstride = h->cstride; L.Q0 = h->Q0; L.qstride = h->qstride;
   L.X0 = dX0; L.Y0 = dY0; L.batch = B; L.X = h->X; L.Y = h->Y; L.L = h->L; L.res = h->d_res;
   MPAX_CUDA(cudaEventRecord(h->ev0, s));
-  TRY(instance_solve(h->P, *o, L, s, h->queue, &h->work, &h->work_bytes));
+  int rc = (o->path == LP_PATH_AUTO) ? tiny_solve(h->P, *o, L, s, h->queue) : LP_ERR_UNSUPPORTED;
+  if (rc == LP_ERR_UNSUPPORTED) rc = instance_solve(h->P, *o, L, s, h->queue, &h->work, &h->work_bytes);
+  TRY(rc);
   MPAX_CUDA(cudaEventRecord(h->ev1, s));
   MPAX_CUDA(cudaMemcpyAsync(h->h_res, h->d_res, (size_t)B * sizeof(lp_result), cudaMemcpyDeviceToHost, s));
   MPAX_CUDA(cudaStreamSynchronize(s));

@@ -5,23 +5,27 @@
 // instance from a device queue (batch scheduler).  No host
 // synchronisation happens until every instance is done.
 //
-// Iteration: DESIGN.md §3 (= SURVEY §8(c) c.2), steps 2-6:
-//   step 3: x' = proj_X(x - tau (c~ - K~'y)); K~x'; y' = proj_Y(y + sigma (q~ - 2K~x' + K~x))
-//           (PAPER.md Eq. (pdhg)), eta_bar = M / (2|<dy, K~x' - K~x>|), accept iff
-//           eta <= eta_bar, eta <- min((1-(j+1)^-.3) eta_bar, (1+(j+1)^-.6) eta)
-//   step 4: K~'y'; raPDHG: z <- z', eta-weighted average;
-//           r2HPDHG: z <- (k+1)/(k+2) (2z' - z) + 1/(k+2) z0 on x, y AND the cached
-//           products (Eq. (hrpdhg))
-//   step 5: every check_frequency accepted steps: original-space KKT
-//           termination test, restart test on KKT_omega (ra) / fixed-point residual
-//           (r2), restart + primal weight sqrt(omega dy/dx).
+// Iteration: DESIGN.md §3 (= SURVEY §8(c) c.2), steps 2-6, organised like the
+// grid kernel into two fused phases per attempt:
+//   phase A (columns): [if the previous attempt was accepted] K~'_j y' (SpMV #2)
+//       and the n-side commit -- raPDHG: eta-weighted average and z <- z';
+//       r2HPDHG: z <- (k+1)/(k+2)(2z' - z) + 1/(k+2) z0 on x and the cached K~'y
+//       (Eq. (hrpdhg)) -- then the next primal step
+//       x'_j = proj(x_j - tau (c~_j - (K~'y)_j)) (Eq. (pdhg));
+//   phase B (rows): [accepted] m-side commit, then K~_i x' (SpMV #1) and the dual
+//       step y'_i = proj(y_i + sigma (q~_i - 2 K~_i x' + (K~x)_i));
+//   then one fixed-order block reduction of ||dx||^2, ||dy||^2, <dy, K~dx> and the
+//   line-search decision, taken redundantly by every thread.
+// Every check_frequency accepted steps: a commit-only phase, the
+// average's two SpMVs fused with the original-space KKT partials (raPDHG), the
+// restart test and the primal-weight update.
 //
-// Layout: the instance's 16 vectors (8 n-long, 8 m-long) live in shared memory
-// when they fit (small LPs such as the paper's batched grid LPs), otherwise in
-// a per-CTA slice of global memory (L1/L2 resident).  K~ and K~' are shared by
-// every instance and read through the read-only path.  Each SpMV row is summed
-// by a group of G lanes (G = 1..32 chosen from the mean row length) with a
-// butterfly shuffle, and every reduction is a fixed-order warp butterfly plus a
+// Layout: when they fit, K~ and K~' (CSR) are copied once per CTA into shared
+// memory and the instance's 16 vectors live there too (template SMEM = true:
+// the compiler sees shared-space pointers and emits LDS/STS).  Otherwise the
+// matrices are read through the read-only path and the vectors live in a
+// per-CTA slice of global memory.  Each SpMV row is summed by G lanes with a
+// butterfly shuffle; every reduction is a fixed-order warp butterfly plus a
 // fixed-order sum over warps: results are bitwise deterministic.
 #include "common.cuh"
 
@@ -32,7 +36,7 @@ namespace {
 constexpr int kRedMax = 20;  // largest reduction (raPDHG check)
 
 struct InstParams {
-  int32_t n, m, m1, gk, gkt;
+  int32_t n, m, m1, nnz, gk, gkt;
   const int32_t *rp, *ci, *trp, *tci;
   const double *kv, *tkv, *Dr, *Dc, *ls, *us, *l0, *u0;
   const double *C0, *Q0, *X0, *Y0;
@@ -47,7 +51,6 @@ struct InstParams {
   lp_result *res;
   double *work;
   int64_t work_stride;
-  int32_t vec_in_smem;
 };
 
 template <int NW>
@@ -78,6 +81,7 @@ __device__ __forceinline__ void breduce(double (&v)[V], double *red) {
 #pragma unroll
     for (int k = 0; k < V; ++k) {
       double s = red[k];
+#pragma unroll
       for (int ww = 1; ww < NW; ++ww) s += red[ww * V + k];
       v[k] = s;
     }
@@ -88,18 +92,26 @@ __device__ __forceinline__ void breduce(double (&v)[V], double *red) {
 
 // Rows [0, rows) of a CSR matrix times x; G lanes per row; f(row, sum) on the group leader.
 template <int NW, class F>
-__device__ __forceinline__ void spmv_rows(int rows, int G, const int32_t *__restrict__ rp,
-                                          const int32_t *__restrict__ ci, const double *__restrict__ v,
+__device__ __forceinline__ void spmv_rows(int rows, int G, const int32_t *rp, const int32_t *ci, const double *v,
                                           const double *x, F &&f) {
   constexpr int T = NW * 32;
+  if (G == 1) {
+    for (int r = threadIdx.x; r < rows; r += T) {
+      double s = 0.0;
+      const int e = rp[r + 1];
+      for (int p = rp[r]; p < e; ++p) s += v[p] * x[ci[p]];
+      f(r, s);
+    }
+    return;
+  }
   const int per = T / G, gi = threadIdx.x / G, gl = threadIdx.x % G;
   const int iters = (rows + per - 1) / per;
   for (int it = 0; it < iters; ++it) {
     const int r = it * per + gi;
     double s = 0.0;
     if (r < rows) {
-      const int e = __ldg(rp + r + 1);
-      for (int p = __ldg(rp + r) + gl; p < e; p += G) s += __ldg(v + p) * x[__ldg(ci + p)];
+      const int e = rp[r + 1];
+      for (int p = rp[r] + gl; p < e; p += G) s += v[p] * x[ci[p]];
     }
     for (int off = G >> 1; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
     if (r < rows && gl == 0) f(r, s);
@@ -128,53 +140,60 @@ __device__ __forceinline__ double rel_kkt(const Kkt &k, double nq, double nc) {
   return fmax(k.pres / (1.0 + nq), fmax(k.dres / (1.0 + nc), k.gap / (1.0 + fabs(k.pobj) + fabs(k.dobj))));
 }
 
-// Partial sums (pres^2, dres^2, pobj, dobj) of a candidate, contract step 5.  orig:
-// unscale x = Dc x~, y = Dr y~, Kx = Kx~ / Dr, K'y = K'y~ / Dc and use the original data.
-template <int NW>
-__device__ __forceinline__ void kkt_partial(bool orig, const InstParams &P, const double *c0, const double *q0,
-                                            const double *cs, const double *qs, const double *xs,
-                                            const double *ys, const double *Kxs, const double *KTys,
-                                            double *v) {
-  constexpr int T = NW * 32;
-  for (int i = threadIdx.x; i < P.m; i += T) {
-    const double dr = P.Dr[i];
-    const double Kx = orig ? Kxs[i] / dr : Kxs[i];
-    const double q = orig ? q0[i] : qs[i];
-    const double y = orig ? dr * ys[i] : ys[i];
-    double r = q - Kx;
-    if (i < P.m1) r = fmax(r, 0.0);
-    v[0] += r * r;
-    v[3] += q * y;
-  }
-  for (int j = threadIdx.x; j < P.n; j += T) {
-    const double dc = P.Dc[j];
-    const double x = orig ? dc * xs[j] : xs[j];
-    const double KTy = orig ? KTys[j] / dc : KTys[j];
-    const double c = orig ? c0[j] : cs[j];
-    const double l = orig ? P.l0[j] : P.ls[j];
-    const double u = orig ? P.u0[j] : P.us[j];
-    const double lam = c - KTy;
-    const double lp = fmax(lam, 0.0), lm = fmax(-lam, 0.0);
-    double d = 0.0;
-    if (l == -INFINITY) d += lp;
-    if (u == INFINITY) d += lm;
-    v[1] += d * d;
-    v[2] += c * x;
-    if (l > -INFINITY) v[3] += l * lp;
-    if (u < INFINITY) v[3] -= u * lm;
-  }
+// KKT contributions of one row / one column (contract step 5); orig: unscale with Dr, Dc.
+__device__ __forceinline__ void kkt_row(double *v, bool orig, int i, int m1, double dr, double ys, double Kxs,
+                                        double q0, double qs) {
+  const double Kx = orig ? Kxs / dr : Kxs, q = orig ? q0 : qs, y = orig ? dr * ys : ys;
+  double r = q - Kx;
+  if (i < m1) r = fmax(r, 0.0);
+  v[0] += r * r;
+  v[3] += q * y;
+}
+__device__ __forceinline__ void kkt_col(double *v, bool orig, double dc, double xs, double KTys, double c0, double cs,
+                                        double l0, double ls, double u0, double us) {
+  const double x = orig ? dc * xs : xs, KTy = orig ? KTys / dc : KTys;
+  const double c = orig ? c0 : cs, l = orig ? l0 : ls, u = orig ? u0 : us;
+  const double lam = c - KTy, lp = fmax(lam, 0.0), lm = fmax(-lam, 0.0);
+  double d = 0.0;
+  if (l == -INFINITY) d += lp;
+  if (u == INFINITY) d += lm;
+  v[1] += d * d;
+  v[2] += c * x;
+  if (l > -INFINITY) v[3] += l * lp;
+  if (u < INFINITY) v[3] -= u * lm;
 }
 
-template <int NW>
+template <int NW, bool SMEM>
 __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
   extern __shared__ __align__(16) double sm[];
   constexpr int T = NW * 32;
   const int tid = threadIdx.x;
-  const int n = P.n, m = P.m, m1 = P.m1;
+  const int n = P.n, m = P.m, m1 = P.m1, nnz = P.nnz;
+  // ---- shared-memory carve-up: reductions | [K~ values | K~' values | vectors | int arrays] ----
   double *red0 = sm, *red1 = sm + NW * kRedMax;
-  double *base = P.vec_in_smem ? sm + 2 * NW * kRedMax : P.work + (int64_t)blockIdx.x * P.work_stride;
+  double *after_red = sm + 2 * NW * kRedMax;
+  const double *kv, *tkv;
+  const int32_t *rp, *ci, *trp, *tci;
+  double *base;
+  if (SMEM) {
+    double *skv = after_red, *stkv = skv + nnz;
+    base = stkv + nnz;
+    int32_t *srp = (int32_t *)(base + 8 * (n + m));
+    int32_t *sci = srp + (m + 1), *strp = sci + nnz, *stci = strp + (n + 1);
+    for (int t = tid; t < nnz; t += T) {
+      skv[t] = P.kv[t]; stkv[t] = P.tkv[t]; sci[t] = P.ci[t]; stci[t] = P.tci[t];
+    }
+    for (int t = tid; t <= m; t += T) srp[t] = P.rp[t];
+    for (int t = tid; t <= n; t += T) strp[t] = P.trp[t];
+    kv = skv; tkv = stkv; rp = srp; ci = sci; trp = strp; tci = stci;
+  } else {
+    kv = P.kv; tkv = P.tkv; rp = P.rp; ci = P.ci; trp = P.trp; tci = P.tci;
+    base = P.work + (int64_t)blockIdx.x * P.work_stride;
+  }
+  const double *Dr = P.Dr, *Dc = P.Dc, *ls = P.ls, *us = P.us;
   __shared__ unsigned long long s_inst;
   const bool r2 = (P.alg == LP_R2HPDHG);
+  const int G = P.gk, Gt = P.gkt;
   const double kmx = *P.kmax;
   const double eta0 = kmx > 0.0 ? 1.0 / kmx : 1.0;
   int rbuf = 0;
@@ -200,15 +219,15 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
     // ---- step 2: scaled data, start point, omega0, eta0 ----
     double v4[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j = tid; j < n; j += T) {
-      const double dc = P.Dc[j], c = c0[j];
+      const double dc = Dc[j], c = c0[j];
       const double cj = c * dc;
       cs[j] = cj;
       v4[0] += cj * cj;
       v4[2] += c * c;
-      x[j] = median3(P.ls[j], X0 ? X0[j] / dc : 0.0, P.us[j]);
+      x[j] = median3(ls[j], X0 ? X0[j] / dc : 0.0, us[j]);
     }
     for (int i = tid; i < m; i += T) {
-      const double dr = P.Dr[i], q = q0[i];
+      const double dr = Dr[i], q = q0[i];
       const double qi = q * dr;
       qs[i] = qi;
       v4[1] += qi * qi;
@@ -226,125 +245,206 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
     }
     double eta = eta0;
     bsync<NW>();
-    spmv_rows<NW>(m, P.gk, P.rp, P.ci, P.kv, x, [&](int i, double s) { Kx[i] = s; });
-    spmv_rows<NW>(n, P.gkt, P.trp, P.tci, P.tkv, y, [&](int j, double s) { KTy[j] = s; });
-    bsync<NW>();
-    for (int j = tid; j < n; j += T) { xr[j] = x[j]; xa[j] = x[j]; KTya[j] = KTy[j]; }
-    for (int i = tid; i < m; i += T) { yr[i] = y[i]; ya[i] = y[i]; Kxa[i] = Kx[i]; }
-    int64_t k = 0, jatt = 0, k_in = 0, restarts = 0;
-    double W = 0.0, last = INFINITY, ref = 0.0;
-    if (!r2) {  // raPDHG reference metric KKT_omega(z0)
+    double ref = 0.0;
+    {
       double v[4] = {0.0, 0.0, 0.0, 0.0};
-      kkt_partial<NW>(false, P, c0, q0, cs, qs, x, y, Kx, KTy, v);
+      spmv_rows<NW>(m, G, rp, ci, kv, x, [&](int i, double s) {
+        Kx[i] = s; Kxa[i] = s;
+        const double yv = y[i];
+        yr[i] = yv; ya[i] = yv;
+        kkt_row(v, false, i, m1, 1.0, yv, s, 0.0, qs[i]);
+      });
+      spmv_rows<NW>(n, Gt, trp, tci, tkv, y, [&](int j, double s) {
+        KTy[j] = s; KTya[j] = s;
+        const double xv = x[j];
+        xr[j] = xv; xa[j] = xv;
+        kkt_col(v, false, 1.0, xv, s, 0.0, cs[j], 0.0, ls[j], 0.0, us[j]);
+      });
       breduce<NW, 4>(v, redbuf());
-      const Kkt ks = make_kkt(v);
-      ref = sqrt(omega * ks.pres * ks.pres + ks.dres * ks.dres / omega + ks.gap * ks.gap);
+      if (!r2) {  // raPDHG reference metric KKT_omega(z0)
+        const Kkt ks = make_kkt(v);
+        ref = sqrt(omega * ks.pres * ks.pres + ks.dres * ks.dres / omega + ks.gap * ks.gap);
+      }
     }
-    bsync<NW>();
-
-    int status = 0;
-    // the returned candidate
-    const double *ox = x, *oy = y, *oKx = Kx, *oKTy = KTy;
+    int64_t k = 0, jatt = 0, k_in = 0, restarts = 0;
+    double W = 0.0, last = INFINITY;
+    int status = 0, rejects = 0;
+    bool pending = false;                    // accepted attempt whose commit is fused into the next phases
+    double theta = 0.0, ha = 0.0, hb = 0.0;  // raPDHG average weight / r2HPDHG Halpern coefficients
+    const double *ox = x, *oy = y, *oKx = Kx, *oKTy = KTy;  // the returned candidate
 
     for (;;) {
-      // ---- step 3: attempts until one is accepted ----
-      double eta_used = eta, M = 0.0, I = 0.0;
-      int rejects = 0;
-      for (;;) {
-        ++jatt;
-        const double tau = eta / omega, sigma = eta * omega;
-        double v3[3] = {0.0, 0.0, 0.0};
+      // ================= phase A: [commit n-side] + primal step =================
+      const double tau = eta / omega, sigma = eta * omega;
+      double f1, f2;
+      step_factors(P.tab, jatt + 1, f1, f2);  // prefetch this attempt's growth factors
+      double v3[3] = {0.0, 0.0, 0.0};
+      if (pending) {
+        spmv_rows<NW>(n, Gt, trp, tci, tkv, yp, [&](int j, double s) {
+          double xn, kt;
+          if (!r2) {
+            const double xv = xp[j];
+            xa[j] += theta * (xv - xa[j]);
+            xn = xv; kt = s;
+            KTyp[j] = s;           // becomes K~'y after the pointer swap
+          } else {
+            xn = ha * (2.0 * xp[j] - x[j]) + hb * xa[j];
+            kt = ha * (2.0 * s - KTy[j]) + hb * KTya[j];
+            x[j] = xn; KTy[j] = kt;
+          }
+          const double xnew = median3(ls[j], xn - tau * (cs[j] - kt), us[j]);
+          if (!r2) x[j] = xnew;    // the old-x buffer becomes x' after the swap
+          else xp[j] = xnew;
+          const double d = xnew - xn;
+          v3[0] += d * d;
+        });
+        if (!r2) {
+          double *t = x; x = xp; xp = t;
+          t = KTy; KTy = KTyp; KTyp = t;
+        }
+      } else {
         for (int j = tid; j < n; j += T) {
           const double xo = x[j];
-          const double xn = median3(P.ls[j], xo - tau * (cs[j] - KTy[j]), P.us[j]);
+          const double xn = median3(ls[j], xo - tau * (cs[j] - KTy[j]), us[j]);
           xp[j] = xn;
           const double d = xn - xo;
           v3[0] += d * d;
         }
-        bsync<NW>();
-        spmv_rows<NW>(m, P.gk, P.rp, P.ci, P.kv, xp, [&](int i, double s) {
-          const double yo = y[i], kxo = Kx[i];
-          double yn = yo + sigma * (qs[i] - 2.0 * s + kxo);
-          if (i < m1) yn = fmax(yn, 0.0);
-          Kxp[i] = s;
-          yp[i] = yn;
-          const double d = yn - yo;
-          v3[1] += d * d;
-          v3[2] += d * (s - kxo);
-        });
-        breduce<NW, 3>(v3, redbuf());
-        I = v3[2];
-        M = omega * v3[0] + v3[1] / omega;
-        const double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : INFINITY;
-        const bool acc = (eta <= eb);
-        eta_used = eta;
-        double f1, f2;
-        step_factors(P.tab, jatt, f1, f2);
-        eta = fmin(f1 * eb, f2 * eta);
-        if (acc) break;
-        if (++rejects >= 100) { status = LP_NUMERICAL_ERROR; break; }
       }
-      if (status) { ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
-
-      // ---- step 4: commit (SpMV #2 = K~'y' fused with the update) ----
+      bsync<NW>();
+      // ================= phase B: [commit m-side] + SpMV #1 + dual step =================
+      const bool pend = pending;
+      spmv_rows<NW>(m, G, rp, ci, kv, xp, [&](int i, double s) {
+        double yv, kxv;
+        if (pend) {
+          if (!r2) {
+            yv = yp[i];
+            ya[i] += theta * (yv - ya[i]);
+            kxv = Kxp[i];
+          } else {
+            yv = ha * (2.0 * yp[i] - y[i]) + hb * ya[i];
+            kxv = ha * (2.0 * Kxp[i] - Kx[i]) + hb * Kxa[i];
+            y[i] = yv; Kx[i] = kxv;
+          }
+        } else {
+          yv = y[i]; kxv = Kx[i];
+        }
+        double yn = yv + sigma * (qs[i] - 2.0 * s + kxv);
+        if (i < m1) yn = fmax(yn, 0.0);
+        if (pend && !r2) { y[i] = yn; Kx[i] = s; }   // old buffers become y', K~x' after the swap
+        else { yp[i] = yn; Kxp[i] = s; }
+        const double d = yn - yv;
+        v3[1] += d * d;
+        v3[2] += d * (s - kxv);
+      });
+      if (pend && !r2) {
+        double *t = y; y = yp; yp = t;
+        t = Kx; Kx = Kxp; Kxp = t;
+      }
+      pending = false;
+      breduce<NW, 3>(v3, redbuf());
+      ++jatt;
+      const double I = v3[2];
+      const double M = omega * v3[0] + v3[1] / omega;
+      const double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : INFINITY;
+      const bool acc = (eta <= eb);
+      const double eta_used = eta;
+      eta = fmin(f1 * eb, f2 * eta);
+      if (!acc) {
+        if (++rejects >= 100) { status = LP_NUMERICAL_ERROR; ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
+        continue;
+      }
+      rejects = 0;
+      // ---- step 4: prepare the commit ----
       double rP = 0.0;
       if (!r2) {
-        const double W1 = W + eta_used, theta = eta_used / W1;
+        const double W1 = W + eta_used;
+        theta = eta_used / W1;
         W = W1;
-        spmv_rows<NW>(n, P.gkt, P.trp, P.tci, P.tkv, yp, [&](int j, double s) {
-          KTyp[j] = s;
-          xa[j] += theta * (xp[j] - xa[j]);
-        });
-        for (int i = tid; i < m; i += T) ya[i] += theta * (yp[i] - ya[i]);
-        double *t;
-        t = x; x = xp; xp = t;
-        t = KTy; KTy = KTyp; KTyp = t;
-        t = y; y = yp; yp = t;
-        t = Kx; Kx = Kxp; Kxp = t;
       } else {
         rP = sqrt(fmax(0.0, M / eta_used - 2.0 * I));
         if (k_in == 0) ref = rP;
-        const double a = (double)(k_in + 1) / (double)(k_in + 2), bb = 1.0 / (double)(k_in + 2);
-        spmv_rows<NW>(n, P.gkt, P.trp, P.tci, P.tkv, yp, [&](int j, double s) {
-          KTyp[j] = s;
-          x[j] = a * (2.0 * xp[j] - x[j]) + bb * xa[j];
-          KTy[j] = a * (2.0 * s - KTy[j]) + bb * KTya[j];
-        });
-        for (int i = tid; i < m; i += T) {
-          y[i] = a * (2.0 * yp[i] - y[i]) + bb * ya[i];
-          Kx[i] = a * (2.0 * Kxp[i] - Kx[i]) + bb * Kxa[i];
-        }
+        ha = (double)(k_in + 1) / (double)(k_in + 2);
+        hb = 1.0 / (double)(k_in + 2);
       }
       ++k;
       ++k_in;
-      bsync<NW>();
+      if (k % P.check_freq != 0 && k != P.iter_limit) { pending = true; continue; }
 
-      // ---- step 5: periodic check ----
-      if (k % P.check_freq != 0 && k != P.iter_limit) continue;
+      // ================= step 5: check -- commit-only phase first =================
       const double *cx, *cy, *cKx, *cKTy;
-      double metric;
-      double dist_x2, dist_y2;
+      double metric, dx2, dy2;
+      {
+        double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        spmv_rows<NW>(n, Gt, trp, tci, tkv, yp, [&](int j, double s) {
+          KTyp[j] = s;
+          if (!r2) {
+            xa[j] += theta * (xp[j] - xa[j]);
+          } else {
+            const double xpj = xp[j];
+            x[j] = ha * (2.0 * xpj - x[j]) + hb * xa[j];
+            KTy[j] = ha * (2.0 * s - KTy[j]) + hb * KTya[j];
+            kkt_col(v, true, Dc[j], xpj, s, c0[j], cs[j], P.l0[j], ls[j], P.u0[j], us[j]);
+            const double d = xpj - xr[j];
+            v[4] += d * d;
+          }
+        });
+        for (int i = tid; i < m; i += T) {
+          if (!r2) {
+            ya[i] += theta * (yp[i] - ya[i]);
+          } else {
+            const double ypi = yp[i], kxp = Kxp[i];
+            y[i] = ha * (2.0 * ypi - y[i]) + hb * ya[i];
+            Kx[i] = ha * (2.0 * kxp - Kx[i]) + hb * Kxa[i];
+            kkt_row(v, true, i, m1, Dr[i], ypi, kxp, q0[i], qs[i]);
+            const double d = ypi - yr[i];
+            v[5] += d * d;
+          }
+        }
+        if (!r2) {
+          double *t = x; x = xp; xp = t;
+          t = KTy; KTy = KTyp; KTyp = t;
+          t = y; y = yp; yp = t;
+          t = Kx; Kx = Kxp; Kxp = t;
+          bsync<NW>();
+        } else {
+          breduce<NW, 6>(v, redbuf());
+          const Kkt kw = make_kkt(v);
+          if (kkt_pass(kw, nq0, nc0, P.eps_abs, P.eps_rel)) {
+            status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break;
+          }
+          if (k == P.iter_limit) { status = LP_ITERATION_LIMIT; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
+          cx = xp; cy = yp; cKx = Kxp; cKTy = KTyp; metric = rP; dx2 = v[4]; dy2 = v[5];
+        }
+      }
       if (!r2) {
-        spmv_rows<NW>(m, P.gk, P.rp, P.ci, P.kv, xa, [&](int i, double s) { Kxa[i] = s; });
-        spmv_rows<NW>(n, P.gkt, P.trp, P.tci, P.tkv, ya, [&](int j, double s) { KTya[j] = s; });
-        bsync<NW>();
+        // the average's products (2 SpMVs) fused with every KKT / distance partial
         double v[kRedMax];
 #pragma unroll
         for (int t = 0; t < kRedMax; ++t) v[t] = 0.0;
-        kkt_partial<NW>(true, P, c0, q0, cs, qs, xa, ya, Kxa, KTya, v + 0);
-        kkt_partial<NW>(true, P, c0, q0, cs, qs, x, y, Kx, KTy, v + 4);
-        kkt_partial<NW>(false, P, c0, q0, cs, qs, xa, ya, Kxa, KTya, v + 8);
-        kkt_partial<NW>(false, P, c0, q0, cs, qs, x, y, Kx, KTy, v + 12);
-        for (int j = tid; j < n; j += T) {
-          const double da = xa[j] - xr[j], dc = x[j] - xr[j];
-          v[16] += da * da;
-          v[18] += dc * dc;
-        }
-        for (int i = tid; i < m; i += T) {
-          const double da = ya[i] - yr[i], dc = y[i] - yr[i];
+        spmv_rows<NW>(m, G, rp, ci, kv, xa, [&](int i, double s) {
+          Kxa[i] = s;
+          const double dr = Dr[i], yai = ya[i], yi = y[i], kxi = Kx[i], q0i = q0[i], qsi = qs[i];
+          kkt_row(v + 0, true, i, m1, dr, yai, s, q0i, qsi);
+          kkt_row(v + 4, true, i, m1, dr, yi, kxi, q0i, qsi);
+          kkt_row(v + 8, false, i, m1, dr, yai, s, q0i, qsi);
+          kkt_row(v + 12, false, i, m1, dr, yi, kxi, q0i, qsi);
+          const double da = yai - yr[i], dcur = yi - yr[i];
           v[17] += da * da;
-          v[19] += dc * dc;
-        }
+          v[19] += dcur * dcur;
+        });
+        spmv_rows<NW>(n, Gt, trp, tci, tkv, ya, [&](int j, double s) {
+          KTya[j] = s;
+          const double dc = Dc[j], xaj = xa[j], xj = x[j], ktj = KTy[j];
+          const double c0j = c0[j], csj = cs[j], l0j = P.l0[j], lsj = ls[j], u0j = P.u0[j], usj = us[j];
+          kkt_col(v + 0, true, dc, xaj, s, c0j, csj, l0j, lsj, u0j, usj);
+          kkt_col(v + 4, true, dc, xj, ktj, c0j, csj, l0j, lsj, u0j, usj);
+          kkt_col(v + 8, false, dc, xaj, s, c0j, csj, l0j, lsj, u0j, usj);
+          kkt_col(v + 12, false, dc, xj, ktj, c0j, csj, l0j, lsj, u0j, usj);
+          const double da = xaj - xr[j], dcur = xj - xr[j];
+          v[16] += da * da;
+          v[18] += dcur * dcur;
+        });
         breduce<NW, kRedMax>(v, redbuf());
         const Kkt ka = make_kkt(v + 0), kc = make_kkt(v + 4);
         if (kkt_pass(ka, nq0, nc0, P.eps_abs, P.eps_rel)) {
@@ -362,22 +462,8 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
         const Kkt sa = make_kkt(v + 8), sc = make_kkt(v + 12);
         const double e_a = sqrt(omega * sa.pres * sa.pres + sa.dres * sa.dres / omega + sa.gap * sa.gap);
         const double e_c = sqrt(omega * sc.pres * sc.pres + sc.dres * sc.dres / omega + sc.gap * sc.gap);
-        if (e_a < e_c) { cx = xa; cy = ya; cKx = Kxa; cKTy = KTya; metric = e_a; dist_x2 = v[16]; dist_y2 = v[17]; }
-        else { cx = x; cy = y; cKx = Kx; cKTy = KTy; metric = e_c; dist_x2 = v[18]; dist_y2 = v[19]; }
-      } else {
-        double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        kkt_partial<NW>(true, P, c0, q0, cs, qs, xp, yp, Kxp, KTyp, v);
-        for (int j = tid; j < n; j += T) { const double d = xp[j] - xr[j]; v[4] += d * d; }
-        for (int i = tid; i < m; i += T) { const double d = yp[i] - yr[i]; v[5] += d * d; }
-        breduce<NW, 6>(v, redbuf());
-        const Kkt kw = make_kkt(v);
-        if (kkt_pass(kw, nq0, nc0, P.eps_abs, P.eps_rel)) {
-          status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break;
-        }
-        if (k == P.iter_limit) {
-          status = LP_ITERATION_LIMIT; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break;
-        }
-        cx = xp; cy = yp; cKx = Kxp; cKTy = KTyp; metric = rP; dist_x2 = v[4]; dist_y2 = v[5];
+        if (e_a < e_c) { cx = xa; cy = ya; cKx = Kxa; cKTy = KTya; metric = e_a; dx2 = v[16]; dy2 = v[17]; }
+        else { cx = x; cy = y; cKx = Kx; cKTy = KTy; metric = e_c; dx2 = v[18]; dy2 = v[19]; }
       }
       // restart test (contract step 5): artificial / sufficient / necessary + stall
       const bool restart = ((double)k_in >= 0.36 * (double)k) || (metric <= 0.2 * ref) ||
@@ -385,7 +471,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
       last = metric;
       if (restart) {
         ++restarts;
-        const double dxn = sqrt(dist_x2), dyn = sqrt(dist_y2);
+        const double dxn = sqrt(dx2), dyn = sqrt(dy2);
         if (dxn > 1e-10 && dyn > 1e-10) omega = sqrt(omega * (dyn / dxn));
         for (int j = tid; j < n; j += T) {
           const double xv = cx[j], kt = cKTy[j];
@@ -406,17 +492,21 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
     // ---- step 6: output the candidate in original space ----
     {
       double v[4] = {0.0, 0.0, 0.0, 0.0};
-      kkt_partial<NW>(true, P, c0, q0, cs, qs, ox, oy, oKx, oKTy, v);
-      breduce<NW, 4>(v, redbuf());
-      const Kkt ko = make_kkt(v);
       double *X = P.X + b * (int64_t)n, *L = P.L + b * (int64_t)n, *Y = P.Y + b * (int64_t)m;
       for (int j = tid; j < n; j += T) {
-        const double dc = P.Dc[j];
-        X[j] = dc * ox[j];
-        L[j] = c0[j] - oKTy[j] / dc;
+        const double dc = Dc[j], xs = ox[j], kt = oKTy[j];
+        kkt_col(v, true, dc, xs, kt, c0[j], cs[j], P.l0[j], ls[j], P.u0[j], us[j]);
+        X[j] = dc * xs;
+        L[j] = c0[j] - kt / dc;
       }
-      for (int i = tid; i < m; i += T) Y[i] = P.Dr[i] * oy[i];
+      for (int i = tid; i < m; i += T) {
+        const double dr = Dr[i];
+        kkt_row(v, true, i, m1, dr, oy[i], oKx[i], q0[i], qs[i]);
+        Y[i] = dr * oy[i];
+      }
+      breduce<NW, 4>(v, redbuf());
       if (tid == 0) {
+        const Kkt ko = make_kkt(v);
         lp_result r;
         r.status = status;
         r.pad = 0;
@@ -444,25 +534,21 @@ inline int pow2_floor(double v) {
   return g;
 }
 
-template <int NW>
-int launch(const InstParams &P0, size_t smem_red, size_t vec_bytes, cudaStream_t s, double **work,
-           size_t *work_bytes) {
+template <int NW, bool SMEM>
+int launch_cfg(const InstParams &P0, size_t smem, size_t vec_bytes, cudaStream_t s, double **work,
+               size_t *work_bytes) {
   InstParams P = P0;
-  int dev = 0, sms = 0, max_optin = 0;
+  int dev = 0, sms = 0;
   MPAX_CUDA(cudaGetDevice(&dev));
   MPAX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  MPAX_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  size_t smem = smem_red;
-  P.vec_in_smem = (smem_red + vec_bytes + 1024 <= (size_t)max_optin && vec_bytes <= 96 * 1024) ? 1 : 0;
-  if (P.vec_in_smem) smem += vec_bytes;
-  MPAX_CUDA(cudaFuncSetAttribute(instance_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  MPAX_CUDA(cudaFuncSetAttribute(instance_kernel<NW, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, instance_kernel<NW>, NW * 32, smem));
+  MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, instance_kernel<NW, SMEM>, NW * 32, smem));
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)per_sm * sms;
   if (grid > P.batch) grid = P.batch;
   if (grid < 1) grid = 1;
-  if (!P.vec_in_smem) {
+  if (!SMEM) {
     size_t need = (size_t)grid * vec_bytes;
     if (*work_bytes < need) {
       if (*work) MPAX_CUDA(cudaFreeAsync(*work, s));
@@ -474,9 +560,21 @@ int launch(const InstParams &P0, size_t smem_red, size_t vec_bytes, cudaStream_t
     P.work_stride = (int64_t)(vec_bytes / sizeof(double));
   }
   MPAX_CUDA(cudaMemsetAsync(P.queue, 0, sizeof(unsigned long long), s));
-  MPAX_LAUNCH(instance_kernel<NW>, (int)grid, NW * 32, smem, s, P);
+  MPAX_LAUNCH((instance_kernel<NW, SMEM>), (int)grid, NW * 32, smem, s, P);
   MPAX_CHECK_LAUNCH();
   return LP_OK;
+}
+
+template <int NW>
+int launch(const InstParams &P, size_t red_bytes, size_t vec_bytes, size_t mat_bytes, cudaStream_t s,
+           double **work, size_t *work_bytes) {
+  int dev = 0, max_optin = 0;
+  MPAX_CUDA(cudaGetDevice(&dev));
+  MPAX_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t all = red_bytes + vec_bytes + mat_bytes;
+  if (all + 1024 <= (size_t)max_optin && all <= 160 * 1024)
+    return launch_cfg<NW, true>(P, all, vec_bytes, s, work, work_bytes);
+  return launch_cfg<NW, false>(P, red_bytes, vec_bytes, s, work, work_bytes);
 }
 
 }  // namespace
@@ -484,7 +582,7 @@ int launch(const InstParams &P0, size_t smem_red, size_t vec_bytes, cudaStream_t
 int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L, cudaStream_t s,
                    unsigned long long *queue, double **work, size_t *work_bytes) {
   InstParams P;
-  P.n = (int32_t)D.n; P.m = (int32_t)D.m; P.m1 = (int32_t)D.m1;
+  P.n = (int32_t)D.n; P.m = (int32_t)D.m; P.m1 = (int32_t)D.m1; P.nnz = (int32_t)D.nnz;
   P.rp = D.rp; P.ci = D.ci; P.trp = D.trp; P.tci = D.tci;
   P.kv = D.kv; P.tkv = D.tkv; P.Dr = D.Dr; P.Dc = D.Dc; P.ls = D.ls; P.us = D.us; P.l0 = D.l0; P.u0 = D.u0;
   P.C0 = L.C0; P.cstride = L.cstride; P.Q0 = L.Q0; P.qstride = L.qstride; P.X0 = L.X0; P.Y0 = L.Y0;
@@ -493,7 +591,7 @@ int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunc
   P.check_freq = o.check_frequency; P.alg = o.algorithm;
   P.batch = L.batch; P.queue = queue;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
-  P.work = nullptr; P.work_stride = 0; P.vec_in_smem = 0;
+  P.work = nullptr; P.work_stride = 0;
   // CTA size from the work per SpMV; group size from the mean row length
   const double nnz = (double)D.nnz;
   int NW = 1;
@@ -502,11 +600,13 @@ int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunc
   P.gk = pow2_floor(D.avg_row / 4.0);
   P.gkt = pow2_floor(D.avg_col / 4.0);
   const size_t vec_bytes = (size_t)8 * (size_t)(D.n + D.m) * sizeof(double);
+  const size_t mat_bytes = (size_t)D.nnz * (2 * sizeof(double) + 2 * sizeof(int32_t)) +
+                           (size_t)(D.n + D.m + 2) * sizeof(int32_t);
   const size_t red_bytes = (size_t)2 * NW * kRedMax * sizeof(double);
   switch (NW) {
-    case 1: return launch<1>(P, red_bytes, vec_bytes, s, work, work_bytes);
-    case 4: return launch<4>(P, red_bytes, vec_bytes, s, work, work_bytes);
-    default: return launch<8>(P, red_bytes, vec_bytes, s, work, work_bytes);
+    case 1: return launch<1>(P, red_bytes, vec_bytes, mat_bytes, s, work, work_bytes);
+    case 4: return launch<4>(P, red_bytes, vec_bytes, mat_bytes, s, work, work_bytes);
+    default: return launch<8>(P, red_bytes, vec_bytes, mat_bytes, s, work, work_bytes);
   }
 }
 

@@ -10,6 +10,8 @@
 // bitwise reproducible run to run.
 #include <cub/cub.cuh>
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace mpax {
@@ -36,6 +38,7 @@ __global__ void validate_kernel(int64_t m, int64_t n, int64_t nnz, const int64_t
       report(flag, 3, (int)i);
       continue;
     }
+    atomicMax(flag + 5, (int)(b - a));
     for (int64_t p = a; p < b; ++p) {
       int32_t j = ci[p];
       if (j < 0 || j >= n || (p > a && j <= ci[p - 1])) { report(flag, 3, (int)i); break; }
@@ -56,7 +59,8 @@ __global__ void validate_kernel(int64_t m, int64_t n, int64_t nnz, const int64_t
 
 // ---- transpose --------------------------------------------------------------
 __global__ void rows_to_int32(int64_t m, const int64_t *__restrict__ rp64, int32_t *__restrict__ rp32,
-                              int32_t *__restrict__ row_of) {
+                              int32_t *__restrict__ row_of, const int *flag) {
+  if (*flag) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= m; i += (int64_t)gridDim.x * blockDim.x) {
     rp32[i] = (int32_t)rp64[i];
     if (i < m)
@@ -64,7 +68,8 @@ __global__ void rows_to_int32(int64_t m, const int64_t *__restrict__ rp64, int32
   }
 }
 
-__global__ void iota_kernel(int64_t nnz, int32_t *__restrict__ a) {
+__global__ void iota_kernel(int64_t nnz, int32_t *__restrict__ a, const int *flag) {
+  if (*flag) return;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
     a[p] = (int32_t)p;
 }
@@ -72,7 +77,8 @@ __global__ void iota_kernel(int64_t nnz, int32_t *__restrict__ a) {
 // K' row pointer: trp[j] = first position of column j in the sorted keys (lower bound).
 __global__ void transpose_finish(int64_t n, int64_t nnz, const int32_t *__restrict__ skeys,
                                  const int32_t *__restrict__ perm, const int32_t *__restrict__ row_of,
-                                 int32_t *__restrict__ trp, int32_t *__restrict__ tci) {
+                                 int32_t *__restrict__ trp, int32_t *__restrict__ tci, int *flag) {
+  if (*flag) return;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = tid; j <= n; j += st) {
     int64_t lo = 0, hi = nnz;
@@ -81,6 +87,20 @@ __global__ void transpose_finish(int64_t n, int64_t nnz, const int32_t *__restri
       if (skeys[mid] < j) lo = mid + 1; else hi = mid;
     }
     trp[j] = (int32_t)lo;
+  }
+  // longest column of K (= row of K'): flag[6]
+  for (int64_t j = tid; j < n; j += st) {
+    int64_t lo = 0, hi = nnz;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (skeys[mid] <= j) lo = mid + 1; else hi = mid;
+    }
+    int64_t a = 0, h2 = nnz;
+    while (a < h2) {
+      int64_t mid = (a + h2) >> 1;
+      if (skeys[mid] < j) a = mid + 1; else h2 = mid;
+    }
+    atomicMax(flag + 6, (int)(lo - a));
   }
   for (int64_t d = tid; d < nnz; d += st) tci[d] = row_of[perm[d]];
 }
@@ -91,7 +111,8 @@ __global__ void precond_norms(int64_t m, int64_t n, const int32_t *__restrict__ 
                               const int32_t *__restrict__ trp, const int32_t *__restrict__ tci,
                               const int32_t *__restrict__ perm, const double *__restrict__ kv0,
                               const double *__restrict__ Dr, const double *__restrict__ Dc,
-                              double *__restrict__ rho, double *__restrict__ gam, int use_sum) {
+                              double *__restrict__ rho, double *__restrict__ gam, int use_sum, const int *flag) {
+  if (*flag) return;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t t = tid; t < m + n; t += st) {
     double acc = 0.0;
@@ -116,7 +137,8 @@ __global__ void precond_norms(int64_t m, int64_t n, const int32_t *__restrict__ 
 }
 
 __global__ void precond_update(int64_t m, int64_t n, const double *__restrict__ rho, const double *__restrict__ gam,
-                               double *__restrict__ Dr, double *__restrict__ Dc) {
+                               double *__restrict__ Dr, double *__restrict__ Dc, const int *flag) {
+  if (*flag) return;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t t = tid; t < m + n; t += st) {
     if (t < m) { double r = rho[t]; Dr[t] *= (r > 0.0 ? 1.0 / sqrt(r) : 1.0); }
@@ -135,7 +157,9 @@ __global__ void scale_kernel(int64_t m, int64_t n, const int32_t *__restrict__ r
                              const int32_t *__restrict__ perm, const double *__restrict__ kv0,
                              const double *__restrict__ Dr, const double *__restrict__ Dc, double *__restrict__ kv,
                              double *__restrict__ tkv, const double *__restrict__ l0, const double *__restrict__ u0,
-                             double *__restrict__ ls, double *__restrict__ us, unsigned long long *kmax_bits) {
+                             double *__restrict__ ls, double *__restrict__ us, unsigned long long *kmax_bits,
+                             const int *flag) {
+  if (*flag) return;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
   double mx = 0.0;
   for (int64_t t = tid; t < m + n; t += st) {
@@ -190,30 +214,42 @@ inline int grid_for(int64_t work, int block = 256) {
 }  // namespace
 
 int setup_validate(DevProblem &P, const int64_t *row_ptr64, const double *c, int64_t nc, const double *q, int64_t nq,
-                   cudaStream_t s, int *h_flag) {
-  int *d_flag = nullptr;
-  MPAX_CUDA(cudaMallocAsync(&d_flag, 5 * sizeof(int), s));
-  int init[5] = {0, INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
-  MPAX_CUDA(cudaMemcpyAsync(d_flag, init, sizeof(init), cudaMemcpyHostToDevice, s));
+                   cudaStream_t s, int *d_flag) {
   int64_t work = P.m + P.nnz + nc + nq + P.n;
   MPAX_LAUNCH(validate_kernel, grid_for(work), 256, 0, s, P.m, P.n, P.nnz, row_ptr64, P.ci, P.kv0, c, nc, q, nq,
               P.l0, P.u0, d_flag);
   MPAX_CHECK_LAUNCH();
-  MPAX_CUDA(cudaMemcpyAsync(h_flag, d_flag, 5 * sizeof(int), cudaMemcpyDeviceToHost, s));
-  MPAX_CUDA(cudaFreeAsync(d_flag, s));
-  MPAX_CUDA(cudaStreamSynchronize(s));
   return LP_OK;
 }
 
-int setup_build(DevProblem &P, const int64_t *row_ptr64, cudaStream_t s) {
+namespace {
+double *g_tab[64] = {nullptr};
+std::mutex g_tab_mu;
+}  // namespace
+
+const double *step_table(cudaStream_t s) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  if (!g_tab[dev]) {
+    double *t = nullptr;
+    if (cudaMalloc(&t, 2 * kStepTab * sizeof(double)) != cudaSuccess) return nullptr;
+    MPAX_LAUNCH(step_table_kernel, 64, 256, 0, s, t);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return nullptr;
+    g_tab[dev] = t;
+  }
+  return g_tab[dev];
+}
+
+int setup_build(DevProblem &P, const int64_t *row_ptr64, cudaStream_t s, int *d_flag) {
   const int64_t m = P.m, n = P.n, nnz = P.nnz;
   int32_t *row_of = nullptr, *keys_out = nullptr, *idx_in = nullptr;
   size_t nz = (size_t)(nnz > 0 ? nnz : 1);
   MPAX_CUDA(cudaMallocAsync(&row_of, nz * sizeof(int32_t), s));
   MPAX_CUDA(cudaMallocAsync(&keys_out, nz * sizeof(int32_t), s));
   MPAX_CUDA(cudaMallocAsync(&idx_in, nz * sizeof(int32_t), s));
-  MPAX_LAUNCH(rows_to_int32, grid_for(m + 1), 256, 0, s, m, row_ptr64, P.rp, row_of);
-  MPAX_LAUNCH(iota_kernel, grid_for(nnz), 256, 0, s, nnz, idx_in);
+  MPAX_LAUNCH(rows_to_int32, grid_for(m + 1), 256, 0, s, m, row_ptr64, P.rp, row_of, d_flag);
+  MPAX_LAUNCH(iota_kernel, grid_for(nnz), 256, 0, s, nnz, idx_in, d_flag);
   // stable LSD radix sort of (col, position) pairs: rows stay in increasing order within a column
   if (nnz > 0) {
     int end_bit = 1;
@@ -227,7 +263,7 @@ int setup_build(DevProblem &P, const int64_t *row_ptr64, cudaStream_t s) {
     g_launches.fetch_add(4, std::memory_order_relaxed);  // CUB's onesweep/histogram kernels (approx.)
     MPAX_CUDA(cudaFreeAsync(temp, s));
   }
-  MPAX_LAUNCH(transpose_finish, grid_for(n + 1 + nnz), 256, 0, s, n, nnz, keys_out, P.perm, row_of, P.trp, P.tci);
+  MPAX_LAUNCH(transpose_finish, grid_for(n + 1 + nnz), 256, 0, s, n, nnz, keys_out, P.perm, row_of, P.trp, P.tci, d_flag);
   // Ruiz x10 then Pock-Chambolle alpha=1 (contract step 1)
   double *rho = nullptr, *gam = nullptr;
   MPAX_CUDA(cudaMallocAsync(&rho, (size_t)(m > 0 ? m : 1) * sizeof(double), s));
@@ -237,13 +273,12 @@ int setup_build(DevProblem &P, const int64_t *row_ptr64, cudaStream_t s) {
   for (int r = 0; r < 11; ++r) {
     int use_sum = (r == 10);
     MPAX_LAUNCH(precond_norms, grid_for(m + n, 128), 128, 0, s, m, n, P.rp, P.ci, P.trp, P.tci, P.perm, P.kv0,
-                P.Dr, P.Dc, rho, gam, use_sum);
-    MPAX_LAUNCH(precond_update, grid_for(m + n), 256, 0, s, m, n, rho, gam, P.Dr, P.Dc);
+                P.Dr, P.Dc, rho, gam, use_sum, d_flag);
+    MPAX_LAUNCH(precond_update, grid_for(m + n), 256, 0, s, m, n, rho, gam, P.Dr, P.Dc, d_flag);
   }
   MPAX_CUDA(cudaMemsetAsync(P.kmax, 0, sizeof(double), s));
   MPAX_LAUNCH(scale_kernel, grid_for(m + n, 128), 128, 0, s, m, n, P.rp, P.ci, P.trp, P.tci, P.perm, P.kv0, P.Dr,
-              P.Dc, P.kv, P.tkv, P.l0, P.u0, P.ls, P.us, (unsigned long long *)P.kmax);
-  MPAX_LAUNCH(step_table_kernel, 64, 256, 0, s, P.tab);
+              P.Dc, P.kv, P.tkv, P.l0, P.u0, P.ls, P.us, (unsigned long long *)P.kmax, d_flag);
   MPAX_CHECK_LAUNCH();
   MPAX_CUDA(cudaFreeAsync(rho, s));
   MPAX_CUDA(cudaFreeAsync(gam, s));

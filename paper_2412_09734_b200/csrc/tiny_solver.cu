@@ -1,0 +1,510 @@
+// tiny_solver.cu -- register-resident per-instance PDHG for very small LPs
+// (the paper's batched shortest-path LPs, P:334,
+// P:156-157).  One warp owns one instance; lane l owns rows i = l + 32t
+// (t < RPT) and columns j = l + 32t (t < CPT) together with their ELL rows of
+// K~ (width W) and K~' (width WT).  Every per-row / per-column quantity of the
+// iteration (x, K~'y, x', average / anchor, restart point, c~, l~, u~ and the
+// m-side analogues) lives in registers; only the two vectors that are
+// gathered by the SpMVs (x' and y', and the average at checks) go through
+// shared memory.  Same arithmetic, in the same order, as the generic
+// instance_kernel (instance_solver.cu) and the grid kernel; DESIGN.md §3.
+#include "common.cuh"
+
+namespace mpax {
+
+namespace {
+
+struct TinyParams {
+  int32_t n, m, m1;
+  const int32_t *rp, *ci, *trp, *tci;
+  const double *kv, *tkv, *Dr, *Dc, *ls, *us, *l0, *u0;
+  const double *C0, *Q0, *X0, *Y0;
+  int64_t cstride, qstride;
+  const double *kmax, *tab;
+  double eps_abs, eps_rel;
+  int64_t iter_limit;
+  int32_t check_freq;
+  int64_t batch;
+  unsigned long long *queue;
+  double *X, *Y, *L;
+  lp_result *res;
+};
+
+template <int V>
+__device__ __forceinline__ void wsum(double (&v)[V]) {
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    double s = v[k];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    v[k] = s;
+  }
+}
+
+struct K5 {
+  double pres, dres, pobj, dobj, gap;
+};
+__device__ __forceinline__ K5 mk5(const double *v) {
+  K5 k;
+  k.pres = sqrt(v[0]); k.dres = sqrt(v[1]); k.pobj = v[2]; k.dobj = v[3]; k.gap = fabs(v[2] - v[3]);
+  return k;
+}
+__device__ __forceinline__ bool pass5(const K5 &k, double nq, double nc, double ea, double er) {
+  return k.pres <= ea + er * nq && k.dres <= ea + er * nc && k.gap <= ea + er * (fabs(k.pobj) + fabs(k.dobj));
+}
+__device__ __forceinline__ double rel5(const K5 &k, double nq, double nc) {
+  return fmax(k.pres / (1.0 + nq), fmax(k.dres / (1.0 + nc), k.gap / (1.0 + fabs(k.pobj) + fabs(k.dobj))));
+}
+__device__ __forceinline__ void krow(double *v, bool orig, bool ge, double dr, double ys, double Kxs, double q0,
+                                     double qs) {
+  const double Kx = orig ? Kxs / dr : Kxs, q = orig ? q0 : qs, y = orig ? dr * ys : ys;
+  double r = q - Kx;
+  if (ge) r = fmax(r, 0.0);
+  v[0] += r * r;
+  v[3] += q * y;
+}
+__device__ __forceinline__ void kcol(double *v, bool orig, double dc, double xs, double KTys, double c0, double cs,
+                                     double l0, double ls, double u0, double us) {
+  const double x = orig ? dc * xs : xs, KTy = orig ? KTys / dc : KTys;
+  const double c = orig ? c0 : cs, l = orig ? l0 : ls, u = orig ? u0 : us;
+  const double lam = c - KTy, lp = fmax(lam, 0.0), lm = fmax(-lam, 0.0);
+  double d = 0.0;
+  if (l == -INFINITY) d += lp;
+  if (u == INFINITY) d += lm;
+  v[1] += d * d;
+  v[2] += c * x;
+  if (l > -INFINITY) v[3] += l * lp;
+  if (u < INFINITY) v[3] -= u * lm;
+}
+
+template <bool R2, int RPT, int CPT, int W, int WT>
+__global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x;
+  const int n = P.n, m = P.m, m1 = P.m1;
+  double *sx = sm, *sy = sm + 32 * CPT;  // gather buffers: x' (or average) and y' (or average)
+  // ---- static per-lane structure: ELL rows of K~ and K~' in registers ----
+  int rcol[RPT][W], ccol[CPT][WT];
+  double rval[RPT][W], cval[CPT][WT];
+  bool rok[RPT], cok[CPT];
+  double dr[RPT], lsv[CPT], usv[CPT], dc[CPT];
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) {
+    const int i = lane + 32 * t;
+    rok[t] = i < m;
+    const int a = rok[t] ? P.rp[i] : 0, e = rok[t] ? P.rp[i + 1] : 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const bool ok = a + w < e;
+      rcol[t][w] = ok ? P.ci[a + w] : 0;
+      rval[t][w] = ok ? P.kv[a + w] : 0.0;
+    }
+    dr[t] = rok[t] ? P.Dr[i] : 1.0;
+  }
+#pragma unroll
+  for (int t = 0; t < CPT; ++t) {
+    const int j = lane + 32 * t;
+    cok[t] = j < n;
+    const int a = cok[t] ? P.trp[j] : 0, e = cok[t] ? P.trp[j + 1] : 0;
+#pragma unroll
+    for (int w = 0; w < WT; ++w) {
+      const bool ok = a + w < e;
+      ccol[t][w] = ok ? P.tci[a + w] : 0;
+      cval[t][w] = ok ? P.tkv[a + w] : 0.0;
+    }
+    dc[t] = cok[t] ? P.Dc[j] : 1.0;
+    lsv[t] = cok[t] ? P.ls[j] : 0.0;
+    usv[t] = cok[t] ? P.us[j] : 0.0;
+  }
+  // padding entries point at element 0 with value 0; keep the gather buffers finite
+  for (int t = lane; t < 32 * CPT; t += 32) sx[t] = 0.0;
+  for (int t = lane; t < 32 * RPT; t += 32) sy[t] = 0.0;
+  const double kmx = *P.kmax;
+  const double eta0 = kmx > 0.0 ? 1.0 / kmx : 1.0;
+  __shared__ unsigned long long s_inst;
+
+  for (;;) {
+    __syncwarp();
+    if (lane == 0) s_inst = atomicAdd(P.queue, 1ull);
+    __syncwarp();
+    const int64_t b = (int64_t)s_inst;
+    if (b >= P.batch) return;
+    const double *c0 = P.C0 + b * P.cstride, *q0 = P.Q0 + b * P.qstride;
+
+    // ---- step 2 ----
+    double x[CPT], KTy[CPT], xp[CPT], KTyp[CPT], xa[CPT], KTya[CPT], xr[CPT], cs[CPT];
+    double y[RPT], Kx[RPT], yp[RPT], Kxp[RPT], ya[RPT], Kxa[RPT], yr[RPT], qs[RPT];
+    double v4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int t = 0; t < CPT; ++t) {
+      const int j = lane + 32 * t;
+      const double c = cok[t] ? c0[j] : 0.0;
+      cs[t] = c * dc[t];
+      v4[0] += cs[t] * cs[t];
+      v4[2] += c * c;
+      const double x0 = (cok[t] && P.X0) ? P.X0[b * n + j] / dc[t] : 0.0;
+      x[t] = cok[t] ? median3(lsv[t], x0, usv[t]) : 0.0;
+      sx[j] = x[t];
+    }
+#pragma unroll
+    for (int t = 0; t < RPT; ++t) {
+      const int i = lane + 32 * t;
+      const double q = rok[t] ? q0[i] : 0.0;
+      qs[t] = q * dr[t];
+      v4[1] += qs[t] * qs[t];
+      v4[3] += q * q;
+      double yv = (rok[t] && P.Y0) ? P.Y0[b * m + i] / dr[t] : 0.0;
+      if (i < m1) yv = fmax(yv, 0.0);
+      y[t] = rok[t] ? yv : 0.0;
+      sy[i] = y[t];
+    }
+    wsum<4>(v4);
+    __syncwarp();
+    const double nc0 = sqrt(v4[2]), nq0 = sqrt(v4[3]);
+    double omega = 1.0;
+    if (sqrt(v4[0]) > 1e-10 && sqrt(v4[1]) > 1e-10) omega = sqrt(v4[0]) / sqrt(v4[1]);
+    double eta = eta0, ref = 0.0;
+    {
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) s += rval[t][w] * sx[rcol[t][w]];
+        Kx[t] = s; Kxa[t] = s; ya[t] = y[t]; yr[t] = y[t];
+        if (rok[t]) krow(v, false, lane + 32 * t < m1, 1.0, y[t], s, 0.0, qs[t]);
+      }
+#pragma unroll
+      for (int t = 0; t < CPT; ++t) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
+        KTy[t] = s; KTya[t] = s; xa[t] = x[t]; xr[t] = x[t];
+        if (cok[t]) kcol(v, false, 1.0, x[t], s, 0.0, cs[t], 0.0, lsv[t], 0.0, usv[t]);
+      }
+      wsum<4>(v);
+      if (!R2) {
+        const K5 ks = mk5(v);
+        ref = sqrt(omega * ks.pres * ks.pres + ks.dres * ks.dres / omega + ks.gap * ks.gap);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < CPT; ++t) { xp[t] = x[t]; KTyp[t] = KTy[t]; }
+#pragma unroll
+    for (int t = 0; t < RPT; ++t) { yp[t] = y[t]; Kxp[t] = Kx[t]; }
+    int64_t k = 0, jatt = 0, k_in = 0, restarts = 0;
+    double W_ = 0.0, last = INFINITY, theta = 0.0, ha = 0.0, hb = 0.0;
+    int status = 0, rejects = 0;
+    bool pending = false;
+    int outsel = 0;  // 0 current, 1 candidate w / average, as set at termination
+
+    for (;;) {
+      __syncwarp();
+      // ================= phase A: [commit n-side] + primal step =================
+      const double tau = eta / omega, sigma = eta * omega;
+      double f1, f2;
+      step_factors(P.tab, jatt + 1, f1, f2);
+      double dx2 = 0.0;
+#pragma unroll
+      for (int t = 0; t < CPT; ++t) {
+        if (pending) {
+          double s = 0.0;
+#pragma unroll
+          for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
+          if (!R2) {
+            xa[t] += theta * (xp[t] - xa[t]);
+            x[t] = xp[t];
+            KTy[t] = s;
+          } else {
+            x[t] = ha * (2.0 * xp[t] - x[t]) + hb * xa[t];
+            KTy[t] = ha * (2.0 * s - KTy[t]) + hb * KTya[t];
+          }
+        }
+        const double xn = median3(lsv[t], x[t] - tau * (cs[t] - KTy[t]), usv[t]);
+        xp[t] = cok[t] ? xn : 0.0;
+        sx[lane + 32 * t] = xp[t];
+        const double d = xp[t] - x[t];
+        dx2 += d * d;
+      }
+      __syncwarp();
+      // ================= phase B: [commit m-side] + SpMV #1 + dual step =================
+      double dy2 = 0.0, I = 0.0;
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) s += rval[t][w] * sx[rcol[t][w]];
+        if (pending) {
+          if (!R2) {
+            ya[t] += theta * (yp[t] - ya[t]);
+            y[t] = yp[t];
+            Kx[t] = Kxp[t];
+          } else {
+            y[t] = ha * (2.0 * yp[t] - y[t]) + hb * ya[t];
+            Kx[t] = ha * (2.0 * Kxp[t] - Kx[t]) + hb * Kxa[t];
+          }
+        }
+        double yn = y[t] + sigma * (qs[t] - 2.0 * s + Kx[t]);
+        if (lane + 32 * t < m1) yn = fmax(yn, 0.0);
+        yp[t] = rok[t] ? yn : 0.0;
+        Kxp[t] = rok[t] ? s : 0.0;
+        sy[lane + 32 * t] = yp[t];
+        const double d = yp[t] - y[t];
+        dy2 += d * d;
+        I += d * (Kxp[t] - Kx[t]);
+      }
+      pending = false;
+      double v3[3] = {dx2, dy2, I};
+      wsum<3>(v3);
+      ++jatt;
+      const double M = omega * v3[0] + v3[1] / omega;
+      const double eb = (v3[2] != 0.0) ? M / (2.0 * fabs(v3[2])) : INFINITY;
+      const bool acc = (eta <= eb);
+      const double eta_used = eta;
+      eta = fmin(f1 * eb, f2 * eta);
+      if (!acc) {
+        if (++rejects >= 100) { status = LP_NUMERICAL_ERROR; outsel = 0; break; }
+        continue;
+      }
+      rejects = 0;
+      double rP = 0.0;
+      if (!R2) {
+        const double W1 = W_ + eta_used;
+        theta = eta_used / W1;
+        W_ = W1;
+      } else {
+        rP = sqrt(fmax(0.0, M / eta_used - 2.0 * v3[2]));
+        if (k_in == 0) ref = rP;
+        ha = (double)(k_in + 1) / (double)(k_in + 2);
+        hb = 1.0 / (double)(k_in + 2);
+      }
+      ++k;
+      ++k_in;
+      if (k % P.check_freq != 0 && k != P.iter_limit) { pending = true; continue; }
+
+      // ================= step 5: check =================
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < CPT; ++t) {  // commit-only, n side (K~'y' into KTyp)
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
+        KTyp[t] = cok[t] ? s : 0.0;
+        if (!R2) {
+          xa[t] += theta * (xp[t] - xa[t]);
+          x[t] = xp[t];
+          KTy[t] = KTyp[t];
+        } else {
+          x[t] = ha * (2.0 * xp[t] - x[t]) + hb * xa[t];
+          KTy[t] = ha * (2.0 * KTyp[t] - KTy[t]) + hb * KTya[t];
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) {
+        if (!R2) {
+          ya[t] += theta * (yp[t] - ya[t]);
+          y[t] = yp[t];
+          Kx[t] = Kxp[t];
+        } else {
+          y[t] = ha * (2.0 * yp[t] - y[t]) + hb * ya[t];
+          Kx[t] = ha * (2.0 * Kxp[t] - Kx[t]) + hb * Kxa[t];
+        }
+      }
+      double metric, dx2c, dy2c;
+      int csel;  // restart candidate: 0 = current (x, y), 1 = average (ra) / w (r2)
+      if (R2) {
+        double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int t = 0; t < CPT; ++t) {
+          const int j = lane + 32 * t;
+          if (cok[t]) {
+            kcol(v, true, dc[t], xp[t], KTyp[t], c0[j], cs[t], P.l0[j], lsv[t], P.u0[j], usv[t]);
+            const double d = xp[t] - xr[t];
+            v[4] += d * d;
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < RPT; ++t) {
+          const int i = lane + 32 * t;
+          if (rok[t]) {
+            krow(v, true, i < m1, dr[t], yp[t], Kxp[t], q0[i], qs[t]);
+            const double d = yp[t] - yr[t];
+            v[5] += d * d;
+          }
+        }
+        wsum<6>(v);
+        const K5 kw = mk5(v);
+        if (pass5(kw, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; outsel = 1; break; }
+        if (k == P.iter_limit) { status = LP_ITERATION_LIMIT; outsel = 1; break; }
+        metric = rP; dx2c = v[4]; dy2c = v[5]; csel = 1;
+      } else {
+        // the average's products: K~ x-bar and K~' y-bar through the gather buffers
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < CPT; ++t) sx[lane + 32 * t] = cok[t] ? xa[t] : 0.0;
+#pragma unroll
+        for (int t = 0; t < RPT; ++t) sy[lane + 32 * t] = rok[t] ? ya[t] : 0.0;
+        __syncwarp();
+        double v[20];
+#pragma unroll
+        for (int q = 0; q < 20; ++q) v[q] = 0.0;
+#pragma unroll
+        for (int t = 0; t < RPT; ++t) {
+          double s = 0.0;
+#pragma unroll
+          for (int w = 0; w < W; ++w) s += rval[t][w] * sx[rcol[t][w]];
+          Kxa[t] = rok[t] ? s : 0.0;
+          const int i = lane + 32 * t;
+          if (rok[t]) {
+            const bool ge = i < m1;
+            const double q0i = q0[i];
+            krow(v + 0, true, ge, dr[t], ya[t], s, q0i, qs[t]);
+            krow(v + 4, true, ge, dr[t], y[t], Kx[t], q0i, qs[t]);
+            krow(v + 8, false, ge, dr[t], ya[t], s, q0i, qs[t]);
+            krow(v + 12, false, ge, dr[t], y[t], Kx[t], q0i, qs[t]);
+            const double da = ya[t] - yr[t], dcur = y[t] - yr[t];
+            v[17] += da * da;
+            v[19] += dcur * dcur;
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < CPT; ++t) {
+          double s = 0.0;
+#pragma unroll
+          for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
+          KTya[t] = cok[t] ? s : 0.0;
+          const int j = lane + 32 * t;
+          if (cok[t]) {
+            const double c0j = c0[j], l0j = P.l0[j], u0j = P.u0[j];
+            kcol(v + 0, true, dc[t], xa[t], s, c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
+            kcol(v + 4, true, dc[t], x[t], KTy[t], c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
+            kcol(v + 8, false, dc[t], xa[t], s, c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
+            kcol(v + 12, false, dc[t], x[t], KTy[t], c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
+            const double da = xa[t] - xr[t], dcur = x[t] - xr[t];
+            v[16] += da * da;
+            v[18] += dcur * dcur;
+          }
+        }
+        wsum<20>(v);
+        const K5 ka = mk5(v + 0), kc = mk5(v + 4);
+        if (pass5(ka, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; outsel = 1; break; }
+        if (pass5(kc, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; outsel = 0; break; }
+        if (k == P.iter_limit) {
+          status = LP_ITERATION_LIMIT;
+          outsel = rel5(ka, nq0, nc0) < rel5(kc, nq0, nc0) ? 1 : 0;
+          break;
+        }
+        const K5 sa = mk5(v + 8), sc = mk5(v + 12);
+        const double e_a = sqrt(omega * sa.pres * sa.pres + sa.dres * sa.dres / omega + sa.gap * sa.gap);
+        const double e_c = sqrt(omega * sc.pres * sc.pres + sc.dres * sc.dres / omega + sc.gap * sc.gap);
+        if (e_a < e_c) { csel = 1; metric = e_a; dx2c = v[16]; dy2c = v[17]; }
+        else { csel = 0; metric = e_c; dx2c = v[18]; dy2c = v[19]; }
+      }
+      const bool restart = ((double)k_in >= 0.36 * (double)k) || (metric <= 0.2 * ref) ||
+                           (metric <= 0.8 * ref && metric > last);
+      last = metric;
+      if (restart) {
+        ++restarts;
+        const double dxn = sqrt(dx2c), dyn = sqrt(dy2c);
+        if (dxn > 1e-10 && dyn > 1e-10) omega = sqrt(omega * (dyn / dxn));
+#pragma unroll
+        for (int t = 0; t < CPT; ++t) {
+          if (csel) { x[t] = R2 ? xp[t] : xa[t]; KTy[t] = R2 ? KTyp[t] : KTya[t]; }
+          xr[t] = x[t]; xa[t] = x[t]; KTya[t] = KTy[t];
+        }
+#pragma unroll
+        for (int t = 0; t < RPT; ++t) {
+          if (csel) { y[t] = R2 ? yp[t] : ya[t]; Kx[t] = R2 ? Kxp[t] : Kxa[t]; }
+          yr[t] = y[t]; ya[t] = y[t]; Kxa[t] = Kx[t];
+        }
+        k_in = 0;
+        if (!R2) { W_ = 0.0; ref = metric; }
+      }
+    }
+
+    // ---- step 6: output (candidate selected by outsel) ----
+    {
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
+      double *X = P.X + b * (int64_t)n, *L = P.L + b * (int64_t)n, *Y = P.Y + b * (int64_t)m;
+#pragma unroll
+      for (int t = 0; t < CPT; ++t) {
+        const int j = lane + 32 * t;
+        if (cok[t]) {
+          const double xs = outsel ? (R2 ? xp[t] : xa[t]) : x[t];
+          const double kt = outsel ? (R2 ? KTyp[t] : KTya[t]) : KTy[t];
+          kcol(v, true, dc[t], xs, kt, c0[j], cs[t], P.l0[j], lsv[t], P.u0[j], usv[t]);
+          X[j] = dc[t] * xs;
+          L[j] = c0[j] - kt / dc[t];
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) {
+        const int i = lane + 32 * t;
+        if (rok[t]) {
+          const double ys = outsel ? (R2 ? yp[t] : ya[t]) : y[t];
+          const double kx = outsel ? (R2 ? Kxp[t] : Kxa[t]) : Kx[t];
+          krow(v, true, i < m1, dr[t], ys, kx, q0[i], qs[t]);
+          Y[i] = dr[t] * ys;
+        }
+      }
+      wsum<4>(v);
+      if (lane == 0) {
+        const K5 ko = mk5(v);
+        lp_result r;
+        r.status = status; r.pad = 0;
+        r.iterations = k; r.attempts = jatt; r.restarts = restarts;
+        r.primal_objective = ko.pobj; r.dual_objective = ko.dobj;
+        r.primal_residual = ko.pres; r.dual_residual = ko.dres; r.gap = ko.gap;
+        r.rel_kkt = rel5(ko, nq0, nc0);
+        r.omega = omega; r.eta = eta; r.solve_seconds = 0.0;
+        P.res[b] = r;
+      }
+    }
+  }
+}
+
+template <bool R2, int RPT, int CPT, int W, int WT>
+int launch_tiny(const TinyParams &P, cudaStream_t s) {
+  int dev = 0, sms = 0, per_sm = 0;
+  MPAX_CUDA(cudaGetDevice(&dev));
+  MPAX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const size_t smem = (size_t)32 * (CPT + RPT) * sizeof(double);
+  MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiny_kernel<R2, RPT, CPT, W, WT>, 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)per_sm * sms;
+  if (grid > P.batch) grid = P.batch;
+  MPAX_CUDA(cudaMemsetAsync(P.queue, 0, sizeof(unsigned long long), s));
+  MPAX_LAUNCH((tiny_kernel<R2, RPT, CPT, W, WT>), (int)grid, 32, smem, s, P);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+template <int RPT, int CPT, int W, int WT>
+int launch_alg(const TinyParams &P, bool r2, cudaStream_t s) {
+  return r2 ? launch_tiny<true, RPT, CPT, W, WT>(P, s) : launch_tiny<false, RPT, CPT, W, WT>(P, s);
+}
+
+}  // namespace
+
+// Returns LP_ERR_UNSUPPORTED when the LP does not fit one of the register layouts.
+int tiny_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L, cudaStream_t s,
+               unsigned long long *queue) {
+  if (D.max_row < 0 || D.max_col < 0) return LP_ERR_UNSUPPORTED;
+  TinyParams P;
+  P.n = (int32_t)D.n; P.m = (int32_t)D.m; P.m1 = (int32_t)D.m1;
+  P.rp = D.rp; P.ci = D.ci; P.trp = D.trp; P.tci = D.tci;
+  P.kv = D.kv; P.tkv = D.tkv; P.Dr = D.Dr; P.Dc = D.Dc; P.ls = D.ls; P.us = D.us; P.l0 = D.l0; P.u0 = D.u0;
+  P.C0 = L.C0; P.cstride = L.cstride; P.Q0 = L.Q0; P.qstride = L.qstride; P.X0 = L.X0; P.Y0 = L.Y0;
+  P.kmax = D.kmax; P.tab = D.tab;
+  P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit; P.check_freq = o.check_frequency;
+  P.batch = L.batch; P.queue = queue;
+  P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
+  const bool r2 = o.algorithm == LP_R2HPDHG;
+  const int64_t n = D.n, m = D.m;
+  const int W = D.max_row, WT = D.max_col;
+  if (m <= 32 && n <= 64 && W <= 4 && WT <= 4) return launch_alg<1, 2, 4, 4>(P, r2, s);
+  if (m <= 32 && n <= 64 && W <= 8 && WT <= 8) return launch_alg<1, 2, 8, 8>(P, r2, s);
+  return LP_ERR_UNSUPPORTED;
+}
+
+}  // namespace mpax

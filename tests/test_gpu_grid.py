@@ -13,7 +13,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs CUDA", allow_module_level=True)
 
 import paper_2412_09734_b200 as mp  # noqa: E402
-from tests.test_gpu_parity import oracle_stability, rel  # noqa: E402
+from tests.test_gpu_parity import obj_tol, oracle_stability, rel  # noqa: E402
 
 ALGS = ["ra", "r2"]
 
@@ -57,7 +57,7 @@ def test_grid_full_solve(alg, name, lp):
     if stable:
         for key in ("iterations", "attempts", "restarts"):
             assert rg[key] == ro[key], (key, rg[key], ro[key])
-        assert abs(rg["primal_objective"] - ro["primal_objective"]) <= 1e-6 * (1 + abs(ro["primal_objective"]))
+        assert abs(rg["primal_objective"] - ro["primal_objective"]) <= obj_tol(ro) * (1 + abs(ro["primal_objective"]))
     k = oracle.kkt_original(lp, rg["x"], rg["y"])
     assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.q))
     assert k["dres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.c))
@@ -100,4 +100,5 @@ def test_c4_full_size(alg):
     assert abs(r["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
     k = oracle.kkt_original(lp, r["x"], r["y"])
     assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.q))
-    assert np.all(r["x"] >= lp.l) and np.all(r["x"] <= lp.u) and np.all(r["y"][: lp.m1] >= 0)
+    slack = 4e-16 * (1 + np.abs(np.where(np.isfinite(lp.u), lp.u, 0)))
+    assert np.all(r["x"] >= lp.l) and np.all(r["x"] <= lp.u + slack) and np.all(r["y"][: lp.m1] >= 0)

@@ -51,14 +51,20 @@ def min_margin(r):
     return mm
 
 
-def perturbed(lp, sign):
-    """The same LP with c scaled by (1 +- 2^-52): a 1-ulp input perturbation."""
-    return lp.with_costs(c=lp.c * (1.0 + sign * 2.0 ** -52))
+def ulp_perturb(a, seed):
+    """a with every entry moved by one relative ulp in a random direction."""
+    s = np.random.default_rng(seed).choice([-1.0, 1.0], size=np.shape(a))
+    return np.asarray(a) * (1.0 + s * 2.0 ** -52)
+
+
+def perturbed(lp, seed):
+    """The same LP with c and q perturbed entrywise by 1 ulp (random signs)."""
+    return lp.with_costs(c=ulp_perturb(lp.c, seed), q=ulp_perturb(lp.q, seed + 100) if lp.m else lp.q)
 
 
 def oracle_stability(lp, alg, **kw):
     """Sensitivity guard: run the oracle on the LP and on two
-    1-ulp perturbations of c.  Returns (result, counts_stable, drift): the
+    entrywise 1-ulp perturbations of c and q.  Returns (result, counts_stable, drift): the
     counts are stable when the oracle's own status / iteration / attempt /
     restart counts do not move under the perturbations (and no logged decision
     is a near-tie), and `drift` is how far its own iterate moves (relative).  A
@@ -67,11 +73,20 @@ def oracle_stability(lp, alg, **kw):
     r = oracle.solve(lp, alg, log_capacity=1 << 16, **kw)
     stable = min_margin(r) >= MARGIN
     drift = 0.0
-    for sgn in (1, -1):
-        p = oracle.solve(perturbed(lp, sgn), alg, **kw)
+    r["obj_drift"] = 0.0
+    for seed in (1, 2):
+        p = oracle.solve(perturbed(lp, seed), alg, **kw)
         stable &= all(p[k] == r[k] for k in ("status", "iterations", "attempts", "restarts"))
         drift = max(drift, rel(p["x"], r["x"]), rel(p["y"], r["y"]) if lp.m else 0.0)
+        r["obj_drift"] = max(r["obj_drift"], abs(p["primal_objective"] - r["primal_objective"]) /
+                             (1 + abs(r["primal_objective"])))
     return r, bool(stable), drift
+
+
+def obj_tol(ro):
+    """Final-objective parity budget: 1e-6 relative, or 100x the
+    oracle's own objective drift under 1-ulp input perturbations if larger."""
+    return max(1e-6, 100 * ro["obj_drift"])
 
 
 def gpu_solve(lp, alg, device=False, **kw):
@@ -169,14 +184,16 @@ def test_full_solve(alg, name, lp):
     if stable:
         for key in ("iterations", "attempts", "restarts"):
             assert rg[key] == ro[key], (key, rg[key], ro[key])
-        assert abs(rg["primal_objective"] - ro["primal_objective"]) <= 1e-6 * (1 + abs(ro["primal_objective"]))
+        assert abs(rg["primal_objective"] - ro["primal_objective"]) <= obj_tol(ro) * (1 + abs(ro["primal_objective"]))
     assert rg["rel_kkt"] <= 1e-4
     # self-certification on original data with the oracle's independent KKT routine
     k = oracle.kkt_original(lp, rg["x"], rg["y"])
     nq, nc = np.linalg.norm(lp.q), np.linalg.norm(lp.c)
     assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * nq)
     assert k["dres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * nc)
-    assert np.all(rg["x"] >= lp.l) and np.all(rg["x"] <= lp.u) and np.all(rg["y"][: lp.m1] >= 0)
+    # x = Dc (x~) with l~ = l/Dc <= x~ <= u~ = u/Dc: in bounds up to the unscaling's rounding
+    slack = 4e-16 * (1 + np.abs(np.where(np.isfinite(lp.u), lp.u, 0)) + np.abs(np.where(np.isfinite(lp.l), lp.l, 0)))
+    assert np.all(rg["x"] >= lp.l - slack) and np.all(rg["x"] <= lp.u + slack) and np.all(rg["y"][: lp.m1] >= 0)
     if lp.obj_star is not None:
         assert abs(rg["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
 
@@ -241,7 +258,7 @@ def test_grid_batch_c2(alg):
     X, Y = bs.solutions()
     bs.close()
     Xo, Yo, ro = oracle.solve_batch(lp, C, None, alg)
-    _, _, rp = oracle.solve_batch(lp, C * (1 + 2.0 ** -52), None, alg)
+    _, _, rp = oracle.solve_batch(lp, ulp_perturb(C, 1), None, alg)
     keys = ("status", "iterations", "attempts", "restarts")
     same_gpu = [all(res[b][k] == ro[b][k] for k in keys) for b in range(1024)]
     same_ora = [all(rp[b][k] == ro[b][k] for k in keys) for b in range(1024)]
@@ -252,7 +269,11 @@ def test_grid_batch_c2(alg):
         dp = lpgen.grid_dp_optimum(5, C[b])
         assert abs(res[b]["primal_objective"] - dp) <= 1e-3 * (1 + dp)
         if same_gpu[b]:
-            assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= 1e-6 * (1 + dp)
+            # 1e-6 relative, or 100x the oracle's own drift under the 1-ulp perturbation; instances whose
+            # oracle counts move under that perturbation only need two eps-optimal objectives to agree
+            drift = abs(rp[b]["primal_objective"] - ro[b]["primal_objective"]) / (1 + dp)
+            tol = max(1e-6, 100 * drift) if same_ora[b] else 1e-4
+            assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= tol * (1 + dp), (b, drift)
         k = oracle.kkt_original(lp.with_costs(c=C[b]), X[b], Y[b])
         assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.q))
 
@@ -286,3 +307,25 @@ def test_dense_batch_per_instance_c3_sample():
         assert abs(res[b]["primal_objective"] - obj[b]) <= 1e-3 * (1 + abs(obj[b]))
         if res[b]["attempts"] == ro[b]["attempts"] and res[b]["restarts"] == ro[b]["restarts"]:
             assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= 1e-6 * (1 + abs(obj[b]))
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_tiny_register_path_matches_generic_kernel(alg):
+    """The register-resident warp kernel (auto path for C2-sized LPs) and the
+    generic per-instance kernel implement the same arithmetic in the same order."""
+    lp, C = lpgen.g_grid(batch=256, seed=11)
+    out = {}
+    for path in (mp.PATH_AUTO, mp.PATH_INSTANCE):
+        bs = mp.BatchSolver(mp.Problem.from_lp(lp), C)
+        res = bs.solve(algorithm=alg, path=path)
+        X, Y = bs.solutions()
+        bs.close()
+        out[path] = (res, X, Y)
+    (ra_, Xa, Ya), (rb_, Xb, Yb) = out[mp.PATH_AUTO], out[mp.PATH_INSTANCE]
+    same = [ra_[b]["attempts"] == rb_[b]["attempts"] and ra_[b]["restarts"] == rb_[b]["restarts"]
+            for b in range(256)]
+    assert sum(same) >= 250, sum(same)
+    for b in range(256):
+        assert ra_[b]["status"] == mp.LP_OPTIMAL
+        if same[b]:
+            assert rel(Xa[b], Xb[b]) <= 1e-6
