@@ -45,7 +45,7 @@ WORKLOAD = ("C2: batch of 1024 PyEPO-style 5x5 shortest-path LPs (40 arcs, 25 fl
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=1024)
@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--large-m", type=int, default=100_000)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
+
+
+def log(msg):
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
 
 
 def dist_env():
@@ -230,7 +234,7 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     def step(prob, Cx, X, Y, mem, alg=args.alg):
         bs = mp.BatchSolver(prob, Cx)
-        res = bs.solve(algorithm=alg)
+        res = bs.solve(algorithm=alg, iteration_limit=200_000)   # safety net; every instance must be OPTIMAL
         bs.solutions(memory=mem, X=X, Y=Y)
         bs.close()
         return res
@@ -254,6 +258,7 @@ def run_ours(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    log("warm-up")
     for _ in range(max(args.warmup, 3)):
         step(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE)
         step(prob_p, C_p, X_p, Y_p, mp.LP_HOST)
@@ -264,16 +269,19 @@ def run_ours(args):
     sampler.start()
     n0 = mp.launch_count()
     barrier()
+    log("timed region (device-resident)")
     ms, results = timed(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, args.steps, True)
     barrier()
     launches = mp.launch_count() - n0
     clocks = sampler.stop()
     # ---- end-to-end timed region (host buffers through the C ABI) ----
     barrier()
+    log("timed region (end to end)")
     ms_e2e, _ = timed(prob_p, C_p, X_p, Y_p, mp.LP_HOST, args.steps, False)
     barrier()
     # ---- secondary: the other algorithm on the same workload (context, not the headline) ----
     alg2 = "r2" if args.alg == "ra" else "ra"
+    log("secondary algorithm")
     step(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, alg2)
     barrier()
     ms2, res2 = timed(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, args.secondary_steps, True, alg2)
@@ -333,8 +341,10 @@ def run_ours(args):
         "secondary": secondary,
     }
     if not args.no_large:
+        log("large-LP leg")
         line["large_lp"] = large_lp_leg(mp, torch, dev, stream, peaks, args)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        log("cpu baseline")
         line["cpu_baseline"] = cpu_baseline(lp, C, args.alg, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -364,10 +374,11 @@ def large_lp_leg(mp, torch, dev, stream, peaks, args):
     hbm = peaks.get("hbm_gbs", 6546.6)
     for alg in ("ra", "r2"):
         with mp.Solver(prob) as s:
-            s.solve(algorithm=alg, path=mp.PATH_GRID)                       # warm-up
+            log(f"large leg {alg}: warm-up")
+            s.solve(algorithm=alg, path=mp.PATH_GRID, iteration_limit=20_000)   # warm-up
             best = None
             for _ in range(3):
-                r = s.solve(algorithm=alg, path=mp.PATH_GRID)
+                r = s.solve(algorithm=alg, path=mp.PATH_GRID, iteration_limit=20_000)
                 best = r if best is None or r["solve_seconds"] < best["solve_seconds"] else best
         pair, acc = attempt_bytes(lp.n, lp.m, lp.nnz, alg)
         rej = best["attempts"] - best["iterations"]

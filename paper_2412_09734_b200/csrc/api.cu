@@ -5,6 +5,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -41,6 +42,37 @@ struct lp_handle_s {
 namespace {
 
 std::once_flag g_pool_once;
+
+// Pinned host buffers (result / flag staging) are recycled across handles:
+// cudaMallocHost costs far more than a whole small-batch solve.
+std::mutex g_pin_mu;
+std::multimap<size_t, void *> g_pin_free;
+
+size_t pin_class(size_t bytes) {
+  size_t c = 256;
+  while (c < bytes) c <<= 1;
+  return c;
+}
+void *pin_get(size_t bytes) {
+  const size_t c = pin_class(bytes);
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_free.find(c);
+    if (it != g_pin_free.end()) {
+      void *p = it->second;
+      g_pin_free.erase(it);
+      return p;
+    }
+  }
+  void *p = nullptr;
+  if (cudaMallocHost(&p, c) != cudaSuccess) return nullptr;
+  return p;
+}
+void pin_put(void *p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.emplace(pin_class(bytes), p);
+}
 
 void init_pool() {
   std::call_once(g_pool_once, [] {
@@ -80,11 +112,11 @@ void free_handle(lp_handle h) {
   cudaStream_t s = h->stream;
   for (void *p : {(void *)h->arena, (void *)h->X0, (void *)h->Y0, (void *)h->work})
     if (p) cudaFreeAsync(p, s);
-  if (h->h_res) cudaFreeHost(h->h_res);
-  if (h->h_flag) cudaFreeHost(h->h_flag);
+  // every D2H into the pinned buffers was followed by a stream sync, so they can be recycled now
+  pin_put(h->h_res, (size_t)h->batch * sizeof(lp_result));
+  pin_put(h->h_flag, 8 * sizeof(int));
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
-  cudaStreamSynchronize(s);
   delete h;
 }
 
@@ -160,9 +192,9 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
   }
   P.tab = const_cast<double *>(step_table(s));
   if (!P.tab) return cleanup(fail(LP_ERR_CUDA, "line-search table"));
-  if (cudaMallocHost((void **)&h->h_res, (size_t)batch * sizeof(lp_result)) != cudaSuccess ||
-      cudaMallocHost((void **)&h->h_flag, 8 * sizeof(int)) != cudaSuccess)
-    return cleanup(fail(LP_ERR_OUT_OF_MEMORY, "pinned host buffers"));
+  h->h_res = (lp_result *)pin_get((size_t)batch * sizeof(lp_result));
+  h->h_flag = (int *)pin_get(8 * sizeof(int));
+  if (!h->h_res || !h->h_flag) return cleanup(fail(LP_ERR_OUT_OF_MEMORY, "pinned host buffers"));
   if (cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess)
     return cleanup(fail(LP_ERR_CUDA, "event create"));
   auto cp = [&](void *dst, const void *src, size_t bytes) -> int {
@@ -182,8 +214,12 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
     memcpy(h->h_flag, init, sizeof(init));
     CK(cp(h->d_flag, h->h_flag, sizeof(init)));
   }
-  CK(setup_validate(P, h->rp64, h->C0, perC ? batch * n : n, h->Q0, perQ ? batch * m : m, s, h->d_flag));
-  CK(setup_build(P, h->rp64, s, h->d_flag));
+  if (setup_small_ok(P)) {
+    CK(setup_small(P, h->rp64, h->C0, perC ? batch * n : n, h->Q0, perQ ? batch * m : m, s, h->d_flag));
+  } else {
+    CK(setup_validate(P, h->rp64, h->C0, perC ? batch * n : n, h->Q0, perQ ? batch * m : m, s, h->d_flag));
+    CK(setup_build(P, h->rp64, s, h->d_flag));
+  }
   CK(cp(h->h_flag, h->d_flag, 8 * sizeof(int)));
   if (cudaStreamSynchronize(s) != cudaSuccess) return cleanup(fail(LP_ERR_CUDA, "setup"));
   const int *flag = h->h_flag;

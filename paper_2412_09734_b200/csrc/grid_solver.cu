@@ -24,6 +24,8 @@
 // mean row length.  Results are bitwise deterministic.
 #include <cooperative_groups.h>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -93,16 +95,34 @@ __device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p);
 __device__ __forceinline__ int32_t ld_stream(const int32_t *p) { return __ldcs(p); }
 
 // Sum of row r of a CSR matrix times x, G lanes per row (all lanes get the sum).
+// Each lane takes its entries four at a time (index and value loads first, then
+// the four gathers, then the FMAs) so that twelve loads are in flight per lane;
+// two interleaved accumulators.  Fixed order: deterministic.
 __device__ __forceinline__ double row_dot(int64_t r, bool valid, int G, int gl, const int32_t *__restrict__ rp,
                                           const int32_t *__restrict__ ci, const double *__restrict__ v,
                                           const double *x) {
-  double s = 0.0;
+  double s0 = 0.0, s1 = 0.0;
   if (valid) {
     const int32_t e = __ldg(rp + r + 1);
-    int32_t p = __ldg(rp + r) + gl;
-#pragma unroll 4
-    for (; p < e; p += G) s += ld_stream(v + p) * x[ld_stream(ci + p)];
+    for (int32_t p = __ldg(rp + r) + gl; p < e; p += 4 * G) {
+      int32_t c[4];
+      double w[4], xv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int32_t q = p + k * G;
+        const bool ok = q < e;
+        c[k] = ok ? ld_stream(ci + q) : 0;
+        w[k] = ok ? ld_stream(v + q) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) xv[k] = (p + k * G < e) ? x[c[k]] : 0.0;
+      s0 += w[0] * xv[0];
+      s1 += w[1] * xv[1];
+      s0 += w[2] * xv[2];
+      s1 += w[3] * xv[3];
+    }
   }
+  double s = s0 + s1;
   for (int off = G >> 1; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
   return s;
 }
@@ -125,26 +145,35 @@ __device__ __forceinline__ void block_partials(double (&v)[V], double *part, dou
   }
 }
 
-// After a grid barrier: every CTA sums the per-CTA partials in the same fixed order.
+// After a grid barrier: every CTA sums the per-CTA partials in the same fixed order
+// (warp k reduces value k: lanes take CTAs b = lane + 32i into 4 interleaved
+// accumulators, then a butterfly; identical code and data in every CTA).
 template <int V>
 __device__ __forceinline__ void grid_totals(double (&t)[V], const double *part, double *s_tot) {
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x < 32) {
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      double s = 0.0;
-      for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(part + (int64_t)b * kNP + k);
-#pragma unroll
-      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
-      if (lane == 0) s_tot[k] = s;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nb = (int)gridDim.x;
+  for (int k = w; k < V; k += kBS / 32) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int b = lane;
+    for (; b + 96 < nb; b += 128) {
+      a0 += __ldcg(part + (int64_t)b * kNP + k);
+      a1 += __ldcg(part + (int64_t)(b + 32) * kNP + k);
+      a2 += __ldcg(part + (int64_t)(b + 64) * kNP + k);
+      a3 += __ldcg(part + (int64_t)(b + 96) * kNP + k);
     }
+    for (; b < nb; b += 32) a0 += __ldcg(part + (int64_t)b * kNP + k);
+    double s = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    if (lane == 0) s_tot[k] = s;
   }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < V; ++k) t[k] = s_tot[k];
 }
 
-__global__ void __launch_bounds__(kBS) grid_kernel(GridParams P) {
+template <int MINB>
+__global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double s_red[kBS / 32][kNP];
   __shared__ double s_tot[kNP];
@@ -245,21 +274,26 @@ __global__ void __launch_bounds__(kBS) grid_kernel(GridParams P) {
     if (pending) {
       for (int64_t it = 0; it < col_iters; ++it) {
         const int64_t j = it * ngrpt + grpt;
-        const bool ok = j < n;
+        const bool ok = j < n, lead = ok && glt == 0;
+        // operands of the epilogue, loaded before the dot so they are in flight with it
+        double o_xp = 0.0, o_xa = 0.0, o_x = 0.0, o_kt = 0.0, o_kta = 0.0, o_cs = 0.0, o_ls = 0.0, o_us = 0.0;
+        if (lead) {
+          o_xp = xp[j]; o_xa = xa[j]; o_cs = cs[j]; o_ls = P.ls[j]; o_us = P.us[j];
+          if (r2) { o_x = x[j]; o_kt = KTy[j]; o_kta = KTya[j]; }
+        }
         const double s = row_dot(j, ok, Gt, glt, P.trp, P.tci, P.tkv, yp);
-        if (ok && glt == 0) {
+        if (lead) {
           double xn, kt;
           if (!r2) {
-            const double xv = xp[j];
-            xa[j] += theta * (xv - xa[j]);
-            xn = xv; kt = s;
+            xa[j] = o_xa + theta * (o_xp - o_xa);
+            xn = o_xp; kt = s;
             KTyp[j] = s;           // becomes KTy after the pointer swap
           } else {
-            xn = ha * (2.0 * xp[j] - x[j]) + hb * xa[j];
-            kt = ha * (2.0 * s - KTy[j]) + hb * KTya[j];
+            xn = ha * (2.0 * o_xp - o_x) + hb * o_xa;
+            kt = ha * (2.0 * s - o_kt) + hb * o_kta;
             x[j] = xn; KTy[j] = kt;
           }
-          const double xnew = median3(P.ls[j], xn - tau * (cs[j] - kt), P.us[j]);
+          const double xnew = median3(o_ls, xn - tau * (o_cs - kt), o_us);
           if (!r2) x[j] = xnew;    // x (old-x buffer) becomes x' after the swap
           else xp[j] = xnew;
           const double d = xnew - xn;
@@ -284,24 +318,34 @@ __global__ void __launch_bounds__(kBS) grid_kernel(GridParams P) {
     {
       for (int64_t it = 0; it < row_iters; ++it) {
         const int64_t i = it * ngrp + grp;
-        const bool ok = i < m;
+        const bool ok = i < m, lead = ok && gl == 0;
+        double o_y = 0.0, o_kx = 0.0, o_yp = 0.0, o_ya = 0.0, o_kxp = 0.0, o_kxa = 0.0, o_qs = 0.0;
+        if (lead) {
+          o_qs = qs[i];
+          if (pending) {
+            o_yp = yp[i]; o_ya = ya[i]; o_kxp = Kxp[i];
+            if (r2) { o_y = y[i]; o_kx = Kx[i]; o_kxa = Kxa[i]; }
+          } else {
+            o_y = y[i]; o_kx = Kx[i];
+          }
+        }
         const double s = row_dot(i, ok, G, gl, P.rp, P.ci, P.kv, xp);
-        if (ok && gl == 0) {
+        if (lead) {
           double yv, kxv;
           if (pending) {
             if (!r2) {
-              yv = yp[i];
-              ya[i] += theta * (yv - ya[i]);
-              kxv = Kxp[i];
+              yv = o_yp;
+              ya[i] = o_ya + theta * (o_yp - o_ya);
+              kxv = o_kxp;
             } else {
-              yv = ha * (2.0 * yp[i] - y[i]) + hb * ya[i];
-              kxv = ha * (2.0 * Kxp[i] - Kx[i]) + hb * Kxa[i];
+              yv = ha * (2.0 * o_yp - o_y) + hb * o_ya;
+              kxv = ha * (2.0 * o_kxp - o_kx) + hb * o_kxa;
               y[i] = yv; Kx[i] = kxv;
             }
           } else {
-            yv = y[i]; kxv = Kx[i];
+            yv = o_y; kxv = o_kx;
           }
-          double yn = yv + sigma * (qs[i] - 2.0 * s + kxv);
+          double yn = yv + sigma * (o_qs - 2.0 * s + kxv);
           if (i < m1) yn = fmax(yn, 0.0);
           if (pending && !r2) { y[i] = yn; Kx[i] = s; }   // old buffers become y', K~x' after the swap
           else { yp[i] = yn; Kxp[i] = s; }
@@ -526,8 +570,12 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   MPAX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   MPAX_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return LP_ERR_UNSUPPORTED;
+  // register budget: 2 CTAs/SM (64 regs) by default; MPAX_GRID_MINB=1 gives 128 regs
+  const char *env = getenv("MPAX_GRID_MINB");
+  const int minb = (env && atoi(env) == 1) ? 1 : 2;
+  void *kfn = minb == 1 ? (void *)grid_kernel<1> : (void *)grid_kernel<2>;
   int per_sm = 0;
-  MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_kernel, kBS, 0));
+  MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kBS, 0));
   if (per_sm < 1) return LP_ERR_UNSUPPORTED;
   const int64_t n = D.n, m = D.m;
   int blocks = per_sm * sms;
@@ -561,7 +609,7 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   P.gkt = pow2_floor(D.avg_col / 4.0);
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   void *args[] = {&P};
-  MPAX_CUDA(cudaLaunchCooperativeKernel((void *)grid_kernel, dim3(blocks), dim3(kBS), args, 0, s));
+  MPAX_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(kBS), args, 0, s));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   MPAX_CHECK_LAUNCH();
   return LP_OK;

@@ -204,6 +204,154 @@ __global__ void spmv_kernel(int64_t rows, const int32_t *__restrict__ rp, const 
   }
 }
 
+
+// ---- fused single-CTA setup for small LPs --------------------------------------
+// Same checks and the same arithmetic, in the same order, as validate_kernel +
+// transpose + precond_norms/update + scale_kernel, in ONE launch with block
+// barriers between the phases (the multi-kernel path costs ~35 launches, which
+// dominates the per-batch setup of the paper's small LPs).  The transpose places
+// column j's entries by scanning K in row-major order, which is the stable order.
+constexpr int kSmallT = 1024;
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int *warp_tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = v;
+  for (int off = 1; off < 32; off <<= 1) {
+    const int t = __shfl_up_sync(FULL, incl, off);
+    if (lane >= off) incl += t;
+  }
+  if (lane == 31) warp_tot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < kSmallT / 32 ? warp_tot[lane] : 0;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int u = __shfl_up_sync(FULL, t, off);
+      if (lane >= off) t += u;
+    }
+    if (lane < kSmallT / 32) warp_tot[lane] = t;  // inclusive over warps
+  }
+  __syncthreads();
+  const int before = w ? warp_tot[w - 1] : 0;
+  const int res = before + incl - v;
+  __syncthreads();
+  return res;
+}
+
+__global__ void __launch_bounds__(kSmallT) setup_small_kernel(
+    int m, int n, int nnz, const int64_t *__restrict__ rp64, const int32_t *__restrict__ ci,
+    const double *__restrict__ kv0, const double *__restrict__ c, int64_t nc, const double *__restrict__ q, int64_t nq,
+    const double *__restrict__ l0, const double *__restrict__ u0, int32_t *__restrict__ rp, int32_t *__restrict__ trp,
+    int32_t *__restrict__ tci, int32_t *__restrict__ perm, double *__restrict__ kv, double *__restrict__ tkv,
+    double *__restrict__ ls, double *__restrict__ us, double *__restrict__ Dr, double *__restrict__ Dc,
+    double *__restrict__ kmax, int *flag) {
+  extern __shared__ double sh[];
+  double *rho = sh, *gam = sh + m;
+  __shared__ int warp_tot[kSmallT / 32];
+  __shared__ unsigned long long s_kmax;
+  const int tid = threadIdx.x;
+  // phase 0: validation (validate_kernel's checks)
+  for (int i = tid; i < m; i += kSmallT) {
+    const int64_t a = rp64[i], b = rp64[i + 1];
+    if ((i == 0 && a != 0) || (i == m - 1 && b != nnz) || b < a || a < 0 || b > nnz) { report(flag, 3, i); continue; }
+    atomicMax(flag + 5, (int)(b - a));
+    for (int64_t p = a; p < b; ++p) {
+      const int32_t j = ci[p];
+      if (j < 0 || j >= n || (p > a && j <= ci[p - 1])) { report(flag, 3, i); break; }
+    }
+  }
+  for (int p = tid; p < nnz; p += kSmallT) if (!isfinite(kv0[p])) report(flag, 2, p);
+  for (int64_t j = tid; j < nc; j += kSmallT) if (!isfinite(c[j])) report(flag, 2, (int)j);
+  for (int64_t i = tid; i < nq; i += kSmallT) if (!isfinite(q[i])) report(flag, 2, (int)i);
+  for (int j = tid; j < n; j += kSmallT) {
+    const double lj = l0[j], uj = u0[j];
+    if (isnan(lj) || isnan(uj)) report(flag, 2, j);
+    else if (lj == INFINITY || uj == -INFINITY || lj > uj) report(flag, 1, j);
+  }
+  if (tid == 0) s_kmax = 0ull;
+  __syncthreads();
+  if (*(volatile int *)flag) return;
+  // phase 1: row pointers, column counts, K' row pointers (block scan), stable placement
+  for (int i = tid; i <= m; i += kSmallT) rp[i] = (int32_t)rp64[i];
+  int running = 0;
+  for (int j0 = 0; j0 < n; j0 += kSmallT) {
+    const int j = j0 + tid;
+    int cnt = 0;
+    if (j < n)
+      for (int p = 0; p < nnz; ++p) cnt += (ci[p] == j);
+    if (j < n) atomicMax(flag + 6, cnt);
+    const int off = block_exclusive_scan(cnt, warp_tot);
+    if (j < n) trp[j] = running + off;
+    // block total for the next chunk
+    if (tid == kSmallT - 1) warp_tot[0] = off + cnt;
+    __syncthreads();
+    running += warp_tot[0];
+    __syncthreads();
+  }
+  if (tid == 0) trp[n] = nnz;
+  __syncthreads();
+  for (int j = tid; j < n; j += kSmallT) {
+    int d = trp[j];
+    int row = 0;
+    for (int p = 0; p < nnz; ++p) {
+      while (rp[row + 1] <= p) ++row;
+      if (ci[p] == j) { tci[d] = row; perm[d] = p; ++d; }
+    }
+  }
+  for (int i = tid; i < m; i += kSmallT) Dr[i] = 1.0;
+  for (int j = tid; j < n; j += kSmallT) Dc[j] = 1.0;
+  __syncthreads();
+  // phase 2: Ruiz x10 + Pock-Chambolle (alpha = 1), as precond_norms / precond_update
+  for (int r = 0; r < 11; ++r) {
+    const bool use_sum = (r == 10);
+    for (int t = tid; t < m + n; t += kSmallT) {
+      double acc = 0.0;
+      if (t < m) {
+        const double dr = Dr[t];
+        for (int p = rp[t]; p < rp[t + 1]; ++p) {
+          const double a = (fabs(kv0[p]) * dr) * Dc[ci[p]];
+          acc = use_sum ? acc + a : fmax(acc, a);
+        }
+        rho[t] = acc;
+      } else {
+        const int j = t - m;
+        const double dc = Dc[j];
+        for (int d = trp[j]; d < trp[j + 1]; ++d) {
+          const double a = (fabs(kv0[perm[d]]) * Dr[tci[d]]) * dc;
+          acc = use_sum ? acc + a : fmax(acc, a);
+        }
+        gam[j] = acc;
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < m + n; t += kSmallT) {
+      if (t < m) { const double rr = rho[t]; Dr[t] *= (rr > 0.0 ? 1.0 / sqrt(rr) : 1.0); }
+      else { const double g = gam[t - m]; Dc[t - m] *= (g > 0.0 ? 1.0 / sqrt(g) : 1.0); }
+    }
+    __syncthreads();
+  }
+  // phase 3: scaled values, bounds, max |K~|
+  double mx = 0.0;
+  for (int t = tid; t < m + n; t += kSmallT) {
+    if (t < m) {
+      const double dr = Dr[t];
+      for (int p = rp[t]; p < rp[t + 1]; ++p) {
+        const double sv = (kv0[p] * dr) * Dc[ci[p]];
+        kv[p] = sv;
+        mx = fmax(mx, fabs(sv));
+      }
+    } else {
+      const int j = t - m;
+      const double dc = Dc[j];
+      for (int d = trp[j]; d < trp[j + 1]; ++d) tkv[d] = (kv0[perm[d]] * Dr[tci[d]]) * dc;
+      ls[j] = l0[j] / dc;
+      us[j] = u0[j] / dc;
+    }
+  }
+  if (mx > 0.0) atomicMax(&s_kmax, (unsigned long long)__double_as_longlong(mx));
+  __syncthreads();
+  if (tid == 0) *kmax = __longlong_as_double((long long)s_kmax);
+}
+
 inline int grid_for(int64_t work, int block = 256) {
   int64_t g = (work + block - 1) / block;
   if (g < 1) g = 1;
@@ -287,6 +435,21 @@ int setup_build(DevProblem &P, const int64_t *row_ptr64, cudaStream_t s, int *d_
   MPAX_CUDA(cudaFreeAsync(idx_in, s));
   P.avg_row = m > 0 ? (double)nnz / (double)m : 0.0;
   P.avg_col = (double)nnz / (double)n;
+  return LP_OK;
+}
+
+bool setup_small_ok(const DevProblem &P) {
+  return P.m + P.n <= 4096 && (double)P.n * (double)P.nnz <= (double)(1 << 22);
+}
+
+int setup_small(DevProblem &P, const int64_t *row_ptr64, const double *c, int64_t nc, const double *q, int64_t nq,
+                cudaStream_t s, int *d_flag) {
+  const size_t smem = (size_t)(P.m + P.n) * sizeof(double);
+  MPAX_LAUNCH(setup_small_kernel, 1, kSmallT, smem, s, (int)P.m, (int)P.n, (int)P.nnz, row_ptr64, P.ci, P.kv0, c, nc,
+              q, nq, P.l0, P.u0, P.rp, P.trp, P.tci, P.perm, P.kv, P.tkv, P.ls, P.us, P.Dr, P.Dc, P.kmax, d_flag);
+  MPAX_CHECK_LAUNCH();
+  P.avg_row = P.m > 0 ? (double)P.nnz / (double)P.m : 0.0;
+  P.avg_col = (double)P.nnz / (double)P.n;
   return LP_OK;
 }
 

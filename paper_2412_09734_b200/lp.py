@@ -61,6 +61,11 @@ class Result(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad"}
 
 
+RESULT_DTYPE = np.dtype([(f, np.int32 if t is C.c_int32 else np.int64 if t is C.c_int64 else np.float64)
+                         for f, t in Result._fields_], align=True)
+assert RESULT_DTYPE.itemsize == C.sizeof(Result)
+
+
 def library_path() -> str:
     return _LIBPATH
 
@@ -345,12 +350,14 @@ class BatchSolver:
         _check(lib().lp_update_batch(self._h, ca.ptr, qa.ptr, _same_mem([C_, Q])), "lp_update_batch")
 
     def solve(self, X0=None, Y0=None, **opts):
+        """Returns a numpy structured array of `batch` results (fields as lp_result);
+        res[b]["status"], res["iterations"], ... (no per-instance Python objects)."""
         o = default_options(**opts)
         a, b = _Arr(X0, np.float64), _Arr(Y0, np.float64)
-        res = (Result * self.batch)()
-        _check(lib().lp_solve_batch(self._h, C.byref(o), a.ptr, b.ptr, _same_mem([X0, Y0]), res),
+        res = np.zeros(self.batch, dtype=RESULT_DTYPE)
+        _check(lib().lp_solve_batch(self._h, C.byref(o), a.ptr, b.ptr, _same_mem([X0, Y0]), res.ctypes.data),
                "lp_solve_batch")
-        return [r.as_dict() for r in res]
+        return res
 
     def solutions(self, memory=LP_HOST, X=None, Y=None):
         n, m, B = self.problem.n, self.problem.m, self.batch
