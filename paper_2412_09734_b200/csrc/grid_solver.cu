@@ -102,6 +102,25 @@ __device__ __forceinline__ double row_dot(int64_t r, bool valid, int G, int gl, 
                                           const int32_t *__restrict__ ci, const double *__restrict__ v,
                                           const double *x) {
   double s0 = 0.0, s1 = 0.0;
+  if (G == 1) {  // thread per row: no idle lanes in the epilogue, four entries per step in flight
+    if (valid) {
+      const int32_t e = __ldg(rp + r + 1);
+      int32_t p = __ldg(rp + r);
+      for (; p + 3 < e; p += 4) {
+        const int32_t c0 = ld_stream(ci + p), c1 = ld_stream(ci + p + 1), c2 = ld_stream(ci + p + 2),
+                      c3 = ld_stream(ci + p + 3);
+        const double w0 = ld_stream(v + p), w1 = ld_stream(v + p + 1), w2 = ld_stream(v + p + 2),
+                     w3 = ld_stream(v + p + 3);
+        const double x0 = x[c0], x1 = x[c1], x2 = x[c2], x3 = x[c3];
+        s0 += w0 * x0;
+        s1 += w1 * x1;
+        s0 += w2 * x2;
+        s1 += w3 * x3;
+      }
+      for (; p < e; ++p) s0 += ld_stream(v + p) * x[ld_stream(ci + p)];
+    }
+    return s0 + s1;
+  }
   if (valid) {
     const int32_t e = __ldg(rp + r + 1);
     for (int32_t p = __ldg(rp + r) + gl; p < e; p += 4 * G) {
@@ -570,9 +589,10 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   MPAX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   MPAX_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return LP_ERR_UNSUPPORTED;
-  // register budget: 2 CTAs/SM (64 regs) by default; MPAX_GRID_MINB=1 gives 128 regs
+  // register budget: 1 CTA of 512 threads per SM (128 regs, no spills in the phase loops) by default;
+  // MPAX_GRID_MINB=2 gives 2 CTAs/SM at 64 regs (measured slower: spills)
   const char *env = getenv("MPAX_GRID_MINB");
-  const int minb = (env && atoi(env) == 1) ? 1 : 2;
+  const int minb = (env && atoi(env) == 2) ? 2 : 1;
   void *kfn = minb == 1 ? (void *)grid_kernel<1> : (void *)grid_kernel<2>;
   int per_sm = 0;
   MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kBS, 0));
@@ -605,8 +625,13 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   P.part = w;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
   P.check_freq = o.check_frequency; P.alg = o.algorithm;
-  P.gk = pow2_floor(D.avg_row / 4.0);
-  P.gkt = pow2_floor(D.avg_col / 4.0);
+  // thread per row for short rows (all lanes do useful epilogue work), 8 or 32 lanes for long rows
+  // G ~ mean row length / 4 (measured on B200 for this persistent kernel: 4 lanes per 20-entry
+  // row beat 1 and 8; each group walks its rows sequentially, so shorter groups mean longer
+  // dependent chains; scripts/micro/spmv_bench.cu has the standalone-SpMV comparison)
+  auto group = [](double avg) { return pow2_floor(avg / 4.0); };
+  P.gk = group(D.avg_row);
+  P.gkt = group(D.avg_col);
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   void *args[] = {&P};
   MPAX_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(kBS), args, 0, s));
