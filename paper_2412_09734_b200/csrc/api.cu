@@ -262,7 +262,7 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
     MPAX_CUDA(cudaMemcpyAsync(h->Y0, Y0, (size_t)(B * m) * sizeof(double), cudaMemcpyDefault, s));
     dY0 = h->Y0;
   }
-  if (o->path == LP_PATH_DMMA) return fail(LP_ERR_UNSUPPORTED, "requested path not available in this build");
+  if (o->path == LP_PATH_DMMA && !h->P.dense) return fail(LP_ERR_UNSUPPORTED, "the DMMA path needs a dense K");
   const bool big = h->P.nnz >= 32768 || h->P.n + h->P.m >= 4096;
   const bool use_grid = (B == 1) && (o->path == LP_PATH_GRID || (o->path == LP_PATH_AUTO && big));
   if (o->path == LP_PATH_GRID && B != 1) return fail(LP_ERR_UNSUPPORTED, "the grid path solves one LP");
@@ -286,8 +286,24 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
   InstanceLaunch L;
   L.C0 = h->C0; L.cstride = h->cstride; L.Q0 = h->Q0; L.qstride = h->qstride;
   L.X0 = dX0; L.Y0 = dY0; L.batch = B; L.X = h->X; L.Y = h->Y; L.L = h->L; L.res = h->d_res;
+  // a batch sharing a dense K: fp64 tensor-core path (auto from 8 instances on)
+  const bool dmma = h->P.dense && (o->path == LP_PATH_DMMA || (o->path == LP_PATH_AUTO && B >= 8));
+  if (dmma) {
+    const size_t need = dmma_workspace_doubles(n, m, B) * sizeof(double);
+    if (h->work_bytes < need) {
+      if (h->work) MPAX_CUDA(cudaFreeAsync(h->work, s));
+      h->work = nullptr;
+      TRY(dalloc((char **)&h->work, need, s));
+      h->work_bytes = need;
+    }
+  }
   MPAX_CUDA(cudaEventRecord(h->ev0, s));
-  int rc = (o->path == LP_PATH_AUTO) ? tiny_solve(h->P, *o, L, s, h->queue) : LP_ERR_UNSUPPORTED;
+  int rc = LP_ERR_UNSUPPORTED;
+  if (dmma) {
+    rc = dmma_solve(h->P, *o, L, s, h->queue, h->work);
+    if (rc == LP_ERR_UNSUPPORTED && o->path == LP_PATH_DMMA) return fail(rc, "dense K too large for the DMMA path");
+  }
+  if (rc == LP_ERR_UNSUPPORTED && o->path == LP_PATH_AUTO) rc = tiny_solve(h->P, *o, L, s, h->queue);
   if (rc == LP_ERR_UNSUPPORTED) rc = instance_solve(h->P, *o, L, s, h->queue, &h->work, &h->work_bytes);
   TRY(rc);
   MPAX_CUDA(cudaEventRecord(h->ev1, s));

@@ -1,0 +1,768 @@
+// dmma_solver.cu -- batches that share one DENSE K:
+// the two products of every PDHG attempt become fp64 tensor-core contractions
+// ("a vector-vector multiplication can be transformed into a matrix-vector
+// multiplication"; here 8 instances form the N = 8 side of DMMA.8x8x4).
+//
+// Design (B200): a thread-block cluster of CL CTAs serves a group of 8 instances.
+// CTA c keeps the column slice K~[:, slice_c] resident in shared memory for the
+// whole solve (C3: 200 x 100 fp64 = 160 KB), so K~ is read from HBM/L2 once, not
+// once per instance per attempt as in the per-instance path.  Per attempt:
+//   GEMM1   K~'y'  = K~_c' Y'      (n_c x 8, K = m)  -> n-side commit + primal step
+//   GEMM2   P_c    = K~_c X'_c     (m x 8, K = n_c)  partial of K~x'
+//   cluster barrier; CTA c sums the CL partials of its own row slice in rank order
+//   through distributed shared memory (DSMEM) -> m-side commit + dual step;
+//   per-instance ||dx||^2, ||dy||^2, <dy, K~dx> partials; cluster barrier; every CTA
+//   sums the partials in rank order and takes each instance's line-search decision;
+//   the Y' rows of the peers are copied into the local full Y' for the next GEMM1.
+// Instances keep their own step sizes, accept/reject, commits, checks,
+// restarts and termination; a finished instance is frozen until all 8 are done,
+// then the cluster pulls the next group from a device queue.
+//
+// Arithmetic: the same contract as the other solvers; only the
+// summation order of the products differs (tensor-core k-order), so results agree
+// with the oracle to rounding.  mma.sync f64 lowers to DMMA on sm_100a (there is
+// no f64 kind of tcgen05.mma).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+#ifdef MPAX_DEBUG
+#include <cstdio>
+#define DCHK(c)                                                                         \
+  do {                                                                                  \
+    if (!(c)) {                                                                         \
+      printf("DCHK failed %s:%d block %d thread %d\n", __FILE__, __LINE__, blockIdx.x, threadIdx.x); \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#else
+#define DCHK(c) \
+  do {          \
+  } while (0)
+#endif
+
+namespace mpax {
+
+namespace {
+
+constexpr int kThreads = 256;  // 8 warps per CTA
+constexpr int kS = 8;          // instances per group (= DMMA N)
+
+struct DmmaParams {
+  int32_t n, m, m1, nc, np, mp, mc;  // n, m, m1; column slice width, padded slice width, padded m, row slice
+  const double *K;                   // scaled dense K~, row-major m x n
+  const double *Dr, *Dc, *ls, *us, *l0, *u0;
+  const double *C0, *Q0, *X0, *Y0;
+  int64_t cstride, qstride;
+  const double *kmax, *tab;
+  double eps_abs, eps_rel;
+  int64_t iter_limit;
+  int32_t check_freq, alg;
+  int64_t batch;
+  unsigned long long *queue;
+  // per-instance state, instance-major [B][n] / [B][m]
+  double *x, *KTy, *xa, *KTya, *xr, *cs, *xp, *KTyp;
+  double *y, *Kx, *ya, *Kxa, *yr, *qs, *yp, *Kxp;
+  double *X, *Y, *L;
+  lp_result *res;
+};
+
+// per-instance scalar state (identical copy in every CTA of the cluster)
+struct Inst {
+  double omega, eta, W, ref, last, theta, ha, hb, rP, nc0, nq0, metric, dx2c, dy2c, eta_used, M, I;
+  long long k, j, k_in, restarts;
+  int rejects, status, pending, done, check, outsel, csel, valid;
+};
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+struct K5 {
+  double pres, dres, pobj, dobj, gap;
+};
+__device__ __forceinline__ K5 mk5(const double *v) {
+  K5 k;
+  k.pres = sqrt(v[0]); k.dres = sqrt(v[1]); k.pobj = v[2]; k.dobj = v[3]; k.gap = fabs(v[2] - v[3]);
+  return k;
+}
+__device__ __forceinline__ bool pass5(const K5 &k, double nq, double nc, double ea, double er) {
+  return k.pres <= ea + er * nq && k.dres <= ea + er * nc && k.gap <= ea + er * (fabs(k.pobj) + fabs(k.dobj));
+}
+__device__ __forceinline__ double rel5(const K5 &k, double nq, double nc) {
+  return fmax(k.pres / (1.0 + nq), fmax(k.dres / (1.0 + nc), k.gap / (1.0 + fabs(k.pobj) + fabs(k.dobj))));
+}
+__device__ __forceinline__ void krow(double *v, bool orig, bool ge, double dr, double ys, double Kxs, double q0,
+                                     double qs) {
+  const double Kx = orig ? Kxs / dr : Kxs, q = orig ? q0 : qs, y = orig ? dr * ys : ys;
+  double r = q - Kx;
+  if (ge) r = fmax(r, 0.0);
+  v[0] += r * r;
+  v[3] += q * y;
+}
+__device__ __forceinline__ void kcol(double *v, bool orig, double dc, double xs, double KTys, double c0, double cs,
+                                     double l0, double ls, double u0, double us) {
+  const double x = orig ? dc * xs : xs, KTy = orig ? KTys / dc : KTys;
+  const double c = orig ? c0 : cs, l = orig ? l0 : ls, u = orig ? u0 : us;
+  const double lam = c - KTy, lp = fmax(lam, 0.0), lm = fmax(-lam, 0.0);
+  double d = 0.0;
+  if (l == -INFINITY) d += lp;
+  if (u == INFINITY) d += lm;
+  v[1] += d * d;
+  v[2] += c * x;
+  if (l > -INFINITY) v[3] += l * lp;
+  if (u < INFINITY) v[3] -= u * lm;
+}
+
+// Shared-memory layout of one CTA.
+struct Smem {
+  double *Ks;    // mp x np  : K~[:, slice] (zero padded)
+  double *Yf;    // mp x 8   : full Y' (or y-bar at raPDHG checks), instance fastest
+  double *Xc;    // np x 8   : X'_c (or x-bar slice)
+  double *Pc;    // mp x 8   : partial K~_c X'_c
+  double *part;  // 8 x 24   : per-instance partial sums of this CTA
+  double *wpart; // 8 warps x 8 x 24
+  Inst *inst;    // 8
+  int *grp;
+};
+
+// GEMM1: D(j, s) = sum_i Ks[i][j] * Yf[i][s] for the CTA's np columns; calls f(j, s, value).
+template <class F>
+__device__ __forceinline__ void gemm1(const Smem &S, int np, int mp, F &&f) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  for (int jt = w; jt * 8 < np; jt += kThreads / 32) {
+    double d0 = 0.0, d1 = 0.0;
+    const int j = jt * 8 + r;
+    DCHK(j < np);
+    for (int kt = 0; kt < mp; kt += 4) {
+      DCHK(kt + q < mp);
+      const double a = S.Ks[(kt + q) * np + j];        // A(j, i=kt+q)
+      const double b = S.Yf[(kt + q) * kS + r];        // B(i=kt+q, s=r)
+      dmma(d0, d1, a, b);
+    }
+    f(j, 2 * q, d0);
+    f(j, 2 * q + 1, d1);
+  }
+}
+
+// GEMM2: Pc(i, s) = sum_j Ks[i][j] * Xc[j][s].
+__device__ __forceinline__ void gemm2(const Smem &S, int np, int mp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  for (int it = w; it * 8 < mp; it += kThreads / 32) {
+    double d0 = 0.0, d1 = 0.0;
+    const int i = it * 8 + r;
+    DCHK(i < mp);
+    for (int kt = 0; kt < np; kt += 4) {
+      DCHK(kt + q < np);
+      const double a = S.Ks[i * np + kt + q];          // A(i, j=kt+q)
+      const double b = S.Xc[(kt + q) * kS + r];        // B(j=kt+q, s=r)
+      dmma(d0, d1, a, b);
+    }
+    S.Pc[i * kS + 2 * q] = d0;
+    S.Pc[i * kS + 2 * q + 1] = d1;
+  }
+}
+
+// Per-instance partial sums: v[s][0..V) accumulated per thread -> S.part[s][0..V) (fixed order).
+template <int V>
+__device__ __forceinline__ void cta_partials(double (&v)[kS][V], const Smem &S) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int s = 0; s < kS; ++s)
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      double t = v[s][k];
+#pragma unroll
+      for (int off = 16; off; off >>= 1) t += __shfl_xor_sync(FULL, t, off);
+      if (lane == 0) S.wpart[(w * kS + s) * 24 + k] = t;
+    }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kS * V; t += kThreads) {
+    const int s = t / V, k = t % V;
+    double a = 0.0;
+    for (int ww = 0; ww < kThreads / 32; ++ww) a += S.wpart[(ww * kS + s) * 24 + k];
+    S.part[s * 24 + k] = a;
+  }
+}
+
+// After a cluster barrier: tot[s][k] = sum over cluster ranks (in rank order) of part.
+template <int CL, int V>
+__device__ __forceinline__ void cluster_totals(cg::cluster_group &cl, const Smem &S, double *tot /* kS*24 */) {
+  for (int t = threadIdx.x; t < kS * V; t += kThreads) {
+    const int s = t / V, k = t % V;
+    double a = 0.0;
+#pragma unroll
+    for (int c = 0; c < CL; ++c) a += cl.map_shared_rank(S.part, c)[s * 24 + k];
+    tot[s * 24 + k] = a;
+  }
+  __syncthreads();
+}
+
+template <int CL>
+__global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = (int)cl.block_rank();
+  extern __shared__ __align__(16) double sm[];
+  const int n = P.n, m = P.m, m1 = P.m1, np = P.np, mp = P.mp;
+  Smem S;
+  S.Ks = sm;
+  S.Yf = S.Ks + (size_t)mp * np;
+  S.Xc = S.Yf + (size_t)mp * kS;
+  S.Pc = S.Xc + (size_t)np * kS;
+  S.part = S.Pc + (size_t)mp * kS;
+  S.wpart = S.part + kS * 24;
+  double *tot = S.wpart + (kThreads / 32) * kS * 24;
+  S.inst = (Inst *)(tot + kS * 24);
+  S.grp = (int *)(S.inst + kS);
+  const int tid = threadIdx.x;
+#ifdef MPAX_DEBUG
+  if (tid == 0) printf("dmma block %d rank %d n %d m %d nc %d np %d mp %d mc %d batch %lld\n", blockIdx.x, crank, n, m,
+                       P.nc, np, mp, P.mc, (long long)P.batch);
+#endif
+  const int j0 = crank * P.nc, jn = min(n, j0 + P.nc) - j0;      // this CTA's columns [j0, j0 + jn)
+  const int i0 = crank * P.mc, in_ = max(0, min(m, i0 + P.mc) - i0);  // this CTA's rows [i0, i0 + in_)
+  const bool r2 = P.alg == LP_R2HPDHG;
+  // ---- K~ column slice into shared memory once (zero padded) ----
+  for (int t = tid; t < mp * np; t += kThreads) {
+    const int i = t / np, jj = t % np;
+    S.Ks[t] = (i < m && jj < jn) ? P.K[(size_t)i * n + j0 + jj] : 0.0;
+  }
+  for (int t = tid; t < mp * kS; t += kThreads) { S.Yf[t] = 0.0; S.Pc[t] = 0.0; }
+  for (int t = tid; t < np * kS; t += kThreads) S.Xc[t] = 0.0;
+  const double kmx = *P.kmax;
+  const double eta0 = kmx > 0.0 ? 1.0 / kmx : 1.0;
+
+  for (;;) {
+    // ---- next group of 8 instances (rank 0 pulls from the queue) ----
+    cl.sync();
+    if (crank == 0 && tid == 0) *S.grp = (int)atomicAdd(P.queue, 1ull);
+    cl.sync();
+    const int64_t g = *cl.map_shared_rank(S.grp, 0);
+    cl.sync();  // nobody leaves (or reuses S.grp) while a peer still reads rank 0's S.grp
+    if (g * kS >= P.batch) return;
+    const int64_t b0 = g * kS;
+    if (tid < kS) {
+      Inst &I = S.inst[tid];
+      I = Inst();
+      I.valid = (b0 + tid) < P.batch;
+      I.done = !I.valid;
+    }
+    __syncthreads();
+    // ---- step 2: scaled data, start point, norms (partials: |c~|^2, |q~|^2, |c|^2, |q|^2) ----
+    {
+      double v[kS][4] = {};
+      for (int t = tid; t < jn * kS; t += kThreads) {
+        const int s = t / jn, jj = t % jn, j = j0 + jj;
+        if (!S.inst[s].valid) continue;
+        const int64_t b = b0 + s;
+        const double dc = P.Dc[j], c = P.C0[b * P.cstride + j], cj = c * dc;
+        P.cs[b * n + j] = cj;
+        v[s][0] += cj * cj;
+        v[s][2] += c * c;
+        const double xv = median3(P.ls[j], P.X0 ? P.X0[b * n + j] / dc : 0.0, P.us[j]);
+        P.x[b * n + j] = xv; P.xa[b * n + j] = xv; P.xr[b * n + j] = xv; P.xp[b * n + j] = xv;
+        S.Xc[jj * kS + s] = xv;
+      }
+      for (int t = tid; t < in_ * kS; t += kThreads) {
+        const int s = t / in_, ii = t % in_, i = i0 + ii;
+        if (!S.inst[s].valid) continue;
+        const int64_t b = b0 + s;
+        const double dr = P.Dr[i], qv = P.Q0[b * P.qstride + i], qi = qv * dr;
+        P.qs[b * m + i] = qi;
+        v[s][1] += qi * qi;
+        v[s][3] += qv * qv;
+        double yv = P.Y0 ? P.Y0[b * m + i] / dr : 0.0;
+        if (i < m1) yv = fmax(yv, 0.0);
+        P.y[b * m + i] = yv; P.ya[b * m + i] = yv; P.yr[b * m + i] = yv; P.yp[b * m + i] = yv;
+        S.Yf[i * kS + s] = yv;
+      }
+      cta_partials<4>(v, S);
+      cl.sync();
+      cluster_totals<CL, 4>(cl, S, tot);
+      if (tid < kS && S.inst[tid].valid) {
+        Inst &I = S.inst[tid];
+        const double* t4 = tot + tid * 24;
+        I.nc0 = sqrt(t4[2]); I.nq0 = sqrt(t4[3]);
+        I.omega = 1.0;
+        if (sqrt(t4[0]) > 1e-10 && sqrt(t4[1]) > 1e-10) I.omega = sqrt(t4[0]) / sqrt(t4[1]);
+        I.eta = eta0; I.last = INFINITY;
+      }
+      // full y0 from the peers' row slices
+      for (int c = 0; c < CL; ++c) {
+        if (c == crank) continue;
+        const int ci0 = c * P.mc, cin = max(0, min(m, ci0 + P.mc) - ci0);
+        const double *rem = cl.map_shared_rank(S.Yf, c);
+        for (int t = tid; t < cin * kS; t += kThreads) S.Yf[(ci0 + t / kS) * kS + t % kS] = rem[(ci0 + t / kS) * kS + t % kS];
+      }
+      __syncthreads();
+    }
+    // K~x0 (GEMM2 + cluster reduce) and K~'y0 (GEMM1); raPDHG reference KKT_omega(z0)
+    gemm2(S, np, mp);
+    cl.sync();
+    {
+      double v[kS][4] = {};
+      for (int t = tid; t < in_ * kS; t += kThreads) {
+        const int ii = t / kS, s = t % kS, i = i0 + ii;
+        if (!S.inst[s].valid) continue;
+        double a = 0.0;
+        for (int c = 0; c < CL; ++c) a += cl.map_shared_rank(S.Pc, c)[i * kS + s];
+        const int64_t b = b0 + s;
+        P.Kx[b * m + i] = a; P.Kxa[b * m + i] = a; P.Kxp[b * m + i] = a;
+        krow(v[s], false, i < m1, 1.0, P.y[b * m + i], a, 0.0, P.qs[b * m + i]);
+      }
+      gemm1(S, np, mp, [&](int jj, int s, double val) {
+        if (jj >= jn || !S.inst[s].valid) return;
+        const int64_t b = b0 + s;
+        const int j = j0 + jj;
+        P.KTy[b * n + j] = val; P.KTya[b * n + j] = val; P.KTyp[b * n + j] = val;
+        kcol(v[s], false, 1.0, P.x[b * n + j], val, 0.0, P.cs[b * n + j], 0.0, P.ls[j], 0.0, P.us[j]);
+      });
+      cta_partials<4>(v, S);
+      cl.sync();
+      cluster_totals<CL, 4>(cl, S, tot);
+      if (tid < kS && S.inst[tid].valid && !r2) {
+        Inst &I = S.inst[tid];
+        const K5 ks = mk5(tot + tid * 24);
+        I.ref = sqrt(I.omega * ks.pres * ks.pres + ks.dres * ks.dres / I.omega + ks.gap * ks.gap);
+      }
+      __syncthreads();
+    }
+
+    // ====================== attempts (lock-step over the group) ======================
+    for (;;) {
+      bool all_done = true;
+      for (int s = 0; s < kS; ++s) all_done &= (bool)S.inst[s].done;
+      if (all_done) break;
+      // ---- phase A: GEMM1 = K~_c' Y' ; [commit n-side] ; primal step ; X'_c ----
+      double va[kS][1] = {};
+      gemm1(S, np, mp, [&](int jj, int s, double kty) {
+        const Inst &I = S.inst[s];
+        if (jj >= jn || I.done) { if (jj < np) S.Xc[jj * kS + s] = 0.0; return; }
+        const int64_t b = b0 + s;
+        const int j = j0 + jj;
+        const int64_t o = b * n + j;
+        double xv = P.x[o], kt = P.KTy[o];
+        if (I.pending) {
+          const double xpv = P.xp[o];
+          if (!r2) {
+            P.xa[o] += I.theta * (xpv - P.xa[o]);
+            xv = xpv; kt = kty;
+          } else {
+            xv = I.ha * (2.0 * xpv - xv) + I.hb * P.xa[o];
+            kt = I.ha * (2.0 * kty - kt) + I.hb * P.KTya[o];
+          }
+          P.x[o] = xv; P.KTy[o] = kt;
+        }
+        const double tau = I.eta / I.omega;
+        const double xn = median3(P.ls[j], xv - tau * (P.cs[o] - kt), P.us[j]);
+        P.xp[o] = xn;
+        S.Xc[jj * kS + s] = xn;
+        const double d = xn - xv;
+        va[s][0] += d * d;
+      });
+      __syncthreads();
+      // ---- GEMM2: partial K~_c X'_c ----
+      gemm2(S, np, mp);
+      cl.sync();
+      // ---- phase B: reduce K~x' for own rows; [commit m-side]; dual step ----
+      double vb[kS][3] = {};
+      for (int s = 0; s < kS; ++s) vb[s][0] = va[s][0];
+      for (int t = tid; t < in_ * kS; t += kThreads) {
+        const int ii = t / kS, s = t % kS, i = i0 + ii;
+        const Inst &I = S.inst[s];
+        if (I.done) continue;
+        double kxp = 0.0;
+        for (int c = 0; c < CL; ++c) kxp += cl.map_shared_rank(S.Pc, c)[i * kS + s];
+        const int64_t b = b0 + s;
+        const int64_t o = b * m + i;
+        double yv = P.y[o], kxv = P.Kx[o];
+        if (I.pending) {
+          const double ypv = P.yp[o], kxpo = P.Kxp[o];
+          if (!r2) {
+            P.ya[o] += I.theta * (ypv - P.ya[o]);
+            yv = ypv; kxv = kxpo;
+          } else {
+            yv = I.ha * (2.0 * ypv - yv) + I.hb * P.ya[o];
+            kxv = I.ha * (2.0 * kxpo - kxv) + I.hb * P.Kxa[o];
+          }
+          P.y[o] = yv; P.Kx[o] = kxv;
+        }
+        const double sigma = I.eta * I.omega;
+        double yn = yv + sigma * (P.qs[o] - 2.0 * kxp + kxv);
+        if (i < m1) yn = fmax(yn, 0.0);
+        P.yp[o] = yn; P.Kxp[o] = kxp;
+        S.Yf[i * kS + s] = yn;
+        const double d = yn - yv;
+        vb[s][1] += d * d;
+        vb[s][2] += d * (kxp - kxv);
+      }
+      cta_partials<3>(vb, S);
+      cl.sync();
+      cluster_totals<CL, 3>(cl, S, tot);
+      // peers' Y' rows for the next GEMM1
+      for (int c = 0; c < CL; ++c) {
+        if (c == crank) continue;
+        const int ci0 = c * P.mc, cin = max(0, min(m, ci0 + P.mc) - ci0);
+        const double *rem = cl.map_shared_rank(S.Yf, c);
+        for (int t = tid; t < cin * kS; t += kThreads) S.Yf[ci0 * kS + t] = rem[ci0 * kS + t];
+      }
+      // ---- decisions (step 3 / 4 bookkeeping), one thread per instance ----
+      if (tid < kS) {
+        Inst &I = S.inst[tid];
+        I.check = 0;
+        if (!I.done) {
+          const double *t3 = tot + tid * 24;
+          I.pending = 0;
+          I.j += 1;
+          double f1, f2;
+          step_factors(P.tab, I.j, f1, f2);
+          const double Iv = t3[2];
+          const double M = I.omega * t3[0] + t3[1] / I.omega;
+          const double eb = (Iv != 0.0) ? M / (2.0 * fabs(Iv)) : INFINITY;
+          const bool acc = I.eta <= eb;
+          const double eta_used = I.eta;
+          I.eta = fmin(f1 * eb, f2 * I.eta);
+          if (!acc) {
+            if (++I.rejects >= 100) { I.status = LP_NUMERICAL_ERROR; I.done = 1; I.outsel = 0; }
+          } else {
+            I.rejects = 0;
+            if (!r2) {
+              const double W1 = I.W + eta_used;
+              I.theta = eta_used / W1;
+              I.W = W1;
+            } else {
+              I.rP = sqrt(fmax(0.0, M / eta_used - 2.0 * Iv));
+              if (I.k_in == 0) I.ref = I.rP;
+              I.ha = (double)(I.k_in + 1) / (double)(I.k_in + 2);
+              I.hb = 1.0 / (double)(I.k_in + 2);
+            }
+            I.k += 1;
+            I.k_in += 1;
+            I.pending = 1;
+            if (I.k % P.check_freq == 0 || I.k == P.iter_limit) I.check = 1;
+          }
+        }
+      }
+      __syncthreads();
+      bool any_check = false;
+      for (int s = 0; s < kS; ++s) any_check |= (bool)S.inst[s].check;
+      if (!any_check) continue;
+
+      // ====================== check (step 5) for the flagged instances ======================
+      // commit-only, both sides, for every pending instance; K~'y' from GEMM1
+      double vc[kS][6] = {};
+      gemm1(S, np, mp, [&](int jj, int s, double kty) {
+        const Inst &I = S.inst[s];
+        if (jj >= jn || I.done || !I.pending) return;
+        const int64_t b = b0 + s;
+        const int j = j0 + jj;
+        const int64_t o = b * n + j;
+        const double xpv = P.xp[o];
+        P.KTyp[o] = kty;
+        if (!r2) {
+          P.xa[o] += I.theta * (xpv - P.xa[o]);
+          P.x[o] = xpv; P.KTy[o] = kty;
+        } else {
+          P.x[o] = I.ha * (2.0 * xpv - P.x[o]) + I.hb * P.xa[o];
+          P.KTy[o] = I.ha * (2.0 * kty - P.KTy[o]) + I.hb * P.KTya[o];
+          if (I.check) {
+            kcol(vc[s], true, P.Dc[j], xpv, kty, P.C0[b * P.cstride + j], P.cs[o], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+            const double d = xpv - P.xr[o];
+            vc[s][4] += d * d;
+          }
+        }
+      });
+      for (int t = tid; t < in_ * kS; t += kThreads) {
+        const int ii = t / kS, s = t % kS, i = i0 + ii;
+        const Inst &I = S.inst[s];
+        if (I.done || !I.pending) continue;
+        const int64_t b = b0 + s;
+        const int64_t o = b * m + i;
+        const double ypv = P.yp[o], kxp = P.Kxp[o];
+        if (!r2) {
+          P.ya[o] += I.theta * (ypv - P.ya[o]);
+          P.y[o] = ypv; P.Kx[o] = kxp;
+        } else {
+          P.y[o] = I.ha * (2.0 * ypv - P.y[o]) + I.hb * P.ya[o];
+          P.Kx[o] = I.ha * (2.0 * kxp - P.Kx[o]) + I.hb * P.Kxa[o];
+          if (I.check) {
+            krow(vc[s], true, i < m1, P.Dr[i], ypv, kxp, P.Q0[b * P.qstride + i], P.qs[o]);
+            const double d = ypv - P.yr[o];
+            vc[s][5] += d * d;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid < kS) S.inst[tid].pending = 0;
+      cl.sync();  // every rank's commits (global state) visible before they are read across slices
+      if (r2) {
+        cta_partials<6>(vc, S);
+        cl.sync();
+        cluster_totals<CL, 6>(cl, S, tot);
+        if (tid < kS) {
+          Inst &I = S.inst[tid];
+          if (I.check) {
+            const double *t6 = tot + tid * 24;
+            const K5 kw = mk5(t6);
+            if (pass5(kw, I.nq0, I.nc0, P.eps_abs, P.eps_rel)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 1; }
+            else if (I.k == P.iter_limit) { I.status = LP_ITERATION_LIMIT; I.done = 1; I.outsel = 1; }
+            else { I.metric = I.rP; I.dx2c = t6[4]; I.dy2c = t6[5]; I.csel = 1; }
+          }
+        }
+      } else {
+        // average's products: X-bar slice -> GEMM2 -> reduce; full Y-bar -> GEMM1
+        __syncthreads();
+        for (int t = tid; t < np * kS; t += kThreads) {
+          const int jj = t / kS, s = t % kS;
+          S.Xc[t] = (jj < jn && S.inst[s].check) ? P.xa[(b0 + s) * n + j0 + jj] : 0.0;
+        }
+        for (int t = tid; t < mp * kS; t += kThreads) {
+          const int i = t / kS, s = t % kS;
+          S.Yf[t] = (i < m && S.inst[s].check) ? P.ya[(b0 + s) * m + i] : 0.0;
+        }
+        __syncthreads();
+        gemm2(S, np, mp);
+        cl.sync();
+        double v[kS][20] = {};
+        for (int t = tid; t < in_ * kS; t += kThreads) {
+          const int ii = t / kS, s = t % kS, i = i0 + ii;
+          if (!S.inst[s].check) continue;
+          double kxa = 0.0;
+          for (int c = 0; c < CL; ++c) kxa += cl.map_shared_rank(S.Pc, c)[i * kS + s];
+          const int64_t b = b0 + s;
+          const int64_t o = b * m + i;
+          P.Kxa[o] = kxa;
+          const double dr = P.Dr[i], yai = P.ya[o], yi = P.y[o], kxi = P.Kx[o], q0 = P.Q0[b * P.qstride + i],
+                       qsi = P.qs[o];
+          const bool ge = i < m1;
+          krow(v[s] + 0, true, ge, dr, yai, kxa, q0, qsi);
+          krow(v[s] + 4, true, ge, dr, yi, kxi, q0, qsi);
+          krow(v[s] + 8, false, ge, dr, yai, kxa, q0, qsi);
+          krow(v[s] + 12, false, ge, dr, yi, kxi, q0, qsi);
+          const double da = yai - P.yr[o], dcur = yi - P.yr[o];
+          v[s][17] += da * da;
+          v[s][19] += dcur * dcur;
+        }
+        gemm1(S, np, mp, [&](int jj, int s, double kta) {
+          if (jj >= jn || !S.inst[s].check) return;
+          const int64_t b = b0 + s;
+          const int j = j0 + jj;
+          const int64_t o = b * n + j;
+          P.KTya[o] = kta;
+          const double dc = P.Dc[j], xaj = P.xa[o], xj = P.x[o], ktj = P.KTy[o];
+          const double c0 = P.C0[b * P.cstride + j], csj = P.cs[o], l0 = P.l0[j], lsj = P.ls[j], u0 = P.u0[j],
+                       usj = P.us[j];
+          kcol(v[s] + 0, true, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
+          kcol(v[s] + 4, true, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+          kcol(v[s] + 8, false, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
+          kcol(v[s] + 12, false, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+          const double da = xaj - P.xr[o], dcur = xj - P.xr[o];
+          v[s][16] += da * da;
+          v[s][18] += dcur * dcur;
+        });
+        cta_partials<20>(v, S);
+        cl.sync();
+        cluster_totals<CL, 20>(cl, S, tot);
+        if (tid < kS) {
+          Inst &I = S.inst[tid];
+          if (I.check) {
+            const double *t = tot + tid * 24;
+            const K5 ka = mk5(t + 0), kc = mk5(t + 4);
+            if (pass5(ka, I.nq0, I.nc0, P.eps_abs, P.eps_rel)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 1; }
+            else if (pass5(kc, I.nq0, I.nc0, P.eps_abs, P.eps_rel)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 0; }
+            else if (I.k == P.iter_limit) {
+              I.status = LP_ITERATION_LIMIT; I.done = 1;
+              I.outsel = rel5(ka, I.nq0, I.nc0) < rel5(kc, I.nq0, I.nc0) ? 1 : 0;
+            } else {
+              const K5 sa = mk5(t + 8), sc = mk5(t + 12);
+              const double om = I.omega;
+              const double e_a = sqrt(om * sa.pres * sa.pres + sa.dres * sa.dres / om + sa.gap * sa.gap);
+              const double e_c = sqrt(om * sc.pres * sc.pres + sc.dres * sc.dres / om + sc.gap * sc.gap);
+              if (e_a < e_c) { I.csel = 1; I.metric = e_a; I.dx2c = t[16]; I.dy2c = t[17]; }
+              else { I.csel = 0; I.metric = e_c; I.dx2c = t[18]; I.dy2c = t[19]; }
+            }
+          }
+        }
+      }
+      // restart test and primal weight (contract step 5), one thread per instance
+      __syncthreads();
+      if (tid < kS) {
+        Inst &I = S.inst[tid];
+        I.pending = 0;
+        if (I.check && !I.done) {
+          const bool restart = ((double)I.k_in >= 0.36 * (double)I.k) || (I.metric <= 0.2 * I.ref) ||
+                               (I.metric <= 0.8 * I.ref && I.metric > I.last);
+          I.last = I.metric;
+          I.check = restart ? 2 : 0;
+          if (restart) {
+            I.restarts += 1;
+            const double dxn = sqrt(I.dx2c), dyn = sqrt(I.dy2c);
+            if (dxn > 1e-10 && dyn > 1e-10) I.omega = sqrt(I.omega * (dyn / dxn));
+            I.k_in = 0;
+            if (!r2) { I.W = 0.0; I.ref = I.metric; }
+          }
+        } else if (I.check) {
+          I.check = 0;
+        }
+      }
+      __syncthreads();
+      // restart copies (check == 2): candidate -> current, anchor / average, restart point
+      for (int t = tid; t < jn * kS; t += kThreads) {
+        const int s = t / jn, jj = t % jn;
+        const Inst &I = S.inst[s];
+        if (I.check != 2) continue;
+        const int64_t o = (b0 + s) * n + j0 + jj;
+        double xv = P.x[o], kt = P.KTy[o];
+        if (I.csel) { xv = r2 ? P.xp[o] : P.xa[o]; kt = r2 ? P.KTyp[o] : P.KTya[o]; }
+        P.x[o] = xv; P.xr[o] = xv; P.xa[o] = xv; P.KTy[o] = kt; P.KTya[o] = kt;
+      }
+      for (int t = tid; t < in_ * kS; t += kThreads) {
+        const int s = t / in_, ii = t % in_;
+        const Inst &I = S.inst[s];
+        if (I.check != 2) continue;
+        const int64_t o = (b0 + s) * m + i0 + ii;
+        double yv = P.y[o], kx = P.Kx[o];
+        if (I.csel) { yv = r2 ? P.yp[o] : P.ya[o]; kx = r2 ? P.Kxp[o] : P.Kxa[o]; }
+        P.y[o] = yv; P.yr[o] = yv; P.ya[o] = yv; P.Kx[o] = kx; P.Kxa[o] = kx;
+      }
+      // the next attempt restarts from committed state: refresh the full current y in Yf
+      __syncthreads();
+      cl.sync();
+      for (int t = tid; t < mp * kS; t += kThreads) {
+        const int i = t / kS, s = t % kS;
+        S.Yf[t] = (i < m && !S.inst[s].done) ? P.y[(b0 + s) * m + i] : 0.0;
+      }
+      __syncthreads();
+      if (tid < kS) S.inst[tid].check = 0;
+      __syncthreads();
+    }
+
+    // ====================== step 6: output every instance of the group ======================
+    {
+      double v[kS][4] = {};
+      for (int t = tid; t < jn * kS; t += kThreads) {
+        const int s = t / jn, jj = t % jn, j = j0 + jj;
+        const Inst &I = S.inst[s];
+        if (!I.valid) continue;
+        const int64_t b = b0 + s;
+        const int64_t o = b * n + j;
+        const double xs = I.outsel ? (r2 ? P.xp[o] : P.xa[o]) : P.x[o];
+        const double kt = I.outsel ? (r2 ? P.KTyp[o] : P.KTya[o]) : P.KTy[o];
+        const double dc = P.Dc[j], c0 = P.C0[b * P.cstride + j];
+        kcol(v[s], true, dc, xs, kt, c0, P.cs[o], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+        P.X[o] = dc * xs;
+        P.L[o] = c0 - kt / dc;
+      }
+      for (int t = tid; t < in_ * kS; t += kThreads) {
+        const int s = t / in_, ii = t % in_, i = i0 + ii;
+        const Inst &I = S.inst[s];
+        if (!I.valid) continue;
+        const int64_t b = b0 + s;
+        const int64_t o = b * m + i;
+        const double ys = I.outsel ? (r2 ? P.yp[o] : P.ya[o]) : P.y[o];
+        const double kx = I.outsel ? (r2 ? P.Kxp[o] : P.Kxa[o]) : P.Kx[o];
+        const double dr = P.Dr[i];
+        krow(v[s], true, i < m1, dr, ys, kx, P.Q0[b * P.qstride + i], P.qs[o]);
+        P.Y[o] = dr * ys;
+      }
+      cta_partials<4>(v, S);
+      cl.sync();
+      cluster_totals<CL, 4>(cl, S, tot);
+      if (crank == 0 && tid < kS && S.inst[tid].valid) {
+        const Inst &I = S.inst[tid];
+        const K5 ko = mk5(tot + tid * 24);
+        lp_result r;
+        r.status = I.status; r.pad = 0;
+        r.iterations = I.k; r.attempts = I.j; r.restarts = I.restarts;
+        r.primal_objective = ko.pobj; r.dual_objective = ko.dobj;
+        r.primal_residual = ko.pres; r.dual_residual = ko.dres; r.gap = ko.gap;
+        r.rel_kkt = rel5(ko, I.nq0, I.nc0);
+        r.omega = I.omega; r.eta = I.eta; r.solve_seconds = 0.0;
+        P.res[b0 + tid] = r;
+      }
+    }
+  }
+}
+
+template <int CL>
+int launch_dmma(const DmmaParams &P, size_t smem, cudaStream_t s) {
+  MPAX_CUDA(cudaFuncSetAttribute(dmma_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  MPAX_CUDA(cudaFuncSetAttribute(dmma_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int max_clusters = 0;
+  cfg.gridDim = dim3(CL);
+  MPAX_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, (void *)dmma_kernel<CL>, &cfg));
+  if (max_clusters < 1) return LP_ERR_UNSUPPORTED;
+  const int64_t groups = (P.batch + kS - 1) / kS;
+  const int64_t clusters = groups < max_clusters ? groups : max_clusters;
+  cfg.gridDim = dim3((unsigned)(clusters * CL));
+  MPAX_CUDA(cudaMemsetAsync(P.queue, 0, sizeof(unsigned long long), s));
+  MPAX_CUDA(cudaLaunchKernelEx(&cfg, dmma_kernel<CL>, P));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+}  // namespace
+
+size_t dmma_workspace_doubles(int64_t n, int64_t m, int64_t batch) { return (size_t)batch * (size_t)(8 * n + 8 * m); }
+
+int dmma_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L, cudaStream_t s,
+               unsigned long long *queue, double *work) {
+  if (!D.dense) return LP_ERR_UNSUPPORTED;
+  const int n = (int)D.n, m = (int)D.m;
+  const int mp = (m + 7) / 8 * 8;
+  int dev = 0, max_optin = 0;
+  MPAX_CUDA(cudaGetDevice(&dev));
+  MPAX_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  // smallest cluster whose column slice fits in shared memory
+  for (int CL : {1, 2, 4, 8}) {
+    const int nc = (n + CL - 1) / CL;
+    const int np = (nc + 7) / 8 * 8;
+    const size_t smem = sizeof(double) * ((size_t)mp * np + (size_t)mp * kS + (size_t)np * kS + (size_t)mp * kS +
+                                          kS * 24 + (kThreads / 32) * kS * 24 + kS * 24) +
+                        sizeof(Inst) * kS + 64;
+    if (smem + 1024 > (size_t)max_optin) continue;
+    DmmaParams P;
+    P.n = n; P.m = m; P.m1 = (int)D.m1; P.nc = nc; P.np = np; P.mp = mp; P.mc = (m + CL - 1) / CL;
+    P.K = D.kv;
+    P.Dr = D.Dr; P.Dc = D.Dc; P.ls = D.ls; P.us = D.us; P.l0 = D.l0; P.u0 = D.u0;
+    P.C0 = L.C0; P.Q0 = L.Q0; P.X0 = L.X0; P.Y0 = L.Y0; P.cstride = L.cstride; P.qstride = L.qstride;
+    P.kmax = D.kmax; P.tab = D.tab;
+    P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
+    P.check_freq = o.check_frequency; P.alg = o.algorithm;
+    P.batch = L.batch; P.queue = queue;
+    const size_t BN = (size_t)L.batch * n, BM = (size_t)L.batch * m;
+    double *w = work;
+    P.x = w; w += BN; P.KTy = w; w += BN; P.xa = w; w += BN; P.KTya = w; w += BN; P.xr = w; w += BN;
+    P.cs = w; w += BN; P.xp = w; w += BN; P.KTyp = w; w += BN;
+    P.y = w; w += BM; P.Kx = w; w += BM; P.ya = w; w += BM; P.Kxa = w; w += BM; P.yr = w; w += BM;
+    P.qs = w; w += BM; P.yp = w; w += BM; P.Kxp = w; w += BM;
+    P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
+    switch (CL) {
+      case 1: return launch_dmma<1>(P, smem, s);
+      case 2: return launch_dmma<2>(P, smem, s);
+      case 4: return launch_dmma<4>(P, smem, s);
+      default: return launch_dmma<8>(P, smem, s);
+    }
+  }
+  return LP_ERR_UNSUPPORTED;
+}
+
+}  // namespace mpax

@@ -9,7 +9,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIBPATH = os.path.join(_HERE, "libmpax_b200.so")
+_LIBPATH = os.environ.get("MPAX_LIB") or os.path.join(_HERE, "libmpax_b200.so")
 _lock = threading.Lock()
 _lib = None
 
