@@ -183,6 +183,31 @@ int lp_get_scaling(lp_handle h, double *Dr, double *Dc, int32_t memory);
 int lp_spmv_scaled(lp_handle h, const double *v, double *Kv, const double *w, double *KTw,
                    int32_t memory);
 
+/* ---- one LP row-sharded across GPUs (§3.5) ----
+ * Process `rank` of `nranks` (one process per GPU) passes ITS block of rows:
+ * rows [global_row_offset, global_row_offset + m_local) of K = [G; A], with
+ * local_rows->m1 = number of those rows that are ">=" rows (all of them come
+ * first, as globally), local q, and the FULL c, l, u (n).  nccl_comm is a
+ * borrowed ncclComm_t (NULL allowed when nranks == 1); the caller keeps it alive.
+ * Column norms of the preconditioner and every cross-shard sum of the iteration
+ * go through ncclAllReduce on the handle's stream.  lp_solve then takes x0 (n)
+ * and y0 (this rank's m_local rows); lp_get_solution returns x, reduced costs (n)
+ * and this rank's rows of y. */
+int lp_create_sharded(const lp_problem_desc *local_rows, int64_t global_row_offset, int64_t m1_global,
+                      int64_t m2_global, void *nccl_comm, int rank, int nranks, void *cuda_stream, lp_handle *out);
+
+/* The same sharded engine with `shards` row blocks (balanced by nnz) on the
+ * CURRENT device and a fixed-order device sum in place of NCCL: the partitioned
+ * arithmetic of lp_create_sharded, testable on one GPU.  y covers all m rows. */
+int lp_create_sharded_virtual(const lp_problem_desc *p, int32_t shards, void *cuda_stream, lp_handle *out);
+
+/* NCCL communicator helpers (so callers need no NCCL headers): rank 0 calls
+ * lp_nccl_unique_id (128 bytes) and broadcasts it (e.g. torch.distributed),
+ * then every rank calls lp_nccl_comm_init with its CUDA device current. */
+int lp_nccl_unique_id(void *out_id128);
+int lp_nccl_comm_init(void **comm, int nranks, const void *id128, int rank);
+int lp_nccl_comm_destroy(void *comm);
+
 /* Number of kernels this library has launched in the calling process so far
  * (bench.py reports the difference across its timed region). */
 int64_t lp_kernel_launch_count(void);

@@ -5,11 +5,16 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <string>
 
 #include "common.cuh"
+
+#ifdef MPAX_HAVE_NCCL
+#include <nccl.h>
+#endif
 
 namespace mpax {
 std::atomic<int64_t> g_launches{0};
@@ -35,6 +40,7 @@ struct lp_handle_s {
   int64_t *rp64 = nullptr;
   int *d_flag = nullptr, *h_flag = nullptr;
   void *arena = nullptr;  // one allocation holding every per-handle array
+  ShardedLP *sharded = nullptr;  // row-sharded handle (lp_create_sharded / _virtual)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool solved = false;
 };
@@ -109,6 +115,11 @@ int dalloc(T **p, size_t count, cudaStream_t s) {
 
 void free_handle(lp_handle h) {
   if (!h) return;
+  if (h->sharded) {
+    sharded_free(h->sharded);
+    delete h;
+    return;
+  }
   cudaStream_t s = h->stream;
   for (void *p : {(void *)h->arena, (void *)h->X0, (void *)h->Y0, (void *)h->work})
     if (p) cudaFreeAsync(p, s);
@@ -243,11 +254,31 @@ int check_options(const lp_options *o) {
   return LP_OK;
 }
 
+int run_sharded(lp_handle h, const lp_options *o, const double *X0, const double *Y0, lp_result *out) {
+  cudaStream_t s = h->stream;
+  const int64_t n = sharded_n(h->sharded), ml = sharded_m_local(h->sharded);
+  const double *dX0 = nullptr, *dY0 = nullptr;
+  if (X0) {
+    if (!h->X0) TRY(dalloc(&h->X0, n, s));
+    MPAX_CUDA(cudaMemcpyAsync(h->X0, X0, (size_t)n * sizeof(double), cudaMemcpyDefault, s));
+    dX0 = h->X0;
+  }
+  if (Y0 && ml > 0) {
+    if (!h->Y0) TRY(dalloc(&h->Y0, ml, s));
+    MPAX_CUDA(cudaMemcpyAsync(h->Y0, Y0, (size_t)ml * sizeof(double), cudaMemcpyDefault, s));
+    dY0 = h->Y0;
+  }
+  const int rc = sharded_solve(*h->sharded, *o, dX0, dY0, out);
+  if (rc == LP_OK) h->solved = true;
+  return rc;
+}
+
 int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *Y0, int32_t memory,
               lp_result *out) {
   if (!h || !out) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle or result");
   TRY(check_options(o));
   if (memory != LP_HOST && memory != LP_DEVICE) return fail(LP_ERR_INVALID_ARGUMENT, "bad memory kind");
+  if (h->sharded) return run_sharded(h, o, X0, Y0, out);
   cudaStream_t s = h->stream;
   const int64_t n = h->P.n, m = h->P.m, B = h->batch;
   // warm starts: staged into library memory (original space; scaled in-kernel)
@@ -381,6 +412,11 @@ int lp_solve_batch(lp_handle h, const lp_options *o, const double *X0, const dou
 int lp_get_solution(lp_handle h, int64_t instance, double *x, double *y, double *rc, int32_t memory) {
   if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
   if (!h->solved) return fail(LP_ERR_NOT_SOLVED, "no solve yet");
+  if (h->sharded) {
+    if (instance != 0) return fail(LP_ERR_BATCH_SHAPE, "instance out of range");
+    const int r = sharded_get(h->sharded, x, y, rc);
+    return r == LP_OK ? r : fail(r, "sharded get");
+  }
   if (instance < 0 || instance >= h->batch) return fail(LP_ERR_BATCH_SHAPE, "instance out of range");
   cudaStream_t s = h->stream;
   const int64_t n = h->P.n, m = h->P.m;
@@ -404,6 +440,13 @@ int lp_get_solutions(lp_handle h, double *X, double *Y, int32_t memory) {
 
 int lp_get_shape(lp_handle h, int64_t *n, int64_t *m1, int64_t *m2, int64_t *batch) {
   if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  if (h->sharded) {
+    if (n) *n = sharded_n(h->sharded);
+    if (m1) *m1 = 0;
+    if (m2) *m2 = sharded_m_local(h->sharded);
+    if (batch) *batch = 1;
+    return LP_OK;
+  }
   if (n) *n = h->P.n;
   if (m1) *m1 = h->P.m1;
   if (m2) *m2 = h->P.m2;
@@ -440,6 +483,115 @@ int lp_spmv_scaled(lp_handle h, const double *v, double *Kv, const double *w, do
     if (p) cudaFreeAsync(p, s);
   MPAX_CUDA(cudaStreamSynchronize(s));
   return LP_OK;
+}
+
+int lp_create_sharded(const lp_problem_desc *local_rows, int64_t global_row_offset, int64_t m1_global,
+                      int64_t m2_global, void *nccl_comm, int rank, int nranks, void *cuda_stream, lp_handle *out) {
+  TRY(check_desc(local_rows));
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks || global_row_offset < 0 || m1_global < 0 || m2_global < 0)
+    return fail(LP_ERR_INVALID_ARGUMENT, "bad sharding arguments");
+  const int64_t ml = local_rows->m1 + local_rows->m2;
+  const int64_t want_m1 = std::max<int64_t>(0, std::min<int64_t>(m1_global - global_row_offset, ml));
+  if (local_rows->m1 != want_m1 || global_row_offset + ml > m1_global + m2_global)
+    return fail(LP_ERR_DIMENSION, "local m1/m2 inconsistent with the global row split");
+  if (nranks > 1 && !nccl_comm) return fail(LP_ERR_INVALID_ARGUMENT, "nccl_comm needed for nranks > 1");
+  init_pool();
+  lp_handle h = new lp_handle_s();
+  h->stream = (cudaStream_t)cuda_stream;
+  h->sharded = sharded_new(h->stream);
+  std::vector<lp_problem_desc> d{*local_rows};
+  std::vector<int64_t> off{global_row_offset};
+  const int rc = sharded_create(h->sharded, d, off, local_rows->n, m1_global, m2_global, nccl_comm, rank, nranks,
+                                false);
+  if (rc != LP_OK) {
+    free_handle(h);
+    return fail(rc, "sharded setup failed");
+  }
+  *out = h;
+  return LP_OK;
+}
+
+int lp_create_sharded_virtual(const lp_problem_desc *p, int32_t shards, void *cuda_stream, lp_handle *out) {
+  TRY(check_desc(p));
+  if (!out || shards < 1 || shards > 64) return fail(LP_ERR_INVALID_ARGUMENT, "shards must be in [1, 64]");
+  const int64_t m = p->m1 + p->m2;
+  // row split balanced by nnz: a cut on the row_ptr prefix
+  std::vector<int64_t> rp(m + 1);
+  if (cudaMemcpy(rp.data(), p->row_ptr, (m + 1) * sizeof(int64_t), cudaMemcpyDefault) != cudaSuccess)
+    return fail(LP_ERR_CUDA, "row_ptr read");
+  std::vector<int64_t> cut(shards + 1, 0);
+  cut[shards] = m;
+  for (int g = 1; g < shards; ++g) {
+    const int64_t target = rp[m] * g / shards;
+    cut[g] = std::lower_bound(rp.begin(), rp.end(), target) - rp.begin();
+    if (cut[g] < cut[g - 1]) cut[g] = cut[g - 1];
+    if (cut[g] > m) cut[g] = m;
+  }
+  std::vector<std::vector<int64_t>> lrp(shards);
+  std::vector<lp_problem_desc> d(shards);
+  std::vector<int64_t> off(shards);
+  for (int g = 0; g < shards; ++g) {
+    const int64_t r0 = cut[g], r1 = cut[g + 1];
+    lrp[g].resize(r1 - r0 + 1);
+    for (int64_t i = r0; i <= r1; ++i) lrp[g][i - r0] = rp[i] - rp[r0];
+    d[g] = *p;
+    d[g].m1 = std::max<int64_t>(0, std::min<int64_t>(p->m1 - r0, r1 - r0));
+    d[g].m2 = (r1 - r0) - d[g].m1;
+    d[g].nnz = rp[r1] - rp[r0];
+    d[g].row_ptr = lrp[g].data();
+    d[g].col_idx = p->col_idx + rp[r0];
+    d[g].values = p->values + rp[r0];
+    d[g].q = p->q + r0;
+    d[g].dense = 0;
+    off[g] = r0;
+  }
+  init_pool();
+  lp_handle h = new lp_handle_s();
+  h->stream = (cudaStream_t)cuda_stream;
+  h->sharded = sharded_new(h->stream);
+  const int rc = sharded_create(h->sharded, d, off, p->n, p->m1, p->m2, nullptr, 0, 1, true);
+  if (rc != LP_OK) {
+    free_handle(h);
+    return fail(rc, "sharded setup failed");
+  }
+  *out = h;
+  return LP_OK;
+}
+
+int lp_nccl_unique_id(void *out_id128) {
+#ifdef MPAX_HAVE_NCCL
+  if (!out_id128) return fail(LP_ERR_INVALID_ARGUMENT, "NULL id buffer");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return fail(LP_ERR_NCCL, "ncclGetUniqueId");
+  memcpy(out_id128, &id, sizeof(id));
+  return LP_OK;
+#else
+  return fail(LP_ERR_UNSUPPORTED, "built without NCCL");
+#endif
+}
+
+int lp_nccl_comm_init(void **comm, int nranks, const void *id128, int rank) {
+#ifdef MPAX_HAVE_NCCL
+  if (!comm || !id128) return fail(LP_ERR_INVALID_ARGUMENT, "NULL argument");
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  ncclComm_t c;
+  const ncclResult_t r = ncclCommInitRank(&c, nranks, id, rank);
+  if (r != ncclSuccess) return fail(LP_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  *comm = (void *)c;
+  return LP_OK;
+#else
+  return fail(LP_ERR_UNSUPPORTED, "built without NCCL");
+#endif
+}
+
+int lp_nccl_comm_destroy(void *comm) {
+#ifdef MPAX_HAVE_NCCL
+  if (comm) ncclCommDestroy((ncclComm_t)comm);
+  return LP_OK;
+#else
+  return fail(LP_ERR_UNSUPPORTED, "built without NCCL");
+#endif
 }
 
 int64_t lp_kernel_launch_count(void) { return g_launches.load(); }

@@ -389,7 +389,7 @@ const double *step_table(cudaStream_t s) {
   return g_tab[dev];
 }
 
-int setup_build(DevProblem &P, const int64_t *row_ptr64, cudaStream_t s, int *d_flag) {
+int setup_transpose(DevProblem &P, const int64_t *row_ptr64, cudaStream_t s, int *d_flag) {
   const int64_t m = P.m, n = P.n, nnz = P.nnz;
   int32_t *row_of = nullptr, *keys_out = nullptr, *idx_in = nullptr;
   size_t nz = (size_t)(nnz > 0 ? nnz : 1);
@@ -411,30 +411,60 @@ int setup_build(DevProblem &P, const int64_t *row_ptr64, cudaStream_t s, int *d_
     g_launches.fetch_add(4, std::memory_order_relaxed);  // CUB's onesweep/histogram kernels (approx.)
     MPAX_CUDA(cudaFreeAsync(temp, s));
   }
-  MPAX_LAUNCH(transpose_finish, grid_for(n + 1 + nnz), 256, 0, s, n, nnz, keys_out, P.perm, row_of, P.trp, P.tci, d_flag);
-  // Ruiz x10 then Pock-Chambolle alpha=1 (contract step 1)
-  double *rho = nullptr, *gam = nullptr;
-  MPAX_CUDA(cudaMallocAsync(&rho, (size_t)(m > 0 ? m : 1) * sizeof(double), s));
-  MPAX_CUDA(cudaMallocAsync(&gam, (size_t)n * sizeof(double), s));
-  MPAX_LAUNCH(set_ones, grid_for(m), 256, 0, s, m, P.Dr);
-  MPAX_LAUNCH(set_ones, grid_for(n), 256, 0, s, n, P.Dc);
-  for (int r = 0; r < 11; ++r) {
-    int use_sum = (r == 10);
-    MPAX_LAUNCH(precond_norms, grid_for(m + n, 128), 128, 0, s, m, n, P.rp, P.ci, P.trp, P.tci, P.perm, P.kv0,
-                P.Dr, P.Dc, rho, gam, use_sum, d_flag);
-    MPAX_LAUNCH(precond_update, grid_for(m + n), 256, 0, s, m, n, rho, gam, P.Dr, P.Dc, d_flag);
-  }
-  MPAX_CUDA(cudaMemsetAsync(P.kmax, 0, sizeof(double), s));
-  MPAX_LAUNCH(scale_kernel, grid_for(m + n, 128), 128, 0, s, m, n, P.rp, P.ci, P.trp, P.tci, P.perm, P.kv0, P.Dr,
-              P.Dc, P.kv, P.tkv, P.l0, P.u0, P.ls, P.us, (unsigned long long *)P.kmax, d_flag);
+  MPAX_LAUNCH(transpose_finish, grid_for(n + 1 + nnz), 256, 0, s, n, nnz, keys_out, P.perm, row_of, P.trp, P.tci,
+              d_flag);
   MPAX_CHECK_LAUNCH();
-  MPAX_CUDA(cudaFreeAsync(rho, s));
-  MPAX_CUDA(cudaFreeAsync(gam, s));
   MPAX_CUDA(cudaFreeAsync(row_of, s));
   MPAX_CUDA(cudaFreeAsync(keys_out, s));
   MPAX_CUDA(cudaFreeAsync(idx_in, s));
   P.avg_row = m > 0 ? (double)nnz / (double)m : 0.0;
   P.avg_col = (double)nnz / (double)n;
+  return LP_OK;
+}
+
+int setup_precond_init(DevProblem &P, cudaStream_t s) {
+  MPAX_LAUNCH(set_ones, grid_for(P.m), 256, 0, s, P.m, P.Dr);
+  MPAX_LAUNCH(set_ones, grid_for(P.n), 256, 0, s, P.n, P.Dc);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+int setup_precond_norms(DevProblem &P, double *rho, double *gam, int use_sum, cudaStream_t s, int *d_flag) {
+  MPAX_LAUNCH(precond_norms, grid_for(P.m + P.n, 128), 128, 0, s, P.m, P.n, P.rp, P.ci, P.trp, P.tci, P.perm, P.kv0,
+              P.Dr, P.Dc, rho, gam, use_sum, d_flag);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+int setup_precond_update(DevProblem &P, const double *rho, const double *gam, cudaStream_t s, int *d_flag) {
+  MPAX_LAUNCH(precond_update, grid_for(P.m + P.n), 256, 0, s, P.m, P.n, rho, gam, P.Dr, P.Dc, d_flag);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+int setup_scale(DevProblem &P, cudaStream_t s, int *d_flag) {
+  MPAX_CUDA(cudaMemsetAsync(P.kmax, 0, sizeof(double), s));
+  MPAX_LAUNCH(scale_kernel, grid_for(P.m + P.n, 128), 128, 0, s, P.m, P.n, P.rp, P.ci, P.trp, P.tci, P.perm, P.kv0,
+              P.Dr, P.Dc, P.kv, P.tkv, P.l0, P.u0, P.ls, P.us, (unsigned long long *)P.kmax, d_flag);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+int setup_build(DevProblem &P, const int64_t *row_ptr64, cudaStream_t s, int *d_flag) {
+  int rc = setup_transpose(P, row_ptr64, s, d_flag);
+  if (rc) return rc;
+  // Ruiz x10 then Pock-Chambolle alpha=1 (contract step 1)
+  double *rho = nullptr, *gam = nullptr;
+  MPAX_CUDA(cudaMallocAsync(&rho, (size_t)(P.m > 0 ? P.m : 1) * sizeof(double), s));
+  MPAX_CUDA(cudaMallocAsync(&gam, (size_t)P.n * sizeof(double), s));
+  if ((rc = setup_precond_init(P, s))) return rc;
+  for (int r = 0; r < 11; ++r) {
+    if ((rc = setup_precond_norms(P, rho, gam, r == 10, s, d_flag))) return rc;
+    if ((rc = setup_precond_update(P, rho, gam, s, d_flag))) return rc;
+  }
+  if ((rc = setup_scale(P, s, d_flag))) return rc;
+  MPAX_CUDA(cudaFreeAsync(rho, s));
+  MPAX_CUDA(cudaFreeAsync(gam, s));
   return LP_OK;
 }
 

@@ -1,0 +1,835 @@
+// sharded.cu -- one LP whose constraint matrix is ROW-SHARDED across GPUs
+// (§3.5 device parallelism: "the constraint
+// matrix is ... the primary candidate for sharding", listing P:234-241 shards
+// axis 0).  GPU g holds rows [r_g, r_g + m_g) of K = [G; A], the matching q and
+// dual iterate, the CSR of its K~_g' (n x m_g), and a replicated copy of every
+// n-long vector (x, K~'y, averages ...).  Per attempt (DESIGN.md §3 step 3/4):
+//   K~_g' y'_g  (local partial, n)  --ncclAllReduce(sum)-->  K~'y'    [SpMV #2]
+//   commit n-side + primal step x'   (replicated, identical on every GPU)
+//   commit m-side + K~_g x' + dual step y'_g                            [SpMV #1]
+//   ||dy||^2, <dy, K~dx> local partials --ncclAllReduce(sum)--> line-search decision
+// The decision state lives in device memory; the host only enqueues work: since
+// k grows by at most one per attempt, it enqueues (next_check - k) attempts and
+// synchronises once per 64 accepted steps to run the check.
+// Preconditioning reduces the column norms across GPUs (max for Ruiz, sum for
+// Pock-Chambolle).  With one GPU this is a multi-kernel single-GPU path; the
+// "virtual" mode runs p row shards on ONE GPU with a fixed-order device sum in
+// place of NCCL, which is how the partitioned arithmetic is tested here.
+#include <stdio.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+#ifdef MPAX_HAVE_NCCL
+#include <nccl.h>
+#endif
+
+namespace mpax {
+
+namespace {
+
+constexpr int kB = 256;  // threads per block
+constexpr int kV = 24;   // partial-sum slots
+
+struct ShState {
+  double omega, eta, W, ref, last, theta, ha, hb, rP, M, Iv, eta_used, metric, nc0, nq0, eta0;
+  long long k, j, k_in, restarts;
+  int rejects, status, pending, halt, restart, outsel, csel, r2;
+  double colsum[kV];  // totals over this GPU's columns (replicated data: identical on every GPU)
+  double rowsum[kV];  // totals over this GPU's rows; reduced across GPUs in place
+  unsigned int cnt_cols, cnt_rows;
+};
+
+struct Vecs {
+  double *x, *KTy, *xp, *KTyp, *xa, *KTya, *xr, *cs, *red;  // n
+  double *y, *Kx, *yp, *Kxp, *ya, *Kxa, *yr, *qs;           // m_local
+  double *part;                                             // blocks x kV
+  const double *c0, *q0, *X0, *Y0;
+};
+
+__device__ __forceinline__ void kkt_row(double *v, bool orig, bool ge, double dr, double ys, double Kxs, double q0,
+                                        double qs) {
+  const double Kx = orig ? Kxs / dr : Kxs, q = orig ? q0 : qs, y = orig ? dr * ys : ys;
+  double r = q - Kx;
+  if (ge) r = fmax(r, 0.0);
+  v[0] += r * r;
+  v[3] += q * y;
+}
+__device__ __forceinline__ void kkt_col(double *v, bool orig, double dc, double xs, double KTys, double c0, double cs,
+                                        double l0, double ls, double u0, double us) {
+  const double x = orig ? dc * xs : xs, KTy = orig ? KTys / dc : KTys;
+  const double c = orig ? c0 : cs, l = orig ? l0 : ls, u = orig ? u0 : us;
+  const double lam = c - KTy, lp = fmax(lam, 0.0), lm = fmax(-lam, 0.0);
+  double d = 0.0;
+  if (l == -INFINITY) d += lp;
+  if (u == INFINITY) d += lm;
+  v[1] += d * d;
+  v[2] += c * x;
+  if (l > -INFINITY) v[3] += l * lp;
+  if (u < INFINITY) v[3] -= u * lm;
+}
+
+struct K5 {
+  double pres, dres, pobj, dobj, gap;
+};
+__device__ __forceinline__ K5 mk5(const double *v) {
+  K5 k;
+  k.pres = sqrt(v[0]); k.dres = sqrt(v[1]); k.pobj = v[2]; k.dobj = v[3]; k.gap = fabs(v[2] - v[3]);
+  return k;
+}
+__device__ __forceinline__ bool pass5(const K5 &k, double nq, double nc, double ea, double er) {
+  return k.pres <= ea + er * nq && k.dres <= ea + er * nc && k.gap <= ea + er * (fabs(k.pobj) + fabs(k.dobj));
+}
+__device__ __forceinline__ double rel5(const K5 &k, double nq, double nc) {
+  return fmax(k.pres / (1.0 + nq), fmax(k.dres / (1.0 + nc), k.gap / (1.0 + fabs(k.pobj) + fabs(k.dobj))));
+}
+
+// row r of a CSR matrix times x with G lanes (all lanes get the sum); 4 entries in flight per lane
+__device__ __forceinline__ double row_dot(int64_t r, bool valid, int G, int gl, const int32_t *__restrict__ rp,
+                                          const int32_t *__restrict__ ci, const double *__restrict__ v,
+                                          const double *__restrict__ x) {
+  double s0 = 0.0, s1 = 0.0;
+  if (valid) {
+    const int32_t e = __ldg(rp + r + 1);
+    for (int32_t p = __ldg(rp + r) + gl; p < e; p += 4 * G) {
+      int32_t c[4];
+      double w[4], xv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int32_t q = p + k * G;
+        const bool ok = q < e;
+        c[k] = ok ? __ldcs(ci + q) : 0;
+        w[k] = ok ? __ldcs(v + q) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) xv[k] = (p + k * G < e) ? x[c[k]] : 0.0;
+      s0 += w[0] * xv[0];
+      s1 += w[1] * xv[1];
+      s0 += w[2] * xv[2];
+      s1 += w[3] * xv[3];
+    }
+  }
+  double s = s0 + s1;
+  for (int off = G >> 1; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+  return s;
+}
+
+// Block partials of V values into part[block][.]; the last block to finish sums
+// them in block order (all 256 threads, fixed assignment + fixed tree) into out.
+template <int V>
+__device__ __forceinline__ void last_block_sum(double (&v)[V], double *part, unsigned int *counter, double *out) {
+  __shared__ double sred[kB / 32][kV];
+  __shared__ double stree[kB];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    double s = v[k];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    if (lane == 0) sred[w][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < V) {
+    double a = 0.0;
+    for (int ww = 0; ww < kB / 32; ++ww) a += sred[ww][threadIdx.x];
+    part[(int64_t)blockIdx.x * kV + threadIdx.x] = a;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int k = 0; k < V; ++k) {
+    double a = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kB) a += __ldcg(part + (int64_t)b * kV + k);
+    stree[threadIdx.x] = a;
+    __syncthreads();
+    for (int h = kB / 2; h; h >>= 1) {
+      if (threadIdx.x < h) stree[threadIdx.x] += stree[threadIdx.x + h];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[k] = stree[0];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+inline int blocks_for(int64_t work) {
+  int64_t g = (work + kB - 1) / kB;
+  if (g < 1) g = 1;
+  if (g > 148 * 8) g = 148 * 8;
+  return (int)g;
+}
+
+// ------------------------------------------------------------------ kernels --
+
+__global__ void k_cols_spmv(const ShState *st, int64_t n, int G, const int32_t *trp, const int32_t *tci,
+                            const double *tkv, const double *ysrc, double *out) {
+  if (st->halt) return;
+  const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x, ng = (int64_t)gridDim.x * kB / G;
+  const int gl = (int)(gt % G);
+  const int64_t iters = (n + ng - 1) / ng;
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t j = it * ng + gt / G;
+    const double s = row_dot(j, j < n, G, gl, trp, tci, tkv, ysrc);
+    if (j < n && gl == 0) out[j] = s;
+  }
+}
+
+enum { COLS_STEP = 0, COLS_COMMIT_ONLY = 1, COLS_AVG = 2, COLS_INIT = 3, COLS_INIT2 = 4, COLS_OUT = 5 };
+enum { ROWS_STEP = 0, ROWS_COMMIT_ONLY = 1, ROWS_AVG = 2, ROWS_INIT = 3, ROWS_INIT2 = 4, ROWS_OUT = 5 };
+
+__global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, const Vecs V) {
+  if (st->halt && mode != COLS_OUT) return;
+  const bool r2 = st->r2, pend = st->pending;
+  const double tau = st->eta / st->omega, theta = st->theta, ha = st->ha, hb = st->hb;
+  double v[20] = {};
+  const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x, st_ = (int64_t)gridDim.x * kB;
+  for (int64_t j = gt; j < n; j += st_) {
+    const double dc = P.Dc[j];
+    if (mode == COLS_STEP || mode == COLS_COMMIT_ONLY) {
+      double xv = V.x[j], kt = V.KTy[j];
+      const double kty = V.red[j];
+      if (pend) {
+        const double xpv = V.xp[j];
+        if (!r2) {
+          V.xa[j] += theta * (xpv - V.xa[j]);
+          xv = xpv; kt = kty;
+        } else {
+          xv = ha * (2.0 * xpv - xv) + hb * V.xa[j];
+          kt = ha * (2.0 * kty - kt) + hb * V.KTya[j];
+        }
+        V.x[j] = xv; V.KTy[j] = kt;
+      }
+      if (mode == COLS_STEP) {
+        const double xn = median3(P.ls[j], xv - tau * (V.cs[j] - kt), P.us[j]);
+        V.xp[j] = xn;
+        const double d = xn - xv;
+        v[0] += d * d;
+      } else {
+        V.KTyp[j] = kty;
+        if (r2 && pend) {
+          const double xpv = V.xp[j];
+          kkt_col(v, true, dc, xpv, kty, V.c0[j], V.cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+          const double d = xpv - V.xr[j];
+          v[4] += d * d;
+        }
+      }
+    } else if (mode == COLS_AVG) {
+      const double kta = V.red[j];
+      V.KTya[j] = kta;
+      const double xaj = V.xa[j], xj = V.x[j], ktj = V.KTy[j], c0 = V.c0[j], csj = V.cs[j], l0 = P.l0[j],
+                   lsj = P.ls[j], u0 = P.u0[j], usj = P.us[j];
+      kkt_col(v + 0, true, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
+      kkt_col(v + 4, true, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+      kkt_col(v + 8, false, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
+      kkt_col(v + 12, false, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+      const double da = xaj - V.xr[j], dcur = xj - V.xr[j];
+      v[16] += da * da;
+      v[18] += dcur * dcur;
+    } else if (mode == COLS_INIT) {
+      const double c = V.c0[j], cj = c * dc;
+      V.cs[j] = cj;
+      v[0] += cj * cj;
+      v[1] += c * c;
+      const double xv = median3(P.ls[j], V.X0 ? V.X0[j] / dc : 0.0, P.us[j]);
+      V.x[j] = xv; V.xa[j] = xv; V.xr[j] = xv; V.xp[j] = xv;
+    } else if (mode == COLS_INIT2) {
+      const double kty = V.red[j];
+      V.KTy[j] = kty; V.KTya[j] = kty; V.KTyp[j] = kty;
+      kkt_col(v, false, dc, V.x[j], kty, 0.0, V.cs[j], 0.0, P.ls[j], 0.0, P.us[j]);
+    } else {  // COLS_OUT
+      const int sel = st->outsel;
+      const double xs = sel ? (r2 ? V.xp[j] : V.xa[j]) : V.x[j];
+      const double kt = sel ? (r2 ? V.KTyp[j] : V.KTya[j]) : V.KTy[j];
+      kkt_col(v, true, dc, xs, kt, V.c0[j], V.cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+      V.red[j] = dc * xs;                    // unscaled x (output buffer)
+      V.KTyp[j] = V.c0[j] - kt / dc;         // reduced costs (output buffer)
+    }
+  }
+  last_block_sum<20>(v, V.part, &st->cnt_cols, st->colsum);
+}
+
+__global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, const DevProblem P, const Vecs V) {
+  if (st->halt && mode != ROWS_OUT) return;
+  const bool r2 = st->r2, pend = st->pending;
+  const double sigma = st->eta * st->omega, theta = st->theta, ha = st->ha, hb = st->hb;
+  double v[20] = {};
+  const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x;
+  const bool spmv = (mode == ROWS_STEP || mode == ROWS_AVG || mode == ROWS_INIT2);
+  const int g = spmv ? G : 1;
+  const int64_t ng = (int64_t)gridDim.x * kB / g;
+  const int gl = (int)(gt % g);
+  const int64_t iters = (m + ng - 1) / ng;
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t i = it * ng + gt / g;
+    const bool ok = i < m;
+    const bool lead = ok && gl == 0;
+    const double *src = mode == ROWS_AVG ? V.xa : (mode == ROWS_INIT2 ? V.x : V.xp);
+    const double s = spmv ? row_dot(i, ok, g, gl, P.rp, P.ci, P.kv, src) : 0.0;
+    if (!lead) continue;
+    const double dr = P.Dr[i];
+    const bool ge = i < m1;
+    if (mode == ROWS_STEP || mode == ROWS_COMMIT_ONLY) {
+      double yv = V.y[i], kxv = V.Kx[i];
+      if (pend) {
+        const double ypv = V.yp[i], kxp = V.Kxp[i];
+        if (!r2) {
+          V.ya[i] += theta * (ypv - V.ya[i]);
+          yv = ypv; kxv = kxp;
+        } else {
+          yv = ha * (2.0 * ypv - yv) + hb * V.ya[i];
+          kxv = ha * (2.0 * kxp - kxv) + hb * V.Kxa[i];
+        }
+        V.y[i] = yv; V.Kx[i] = kxv;
+      }
+      if (mode == ROWS_STEP) {
+        double yn = yv + sigma * (V.qs[i] - 2.0 * s + kxv);
+        if (ge) yn = fmax(yn, 0.0);
+        V.yp[i] = yn; V.Kxp[i] = s;
+        const double d = yn - yv;
+        v[0] += d * d;
+        v[1] += d * (s - kxv);
+      } else if (r2 && pend) {
+        const double ypv = V.yp[i], kxp = V.Kxp[i];
+        kkt_row(v, true, ge, dr, ypv, kxp, V.q0[i], V.qs[i]);
+        const double d = ypv - V.yr[i];
+        v[5] += d * d;
+      }
+    } else if (mode == ROWS_AVG) {
+      V.Kxa[i] = s;
+      const double yai = V.ya[i], yi = V.y[i], kxi = V.Kx[i], q0 = V.q0[i], qsi = V.qs[i];
+      kkt_row(v + 0, true, ge, dr, yai, s, q0, qsi);
+      kkt_row(v + 4, true, ge, dr, yi, kxi, q0, qsi);
+      kkt_row(v + 8, false, ge, dr, yai, s, q0, qsi);
+      kkt_row(v + 12, false, ge, dr, yi, kxi, q0, qsi);
+      const double da = yai - V.yr[i], dcur = yi - V.yr[i];
+      v[17] += da * da;
+      v[19] += dcur * dcur;
+    } else if (mode == ROWS_INIT) {
+      const double q = V.q0[i], qi = q * dr;
+      V.qs[i] = qi;
+      v[0] += qi * qi;
+      v[1] += q * q;
+      double yv = V.Y0 ? V.Y0[i] / dr : 0.0;
+      if (ge) yv = fmax(yv, 0.0);
+      V.y[i] = yv; V.ya[i] = yv; V.yr[i] = yv; V.yp[i] = yv;
+    } else if (mode == ROWS_INIT2) {
+      V.Kx[i] = s; V.Kxa[i] = s; V.Kxp[i] = s;
+      kkt_row(v, false, ge, dr, V.y[i], s, 0.0, V.qs[i]);
+    } else {  // ROWS_OUT
+      const int sel = st->outsel;
+      const double ys = sel ? (r2 ? V.yp[i] : V.ya[i]) : V.y[i];
+      const double kx = sel ? (r2 ? V.Kxp[i] : V.Kxa[i]) : V.Kx[i];
+      kkt_row(v, true, ge, dr, ys, kx, V.q0[i], V.qs[i]);
+      V.Kxp[i] = dr * ys;  // unscaled y (output buffer)
+    }
+  }
+  last_block_sum<20>(v, V.part, &st->cnt_rows, st->rowsum);
+}
+
+// ---- single-thread decisions (identical inputs on every GPU) ----
+__global__ void k_init_decide(ShState *st, int stage) {
+  if (stage == 0) {  // norms: colsum = (|c~|^2, |c|^2) replicated; rowsum = (|q~|^2, |q|^2) reduced
+    const double nc = sqrt(st->colsum[0]), nq = sqrt(st->rowsum[0]);
+    st->nc0 = sqrt(st->colsum[1]);
+    st->nq0 = sqrt(st->rowsum[1]);
+    st->omega = (nc > 1e-10 && nq > 1e-10) ? nc / nq : 1.0;
+    st->eta = st->eta0;
+  } else if (!st->r2) {  // raPDHG reference KKT_omega(z0): rows (reduced) + columns
+    double t[4];
+    for (int k = 0; k < 4; ++k) t[k] = st->rowsum[k] + st->colsum[k];
+    const K5 ks = mk5(t);
+    st->ref = sqrt(st->omega * ks.pres * ks.pres + ks.dres * ks.dres / st->omega + ks.gap * ks.gap);
+  }
+}
+
+__global__ void k_decide(ShState *st, const double *tab, int64_t check_freq, int64_t iter_limit) {
+  if (st->halt) return;
+  st->j += 1;
+  double f1, f2;
+  step_factors(tab, st->j, f1, f2);
+  const double dx2 = st->colsum[0], dy2 = st->rowsum[0], I = st->rowsum[1];
+  const double M = st->omega * dx2 + dy2 / st->omega;
+  const double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : INFINITY;
+  const bool acc = st->eta <= eb;
+  const double eta_used = st->eta;
+  st->eta = fmin(f1 * eb, f2 * st->eta);
+  if (!acc) {
+    st->pending = 0;
+    if (++st->rejects >= 100) { st->status = LP_NUMERICAL_ERROR; st->halt = 1; st->outsel = 0; }
+    return;
+  }
+  st->rejects = 0;
+  if (!st->r2) {
+    const double W1 = st->W + eta_used;
+    st->theta = eta_used / W1;
+    st->W = W1;
+  } else {
+    st->rP = sqrt(fmax(0.0, M / eta_used - 2.0 * I));
+    if (st->k_in == 0) st->ref = st->rP;
+    st->ha = (double)(st->k_in + 1) / (double)(st->k_in + 2);
+    st->hb = 1.0 / (double)(st->k_in + 2);
+  }
+  st->k += 1;
+  st->k_in += 1;
+  st->pending = 1;
+}
+
+__global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, int64_t iter_limit) {
+  double t[20];
+  for (int k = 0; k < 20; ++k) t[k] = st->colsum[k] + st->rowsum[k];
+  st->pending = 0;
+  st->restart = 0;
+  const double nq0 = st->nq0, nc0 = st->nc0;
+  if (st->r2) {
+    const K5 kw = mk5(t);
+    if (pass5(kw, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
+    if (st->k == iter_limit) { st->status = LP_ITERATION_LIMIT; st->halt = 1; st->outsel = 1; return; }
+    st->metric = st->rP;
+    st->csel = 1;
+    st->colsum[22] = t[4];
+    st->colsum[23] = t[5];
+  } else {
+    const K5 ka = mk5(t + 0), kc = mk5(t + 4);
+    if (pass5(ka, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
+    if (pass5(kc, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 0; return; }
+    if (st->k == iter_limit) {
+      st->status = LP_ITERATION_LIMIT; st->halt = 1;
+      st->outsel = rel5(ka, nq0, nc0) < rel5(kc, nq0, nc0) ? 1 : 0;
+      return;
+    }
+    const K5 sa = mk5(t + 8), sc = mk5(t + 12);
+    const double om = st->omega;
+    const double e_a = sqrt(om * sa.pres * sa.pres + sa.dres * sa.dres / om + sa.gap * sa.gap);
+    const double e_c = sqrt(om * sc.pres * sc.pres + sc.dres * sc.dres / om + sc.gap * sc.gap);
+    if (e_a < e_c) { st->csel = 1; st->metric = e_a; st->colsum[22] = t[16]; st->colsum[23] = t[17]; }
+    else { st->csel = 0; st->metric = e_c; st->colsum[22] = t[18]; st->colsum[23] = t[19]; }
+  }
+  const double metric = st->metric;
+  const bool restart = ((double)st->k_in >= 0.36 * (double)st->k) || (metric <= 0.2 * st->ref) ||
+                       (metric <= 0.8 * st->ref && metric > st->last);
+  st->last = metric;
+  if (restart) {
+    st->restart = 1;
+    st->restarts += 1;
+    const double dxn = sqrt(st->colsum[22]), dyn = sqrt(st->colsum[23]);
+    if (dxn > 1e-10 && dyn > 1e-10) st->omega = sqrt(st->omega * (dyn / dxn));
+    st->k_in = 0;
+    if (!st->r2) { st->W = 0.0; st->ref = metric; }
+  }
+}
+
+__global__ void k_restart(const ShState *st, int64_t n, int64_t m, const Vecs V) {
+  if (!st->restart) return;
+  const bool r2 = st->r2, csel = st->csel;
+  const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x, s = (int64_t)gridDim.x * kB;
+  for (int64_t j = gt; j < n; j += s) {
+    double xv = V.x[j], kt = V.KTy[j];
+    if (csel) { xv = r2 ? V.xp[j] : V.xa[j]; kt = r2 ? V.KTyp[j] : V.KTya[j]; }
+    V.x[j] = xv; V.xr[j] = xv; V.xa[j] = xv; V.KTy[j] = kt; V.KTya[j] = kt;
+  }
+  for (int64_t i = gt; i < m; i += s) {
+    double yv = V.y[i], kx = V.Kx[i];
+    if (csel) { yv = r2 ? V.yp[i] : V.ya[i]; kx = r2 ? V.Kxp[i] : V.Kxa[i]; }
+    V.y[i] = yv; V.yr[i] = yv; V.ya[i] = yv; V.Kx[i] = kx; V.Kxa[i] = kx;
+  }
+}
+
+__global__ void k_final(const ShState *st, lp_result *res) {
+  double t[4];
+  for (int k = 0; k < 4; ++k) t[k] = st->colsum[k] + st->rowsum[k];
+  const K5 ko = mk5(t);
+  lp_result r;
+  r.status = st->status; r.pad = 0;
+  r.iterations = st->k; r.attempts = st->j; r.restarts = st->restarts;
+  r.primal_objective = ko.pobj; r.dual_objective = ko.dobj;
+  r.primal_residual = ko.pres; r.dual_residual = ko.dres; r.gap = ko.gap;
+  r.rel_kkt = rel5(ko, st->nq0, st->nc0);
+  r.omega = st->omega; r.eta = st->eta; r.solve_seconds = 0.0;
+  *res = r;
+}
+
+// fixed-order reduction over p same-device shard buffers (virtual mode)
+__global__ void k_vreduce(double *const *ptrs, int p, int64_t count, int op_max) {
+  for (int64_t t = blockIdx.x * (int64_t)kB + threadIdx.x; t < count; t += (int64_t)gridDim.x * kB) {
+    double a = ptrs[0][t];
+    for (int s = 1; s < p; ++s) a = op_max ? fmax(a, ptrs[s][t]) : a + ptrs[s][t];
+    for (int s = 0; s < p; ++s) ptrs[s][t] = a;
+  }
+}
+
+__global__ void k_set_eta0(ShState *st, const double *kmax, int r2) {
+  const double k = *kmax;
+  st->eta0 = k > 0.0 ? 1.0 / k : 1.0;
+  st->r2 = r2;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ engine --
+
+struct ShardData {
+  DevProblem P;
+  int64_t row_offset = 0;
+  int64_t *rp64 = nullptr;
+  Vecs V{};
+  ShState *st = nullptr;
+  double *X = nullptr, *Y = nullptr, *L = nullptr;
+  void *arena = nullptr;
+  void *vecs = nullptr;
+  int nb = 0;
+};
+
+struct ShardedLP {
+  cudaStream_t s = nullptr;
+  int nranks = 1, rank = 0;
+  bool virt = false;
+  void *comm = nullptr;  // ncclComm_t (borrowed)
+  int64_t n = 0, m_global = 0, m1_global = 0;
+  std::vector<ShardData> sh;
+  double **d_ptrs = nullptr;  // virtual mode: per-shard pointer tables
+  ShState *h_st = nullptr;
+  lp_result *d_res = nullptr, *h_res = nullptr;
+  int *d_flags = nullptr, *h_flags = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool solved = false;
+};
+
+namespace {
+
+int reduce_across(ShardedLP &E, int slot, int64_t count, bool op_max, double *const *bufs_host) {
+  if (E.virt) {
+    if (E.sh.size() < 2) return LP_OK;
+    double **tab = E.d_ptrs + slot * 64;
+    MPAX_CUDA(cudaMemcpyAsync(tab, bufs_host, E.sh.size() * sizeof(double *), cudaMemcpyHostToDevice, E.s));
+    MPAX_LAUNCH(k_vreduce, blocks_for(count), kB, 0, E.s, tab, (int)E.sh.size(), count, op_max ? 1 : 0);
+    MPAX_CHECK_LAUNCH();
+    return LP_OK;
+  }
+  if (E.nranks <= 1) return LP_OK;
+#ifdef MPAX_HAVE_NCCL
+  ncclResult_t r = ncclAllReduce(bufs_host[0], bufs_host[0], (size_t)count, ncclDouble, op_max ? ncclMax : ncclSum,
+                                 (ncclComm_t)E.comm, E.s);
+  if (r != ncclSuccess) {
+    set_error_detail(std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+    return LP_ERR_NCCL;
+  }
+  return LP_OK;
+#else
+  set_error_detail("built without NCCL");
+  return LP_ERR_UNSUPPORTED;
+#endif
+}
+
+#define STRY(x)              \
+  do {                       \
+    int r_ = (x);            \
+    if (r_ != LP_OK) return r_; \
+  } while (0)
+
+int reduce_vec(ShardedLP &E, int slot, std::vector<double *> bufs, int64_t count, bool op_max) {
+  return reduce_across(E, slot, count, op_max, bufs.data());
+}
+
+int reduce_rowsum(ShardedLP &E, int slot) {
+  std::vector<double *> b;
+  for (auto &d : E.sh) b.push_back(d.st->rowsum);
+  return reduce_vec(E, slot, b, kV, false);
+}
+
+}  // namespace
+
+// Build the shards: validate, transpose, cross-shard preconditioning, scaling.
+int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const std::vector<int64_t> &offsets) {
+  cudaStream_t s = E.s;
+  const int p = (int)descs.size();
+  E.sh.resize(p);
+  MPAX_CUDA(cudaMallocAsync((void **)&E.d_ptrs, 8 * 64 * sizeof(double *), s));
+  for (int g = 0; g < p; ++g) {
+    const lp_problem_desc &d = descs[g];
+    ShardData &S = E.sh[g];
+    DevProblem &P = S.P;
+    P.n = d.n; P.m1 = d.m1; P.m2 = d.m2; P.m = d.m1 + d.m2; P.nnz = d.nnz;
+    S.row_offset = offsets[g];
+    const int64_t n = P.n, m = P.m, nnz = P.nnz;
+    size_t bytes = 0;
+    auto al = [&](size_t b) { size_t o = bytes; bytes += (b + 255) & ~(size_t)255; return o; };
+    const size_t o_rp64 = al((m + 1) * 8), o_rp = al((m + 1) * 4), o_ci = al(nnz * 4 + 4), o_kv0 = al(nnz * 8 + 8),
+                 o_kv = al(nnz * 8 + 8), o_trp = al((n + 1) * 4), o_tci = al(nnz * 4 + 4), o_perm = al(nnz * 4 + 4),
+                 o_tkv = al(nnz * 8 + 8), o_l0 = al(n * 8), o_u0 = al(n * 8), o_ls = al(n * 8), o_us = al(n * 8),
+                 o_Dr = al(m * 8 + 8), o_Dc = al(n * 8), o_kmax = al(8), o_c0 = al(n * 8), o_q0 = al(m * 8 + 8),
+                 o_st = al(sizeof(ShState)), o_flag = al(64);
+    char *base = nullptr;
+    MPAX_CUDA(cudaMallocAsync((void **)&base, bytes, s));
+    S.arena = base;
+    S.rp64 = (int64_t *)(base + o_rp64); P.rp = (int32_t *)(base + o_rp); P.ci = (int32_t *)(base + o_ci);
+    P.kv0 = (double *)(base + o_kv0); P.kv = (double *)(base + o_kv); P.trp = (int32_t *)(base + o_trp);
+    P.tci = (int32_t *)(base + o_tci); P.perm = (int32_t *)(base + o_perm); P.tkv = (double *)(base + o_tkv);
+    P.l0 = (double *)(base + o_l0); P.u0 = (double *)(base + o_u0); P.ls = (double *)(base + o_ls);
+    P.us = (double *)(base + o_us); P.Dr = (double *)(base + o_Dr); P.Dc = (double *)(base + o_Dc);
+    P.kmax = (double *)(base + o_kmax);
+    double *c0 = (double *)(base + o_c0), *q0 = (double *)(base + o_q0);
+    S.st = (ShState *)(base + o_st);
+    int *flag = (int *)(base + o_flag);
+    P.tab = const_cast<double *>(step_table(s));
+    auto cp = [&](void *dst, const void *src, size_t b) -> int {
+      if (b) MPAX_CUDA(cudaMemcpyAsync(dst, src, b, cudaMemcpyDefault, s));
+      return LP_OK;
+    };
+    STRY(cp(S.rp64, d.row_ptr, (m + 1) * 8));
+    STRY(cp(P.ci, d.col_idx, nnz * 4));
+    STRY(cp(P.kv0, d.values, nnz * 8));
+    STRY(cp(P.l0, d.l, n * 8));
+    STRY(cp(P.u0, d.u, n * 8));
+    STRY(cp(c0, d.c, n * 8));
+    STRY(cp(q0, d.q, m * 8));
+    MPAX_CUDA(cudaMemsetAsync(S.st, 0, sizeof(ShState), s));
+    const int init[8] = {0, INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX, 0, 0, 0};
+    memcpy(E.h_flags + 8 * g, init, sizeof(init));
+    STRY(cp(flag, E.h_flags + 8 * g, sizeof(init)));
+    STRY(setup_validate(P, S.rp64, c0, n, q0, m, s, flag));
+    STRY(setup_transpose(P, S.rp64, s, flag));
+    STRY(cp(E.h_flags + 8 * g, flag, 8 * sizeof(int)));
+    // vectors
+    double *vec = nullptr;
+    S.nb = 148 * 8;
+    const size_t nv = 9 * (size_t)n + 8 * (size_t)(m > 0 ? m : 1) + (size_t)S.nb * kV + 3 * (size_t)n +
+                      (size_t)(m > 0 ? m : 1);
+    MPAX_CUDA(cudaMallocAsync((void **)&vec, nv * sizeof(double), s));
+    S.vecs = vec;
+    Vecs &V = S.V;
+    double *w = vec;
+    V.x = w; w += n; V.KTy = w; w += n; V.xp = w; w += n; V.KTyp = w; w += n; V.xa = w; w += n; V.KTya = w; w += n;
+    V.xr = w; w += n; V.cs = w; w += n; V.red = w; w += n;
+    const int64_t mm = m > 0 ? m : 1;
+    V.y = w; w += mm; V.Kx = w; w += mm; V.yp = w; w += mm; V.Kxp = w; w += mm; V.ya = w; w += mm;
+    V.Kxa = w; w += mm; V.yr = w; w += mm; V.qs = w; w += mm;
+    V.part = w; w += (size_t)S.nb * kV;
+    S.X = w; w += n; S.L = w; w += n; w += n; S.Y = w; w += mm;
+    V.c0 = c0; V.q0 = q0;
+  }
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  for (int g = 0; g < p; ++g) {
+    const int *f = E.h_flags + 8 * g;
+    if (f[0] == 3) return LP_ERR_DIMENSION;
+    if (f[0] == 2) return LP_ERR_NAN;
+    if (f[0] == 1) return LP_ERR_CROSSED_BOUNDS;
+  }
+  // preconditioning with column norms reduced across shards
+  std::vector<double *> rho(p), gam(p);
+  for (int g = 0; g < p; ++g) {
+    MPAX_CUDA(cudaMallocAsync((void **)&rho[g], (size_t)(E.sh[g].P.m + 1) * sizeof(double), s));
+    MPAX_CUDA(cudaMallocAsync((void **)&gam[g], (size_t)E.n * sizeof(double), s));
+    STRY(setup_precond_init(E.sh[g].P, s));
+  }
+  int *noflag = nullptr;
+  MPAX_CUDA(cudaMallocAsync((void **)&noflag, sizeof(int), s));
+  MPAX_CUDA(cudaMemsetAsync(noflag, 0, sizeof(int), s));
+  for (int r = 0; r < 11; ++r) {
+    for (int g = 0; g < p; ++g) STRY(setup_precond_norms(E.sh[g].P, rho[g], gam[g], r == 10, s, noflag));
+    STRY(reduce_vec(E, 1, gam, E.n, r < 10));
+    for (int g = 0; g < p; ++g) STRY(setup_precond_update(E.sh[g].P, rho[g], gam[g], s, noflag));
+  }
+  std::vector<double *> km(p);
+  for (int g = 0; g < p; ++g) {
+    STRY(setup_scale(E.sh[g].P, s, noflag));
+    km[g] = E.sh[g].P.kmax;
+  }
+  STRY(reduce_vec(E, 2, km, 1, true));
+  for (int g = 0; g < p; ++g) {
+    MPAX_CUDA(cudaFreeAsync(rho[g], s));
+    MPAX_CUDA(cudaFreeAsync(gam[g], s));
+  }
+  MPAX_CUDA(cudaFreeAsync(noflag, s));
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  return LP_OK;
+}
+
+namespace {
+
+inline int group_of(double avg) {
+  int g = 1;
+  while (g * 2 <= avg / 4.0 && g < 32) g *= 2;
+  return g;
+}
+
+int launch_cols(ShardedLP &E, int mode) {
+  for (auto &S : E.sh) {
+    MPAX_LAUNCH(k_cols, blocks_for(E.n), kB, 0, E.s, S.st, mode, E.n, S.P, S.V);
+  }
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+int launch_rows(ShardedLP &E, int mode) {
+  for (auto &S : E.sh) {
+    const int G = group_of(S.P.avg_row);
+    const bool spmv = (mode == ROWS_STEP || mode == ROWS_AVG || mode == ROWS_INIT2);
+    MPAX_LAUNCH(k_rows, blocks_for(S.P.m * (spmv ? G : 1)), kB, 0, E.s, S.st, mode, S.P.m, S.P.m1, G, S.P, S.V);
+  }
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+// K~_g' src_g into red (every shard), then the cross-shard sum
+int cols_spmv(ShardedLP &E, int which /*0: yp, 1: y, 2: ya*/) {
+  std::vector<double *> bufs;
+  for (auto &S : E.sh) {
+    const int G = group_of(S.P.avg_col);
+    const double *src = which == 0 ? S.V.yp : (which == 1 ? S.V.y : S.V.ya);
+    MPAX_LAUNCH(k_cols_spmv, blocks_for(E.n * G), kB, 0, E.s, S.st, E.n, G, S.P.trp, S.P.tci, S.P.tkv, src, S.V.red);
+    bufs.push_back(S.V.red);
+  }
+  MPAX_CHECK_LAUNCH();
+  return reduce_vec(E, 0, bufs, E.n, false);
+}
+
+}  // namespace
+
+int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const double *Y0, lp_result *out) {
+  cudaStream_t s = E.s;
+  const bool r2 = o.algorithm == LP_R2HPDHG;
+  for (auto &S : E.sh) {
+    MPAX_CUDA(cudaMemsetAsync(S.st, 0, sizeof(ShState), s));
+    S.V.X0 = X0;                                        // full n (replicated)
+    S.V.Y0 = Y0 ? Y0 + S.row_offset - (E.virt ? 0 : 0) : nullptr;
+    MPAX_LAUNCH(k_set_eta0, 1, 1, 0, s, S.st, S.P.kmax, r2 ? 1 : 0);
+  }
+  if (!E.virt) for (auto &S : E.sh) S.V.Y0 = Y0;        // a real rank passes its own rows
+  MPAX_CUDA(cudaEventRecord(E.ev0, s));
+  // ---- step 2 ----
+  STRY(launch_cols(E, COLS_INIT));
+  STRY(launch_rows(E, ROWS_INIT));
+  STRY(reduce_rowsum(E, 3));
+  for (auto &S : E.sh) MPAX_LAUNCH(k_init_decide, 1, 1, 0, s, S.st, 0);
+  STRY(cols_spmv(E, 1));
+  STRY(launch_cols(E, COLS_INIT2));
+  STRY(launch_rows(E, ROWS_INIT2));
+  STRY(reduce_rowsum(E, 3));
+  for (auto &S : E.sh) MPAX_LAUNCH(k_init_decide, 1, 1, 0, s, S.st, 1);
+  MPAX_CHECK_LAUNCH();
+  // ---- attempts, checks ----
+  const int64_t F = o.check_frequency, LIM = o.iteration_limit;
+  int64_t k = 0;
+  for (;;) {
+    int64_t next = ((k / F) + 1) * F;
+    if (next > LIM) next = LIM;
+    const int64_t chunk = next - k;
+    for (int64_t a = 0; a < chunk; ++a) {
+      STRY(cols_spmv(E, 0));
+      STRY(launch_cols(E, COLS_STEP));
+      STRY(launch_rows(E, ROWS_STEP));
+      STRY(reduce_rowsum(E, 3));
+      for (auto &S : E.sh) MPAX_LAUNCH(k_decide, 1, 1, 0, s, S.st, S.P.tab, F, LIM);
+    }
+    MPAX_CHECK_LAUNCH();
+    MPAX_CUDA(cudaMemcpyAsync(E.h_st, E.sh[0].st, sizeof(ShState), cudaMemcpyDeviceToHost, s));
+    MPAX_CUDA(cudaStreamSynchronize(s));
+    if (E.h_st->halt) break;
+    k = E.h_st->k;
+    if (k != next) continue;
+    // check (step 5): commit-only; raPDHG: average products + every KKT partial
+    STRY(cols_spmv(E, 0));
+    STRY(launch_cols(E, COLS_COMMIT_ONLY));
+    STRY(launch_rows(E, ROWS_COMMIT_ONLY));
+    if (!r2) {
+      STRY(launch_rows(E, ROWS_AVG));
+      STRY(cols_spmv(E, 2));
+      STRY(launch_cols(E, COLS_AVG));
+    }
+    STRY(reduce_rowsum(E, 3));
+    for (auto &S : E.sh) MPAX_LAUNCH(k_check_decide, 1, 1, 0, s, S.st, o.eps_abs, o.eps_rel, LIM);
+    for (auto &S : E.sh)
+      MPAX_LAUNCH(k_restart, blocks_for(E.n > S.P.m ? E.n : S.P.m), kB, 0, s, S.st, E.n, S.P.m, S.V);
+    MPAX_CHECK_LAUNCH();
+    MPAX_CUDA(cudaMemcpyAsync(E.h_st, E.sh[0].st, sizeof(ShState), cudaMemcpyDeviceToHost, s));
+    MPAX_CUDA(cudaStreamSynchronize(s));
+    if (E.h_st->halt) break;
+  }
+  // ---- step 6: output ----
+  STRY(launch_cols(E, COLS_OUT));
+  STRY(launch_rows(E, ROWS_OUT));
+  STRY(reduce_rowsum(E, 3));
+  MPAX_LAUNCH(k_final, 1, 1, 0, s, E.sh[0].st, E.d_res);
+  MPAX_CHECK_LAUNCH();
+  for (auto &S : E.sh) {
+    MPAX_CUDA(cudaMemcpyAsync(S.X, S.V.red, E.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    MPAX_CUDA(cudaMemcpyAsync(S.L, S.V.KTyp, E.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (S.P.m) MPAX_CUDA(cudaMemcpyAsync(S.Y, S.V.Kxp, S.P.m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  MPAX_CUDA(cudaEventRecord(E.ev1, s));
+  MPAX_CUDA(cudaMemcpyAsync(E.h_res, E.d_res, sizeof(lp_result), cudaMemcpyDeviceToHost, s));
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  float ms = 0.0f;
+  MPAX_CUDA(cudaEventElapsedTime(&ms, E.ev0, E.ev1));
+  *out = *E.h_res;
+  out->solve_seconds = ms * 1e-3;
+  E.solved = true;
+  return LP_OK;
+}
+
+ShardedLP *sharded_new(cudaStream_t s) {
+  ShardedLP *E = new ShardedLP();
+  E->s = s;
+  if (cudaMallocHost((void **)&E->h_st, sizeof(ShState)) != cudaSuccess ||
+      cudaMallocHost((void **)&E->h_res, sizeof(lp_result)) != cudaSuccess ||
+      cudaMallocHost((void **)&E->h_flags, 8 * 64 * sizeof(int)) != cudaSuccess ||
+      cudaMallocAsync((void **)&E->d_res, sizeof(lp_result), s) != cudaSuccess ||
+      cudaEventCreate(&E->ev0) != cudaSuccess || cudaEventCreate(&E->ev1) != cudaSuccess) {
+    return E;  // caller checks h_st
+  }
+  return E;
+}
+
+void sharded_free(ShardedLP *E) {
+  if (!E) return;
+  for (auto &S : E->sh) {
+    if (S.arena) cudaFreeAsync(S.arena, E->s);
+    if (S.vecs) cudaFreeAsync(S.vecs, E->s);
+  }
+  if (E->d_ptrs) cudaFreeAsync(E->d_ptrs, E->s);
+  if (E->d_res) cudaFreeAsync(E->d_res, E->s);
+  cudaStreamSynchronize(E->s);
+  if (E->h_st) cudaFreeHost(E->h_st);
+  if (E->h_res) cudaFreeHost(E->h_res);
+  if (E->h_flags) cudaFreeHost(E->h_flags);
+  if (E->ev0) cudaEventDestroy(E->ev0);
+  if (E->ev1) cudaEventDestroy(E->ev1);
+  delete E;
+}
+
+int sharded_get(ShardedLP *E, double *x, double *y, double *rc) {
+  if (!E->solved) return LP_ERR_NOT_SOLVED;
+  cudaStream_t s = E->s;
+  if (x) MPAX_CUDA(cudaMemcpyAsync(x, E->sh[0].X, E->n * sizeof(double), cudaMemcpyDefault, s));
+  if (rc) MPAX_CUDA(cudaMemcpyAsync(rc, E->sh[0].L, E->n * sizeof(double), cudaMemcpyDefault, s));
+  if (y) {
+    int64_t off = 0;
+    for (auto &S : E->sh) {
+      if (S.P.m) MPAX_CUDA(cudaMemcpyAsync(y + off, S.Y, S.P.m * sizeof(double), cudaMemcpyDefault, s));
+      off += S.P.m;
+    }
+  }
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  return LP_OK;
+}
+
+int64_t sharded_n(const ShardedLP *E) { return E->n; }
+int64_t sharded_m_local(const ShardedLP *E) {
+  int64_t m = 0;
+  for (auto &S : E->sh) m += S.P.m;
+  return m;
+}
+
+// Create: `descs` are this process's row shards (one per GPU rank, p for virtual mode).
+int sharded_create(ShardedLP *E, const std::vector<lp_problem_desc> &descs, const std::vector<int64_t> &offsets,
+                   int64_t n, int64_t m1g, int64_t m2g, void *comm, int rank, int nranks, bool virt) {
+  E->n = n; E->m1_global = m1g; E->m_global = m1g + m2g;
+  E->comm = comm; E->rank = rank; E->nranks = nranks; E->virt = virt;
+  if (!E->h_st || !E->d_res) return LP_ERR_OUT_OF_MEMORY;
+  return sharded_setup(*E, descs, offsets);
+}
+
+}  // namespace mpax

@@ -4,7 +4,6 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
-from typing import Optional, Sequence
 
 import numpy as np
 
@@ -22,6 +21,8 @@ EXPORTED_SYMBOLS = [
     "lp_default_options", "lp_create", "lp_create_batch", "lp_update_batch", "lp_solve", "lp_solve_batch",
     "lp_get_solution", "lp_get_solutions", "lp_get_shape", "lp_get_scaling", "lp_spmv_scaled",
     "lp_kernel_launch_count", "lp_error_string", "lp_last_error_detail", "lp_destroy",
+    "lp_create_sharded", "lp_create_sharded_virtual", "lp_nccl_unique_id", "lp_nccl_comm_init",
+    "lp_nccl_comm_destroy",
 ]
 
 
@@ -91,6 +92,12 @@ def lib():
             L.lp_get_scaling.argtypes = [V, V, V, C.c_int32]
             L.lp_spmv_scaled.argtypes = [V, V, V, V, V, C.c_int32]
             L.lp_kernel_launch_count.restype = C.c_int64
+            L.lp_create_sharded.argtypes = [P(ProblemDesc), C.c_int64, C.c_int64, C.c_int64, V, C.c_int, C.c_int,
+                                            V, P(V)]
+            L.lp_create_sharded_virtual.argtypes = [P(ProblemDesc), C.c_int32, V, P(V)]
+            L.lp_nccl_unique_id.argtypes = [V]
+            L.lp_nccl_comm_init.argtypes = [P(V), C.c_int, V, C.c_int]
+            L.lp_nccl_comm_destroy.argtypes = [V]
             L.lp_error_string.argtypes = [C.c_int]
             L.lp_error_string.restype = C.c_char_p
             L.lp_last_error_detail.restype = C.c_char_p
@@ -377,3 +384,70 @@ class BatchSolver:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------------------- sharded ------
+
+def row_partition(row_ptr, parts: int):
+    """Contiguous row blocks balanced by nnz (a cut on the row_ptr prefix,
+    SURVEY §8(e)); returns parts+1 cut points.  Same rule as the library's
+    virtual shards."""
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    m = rp.size - 1
+    cuts = [0]
+    for g in range(1, parts):
+        t = int(rp[-1]) * g // parts
+        c = int(np.searchsorted(rp, t, side="left"))
+        cuts.append(min(max(c, cuts[-1]), m))
+    cuts.append(m)
+    return cuts
+
+
+def local_rows(problem: Problem, r0: int, r1: int) -> Problem:
+    """Rows [r0, r1) of K = [G; A] as a local problem for lp_create_sharded:
+    local m1 = the ">=" rows among them; full c, l, u."""
+    rp = np.asarray(problem.row_ptr, dtype=np.int64)
+    lrp = rp[r0:r1 + 1] - rp[r0]
+    m1 = max(0, min(problem.m1 - r0, r1 - r0))
+    sl = slice(int(rp[r0]), int(rp[r1]))
+    return Problem(problem.n, m1, (r1 - r0) - m1, lrp, np.asarray(problem.col_idx)[sl],
+                   np.asarray(problem.values)[sl], problem.c, np.asarray(problem.q)[r0:r1], problem.l, problem.u)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().lp_nccl_unique_id(buf), "lp_nccl_unique_id")
+    return buf.raw
+
+
+def nccl_comm_init(nranks: int, uid: bytes, rank: int) -> int:
+    comm = C.c_void_p()
+    buf = C.create_string_buffer(bytes(uid), 128)
+    _check(lib().lp_nccl_comm_init(C.byref(comm), nranks, buf, rank), "lp_nccl_comm_init")
+    return comm.value
+
+
+def nccl_comm_destroy(comm: int):
+    lib().lp_nccl_comm_destroy(comm)
+
+
+class ShardedSolver(Solver):
+    """One LP row-sharded across GPUs (lp_create_sharded), or across `virtual_shards`
+    row blocks on one GPU (lp_create_sharded_virtual)."""
+
+    def __init__(self, problem: Problem, global_row_offset=0, m1_global=None, m2_global=None, comm=None,
+                 rank=0, nranks=1, virtual_shards=None, stream=None):
+        self.problem = problem
+        d, keep = problem._desc()
+        self._device = problem.c.device if _is_torch(problem.c) else None
+        h = C.c_void_p()
+        if virtual_shards is not None:
+            _check(lib().lp_create_sharded_virtual(C.byref(d), int(virtual_shards), _stream_handle(stream),
+                                                   C.byref(h)), "lp_create_sharded_virtual")
+        else:
+            m1g = problem.m1 if m1_global is None else m1_global
+            m2g = problem.m2 if m2_global is None else m2_global
+            _check(lib().lp_create_sharded(C.byref(d), int(global_row_offset), int(m1g), int(m2g), comm, int(rank),
+                                           int(nranks), _stream_handle(stream), C.byref(h)), "lp_create_sharded")
+        self._h = h
+        del keep

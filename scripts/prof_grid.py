@@ -18,3 +18,9 @@ with mp.Solver(mp.Problem.from_lp(lp)) as s:
         r = s.solve(algorithm=alg, path=mp.PATH_GRID, iteration_limit=K, eps_abs=0.0, eps_rel=0.0)
         print(rep, r["status"], r["iterations"], r["attempts"], r["solve_seconds"] * 1e3, "ms",
               r["solve_seconds"] * 1e6 / r["attempts"], "us/attempt", flush=True)
+if os.environ.get("PROF_SHARDED"):
+    with mp.ShardedSolver(mp.Problem.from_lp(lp), virtual_shards=1) as s:
+        for rep in range(2):
+            r = s.solve(algorithm=alg, iteration_limit=K, eps_abs=0.0, eps_rel=0.0)
+            print("sharded-1", rep, r["status"], r["iterations"], r["attempts"], r["solve_seconds"] * 1e3, "ms",
+                  r["solve_seconds"] * 1e6 / r["attempts"], "us/attempt", flush=True)

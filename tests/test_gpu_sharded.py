@@ -1,0 +1,94 @@
+"""GPU parity of the row-sharded engine against the CPU oracle.
+One GPU: `virtual` shards (p row blocks on one device, fixed-order device sum in
+place of NCCL) exercise the partitioned arithmetic; a real 1-rank NCCL
+communicator exercises the NCCL plumbing."""
+import numpy as np
+import pytest
+
+import lpgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_2412_09734_b200 as mp  # noqa: E402
+from tests.test_gpu_parity import obj_tol, oracle_stability, rel  # noqa: E402
+
+ALGS = ["ra", "r2"]
+CASES = [("C1", lpgen.g_rand(50, 100, 10, seed=1)), ("mid", lpgen.g_rand(3000, 5000, 12, seed=3)),
+         ("tiny", lpgen.tiny_spec())]
+
+
+def sharded(lp, alg, shards, **kw):
+    with mp.ShardedSolver(mp.Problem.from_lp(lp), virtual_shards=shards) as s:
+        r = s.solve(algorithm=alg, **kw)
+        x, y, lam = s.solution()
+    r.update(x=x, y=y, lam=lam)
+    return r
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("K", [1, 2, 64])
+@pytest.mark.parametrize("shards", [1, 2, 3])
+@pytest.mark.parametrize("name,lp", CASES)
+def test_sharded_fixed_K(alg, K, shards, name, lp):
+    if shards > lp.m:
+        pytest.skip("more shards than rows")
+    ro, stable, drift = oracle_stability(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=K)
+    rg = sharded(lp, alg, shards, eps_abs=0.0, eps_rel=0.0, iteration_limit=K)
+    if not stable:
+        pytest.skip("ill-conditioned at this K: the oracle's own counts move under a 1-ulp perturbation")
+    tol = max(1e-9, 100 * drift)
+    for key in ("status", "iterations", "attempts", "restarts"):
+        assert rg[key] == ro[key], (key, rg[key], ro[key])
+    assert rel(rg["x"], ro["x"]) <= tol
+    if lp.m:
+        assert rel(rg["y"], ro["y"]) <= tol
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("shards", [1, 4])
+@pytest.mark.parametrize("name,lp", CASES[:2])
+def test_sharded_full_solve(alg, shards, name, lp):
+    ro, stable, drift = oracle_stability(lp, alg)
+    rg = sharded(lp, alg, shards)
+    assert rg["status"] == mp.LP_OPTIMAL and rg["rel_kkt"] <= 1e-4
+    if stable:
+        assert rg["iterations"] == ro["iterations"] and rg["restarts"] == ro["restarts"]
+        assert abs(rg["primal_objective"] - ro["primal_objective"]) <= obj_tol(ro) * (1 + abs(ro["primal_objective"]))
+    k = oracle.kkt_original(lp, rg["x"], rg["y"])
+    assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.q))
+    assert k["dres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.c))
+    assert abs(rg["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
+
+
+def test_nccl_one_rank_equals_virtual_one_shard():
+    lp = lpgen.g_rand(3000, 5000, 12, seed=3)
+    uid = mp.nccl_unique_id()
+    comm = mp.nccl_comm_init(1, uid, 0)
+    try:
+        with mp.ShardedSolver(mp.Problem.from_lp(lp), 0, lp.m1, lp.m2, comm=comm, rank=0, nranks=1) as s:
+            a = s.solve(algorithm="r2", iteration_limit=200, eps_abs=0.0, eps_rel=0.0)
+            xa, ya, _ = s.solution()
+    finally:
+        mp.nccl_comm_destroy(comm)
+    b = sharded(lp, "r2", 1, iteration_limit=200, eps_abs=0.0, eps_rel=0.0)
+    assert a["attempts"] == b["attempts"] and np.array_equal(xa, b["x"]) and np.array_equal(ya, b["y"])
+
+
+def test_sharded_local_rows_api_matches_virtual():
+    """A 'rank' built from python-side local_rows(row_partition(...)) solves its
+    block exactly like the library's own virtual split (same cut rule)."""
+    lp = lpgen.g_rand(400, 700, 8, seed=6)
+    prob = mp.Problem.from_lp(lp)
+    cuts = mp.row_partition(lp.row_ptr, 3)
+    assert cuts[0] == 0 and cuts[-1] == lp.m and all(a <= b for a, b in zip(cuts, cuts[1:]))
+    loc = mp.local_rows(prob, cuts[1], cuts[2])
+    assert loc.m1 == max(0, min(lp.m1 - cuts[1], cuts[2] - cuts[1]))
+    K = lp.dense_K()
+    Kl = lpgen.LP(loc.n, loc.m1, loc.m2, np.asarray(loc.row_ptr), np.asarray(loc.col_idx),
+                  np.asarray(loc.values), lp.c, np.asarray(loc.q), lp.l, lp.u).dense_K()
+    assert np.array_equal(Kl, K[cuts[1]:cuts[2]])
