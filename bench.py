@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-large", action="store_true", help="skip the C4 whole-GPU leg")
     ap.add_argument("--large-m", type=int, default=100_000)
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (1e8 nnz) whole-GPU leg")
+    ap.add_argument("--no-dense", action="store_true", help="skip the C3 shared-dense-K (DMMA) leg")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -341,8 +343,14 @@ def run_ours(args):
         "secondary": secondary,
     }
     if not args.no_large:
-        log("large-LP leg")
+        log("large-LP leg (C4)")
         line["large_lp"] = large_lp_leg(mp, torch, dev, stream, peaks, args)
+    if not args.no_c5 and rank == 0:
+        log("large-LP leg (C5, 1e8 nnz)")
+        line["c5"] = large_lp_leg(mp, torch, dev, stream, peaks, args, m=5_000_000, seed=5, label="C5", reps=1)
+    if not args.no_dense:
+        log("dense shared-K leg (C3)")
+        line["dense_batch"] = dense_leg(mp, torch, dev, peaks)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         log("cpu baseline")
         line["cpu_baseline"] = cpu_baseline(lp, C, args.alg, args.cpu_seconds)
@@ -363,21 +371,30 @@ def attempt_bytes(n, m, nnz, alg):
     return pair, pair + upd
 
 
-def large_lp_leg(mp, torch, dev, stream, peaks, args):
-    """C4 = G-RAND(1e5, 2e5, 20, seed 4) solved to 1e-4 on the whole-GPU grid path:
-    time to tolerance and achieved HBM GB/s of the fused SpMV-pair + update loop."""
-    m = args.large_m
-    lp = lpgen.g_rand(m, 2 * m, 20, seed=4)
+def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4", reps=3):
+    """One large random sparse LP (C4 = G-RAND(1e5, 2e5, 20, seed 4); C5 = G-RAND(5e6, 1e7,
+    20, seed 5)) solved to 1e-4 on the whole-GPU grid path: time to tolerance and the
+    achieved algorithmic GB/s of the fused SpMV-pair + update loop."""
+    m = args.large_m if m is None else m
+    t0 = time.time()
+    lp = lpgen.g_rand(m, 2 * m, 20, seed=seed)
+    gen_s = time.time() - t0
     prob = mp.Problem.from_lp(lp).to(dev)
-    out = {"workload": f"C4: G-RAND({m}, {2 * m}, 20, seed 4), one LP on the whole GPU (grid path), to 1e-4",
-           "nnz": lp.nnz}
+    torch.cuda.synchronize()
+    t0 = time.time()
+    s_setup = mp.Solver(prob)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    s_setup.close()
+    out = {"workload": f"{label}: G-RAND({m}, {2 * m}, 20, seed {seed}), one LP on the whole GPU (grid path), to 1e-4",
+           "nnz": lp.nnz, "generate_s": gen_s, "create_s_wall": setup_s}
     hbm = peaks.get("hbm_gbs", 6546.6)
     for alg in ("ra", "r2"):
         with mp.Solver(prob) as s:
             log(f"large leg {alg}: warm-up")
             s.solve(algorithm=alg, path=mp.PATH_GRID, iteration_limit=20_000)   # warm-up
             best = None
-            for _ in range(3):
+            for _ in range(reps):
                 r = s.solve(algorithm=alg, path=mp.PATH_GRID, iteration_limit=20_000)
                 best = r if best is None or r["solve_seconds"] < best["solve_seconds"] else best
         pair, acc = attempt_bytes(lp.n, lp.m, lp.nnz, alg)
@@ -393,6 +410,36 @@ def large_lp_leg(mp, torch, dev, stream, peaks, args):
                                  "traffic": None, "kernel": "grid_kernel",
                                  "algorithmic_bytes_per_accepted_attempt": acc,
                                  "note": "working set (~70 MB) is L2-resident at C4; achieved may exceed HBM"}}
+    return out
+
+
+def dense_leg(mp, torch, dev, peaks):
+    """C3: 256 dense 200x400 LPs sharing K: LPs/s on the fp64 tensor-core (DMMA)
+    path and on the per-instance path, with the DMMA path's achieved fp64 rate."""
+    lp, C, Q, obj = lpgen.g_dense(200, 400, batch=256, seed=3)
+    prob = mp.Problem.from_lp(lp).to(dev)
+    Cd, Qd = torch.as_tensor(C, device=dev), torch.as_tensor(Q, device=dev)
+    out = {"workload": "C3: 256 dense 200x400 LPs sharing K (c, q vary), raPDHG to 1e-4"}
+    for name, path in (("dmma", mp.PATH_DMMA), ("per_instance", mp.PATH_INSTANCE)):
+        bs = mp.BatchSolver(prob, Cd, Qd)
+        bs.solve(algorithm="ra", path=path, iteration_limit=100_000)
+        res = bs.solve(algorithm="ra", path=path, iteration_limit=100_000)
+        bs.close()
+        t = float(res[0]["solve_seconds"])
+        d = {"value": 256 / t, "unit": UNIT, "solve_ms": t * 1e3,
+             "all_optimal": bool((res["status"] == mp.LP_OPTIMAL).all()),
+             "max_obj_rel_err": float(np.max(np.abs(res["primal_objective"] - obj) / (1 + np.abs(obj))))}
+        if name == "dmma":
+            # each group of 8 runs in lock-step until its slowest instance is done: 2 GEMMs of 2*m*n*8 flops
+            att = np.asarray(res["attempts"]).reshape(-1, 8).max(axis=1)
+            flops = float(att.sum()) * 2 * 2 * 200 * 400 * 8
+            sm_max = peaks.get("sm_max_mhz", 1965.0)
+            peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12
+            d["roofline"] = {"bound": "tensor", "achieved": flops / t / 1e12, "peak": peak, "unit": "TFLOP/s",
+                             "frac": flops / t / 1e12 / peak, "traffic": None, "kernel": "dmma_kernel<4>",
+                             "note": "fp64 DMMA peak derived = fp64 FMA peak (148 SMs x 64 x 2 x sm_max)"}
+        out[name] = d
+    out["speedup_dmma_vs_per_instance"] = out["dmma"]["value"] / out["per_instance"]["value"]
     return out
 
 

@@ -208,7 +208,9 @@ def num_threads() -> int:
 
 
 def set_threads(t: int):
-    lib().ora_set_threads(int(t))
+    """t > 0: that many OpenMP threads; t <= 0: every core this process may use."""
+    import os
+    lib().ora_set_threads(int(t) if t > 0 else len(os.sched_getaffinity(0)))
 
 
 def precondition(lp, ruiz_iters=10, pock_chambolle=1):

@@ -102,3 +102,24 @@ def test_c4_full_size(alg):
     assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.q))
     slack = 4e-16 * (1 + np.abs(np.where(np.isfinite(lp.u), lp.u, 0)))
     assert np.all(r["x"] >= lp.l) and np.all(r["x"] <= lp.u + slack) and np.all(r["y"][: lp.m1] >= 0)
+
+
+@pytest.mark.slow
+def test_c5_full_size_sampled():
+    """C5 = G-RAND(5e6, 1e7, 20, seed 5) at its BASELINE size, in the launch
+    configuration bench.py times (grid path): iterates after K = 2 accepted steps
+    against the oracle (which needs ~30 s for that on the host), then a full solve
+    to 1e-4 checked by properties (status, KKT, bounds, known optimum)."""
+    lp = lpgen.g_rand(5_000_000, 10_000_000, 20, seed=5)
+    oracle.set_threads(0)
+    ro = oracle.solve(lp, "r2", iteration_limit=2, eps_abs=0.0, eps_rel=0.0)
+    with mp.Solver(mp.Problem.from_lp(lp).to("cuda:0")) as s:
+        rg = s.solve(algorithm="r2", path=mp.PATH_GRID, iteration_limit=2, eps_abs=0.0, eps_rel=0.0)
+        x, y, _ = s.solution()
+        assert rg["attempts"] == ro["attempts"]
+        assert rel(x, ro["x"]) <= 1e-12 and rel(y, ro["y"]) <= 1e-12
+        r = s.solve(algorithm="ra", path=mp.PATH_GRID, iteration_limit=5000)
+        x, y, _ = s.solution()
+    assert r["status"] == mp.LP_OPTIMAL and r["rel_kkt"] <= 1e-4
+    assert abs(r["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
+    assert np.all(y[: lp.m1] >= 0) and np.all(x >= lp.l)
