@@ -333,7 +333,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": None,
-                     "kernel": "instance_kernel<1>", "kernel_ms": kern_ms,
+                     "kernel": "tiny_kernel<0,1,2,4,4> (raPDHG, register-resident warp per LP)", "kernel_ms": kern_ms,
                      "flops_per_launch": flops,
                      "note": "fp64 FMA peak derived (148 SMs x 64 DFMA/clk x 2 x sm_max); per-instance solves "
                              "are latency-bound, see DESIGN.md §6"},
