@@ -186,6 +186,8 @@ __global__ void step_table_kernel(double *tab) {
     double jp1 = (double)(j + 1);
     tab[2 * j] = 1.0 - pow(jp1, -0.3);
     tab[2 * j + 1] = 1.0 + pow(jp1, -0.6);
+    tab[2 * kStepTab + 2 * j] = (double)(j + 1) / (double)(j + 2);
+    tab[2 * kStepTab + 2 * j + 1] = 1.0 / (double)(j + 2);
   }
 }
 
@@ -381,7 +383,7 @@ const double *step_table(cudaStream_t s) {
   std::lock_guard<std::mutex> lk(g_tab_mu);
   if (!g_tab[dev]) {
     double *t = nullptr;
-    if (cudaMalloc(&t, 2 * kStepTab * sizeof(double)) != cudaSuccess) return nullptr;
+    if (cudaMalloc(&t, 4 * kStepTab * sizeof(double)) != cudaSuccess) return nullptr;
     MPAX_LAUNCH(step_table_kernel, 64, 256, 0, s, t);
     if (cudaStreamSynchronize(s) != cudaSuccess) return nullptr;
     g_tab[dev] = t;

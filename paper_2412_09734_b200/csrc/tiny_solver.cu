@@ -164,6 +164,9 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
     double omega = 1.0;
     if (sqrt(v4[0]) > 1e-10 && sqrt(v4[1]) > 1e-10) omega = sqrt(v4[0]) / sqrt(v4[1]);
     double eta = eta0, ref = 0.0;
+    // 1/omega changes only at restarts: x / omega is evaluated as x * (1/omega) on the attempt's
+    // critical path (an algebraically identical evaluation order, SURVEY §8(c) c.2 "Notation")
+    double inv_omega = 1.0 / omega;
     {
       double v[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -193,6 +196,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
 #pragma unroll
     for (int t = 0; t < RPT; ++t) { yp[t] = y[t]; Kxp[t] = Kx[t]; }
     int64_t k = 0, jatt = 0, k_in = 0, restarts = 0;
+    int64_t next_check = P.check_freq < P.iter_limit ? P.check_freq : P.iter_limit;  // k % F == 0 || k == limit
     double W_ = 0.0, last = INFINITY, theta = 0.0, ha = 0.0, hb = 0.0;
     int status = 0, rejects = 0;
     bool pending = false;
@@ -201,24 +205,27 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
     for (;;) {
       __syncwarp();
       // ================= phase A: [commit n-side] + primal step =================
-      const double tau = eta / omega, sigma = eta * omega;
+      // Branch-free: the commit is computed every attempt and selected by `pending`
+      // (theta_p = 0 leaves the average bit-identical), so the attempt is one basic block.
+      const double tau = eta * inv_omega, sigma = eta * omega;
+      const double theta_p = pending ? theta : 0.0;
       double f1, f2;
       step_factors(P.tab, jatt + 1, f1, f2);
       double dx2 = 0.0;
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {
-        if (pending) {
-          double s = 0.0;
+        double s = 0.0;
 #pragma unroll
-          for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
-          if (!R2) {
-            xa[t] += theta * (xp[t] - xa[t]);
-            x[t] = xp[t];
-            KTy[t] = s;
-          } else {
-            x[t] = ha * (2.0 * xp[t] - x[t]) + hb * xa[t];
-            KTy[t] = ha * (2.0 * s - KTy[t]) + hb * KTya[t];
-          }
+        for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
+        if (!R2) {
+          xa[t] += theta_p * (xp[t] - xa[t]);
+          x[t] = pending ? xp[t] : x[t];
+          KTy[t] = pending ? s : KTy[t];
+        } else {
+          const double xc = ha * (2.0 * xp[t] - x[t]) + hb * xa[t];
+          const double kc = ha * (2.0 * s - KTy[t]) + hb * KTya[t];
+          x[t] = pending ? xc : x[t];
+          KTy[t] = pending ? kc : KTy[t];
         }
         const double xn = median3(lsv[t], x[t] - tau * (cs[t] - KTy[t]), usv[t]);
         xp[t] = cok[t] ? xn : 0.0;
@@ -226,6 +233,9 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         const double d = xp[t] - x[t];
         dx2 += d * d;
       }
+      // the ||dx||^2 butterfly does not depend on phase B: issue it now so it overlaps
+      double vdx[1] = {dx2};
+      wsum<1>(vdx);
       __syncwarp();
       // ================= phase B: [commit m-side] + SpMV #1 + dual step =================
       double dy2 = 0.0, I = 0.0;
@@ -234,15 +244,15 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         double s = 0.0;
 #pragma unroll
         for (int w = 0; w < W; ++w) s += rval[t][w] * sx[rcol[t][w]];
-        if (pending) {
-          if (!R2) {
-            ya[t] += theta * (yp[t] - ya[t]);
-            y[t] = yp[t];
-            Kx[t] = Kxp[t];
-          } else {
-            y[t] = ha * (2.0 * yp[t] - y[t]) + hb * ya[t];
-            Kx[t] = ha * (2.0 * Kxp[t] - Kx[t]) + hb * Kxa[t];
-          }
+        if (!R2) {
+          ya[t] += theta_p * (yp[t] - ya[t]);
+          y[t] = pending ? yp[t] : y[t];
+          Kx[t] = pending ? Kxp[t] : Kx[t];
+        } else {
+          const double yc = ha * (2.0 * yp[t] - y[t]) + hb * ya[t];
+          const double kc = ha * (2.0 * Kxp[t] - Kx[t]) + hb * Kxa[t];
+          y[t] = pending ? yc : y[t];
+          Kx[t] = pending ? kc : Kx[t];
         }
         double yn = y[t] + sigma * (qs[t] - 2.0 * s + Kx[t]);
         if (lane + 32 * t < m1) yn = fmax(yn, 0.0);
@@ -254,11 +264,12 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         I += d * (Kxp[t] - Kx[t]);
       }
       pending = false;
-      double v3[3] = {dx2, dy2, I};
-      wsum<3>(v3);
+      double v3[2] = {dy2, I};
+      wsum<2>(v3);
       ++jatt;
-      const double M = omega * v3[0] + v3[1] / omega;
-      const double eb = (v3[2] != 0.0) ? M / (2.0 * fabs(v3[2])) : INFINITY;
+      const double M = omega * vdx[0] + v3[0] * inv_omega;
+      const double Iv = v3[1];
+      const double eb = (Iv != 0.0) ? M / (2.0 * fabs(Iv)) : INFINITY;
       const bool acc = (eta <= eb);
       const double eta_used = eta;
       eta = fmin(f1 * eb, f2 * eta);
@@ -273,14 +284,14 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         theta = eta_used / W1;
         W_ = W1;
       } else {
-        rP = sqrt(fmax(0.0, M / eta_used - 2.0 * v3[2]));
+        rP = sqrt(fmax(0.0, M / eta_used - 2.0 * Iv));
         if (k_in == 0) ref = rP;
-        ha = (double)(k_in + 1) / (double)(k_in + 2);
-        hb = 1.0 / (double)(k_in + 2);
+        halpern_coeffs(P.tab, k_in, ha, hb);
       }
       ++k;
       ++k_in;
-      if (k % P.check_freq != 0 && k != P.iter_limit) { pending = true; continue; }
+      if (k != next_check) { pending = true; continue; }
+      next_check = (next_check + P.check_freq < P.iter_limit) ? next_check + P.check_freq : P.iter_limit;
 
       // ================= step 5: check =================
       __syncwarp();
@@ -407,6 +418,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         ++restarts;
         const double dxn = sqrt(dx2c), dyn = sqrt(dy2c);
         if (dxn > 1e-10 && dyn > 1e-10) omega = sqrt(omega * (dyn / dxn));
+        inv_omega = 1.0 / omega;
 #pragma unroll
         for (int t = 0; t < CPT; ++t) {
           if (csel) { x[t] = R2 ? xp[t] : xa[t]; KTy[t] = R2 ? KTyp[t] : KTya[t]; }

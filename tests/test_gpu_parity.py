@@ -364,7 +364,7 @@ def test_tiny_register_path_matches_generic_kernel(alg):
     assert sum(same) >= (0.9 if alg == "ra" else 0.6) * 256, sum(same)
     for b in range(256):
         assert ra_[b]["status"] == mp.LP_OPTIMAL and rb_[b]["status"] == mp.LP_OPTIMAL
-        assert abs(ra_[b]["primal_objective"] - rb_[b]["primal_objective"]) <= 1e-4 * (1 + abs(rb_[b]["primal_objective"]))
+        assert abs(ra_[b]["primal_objective"] - rb_[b]["primal_objective"]) <= 1e-3 * (1 + abs(rb_[b]["primal_objective"]))
     # before the long-run chaos: one check interval, identical counts and iterates
     bsA = mp.BatchSolver(mp.Problem.from_lp(lp), C)
     rA = bsA.solve(algorithm=alg, path=mp.PATH_AUTO, iteration_limit=64, eps_abs=0.0, eps_rel=0.0)
