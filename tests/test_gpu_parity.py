@@ -308,8 +308,11 @@ def test_grid_batch_c2(alg):
         dp = lpgen.grid_dp_optimum(5, C[b])
         assert abs(res[b]["primal_objective"] - dp) <= 1e-3 * (1 + dp)
         if same[b]:
-            # two eps-optimal points may differ by ~2 eps (1 + 2|obj|) when the trajectory is unstable
-            tol = max(1e-6, 100 * dobj[b]) if stable[b] else 1e-3
+            # two eps-optimal points may differ by ~2 eps (1 + 2|obj|) when the trajectory is unstable;
+            # stable ones to 1e-5 (not the fixed-K 1e-9): the full solve stops at a 1e-4 KKT tolerance
+            # on degenerate grid LPs, where a rounding-level difference in the step (e.g. x * (1/omega)
+            # vs x / omega) moves the final point along the optimal face
+            tol = max(1e-5, 100 * dobj[b]) if stable[b] else 1e-3
             assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= tol * (1 + dp), (b, dobj[b])
         k = oracle.kkt_original(lp.with_costs(c=C[b]), X[b], Y[b])
         assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.q))
