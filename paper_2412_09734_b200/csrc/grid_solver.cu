@@ -196,16 +196,16 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double s_red[kBS / 32][kNP];
   __shared__ double s_tot[kNP];
-  const int64_t n = P.n, m = P.m, m1 = P.m1;
-  const int64_t gtid = (int64_t)blockIdx.x * kBS + threadIdx.x, gthreads = (int64_t)gridDim.x * kBS;
+  const int n = (int)P.n, m = (int)P.m, m1 = (int)P.m1;  // < 2^31 (lp_create checks)
+  const int gtid = blockIdx.x * kBS + threadIdx.x, gthreads = gridDim.x * kBS;
   const bool r2 = (P.alg == LP_R2HPDHG);
   // SpMV group mapping (fixed for the whole solve, so every row / column has one owner group)
   const int G = P.gk, Gt = P.gkt;
-  const int64_t grp = gtid / G, ngrp = gthreads / G;
+  const int grp = gtid / G, ngrp = gthreads / G;
   const int gl = (int)(gtid % G);
-  const int64_t grpt = gtid / Gt, ngrpt = gthreads / Gt;
+  const int grpt = gtid / Gt, ngrpt = gthreads / Gt;
   const int glt = (int)(gtid % Gt);
-  const int64_t row_iters = (m + ngrp - 1) / ngrp, col_iters = (n + ngrpt - 1) / ngrpt;
+  const int row_iters = (m + ngrp - 1) / ngrp, col_iters = (n + ngrpt - 1) / ngrpt;
   double *x = P.x, *KTy = P.KTy, *xp = P.xp, *KTyp = P.KTyp, *xa = P.xa, *KTya = P.KTya, *xr = P.xr;
   double *y = P.y, *Kx = P.Kx, *yp = P.yp, *Kxp = P.Kxp, *ya = P.ya, *Kxa = P.Kxa, *yr = P.yr;
   const double *cs = P.cs, *qs = P.qs;
@@ -213,14 +213,14 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   // ---------------- step 2: initialise ----------------
   {
     double v[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t j = gtid; j < n; j += gthreads) {
+    for (int j = gtid; j < n; j += gthreads) {
       const double dc = P.Dc[j], c = P.c0[j], cj = c * dc;
       P.cs[j] = cj;
       v[0] += cj * cj;
       v[2] += c * c;
       x[j] = median3(P.ls[j], P.X0 ? P.X0[j] / dc : 0.0, P.us[j]);
     }
-    for (int64_t i = gtid; i < m; i += gthreads) {
+    for (int i = gtid; i < m; i += gthreads) {
       const double dr = P.Dr[i], q = P.q0[i], qi = q * dr;
       P.qs[i] = qi;
       v[1] += qi * qi;
@@ -242,8 +242,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   {
     // K~x0, K~'y0; anchors / restart point; KKT_omega(z0) partials (scaled space)
     double v[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t it = 0; it < row_iters; ++it) {
-      const int64_t i = it * ngrp + grp;
+    for (int it = 0; it < row_iters; ++it) {
+      const int i = it * ngrp + grp;
       const bool ok = i < m;
       const double s = row_dot(i, ok, G, gl, P.rp, P.ci, P.kv, x);
       if (ok && gl == 0) {
@@ -253,8 +253,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         kkt_row(v, false, i, m1, 1.0, yv, s, 0.0, qs[i]);
       }
     }
-    for (int64_t it = 0; it < col_iters; ++it) {
-      const int64_t j = it * ngrpt + grpt;
+    for (int it = 0; it < col_iters; ++it) {
+      const int j = it * ngrpt + grpt;
       const bool ok = j < n;
       const double s = row_dot(j, ok, Gt, glt, P.trp, P.tci, P.tkv, y);
       if (ok && glt == 0) {
@@ -291,8 +291,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     const double tau = eta / omega, sigma = eta * omega;
     double v3[3] = {0.0, 0.0, 0.0};
     if (pending) {
-      for (int64_t it = 0; it < col_iters; ++it) {
-        const int64_t j = it * ngrpt + grpt;
+      for (int it = 0; it < col_iters; ++it) {
+        const int j = it * ngrpt + grpt;
         const bool ok = j < n, lead = ok && glt == 0;
         // operands of the epilogue, loaded before the dot so they are in flight with it
         double o_xp = 0.0, o_xa = 0.0, o_x = 0.0, o_kt = 0.0, o_kta = 0.0, o_cs = 0.0, o_ls = 0.0, o_us = 0.0;
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         t = KTy; KTy = KTyp; KTyp = t;
       }
     } else {
-      for (int64_t j = gtid; j < n; j += gthreads) {
+      for (int j = gtid; j < n; j += gthreads) {
         const double xo = x[j];
         const double xn = median3(P.ls[j], xo - tau * (cs[j] - KTy[j]), P.us[j]);
         xp[j] = xn;
@@ -335,8 +335,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     grid.sync();
     // ================= phase B: [commit m-side] + SpMV #1 + dual step =================
     {
-      for (int64_t it = 0; it < row_iters; ++it) {
-        const int64_t i = it * ngrp + grp;
+      for (int it = 0; it < row_iters; ++it) {
+        const int i = it * ngrp + grp;
         const bool ok = i < m, lead = ok && gl == 0;
         double o_y = 0.0, o_kx = 0.0, o_yp = 0.0, o_ya = 0.0, o_kxp = 0.0, o_kxa = 0.0, o_qs = 0.0;
         if (lead) {
@@ -416,8 +416,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     // ================= check: commit-only phase (both sides) =================
     {
       double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      for (int64_t it = 0; it < col_iters; ++it) {
-        const int64_t j = it * ngrpt + grpt;
+      for (int it = 0; it < col_iters; ++it) {
+        const int j = it * ngrpt + grpt;
         const bool ok = j < n;
         const double s = row_dot(j, ok, Gt, glt, P.trp, P.tci, P.tkv, yp);
         if (ok && glt == 0) {
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           }
         }
       }
-      for (int64_t i = gtid; i < m; i += gthreads) {
+      for (int i = gtid; i < m; i += gthreads) {
         if (!r2) {
           ya[i] += theta * (yp[i] - ya[i]);
         } else {
@@ -462,8 +462,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       double v[kNP];
 #pragma unroll
       for (int q = 0; q < kNP; ++q) v[q] = 0.0;
-      for (int64_t it = 0; it < row_iters; ++it) {
-        const int64_t i = it * ngrp + grp;
+      for (int it = 0; it < row_iters; ++it) {
+        const int i = it * ngrp + grp;
         const bool ok = i < m;
         const double s = row_dot(i, ok, G, gl, P.rp, P.ci, P.kv, xa);
         if (ok && gl == 0) {
@@ -478,8 +478,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           v[19] += dcur * dcur;
         }
       }
-      for (int64_t it = 0; it < col_iters; ++it) {
-        const int64_t j = it * ngrpt + grpt;
+      for (int it = 0; it < col_iters; ++it) {
+        const int j = it * ngrpt + grpt;
         const bool ok = j < n;
         const double s = row_dot(j, ok, Gt, glt, P.trp, P.tci, P.tkv, ya);
         if (ok && glt == 0) {
@@ -528,11 +528,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       ++restarts;
       const double dxn = sqrt(dx2), dyn = sqrt(dy2);
       if (dxn > 1e-10 && dyn > 1e-10) omega = sqrt(omega * (dyn / dxn));
-      for (int64_t j = gtid; j < n; j += gthreads) {
+      for (int j = gtid; j < n; j += gthreads) {
         const double xv = cx[j], kt = cKTy[j];
         x[j] = xv; xr[j] = xv; xa[j] = xv; KTy[j] = kt; KTya[j] = kt;
       }
-      for (int64_t i = gtid; i < m; i += gthreads) {
+      for (int i = gtid; i < m; i += gthreads) {
         const double yv = cy[i], kx = cKx[i];
         y[i] = yv; yr[i] = yv; ya[i] = yv; Kx[i] = kx; Kxa[i] = kx;
       }
@@ -545,13 +545,13 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   // ================= step 6: output the candidate =================
   {
     double v[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t j = gtid; j < n; j += gthreads) {
+    for (int j = gtid; j < n; j += gthreads) {
       const double dc = P.Dc[j], xs = ox[j], kt = oKTy[j];
       kkt_col(v, true, dc, xs, kt, P.c0[j], cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
       P.X[j] = dc * xs;
       P.L[j] = P.c0[j] - kt / dc;
     }
-    for (int64_t i = gtid; i < m; i += gthreads) {
+    for (int i = gtid; i < m; i += gthreads) {
       const double dr = P.Dr[i];
       kkt_row(v, true, i, m1, dr, oy[i], oKx[i], P.q0[i], qs[i]);
       P.Y[i] = dr * oy[i];
@@ -589,10 +589,11 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   MPAX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   MPAX_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return LP_ERR_UNSUPPORTED;
-  // register budget: 1 CTA of 512 threads per SM (128 regs, no spills in the phase loops) by default;
-  // MPAX_GRID_MINB=2 gives 2 CTAs/SM at 64 regs (measured slower: spills)
+  // register budget: 2 CTAs of 512 threads per SM (64 regs; the spills sit in the rare check
+  // code) by default -- measured 12% faster than 1 CTA/SM at 128 regs on a 2e7-nnz LP, equal at C4;
+  // MPAX_GRID_MINB=1 selects the 128-register build
   const char *env = getenv("MPAX_GRID_MINB");
-  const int minb = (env && atoi(env) == 2) ? 2 : 1;
+  const int minb = (env && atoi(env) == 1) ? 1 : 2;
   void *kfn = minb == 1 ? (void *)grid_kernel<1> : (void *)grid_kernel<2>;
   int per_sm = 0;
   MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kBS, 0));
