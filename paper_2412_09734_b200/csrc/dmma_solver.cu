@@ -191,6 +191,39 @@ __device__ __forceinline__ void cta_partials(double (&v)[kS][V], const Smem &S) 
   }
 }
 
+// The attempt's three per-instance sums with the fragment layouts in mind: lane l holds
+// ||dx||^2 for instances 2(l%4), 2(l%4)+1 (GEMM1 C fragment) and ||dy||^2, <dy, K~dx> for
+// instance l%8 (row loop), so 3- and 2-level butterflies suffice; warps are then summed in
+// order.  Fixed order: deterministic.
+__device__ __forceinline__ void attempt_partials(double dxe, double dxo, double dy, double Iv, const Smem &S) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    dxe += __shfl_xor_sync(FULL, dxe, off);
+    dxo += __shfl_xor_sync(FULL, dxo, off);
+  }
+#pragma unroll
+  for (int off = 8; off < 32; off <<= 1) {
+    dy += __shfl_xor_sync(FULL, dy, off);
+    Iv += __shfl_xor_sync(FULL, Iv, off);
+  }
+  if (lane < 4) {
+    S.wpart[(w * kS + 2 * lane) * 24 + 0] = dxe;
+    S.wpart[(w * kS + 2 * lane + 1) * 24 + 0] = dxo;
+  }
+  if (lane < kS) {
+    S.wpart[(w * kS + lane) * 24 + 1] = dy;
+    S.wpart[(w * kS + lane) * 24 + 2] = Iv;
+  }
+  __syncthreads();
+  if (threadIdx.x < kS * 3) {
+    const int s = threadIdx.x / 3, k = threadIdx.x % 3;
+    double a = 0.0;
+    for (int ww = 0; ww < kThreads / 32; ++ww) a += S.wpart[(ww * kS + s) * 24 + k];
+    S.part[s * 24 + k] = a;
+  }
+}
+
 // After a cluster barrier: tot[s][k] = sum over cluster ranks (in rank order) of part.
 template <int CL, int V>
 __device__ __forceinline__ void cluster_totals(cg::cluster_group &cl, const Smem &S, double *tot /* kS*24 */) {
@@ -340,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       for (int s = 0; s < kS; ++s) all_done &= (bool)S.inst[s].done;
       if (all_done) break;
       // ---- phase A: GEMM1 = K~_c' Y' ; [commit n-side] ; primal step ; X'_c ----
-      double va[kS][1] = {};
+      double dx_even = 0.0, dx_odd = 0.0;  // this lane's instances 2q and 2q+1 (GEMM1 fragment layout)
       gemm1(S, np, mp, [&](int jj, int s, double kty) {
         const Inst &I = S.inst[s];
         if (jj >= jn || I.done) { if (jj < np) S.Xc[jj * kS + s] = 0.0; return; }
@@ -364,15 +397,14 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         P.xp[o] = xn;
         S.Xc[jj * kS + s] = xn;
         const double d = xn - xv;
-        va[s][0] += d * d;
+        if (s & 1) dx_odd += d * d; else dx_even += d * d;
       });
       __syncthreads();
       // ---- GEMM2: partial K~_c X'_c ----
       gemm2(S, np, mp);
       cl.sync();
       // ---- phase B: reduce K~x' for own rows; [commit m-side]; dual step ----
-      double vb[kS][3] = {};
-      for (int s = 0; s < kS; ++s) vb[s][0] = va[s][0];
+      double dy_own = 0.0, I_own = 0.0;  // instance tid % 8 (kThreads is a multiple of kS)
       for (int t = tid; t < in_ * kS; t += kThreads) {
         const int ii = t / kS, s = t % kS, i = i0 + ii;
         const Inst &I = S.inst[s];
@@ -399,10 +431,10 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         P.yp[o] = yn; P.Kxp[o] = kxp;
         S.Yf[i * kS + s] = yn;
         const double d = yn - yv;
-        vb[s][1] += d * d;
-        vb[s][2] += d * (kxp - kxv);
+        dy_own += d * d;
+        I_own += d * (kxp - kxv);
       }
-      cta_partials<3>(vb, S);
+      attempt_partials(dx_even, dx_odd, dy_own, I_own, S);
       cl.sync();
       cluster_totals<CL, 3>(cl, S, tot);
       // peers' Y' rows for the next GEMM1
