@@ -124,7 +124,8 @@ struct Smem {
   double *Yf;    // mp x 8   : full Y' (or y-bar at raPDHG checks), instance fastest
   double *Xc;    // np x 8   : X'_c (or x-bar slice)
   double *Pc;    // mp x 8   : partial K~_c X'_c
-  double *part;  // 8 x 24   : per-instance partial sums of this CTA
+  double *part;  // 8 x 24   : per-instance partial sums of this CTA (current of two buffers)
+  double *part_a, *part_b;
   double *wpart; // 8 warps x 8 x 24
   Inst *inst;    // 8
   int *grp;
@@ -248,8 +249,10 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
   S.Yf = S.Ks + (size_t)mp * np;
   S.Xc = S.Yf + (size_t)mp * kS;
   S.Pc = S.Xc + (size_t)np * kS;
-  S.part = S.Pc + (size_t)mp * kS;
-  S.wpart = S.part + kS * 24;
+  S.part_a = S.Pc + (size_t)mp * kS;
+  S.part_b = S.part_a + kS * 24;
+  S.part = S.part_b;
+  S.wpart = S.part_b + kS * 24;
   double *tot = S.wpart + (kThreads / 32) * kS * 24;
   S.inst = (Inst *)(tot + kS * 24);
   S.grp = (int *)(S.inst + kS);
@@ -315,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         P.y[b * m + i] = yv; P.ya[b * m + i] = yv; P.yr[b * m + i] = yv; P.yp[b * m + i] = yv;
         S.Yf[i * kS + s] = yv;
       }
+      S.part = (S.part == S.part_a) ? S.part_b : S.part_a;  // double-buffered (see grid_solver.cu)
       cta_partials<4>(v, S);
       cl.sync();
       cluster_totals<CL, 4>(cl, S, tot);
@@ -356,6 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         P.KTy[b * n + j] = val; P.KTya[b * n + j] = val; P.KTyp[b * n + j] = val;
         kcol(v[s], false, 1.0, P.x[b * n + j], val, 0.0, P.cs[b * n + j], 0.0, P.ls[j], 0.0, P.us[j]);
       });
+      S.part = (S.part == S.part_a) ? S.part_b : S.part_a;  // double-buffered (see grid_solver.cu)
       cta_partials<4>(v, S);
       cl.sync();
       cluster_totals<CL, 4>(cl, S, tot);
@@ -434,6 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         dy_own += d * d;
         I_own += d * (kxp - kxv);
       }
+      S.part = (S.part == S.part_a) ? S.part_b : S.part_a;
       attempt_partials(dx_even, dx_odd, dy_own, I_own, S);
       cl.sync();
       cluster_totals<CL, 3>(cl, S, tot);
@@ -534,6 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       if (tid < kS) S.inst[tid].pending = 0;
       cl.sync();  // every rank's commits (global state) visible before they are read across slices
       if (r2) {
+        S.part = (S.part == S.part_a) ? S.part_b : S.part_a;
         cta_partials<6>(vc, S);
         cl.sync();
         cluster_totals<CL, 6>(cl, S, tot);
@@ -598,6 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           v[s][16] += da * da;
           v[s][18] += dcur * dcur;
         });
+        S.part = (S.part == S.part_a) ? S.part_b : S.part_a;
         cta_partials<20>(v, S);
         cl.sync();
         cluster_totals<CL, 20>(cl, S, tot);
@@ -703,6 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         krow(v[s], true, i < m1, dr, ys, kx, P.Q0[b * P.qstride + i], P.qs[o]);
         P.Y[o] = dr * ys;
       }
+      S.part = (S.part == S.part_a) ? S.part_b : S.part_a;  // double-buffered (see grid_solver.cu)
       cta_partials<4>(v, S);
       cl.sync();
       cluster_totals<CL, 4>(cl, S, tot);
@@ -768,7 +777,7 @@ int dmma_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
     const int nc = (n + CL - 1) / CL;
     const int np = (nc + 7) / 8 * 8;
     const size_t smem = sizeof(double) * ((size_t)mp * np + (size_t)mp * kS + (size_t)np * kS + (size_t)mp * kS +
-                                          kS * 24 + (kThreads / 32) * kS * 24 + kS * 24) +
+                                          2 * kS * 24 + (kThreads / 32) * kS * 24 + kS * 24) +
                         sizeof(Inst) * kS + 64;
     if (smem + 1024 > (size_t)max_optin) continue;
     DmmaParams P;

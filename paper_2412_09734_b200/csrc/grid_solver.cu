@@ -209,6 +209,12 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   double *x = P.x, *KTy = P.KTy, *xp = P.xp, *KTyp = P.KTyp, *xa = P.xa, *KTya = P.KTya, *xr = P.xr;
   double *y = P.y, *Kx = P.Kx, *yp = P.yp, *Kxp = P.Kxp, *ya = P.ya, *Kxa = P.Kxa, *yr = P.yr;
   const double *cs = P.cs, *qs = P.qs;
+  // Per-CTA partials are double-buffered: reduction r writes buffer r % 2, so a CTA that has
+  // moved on can never overwrite partials a slower CTA is still summing (that would let CTAs
+  // take different decisions and then wait at different grid barriers).
+  int pbuf = 1;
+  auto next_part = [&]() { pbuf ^= 1; return P.part + (size_t)pbuf * gridDim.x * kNP; };
+  auto cur_part = [&]() { return (const double *)(P.part + (size_t)pbuf * gridDim.x * kNP); };
 
   // ---------------- step 2: initialise ----------------
   {
@@ -229,11 +235,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       if (i < m1) yv = fmax(yv, 0.0);
       y[i] = yv;
     }
-    block_partials<4>(v, P.part, s_red);
+    block_partials<4>(v, next_part(), s_red);
   }
   grid.sync();
   double tot4[4];
-  grid_totals<4>(tot4, P.part, s_tot);
+  grid_totals<4>(tot4, cur_part(), s_tot);
   const double nc0 = sqrt(tot4[2]), nq0 = sqrt(tot4[3]);
   double omega = 1.0;
   if (sqrt(tot4[0]) > 1e-10 && sqrt(tot4[1]) > 1e-10) omega = sqrt(tot4[0]) / sqrt(tot4[1]);
@@ -264,14 +270,14 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         kkt_col(v, false, 1.0, xv, s, 0.0, cs[j], 0.0, P.ls[j], 0.0, P.us[j]);
       }
     }
-    block_partials<4>(v, P.part, s_red);
+    block_partials<4>(v, next_part(), s_red);
   }
   grid.sync();
   int64_t k = 0, jatt = 0, k_in = 0, restarts = 0;
   double W = 0.0, last = INFINITY, ref = 0.0;
   {
     double t[4];
-    grid_totals<4>(t, P.part, s_tot);
+    grid_totals<4>(t, cur_part(), s_tot);
     if (!r2) {
       const KktT ks = mk(t);
       ref = sqrt(omega * ks.pres * ks.pres + ks.dres * ks.dres / omega + ks.gap * ks.gap);
@@ -378,11 +384,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         t = Kx; Kx = Kxp; Kxp = t;
       }
       pending = false;
-      block_partials<3>(v3, P.part, s_red);
+      block_partials<3>(v3, next_part(), s_red);
     }
     grid.sync();
     double t3[3];
-    grid_totals<3>(t3, P.part, s_tot);
+    grid_totals<3>(t3, cur_part(), s_tot);
     ++jatt;
     const double I = t3[2];
     const double M = omega * t3[0] + t3[1] / omega;
@@ -452,7 +458,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         t = y; y = yp; yp = t;
         t = Kx; Kx = Kxp; Kxp = t;
       }
-      if (r2) block_partials<6>(v, P.part, s_red);
+      if (r2) block_partials<6>(v, next_part(), s_red);
     }
     grid.sync();
     const double *cx, *cy, *cKx, *cKTy;
@@ -495,10 +501,10 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           v[18] += dcur * dcur;
         }
       }
-      block_partials<kNP>(v, P.part, s_red);
+      block_partials<kNP>(v, next_part(), s_red);
       grid.sync();
       double t[kNP];
-      grid_totals<kNP>(t, P.part, s_tot);
+      grid_totals<kNP>(t, cur_part(), s_tot);
       const KktT ka = mk(t + 0), kc = mk(t + 4);
       if (pass(ka, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; break; }
       if (pass(kc, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
@@ -515,7 +521,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       else { cx = x; cy = y; cKx = Kx; cKTy = KTy; metric = e_c; dx2 = t[18]; dy2 = t[19]; }
     } else {
       double t[6];
-      grid_totals<6>(t, P.part, s_tot);
+      grid_totals<6>(t, cur_part(), s_tot);
       const KktT kw = mk(t);
       if (pass(kw, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
       if (k == P.iter_limit) { status = LP_ITERATION_LIMIT; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
@@ -556,11 +562,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       kkt_row(v, true, i, m1, dr, oy[i], oKx[i], P.q0[i], qs[i]);
       P.Y[i] = dr * oy[i];
     }
-    block_partials<4>(v, P.part, s_red);
+    block_partials<4>(v, next_part(), s_red);
   }
   grid.sync();
   double t[4];
-  grid_totals<4>(t, P.part, s_tot);
+  grid_totals<4>(t, cur_part(), s_tot);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const KktT ko = mk(t);
     lp_result r;
@@ -603,7 +609,7 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   // small problems do not need the whole GPU
   const int64_t work_items = (D.nnz + n + m);
   while (blocks > sms && (int64_t)blocks * kBS > 4 * work_items) blocks -= sms;
-  const size_t vec = (size_t)(8 * n + 8 * m) + (size_t)blocks * kNP;
+  const size_t vec = (size_t)(8 * n + 8 * m) + 2 * (size_t)blocks * kNP;
   const size_t need = vec * sizeof(double);
   if (*work_bytes < need) {
     if (*work) MPAX_CUDA(cudaFreeAsync(*work, s));
