@@ -65,6 +65,9 @@ typedef struct {
   int32_t algorithm;            /* ORA_RAPDHG / ORA_R2HPDHG */
   int32_t ruiz_iters;           /* contract c.3 #3: 10 */
   int32_t pock_chambolle;       /* contract c.3 #3: 1 = apply one PC(alpha=1) round */
+  int32_t step_rule;            /* 0: adaptive line search (contract step 3); 1: constant step
+                                   eta = 0.998 / sigma_max(K~) (DESIGN reading 34) */
+  int32_t power_iters;          /* power-iteration steps for sigma_max(K~), default 200 */
 } ora_options;
 
 typedef struct {
@@ -143,6 +146,32 @@ static double dmax(double a, double b) { return fmax(a, b); }
 
 /* median(l, v, u) = min(max(v, l), u): proj_X of Eq. (pdhg), X = {l <= x <= u}. */
 static double median3(double l, double v, double u) { return dmin(dmax(v, l), u); }
+
+/* Largest singular value of M by power iteration on M'M (used by the
+ * constant-step variant, DESIGN reading 34).  Deterministic start vector
+ * v_j = frac(j * 2654435761 / 2^32) + 0.5 (integer hash, exact in double), normalised;
+ * then `iters` times: u = M v, w = M'u, s = ||w||, v = w / s, sigma = sqrt(s).
+ * Returns 0 for a zero matrix. */
+static double power_sigma(const csr *M, const csr *MT, int32_t iters) {
+  const int64_t n = M->ncols, m = M->nrows;
+  double *v = (double *)malloc((size_t)n * sizeof(double));
+  double *u = (double *)malloc((size_t)(m ? m : 1) * sizeof(double));
+  double *w = (double *)malloc((size_t)n * sizeof(double));
+  for (int64_t j = 0; j < n; ++j) v[j] = (double)((uint32_t)((uint64_t)j * 2654435761ull)) / 4294967296.0 + 0.5;
+  double nv = norm2(v, n);
+  for (int64_t j = 0; j < n; ++j) v[j] /= nv;
+  double sigma = 0.0;
+  for (int32_t t = 0; t < iters; ++t) {
+    csr_spmv(M, v, u);
+    csr_spmv(MT, u, w);
+    double sw = norm2(w, n);
+    if (!(sw > 0.0)) { sigma = 0.0; break; }
+    for (int64_t j = 0; j < n; ++j) v[j] = w[j] / sw;
+    sigma = sqrt(sw);
+  }
+  free(v); free(u); free(w);
+  return sigma;
+}
 
 /* ------------------------------------------------------------ Step 0 ----- */
 
@@ -453,10 +482,15 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
     if (nc > 1e-10 && nq > 1e-10) omega = nc / nq;
   }
   double eta = 1.0;
-  {
+  const int const_step = (o->step_rule == 1);
+  if (!const_step) {
     double mx = 0.0;
     for (int64_t k = 0; k < S->K.nnz; ++k) mx = dmax(mx, fabs(S->K.v[k]));
     if (mx > 0.0) eta = 1.0 / mx;
+  } else {
+    /* constant step: eta = 0.998 / sigma_max(K~), so tau sigma ||K~||^2 = eta^2 sigma^2 < 1 */
+    double sg = power_sigma(&S->K, &S->KT, o->power_iters);
+    if (sg > 0.0) eta = 0.998 / sg;
   }
   for (int64_t jj = 0; jj < n; ++jj) x[jj] = median3(S->l[jj], x0 ? x0[jj] / S->Dc[jj] : 0.0, S->u[jj]);
   for (int64_t i = 0; i < m; ++i) y[i] = y0 ? y0[i] / S->Dr[i] : 0.0;
@@ -496,6 +530,7 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
       double eta_bar, eta_next;
       eta_used = eta;
       ora_step_size(eta, omega, dx2, dy2, I, j, &eta_bar, &acc, &eta_next);
+      if (const_step) { acc = 1; eta_next = eta; }   /* no line search: every step accepted */
       log_attempt(g, j, acc, eta_used, eta_bar);
       eta = eta_next;
       if (!acc && ++rejects >= 100) {
@@ -602,6 +637,7 @@ void ora_default_options(ora_options *o) {
   o->check_frequency = 64;                       /* P:96, P:310 */
   o->algorithm = ORA_R2HPDHG;
   o->ruiz_iters = 10; o->pock_chambolle = 1;     /* contract c.3 #3 */
+  o->step_rule = 0; o->power_iters = 200;
 }
 
 int ora_num_threads(void) {
@@ -621,7 +657,8 @@ void ora_set_threads(int t) {
 
 static int check_options(const ora_options *o) {
   if (!o || !(o->eps_abs >= 0.0) || !(o->eps_rel >= 0.0) || o->iteration_limit < 1 ||
-      o->check_frequency < 1 || (o->algorithm != ORA_RAPDHG && o->algorithm != ORA_R2HPDHG))
+      o->check_frequency < 1 || (o->algorithm != ORA_RAPDHG && o->algorithm != ORA_R2HPDHG) ||
+      o->step_rule < 0 || o->step_rule > 1 || o->power_iters < 1)
     return ORA_ERR_INVALID;
   return ORA_OK;
 }
@@ -755,4 +792,14 @@ int ora_kkt_original(const ora_problem *p, const double *x, const double *y, ora
   kkt_residuals(n, m, p->m1, x, y, Kx, KTy, p->c, p->q, p->l, p->u, out);
   free(Kx); free(KTy);
   return e;
+}
+
+/* sigma_max of the problem's K (as given) by the same power iteration (pins: SPEC S:144-146). */
+int ora_spectral_norm(const ora_problem *p, int32_t iters, double *sigma) {
+  csr K = { p->m1 + p->m2, p->n, p->nnz, (int64_t *)p->row_ptr, (int32_t *)p->col_idx, (double *)p->val };
+  csr KT;
+  if (csr_transpose(&K, &KT)) return ORA_ERR_OOM;
+  *sigma = power_sigma(&K, &KT, iters);
+  csr_free(&KT);
+  return ORA_OK;
 }

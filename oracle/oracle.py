@@ -42,7 +42,8 @@ class Problem(C.Structure):
 class Options(C.Structure):
     _fields_ = [("eps_abs", C.c_double), ("eps_rel", C.c_double), ("iteration_limit", C.c_int64),
                 ("check_frequency", C.c_int32), ("algorithm", C.c_int32),
-                ("ruiz_iters", C.c_int32), ("pock_chambolle", C.c_int32)]
+                ("ruiz_iters", C.c_int32), ("pock_chambolle", C.c_int32),
+                ("step_rule", C.c_int32), ("power_iters", C.c_int32)]
 
 
 class Result(C.Structure):
@@ -105,6 +106,7 @@ def lib():
             L.ora_default_options.argtypes = [P(Options)]
             L.ora_num_threads.restype = C.c_int
             L.ora_set_threads.argtypes = [C.c_int]
+            L.ora_spectral_norm.argtypes = [P(Problem), C.c_int32, P(C.c_double)]
             _lib = L
     return _lib
 
@@ -132,7 +134,7 @@ class _Bound:
 
 
 def options(algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, check_frequency=64,
-            ruiz_iters=10, pock_chambolle=1):
+            ruiz_iters=10, pock_chambolle=1, step_rule=0, power_iters=200):
     o = Options()
     lib().ora_default_options(C.byref(o))
     o.algorithm = R2HPDHG if algorithm in ("r2", "r2hpdhg", R2HPDHG) else RAPDHG
@@ -141,6 +143,8 @@ def options(algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, ch
         o.iteration_limit = int(iteration_limit)
     o.check_frequency = check_frequency
     o.ruiz_iters, o.pock_chambolle = ruiz_iters, pock_chambolle
+    o.step_rule = 1 if step_rule in (1, "constant") else 0
+    o.power_iters = power_iters
     return o
 
 
@@ -150,12 +154,12 @@ def validate(lp) -> int:
 
 
 def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, x0=None, y0=None,
-          check_frequency=64, log_capacity=0):
+          check_frequency=64, log_capacity=0, step_rule=0):
     """Full solve (contract steps 0-6).  Returns a dict with x, y, lam, the
     result fields, and (if log_capacity) the attempt/check decision logs."""
     b = _Bound(lp)
     m = lp.m1 + lp.m2
-    o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency)
+    o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule)
     x = np.zeros(lp.n)
     y = np.zeros(m)
     lam = np.zeros(lp.n)
@@ -181,14 +185,14 @@ def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, 
 
 
 def solve_batch(lp, C_=None, Q=None, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None,
-                X0=None, Y0=None, check_frequency=64, threads=None):
+                X0=None, Y0=None, check_frequency=64, threads=None, step_rule=0):
     """Batch solve sharing K, l, u; one instance per OpenMP thread."""
     b = _Bound(lp)
     m = lp.m1 + lp.m2
     Cm = None if C_ is None else _f64(C_)
     Qm = None if Q is None else _f64(Q)
     B = Cm.shape[0] if Cm is not None else Qm.shape[0]
-    o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency)
+    o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule)
     X = np.zeros((B, lp.n))
     Y = np.zeros((B, m))
     res = (Result * B)()
@@ -321,3 +325,11 @@ def project_dual(y, m1):
     y = _f64(y).copy()
     lib().ora_project_dual(m1, y.ctypes.data)
     return y
+
+
+def spectral_norm(lp, iters=200):
+    """sigma_max(K) of the problem's (unscaled) K by the oracle's power iteration."""
+    b = _Bound(lp)
+    s = C.c_double()
+    lib().ora_spectral_norm(C.byref(b.s), iters, C.byref(s))
+    return s.value

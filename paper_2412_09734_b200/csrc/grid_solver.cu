@@ -639,6 +639,8 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   auto group = [](double avg) { return pow2_floor(avg / 4.0); };
   P.gk = group(D.avg_row);
   P.gkt = group(D.avg_col);
+  if (const char *e = getenv("MPAX_GRID_G")) P.gk = atoi(e);     // tuning experiments only
+  if (const char *e = getenv("MPAX_GRID_GT")) P.gkt = atoi(e);
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   void *args[] = {&P};
   MPAX_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(kBS), args, 0, s));

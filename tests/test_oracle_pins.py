@@ -292,3 +292,19 @@ def test_restart_s415_417():
     assert oracle.restart_test(36, 100, 1.0, 1.0, 0.5) is True
     assert oracle.restart_test(5, 100, 0.2, 1.0, 0.1) is True        # boundary (<=) sufficient
     assert oracle.restart_test(5, 100, 0.8, 1.0, 0.8) is False       # not rising
+
+
+# ------------------------------------------------- constant-step variant --
+
+def test_spectral_norm_s144_146():
+    """Power iteration for sigma_max: closed forms and the SVD."""
+    assert oracle.spectral_norm(lpgen.stack([0, 0.0], A=[[3, 0], [0, 1]], b=[0, 0])) == pytest.approx(3.0, rel=1e-12)
+    assert oracle.spectral_norm(lpgen.stack([0, 0.0], A=[[0, 1], [0, 0]], b=[0, 0])) == pytest.approx(1.0, rel=1e-12)
+    rng = np.random.default_rng(4)
+    for shape in [(10, 10), (25, 40), (60, 30)]:
+        K = rng.normal(size=shape)
+        lp = lpgen.stack(np.zeros(shape[1]), A=K, b=np.zeros(shape[0]))
+        s = oracle.spectral_norm(lp, iters=2000)
+        assert s == pytest.approx(np.linalg.svd(K, compute_uv=False)[0], rel=1e-8)
+        assert s <= np.linalg.svd(K, compute_uv=False)[0] * (1 + 1e-12)      # never above sigma_max
+    assert oracle.spectral_norm(lpgen.stack([0, 0.0], A=np.zeros((2, 2)), b=[0, 0])) == 0.0

@@ -146,3 +146,22 @@ def test_iteration_limit_and_degenerate(alg):
     lpz = lpgen.stack([1.0, 1.0], G=[[1.0, 0.0], [0.0, 0.0]], h=[1.0, -1.0], l=[0, 0], u=[5, 5])
     r = oracle.solve(lpz, alg, eps_abs=1e-9, eps_rel=1e-9)
     assert r["status"] == oracle.OPTIMAL and abs(r["primal_objective"] - 1.0) <= 1e-7
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_constant_step_variant(alg):
+    """Constant step eta = 0.998 / sigma_max(K~): no line search,
+    so every attempt is accepted; same optima (plain definitions as above)."""
+    r = oracle.solve(lpgen.tiny_spec(), alg, eps_abs=1e-8, eps_rel=1e-8, step_rule=1)
+    assert r["status"] == oracle.OPTIMAL and abs(r["primal_objective"] - 1.0) <= 1e-6
+    assert r["attempts"] == r["iterations"]
+    lp = lpgen.g_rand(50, 100, 10, seed=1)
+    r = oracle.solve(lp, alg, eps_abs=1e-8, eps_rel=1e-8, iteration_limit=400000, step_rule=1)
+    assert r["status"] == oracle.OPTIMAL and r["attempts"] == r["iterations"]
+    assert abs(r["primal_objective"] - lp.obj_star) <= 1e-6 * (1 + abs(lp.obj_star))
+    lpg, C = lpgen.g_grid(batch=16)
+    _, _, res = oracle.solve_batch(lpg, C, None, alg, step_rule=1)
+    for b in range(16):
+        dp = lpgen.grid_dp_optimum(5, C[b])
+        assert res[b]["status"] == oracle.OPTIMAL and abs(res[b]["primal_objective"] - dp) <= 1e-3 * (1 + dp)
+        assert res[b]["attempts"] == res[b]["iterations"]
