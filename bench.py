@@ -234,20 +234,21 @@ def run_ours(args):
     X_d = torch.empty((args.batch, lp.n), dtype=torch.float64, device=dev)
     Y_d = torch.empty((args.batch, lp.m), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
-    def step(prob, Cx, X, Y, mem, alg=args.alg):
+    def step(prob, Cx, X, Y, mem, alg=args.alg, rule="adaptive"):
         bs = mp.BatchSolver(prob, Cx)
-        res = bs.solve(algorithm=alg, iteration_limit=200_000)   # safety net; every instance must be OPTIMAL
+        # iteration_limit: safety net; every instance must be OPTIMAL
+        res = bs.solve(algorithm=alg, iteration_limit=200_000, step_rule=rule)
         bs.solutions(memory=mem, X=X, Y=Y)
         bs.close()
         return res
 
-    def timed(prob, Cx, X, Y, mem, steps, collect, alg=args.alg):
+    def timed(prob, Cx, X, Y, mem, steps, collect, alg=args.alg, rule="adaptive"):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         all_res = []
         for s in range(steps):
             flush.zero_()                       # evict L2 between steps (outside the event pair)
             ev[s][0].record(stream)
-            res = step(prob, Cx, X, Y, mem, alg)
+            res = step(prob, Cx, X, Y, mem, alg, rule)
             ev[s][1].record(stream)
             if collect:
                 all_res.append(res)
@@ -288,10 +289,29 @@ def run_ours(args):
     barrier()
     ms2, res2 = timed(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, args.secondary_steps, True, alg2)
     barrier()
-    t = torch.tensor([ms, ms_e2e, ms2], dtype=torch.float64, device=dev)
+    # ---- constant-step variants (reading 34), same workload ----
+    log("constant-step variants")
+    var_ms, var_res = {}, {}
+    for va in ("r2", "ra"):
+        step(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, va, "constant")
+        barrier()
+        var_ms[va], var_res[va] = timed(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, args.secondary_steps, True, va,
+                                        "constant")
+        barrier()
+    t = torch.tensor([ms, ms_e2e, ms2, var_ms["r2"], var_ms["ra"]], dtype=torch.float64, device=dev)
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms, ms_e2e, ms2 = float(t[0]), float(t[1]), float(t[2])
+    var_ms = {"r2": float(t[3]), "ra": float(t[4])}
+    variants = {}
+    for va in ("r2", "ra"):
+        itv = np.array([r["iterations"] for r in var_res[va][-1]])
+        variants[("r2hpdhg" if va == "r2" else "rapdhg") + "_constant_step"] = {
+            "value": args.batch * args.secondary_steps * ws / (var_ms[va] * 1e-3), "unit": UNIT,
+            "ms_per_step": var_ms[va] / args.secondary_steps,
+            "all_optimal": all(r["status"] == mp.LP_OPTIMAL for res in var_res[va] for r in res),
+            "iterations": {"p50": float(np.median(itv)), "p99": float(np.percentile(itv, 99)), "max": int(itv.max())},
+            "step": "eta = 0.998 / sigma_max(K~), 200 power iterations (inside the timed step)"}
     it2 = np.array([r["iterations"] for r in res2[-1]])
     secondary = {"algorithm": "r2hpdhg" if alg2 == "r2" else "rapdhg",
                  "value": args.batch * args.secondary_steps * ws / (ms2 * 1e-3), "unit": UNIT,
@@ -341,6 +361,7 @@ def run_ours(args):
                        "max": int(iters.max()), "attempts_total": int(atts.sum())},
         "clocks": clocks,
         "secondary": secondary,
+        "variants": variants,
     }
     if not args.no_large:
         log("large-LP leg (C4)")

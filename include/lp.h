@@ -68,6 +68,13 @@ enum lp_status {
 };
 
 enum lp_algorithm { LP_RAPDHG = 0, LP_R2HPDHG = 1 };
+
+/* Step-size rule (lp_options.step_rule).  ADAPTIVE is the line search of P:95
+ * (DESIGN.md §3 reading 4).  CONSTANT uses eta = 0.998 / sigma_max(K~) with
+ * sigma_max from 200 power iterations on K~'K~ (deterministic start vector), every
+ * attempt accepted -- the constant-step r2HPDHG of the cited Halpern work (SURVEY
+ * §8(f) row 4; reading 34). */
+enum lp_step_rule { LP_STEP_ADAPTIVE = 0, LP_STEP_CONSTANT = 1 };
 enum lp_memory { LP_HOST = 0, LP_DEVICE = 1 };
 
 /* Solve path selection (lp_options.path). */
@@ -110,7 +117,7 @@ typedef struct {
   int32_t verbose;              /* reserved */
   int32_t display_frequency;    /* 10, reserved */
   int32_t path;                 /* lp_path, default LP_PATH_AUTO */
-  int32_t reserved;
+  int32_t step_rule;            /* lp_step_rule, default LP_STEP_ADAPTIVE */
 } lp_options;
 
 /* Per-instance outcome.  The objectives and residuals are those of the
@@ -132,7 +139,7 @@ typedef struct {
 } lp_result;
 
 /* Fills o with the Appendix defaults: 1e-4, 1e-4, 1e-8, 1e-8, 1e-6,
- * INT64_MAX, 64, LP_R2HPDHG, 0, 0, 0, 10, LP_PATH_AUTO. */
+ * INT64_MAX, 64, LP_R2HPDHG, 0, 0, 0, 10, LP_PATH_AUTO, LP_STEP_ADAPTIVE. */
 void lp_default_options(lp_options *o);
 
 /* Create a single-LP handle: validates, uploads, builds

@@ -189,7 +189,7 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
     A.take(&h->rp64, m + 1); A.take(&P.rp, m + 1); A.take(&P.ci, nnz); A.take(&P.kv0, nnz); A.take(&P.kv, nnz);
     A.take(&P.trp, n + 1); A.take(&P.tci, nnz); A.take(&P.perm, nnz); A.take(&P.tkv, nnz);
     A.take(&P.l0, n); A.take(&P.u0, n); A.take(&P.ls, n); A.take(&P.us, n); A.take(&P.Dr, m); A.take(&P.Dc, n);
-    A.take(&P.kmax, 1); A.take(&h->C0, perC ? batch * n : n); A.take(&h->Q0, perQ ? batch * m : m);
+    A.take(&P.kmax, 1); A.take(&P.sigma, 1); A.take(&h->C0, perC ? batch * n : n); A.take(&h->Q0, perQ ? batch * m : m);
     A.take(&h->X, batch * n); A.take(&h->Y, batch * m); A.take(&h->L, batch * n);
     A.take(&h->d_res, batch); A.take(&h->queue, 1); A.take(&h->d_flag, 8);
   };
@@ -251,6 +251,8 @@ int check_options(const lp_options *o) {
     return fail(LP_ERR_INVALID_ARGUMENT, "bad option value");
   if (o->feasibility_polishing) return fail(LP_ERR_UNSUPPORTED, "feasibility polishing is not built yet");
   if (o->path < LP_PATH_AUTO || o->path > LP_PATH_DMMA) return fail(LP_ERR_INVALID_ARGUMENT, "bad path");
+  if (o->step_rule != LP_STEP_ADAPTIVE && o->step_rule != LP_STEP_CONSTANT)
+    return fail(LP_ERR_INVALID_ARGUMENT, "bad step_rule");
   return LP_OK;
 }
 
@@ -297,10 +299,12 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
   const bool big = h->P.nnz >= 32768 || h->P.n + h->P.m >= 4096;
   const bool use_grid = (B == 1) && (o->path == LP_PATH_GRID || (o->path == LP_PATH_AUTO && big));
   if (o->path == LP_PATH_GRID && B != 1) return fail(LP_ERR_UNSUPPORTED, "the grid path solves one LP");
+  MPAX_CUDA(cudaEventRecord(h->ev0, s));
+  // constant step rule: sigma_max(K~) once per handle (K is fixed for its lifetime)
+  if (o->step_rule == LP_STEP_CONSTANT && !h->P.sigma_ready) TRY(power_sigma(h->P, s));
   if (use_grid) {
     GridLaunch G;
     G.c0 = h->C0; G.q0 = h->Q0; G.X0 = dX0; G.Y0 = dY0; G.X = h->X; G.Y = h->Y; G.L = h->L; G.res = h->d_res;
-    MPAX_CUDA(cudaEventRecord(h->ev0, s));
     int rc = grid_solve(h->P, *o, G, s, &h->work, &h->work_bytes);
     if (rc == LP_ERR_UNSUPPORTED) return fail(rc, "cooperative launch unavailable");
     TRY(rc);
@@ -328,7 +332,6 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
       h->work_bytes = need;
     }
   }
-  MPAX_CUDA(cudaEventRecord(h->ev0, s));
   int rc = LP_ERR_UNSUPPORTED;
   if (dmma) {
     rc = dmma_solve(h->P, *o, L, s, h->queue, h->work);

@@ -56,10 +56,10 @@ struct DmmaParams {
   const double *Dr, *Dc, *ls, *us, *l0, *u0;
   const double *C0, *Q0, *X0, *Y0;
   int64_t cstride, qstride;
-  const double *kmax, *tab;
+  const double *kmax, *sigma, *tab;
   double eps_abs, eps_rel;
   int64_t iter_limit;
-  int32_t check_freq, alg;
+  int32_t check_freq, alg, const_step;
   int64_t batch;
   unsigned long long *queue;
   // per-instance state, instance-major [B][n] / [B][m]
@@ -271,8 +271,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
   }
   for (int t = tid; t < mp * kS; t += kThreads) { S.Yf[t] = 0.0; S.Pc[t] = 0.0; }
   for (int t = tid; t < np * kS; t += kThreads) S.Xc[t] = 0.0;
-  const double kmx = *P.kmax;
-  const double eta0 = kmx > 0.0 ? 1.0 / kmx : 1.0;
+  const bool cstep = P.const_step != 0;  // constant step rule (reading 34)
+  const double eta0 = initial_eta(P.kmax, P.sigma, cstep);
 
   for (;;) {
     // ---- next group of 8 instances (rank 0 pulls from the queue) ----
@@ -463,9 +463,9 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           const double Iv = t3[2];
           const double M = I.omega * t3[0] + t3[1] / I.omega;
           const double eb = (Iv != 0.0) ? M / (2.0 * fabs(Iv)) : INFINITY;
-          const bool acc = I.eta <= eb;
+          const bool acc = cstep || I.eta <= eb;
           const double eta_used = I.eta;
-          I.eta = fmin(f1 * eb, f2 * I.eta);
+          if (!cstep) I.eta = fmin(f1 * eb, f2 * I.eta);
           if (!acc) {
             if (++I.rejects >= 100) { I.status = LP_NUMERICAL_ERROR; I.done = 1; I.outsel = 0; }
           } else {
@@ -785,7 +785,7 @@ int dmma_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
     P.K = D.kv;
     P.Dr = D.Dr; P.Dc = D.Dc; P.ls = D.ls; P.us = D.us; P.l0 = D.l0; P.u0 = D.u0;
     P.C0 = L.C0; P.Q0 = L.Q0; P.X0 = L.X0; P.Y0 = L.Y0; P.cstride = L.cstride; P.qstride = L.qstride;
-    P.kmax = D.kmax; P.tab = D.tab;
+    P.kmax = D.kmax; P.sigma = D.sigma; P.tab = D.tab; P.const_step = o.step_rule == LP_STEP_CONSTANT;
     P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
     P.check_freq = o.check_frequency; P.alg = o.algorithm;
     P.batch = L.batch; P.queue = queue;

@@ -40,14 +40,14 @@ constexpr int kBS = 512;     // threads per CTA
 struct GridParams {
   int64_t n, m, m1;
   const int32_t *rp, *ci, *trp, *tci;
-  const double *kv, *tkv, *Dr, *Dc, *ls, *us, *l0, *u0, *c0, *q0, *X0, *Y0, *kmax, *tab;
+  const double *kv, *tkv, *Dr, *Dc, *ls, *us, *l0, *u0, *c0, *q0, *X0, *Y0, *kmax, *sigma, *tab;
   double *cs, *qs;
   double *x, *KTy, *xp, *KTyp, *xa, *KTya, *xr;   // n-side
   double *y, *Kx, *yp, *Kxp, *ya, *Kxa, *yr;      // m-side
   double *part;                                   // gridDim.x x kNP
   double eps_abs, eps_rel;
   int64_t iter_limit;
-  int32_t check_freq, alg, gk, gkt;
+  int32_t check_freq, alg, gk, gkt, const_step;
   double *X, *Y, *L;
   lp_result *res;
 };
@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   const double nc0 = sqrt(tot4[2]), nq0 = sqrt(tot4[3]);
   double omega = 1.0;
   if (sqrt(tot4[0]) > 1e-10 && sqrt(tot4[1]) > 1e-10) omega = sqrt(tot4[0]) / sqrt(tot4[1]);
-  const double kmx = *P.kmax;
-  double eta = kmx > 0.0 ? 1.0 / kmx : 1.0;
+  const bool cstep = P.const_step != 0;  // constant step rule (reading 34)
+  double eta = initial_eta(P.kmax, P.sigma, cstep);
   {
     // K~x0, K~'y0; anchors / restart point; KKT_omega(z0) partials (scaled space)
     double v[4] = {0.0, 0.0, 0.0, 0.0};
@@ -393,11 +393,13 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     const double I = t3[2];
     const double M = omega * t3[0] + t3[1] / omega;
     const double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : INFINITY;
-    const bool acc = (eta <= eb);
+    const bool acc = cstep || (eta <= eb);
     const double eta_used = eta;
-    double f1, f2;
-    step_factors(P.tab, jatt, f1, f2);
-    eta = fmin(f1 * eb, f2 * eta);
+    if (!cstep) {
+      double f1, f2;
+      step_factors(P.tab, jatt, f1, f2);
+      eta = fmin(f1 * eb, f2 * eta);
+    }
     if (!acc) {
       if (++rejects >= 100) { status = LP_NUMERICAL_ERROR; ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
       continue;
@@ -622,7 +624,8 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   P.n = n; P.m = m; P.m1 = D.m1;
   P.rp = D.rp; P.ci = D.ci; P.trp = D.trp; P.tci = D.tci;
   P.kv = D.kv; P.tkv = D.tkv; P.Dr = D.Dr; P.Dc = D.Dc; P.ls = D.ls; P.us = D.us; P.l0 = D.l0; P.u0 = D.u0;
-  P.c0 = L.c0; P.q0 = L.q0; P.X0 = L.X0; P.Y0 = L.Y0; P.kmax = D.kmax; P.tab = D.tab;
+  P.c0 = L.c0; P.q0 = L.q0; P.X0 = L.X0; P.Y0 = L.Y0; P.kmax = D.kmax; P.sigma = D.sigma; P.tab = D.tab;
+  P.const_step = o.step_rule == LP_STEP_CONSTANT;
   P.cs = w; w += n;
   P.x = w; w += n; P.KTy = w; w += n; P.xp = w; w += n; P.KTyp = w; w += n; P.xa = w; w += n; P.KTya = w; w += n;
   P.xr = w; w += n;

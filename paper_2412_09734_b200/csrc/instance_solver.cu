@@ -41,10 +41,10 @@ struct InstParams {
   const double *kv, *tkv, *Dr, *Dc, *ls, *us, *l0, *u0;
   const double *C0, *Q0, *X0, *Y0;
   int64_t cstride, qstride;
-  const double *kmax, *tab;
+  const double *kmax, *sigma, *tab;
   double eps_abs, eps_rel;
   int64_t iter_limit;
-  int32_t check_freq, alg;
+  int32_t check_freq, alg, const_step;
   int64_t batch;
   unsigned long long *queue;
   double *X, *Y, *L;
@@ -194,8 +194,8 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
   __shared__ unsigned long long s_inst;
   const bool r2 = (P.alg == LP_R2HPDHG);
   const int G = P.gk, Gt = P.gkt;
-  const double kmx = *P.kmax;
-  const double eta0 = kmx > 0.0 ? 1.0 / kmx : 1.0;
+  const bool cstep = P.const_step != 0;  // constant step rule (reading 34)
+  const double eta0 = initial_eta(P.kmax, P.sigma, cstep);
   int rbuf = 0;
   auto redbuf = [&]() { rbuf ^= 1; return rbuf ? red1 : red0; };
 
@@ -347,9 +347,9 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
       const double I = v3[2];
       const double M = omega * v3[0] + v3[1] / omega;
       const double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : INFINITY;
-      const bool acc = (eta <= eb);
+      const bool acc = cstep || (eta <= eb);
       const double eta_used = eta;
-      eta = fmin(f1 * eb, f2 * eta);
+      if (!cstep) eta = fmin(f1 * eb, f2 * eta);
       if (!acc) {
         if (++rejects >= 100) { status = LP_NUMERICAL_ERROR; ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
         continue;
@@ -586,7 +586,7 @@ int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunc
   P.rp = D.rp; P.ci = D.ci; P.trp = D.trp; P.tci = D.tci;
   P.kv = D.kv; P.tkv = D.tkv; P.Dr = D.Dr; P.Dc = D.Dc; P.ls = D.ls; P.us = D.us; P.l0 = D.l0; P.u0 = D.u0;
   P.C0 = L.C0; P.cstride = L.cstride; P.Q0 = L.Q0; P.qstride = L.qstride; P.X0 = L.X0; P.Y0 = L.Y0;
-  P.kmax = D.kmax; P.tab = D.tab;
+  P.kmax = D.kmax; P.sigma = D.sigma; P.tab = D.tab; P.const_step = o.step_rule == LP_STEP_CONSTANT;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
   P.check_freq = o.check_frequency; P.alg = o.algorithm;
   P.batch = L.batch; P.queue = queue;

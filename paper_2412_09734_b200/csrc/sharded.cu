@@ -35,7 +35,7 @@ constexpr int kV = 24;   // partial-sum slots
 struct ShState {
   double omega, eta, W, ref, last, theta, ha, hb, rP, M, Iv, eta_used, metric, nc0, nq0, eta0;
   long long k, j, k_in, restarts;
-  int rejects, status, pending, halt, restart, outsel, csel, r2;
+  int rejects, status, pending, halt, restart, outsel, csel, r2, cstep;
   double colsum[kV];  // totals over this GPU's columns (replicated data: identical on every GPU)
   double rowsum[kV];  // totals over this GPU's rows; reduced across GPUs in place
   unsigned int cnt_cols, cnt_rows;
@@ -350,14 +350,14 @@ __global__ void k_init_decide(ShState *st, int stage) {
 __global__ void k_decide(ShState *st, const double *tab, int64_t check_freq, int64_t iter_limit) {
   if (st->halt) return;
   st->j += 1;
-  double f1, f2;
-  step_factors(tab, st->j, f1, f2);
+  double f1 = 0.0, f2 = 0.0;
+  if (!st->cstep) step_factors(tab, st->j, f1, f2);
   const double dx2 = st->colsum[0], dy2 = st->rowsum[0], I = st->rowsum[1];
   const double M = st->omega * dx2 + dy2 / st->omega;
   const double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : INFINITY;
-  const bool acc = st->eta <= eb;
+  const bool acc = st->cstep || st->eta <= eb;  // constant step rule: DESIGN.md reading 34
   const double eta_used = st->eta;
-  st->eta = fmin(f1 * eb, f2 * st->eta);
+  if (!st->cstep) st->eta = fmin(f1 * eb, f2 * st->eta);
   if (!acc) {
     st->pending = 0;
     if (++st->rejects >= 100) { st->status = LP_NUMERICAL_ERROR; st->halt = 1; st->outsel = 0; }
@@ -462,10 +462,10 @@ __global__ void k_vreduce(double *const *ptrs, int p, int64_t count, int op_max)
   }
 }
 
-__global__ void k_set_eta0(ShState *st, const double *kmax, int r2) {
-  const double k = *kmax;
-  st->eta0 = k > 0.0 ? 1.0 / k : 1.0;
+__global__ void k_set_eta0(ShState *st, const double *kmax, const double *sigma, int r2, int cstep) {
+  st->eta0 = initial_eta(kmax, sigma, cstep != 0);
   st->r2 = r2;
+  st->cstep = cstep;
 }
 
 }  // namespace
@@ -497,6 +497,7 @@ struct ShardedLP {
   int *d_flags = nullptr, *h_flags = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool solved = false;
+  bool sigma_ready = false;  // sigma_max(K~) computed into every shard's P.sigma
 };
 
 namespace {
@@ -561,7 +562,7 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
     const size_t o_rp64 = al((m + 1) * 8), o_rp = al((m + 1) * 4), o_ci = al(nnz * 4 + 4), o_kv0 = al(nnz * 8 + 8),
                  o_kv = al(nnz * 8 + 8), o_trp = al((n + 1) * 4), o_tci = al(nnz * 4 + 4), o_perm = al(nnz * 4 + 4),
                  o_tkv = al(nnz * 8 + 8), o_l0 = al(n * 8), o_u0 = al(n * 8), o_ls = al(n * 8), o_us = al(n * 8),
-                 o_Dr = al(m * 8 + 8), o_Dc = al(n * 8), o_kmax = al(8), o_c0 = al(n * 8), o_q0 = al(m * 8 + 8),
+                 o_Dr = al(m * 8 + 8), o_Dc = al(n * 8), o_kmax = al(8), o_sigma = al(8), o_c0 = al(n * 8), o_q0 = al(m * 8 + 8),
                  o_st = al(sizeof(ShState)), o_flag = al(64);
     char *base = nullptr;
     MPAX_CUDA(cudaMallocAsync((void **)&base, bytes, s));
@@ -572,6 +573,7 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
     P.l0 = (double *)(base + o_l0); P.u0 = (double *)(base + o_u0); P.ls = (double *)(base + o_ls);
     P.us = (double *)(base + o_us); P.Dr = (double *)(base + o_Dr); P.Dc = (double *)(base + o_Dc);
     P.kmax = (double *)(base + o_kmax);
+    P.sigma = (double *)(base + o_sigma);
     double *c0 = (double *)(base + o_c0), *q0 = (double *)(base + o_q0);
     S.st = (ShState *)(base + o_st);
     int *flag = (int *)(base + o_flag);
@@ -688,17 +690,40 @@ int cols_spmv(ShardedLP &E, int which /*0: yp, 1: y, 2: ya*/) {
 
 }  // namespace
 
+namespace {
+
+// sigma_max(K~) of the row-sharded K~ (power.cu): u_g = K~_g v on each shard's rows,
+// w = sum_g K~_g' u_g reduced across shards, then the replicated normalisation.
+int sharded_power(ShardedLP &E) {
+  cudaStream_t s = E.s;
+  std::vector<PowerState> ps(E.sh.size());
+  for (size_t g = 0; g < E.sh.size(); ++g) STRY(power_begin(ps[g], E.n, E.sh[g].P.m, s));
+  std::vector<double *> ws;
+  for (auto &p : ps) ws.push_back(p.w);
+  for (int t = 0; t < kPowerIters; ++t) {
+    for (size_t g = 0; g < E.sh.size(); ++g) STRY(power_products(E.sh[g].P, ps[g], s));
+    STRY(reduce_vec(E, 4, ws, E.n, false));
+    for (size_t g = 0; g < E.sh.size(); ++g) STRY(power_normalize(ps[g], E.sh[g].P.sigma, s));
+  }
+  for (auto &p : ps) STRY(power_end(p, s));
+  E.sigma_ready = true;
+  return LP_OK;
+}
+
+}  // namespace
+
 int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const double *Y0, lp_result *out) {
   cudaStream_t s = E.s;
-  const bool r2 = o.algorithm == LP_R2HPDHG;
+  const bool r2 = o.algorithm == LP_R2HPDHG, cstep = o.step_rule == LP_STEP_CONSTANT;
+  MPAX_CUDA(cudaEventRecord(E.ev0, s));
+  if (cstep && !E.sigma_ready) STRY(sharded_power(E));
   for (auto &S : E.sh) {
     MPAX_CUDA(cudaMemsetAsync(S.st, 0, sizeof(ShState), s));
     S.V.X0 = X0;                                        // full n (replicated)
     S.V.Y0 = Y0 ? Y0 + S.row_offset - (E.virt ? 0 : 0) : nullptr;
-    MPAX_LAUNCH(k_set_eta0, 1, 1, 0, s, S.st, S.P.kmax, r2 ? 1 : 0);
+    MPAX_LAUNCH(k_set_eta0, 1, 1, 0, s, S.st, S.P.kmax, S.P.sigma, r2 ? 1 : 0, cstep ? 1 : 0);
   }
   if (!E.virt) for (auto &S : E.sh) S.V.Y0 = Y0;        // a real rank passes its own rows
-  MPAX_CUDA(cudaEventRecord(E.ev0, s));
   // ---- step 2 ----
   STRY(launch_cols(E, COLS_INIT));
   STRY(launch_rows(E, ROWS_INIT));

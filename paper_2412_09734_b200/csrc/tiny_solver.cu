@@ -20,7 +20,7 @@ struct TinyParams {
   const double *kv, *tkv, *Dr, *Dc, *ls, *us, *l0, *u0;
   const double *C0, *Q0, *X0, *Y0;
   int64_t cstride, qstride;
-  const double *kmax, *tab;
+  const double *kmax, *sigma, *tab;
   double eps_abs, eps_rel;
   int64_t iter_limit;
   int32_t check_freq;
@@ -77,7 +77,10 @@ __device__ __forceinline__ void kcol(double *v, bool orig, double dc, double xs,
   if (u < INFINITY) v[3] -= u * lm;
 }
 
-template <bool R2, int RPT, int CPT, int W, int WT>
+// CS: constant step rule (eta = 0.998 / sigma_max(K~), every attempt accepted; DESIGN.md
+// reading 34) -- the line-search reductions are then needed only where r2HPDHG uses
+// r_P (restart reference at k_in = 0 and the check), and never for raPDHG.
+template <bool R2, bool CS, int RPT, int CPT, int W, int WT>
 __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x;
@@ -119,8 +122,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
   // padding entries point at element 0 with value 0; keep the gather buffers finite
   for (int t = lane; t < 32 * CPT; t += 32) sx[t] = 0.0;
   for (int t = lane; t < 32 * RPT; t += 32) sy[t] = 0.0;
-  const double kmx = *P.kmax;
-  const double eta0 = kmx > 0.0 ? 1.0 / kmx : 1.0;
+  const double eta0 = initial_eta(P.kmax, P.sigma, CS);
   __shared__ unsigned long long s_inst;
 
   for (;;) {
@@ -209,8 +211,14 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       // (theta_p = 0 leaves the average bit-identical), so the attempt is one basic block.
       const double tau = eta * inv_omega, sigma = eta * omega;
       const double theta_p = pending ? theta : 0.0;
-      double f1, f2;
-      step_factors(P.tab, jatt + 1, f1, f2);
+      double f1 = 0.0, f2 = 0.0;
+      if (!CS) step_factors(P.tab, jatt + 1, f1, f2);
+      // r2HPDHG: the Halpern coefficients this attempt commits with if accepted (index k_in),
+      // loaded now so the table latency overlaps the attempt instead of the next commit
+      double ha_n = 0.0, hb_n = 0.0;
+      if (R2) halpern_coeffs(P.tab, k_in, ha_n, hb_n);
+      // warp-uniform: does this attempt need ||dx||, ||dy||, <dy, K dx>?
+      const bool need = !CS || (R2 && (k_in == 0 || k + 1 == next_check));
       double dx2 = 0.0;
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {
@@ -235,7 +243,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       }
       // the ||dx||^2 butterfly does not depend on phase B: issue it now so it overlaps
       double vdx[1] = {dx2};
-      wsum<1>(vdx);
+      if (need) wsum<1>(vdx);
       __syncwarp();
       // ================= phase B: [commit m-side] + SpMV #1 + dual step =================
       double dy2 = 0.0, I = 0.0;
@@ -265,14 +273,14 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       }
       pending = false;
       double v3[2] = {dy2, I};
-      wsum<2>(v3);
+      if (need) wsum<2>(v3);
       ++jatt;
       const double M = omega * vdx[0] + v3[0] * inv_omega;
       const double Iv = v3[1];
       const double eb = (Iv != 0.0) ? M / (2.0 * fabs(Iv)) : INFINITY;
-      const bool acc = (eta <= eb);
+      const bool acc = CS || (eta <= eb);
       const double eta_used = eta;
-      eta = fmin(f1 * eb, f2 * eta);
+      if (!CS) eta = fmin(f1 * eb, f2 * eta);
       if (!acc) {
         if (++rejects >= 100) { status = LP_NUMERICAL_ERROR; outsel = 0; break; }
         continue;
@@ -284,9 +292,13 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         theta = eta_used / W1;
         W_ = W1;
       } else {
-        rP = sqrt(fmax(0.0, M / eta_used - 2.0 * Iv));
+        // r_P is read only as the restart reference (k_in = 0) and as the check metric:
+        // skip its division and square root on the other attempts (they sit on the
+        // warp's in-order issue path)
+        if (k_in == 0 || k + 1 == next_check) rP = sqrt(fmax(0.0, M / eta_used - 2.0 * Iv));
         if (k_in == 0) ref = rP;
-        halpern_coeffs(P.tab, k_in, ha, hb);
+        ha = ha_n;
+        hb = hb_n;
       }
       ++k;
       ++k_in;
@@ -475,25 +487,26 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
   }
 }
 
-template <bool R2, int RPT, int CPT, int W, int WT>
+template <bool R2, bool CS, int RPT, int CPT, int W, int WT>
 int launch_tiny(const TinyParams &P, cudaStream_t s) {
   int dev = 0, sms = 0, per_sm = 0;
   MPAX_CUDA(cudaGetDevice(&dev));
   MPAX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const size_t smem = (size_t)32 * (CPT + RPT) * sizeof(double);
-  MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiny_kernel<R2, RPT, CPT, W, WT>, 32, smem));
+  MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiny_kernel<R2, CS, RPT, CPT, W, WT>, 32, smem));
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)per_sm * sms;
   if (grid > P.batch) grid = P.batch;
   MPAX_CUDA(cudaMemsetAsync(P.queue, 0, sizeof(unsigned long long), s));
-  MPAX_LAUNCH((tiny_kernel<R2, RPT, CPT, W, WT>), (int)grid, 32, smem, s, P);
+  MPAX_LAUNCH((tiny_kernel<R2, CS, RPT, CPT, W, WT>), (int)grid, 32, smem, s, P);
   MPAX_CHECK_LAUNCH();
   return LP_OK;
 }
 
 template <int RPT, int CPT, int W, int WT>
-int launch_alg(const TinyParams &P, bool r2, cudaStream_t s) {
-  return r2 ? launch_tiny<true, RPT, CPT, W, WT>(P, s) : launch_tiny<false, RPT, CPT, W, WT>(P, s);
+int launch_alg(const TinyParams &P, bool r2, bool cs, cudaStream_t s) {
+  if (cs) return r2 ? launch_tiny<true, true, RPT, CPT, W, WT>(P, s) : launch_tiny<false, true, RPT, CPT, W, WT>(P, s);
+  return r2 ? launch_tiny<true, false, RPT, CPT, W, WT>(P, s) : launch_tiny<false, false, RPT, CPT, W, WT>(P, s);
 }
 
 }  // namespace
@@ -507,15 +520,15 @@ int tiny_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
   P.rp = D.rp; P.ci = D.ci; P.trp = D.trp; P.tci = D.tci;
   P.kv = D.kv; P.tkv = D.tkv; P.Dr = D.Dr; P.Dc = D.Dc; P.ls = D.ls; P.us = D.us; P.l0 = D.l0; P.u0 = D.u0;
   P.C0 = L.C0; P.cstride = L.cstride; P.Q0 = L.Q0; P.qstride = L.qstride; P.X0 = L.X0; P.Y0 = L.Y0;
-  P.kmax = D.kmax; P.tab = D.tab;
+  P.kmax = D.kmax; P.sigma = D.sigma; P.tab = D.tab;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit; P.check_freq = o.check_frequency;
   P.batch = L.batch; P.queue = queue;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
-  const bool r2 = o.algorithm == LP_R2HPDHG;
+  const bool r2 = o.algorithm == LP_R2HPDHG, cs = o.step_rule == LP_STEP_CONSTANT;
   const int64_t n = D.n, m = D.m;
   const int W = D.max_row, WT = D.max_col;
-  if (m <= 32 && n <= 64 && W <= 4 && WT <= 4) return launch_alg<1, 2, 4, 4>(P, r2, s);
-  if (m <= 32 && n <= 64 && W <= 8 && WT <= 8) return launch_alg<1, 2, 8, 8>(P, r2, s);
+  if (m <= 32 && n <= 64 && W <= 4 && WT <= 4) return launch_alg<1, 2, 4, 4>(P, r2, cs, s);
+  if (m <= 32 && n <= 64 && W <= 8 && WT <= 8) return launch_alg<1, 2, 8, 8>(P, r2, cs, s);
   return LP_ERR_UNSUPPORTED;
 }
 

@@ -16,6 +16,7 @@ LP_HOST, LP_DEVICE = 0, 1
 LP_OPTIMAL, LP_ITERATION_LIMIT, LP_NUMERICAL_ERROR = 1, 2, 3
 RAPDHG, R2HPDHG = 0, 1
 PATH_AUTO, PATH_INSTANCE, PATH_GRID, PATH_DMMA = 0, 1, 2, 3
+STEP_ADAPTIVE, STEP_CONSTANT = 0, 1
 
 EXPORTED_SYMBOLS = [
     "lp_default_options", "lp_create", "lp_create_batch", "lp_update_batch", "lp_solve", "lp_solve_batch",
@@ -47,7 +48,7 @@ class Options(C.Structure):
                 ("eps_dual_infeasible", C.c_double), ("eps_feas_polish", C.c_double),
                 ("iteration_limit", C.c_int64), ("check_frequency", C.c_int32), ("algorithm", C.c_int32),
                 ("warm_start", C.c_int32), ("feasibility_polishing", C.c_int32), ("verbose", C.c_int32),
-                ("display_frequency", C.c_int32), ("path", C.c_int32), ("reserved", C.c_int32)]
+                ("display_frequency", C.c_int32), ("path", C.c_int32), ("step_rule", C.c_int32)]
 
 
 class Result(C.Structure):
@@ -251,6 +252,9 @@ def create_lp(c, A=None, b=None, G=None, h=None, l=None, u=None, use_sparse_matr
 def default_options(**kw) -> Options:
     o = Options()
     lib().lp_default_options(C.byref(o))
+    rule = kw.pop("step_rule", None)
+    if rule is not None:
+        o.step_rule = STEP_CONSTANT if rule in ("constant", STEP_CONSTANT) else STEP_ADAPTIVE
     alg = kw.pop("algorithm", None)
     if alg is not None:
         o.algorithm = R2HPDHG if alg in ("r2", "r2hpdhg", "r2HPDHG", R2HPDHG) else RAPDHG
