@@ -323,3 +323,44 @@ def random_small_lp(seed: int, n: int = 4, m1: int = 2, m2: int = 1, box: float 
     b = A @ x0
     c = rng.normal(size=n)
     return stack(c, G=G, h=h, A=A, b=b, l=l, u=u)
+
+
+# ----------------------------------------------------------- G-INFEAS --
+
+def g_infeasible(kind: str, seed: int, m1: int = 12, m2: int = 4, n: int = 24, box: float = 5.0) -> LP:
+    """Small dense LPs infeasible by construction (SURVEY §8(f) row 1 test inputs).
+
+    kind="primal": a feasible random LP (random interior point x0) plus one more
+    ">=" row -sum_i y_i G_i x >= -sum_i y_i h_i + delta with y >= 0 on 3 rows and
+    delta > 0: adding it to sum_i y_i (G_i x >= h_i) gives 0 >= delta, so the
+    rows have no solution at all (Farkas; the box plays no part).
+    kind="dual": a feasible random LP where column j has G[:, j] >= 0, A[:, j] = 0,
+    u_j = +inf and c_j < 0, so x0 + t e_j stays feasible for every t >= 0 while
+    c'x decreases without bound (the LP is unbounded, its dual infeasible)."""
+    rng = np.random.default_rng(seed)
+    G = rng.normal(size=(m1, n)) * (rng.random((m1, n)) < 0.4)
+    A = rng.normal(size=(m2, n)) * (rng.random((m2, n)) < 0.4)
+    l = -rng.uniform(0.5, box, size=n)
+    u = rng.uniform(0.5, box, size=n)
+    x0 = rng.uniform(l, u)
+    c = rng.normal(size=n)
+    if kind == "dual":
+        j = int(rng.integers(n))
+        G[:, j] = np.abs(G[:, j])
+        A[:, j] = 0.0
+        u[j] = INF
+        c[j] = -abs(c[j]) - 0.5
+        x0[j] = l[j] + 1.0
+    h = G @ x0 - rng.uniform(0.0, 1.0, size=m1)
+    b = A @ x0
+    if kind == "primal":
+        rows = rng.choice(m1, size=3, replace=False)
+        y = np.zeros(m1)
+        y[rows] = rng.uniform(0.5, 2.0, size=3)
+        G = np.vstack([G, -(y @ G)])
+        h = np.append(h, -(y @ h) + rng.uniform(0.5, 2.0))
+    elif kind != "dual":
+        raise ValueError(kind)
+    lp = stack(c, G=G, h=h, A=A, b=b, l=l, u=u)
+    lp.meta = dict(generator="G-INFEAS", kind=kind, seed=seed)
+    return lp

@@ -44,7 +44,8 @@
 
 enum { ORA_OK = 0, ORA_ERR_INVALID = -1, ORA_ERR_DIMENSION = -2, ORA_ERR_NAN = -3,
        ORA_ERR_CROSSED_BOUNDS = -4, ORA_ERR_OOM = -6 };
-enum { ORA_OPTIMAL = 1, ORA_ITERATION_LIMIT = 2, ORA_NUMERICAL_ERROR = 3 };
+enum { ORA_OPTIMAL = 1, ORA_ITERATION_LIMIT = 2, ORA_NUMERICAL_ERROR = 3, ORA_PRIMAL_INFEASIBLE = 4,
+       ORA_DUAL_INFEASIBLE = 5 };
 enum { ORA_RAPDHG = 0, ORA_R2HPDHG = 1 };
 
 /* ---------------------------------------------------------------- types -- */
@@ -68,7 +69,26 @@ typedef struct {
   int32_t step_rule;            /* 0: adaptive line search (contract step 3); 1: constant step
                                    eta = 0.998 / sigma_max(K~) (DESIGN reading 34) */
   int32_t power_iters;          /* power-iteration steps for sigma_max(K~), default 200 */
+  double eps_primal_infeasible; /* Appendix, default 1e-8 (< 0: test off) */
+  double eps_dual_infeasible;   /* Appendix, default 1e-8 (< 0: test off) */
 } ora_options;
+
+/* Infeasibility certificate test on ORIGINAL-space rays (reading 35;
+ * SPEC S:419-427).  Both rays are judged after scaling to unit
+ * 2-norm: d_y certifies primal infeasibility iff
+ *     q'd_y + sum_{l_j finite} l_j lam_j^+ - sum_{u_j finite} u_j lam_j^-  >  eps_p,
+ *     with lam = -K'd_y,  and  max( (d_y)_i^- for ">=" rows i,
+ *                                  lam_j^+ for l_j = -inf, lam_j^- for u_j = +inf ) <= eps_p
+ * (the Farkas alternative: K x >=/= q has no solution in the box); d_x certifies
+ * dual infeasibility iff c'd_x < -eps_d and
+ *     max( |(K d_x)_i| for "=" rows, (K d_x)_i^- for ">=" rows,
+ *          (d_x)_j^+ for u_j finite, (d_x)_j^- for l_j finite ) <= eps_d
+ * (a recession direction of the feasible set along which c'x decreases). */
+typedef struct {
+  int32_t primal_infeasible, dual_infeasible;
+  double norm_dy, dual_ray_objective, dual_ray_violation;    /* after / for the unit scaling */
+  double norm_dx, primal_ray_objective, primal_ray_violation;
+} ora_certificate;
 
 typedef struct {
   int32_t status, pad;
@@ -460,6 +480,81 @@ static void fill_result(const scaled_lp *S, const double *xs, const double *ys, 
   if (y_out) for (int64_t i = 0; i < S->m; ++i) y_out[i] = S->Dr[i] * ys[i];
 }
 
+/* The certificate test of reading 35 on original-space rays (see ora_certificate).
+ * dx (n), Kdx = K dx (m), dy (m), KTdy = K'dy (n); bounds / costs are original. */
+static void certificate_test(int64_t n, int64_t m, int64_t m1, const double *c, const double *q,
+                             const double *l, const double *u, const double *dx, const double *Kdx,
+                             const double *dy, const double *KTdy, double eps_p, double eps_d,
+                             ora_certificate *r) {
+  double sy = 0.0, sx = 0.0;
+  for (int64_t i = 0; i < m; ++i) sy += dy[i] * dy[i];
+  for (int64_t j = 0; j < n; ++j) sx += dx[j] * dx[j];
+  r->norm_dy = sqrt(sy);
+  r->norm_dx = sqrt(sx);
+  /* dual ray (primal infeasibility) */
+  double obj = 0.0, viol = 0.0;
+  for (int64_t i = 0; i < m; ++i) {
+    obj += q[i] * dy[i];
+    if (i < m1) viol = dmax(viol, dmax(-dy[i], 0.0));
+  }
+  for (int64_t j = 0; j < n; ++j) {
+    double lam = -KTdy[j], lp = dmax(lam, 0.0), lm = dmax(-lam, 0.0);
+    if (l[j] > -ORA_INF) obj += l[j] * lp; else viol = dmax(viol, lp);
+    if (u[j] < ORA_INF) obj -= u[j] * lm; else viol = dmax(viol, lm);
+  }
+  r->dual_ray_objective = r->norm_dy > 0.0 ? obj / r->norm_dy : 0.0;
+  r->dual_ray_violation = r->norm_dy > 0.0 ? viol / r->norm_dy : 0.0;
+  r->primal_infeasible = eps_p >= 0.0 && r->norm_dy > 0.0 && r->dual_ray_objective > eps_p &&
+                         r->dual_ray_violation <= eps_p;
+  /* primal ray (dual infeasibility) */
+  obj = 0.0; viol = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    obj += c[j] * dx[j];
+    if (u[j] < ORA_INF) viol = dmax(viol, dmax(dx[j], 0.0));
+    if (l[j] > -ORA_INF) viol = dmax(viol, dmax(-dx[j], 0.0));
+  }
+  for (int64_t i = 0; i < m; ++i) viol = dmax(viol, i < m1 ? dmax(-Kdx[i], 0.0) : fabs(Kdx[i]));
+  r->primal_ray_objective = r->norm_dx > 0.0 ? obj / r->norm_dx : 0.0;
+  r->primal_ray_violation = r->norm_dx > 0.0 ? viol / r->norm_dx : 0.0;
+  r->dual_infeasible = eps_d >= 0.0 && r->norm_dx > 0.0 && r->primal_ray_objective < -eps_d &&
+                       r->primal_ray_violation <= eps_d;
+}
+
+/* The candidate rays in original space (reading 35): d = z - z_b for the current
+ * iterate z = (x, y) and a base point z_b -- for r2HPDHG the epoch's Halpern anchor
+ * (= its restart point), for raPDHG the iterate before the last accepted step --
+ * unscaled (x = Dc x~, y = Dr y~), with the products from the cached ones:
+ * K d_x = (K~x~ - K~x~_b) / Dr, K'd_y = (K~'y~ - K~'y~_b) / Dc. */
+static void epoch_rays(const scaled_lp *S, const double *x, const double *y, const double *Kx,
+                       const double *KTy, const double *xr, const double *yr, const double *Kxr,
+                       const double *KTyr, double *dx, double *Kdx, double *dy, double *KTdy) {
+  for (int64_t j = 0; j < S->n; ++j) {
+    dx[j] = S->Dc[j] * (x[j] - xr[j]);
+    KTdy[j] = (KTy[j] - KTyr[j]) / S->Dc[j];
+  }
+  for (int64_t i = 0; i < S->m; ++i) {
+    dy[i] = S->Dr[i] * (y[i] - yr[i]);
+    Kdx[i] = (Kx[i] - Kxr[i]) / S->Dr[i];
+  }
+}
+
+/* Output for an infeasible status: the result fields describe the current
+ * iterate; x_out / y_out / lam_out hold the unit certificate rays d_x/|d_x|,
+ * d_y/|d_y| and -K'd_y/|d_y| (zero where a ray is zero). */
+static void fill_infeasible(const scaled_lp *S, const double *x, const double *y, const double *Kx,
+                            const double *KTy, const double *dx, const double *dy, const double *KTdy,
+                            const ora_certificate *cert, int32_t status, int64_t k, int64_t j,
+                            int64_t restarts, double omega, double eta, double *x_out, double *y_out,
+                            double *lam_out, ora_result *res) {
+  fill_result(S, x, y, Kx, KTy, status, k, j, restarts, omega, eta, NULL, NULL, NULL, res);
+  const double sx = cert->norm_dx > 0.0 ? cert->norm_dx : 1.0, sy = cert->norm_dy > 0.0 ? cert->norm_dy : 1.0;
+  for (int64_t jj = 0; jj < S->n; ++jj) {
+    if (x_out) x_out[jj] = dx[jj] / sx;
+    if (lam_out) lam_out[jj] = -KTdy[jj] / sy;
+  }
+  if (y_out) for (int64_t i = 0; i < S->m; ++i) y_out[i] = dy[i] / sy;
+}
+
 /* One solve on the scaled problem: contract steps 2-6. */
 static void solve_scaled(const scaled_lp *S, const ora_options *o, const double *x0, const double *y0,
                          double *x_out, double *y_out, double *lam_out, ora_result *res, ora_log *g) {
@@ -474,6 +569,10 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
   double *xa = malloc(bn), *KTya = malloc(bn), *ya = malloc(bm), *Kxa = malloc(bm);
   /* last restart point (for the primal weight) and scratch */
   double *xr = malloc(bn), *yr = malloc(bm), *tn = malloc(bn), *tm = malloc(bm);
+  /* infeasibility detection (reading 35): the rays, and for raPDHG the iterate
+     before the last accepted step with its products */
+  double *rdx = malloc(bn), *rKTdy = malloc(bn), *rdy = malloc(bm), *rKdx = malloc(bm);
+  double *xo = malloc(bn), *KTyo = malloc(bn), *yo = malloc(bm), *Kxo = malloc(bm);
 
   /* ---- Step 2: initialise (P:251 zero start; warm start P:249-267) ---- */
   double omega = 1.0;
@@ -542,6 +641,10 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
 
     /* ---- Step 4: commit the accepted step ---- */
     csr_spmv(&S->KT, yp, KTyp);                                   /* SpMV #2 */
+    if (!r2 && ((k + 1) % o->check_frequency == 0 || k + 1 == o->iteration_limit)) {
+      /* raPDHG's ray is the step about to be committed: keep its start point */
+      cpy(xo, x, n); cpy(yo, y, m); cpy(Kxo, Kx, m); cpy(KTyo, KTy, n);
+    }
     k += 1;
     double rP = 0.0;
     if (!r2) {
@@ -562,6 +665,23 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
 
     /* ---- Step 5: periodic check (every 64 iterations) ---- */
     if (k % o->check_frequency != 0 && k != o->iteration_limit) continue;
+    /* infeasibility ("termination, restart, and infeasibility detection";
+       reading 35): after the optimality tests, before the iteration limit */
+#define INFEASIBILITY_CHECK()                                                                        \
+    do {                                                                                             \
+      ora_certificate cert;                                                                          \
+      if (r2) epoch_rays(S, x, y, Kx, KTy, xa, ya, Kxa, KTya, rdx, rKdx, rdy, rKTdy);                \
+      else epoch_rays(S, x, y, Kx, KTy, xo, yo, Kxo, KTyo, rdx, rKdx, rdy, rKTdy);                   \
+      certificate_test(n, m, m1, S->c0, S->q0, S->l0, S->u0, rdx, rKdx, rdy, rKTdy,                  \
+                       o->eps_primal_infeasible, o->eps_dual_infeasible, &cert);                     \
+      if (cert.primal_infeasible || cert.dual_infeasible) {                                          \
+        log_check(g, k, 0.0, ref, last, 0, 3);                                                       \
+        fill_infeasible(S, x, y, Kx, KTy, rdx, rdy, rKTdy, &cert,                                    \
+                        cert.primal_infeasible ? ORA_PRIMAL_INFEASIBLE : ORA_DUAL_INFEASIBLE, k, j,  \
+                        restarts, omega, eta, x_out, y_out, lam_out, res);                           \
+        goto done;                                                                                   \
+      }                                                                                              \
+    } while (0)
     const double *cx, *cy, *cKx, *cKTy;   /* the restart candidate */
     int32_t pass = 0;
     if (!r2) {
@@ -580,6 +700,7 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
         fill_result(S, x, y, Kx, KTy, ORA_OPTIMAL, k, j, restarts, omega, eta, x_out, y_out, lam_out, res);
         goto done;
       }
+      INFEASIBILITY_CHECK();
       if (k == o->iteration_limit) {
         int use_avg = ora_rel_kkt(&ka, S->nq0, S->nc0) < ora_rel_kkt(&kc, S->nq0, S->nc0);
         log_check(g, k, 0.0, ref, last, 0, 0);
@@ -599,6 +720,7 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
         fill_result(S, xp, yp, Kxp, KTyp, ORA_OPTIMAL, k, j, restarts, omega, eta, x_out, y_out, lam_out, res);
         goto done;
       }
+      INFEASIBILITY_CHECK();
       if (k == o->iteration_limit) {
         log_check(g, k, rP, ref, last, 0, 0);
         fill_result(S, xp, yp, Kxp, KTyp, ORA_ITERATION_LIMIT, k, j, restarts, omega, eta, x_out, y_out, lam_out, res);
@@ -627,6 +749,7 @@ done:
   (void)ref_set;
   free(x); free(KTy); free(y); free(Kx); free(xp); free(KTyp); free(yp); free(Kxp);
   free(xa); free(KTya); free(ya); free(Kxa); free(xr); free(yr); free(tn); free(tm);
+  free(rdx); free(rKTdy); free(rdy); free(rKdx); free(xo); free(KTyo); free(yo); free(Kxo);
 }
 
 /* ------------------------------------------------------------ exports ---- */
@@ -638,6 +761,8 @@ void ora_default_options(ora_options *o) {
   o->algorithm = ORA_R2HPDHG;
   o->ruiz_iters = 10; o->pock_chambolle = 1;     /* contract c.3 #3 */
   o->step_rule = 0; o->power_iters = 200;
+  o->eps_primal_infeasible = 1e-8;               /* Appendix */
+  o->eps_dual_infeasible = 1e-8;                 /* Appendix */
 }
 
 int ora_num_threads(void) {
@@ -802,4 +927,16 @@ int ora_spectral_norm(const ora_problem *p, int32_t iters, double *sigma) {
   *sigma = power_sigma(&K, &KT, iters);
   csr_free(&KT);
   return ORA_OK;
+}
+
+/* The certificate test of reading 35 on user-given original-space rays (d_x, d_y),
+ * with products from the unscaled K (pins: SPEC S:425-426 Farkas examples). */
+int ora_certificate_test(const ora_problem *p, const double *dx, const double *dy, double eps_p, double eps_d,
+                         ora_certificate *out) {
+  int64_t n = p->n, m = p->m1 + p->m2;
+  double *Kdx = malloc((size_t)(m ? m : 1) * sizeof(double)), *KTdy = malloc((size_t)n * sizeof(double));
+  int e = ora_spmv_pair(p, dx, Kdx, dy, KTdy);
+  if (!e) certificate_test(n, m, p->m1, p->c, p->q, p->l, p->u, dx, Kdx, dy, KTdy, eps_p, eps_d, out);
+  free(Kdx); free(KTdy);
+  return e;
 }

@@ -19,7 +19,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
-OPTIMAL, ITERATION_LIMIT, NUMERICAL_ERROR = 1, 2, 3
+OPTIMAL, ITERATION_LIMIT, NUMERICAL_ERROR, PRIMAL_INFEASIBLE, DUAL_INFEASIBLE = 1, 2, 3, 4, 5
 RAPDHG, R2HPDHG = 0, 1
 
 
@@ -43,7 +43,15 @@ class Options(C.Structure):
     _fields_ = [("eps_abs", C.c_double), ("eps_rel", C.c_double), ("iteration_limit", C.c_int64),
                 ("check_frequency", C.c_int32), ("algorithm", C.c_int32),
                 ("ruiz_iters", C.c_int32), ("pock_chambolle", C.c_int32),
-                ("step_rule", C.c_int32), ("power_iters", C.c_int32)]
+                ("step_rule", C.c_int32), ("power_iters", C.c_int32),
+                ("eps_primal_infeasible", C.c_double), ("eps_dual_infeasible", C.c_double)]
+
+
+class Certificate(C.Structure):
+    _fields_ = [("primal_infeasible", C.c_int32), ("dual_infeasible", C.c_int32),
+                ("norm_dy", C.c_double), ("dual_ray_objective", C.c_double), ("dual_ray_violation", C.c_double),
+                ("norm_dx", C.c_double), ("primal_ray_objective", C.c_double),
+                ("primal_ray_violation", C.c_double)]
 
 
 class Result(C.Structure):
@@ -107,6 +115,8 @@ def lib():
             L.ora_num_threads.restype = C.c_int
             L.ora_set_threads.argtypes = [C.c_int]
             L.ora_spectral_norm.argtypes = [P(Problem), C.c_int32, P(C.c_double)]
+            L.ora_certificate_test.argtypes = [P(Problem), C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                                               P(Certificate)]
             _lib = L
     return _lib
 
@@ -134,7 +144,8 @@ class _Bound:
 
 
 def options(algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, check_frequency=64,
-            ruiz_iters=10, pock_chambolle=1, step_rule=0, power_iters=200):
+            ruiz_iters=10, pock_chambolle=1, step_rule=0, power_iters=200, eps_primal_infeasible=1e-8,
+            eps_dual_infeasible=1e-8):
     o = Options()
     lib().ora_default_options(C.byref(o))
     o.algorithm = R2HPDHG if algorithm in ("r2", "r2hpdhg", R2HPDHG) else RAPDHG
@@ -145,6 +156,7 @@ def options(algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, ch
     o.ruiz_iters, o.pock_chambolle = ruiz_iters, pock_chambolle
     o.step_rule = 1 if step_rule in (1, "constant") else 0
     o.power_iters = power_iters
+    o.eps_primal_infeasible, o.eps_dual_infeasible = eps_primal_infeasible, eps_dual_infeasible
     return o
 
 
@@ -154,12 +166,13 @@ def validate(lp) -> int:
 
 
 def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, x0=None, y0=None,
-          check_frequency=64, log_capacity=0, step_rule=0):
+          check_frequency=64, log_capacity=0, step_rule=0, eps_primal_infeasible=1e-8, eps_dual_infeasible=1e-8):
     """Full solve (contract steps 0-6).  Returns a dict with x, y, lam, the
     result fields, and (if log_capacity) the attempt/check decision logs."""
     b = _Bound(lp)
     m = lp.m1 + lp.m2
-    o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule)
+    o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule,
+                eps_primal_infeasible=eps_primal_infeasible, eps_dual_infeasible=eps_dual_infeasible)
     x = np.zeros(lp.n)
     y = np.zeros(m)
     lam = np.zeros(lp.n)
@@ -185,14 +198,16 @@ def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, 
 
 
 def solve_batch(lp, C_=None, Q=None, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None,
-                X0=None, Y0=None, check_frequency=64, threads=None, step_rule=0):
+                X0=None, Y0=None, check_frequency=64, threads=None, step_rule=0, eps_primal_infeasible=1e-8,
+                eps_dual_infeasible=1e-8):
     """Batch solve sharing K, l, u; one instance per OpenMP thread."""
     b = _Bound(lp)
     m = lp.m1 + lp.m2
     Cm = None if C_ is None else _f64(C_)
     Qm = None if Q is None else _f64(Q)
     B = Cm.shape[0] if Cm is not None else Qm.shape[0]
-    o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule)
+    o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule,
+                eps_primal_infeasible=eps_primal_infeasible, eps_dual_infeasible=eps_dual_infeasible)
     X = np.zeros((B, lp.n))
     Y = np.zeros((B, m))
     res = (Result * B)()
@@ -333,3 +348,15 @@ def spectral_norm(lp, iters=200):
     s = C.c_double()
     lib().ora_spectral_norm(C.byref(b.s), iters, C.byref(s))
     return s.value
+
+
+def certificate_test(lp, dx, dy, eps_primal_infeasible=1e-8, eps_dual_infeasible=1e-8):
+    """Reading 35's certificate test on original-space rays (d_x, d_y)."""
+    b = _Bound(lp)
+    dxa, dya = _f64(dx), _f64(dy)
+    r = Certificate()
+    e = lib().ora_certificate_test(C.byref(b.s), dxa.ctypes.data, dya.ctypes.data if dya.size else None,
+                                   eps_primal_infeasible, eps_dual_infeasible, C.byref(r))
+    if e != 0:
+        raise ValueError(f"oracle error {e}")
+    return {f: getattr(r, f) for f, _ in r._fields_}
