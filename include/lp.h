@@ -63,9 +63,23 @@ enum lp_status {
   LP_OPTIMAL = 1,          /* relative KKT termination test passed */
   LP_ITERATION_LIMIT = 2,  /* iteration_limit accepted steps reached */
   LP_NUMERICAL_ERROR = 3,  /* 100 consecutive line-search rejections */
-  LP_PRIMAL_INFEASIBLE = 4,/* reserved */
-  LP_DUAL_INFEASIBLE = 5   /* reserved */
+  LP_PRIMAL_INFEASIBLE = 4,/* a dual ray certifies that no x satisfies the rows and bounds */
+  LP_DUAL_INFEASIBLE = 5   /* a primal ray certifies that c'x is unbounded below */
 };
+/* Infeasibility detection ("termination, restart, and infeasibility
+ * detection" every 64 iterations; tolerances P:530-531; reading 35).
+ * At every check, after the optimality test and before the iteration limit, the
+ * candidate rays d = z - z_b in ORIGINAL space -- z_b the iterate before the
+ * last accepted step (raPDHG) or the epoch's Halpern anchor (r2HPDHG) -- are
+ * scaled to unit 2-norm and tested:
+ *   PRIMAL_INFEASIBLE: q'd_y + sum_{l finite} l lam^+ - sum_{u finite} u lam^- > eps_pi with
+ *     lam = -K'd_y, and max((d_y)_G^-, lam^+ on l = -inf, lam^- on u = +inf) <= eps_pi;
+ *   DUAL_INFEASIBLE: c'd_x < -eps_di and max(|A d_x|, (G d_x)^-, (d_x)^+ on finite u,
+ *     (d_x)^- on finite l) <= eps_di.
+ * On either status lp_get_solution returns the unit rays: x = d_x/|d_x|,
+ * y = d_y/|d_y|, reduced_costs = -K'd_y/|d_y| (a zero ray is returned as 0); the
+ * lp_result objectives / residuals describe the current iterate.  A negative
+ * tolerance switches that test off. */
 
 enum lp_algorithm { LP_RAPDHG = 0, LP_R2HPDHG = 1 };
 
@@ -106,8 +120,8 @@ typedef struct {
 typedef struct {
   double eps_abs;               /* 1e-4 */
   double eps_rel;               /* 1e-4 */
-  double eps_primal_infeasible; /* 1e-8, reserved */
-  double eps_dual_infeasible;   /* 1e-8, reserved */
+  double eps_primal_infeasible; /* 1e-8; < 0 disables the test */
+  double eps_dual_infeasible;   /* 1e-8; < 0 disables the test */
   double eps_feas_polish;       /* 1e-6, reserved */
   int64_t iteration_limit;      /* INT64_MAX; accepted steps */
   int32_t check_frequency;      /* 64 */

@@ -327,7 +327,8 @@ def random_small_lp(seed: int, n: int = 4, m1: int = 2, m2: int = 1, box: float 
 
 # ----------------------------------------------------------- G-INFEAS --
 
-def g_infeasible(kind: str, seed: int, m1: int = 12, m2: int = 4, n: int = 24, box: float = 5.0) -> LP:
+def g_infeasible(kind: str, seed: int, m1: int = 12, m2: int = 4, n: int = 24, box: float = 5.0,
+                 density: float = 0.4, dense: bool = False) -> LP:
     """Small dense LPs infeasible by construction (SURVEY §8(f) row 1 test inputs).
 
     kind="primal": a feasible random LP (random interior point x0) plus one more
@@ -338,8 +339,8 @@ def g_infeasible(kind: str, seed: int, m1: int = 12, m2: int = 4, n: int = 24, b
     u_j = +inf and c_j < 0, so x0 + t e_j stays feasible for every t >= 0 while
     c'x decreases without bound (the LP is unbounded, its dual infeasible)."""
     rng = np.random.default_rng(seed)
-    G = rng.normal(size=(m1, n)) * (rng.random((m1, n)) < 0.4)
-    A = rng.normal(size=(m2, n)) * (rng.random((m2, n)) < 0.4)
+    G = rng.normal(size=(m1, n)) * (rng.random((m1, n)) < density)
+    A = rng.normal(size=(m2, n)) * (rng.random((m2, n)) < density)
     l = -rng.uniform(0.5, box, size=n)
     u = rng.uniform(0.5, box, size=n)
     x0 = rng.uniform(l, u)
@@ -361,6 +362,6 @@ def g_infeasible(kind: str, seed: int, m1: int = 12, m2: int = 4, n: int = 24, b
         h = np.append(h, -(y @ h) + rng.uniform(0.5, 2.0))
     elif kind != "dual":
         raise ValueError(kind)
-    lp = stack(c, G=G, h=h, A=A, b=b, l=l, u=u)
+    lp = stack(c, G=G, h=h, A=A, b=b, l=l, u=u, dense=dense)
     lp.meta = dict(generator="G-INFEAS", kind=kind, seed=seed)
     return lp

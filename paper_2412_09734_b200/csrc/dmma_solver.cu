@@ -57,7 +57,7 @@ struct DmmaParams {
   const double *C0, *Q0, *X0, *Y0;
   int64_t cstride, qstride;
   const double *kmax, *sigma, *tab;
-  double eps_abs, eps_rel;
+  double eps_abs, eps_rel, eps_pi, eps_di;
   int64_t iter_limit;
   int32_t check_freq, alg, const_step;
   int64_t batch;
@@ -72,8 +72,9 @@ struct DmmaParams {
 // per-instance scalar state (identical copy in every CTA of the cluster)
 struct Inst {
   double omega, eta, W, ref, last, theta, ha, hb, rP, nc0, nq0, metric, dx2c, dy2c, eta_used, M, I;
+  double ray_ny, ray_nx;  // infeasibility rays' norms (reading 35)
   long long k, j, k_in, restarts;
-  int rejects, status, pending, done, check, outsel, csel, valid;
+  int rejects, status, pending, done, check, outsel, csel, valid, cert, rays;
 };
 
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
@@ -171,7 +172,8 @@ __device__ __forceinline__ void gemm2(const Smem &S, int np, int mp) {
 }
 
 // Per-instance partial sums: v[s][0..V) accumulated per thread -> S.part[s][0..V) (fixed order).
-template <int V>
+// MX: bit k set = value k is max-reduced (non-negative), else summed.
+template <int V, unsigned MX = 0u>
 __device__ __forceinline__ void cta_partials(double (&v)[kS][V], const Smem &S) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -180,14 +182,21 @@ __device__ __forceinline__ void cta_partials(double (&v)[kS][V], const Smem &S) 
     for (int k = 0; k < V; ++k) {
       double t = v[s][k];
 #pragma unroll
-      for (int off = 16; off; off >>= 1) t += __shfl_xor_sync(FULL, t, off);
+      for (int off = 16; off; off >>= 1) {
+        const double o = __shfl_xor_sync(FULL, t, off);
+        t = ((MX >> k) & 1u) ? fmax(t, o) : t + o;
+      }
       if (lane == 0) S.wpart[(w * kS + s) * 24 + k] = t;
     }
   __syncthreads();
   for (int t = threadIdx.x; t < kS * V; t += kThreads) {
     const int s = t / V, k = t % V;
+    const bool mx = (MX >> k) & 1u;
     double a = 0.0;
-    for (int ww = 0; ww < kThreads / 32; ++ww) a += S.wpart[(ww * kS + s) * 24 + k];
+    for (int ww = 0; ww < kThreads / 32; ++ww) {
+      const double o = S.wpart[(ww * kS + s) * 24 + k];
+      a = mx ? fmax(a, o) : a + o;
+    }
     S.part[s * 24 + k] = a;
   }
 }
@@ -226,13 +235,17 @@ __device__ __forceinline__ void attempt_partials(double dxe, double dxo, double 
 }
 
 // After a cluster barrier: tot[s][k] = sum over cluster ranks (in rank order) of part.
-template <int CL, int V>
+template <int CL, int V, unsigned MX = 0u>
 __device__ __forceinline__ void cluster_totals(cg::cluster_group &cl, const Smem &S, double *tot /* kS*24 */) {
   for (int t = threadIdx.x; t < kS * V; t += kThreads) {
     const int s = t / V, k = t % V;
+    const bool mx = (MX >> k) & 1u;
     double a = 0.0;
 #pragma unroll
-    for (int c = 0; c < CL; ++c) a += cl.map_shared_rank(S.part, c)[s * 24 + k];
+    for (int c = 0; c < CL; ++c) {
+      const double o = cl.map_shared_rank(S.part, c)[s * 24 + k];
+      a = mx ? fmax(a, o) : a + o;
+    }
     tot[s * 24 + k] = a;
   }
   __syncthreads();
@@ -493,8 +506,12 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       if (!any_check) continue;
 
       // ====================== check (step 5) for the flagged instances ======================
-      // commit-only, both sides, for every pending instance; K~'y' from GEMM1
+      // commit-only, both sides, for every pending instance; K~'y' from GEMM1.
+      // Infeasibility rays (reading 35) of the checked instances: raPDHG z - (pre-step point),
+      // whose pre-step values are parked in xp / KTyp / yp / Kxp (free until the next attempt),
+      // r2HPDHG z - (Halpern anchor xa ...).
       double vc[kS][6] = {};
+      double vq[kS][6] = {};  // |dy|^2, |dx|^2, dual-ray obj, c'dx | viol_y, viol_x (max)
       gemm1(S, np, mp, [&](int jj, int s, double kty) {
         const Inst &I = S.inst[s];
         if (jj >= jn || I.done || !I.pending) return;
@@ -502,14 +519,26 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         const int j = j0 + jj;
         const int64_t o = b * n + j;
         const double xpv = P.xp[o];
-        P.KTyp[o] = kty;
         if (!r2) {
+          const double xo = P.x[o], kto = P.KTy[o];
           P.xa[o] += I.theta * (xpv - P.xa[o]);
           P.x[o] = xpv; P.KTy[o] = kty;
+          P.xp[o] = xo; P.KTyp[o] = kto;
+          if (I.check) {
+            CertAcc acc;
+            cert_col(acc, P.Dc[j], xpv, xo, kty, kto, P.C0[b * P.cstride + j], P.l0[j], P.u0[j]);
+            vq[s][0] += acc.sy; vq[s][1] += acc.sx; vq[s][2] += acc.oy; vq[s][3] += acc.ox;
+            vq[s][4] = fmax(vq[s][4], acc.vy); vq[s][5] = fmax(vq[s][5], acc.vx);
+          }
         } else {
+          P.KTyp[o] = kty;
           P.x[o] = I.ha * (2.0 * xpv - P.x[o]) + I.hb * P.xa[o];
           P.KTy[o] = I.ha * (2.0 * kty - P.KTy[o]) + I.hb * P.KTya[o];
           if (I.check) {
+            CertAcc acc;
+            cert_col(acc, P.Dc[j], P.x[o], P.xa[o], P.KTy[o], P.KTya[o], P.C0[b * P.cstride + j], P.l0[j], P.u0[j]);
+            vq[s][0] += acc.sy; vq[s][1] += acc.sx; vq[s][2] += acc.oy; vq[s][3] += acc.ox;
+            vq[s][4] = fmax(vq[s][4], acc.vy); vq[s][5] = fmax(vq[s][5], acc.vx);
             kcol(vc[s], true, P.Dc[j], xpv, kty, P.C0[b * P.cstride + j], P.cs[o], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
             const double d = xpv - P.xr[o];
             vc[s][4] += d * d;
@@ -523,13 +552,26 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         const int64_t b = b0 + s;
         const int64_t o = b * m + i;
         const double ypv = P.yp[o], kxp = P.Kxp[o];
+        const double q0i = P.Q0[b * P.qstride + i];
         if (!r2) {
+          const double yo = P.y[o], kxo = P.Kx[o];
           P.ya[o] += I.theta * (ypv - P.ya[o]);
           P.y[o] = ypv; P.Kx[o] = kxp;
+          P.yp[o] = yo; P.Kxp[o] = kxo;
+          if (I.check) {
+            CertAcc acc;
+            cert_row(acc, i < m1, P.Dr[i], ypv, yo, kxp, kxo, q0i);
+            vq[s][0] += acc.sy; vq[s][2] += acc.oy;
+            vq[s][4] = fmax(vq[s][4], acc.vy); vq[s][5] = fmax(vq[s][5], acc.vx);
+          }
         } else {
           P.y[o] = I.ha * (2.0 * ypv - P.y[o]) + I.hb * P.ya[o];
           P.Kx[o] = I.ha * (2.0 * kxp - P.Kx[o]) + I.hb * P.Kxa[o];
           if (I.check) {
+            CertAcc acc;
+            cert_row(acc, i < m1, P.Dr[i], P.y[o], P.ya[o], P.Kx[o], P.Kxa[o], q0i);
+            vq[s][0] += acc.sy; vq[s][2] += acc.oy;
+            vq[s][4] = fmax(vq[s][4], acc.vy); vq[s][5] = fmax(vq[s][5], acc.vx);
             krow(vc[s], true, i < m1, P.Dr[i], ypv, kxp, P.Q0[b * P.qstride + i], P.qs[o]);
             const double d = ypv - P.yr[o];
             vc[s][5] += d * d;
@@ -539,6 +581,21 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       __syncthreads();
       if (tid < kS) S.inst[tid].pending = 0;
       cl.sync();  // every rank's commits (global state) visible before they are read across slices
+      // certificate totals -> per-instance verdict (applied after the optimality tests)
+      S.part = (S.part == S.part_a) ? S.part_b : S.part_a;
+      cta_partials<6, (3u << 4)>(vq, S);
+      cl.sync();
+      cluster_totals<CL, 6, (3u << 4)>(cl, S, tot);
+      if (tid < kS) {
+        Inst &I = S.inst[tid];
+        if (I.check) {
+          const double *t6 = tot + tid * 24;
+          CertAcc t;
+          t.sy = t6[0]; t.sx = t6[1]; t.oy = t6[2]; t.ox = t6[3]; t.vy = t6[4]; t.vx = t6[5];
+          I.cert = cert_decide(t, P.eps_pi, P.eps_di, I.ray_ny, I.ray_nx);
+        }
+      }
+      __syncthreads();
       if (r2) {
         S.part = (S.part == S.part_a) ? S.part_b : S.part_a;
         cta_partials<6>(vc, S);
@@ -550,6 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
             const double *t6 = tot + tid * 24;
             const K5 kw = mk5(t6);
             if (pass5(kw, I.nq0, I.nc0, P.eps_abs, P.eps_rel)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 1; }
+            else if (I.cert) { I.status = I.cert; I.done = 1; I.outsel = 0; I.rays = 1; }
             else if (I.k == P.iter_limit) { I.status = LP_ITERATION_LIMIT; I.done = 1; I.outsel = 1; }
             else { I.metric = I.rP; I.dx2c = t6[4]; I.dy2c = t6[5]; I.csel = 1; }
           }
@@ -616,6 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
             const K5 ka = mk5(t + 0), kc = mk5(t + 4);
             if (pass5(ka, I.nq0, I.nc0, P.eps_abs, P.eps_rel)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 1; }
             else if (pass5(kc, I.nq0, I.nc0, P.eps_abs, P.eps_rel)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 0; }
+            else if (I.cert) { I.status = I.cert; I.done = 1; I.outsel = 0; I.rays = 1; }
             else if (I.k == P.iter_limit) {
               I.status = LP_ITERATION_LIMIT; I.done = 1;
               I.outsel = rel5(ka, I.nq0, I.nc0) < rel5(kc, I.nq0, I.nc0) ? 1 : 0;
@@ -696,8 +755,14 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         const double kt = I.outsel ? (r2 ? P.KTyp[o] : P.KTya[o]) : P.KTy[o];
         const double dc = P.Dc[j], c0 = P.C0[b * P.cstride + j];
         kcol(v[s], true, dc, xs, kt, c0, P.cs[o], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
-        P.X[o] = dc * xs;
-        P.L[o] = c0 - kt / dc;
+        if (I.rays) {  // infeasible: unit rays against the base (r2: anchor; ra: parked pre-step point)
+          const double xb = r2 ? P.xa[o] : P.xp[o], ktb = r2 ? P.KTya[o] : P.KTyp[o];
+          P.X[o] = dc * (xs - xb) / I.ray_nx;
+          P.L[o] = -((kt - ktb) / dc) / I.ray_ny;
+        } else {
+          P.X[o] = dc * xs;
+          P.L[o] = c0 - kt / dc;
+        }
       }
       for (int t = tid; t < in_ * kS; t += kThreads) {
         const int s = t / in_, ii = t % in_, i = i0 + ii;
@@ -709,7 +774,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         const double kx = I.outsel ? (r2 ? P.Kxp[o] : P.Kxa[o]) : P.Kx[o];
         const double dr = P.Dr[i];
         krow(v[s], true, i < m1, dr, ys, kx, P.Q0[b * P.qstride + i], P.qs[o]);
-        P.Y[o] = dr * ys;
+        if (I.rays) P.Y[o] = dr * (ys - (r2 ? P.ya[o] : P.yp[o])) / I.ray_ny;
+        else P.Y[o] = dr * ys;
       }
       S.part = (S.part == S.part_a) ? S.part_b : S.part_a;  // double-buffered (see grid_solver.cu)
       cta_partials<4>(v, S);
@@ -788,6 +854,7 @@ int dmma_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
     P.kmax = D.kmax; P.sigma = D.sigma; P.tab = D.tab; P.const_step = o.step_rule == LP_STEP_CONSTANT;
     P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
     P.check_freq = o.check_frequency; P.alg = o.algorithm;
+    P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
     P.batch = L.batch; P.queue = queue;
     const size_t BN = (size_t)L.batch * n, BM = (size_t)L.batch * m;
     double *w = work;

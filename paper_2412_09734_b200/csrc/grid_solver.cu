@@ -34,7 +34,7 @@ namespace mpax {
 
 namespace {
 
-constexpr int kNP = 20;      // max partial sums per phase
+constexpr int kNP = 26;      // max partial values per phase (raPDHG check: 20 KKT / distance + 6 certificate)
 constexpr int kBS = 512;     // threads per CTA
 
 struct GridParams {
@@ -45,7 +45,7 @@ struct GridParams {
   double *x, *KTy, *xp, *KTyp, *xa, *KTya, *xr;   // n-side
   double *y, *Kx, *yp, *Kxp, *ya, *Kxa, *yr;      // m-side
   double *part;                                   // gridDim.x x kNP
-  double eps_abs, eps_rel;
+  double eps_abs, eps_rel, eps_pi, eps_di;
   int64_t iter_limit;
   int32_t check_freq, alg, gk, gkt, const_step;
   double *X, *Y, *L;
@@ -146,20 +146,25 @@ __device__ __forceinline__ double row_dot(int64_t r, bool valid, int G, int gl, 
   return s;
 }
 
-template <int V>
+// MX: bit k set = value k is max-reduced (non-negative violations), else summed.
+template <int V, unsigned MX = 0u>
 __device__ __forceinline__ void block_partials(double (&v)[V], double *part, double (*s_red)[kNP]) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < V; ++k) {
     double s = v[k];
 #pragma unroll
-    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    for (int off = 16; off; off >>= 1) {
+      const double o = __shfl_xor_sync(FULL, s, off);
+      s = ((MX >> k) & 1u) ? fmax(s, o) : s + o;
+    }
     if (lane == 0) s_red[wid][k] = s;
   }
   __syncthreads();
   if (threadIdx.x < V) {
+    const bool mx = (MX >> threadIdx.x) & 1u;
     double s = 0.0;
-    for (int w = 0; w < kBS / 32; ++w) s += s_red[w][threadIdx.x];
+    for (int w = 0; w < kBS / 32; ++w) s = mx ? fmax(s, s_red[w][threadIdx.x]) : s + s_red[w][threadIdx.x];
     part[(int64_t)blockIdx.x * kNP + threadIdx.x] = s;
   }
 }
@@ -167,11 +172,19 @@ __device__ __forceinline__ void block_partials(double (&v)[V], double *part, dou
 // After a grid barrier: every CTA sums the per-CTA partials in the same fixed order
 // (warp k reduces value k: lanes take CTAs b = lane + 32i into 4 interleaved
 // accumulators, then a butterfly; identical code and data in every CTA).
-template <int V>
+template <int V, unsigned MX = 0u>
 __device__ __forceinline__ void grid_totals(double (&t)[V], const double *part, double *s_tot) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nb = (int)gridDim.x;
   for (int k = w; k < V; k += kBS / 32) {
+    if ((MX >> k) & 1u) {  // max of non-negative partials
+      double s = 0.0;
+      for (int b = lane; b < nb; b += 32) s = fmax(s, __ldcg(part + (int64_t)b * kNP + k));
+#pragma unroll
+      for (int off = 16; off; off >>= 1) s = fmax(s, __shfl_xor_sync(FULL, s, off));
+      if (lane == 0) s_tot[k] = s;
+      continue;
+    }
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int b = lane;
     for (; b + 96 < nb; b += 128) {
@@ -291,6 +304,19 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   // returned candidate (pointers)
   const double *ox = x, *oy = y, *oKx = Kx, *oKTy = KTy;
   bool done = false;
+  // infeasibility (reading 35): t = reduced (|dy|^2, |dx|^2, dual-ray obj, c'dx, viol_y, viol_x);
+  // on a certificate the status is set and the output writes the rays against (bx, by, bKTy)
+  const double *bx = nullptr, *by = nullptr, *bKTy = nullptr;
+  double ray_ny = 1.0, ray_nx = 1.0;
+  auto certify = [&](const double *t, const double *xb, const double *yb, const double *KTyb) {
+    CertAcc tot;
+    tot.sy = t[0]; tot.sx = t[1]; tot.oy = t[2]; tot.ox = t[3]; tot.vy = t[4]; tot.vx = t[5];
+    const int st = cert_decide(tot, P.eps_pi, P.eps_di, ray_ny, ray_nx);
+    if (!st) return false;
+    status = st; ox = x; oy = y; oKx = Kx; oKTy = KTy;
+    bx = xb; by = yb; bKTy = KTyb;
+    return true;
+  };
 
   while (!done) {
     // ================= phase A: [commit n-side] + primal step =================
@@ -422,8 +448,12 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     if (k % P.check_freq != 0 && k != P.iter_limit) { pending = true; continue; }
 
     // ================= check: commit-only phase (both sides) =================
+    // infeasibility rays (reading 35): r2HPDHG z - anchor here, raPDHG z - (pre-step point) below
     {
-      double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      double v[12];
+#pragma unroll
+      for (int q = 0; q < 12; ++q) v[q] = 0.0;
+      CertAcc acc;
       for (int it = 0; it < col_iters; ++it) {
         const int j = it * ngrpt + grpt;
         const bool ok = j < n;
@@ -439,6 +469,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
             kkt_col(v, true, dc, xp[j], s, P.c0[j], cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
             const double d = xp[j] - xr[j];
             v[4] += d * d;
+            cert_col(acc, dc, x[j], xa[j], KTy[j], KTya[j], P.c0[j], P.l0[j], P.u0[j]);
           }
         }
       }
@@ -452,6 +483,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           kkt_row(v, true, i, m1, P.Dr[i], ypi, kxp, P.q0[i], qs[i]);
           const double d = ypi - yr[i];
           v[5] += d * d;
+          cert_row(acc, i < m1, P.Dr[i], y[i], ya[i], Kx[i], Kxa[i], P.q0[i]);
         }
       }
       if (!r2) {
@@ -460,7 +492,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         t = y; y = yp; yp = t;
         t = Kx; Kx = Kxp; Kxp = t;
       }
-      if (r2) block_partials<6>(v, next_part(), s_red);
+      v[6] = acc.sy; v[7] = acc.sx; v[8] = acc.oy; v[9] = acc.ox; v[10] = acc.vy; v[11] = acc.vx;
+      if (r2) block_partials<12, (3u << 10)>(v, next_part(), s_red);
     }
     grid.sync();
     const double *cx, *cy, *cKx, *cKTy;
@@ -470,6 +503,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       double v[kNP];
 #pragma unroll
       for (int q = 0; q < kNP; ++q) v[q] = 0.0;
+      CertAcc acc;
       for (int it = 0; it < row_iters; ++it) {
         const int i = it * ngrp + grp;
         const bool ok = i < m;
@@ -484,6 +518,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           const double da = yai - yr[i], dcur = yi - yr[i];
           v[17] += da * da;
           v[19] += dcur * dcur;
+          cert_row(acc, i < m1, dr, yi, yp[i], kxi, Kxp[i], q0);   // yp, Kxp: the pre-step point
         }
       }
       for (int it = 0; it < col_iters; ++it) {
@@ -501,15 +536,18 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           const double da = xaj - xr[j], dcur = xj - xr[j];
           v[16] += da * da;
           v[18] += dcur * dcur;
+          cert_col(acc, dc, xj, xp[j], ktj, KTyp[j], c0, l0, u0);
         }
       }
-      block_partials<kNP>(v, next_part(), s_red);
+      v[20] = acc.sy; v[21] = acc.sx; v[22] = acc.oy; v[23] = acc.ox; v[24] = acc.vy; v[25] = acc.vx;
+      block_partials<kNP, (3u << 24)>(v, next_part(), s_red);
       grid.sync();
       double t[kNP];
-      grid_totals<kNP>(t, cur_part(), s_tot);
+      grid_totals<kNP, (3u << 24)>(t, cur_part(), s_tot);
       const KktT ka = mk(t + 0), kc = mk(t + 4);
       if (pass(ka, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; break; }
       if (pass(kc, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
+      if (certify(t + 20, xp, yp, KTyp)) break;
       if (k == P.iter_limit) {
         status = LP_ITERATION_LIMIT;
         if (relk(ka, nq0, nc0) < relk(kc, nq0, nc0)) { ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; }
@@ -522,10 +560,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       if (e_a < e_c) { cx = xa; cy = ya; cKx = Kxa; cKTy = KTya; metric = e_a; dx2 = t[16]; dy2 = t[17]; }
       else { cx = x; cy = y; cKx = Kx; cKTy = KTy; metric = e_c; dx2 = t[18]; dy2 = t[19]; }
     } else {
-      double t[6];
-      grid_totals<6>(t, cur_part(), s_tot);
+      double t[12];
+      grid_totals<12, (3u << 10)>(t, cur_part(), s_tot);
       const KktT kw = mk(t);
       if (pass(kw, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
+      if (certify(t + 6, xa, ya, KTya)) break;
       if (k == P.iter_limit) { status = LP_ITERATION_LIMIT; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
       cx = xp; cy = yp; cKx = Kxp; cKTy = KTyp; metric = rP; dx2 = t[4]; dy2 = t[5];
     }
@@ -556,13 +595,18 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     for (int j = gtid; j < n; j += gthreads) {
       const double dc = P.Dc[j], xs = ox[j], kt = oKTy[j];
       kkt_col(v, true, dc, xs, kt, P.c0[j], cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
-      P.X[j] = dc * xs;
-      P.L[j] = P.c0[j] - kt / dc;
+      if (bx) {  // infeasible: the unit rays (reading 35)
+        P.X[j] = dc * (xs - bx[j]) / ray_nx;
+        P.L[j] = -((kt - bKTy[j]) / dc) / ray_ny;
+      } else {
+        P.X[j] = dc * xs;
+        P.L[j] = P.c0[j] - kt / dc;
+      }
     }
     for (int i = gtid; i < m; i += gthreads) {
       const double dr = P.Dr[i];
       kkt_row(v, true, i, m1, dr, oy[i], oKx[i], P.q0[i], qs[i]);
-      P.Y[i] = dr * oy[i];
+      P.Y[i] = bx ? dr * (oy[i] - by[i]) / ray_ny : dr * oy[i];
     }
     block_partials<4>(v, next_part(), s_red);
   }
@@ -634,6 +678,7 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   P.yr = w; w += m;
   P.part = w;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
+  P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
   P.check_freq = o.check_frequency; P.alg = o.algorithm;
   // thread per row for short rows (all lanes do useful epilogue work), 8 or 32 lanes for long rows
   // G ~ mean row length / 4 (measured on B200 for this persistent kernel: 4 lanes per 20-entry

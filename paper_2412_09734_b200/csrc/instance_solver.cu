@@ -42,7 +42,7 @@ struct InstParams {
   const double *C0, *Q0, *X0, *Y0;
   int64_t cstride, qstride;
   const double *kmax, *sigma, *tab;
-  double eps_abs, eps_rel;
+  double eps_abs, eps_rel, eps_pi, eps_di;
   int64_t iter_limit;
   int32_t check_freq, alg, const_step;
   int64_t batch;
@@ -83,6 +83,35 @@ __device__ __forceinline__ void breduce(double (&v)[V], double *red) {
       double s = red[k];
 #pragma unroll
       for (int ww = 1; ww < NW; ++ww) s += red[ww * V + k];
+      v[k] = s;
+    }
+  } else {
+    __syncwarp();
+  }
+}
+
+// The same for maxima of non-negative values (infeasibility violations).
+template <int NW, int V>
+__device__ __forceinline__ void breduce_max(double (&v)[V], double *red) {
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    double s = v[k];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s = fmax(s, __shfl_xor_sync(FULL, s, off));
+    v[k] = s;
+  }
+  if (NW > 1) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) red[w * V + k] = v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      double s = red[k];
+#pragma unroll
+      for (int ww = 1; ww < NW; ++ww) s = fmax(s, red[ww * V + k]);
       v[k] = s;
     }
   } else {
@@ -272,6 +301,24 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
     bool pending = false;                    // accepted attempt whose commit is fused into the next phases
     double theta = 0.0, ha = 0.0, hb = 0.0;  // raPDHG average weight / r2HPDHG Halpern coefficients
     const double *ox = x, *oy = y, *oKx = Kx, *oKTy = KTy;  // the returned candidate
+    const double *bx = nullptr, *by = nullptr, *bKTy = nullptr;  // ray base (infeasible status)
+    double ray_ny = 1.0, ray_nx = 1.0;
+    // infeasibility test (reading 35) of z = (x, y) against the base z_b; true: status set
+    auto infeasible = [&](const double *xb, const double *yb, const double *Kxb, const double *KTyb) {
+      CertAcc acc;
+      for (int j = tid; j < n; j += T) cert_col(acc, Dc[j], x[j], xb[j], KTy[j], KTyb[j], c0[j], P.l0[j], P.u0[j]);
+      for (int i = tid; i < m; i += T) cert_row(acc, i < m1, Dr[i], y[i], yb[i], Kx[i], Kxb[i], q0[i]);
+      double s4[4] = {acc.sy, acc.sx, acc.oy, acc.ox}, m2v[2] = {acc.vy, acc.vx};
+      breduce<NW, 4>(s4, redbuf());
+      breduce_max<NW, 2>(m2v, redbuf());
+      CertAcc tot;
+      tot.sy = s4[0]; tot.sx = s4[1]; tot.oy = s4[2]; tot.ox = s4[3]; tot.vy = m2v[0]; tot.vx = m2v[1];
+      const int st = cert_decide(tot, P.eps_pi, P.eps_di, ray_ny, ray_nx);
+      if (!st) return false;
+      status = st; ox = x; oy = y; oKx = Kx; oKTy = KTy;
+      bx = xb; by = yb; bKTy = KTyb;
+      return true;
+    };
 
     for (;;) {
       // ================= phase A: [commit n-side] + primal step =================
@@ -413,6 +460,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
           if (kkt_pass(kw, nq0, nc0, P.eps_abs, P.eps_rel)) {
             status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break;
           }
+          if (infeasible(xa, ya, Kxa, KTya)) break;   // rays from the epoch's Halpern anchor
           if (k == P.iter_limit) { status = LP_ITERATION_LIMIT; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
           cx = xp; cy = yp; cKx = Kxp; cKTy = KTyp; metric = rP; dx2 = v[4]; dy2 = v[5];
         }
@@ -453,6 +501,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
         if (kkt_pass(kc, nq0, nc0, P.eps_abs, P.eps_rel)) {
           status = LP_OPTIMAL; ox = x; oy = y; oKx = Kx; oKTy = KTy; break;
         }
+        if (infeasible(xp, yp, Kxp, KTyp)) break;     // rays from the last step (pre-commit point)
         if (k == P.iter_limit) {
           status = LP_ITERATION_LIMIT;
           if (rel_kkt(ka, nq0, nc0) < rel_kkt(kc, nq0, nc0)) { ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; }
@@ -496,13 +545,18 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
       for (int j = tid; j < n; j += T) {
         const double dc = Dc[j], xs = ox[j], kt = oKTy[j];
         kkt_col(v, true, dc, xs, kt, c0[j], cs[j], P.l0[j], ls[j], P.u0[j], us[j]);
-        X[j] = dc * xs;
-        L[j] = c0[j] - kt / dc;
+        if (bx) {  // infeasible: the unit rays d_x, d_y and -K'd_y (reading 35)
+          X[j] = dc * (xs - bx[j]) / ray_nx;
+          L[j] = -((kt - bKTy[j]) / dc) / ray_ny;
+        } else {
+          X[j] = dc * xs;
+          L[j] = c0[j] - kt / dc;
+        }
       }
       for (int i = tid; i < m; i += T) {
         const double dr = Dr[i];
         kkt_row(v, true, i, m1, dr, oy[i], oKx[i], q0[i], qs[i]);
-        Y[i] = dr * oy[i];
+        Y[i] = bx ? dr * (oy[i] - by[i]) / ray_ny : dr * oy[i];
       }
       breduce<NW, 4>(v, redbuf());
       if (tid == 0) {
@@ -589,6 +643,7 @@ int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunc
   P.kmax = D.kmax; P.sigma = D.sigma; P.tab = D.tab; P.const_step = o.step_rule == LP_STEP_CONSTANT;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
   P.check_freq = o.check_frequency; P.alg = o.algorithm;
+  P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
   P.batch = L.batch; P.queue = queue;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   P.work = nullptr; P.work_stride = 0;

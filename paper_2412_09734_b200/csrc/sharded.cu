@@ -35,9 +35,13 @@ constexpr int kV = 24;   // partial-sum slots
 struct ShState {
   double omega, eta, W, ref, last, theta, ha, hb, rP, M, Iv, eta_used, metric, nc0, nq0, eta0;
   long long k, j, k_in, restarts;
-  int rejects, status, pending, halt, restart, outsel, csel, r2, cstep;
+  int rejects, status, pending, halt, restart, outsel, csel, r2, cstep, rays;
   double colsum[kV];  // totals over this GPU's columns (replicated data: identical on every GPU)
   double rowsum[kV];  // totals over this GPU's rows; reduced across GPUs in place
+  // infeasibility certificate partials (reading 35): |dy|^2, |dx|^2, dual-ray obj, c'dx (summed),
+  // viol_y, viol_x (max); columns replicated, rows reduced across GPUs (sums, then maxima)
+  double certc[6], certr[6];
+  double ray_ny, ray_nx;
   unsigned int cnt_cols, cnt_rows;
 };
 
@@ -117,7 +121,8 @@ __device__ __forceinline__ double row_dot(int64_t r, bool valid, int G, int gl, 
 
 // Block partials of V values into part[block][.]; the last block to finish sums
 // them in block order (all 256 threads, fixed assignment + fixed tree) into out.
-template <int V>
+// MX: bit k set = value k is max-reduced (non-negative), else summed.
+template <int V, unsigned MX = 0u>
 __device__ __forceinline__ void last_block_sum(double (&v)[V], double *part, unsigned int *counter, double *out) {
   __shared__ double sred[kB / 32][kV];
   __shared__ double stree[kB];
@@ -127,13 +132,17 @@ __device__ __forceinline__ void last_block_sum(double (&v)[V], double *part, uns
   for (int k = 0; k < V; ++k) {
     double s = v[k];
 #pragma unroll
-    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    for (int off = 16; off; off >>= 1) {
+      const double o = __shfl_xor_sync(FULL, s, off);
+      s = ((MX >> k) & 1u) ? fmax(s, o) : s + o;
+    }
     if (lane == 0) sred[w][k] = s;
   }
   __syncthreads();
   if (threadIdx.x < V) {
+    const bool mx = (MX >> threadIdx.x) & 1u;
     double a = 0.0;
-    for (int ww = 0; ww < kB / 32; ++ww) a += sred[ww][threadIdx.x];
+    for (int ww = 0; ww < kB / 32; ++ww) a = mx ? fmax(a, sred[ww][threadIdx.x]) : a + sred[ww][threadIdx.x];
     part[(int64_t)blockIdx.x * kV + threadIdx.x] = a;
   }
   __threadfence();
@@ -143,12 +152,17 @@ __device__ __forceinline__ void last_block_sum(double (&v)[V], double *part, uns
   if (!s_last) return;
   __threadfence();
   for (int k = 0; k < V; ++k) {
+    const bool mx = (MX >> k) & 1u;
     double a = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += kB) a += __ldcg(part + (int64_t)b * kV + k);
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kB) {
+      const double o = __ldcg(part + (int64_t)b * kV + k);
+      a = mx ? fmax(a, o) : a + o;
+    }
     stree[threadIdx.x] = a;
     __syncthreads();
     for (int h = kB / 2; h; h >>= 1) {
-      if (threadIdx.x < h) stree[threadIdx.x] += stree[threadIdx.x + h];
+      if (threadIdx.x < h)
+        stree[threadIdx.x] = mx ? fmax(stree[threadIdx.x], stree[threadIdx.x + h]) : stree[threadIdx.x] + stree[threadIdx.x + h];
       __syncthreads();
     }
     if (threadIdx.x == 0) out[k] = stree[0];
@@ -179,8 +193,8 @@ __global__ void k_cols_spmv(const ShState *st, int64_t n, int G, const int32_t *
   }
 }
 
-enum { COLS_STEP = 0, COLS_COMMIT_ONLY = 1, COLS_AVG = 2, COLS_INIT = 3, COLS_INIT2 = 4, COLS_OUT = 5 };
-enum { ROWS_STEP = 0, ROWS_COMMIT_ONLY = 1, ROWS_AVG = 2, ROWS_INIT = 3, ROWS_INIT2 = 4, ROWS_OUT = 5 };
+enum { COLS_STEP = 0, COLS_COMMIT_ONLY = 1, COLS_AVG = 2, COLS_INIT = 3, COLS_INIT2 = 4, COLS_OUT = 5, COLS_CERT = 6 };
+enum { ROWS_STEP = 0, ROWS_COMMIT_ONLY = 1, ROWS_AVG = 2, ROWS_INIT = 3, ROWS_INIT2 = 4, ROWS_OUT = 5, ROWS_CERT = 6 };
 
 __global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, const Vecs V) {
   if (st->halt && mode != COLS_OUT) return;
@@ -192,6 +206,7 @@ __global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, con
     const double dc = P.Dc[j];
     if (mode == COLS_STEP || mode == COLS_COMMIT_ONLY) {
       double xv = V.x[j], kt = V.KTy[j];
+      const double xold = xv, ktold = kt;
       const double kty = V.red[j];
       if (pend) {
         const double xpv = V.xp[j];
@@ -209,9 +224,12 @@ __global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, con
         V.xp[j] = xn;
         const double d = xn - xv;
         v[0] += d * d;
+      } else if (!r2) {
+        // raPDHG: park the pre-step point in xp / KTyp (the infeasibility rays' base, reading 35)
+        if (pend) { V.xp[j] = xold; V.KTyp[j] = ktold; }
       } else {
         V.KTyp[j] = kty;
-        if (r2 && pend) {
+        if (pend) {
           const double xpv = V.xp[j];
           kkt_col(v, true, dc, xpv, kty, V.c0[j], V.cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
           const double d = xpv - V.xr[j];
@@ -230,6 +248,12 @@ __global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, con
       const double da = xaj - V.xr[j], dcur = xj - V.xr[j];
       v[16] += da * da;
       v[18] += dcur * dcur;
+    } else if (mode == COLS_CERT) {
+      const double *xb = r2 ? V.xa : V.xp, *ktb = r2 ? V.KTya : V.KTyp;
+      CertAcc acc;
+      cert_col(acc, dc, V.x[j], xb[j], V.KTy[j], ktb[j], V.c0[j], P.l0[j], P.u0[j]);
+      v[0] += acc.sy; v[1] += acc.sx; v[2] += acc.oy; v[3] += acc.ox;
+      v[4] = fmax(v[4], acc.vy); v[5] = fmax(v[5], acc.vx);
     } else if (mode == COLS_INIT) {
       const double c = V.c0[j], cj = c * dc;
       V.cs[j] = cj;
@@ -246,9 +270,20 @@ __global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, con
       const double xs = sel ? (r2 ? V.xp[j] : V.xa[j]) : V.x[j];
       const double kt = sel ? (r2 ? V.KTyp[j] : V.KTya[j]) : V.KTy[j];
       kkt_col(v, true, dc, xs, kt, V.c0[j], V.cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
-      V.red[j] = dc * xs;                    // unscaled x (output buffer)
-      V.KTyp[j] = V.c0[j] - kt / dc;         // reduced costs (output buffer)
+      if (st->rays) {  // infeasible: unit rays against the base (reading 35)
+        const double xb = r2 ? V.xa[j] : V.xp[j], ktb = r2 ? V.KTya[j] : V.KTyp[j];
+        V.red[j] = dc * (xs - xb) / st->ray_nx;
+        V.KTyp[j] = -((kt - ktb) / dc) / st->ray_ny;
+      } else {
+        V.red[j] = dc * xs;                    // unscaled x (output buffer)
+        V.KTyp[j] = V.c0[j] - kt / dc;         // reduced costs (output buffer)
+      }
     }
+  }
+  if (mode == COLS_CERT) {
+    double c6[6] = {v[0], v[1], v[2], v[3], v[4], v[5]};
+    last_block_sum<6, (3u << 4)>(c6, V.part, &st->cnt_cols, st->certc);
+    return;
   }
   last_block_sum<20>(v, V.part, &st->cnt_cols, st->colsum);
 }
@@ -275,6 +310,7 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
     const bool ge = i < m1;
     if (mode == ROWS_STEP || mode == ROWS_COMMIT_ONLY) {
       double yv = V.y[i], kxv = V.Kx[i];
+      const double yold = yv, kxold = kxv;
       if (pend) {
         const double ypv = V.yp[i], kxp = V.Kxp[i];
         if (!r2) {
@@ -298,7 +334,15 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
         kkt_row(v, true, ge, dr, ypv, kxp, V.q0[i], V.qs[i]);
         const double d = ypv - V.yr[i];
         v[5] += d * d;
+      } else if (!r2 && pend) {
+        V.yp[i] = yold; V.Kxp[i] = kxold;   // raPDHG: park the pre-step point (reading 35)
       }
+    } else if (mode == ROWS_CERT) {
+      const double *yb = r2 ? V.ya : V.yp, *kxb = r2 ? V.Kxa : V.Kxp;
+      CertAcc acc;
+      cert_row(acc, ge, dr, V.y[i], yb[i], V.Kx[i], kxb[i], V.q0[i]);
+      v[0] += acc.sy; v[1] += acc.sx; v[2] += acc.oy; v[3] += acc.ox;
+      v[4] = fmax(v[4], acc.vy); v[5] = fmax(v[5], acc.vx);
     } else if (mode == ROWS_AVG) {
       V.Kxa[i] = s;
       const double yai = V.ya[i], yi = V.y[i], kxi = V.Kx[i], q0 = V.q0[i], qsi = V.qs[i];
@@ -325,8 +369,14 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
       const double ys = sel ? (r2 ? V.yp[i] : V.ya[i]) : V.y[i];
       const double kx = sel ? (r2 ? V.Kxp[i] : V.Kxa[i]) : V.Kx[i];
       kkt_row(v, true, ge, dr, ys, kx, V.q0[i], V.qs[i]);
-      V.Kxp[i] = dr * ys;  // unscaled y (output buffer)
+      if (st->rays) V.Kxp[i] = dr * (ys - (r2 ? V.ya[i] : V.yp[i])) / st->ray_ny;
+      else V.Kxp[i] = dr * ys;  // unscaled y (output buffer)
     }
+  }
+  if (mode == ROWS_CERT) {
+    double c6[6] = {v[0], v[1], v[2], v[3], v[4], v[5]};
+    last_block_sum<6, (3u << 4)>(c6, V.part, &st->cnt_rows, st->certr);
+    return;
   }
   last_block_sum<20>(v, V.part, &st->cnt_rows, st->rowsum);
 }
@@ -379,15 +429,27 @@ __global__ void k_decide(ShState *st, const double *tab, int64_t check_freq, int
   st->pending = 1;
 }
 
-__global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, int64_t iter_limit) {
+__global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, double eps_pi, double eps_di,
+                               int64_t iter_limit) {
   double t[20];
   for (int k = 0; k < 20; ++k) t[k] = st->colsum[k] + st->rowsum[k];
   st->pending = 0;
   st->restart = 0;
   const double nq0 = st->nq0, nc0 = st->nc0;
+  // infeasibility verdict (reading 35), applied after the optimality tests
+  CertAcc ct;
+  ct.sy = st->certc[0] + st->certr[0]; ct.sx = st->certc[1] + st->certr[1];
+  ct.oy = st->certc[2] + st->certr[2]; ct.ox = st->certc[3] + st->certr[3];
+  ct.vy = fmax(st->certc[4], st->certr[4]); ct.vx = fmax(st->certc[5], st->certr[5]);
+  double ny = 1.0, nx = 1.0;
+  const int cert = cert_decide(ct, eps_pi, eps_di, ny, nx);
   if (st->r2) {
     const K5 kw = mk5(t);
     if (pass5(kw, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
+    if (cert) {
+      st->status = cert; st->halt = 1; st->outsel = 0; st->rays = 1; st->ray_ny = ny; st->ray_nx = nx;
+      return;
+    }
     if (st->k == iter_limit) { st->status = LP_ITERATION_LIMIT; st->halt = 1; st->outsel = 1; return; }
     st->metric = st->rP;
     st->csel = 1;
@@ -397,6 +459,10 @@ __global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, int6
     const K5 ka = mk5(t + 0), kc = mk5(t + 4);
     if (pass5(ka, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
     if (pass5(kc, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 0; return; }
+    if (cert) {
+      st->status = cert; st->halt = 1; st->outsel = 0; st->rays = 1; st->ray_ny = ny; st->ray_nx = nx;
+      return;
+    }
     if (st->k == iter_limit) {
       st->status = LP_ITERATION_LIMIT; st->halt = 1;
       st->outsel = rel5(ka, nq0, nc0) < rel5(kc, nq0, nc0) ? 1 : 0;
@@ -765,7 +831,18 @@ int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const dou
       STRY(launch_cols(E, COLS_AVG));
     }
     STRY(reduce_rowsum(E, 3));
-    for (auto &S : E.sh) MPAX_LAUNCH(k_check_decide, 1, 1, 0, s, S.st, o.eps_abs, o.eps_rel, LIM);
+    // infeasibility certificate partials (reading 35): columns replicated, rows reduced
+    STRY(launch_cols(E, COLS_CERT));
+    STRY(launch_rows(E, ROWS_CERT));
+    {
+      std::vector<double *> sums, maxs;
+      for (auto &S : E.sh) { sums.push_back(S.st->certr); maxs.push_back(S.st->certr + 4); }
+      STRY(reduce_vec(E, 5, sums, 4, false));
+      STRY(reduce_vec(E, 6, maxs, 2, true));
+    }
+    for (auto &S : E.sh)
+      MPAX_LAUNCH(k_check_decide, 1, 1, 0, s, S.st, o.eps_abs, o.eps_rel, o.eps_primal_infeasible,
+                  o.eps_dual_infeasible, LIM);
     for (auto &S : E.sh)
       MPAX_LAUNCH(k_restart, blocks_for(E.n > S.P.m ? E.n : S.P.m), kB, 0, s, S.st, E.n, S.P.m, S.V);
     MPAX_CHECK_LAUNCH();

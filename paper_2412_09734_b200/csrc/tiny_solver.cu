@@ -21,7 +21,7 @@ struct TinyParams {
   const double *C0, *Q0, *X0, *Y0;
   int64_t cstride, qstride;
   const double *kmax, *sigma, *tab;
-  double eps_abs, eps_rel;
+  double eps_abs, eps_rel, eps_pi, eps_di;
   int64_t iter_limit;
   int32_t check_freq;
   int64_t batch;
@@ -37,6 +37,17 @@ __device__ __forceinline__ void wsum(double (&v)[V]) {
     double s = v[k];
 #pragma unroll
     for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    v[k] = s;
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void wmax(double (&v)[V]) {
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    double s = v[k];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s = fmax(s, __shfl_xor_sync(FULL, s, off));
     v[k] = s;
   }
 }
@@ -203,6 +214,25 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
     int status = 0, rejects = 0;
     bool pending = false;
     int outsel = 0;  // 0 current, 1 candidate w / average, as set at termination
+    bool rays = false;  // infeasible: the certificate rays are already written (reading 35)
+    // the unit rays d_x / |d_x|, d_y / |d_y|, -K'd_y / |d_y| against the base point (xb, KTyb, yb)
+    auto write_rays = [&](int64_t bi, double ny, double nx, const double (&xb)[CPT], const double (&KTyb)[CPT],
+                          const double (&yb)[RPT]) {
+      double *X = P.X + bi * (int64_t)n, *L = P.L + bi * (int64_t)n, *Y = P.Y + bi * (int64_t)m;
+#pragma unroll
+      for (int t = 0; t < CPT; ++t) {
+        const int j = lane + 32 * t;
+        if (cok[t]) {
+          X[j] = dc[t] * (x[t] - xb[t]) / nx;
+          L[j] = -((KTy[t] - KTyb[t]) / dc[t]) / ny;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) {
+        const int i = lane + 32 * t;
+        if (rok[t]) Y[i] = dr[t] * (y[t] - yb[t]) / ny;
+      }
+    };
 
     for (;;) {
       __syncwarp();
@@ -307,6 +337,10 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
 
       // ================= step 5: check =================
       __syncwarp();
+      // infeasibility rays (reading 35): raPDHG from the point before this step (xo ...),
+      // r2HPDHG from the epoch's Halpern anchor (xa ...)
+      CertAcc cacc;
+      double xo[CPT], KTyo[CPT], yo[RPT], Kxo[RPT];
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {  // commit-only, n side (K~'y' into KTyp)
         double s = 0.0;
@@ -314,6 +348,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
         KTyp[t] = cok[t] ? s : 0.0;
         if (!R2) {
+          xo[t] = x[t]; KTyo[t] = KTy[t];
           xa[t] += theta * (xp[t] - xa[t]);
           x[t] = xp[t];
           KTy[t] = KTyp[t];
@@ -325,6 +360,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
 #pragma unroll
       for (int t = 0; t < RPT; ++t) {
         if (!R2) {
+          yo[t] = y[t]; Kxo[t] = Kx[t];
           ya[t] += theta * (yp[t] - ya[t]);
           y[t] = yp[t];
           Kx[t] = Kxp[t];
@@ -336,14 +372,18 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       double metric, dx2c, dy2c;
       int csel;  // restart candidate: 0 = current (x, y), 1 = average (ra) / w (r2)
       if (R2) {
-        double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        double v[10];
+#pragma unroll
+        for (int q = 0; q < 10; ++q) v[q] = 0.0;
 #pragma unroll
         for (int t = 0; t < CPT; ++t) {
           const int j = lane + 32 * t;
           if (cok[t]) {
-            kcol(v, true, dc[t], xp[t], KTyp[t], c0[j], cs[t], P.l0[j], lsv[t], P.u0[j], usv[t]);
+            const double l0j = P.l0[j], u0j = P.u0[j];
+            kcol(v, true, dc[t], xp[t], KTyp[t], c0[j], cs[t], l0j, lsv[t], u0j, usv[t]);
             const double d = xp[t] - xr[t];
             v[4] += d * d;
+            cert_col(cacc, dc[t], x[t], xa[t], KTy[t], KTya[t], c0[j], l0j, u0j);
           }
         }
 #pragma unroll
@@ -353,11 +393,25 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
             krow(v, true, i < m1, dr[t], yp[t], Kxp[t], q0[i], qs[t]);
             const double d = yp[t] - yr[t];
             v[5] += d * d;
+            cert_row(cacc, i < m1, dr[t], y[t], ya[t], Kx[t], Kxa[t], q0[i]);
           }
         }
-        wsum<6>(v);
+        v[6] = cacc.sy; v[7] = cacc.sx; v[8] = cacc.oy; v[9] = cacc.ox;
+        wsum<10>(v);
         const K5 kw = mk5(v);
         if (pass5(kw, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; outsel = 1; break; }
+        {
+          double mv[2] = {cacc.vy, cacc.vx};
+          wmax<2>(mv);
+          CertAcc tot;
+          tot.sy = v[6]; tot.sx = v[7]; tot.oy = v[8]; tot.ox = v[9]; tot.vy = mv[0]; tot.vx = mv[1];
+          double ny, nx;
+          const int st = cert_decide(tot, P.eps_pi, P.eps_di, ny, nx);
+          if (st) {
+            write_rays(b, ny, nx, xa, KTya, ya);
+            status = st; outsel = 0; rays = true; break;
+          }
+        }
         if (k == P.iter_limit) { status = LP_ITERATION_LIMIT; outsel = 1; break; }
         metric = rP; dx2c = v[4]; dy2c = v[5]; csel = 1;
       } else {
@@ -368,9 +422,9 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
 #pragma unroll
         for (int t = 0; t < RPT; ++t) sy[lane + 32 * t] = rok[t] ? ya[t] : 0.0;
         __syncwarp();
-        double v[20];
+        double v[24];
 #pragma unroll
-        for (int q = 0; q < 20; ++q) v[q] = 0.0;
+        for (int q = 0; q < 24; ++q) v[q] = 0.0;
 #pragma unroll
         for (int t = 0; t < RPT; ++t) {
           double s = 0.0;
@@ -388,6 +442,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
             const double da = ya[t] - yr[t], dcur = y[t] - yr[t];
             v[17] += da * da;
             v[19] += dcur * dcur;
+            cert_row(cacc, ge, dr[t], y[t], yo[t], Kx[t], Kxo[t], q0i);
           }
         }
 #pragma unroll
@@ -406,12 +461,26 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
             const double da = xa[t] - xr[t], dcur = x[t] - xr[t];
             v[16] += da * da;
             v[18] += dcur * dcur;
+            cert_col(cacc, dc[t], x[t], xo[t], KTy[t], KTyo[t], c0j, l0j, u0j);
           }
         }
-        wsum<20>(v);
+        v[20] = cacc.sy; v[21] = cacc.sx; v[22] = cacc.oy; v[23] = cacc.ox;
+        wsum<24>(v);
         const K5 ka = mk5(v + 0), kc = mk5(v + 4);
         if (pass5(ka, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; outsel = 1; break; }
         if (pass5(kc, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; outsel = 0; break; }
+        {
+          double mv[2] = {cacc.vy, cacc.vx};
+          wmax<2>(mv);
+          CertAcc tot;
+          tot.sy = v[20]; tot.sx = v[21]; tot.oy = v[22]; tot.ox = v[23]; tot.vy = mv[0]; tot.vx = mv[1];
+          double ny, nx;
+          const int st = cert_decide(tot, P.eps_pi, P.eps_di, ny, nx);
+          if (st) {
+            write_rays(b, ny, nx, xo, KTyo, yo);
+            status = st; outsel = 0; rays = true; break;
+          }
+        }
         if (k == P.iter_limit) {
           status = LP_ITERATION_LIMIT;
           outsel = rel5(ka, nq0, nc0) < rel5(kc, nq0, nc0) ? 1 : 0;
@@ -457,8 +526,10 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           const double xs = outsel ? (R2 ? xp[t] : xa[t]) : x[t];
           const double kt = outsel ? (R2 ? KTyp[t] : KTya[t]) : KTy[t];
           kcol(v, true, dc[t], xs, kt, c0[j], cs[t], P.l0[j], lsv[t], P.u0[j], usv[t]);
-          X[j] = dc[t] * xs;
-          L[j] = c0[j] - kt / dc[t];
+          if (!rays) {
+            X[j] = dc[t] * xs;
+            L[j] = c0[j] - kt / dc[t];
+          }
         }
       }
 #pragma unroll
@@ -468,7 +539,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           const double ys = outsel ? (R2 ? yp[t] : ya[t]) : y[t];
           const double kx = outsel ? (R2 ? Kxp[t] : Kxa[t]) : Kx[t];
           krow(v, true, i < m1, dr[t], ys, kx, q0[i], qs[t]);
-          Y[i] = dr[t] * ys;
+          if (!rays) Y[i] = dr[t] * ys;
         }
       }
       wsum<4>(v);
@@ -522,6 +593,7 @@ int tiny_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
   P.C0 = L.C0; P.cstride = L.cstride; P.Q0 = L.Q0; P.qstride = L.qstride; P.X0 = L.X0; P.Y0 = L.Y0;
   P.kmax = D.kmax; P.sigma = D.sigma; P.tab = D.tab;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit; P.check_freq = o.check_frequency;
+  P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
   P.batch = L.batch; P.queue = queue;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   const bool r2 = o.algorithm == LP_R2HPDHG, cs = o.step_rule == LP_STEP_CONSTANT;

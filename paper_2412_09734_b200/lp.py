@@ -13,7 +13,7 @@ _lock = threading.Lock()
 _lib = None
 
 LP_HOST, LP_DEVICE = 0, 1
-LP_OPTIMAL, LP_ITERATION_LIMIT, LP_NUMERICAL_ERROR = 1, 2, 3
+LP_OPTIMAL, LP_ITERATION_LIMIT, LP_NUMERICAL_ERROR, LP_PRIMAL_INFEASIBLE, LP_DUAL_INFEASIBLE = 1, 2, 3, 4, 5
 RAPDHG, R2HPDHG = 0, 1
 PATH_AUTO, PATH_INSTANCE, PATH_GRID, PATH_DMMA = 0, 1, 2, 3
 STEP_ADAPTIVE, STEP_CONSTANT = 0, 1
