@@ -71,6 +71,10 @@ typedef struct {
   int32_t power_iters;          /* power-iteration steps for sigma_max(K~), default 200 */
   double eps_primal_infeasible; /* Appendix, default 1e-8 (< 0: test off) */
   double eps_dual_infeasible;   /* Appendix, default 1e-8 (< 0: test off) */
+  double eps_feas_polish;       /* Appendix, default 1e-6 */
+  int32_t feasibility_polishing;/* Appendix, default 0 (DESIGN reading 36) */
+  int32_t polish_mode;          /* termination test: 0 relative KKT (contract step 5); 1 primal
+                                   residual only; 2 dual residual only (the polishing sub-solves) */
 } ora_options;
 
 /* Infeasibility certificate test on ORIGINAL-space rays (reading 35;
@@ -91,7 +95,7 @@ typedef struct {
 } ora_certificate;
 
 typedef struct {
-  int32_t status, pad;
+  int32_t status, polish;       /* polish: 0 not run, 1 both polish solves converged, 2 one hit the limit */
   int64_t iterations, attempts, restarts;
   double primal_objective, dual_objective, primal_residual, dual_residual, gap, rel_kkt;
   double omega, eta;
@@ -555,6 +559,16 @@ static void fill_infeasible(const scaled_lp *S, const double *x, const double *y
   if (y_out) for (int64_t i = 0; i < S->m; ++i) y_out[i] = dy[i] / sy;
 }
 
+/* The check's pass test: the relative KKT termination (contract step 5), or for the
+ * feasibility-polishing sub-solves (reading 36) the primal (mode 1) or dual (mode 2)
+ * residual alone against eps_feas_polish in the same relative form. */
+static int32_t check_pass(const ora_kkt *r, const scaled_lp *S, const ora_options *o) {
+  const double e = o->eps_feas_polish;
+  if (o->polish_mode == 1) return r->pres <= e + e * S->nq0;
+  if (o->polish_mode == 2) return r->dres <= e + e * S->nc0;
+  return ora_termination(r, S->nq0, S->nc0, o->eps_abs, o->eps_rel);
+}
+
 /* One solve on the scaled problem: contract steps 2-6. */
 static void solve_scaled(const scaled_lp *S, const ora_options *o, const double *x0, const double *y0,
                          double *x_out, double *y_out, double *lam_out, ora_result *res, ora_log *g) {
@@ -690,12 +704,12 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
       ora_kkt ka, kc;
       kkt_original_from_scaled(S, xa, ya, Kxa, KTya, &ka);
       kkt_original_from_scaled(S, x, y, Kx, KTy, &kc);
-      if (ora_termination(&ka, S->nq0, S->nc0, o->eps_abs, o->eps_rel)) {
+      if (check_pass(&ka, S, o)) {
         log_check(g, k, 0.0, ref, last, 0, 1);
         fill_result(S, xa, ya, Kxa, KTya, ORA_OPTIMAL, k, j, restarts, omega, eta, x_out, y_out, lam_out, res);
         goto done;
       }
-      if (ora_termination(&kc, S->nq0, S->nc0, o->eps_abs, o->eps_rel)) {
+      if (check_pass(&kc, S, o)) {
         log_check(g, k, 0.0, ref, last, 0, 2);
         fill_result(S, x, y, Kx, KTy, ORA_OPTIMAL, k, j, restarts, omega, eta, x_out, y_out, lam_out, res);
         goto done;
@@ -715,7 +729,7 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
     } else {
       ora_kkt kw;
       kkt_original_from_scaled(S, xp, yp, Kxp, KTyp, &kw);
-      if (ora_termination(&kw, S->nq0, S->nc0, o->eps_abs, o->eps_rel)) {
+      if (check_pass(&kw, S, o)) {
         log_check(g, k, rP, ref, last, 0, 1);
         fill_result(S, xp, yp, Kxp, KTyp, ORA_OPTIMAL, k, j, restarts, omega, eta, x_out, y_out, lam_out, res);
         goto done;
@@ -752,6 +766,69 @@ done:
   free(rdx); free(rKTdy); free(rdy); free(rKdx); free(xo); free(KTyo); free(yo); free(Kxo);
 }
 
+/* Feasibility polishing ("as a final step, feasibility polishing is applied
+ * ... to further enhance the feasibility of the solution"; SPEC
+ * S:439-447; reading 36).  After an OPTIMAL main solve:
+ *   primal polish: the same LP with c = 0, started at (x*, 0), until the primal residual
+ *     alone passes eps_feas_polish (relative form, mode 1);
+ *   dual polish:   the same LP with q = 0, started at (proj(0), y*), until the dual residual
+ *     alone passes (mode 2);
+ * both with the main algorithm and options, infeasibility detection off.  The result is
+ * (x from the primal polish, y and lambda from the dual polish); its KKT fields are
+ * recomputed on the original data with the unscaled K; counts are summed over the three
+ * solves; `polish` = 1 if both polish solves passed, 2 if one reached the iteration limit. */
+int ora_spmv_pair(const ora_problem *p, const double *x, double *Kx, const double *w, double *KTw);
+
+static void solve_polished(const ora_problem *p, const scaled_lp *S, const ora_options *o, const double *x0,
+                           const double *y0, double *x_out, double *y_out, double *lam_out, ora_result *res,
+                           ora_log *g) {
+  const int64_t n = S->n, m = S->m;
+  if (!o->feasibility_polishing) {
+    solve_scaled(S, o, x0, y0, x_out, y_out, lam_out, res, g);
+    return;
+  }
+  const size_t bn = (size_t)n * sizeof(double), bm = (size_t)(m ? m : 1) * sizeof(double);
+  double *xm = malloc(bn), *ym = malloc(bm), *lm = malloc(bn), *xp = malloc(bn), *yd = malloc(bm), *ld = malloc(bn);
+  double *zn = calloc((size_t)n, sizeof(double)), *zm = calloc((size_t)(m ? m : 1), sizeof(double));
+  double *Kx = malloc(bm), *KTy = malloc(bn);
+  solve_scaled(S, o, x0, y0, xm, ym, lm, res, g);
+  if (res->status != ORA_OPTIMAL) {
+    if (x_out) cpy(x_out, xm, n);
+    if (y_out) cpy(y_out, ym, m);
+    if (lam_out) cpy(lam_out, lm, n);
+  } else {
+    ora_options op = *o;
+    op.feasibility_polishing = 0;
+    op.eps_primal_infeasible = -1.0;
+    op.eps_dual_infeasible = -1.0;
+    ora_result r1, r2;
+    memset(&r1, 0, sizeof(r1)); memset(&r2, 0, sizeof(r2));
+    scaled_lp S1 = *S;                    /* c = 0 (scaled and original) */
+    S1.c = zn; S1.c0 = zn; S1.nc0 = 0.0;
+    op.polish_mode = 1;
+    solve_scaled(&S1, &op, xm, NULL, xp, NULL, NULL, &r1, NULL);
+    scaled_lp S2 = *S;                    /* q = 0 */
+    S2.q = zm; S2.q0 = zm; S2.nq0 = 0.0;
+    op.polish_mode = 2;
+    solve_scaled(&S2, &op, NULL, ym, NULL, yd, ld, &r2, NULL);
+    /* the polished pair on the original data */
+    ora_kkt r;
+    ora_spmv_pair(p, xp, Kx, yd, KTy);
+    kkt_residuals(n, m, p->m1, xp, yd, Kx, KTy, p->c, p->q, p->l, p->u, &r);
+    res->iterations += r1.iterations + r2.iterations;
+    res->attempts += r1.attempts + r2.attempts;
+    res->restarts += r1.restarts + r2.restarts;
+    res->primal_objective = r.pobj; res->dual_objective = r.dobj;
+    res->primal_residual = r.pres; res->dual_residual = r.dres; res->gap = r.gap;
+    res->rel_kkt = ora_rel_kkt(&r, S->nq0, S->nc0);
+    res->polish = (r1.status == ORA_OPTIMAL && r2.status == ORA_OPTIMAL) ? 1 : 2;
+    if (x_out) cpy(x_out, xp, n);
+    if (y_out) cpy(y_out, yd, m);
+    if (lam_out) cpy(lam_out, ld, n);
+  }
+  free(xm); free(ym); free(lm); free(xp); free(yd); free(ld); free(zn); free(zm); free(Kx); free(KTy);
+}
+
 /* ------------------------------------------------------------ exports ---- */
 
 void ora_default_options(ora_options *o) {
@@ -763,6 +840,9 @@ void ora_default_options(ora_options *o) {
   o->step_rule = 0; o->power_iters = 200;
   o->eps_primal_infeasible = 1e-8;               /* Appendix */
   o->eps_dual_infeasible = 1e-8;                 /* Appendix */
+  o->eps_feas_polish = 1e-6;                     /* Appendix */
+  o->feasibility_polishing = 0;                  /* Appendix */
+  o->polish_mode = 0;
 }
 
 int ora_num_threads(void) {
@@ -783,7 +863,8 @@ void ora_set_threads(int t) {
 static int check_options(const ora_options *o) {
   if (!o || !(o->eps_abs >= 0.0) || !(o->eps_rel >= 0.0) || o->iteration_limit < 1 ||
       o->check_frequency < 1 || (o->algorithm != ORA_RAPDHG && o->algorithm != ORA_R2HPDHG) ||
-      o->step_rule < 0 || o->step_rule > 1 || o->power_iters < 1)
+      o->step_rule < 0 || o->step_rule > 1 || o->power_iters < 1 || !(o->eps_feas_polish >= 0.0) ||
+      o->polish_mode < 0 || o->polish_mode > 2)
     return ORA_ERR_INVALID;
   return ORA_OK;
 }
@@ -804,7 +885,7 @@ int ora_solve(const ora_problem *p, const ora_options *o, const double *x0, cons
   if ((e = build_scaled(p, Dr, Dc, NULL, NULL, &S))) { free(Dr); free(Dc); return e; }
   if (g) { g->att_len = 0; g->chk_len = 0; }
   memset(res, 0, sizeof(*res));
-  solve_scaled(&S, o, x0, y0, x_out, y_out, lam_out, res, g);
+  solve_polished(p, &S, o, x0, y0, x_out, y_out, lam_out, res, g);
   scaled_free(&S, 1);
   free(Dr); free(Dc);
   return ORA_OK;
@@ -840,8 +921,8 @@ int ora_solve_batch(const ora_problem *p, int64_t batch, const double *C, const 
     scaled_lp S;
     if (build_scaled(&pb, Dr, Dc, &K, &KT, &S) == ORA_OK) {
       memset(&res[b], 0, sizeof(res[b]));
-      solve_scaled(&S, o, X0 ? X0 + b * n : NULL, Y0 ? Y0 + b * m : NULL,
-                   X_out ? X_out + b * n : NULL, Y_out ? Y_out + b * m : NULL, NULL, &res[b], NULL);
+      solve_polished(&pb, &S, o, X0 ? X0 + b * n : NULL, Y0 ? Y0 + b * m : NULL,
+                     X_out ? X_out + b * n : NULL, Y_out ? Y_out + b * m : NULL, NULL, &res[b], NULL);
     }
     scaled_free(&S, 0);
   }

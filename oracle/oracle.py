@@ -44,7 +44,8 @@ class Options(C.Structure):
                 ("check_frequency", C.c_int32), ("algorithm", C.c_int32),
                 ("ruiz_iters", C.c_int32), ("pock_chambolle", C.c_int32),
                 ("step_rule", C.c_int32), ("power_iters", C.c_int32),
-                ("eps_primal_infeasible", C.c_double), ("eps_dual_infeasible", C.c_double)]
+                ("eps_primal_infeasible", C.c_double), ("eps_dual_infeasible", C.c_double),
+                ("eps_feas_polish", C.c_double), ("feasibility_polishing", C.c_int32), ("polish_mode", C.c_int32)]
 
 
 class Certificate(C.Structure):
@@ -55,7 +56,7 @@ class Certificate(C.Structure):
 
 
 class Result(C.Structure):
-    _fields_ = [("status", C.c_int32), ("pad", C.c_int32), ("iterations", C.c_int64),
+    _fields_ = [("status", C.c_int32), ("polish", C.c_int32), ("iterations", C.c_int64),
                 ("attempts", C.c_int64), ("restarts", C.c_int64),
                 ("primal_objective", C.c_double), ("dual_objective", C.c_double),
                 ("primal_residual", C.c_double), ("dual_residual", C.c_double),
@@ -63,7 +64,7 @@ class Result(C.Structure):
                 ("eta", C.c_double)]
 
     def as_dict(self):
-        return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad"}
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 class Log(C.Structure):
@@ -145,7 +146,7 @@ class _Bound:
 
 def options(algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, check_frequency=64,
             ruiz_iters=10, pock_chambolle=1, step_rule=0, power_iters=200, eps_primal_infeasible=1e-8,
-            eps_dual_infeasible=1e-8):
+            eps_dual_infeasible=1e-8, feasibility_polishing=False, eps_feas_polish=1e-6):
     o = Options()
     lib().ora_default_options(C.byref(o))
     o.algorithm = R2HPDHG if algorithm in ("r2", "r2hpdhg", R2HPDHG) else RAPDHG
@@ -157,6 +158,7 @@ def options(algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, ch
     o.step_rule = 1 if step_rule in (1, "constant") else 0
     o.power_iters = power_iters
     o.eps_primal_infeasible, o.eps_dual_infeasible = eps_primal_infeasible, eps_dual_infeasible
+    o.feasibility_polishing, o.eps_feas_polish = int(bool(feasibility_polishing)), eps_feas_polish
     return o
 
 
@@ -166,13 +168,15 @@ def validate(lp) -> int:
 
 
 def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, x0=None, y0=None,
-          check_frequency=64, log_capacity=0, step_rule=0, eps_primal_infeasible=1e-8, eps_dual_infeasible=1e-8):
+          check_frequency=64, log_capacity=0, step_rule=0, eps_primal_infeasible=1e-8, eps_dual_infeasible=1e-8,
+          feasibility_polishing=False, eps_feas_polish=1e-6):
     """Full solve (contract steps 0-6).  Returns a dict with x, y, lam, the
     result fields, and (if log_capacity) the attempt/check decision logs."""
     b = _Bound(lp)
     m = lp.m1 + lp.m2
     o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule,
-                eps_primal_infeasible=eps_primal_infeasible, eps_dual_infeasible=eps_dual_infeasible)
+                eps_primal_infeasible=eps_primal_infeasible, eps_dual_infeasible=eps_dual_infeasible,
+                feasibility_polishing=feasibility_polishing, eps_feas_polish=eps_feas_polish)
     x = np.zeros(lp.n)
     y = np.zeros(m)
     lam = np.zeros(lp.n)
@@ -199,7 +203,7 @@ def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, 
 
 def solve_batch(lp, C_=None, Q=None, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None,
                 X0=None, Y0=None, check_frequency=64, threads=None, step_rule=0, eps_primal_infeasible=1e-8,
-                eps_dual_infeasible=1e-8):
+                eps_dual_infeasible=1e-8, feasibility_polishing=False, eps_feas_polish=1e-6):
     """Batch solve sharing K, l, u; one instance per OpenMP thread."""
     b = _Bound(lp)
     m = lp.m1 + lp.m2
@@ -207,7 +211,8 @@ def solve_batch(lp, C_=None, Q=None, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4,
     Qm = None if Q is None else _f64(Q)
     B = Cm.shape[0] if Cm is not None else Qm.shape[0]
     o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule,
-                eps_primal_infeasible=eps_primal_infeasible, eps_dual_infeasible=eps_dual_infeasible)
+                eps_primal_infeasible=eps_primal_infeasible, eps_dual_infeasible=eps_dual_infeasible,
+                feasibility_polishing=feasibility_polishing, eps_feas_polish=eps_feas_polish)
     X = np.zeros((B, lp.n))
     Y = np.zeros((B, m))
     res = (Result * B)()
