@@ -122,17 +122,28 @@ typedef struct {
   double eps_rel;               /* 1e-4 */
   double eps_primal_infeasible; /* 1e-8; < 0 disables the test */
   double eps_dual_infeasible;   /* 1e-8; < 0 disables the test */
-  double eps_feas_polish;       /* 1e-6, reserved */
+  double eps_feas_polish;       /* 1e-6 */
   int64_t iteration_limit;      /* INT64_MAX; accepted steps */
   int32_t check_frequency;      /* 64 */
   int32_t algorithm;            /* lp_algorithm, default LP_R2HPDHG */
   int32_t warm_start;           /* informational; a non-NULL x0 / y0 is what warm-starts */
-  int32_t feasibility_polishing;/* must be 0 (reserved) */
+  int32_t feasibility_polishing;/* 0; 1: polish OPTIMAL results (see below; not on sharded handles) */
   int32_t verbose;              /* reserved */
   int32_t display_frequency;    /* 10, reserved */
   int32_t path;                 /* lp_path, default LP_PATH_AUTO */
   int32_t step_rule;            /* lp_step_rule, default LP_STEP_ADAPTIVE */
 } lp_options;
+
+/* Feasibility polishing (reading 36).
+ * With feasibility_polishing = 1, every instance whose solve ends OPTIMAL is followed by
+ * two sub-solves with the same algorithm and options (infeasibility detection off, at most
+ * min(iteration_limit, 100000) accepted steps each): a primal polish of the LP with c = 0
+ * from (x*, 0) until the primal residual alone satisfies
+ * pres <= eps_feas_polish (1 + ||q||), and a dual polish with q = 0 from (proj(0), y*) until
+ * dres <= eps_feas_polish (1 + ||c||).  The returned x is the primal polish's, y and the
+ * reduced costs the dual polish's; primal_residual / dual_residual are theirs, the
+ * objectives, gap and rel_kkt are recomputed on the original c, q, l, u; iterations,
+ * attempts and restarts are summed over the three solves; `polish` flags the outcome. */
 
 /* Per-instance outcome.  The objectives and residuals are those of the
  * returned (x, y) in ORIGINAL space (contract step 5/6):
@@ -142,7 +153,7 @@ typedef struct {
  *   rel_kkt = max(pres/(1+||q||), dres/(1+||c||), gap/(1+|pobj|+|dobj|)). */
 typedef struct {
   int32_t status;       /* lp_status */
-  int32_t pad;
+  int32_t polish;       /* feasibility polishing: 0 not run, 1 both sub-solves passed, 2 one hit its limit */
   int64_t iterations;   /* accepted PDHG steps k */
   int64_t attempts;     /* line-search attempts j (>= iterations) */
   int64_t restarts;

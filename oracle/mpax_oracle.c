@@ -41,6 +41,7 @@
 #endif
 
 #define ORA_INF HUGE_VAL
+#define ORA_POLISH_LIMIT 100000   /* accepted steps per polishing sub-solve (reading 36) */
 
 enum { ORA_OK = 0, ORA_ERR_INVALID = -1, ORA_ERR_DIMENSION = -2, ORA_ERR_NAN = -3,
        ORA_ERR_CROSSED_BOUNDS = -4, ORA_ERR_OOM = -6 };
@@ -773,7 +774,9 @@ done:
  *     alone passes eps_feas_polish (relative form, mode 1);
  *   dual polish:   the same LP with q = 0, started at (proj(0), y*), until the dual residual
  *     alone passes (mode 2);
- * both with the main algorithm and options, infeasibility detection off.  The result is
+ * both with the main algorithm and options, infeasibility detection off, each limited to
+ * min(iteration_limit, ORA_POLISH_LIMIT) accepted steps (the q = 0 problem need not be
+ * solvable even when the LP is, so an unbounded polish is never started).  The result is
  * (x from the primal polish, y and lambda from the dual polish); its KKT fields are
  * recomputed on the original data with the unscaled K; counts are summed over the three
  * solves; `polish` = 1 if both polish solves passed, 2 if one reached the iteration limit. */
@@ -799,6 +802,7 @@ static void solve_polished(const ora_problem *p, const scaled_lp *S, const ora_o
   } else {
     ora_options op = *o;
     op.feasibility_polishing = 0;
+    if (op.iteration_limit > ORA_POLISH_LIMIT) op.iteration_limit = ORA_POLISH_LIMIT;
     op.eps_primal_infeasible = -1.0;
     op.eps_dual_infeasible = -1.0;
     ora_result r1, r2;

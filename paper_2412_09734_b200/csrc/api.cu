@@ -33,6 +33,7 @@ struct lp_handle_s {
   int64_t cstride = 0, qstride = 0;
   double *X = nullptr, *Y = nullptr, *L = nullptr;
   double *X0 = nullptr, *Y0 = nullptr;  // warm-start staging
+  double *pol = nullptr;                // feasibility-polishing buffers (lazily allocated)
   lp_result *d_res = nullptr, *h_res = nullptr;
   unsigned long long *queue = nullptr;
   double *work = nullptr;
@@ -121,7 +122,7 @@ void free_handle(lp_handle h) {
     return;
   }
   cudaStream_t s = h->stream;
-  for (void *p : {(void *)h->arena, (void *)h->X0, (void *)h->Y0, (void *)h->work})
+  for (void *p : {(void *)h->arena, (void *)h->X0, (void *)h->Y0, (void *)h->work, (void *)h->pol})
     if (p) cudaFreeAsync(p, s);
   // every D2H into the pinned buffers was followed by a stream sync, so they can be recycled now
   pin_put(h->h_res, (size_t)h->batch * sizeof(lp_result));
@@ -249,7 +250,8 @@ int check_options(const lp_options *o) {
   if (!(o->eps_abs >= 0.0) || !(o->eps_rel >= 0.0) || o->iteration_limit < 1 || o->check_frequency < 1 ||
       (o->algorithm != LP_RAPDHG && o->algorithm != LP_R2HPDHG))
     return fail(LP_ERR_INVALID_ARGUMENT, "bad option value");
-  if (o->feasibility_polishing) return fail(LP_ERR_UNSUPPORTED, "feasibility polishing is not built yet");
+  if (o->feasibility_polishing && !(o->eps_feas_polish >= 0.0))
+    return fail(LP_ERR_INVALID_ARGUMENT, "bad eps_feas_polish");
   if (o->path < LP_PATH_AUTO || o->path > LP_PATH_DMMA) return fail(LP_ERR_INVALID_ARGUMENT, "bad path");
   if (o->step_rule != LP_STEP_ADAPTIVE && o->step_rule != LP_STEP_CONSTANT)
     return fail(LP_ERR_INVALID_ARGUMENT, "bad step_rule");
@@ -275,12 +277,71 @@ int run_sharded(lp_handle h, const lp_options *o, const double *X0, const double
   return rc;
 }
 
+// ---- feasibility polishing (reading 36): combine the two sub-solves per instance ----
+// Instances whose main status is OPTIMAL take x from the primal polish and y, lambda
+// from the dual polish; the result's residuals are those sub-solves' (computed on the
+// original q / c they kept), the objectives are recomputed on the original data.
+__global__ void polish_combine_kernel(int64_t n, int64_t m, int64_t m1, const double *C0, int64_t cstride,
+                                      const double *Q0, int64_t qstride, const double *l0, const double *u0,
+                                      const double *X1, const lp_result *res1, const double *Y2, const double *L2,
+                                      const lp_result *res2, double *X, double *Y, double *L, lp_result *res) {
+  const int64_t b = blockIdx.x;
+  if (res[b].status != LP_OPTIMAL) return;
+  __shared__ double red[4][8];
+  const double *c = C0 + b * cstride, *q = Q0 + b * qstride;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};  // c'x, dual objective, |c|^2, |q|^2
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const double xj = X1[b * n + j], lam = L2[b * n + j];
+    X[b * n + j] = xj;
+    L[b * n + j] = lam;
+    v[0] += c[j] * xj;
+    v[2] += c[j] * c[j];
+    const double lp = fmax(lam, 0.0), lm = fmax(-lam, 0.0);
+    if (l0[j] > -INFINITY) v[1] += l0[j] * lp;
+    if (u0[j] < INFINITY) v[1] -= u0[j] * lm;
+  }
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const double yi = Y2[b * m + i];
+    Y[b * m + i] = yi;
+    v[1] += q[i] * yi;
+    v[3] += q[i] * q[i];
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = 0; k < 4; ++k) {
+    double s = v[k];
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    if (lane == 0) red[k][w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t[4];
+    for (int k = 0; k < 4; ++k) {
+      t[k] = 0.0;
+      for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) t[k] += red[k][ww];
+    }
+    lp_result r = res[b];
+    const double pres = res1[b].primal_residual, dres = res2[b].dual_residual;
+    const double nc = sqrt(t[2]), nq = sqrt(t[3]), gap = fabs(t[0] - t[1]);
+    r.primal_objective = t[0]; r.dual_objective = t[1];
+    r.primal_residual = pres; r.dual_residual = dres; r.gap = gap;
+    r.rel_kkt = fmax(pres / (1.0 + nq), fmax(dres / (1.0 + nc), gap / (1.0 + fabs(t[0]) + fabs(t[1]))));
+    r.iterations += res1[b].iterations + res2[b].iterations;
+    r.attempts += res1[b].attempts + res2[b].attempts;
+    r.restarts += res1[b].restarts + res2[b].restarts;
+    r.polish = (res1[b].status == LP_OPTIMAL && res2[b].status == LP_OPTIMAL) ? 1 : 2;
+    res[b] = r;
+  }
+}
+
 int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *Y0, int32_t memory,
               lp_result *out) {
   if (!h || !out) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle or result");
   TRY(check_options(o));
   if (memory != LP_HOST && memory != LP_DEVICE) return fail(LP_ERR_INVALID_ARGUMENT, "bad memory kind");
-  if (h->sharded) return run_sharded(h, o, X0, Y0, out);
+  if (h->sharded) {
+    if (o->feasibility_polishing) return fail(LP_ERR_UNSUPPORTED, "feasibility polishing on a sharded handle");
+    return run_sharded(h, o, X0, Y0, out);
+  }
   cudaStream_t s = h->stream;
   const int64_t n = h->P.n, m = h->P.m, B = h->batch;
   // warm starts: staged into library memory (original space; scaled in-kernel)
@@ -299,30 +360,8 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
   const bool big = h->P.nnz >= 32768 || h->P.n + h->P.m >= 4096;
   const bool use_grid = (B == 1) && (o->path == LP_PATH_GRID || (o->path == LP_PATH_AUTO && big));
   if (o->path == LP_PATH_GRID && B != 1) return fail(LP_ERR_UNSUPPORTED, "the grid path solves one LP");
-  MPAX_CUDA(cudaEventRecord(h->ev0, s));
-  // constant step rule: sigma_max(K~) once per handle (K is fixed for its lifetime)
-  if (o->step_rule == LP_STEP_CONSTANT && !h->P.sigma_ready) TRY(power_sigma(h->P, s));
-  if (use_grid) {
-    GridLaunch G;
-    G.c0 = h->C0; G.q0 = h->Q0; G.X0 = dX0; G.Y0 = dY0; G.X = h->X; G.Y = h->Y; G.L = h->L; G.res = h->d_res;
-    int rc = grid_solve(h->P, *o, G, s, &h->work, &h->work_bytes);
-    if (rc == LP_ERR_UNSUPPORTED) return fail(rc, "cooperative launch unavailable");
-    TRY(rc);
-    MPAX_CUDA(cudaEventRecord(h->ev1, s));
-    MPAX_CUDA(cudaMemcpyAsync(h->h_res, h->d_res, sizeof(lp_result), cudaMemcpyDeviceToHost, s));
-    MPAX_CUDA(cudaStreamSynchronize(s));
-    float ms = 0.0f;
-    MPAX_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
-    out[0] = h->h_res[0];
-    out[0].solve_seconds = ms * 1e-3;
-    h->solved = true;
-    return LP_OK;
-  }
-  InstanceLaunch L;
-  L.C0 = h->C0; L.cstride = h->cstride; L.Q0 = h->Q0; L.qstride = h->qstride;
-  L.X0 = dX0; L.Y0 = dY0; L.batch = B; L.X = h->X; L.Y = h->Y; L.L = h->L; L.res = h->d_res;
   // a batch sharing a dense K: fp64 tensor-core path (auto from 8 instances on)
-  const bool dmma = h->P.dense && (o->path == LP_PATH_DMMA || (o->path == LP_PATH_AUTO && B >= 8));
+  const bool dmma = !use_grid && h->P.dense && (o->path == LP_PATH_DMMA || (o->path == LP_PATH_AUTO && B >= 8));
   if (dmma) {
     const size_t need = dmma_workspace_doubles(n, m, B) * sizeof(double);
     if (h->work_bytes < need) {
@@ -332,14 +371,70 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
       h->work_bytes = need;
     }
   }
-  int rc = LP_ERR_UNSUPPORTED;
-  if (dmma) {
-    rc = dmma_solve(h->P, *o, L, s, h->queue, h->work);
-    if (rc == LP_ERR_UNSUPPORTED && o->path == LP_PATH_DMMA) return fail(rc, "dense K too large for the DMMA path");
+  // one solve of the batch (main, or a polishing sub-solve) on the chosen path
+  auto dispatch = [&](const lp_options &oo, InstanceLaunch L) -> int {
+    if (use_grid) {
+      GridLaunch G;
+      G.c0 = L.C0; G.q0 = L.Q0; G.X0 = L.X0; G.Y0 = L.Y0; G.X = L.X; G.Y = L.Y; G.L = L.L; G.res = L.res;
+      G.polish_mode = L.polish_mode;
+      int rc = grid_solve(h->P, oo, G, s, &h->work, &h->work_bytes);
+      if (rc == LP_ERR_UNSUPPORTED) return fail(rc, "cooperative launch unavailable");
+      return rc;
+    }
+    int rc = LP_ERR_UNSUPPORTED;
+    if (dmma) {
+      rc = dmma_solve(h->P, oo, L, s, h->queue, h->work);
+      if (rc == LP_ERR_UNSUPPORTED && oo.path == LP_PATH_DMMA) return fail(rc, "dense K too large for the DMMA path");
+    }
+    if (rc == LP_ERR_UNSUPPORTED && oo.path == LP_PATH_AUTO) rc = tiny_solve(h->P, oo, L, s, h->queue);
+    if (rc == LP_ERR_UNSUPPORTED) rc = instance_solve(h->P, oo, L, s, h->queue, &h->work, &h->work_bytes);
+    return rc;
+  };
+  MPAX_CUDA(cudaEventRecord(h->ev0, s));
+  // constant step rule: sigma_max(K~) once per handle (K is fixed for its lifetime)
+  if (o->step_rule == LP_STEP_CONSTANT && !h->P.sigma_ready) TRY(power_sigma(h->P, s));
+  InstanceLaunch L;
+  L.C0 = h->C0; L.cstride = h->cstride; L.Q0 = h->Q0; L.qstride = h->qstride;
+  L.X0 = dX0; L.Y0 = dY0; L.batch = B; L.X = h->X; L.Y = h->Y; L.L = h->L; L.res = h->d_res;
+  TRY(dispatch(*o, L));
+  if (o->feasibility_polishing) {
+    // (reading 36) primal polish: c = 0 from (x*, 0); dual polish: q = 0 from (proj 0, y*);
+    // residual-only tests, infeasibility detection off, min(limit, kPolishLimit) steps
+    bool run = true;
+    if (use_grid) {  // one LP: run the sub-solves only after an OPTIMAL main solve
+      MPAX_CUDA(cudaMemcpyAsync(h->h_res, h->d_res, sizeof(lp_result), cudaMemcpyDeviceToHost, s));
+      MPAX_CUDA(cudaStreamSynchronize(s));
+      run = h->h_res[0].status == LP_OPTIMAL;
+    }
+    if (run) {
+      if (!h->pol) {
+        const int64_t mm = m > 0 ? m : 1;
+        const size_t dbl = (size_t)(4 * B * n + 3 * B * mm + n + mm);
+        TRY(dalloc((char **)&h->pol, dbl * sizeof(double) + 2 * (size_t)B * sizeof(lp_result), s));
+        MPAX_CUDA(cudaMemsetAsync(h->pol, 0, dbl * sizeof(double), s));
+      }
+      const int64_t mm = m > 0 ? m : 1;
+      double *X1 = h->pol, *L1 = X1 + B * n, *X2 = L1 + B * n, *L2 = X2 + B * n, *Y1 = L2 + B * n,
+             *Y2 = Y1 + B * mm, *zn = Y2 + B * mm, *zm = zn + n;
+      lp_result *res1 = (lp_result *)(zm + mm), *res2 = res1 + B;
+      lp_options op = *o;
+      op.feasibility_polishing = 0;
+      op.eps_primal_infeasible = -1.0;
+      op.eps_dual_infeasible = -1.0;
+      if (op.iteration_limit > kPolishLimit) op.iteration_limit = kPolishLimit;
+      InstanceLaunch L1l = L;
+      L1l.C0 = zn; L1l.cstride = 0; L1l.X0 = h->X; L1l.Y0 = nullptr;
+      L1l.X = X1; L1l.Y = Y1; L1l.L = L1; L1l.res = res1; L1l.polish_mode = 1; L1l.active = h->d_res;
+      TRY(dispatch(op, L1l));
+      InstanceLaunch L2l = L;
+      L2l.Q0 = zm; L2l.qstride = 0; L2l.X0 = nullptr; L2l.Y0 = m > 0 ? h->Y : nullptr;
+      L2l.X = X2; L2l.Y = Y2; L2l.L = L2; L2l.res = res2; L2l.polish_mode = 2; L2l.active = h->d_res;
+      TRY(dispatch(op, L2l));
+      MPAX_LAUNCH(polish_combine_kernel, (int)B, 256, 0, s, n, m, h->P.m1, h->C0, h->cstride, h->Q0, h->qstride,
+                  h->P.l0, h->P.u0, X1, res1, Y2, L2, res2, h->X, h->Y, h->L, h->d_res);
+      MPAX_CHECK_LAUNCH();
+    }
   }
-  if (rc == LP_ERR_UNSUPPORTED && o->path == LP_PATH_AUTO) rc = tiny_solve(h->P, *o, L, s, h->queue);
-  if (rc == LP_ERR_UNSUPPORTED) rc = instance_solve(h->P, *o, L, s, h->queue, &h->work, &h->work_bytes);
-  TRY(rc);
   MPAX_CUDA(cudaEventRecord(h->ev1, s));
   MPAX_CUDA(cudaMemcpyAsync(h->h_res, h->d_res, (size_t)B * sizeof(lp_result), cudaMemcpyDeviceToHost, s));
   MPAX_CUDA(cudaStreamSynchronize(s));

@@ -57,9 +57,10 @@ struct DmmaParams {
   const double *C0, *Q0, *X0, *Y0;
   int64_t cstride, qstride;
   const double *kmax, *sigma, *tab;
-  double eps_abs, eps_rel, eps_pi, eps_di;
+  double eps_abs, eps_rel, eps_pi, eps_di, eps_fp;
   int64_t iter_limit;
-  int32_t check_freq, alg, const_step;
+  int32_t check_freq, alg, const_step, polish_mode;
+  const lp_result *active;
   int64_t batch;
   unsigned long long *queue;
   // per-instance state, instance-major [B][n] / [B][m]
@@ -74,7 +75,7 @@ struct Inst {
   double omega, eta, W, ref, last, theta, ha, hb, rP, nc0, nq0, metric, dx2c, dy2c, eta_used, M, I;
   double ray_ny, ray_nx;  // infeasibility rays' norms (reading 35)
   long long k, j, k_in, restarts;
-  int rejects, status, pending, done, check, outsel, csel, valid, cert, rays;
+  int rejects, status, pending, done, check, outsel, csel, valid, cert, rays, skip;
 };
 
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
@@ -286,6 +287,11 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
   for (int t = tid; t < np * kS; t += kThreads) S.Xc[t] = 0.0;
   const bool cstep = P.const_step != 0;  // constant step rule (reading 34)
   const double eta0 = initial_eta(P.kmax, P.sigma, cstep);
+  // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
+  auto tpass = [&](const K5 &k, double nq, double nc) {
+    return P.polish_mode ? polish_pass(P.polish_mode, k.pres, k.dres, nq, nc, P.eps_fp)
+                         : pass5(k, nq, nc, P.eps_abs, P.eps_rel);
+  };
 
   for (;;) {
     // ---- next group of 8 instances (rank 0 pulls from the queue) ----
@@ -301,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       I = Inst();
       I.valid = (b0 + tid) < P.batch;
       I.done = !I.valid;
+      if (I.valid && P.active && P.active[b0 + tid].status != LP_OPTIMAL) { I.done = 1; I.skip = 1; }
     }
     __syncthreads();
     // ---- step 2: scaled data, start point, norms (partials: |c~|^2, |q~|^2, |c|^2, |q|^2) ----
@@ -606,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           if (I.check) {
             const double *t6 = tot + tid * 24;
             const K5 kw = mk5(t6);
-            if (pass5(kw, I.nq0, I.nc0, P.eps_abs, P.eps_rel)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 1; }
+            if (tpass(kw, I.nq0, I.nc0)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 1; }
             else if (I.cert) { I.status = I.cert; I.done = 1; I.outsel = 0; I.rays = 1; }
             else if (I.k == P.iter_limit) { I.status = LP_ITERATION_LIMIT; I.done = 1; I.outsel = 1; }
             else { I.metric = I.rP; I.dx2c = t6[4]; I.dy2c = t6[5]; I.csel = 1; }
@@ -672,8 +679,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           if (I.check) {
             const double *t = tot + tid * 24;
             const K5 ka = mk5(t + 0), kc = mk5(t + 4);
-            if (pass5(ka, I.nq0, I.nc0, P.eps_abs, P.eps_rel)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 1; }
-            else if (pass5(kc, I.nq0, I.nc0, P.eps_abs, P.eps_rel)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 0; }
+            if (tpass(ka, I.nq0, I.nc0)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 1; }
+            else if (tpass(kc, I.nq0, I.nc0)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 0; }
             else if (I.cert) { I.status = I.cert; I.done = 1; I.outsel = 0; I.rays = 1; }
             else if (I.k == P.iter_limit) {
               I.status = LP_ITERATION_LIMIT; I.done = 1;
@@ -748,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       for (int t = tid; t < jn * kS; t += kThreads) {
         const int s = t / jn, jj = t % jn, j = j0 + jj;
         const Inst &I = S.inst[s];
-        if (!I.valid) continue;
+        if (!I.valid || I.skip) continue;
         const int64_t b = b0 + s;
         const int64_t o = b * n + j;
         const double xs = I.outsel ? (r2 ? P.xp[o] : P.xa[o]) : P.x[o];
@@ -767,7 +774,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       for (int t = tid; t < in_ * kS; t += kThreads) {
         const int s = t / in_, ii = t % in_, i = i0 + ii;
         const Inst &I = S.inst[s];
-        if (!I.valid) continue;
+        if (!I.valid || I.skip) continue;
         const int64_t b = b0 + s;
         const int64_t o = b * m + i;
         const double ys = I.outsel ? (r2 ? P.yp[o] : P.ya[o]) : P.y[o];
@@ -781,11 +788,11 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       cta_partials<4>(v, S);
       cl.sync();
       cluster_totals<CL, 4>(cl, S, tot);
-      if (crank == 0 && tid < kS && S.inst[tid].valid) {
+      if (crank == 0 && tid < kS && S.inst[tid].valid && !S.inst[tid].skip) {
         const Inst &I = S.inst[tid];
         const K5 ko = mk5(tot + tid * 24);
         lp_result r;
-        r.status = I.status; r.pad = 0;
+        r.status = I.status; r.polish = 0;
         r.iterations = I.k; r.attempts = I.j; r.restarts = I.restarts;
         r.primal_objective = ko.pobj; r.dual_objective = ko.dobj;
         r.primal_residual = ko.pres; r.dual_residual = ko.dres; r.gap = ko.gap;
@@ -855,6 +862,7 @@ int dmma_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
     P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
     P.check_freq = o.check_frequency; P.alg = o.algorithm;
     P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
+    P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active;
     P.batch = L.batch; P.queue = queue;
     const size_t BN = (size_t)L.batch * n, BM = (size_t)L.batch * m;
     double *w = work;

@@ -45,9 +45,9 @@ struct GridParams {
   double *x, *KTy, *xp, *KTyp, *xa, *KTya, *xr;   // n-side
   double *y, *Kx, *yp, *Kxp, *ya, *Kxa, *yr;      // m-side
   double *part;                                   // gridDim.x x kNP
-  double eps_abs, eps_rel, eps_pi, eps_di;
+  double eps_abs, eps_rel, eps_pi, eps_di, eps_fp;
   int64_t iter_limit;
-  int32_t check_freq, alg, gk, gkt, const_step;
+  int32_t check_freq, alg, gk, gkt, const_step, polish_mode;
   double *X, *Y, *L;
   lp_result *res;
 };
@@ -258,6 +258,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   if (sqrt(tot4[0]) > 1e-10 && sqrt(tot4[1]) > 1e-10) omega = sqrt(tot4[0]) / sqrt(tot4[1]);
   const bool cstep = P.const_step != 0;  // constant step rule (reading 34)
   double eta = initial_eta(P.kmax, P.sigma, cstep);
+  // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
+  auto tpass = [&](const KktT &k, double nq, double nc) {
+    return P.polish_mode ? polish_pass(P.polish_mode, k.pres, k.dres, nq, nc, P.eps_fp)
+                         : pass(k, nq, nc, P.eps_abs, P.eps_rel);
+  };
   {
     // K~x0, K~'y0; anchors / restart point; KKT_omega(z0) partials (scaled space)
     double v[4] = {0.0, 0.0, 0.0, 0.0};
@@ -545,8 +550,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       double t[kNP];
       grid_totals<kNP, (3u << 24)>(t, cur_part(), s_tot);
       const KktT ka = mk(t + 0), kc = mk(t + 4);
-      if (pass(ka, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; break; }
-      if (pass(kc, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
+      if (tpass(ka, nq0, nc0)) { status = LP_OPTIMAL; ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; break; }
+      if (tpass(kc, nq0, nc0)) { status = LP_OPTIMAL; ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
       if (certify(t + 20, xp, yp, KTyp)) break;
       if (k == P.iter_limit) {
         status = LP_ITERATION_LIMIT;
@@ -563,7 +568,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       double t[12];
       grid_totals<12, (3u << 10)>(t, cur_part(), s_tot);
       const KktT kw = mk(t);
-      if (pass(kw, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
+      if (tpass(kw, nq0, nc0)) { status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
       if (certify(t + 6, xa, ya, KTya)) break;
       if (k == P.iter_limit) { status = LP_ITERATION_LIMIT; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
       cx = xp; cy = yp; cKx = Kxp; cKTy = KTyp; metric = rP; dx2 = t[4]; dy2 = t[5];
@@ -616,7 +621,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const KktT ko = mk(t);
     lp_result r;
-    r.status = status; r.pad = 0;
+    r.status = status; r.polish = 0;
     r.iterations = k; r.attempts = jatt; r.restarts = restarts;
     r.primal_objective = ko.pobj; r.dual_objective = ko.dobj;
     r.primal_residual = ko.pres; r.dual_residual = ko.dres; r.gap = ko.gap;
@@ -679,6 +684,7 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   P.part = w;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
   P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
+  P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode;
   P.check_freq = o.check_frequency; P.alg = o.algorithm;
   // thread per row for short rows (all lanes do useful epilogue work), 8 or 32 lanes for long rows
   // G ~ mean row length / 4 (measured on B200 for this persistent kernel: 4 lanes per 20-entry

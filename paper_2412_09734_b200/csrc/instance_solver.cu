@@ -42,9 +42,10 @@ struct InstParams {
   const double *C0, *Q0, *X0, *Y0;
   int64_t cstride, qstride;
   const double *kmax, *sigma, *tab;
-  double eps_abs, eps_rel, eps_pi, eps_di;
+  double eps_abs, eps_rel, eps_pi, eps_di, eps_fp;
   int64_t iter_limit;
-  int32_t check_freq, alg, const_step;
+  int32_t check_freq, alg, const_step, polish_mode;
+  const lp_result *active;
   int64_t batch;
   unsigned long long *queue;
   double *X, *Y, *L;
@@ -225,6 +226,11 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
   const int G = P.gk, Gt = P.gkt;
   const bool cstep = P.const_step != 0;  // constant step rule (reading 34)
   const double eta0 = initial_eta(P.kmax, P.sigma, cstep);
+  // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
+  auto tpass = [&](const Kkt &k, double nq, double nc) {
+    return P.polish_mode ? polish_pass(P.polish_mode, k.pres, k.dres, nq, nc, P.eps_fp)
+                         : kkt_pass(k, nq, nc, P.eps_abs, P.eps_rel);
+  };
   int rbuf = 0;
   auto redbuf = [&]() { rbuf ^= 1; return rbuf ? red1 : red0; };
 
@@ -234,6 +240,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
     __syncthreads();
     const int64_t b = (int64_t)s_inst;
     if (b >= P.batch) return;
+    if (P.active && P.active[b].status != LP_OPTIMAL) continue;  // polishing: main solve not OPTIMAL
 
     // vectors of this instance (pointers swap for raPDHG commits)
     double *x = base, *KTy = x + n, *xp = KTy + n, *KTyp = xp + n, *xa = KTyp + n, *KTya = xa + n,
@@ -457,7 +464,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
         } else {
           breduce<NW, 6>(v, redbuf());
           const Kkt kw = make_kkt(v);
-          if (kkt_pass(kw, nq0, nc0, P.eps_abs, P.eps_rel)) {
+          if (tpass(kw, nq0, nc0)) {
             status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break;
           }
           if (infeasible(xa, ya, Kxa, KTya)) break;   // rays from the epoch's Halpern anchor
@@ -495,10 +502,10 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
         });
         breduce<NW, kRedMax>(v, redbuf());
         const Kkt ka = make_kkt(v + 0), kc = make_kkt(v + 4);
-        if (kkt_pass(ka, nq0, nc0, P.eps_abs, P.eps_rel)) {
+        if (tpass(ka, nq0, nc0)) {
           status = LP_OPTIMAL; ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; break;
         }
-        if (kkt_pass(kc, nq0, nc0, P.eps_abs, P.eps_rel)) {
+        if (tpass(kc, nq0, nc0)) {
           status = LP_OPTIMAL; ox = x; oy = y; oKx = Kx; oKTy = KTy; break;
         }
         if (infeasible(xp, yp, Kxp, KTyp)) break;     // rays from the last step (pre-commit point)
@@ -563,7 +570,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
         const Kkt ko = make_kkt(v);
         lp_result r;
         r.status = status;
-        r.pad = 0;
+        r.polish = 0;
         r.iterations = k;
         r.attempts = jatt;
         r.restarts = restarts;
@@ -644,6 +651,7 @@ int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunc
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
   P.check_freq = o.check_frequency; P.alg = o.algorithm;
   P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
+  P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active;
   P.batch = L.batch; P.queue = queue;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   P.work = nullptr; P.work_stride = 0;

@@ -510,7 +510,7 @@ __global__ void k_final(const ShState *st, lp_result *res) {
   for (int k = 0; k < 4; ++k) t[k] = st->colsum[k] + st->rowsum[k];
   const K5 ko = mk5(t);
   lp_result r;
-  r.status = st->status; r.pad = 0;
+  r.status = st->status; r.polish = 0;
   r.iterations = st->k; r.attempts = st->j; r.restarts = st->restarts;
   r.primal_objective = ko.pobj; r.dual_objective = ko.dobj;
   r.primal_residual = ko.pres; r.dual_residual = ko.dres; r.gap = ko.gap;

@@ -21,9 +21,10 @@ struct TinyParams {
   const double *C0, *Q0, *X0, *Y0;
   int64_t cstride, qstride;
   const double *kmax, *sigma, *tab;
-  double eps_abs, eps_rel, eps_pi, eps_di;
+  double eps_abs, eps_rel, eps_pi, eps_di, eps_fp;
   int64_t iter_limit;
-  int32_t check_freq;
+  int32_t check_freq, polish_mode;
+  const lp_result *active;
   int64_t batch;
   unsigned long long *queue;
   double *X, *Y, *L;
@@ -134,6 +135,11 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
   for (int t = lane; t < 32 * CPT; t += 32) sx[t] = 0.0;
   for (int t = lane; t < 32 * RPT; t += 32) sy[t] = 0.0;
   const double eta0 = initial_eta(P.kmax, P.sigma, CS);
+  // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
+  auto tpass = [&](const K5 &k, double nq, double nc) {
+    return P.polish_mode ? polish_pass(P.polish_mode, k.pres, k.dres, nq, nc, P.eps_fp)
+                         : pass5(k, nq, nc, P.eps_abs, P.eps_rel);
+  };
   __shared__ unsigned long long s_inst;
 
   for (;;) {
@@ -142,6 +148,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
     __syncwarp();
     const int64_t b = (int64_t)s_inst;
     if (b >= P.batch) return;
+    if (P.active && P.active[b].status != LP_OPTIMAL) continue;  // polishing: main solve not OPTIMAL
     const double *c0 = P.C0 + b * P.cstride, *q0 = P.Q0 + b * P.qstride;
 
     // ---- step 2 ----
@@ -399,7 +406,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         v[6] = cacc.sy; v[7] = cacc.sx; v[8] = cacc.oy; v[9] = cacc.ox;
         wsum<10>(v);
         const K5 kw = mk5(v);
-        if (pass5(kw, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; outsel = 1; break; }
+        if (tpass(kw, nq0, nc0)) { status = LP_OPTIMAL; outsel = 1; break; }
         {
           double mv[2] = {cacc.vy, cacc.vx};
           wmax<2>(mv);
@@ -467,8 +474,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         v[20] = cacc.sy; v[21] = cacc.sx; v[22] = cacc.oy; v[23] = cacc.ox;
         wsum<24>(v);
         const K5 ka = mk5(v + 0), kc = mk5(v + 4);
-        if (pass5(ka, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; outsel = 1; break; }
-        if (pass5(kc, nq0, nc0, P.eps_abs, P.eps_rel)) { status = LP_OPTIMAL; outsel = 0; break; }
+        if (tpass(ka, nq0, nc0)) { status = LP_OPTIMAL; outsel = 1; break; }
+        if (tpass(kc, nq0, nc0)) { status = LP_OPTIMAL; outsel = 0; break; }
         {
           double mv[2] = {cacc.vy, cacc.vx};
           wmax<2>(mv);
@@ -546,7 +553,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       if (lane == 0) {
         const K5 ko = mk5(v);
         lp_result r;
-        r.status = status; r.pad = 0;
+        r.status = status; r.polish = 0;
         r.iterations = k; r.attempts = jatt; r.restarts = restarts;
         r.primal_objective = ko.pobj; r.dual_objective = ko.dobj;
         r.primal_residual = ko.pres; r.dual_residual = ko.dres; r.gap = ko.gap;
@@ -594,6 +601,7 @@ int tiny_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
   P.kmax = D.kmax; P.sigma = D.sigma; P.tab = D.tab;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit; P.check_freq = o.check_frequency;
   P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
+  P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active;
   P.batch = L.batch; P.queue = queue;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   const bool r2 = o.algorithm == LP_R2HPDHG, cs = o.step_rule == LP_STEP_CONSTANT;

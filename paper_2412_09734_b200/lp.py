@@ -52,7 +52,7 @@ class Options(C.Structure):
 
 
 class Result(C.Structure):
-    _fields_ = [("status", C.c_int32), ("pad", C.c_int32), ("iterations", C.c_int64),
+    _fields_ = [("status", C.c_int32), ("polish", C.c_int32), ("iterations", C.c_int64),
                 ("attempts", C.c_int64), ("restarts", C.c_int64),
                 ("primal_objective", C.c_double), ("dual_objective", C.c_double),
                 ("primal_residual", C.c_double), ("dual_residual", C.c_double), ("gap", C.c_double),
@@ -60,7 +60,7 @@ class Result(C.Structure):
                 ("solve_seconds", C.c_double)]
 
     def as_dict(self):
-        return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad"}
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 RESULT_DTYPE = np.dtype([(f, np.int32 if t is C.c_int32 else np.int64 if t is C.c_int64 else np.float64)
