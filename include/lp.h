@@ -197,6 +197,26 @@ int lp_solve(lp_handle h, const lp_options *o, const double *x0, const double *y
 int lp_solve_batch(lp_handle h, const lp_options *o, const double *X0, const double *Y0,
                    int32_t memory, lp_result *out);
 
+/* ---- SPO+ layer ----
+ * SPO+ loss and one subgradient over a batch: PAPER.md Eq. (spo+ loss) and
+ * Eq. (spo+ gradient), as in the training step of P:198-215.  h must be a batch
+ * handle with per-instance costs (lp_create_batch with C != NULL), or a single-LP handle;
+ * its K, q, l, u describe the feasible set S and its costs are overwritten.
+ *   C_pred (batch x n): predicted costs c^;  C_true (batch x n): realised costs c;
+ *   X_true (batch x n): x*(c);  obj_true (batch): c'x*(c).
+ * On the device: the handle's costs become 2c^ - c; the batch is solved with *o (warm != 0:
+ * started from the handle's previous solutions, the warm start of P:263 / P:411; else cold);
+ * then, per instance b with x_b the inner solution and obj_b its primal objective
+ * (2c^_b - c_b)'x_b,
+ *   loss[b] = -obj_b + 2 c^_b'x*(c_b) - obj_true[b],    grad[b] = 2 (x*(c_b) - x_b).
+ * The caller averages over the batch.  out[b] receives the inner solve's result; the
+ * inner solutions stay in the handle (lp_get_solutions).  All arrays live in `memory`
+ * (LP_HOST / LP_DEVICE); loss and grad are written, the inputs are only read.
+ * Errors: LP_ERR_BATCH_SHAPE if the handle shares one c across a batch > 1; as lp_solve_batch. */
+int lp_spo_plus(lp_handle h, const lp_options *o, const double *C_pred, const double *C_true,
+                const double *X_true, const double *obj_true, int32_t warm, int32_t memory, double *loss,
+                double *grad, lp_result *out);
+
 /* Copy out instance `instance`'s solution of the last solve, in original space:
  * x (n), y (m), reduced costs lambda = c - K'y (n).  Any pointer may be NULL. */
 int lp_get_solution(lp_handle h, int64_t instance, double *x, double *y, double *reduced_costs,

@@ -365,3 +365,98 @@ def g_infeasible(kind: str, seed: int, m1: int = 12, m2: int = 4, n: int = 24, b
     lp = stack(c, G=G, h=h, A=A, b=b, l=l, u=u, dense=dense)
     lp.meta = dict(generator="G-INFEAS", kind=kind, seed=seed)
     return lp
+
+
+# ------------------------------------------------------ G-WARCRAFT / G-KNAP --
+# Paper-shaped SPO+ workloads.
+
+WARCRAFT_TERRAIN = np.array([0.8, 1.2, 5.3, 7.7, 9.2])   # Warcraft-map vertex costs (synthetic stand-in)
+
+
+def warcraft_arcs(k: int):
+    """Directed arcs of the 8-connected k x k grid (both directions): for each node in
+    row-major order, its out-arcs to neighbours in (di, dj) order.  k = 12 gives 1012
+    arcs, k = 30 gives 6844."""
+    arcs = []
+    for i in range(k):
+        for j in range(k):
+            for di in (-1, 0, 1):
+                for dj in (-1, 0, 1):
+                    if (di or dj) and 0 <= i + di < k and 0 <= j + dj < k:
+                        arcs.append((i * k + j, (i + di) * k + j + dj))
+    return arcs
+
+
+def warcraft_lp(k: int) -> LP:
+    """PAPER.md Eq. (warcraft shortest path LP) on the 8-connected grid:
+    one equality row per node (+1 on arcs leaving it, -1 on arcs entering it),
+    q = e_s - e_t with s the top-left and t the bottom-right node, 0 <= x <= 1."""
+    arcs = warcraft_arcs(k)
+    V, E = k * k, len(arcs)
+    rows = [[] for _ in range(V)]
+    for e, (s, t) in enumerate(arcs):
+        rows[s].append((e, 1.0))
+        rows[t].append((e, -1.0))
+    row_ptr = np.zeros(V + 1, np.int64)
+    col_idx, val = [], []
+    for v in range(V):
+        ent = sorted(rows[v])
+        col_idx += [e for e, _ in ent]
+        val += [w for _, w in ent]
+        row_ptr[v + 1] = len(col_idx)
+    q = np.zeros(V)
+    q[0], q[V - 1] = 1.0, -1.0
+    lp = LP(E, 0, V, row_ptr, np.asarray(col_idx, np.int32), np.asarray(val), np.ones(E), q,
+            np.zeros(E), np.ones(E))
+    lp.meta = dict(generator="G-WARCRAFT", k=k)
+    return lp
+
+
+def warcraft_costs(k: int, batch: int, seed: int, noise: float = 0.0):
+    """Arc costs of `batch` synthetic maps: each vertex draws a terrain cost, an arc
+    costs its head vertex's terrain (entering cost); optional multiplicative noise
+    U(1 - noise, 1 + noise) stands in for a predictor's error."""
+    rng = np.random.default_rng(seed)
+    heads = np.array([t for _, t in warcraft_arcs(k)])
+    node = WARCRAFT_TERRAIN[rng.integers(0, WARCRAFT_TERRAIN.size, size=(batch, k * k))]
+    C = node[:, heads]
+    if noise:
+        C = C * rng.uniform(1.0 - noise, 1.0 + noise, size=C.shape)
+    return C
+
+
+def warcraft_optimum(k: int, c: np.ndarray) -> float:
+    """Shortest s -> t path cost by Dijkstra (costs > 0; the flow LP is totally unimodular)."""
+    import heapq
+    adj = [[] for _ in range(k * k)]
+    for e, (s, t) in enumerate(warcraft_arcs(k)):
+        adj[s].append((t, float(c[e])))
+    dist = np.full(k * k, INF)
+    dist[0] = 0.0
+    pq = [(0.0, 0)]
+    while pq:
+        d, v = heapq.heappop(pq)
+        if d > dist[v]:
+            continue
+        for t, w in adj[v]:
+            if d + w < dist[t]:
+                dist[t] = d + w
+                heapq.heappush(pq, (d + w, t))
+    return float(dist[-1])
+
+
+def knapsack_lp(N: int, d: int, seed: int, capacity: float = 500.0, dense: bool = True) -> LP:
+    """LP relaxation of the multi-dimensional knapsack of PAPER.md Eq. (knapsack)
+    as a minimisation: min -c'x s.t. -W x >= -h (d rows), 0 <= x <= 1, W_ij ~ U{3..8},
+    h_j = 500; c set per instance by knapsack_values."""
+    rng = np.random.default_rng(seed)
+    W = rng.integers(3, 9, size=(d, N)).astype(np.float64)
+    lp = stack(-np.ones(N), G=-W, h=np.full(d, -capacity), l=np.zeros(N), u=np.ones(N), dense=dense)
+    lp.meta = dict(generator="G-KNAP", N=N, d=d, seed=seed)
+    return lp
+
+
+def knapsack_values(N: int, batch: int, seed: int, deg: int = 4, noise: float = 0.0, p: int = 5):
+    """Item values by the PyEPO polynomial: c = [((B f)/sqrt(p) + 3)^deg + 1] / 3.5^deg
+    times U(1 - noise, 1 + noise); returned as the minimisation costs -c (batch x N)."""
+    return -pyepo_costs(N, batch, seed, deg=deg, noise=noise, p=p, seed_B=seed + 1)

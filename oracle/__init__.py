@@ -6,3 +6,4 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and the ``cpu_baseline`` /
 the contract and citations.
 """
 from .oracle import *  # noqa: F401,F403
+from . import spo  # noqa: F401,E402

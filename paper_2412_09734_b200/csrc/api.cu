@@ -34,6 +34,7 @@ struct lp_handle_s {
   double *X = nullptr, *Y = nullptr, *L = nullptr;
   double *X0 = nullptr, *Y0 = nullptr;  // warm-start staging
   double *pol = nullptr;                // feasibility-polishing buffers (lazily allocated)
+  double *spo = nullptr;                // SPO+ staging for host inputs / outputs (lazily allocated)
   lp_result *d_res = nullptr, *h_res = nullptr;
   unsigned long long *queue = nullptr;
   double *work = nullptr;
@@ -122,7 +123,7 @@ void free_handle(lp_handle h) {
     return;
   }
   cudaStream_t s = h->stream;
-  for (void *p : {(void *)h->arena, (void *)h->X0, (void *)h->Y0, (void *)h->work, (void *)h->pol})
+  for (void *p : {(void *)h->arena, (void *)h->X0, (void *)h->Y0, (void *)h->work, (void *)h->pol, (void *)h->spo})
     if (p) cudaFreeAsync(p, s);
   // every D2H into the pinned buffers was followed by a stream sync, so they can be recycled now
   pin_put(h->h_res, (size_t)h->batch * sizeof(lp_result));
@@ -333,6 +334,37 @@ __global__ void polish_combine_kernel(int64_t n, int64_t m, int64_t m1, const do
   }
 }
 
+// ---- SPO+ (Eq. spo+ loss P:76-78, Eq. spo+ gradient P:80-82) ----
+__global__ void spo_costs_kernel(int64_t count, const double *__restrict__ Cp, const double *__restrict__ Ct,
+                                 double *__restrict__ C0) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
+    C0[t] = 2.0 * Cp[t] - Ct[t];
+}
+
+// one CTA per instance: loss[b] = -obj_b + 2 c^_b'x*_b - obj*_b, grad[b] = 2 (x*_b - x_b)
+__global__ void spo_loss_kernel(int64_t n, const double *__restrict__ Cp, const double *__restrict__ Xt,
+                                const double *__restrict__ ot, const double *__restrict__ X,
+                                const lp_result *__restrict__ res, double *__restrict__ loss,
+                                double *__restrict__ grad) {
+  const int64_t b = blockIdx.x;
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const double xt = Xt[b * n + j];
+    s += Cp[b * n + j] * xt;
+    grad[b * n + j] = 2.0 * (xt - X[b * n + j]);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+  if (lane == 0) red[w] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) t += red[ww];
+    loss[b] = -res[b].primal_objective + 2.0 * t - ot[b];
+  }
+}
+
 int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *Y0, int32_t memory,
               lp_result *out) {
   if (!h || !out) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle or result");
@@ -505,6 +537,46 @@ int lp_solve(lp_handle h, const lp_options *o, const double *x0, const double *y
 int lp_solve_batch(lp_handle h, const lp_options *o, const double *X0, const double *Y0, int32_t memory,
                    lp_result *out) {
   return run_solve(h, o, X0, Y0, memory, out);
+}
+
+int lp_spo_plus(lp_handle h, const lp_options *o, const double *C_pred, const double *C_true,
+                const double *X_true, const double *obj_true, int32_t warm, int32_t memory, double *loss,
+                double *grad, lp_result *out) {
+  if (!h || !o || !C_pred || !C_true || !X_true || !obj_true || !loss || !grad || !out)
+    return fail(LP_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (memory != LP_HOST && memory != LP_DEVICE) return fail(LP_ERR_INVALID_ARGUMENT, "bad memory kind");
+  if (h->sharded) return fail(LP_ERR_UNSUPPORTED, "SPO+ on a sharded handle");
+  const int64_t n = h->P.n, m = h->P.m, B = h->batch;
+  if (B > 1 && h->cstride != n) return fail(LP_ERR_BATCH_SHAPE, "the handle shares one c; SPO+ needs per-instance costs");
+  if (warm && !h->solved) return fail(LP_ERR_NOT_SOLVED, "warm start requested before any solve");
+  cudaStream_t s = h->stream;
+  // device views of the inputs / outputs (staged when they live on the host)
+  const double *Cp = C_pred, *Ct = C_true, *Xt = X_true, *ot = obj_true;
+  double *dl = loss, *dg = grad;
+  if (memory == LP_HOST) {
+    if (!h->spo) TRY(dalloc(&h->spo, (size_t)(4 * B * n + 2 * B), s));
+    double *w = h->spo;
+    double *cp = w, *ct = cp + B * n, *xt = ct + B * n, *otd = xt + B * n;
+    dg = otd + B; dl = dg + B * n;
+    MPAX_CUDA(cudaMemcpyAsync(cp, C_pred, (size_t)(B * n) * sizeof(double), cudaMemcpyHostToDevice, s));
+    MPAX_CUDA(cudaMemcpyAsync(ct, C_true, (size_t)(B * n) * sizeof(double), cudaMemcpyHostToDevice, s));
+    MPAX_CUDA(cudaMemcpyAsync(xt, X_true, (size_t)(B * n) * sizeof(double), cudaMemcpyHostToDevice, s));
+    MPAX_CUDA(cudaMemcpyAsync(otd, obj_true, (size_t)B * sizeof(double), cudaMemcpyHostToDevice, s));
+    Cp = cp; Ct = ct; Xt = xt; ot = otd;
+  }
+  const int64_t cnt = B * n;
+  MPAX_LAUNCH(spo_costs_kernel, (int)std::min<int64_t>((cnt + 255) / 256, 148 * 16), 256, 0, s, cnt, Cp, Ct, h->C0);
+  MPAX_CHECK_LAUNCH();
+  // warm start from the previous inner solutions (copied by run_solve into its staging buffers)
+  TRY(run_solve(h, o, warm ? h->X : nullptr, (warm && m > 0) ? h->Y : nullptr, LP_DEVICE, out));
+  MPAX_LAUNCH(spo_loss_kernel, (int)B, 256, 0, s, n, Cp, Xt, ot, h->X, h->d_res, dl, dg);
+  MPAX_CHECK_LAUNCH();
+  if (memory == LP_HOST) {
+    MPAX_CUDA(cudaMemcpyAsync(loss, dl, (size_t)B * sizeof(double), cudaMemcpyDeviceToHost, s));
+    MPAX_CUDA(cudaMemcpyAsync(grad, dg, (size_t)(B * n) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  return LP_OK;
 }
 
 int lp_get_solution(lp_handle h, int64_t instance, double *x, double *y, double *rc, int32_t memory) {

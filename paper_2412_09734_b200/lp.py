@@ -23,7 +23,7 @@ EXPORTED_SYMBOLS = [
     "lp_get_solution", "lp_get_solutions", "lp_get_shape", "lp_get_scaling", "lp_spmv_scaled",
     "lp_kernel_launch_count", "lp_error_string", "lp_last_error_detail", "lp_destroy",
     "lp_create_sharded", "lp_create_sharded_virtual", "lp_nccl_unique_id", "lp_nccl_comm_init",
-    "lp_nccl_comm_destroy",
+    "lp_nccl_comm_destroy", "lp_spo_plus",
 ]
 
 
@@ -88,6 +88,7 @@ def lib():
             L.lp_solve.argtypes = [V, P(Options), V, V, C.c_int32, P(Result)]
             L.lp_solve_batch.argtypes = [V, P(Options), V, V, C.c_int32, V]
             L.lp_get_solution.argtypes = [V, C.c_int64, V, V, V, C.c_int32]
+            L.lp_spo_plus.argtypes = [V, P(Options), V, V, V, V, C.c_int32, C.c_int32, V, V, V]
             L.lp_get_solutions.argtypes = [V, V, V, C.c_int32]
             L.lp_get_shape.argtypes = [V, P(C.c_int64), P(C.c_int64), P(C.c_int64), P(C.c_int64)]
             L.lp_get_scaling.argtypes = [V, V, V, C.c_int32]
@@ -369,6 +370,23 @@ class BatchSolver:
         _check(lib().lp_solve_batch(self._h, C.byref(o), a.ptr, b.ptr, _same_mem([X0, Y0]), res.ctypes.data),
                "lp_solve_batch")
         return res
+
+    def spo_plus(self, C_pred, C_true, X_true, obj_true, warm=False, **opts):
+        """SPO+ loss and subgradient per instance (lp_spo_plus; Eq. spo+ loss P:76-78 and
+        Eq. spo+ gradient P:80-82): returns (loss[B], grad[B, n], results).  Inputs all on
+        the host (numpy) or all on the device (torch); outputs live where the inputs do."""
+        o = default_options(**opts)
+        mem = _same_mem([C_pred, C_true, X_true, obj_true])
+        ins = [_Arr(a, np.float64) for a in (C_pred, C_true, X_true, obj_true)]
+        B, n = self.batch, self.problem.n
+        dev = C_pred.device if _is_torch(C_pred) else self._device
+        loss = _new_out((B,), mem, dev)
+        grad = _new_out((B, n), mem, dev)
+        p = lambda t: t.data_ptr() if _is_torch(t) else t.ctypes.data
+        res = np.zeros(B, dtype=RESULT_DTYPE)
+        _check(lib().lp_spo_plus(self._h, C.byref(o), ins[0].ptr, ins[1].ptr, ins[2].ptr, ins[3].ptr,
+                                 1 if warm else 0, mem, p(loss), p(grad), res.ctypes.data), "lp_spo_plus")
+        return loss, grad, res
 
     def solutions(self, memory=LP_HOST, X=None, Y=None):
         n, m, B = self.problem.n, self.problem.m, self.batch
