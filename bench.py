@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--large-m", type=int, default=100_000)
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (1e8 nnz) whole-GPU leg")
     ap.add_argument("--no-dense", action="store_true", help="skip the C3 shared-dense-K (DMMA) leg")
+    ap.add_argument("--no-spo", action="store_true", help="skip the SPO+ (Warcraft-shaped) leg")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -372,6 +373,9 @@ def run_ours(args):
     if not args.no_dense:
         log("dense shared-K leg (C3)")
         line["dense_batch"] = dense_leg(mp, torch, dev, peaks)
+    if not args.no_spo and rank == 0:
+        log("SPO+ leg (Warcraft-shaped batches)")
+        line["spo"] = spo_leg(mp, torch, dev)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         log("cpu baseline")
         line["cpu_baseline"] = cpu_baseline(lp, C, args.alg, args.cpu_seconds)
@@ -461,6 +465,55 @@ def dense_leg(mp, torch, dev, peaks):
                              "note": "fp64 DMMA peak derived = fp64 FMA peak (148 SMs x 64 x 2 x sm_max)"}
         out[name] = d
     out["speedup_dmma_vs_per_instance"] = out["dmma"]["value"] / out["per_instance"]["value"]
+    return out
+
+
+def spo_leg(mp, torch, dev, steps=10, ks=(12, 30), batch=70):
+    """SPO+ training-step shape of P:198-215 / P:330-345: Warcraft-shaped
+    8-connected k x k grid LPs, batch 70, synthetic terrain costs and a synthetic
+    predictor whose output moves a little every step (as between optimiser steps).  One step =
+    lp_spo_plus: inner costs 2c^ - c, the batch solve (warm-started from the previous step's
+    inner solutions after the first), loss and subgradient.  Context: the paper's Table 1 average
+    iteration counts at 1e-4."""
+    out = {"workload": "Warcraft-shaped SPO+ steps: 8-connected k x k grid LPs, batch 70, 1e-4",
+           "steps": steps}
+    rng = np.random.default_rng(11)
+    for k in ks:
+        lp = lpgen.warcraft_lp(k)
+        Ct = lpgen.warcraft_costs(k, batch, seed=k)
+        prob = mp.Problem.from_lp(lp).to(dev)
+        T = lambda a: torch.as_tensor(a, device=dev)
+        # x*(c) of the dataset: precomputed once (outside the timed region) at a tight tolerance
+        bs0 = mp.BatchSolver(prob, T(Ct))
+        bs0.solve(algorithm="r2", step_rule="constant", eps_abs=1e-9, eps_rel=1e-9)
+        Xt, _ = bs0.solutions(memory=mp.LP_DEVICE)
+        bs0.close()
+        Ct_d = T(Ct)
+        ot = (Ct_d * Xt).sum(dim=1)
+        base = Ct * rng.uniform(0.5, 1.5, size=Ct.shape)
+        preds = [T(base * rng.uniform(0.97, 1.03, size=Ct.shape)) for _ in range(steps)]
+        row = {"m": lp.m, "n": lp.n, "nnz": lp.nnz}
+        for name, kw in (("rapdhg", dict(algorithm="ra")), ("r2hpdhg_constant_step",
+                                                             dict(algorithm="r2", step_rule="constant"))):
+            bs = mp.BatchSolver(prob, Ct_d)
+            bs.spo_plus(preds[0], Ct_d, Xt, ot, **kw)                # warm-up (cold)
+            stream = torch.cuda.current_stream()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            its, ok = [], True
+            e0.record(stream)
+            for s in range(steps):
+                loss, grad, res = bs.spo_plus(preds[s], Ct_d, Xt, ot, warm=s > 0, **kw)
+                its.append(float(np.mean(res["iterations"])))
+                ok &= bool((res["status"] == mp.LP_OPTIMAL).all())
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            bs.close()
+            row[name] = {"ms_per_step": ms, "value": batch / (ms * 1e-3), "unit": UNIT, "all_optimal": ok,
+                         "mean_iterations_cold": its[0], "mean_iterations_warm": float(np.mean(its[1:])),
+                         "lp_seconds_per_epoch_143_steps": ms * 143 / 1e3}
+        out[f"k{k}"] = row
     return out
 
 

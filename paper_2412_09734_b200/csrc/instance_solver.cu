@@ -27,6 +27,9 @@
 // per-CTA slice of global memory.  Each SpMV row is summed by G lanes with a
 // butterfly shuffle; every reduction is a fixed-order warp butterfly plus a
 // fixed-order sum over warps: results are bitwise deterministic.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mpax {
@@ -126,11 +129,37 @@ __device__ __forceinline__ void spmv_rows(int rows, int G, const int32_t *rp, co
                                           const double *x, F &&f) {
   constexpr int T = NW * 32;
   if (G == 1) {
-    for (int r = threadIdx.x; r < rows; r += T) {
-      double s = 0.0;
-      const int e = rp[r + 1];
-      for (int p = rp[r]; p < e; ++p) s += v[p] * x[ci[p]];
-      f(r, s);
+    // four rows per thread and step, their entries interleaved so that four independent
+    // load chains are in flight (each row's sum keeps its sequential order: same result)
+    constexpr int U = 4;
+    for (int r0 = threadIdx.x; r0 < rows; r0 += U * T) {
+      int a[U], e[U];
+      double s[U];
+      int len = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = r0 + u * T;
+        a[u] = r < rows ? rp[r] : 0;      // (rp / ci / v may live in shared memory: plain loads)
+        e[u] = r < rows ? rp[r + 1] : 0;
+        s[u] = 0.0;
+        len = max(len, e[u] - a[u]);
+      }
+      for (int q = 0; q < len; ++q) {
+        double w[U], xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool ok = a[u] + q < e[u];
+          const int p = ok ? a[u] + q : 0;
+          w[u] = ok ? v[p] : 0.0;
+          xv[u] = ok ? x[ci[p]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (a[u] + q < e[u]) s[u] += w[u] * xv[u];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (r0 + u * T < rows) f(r0 + u * T, s[u]);
     }
     return;
   }
@@ -660,6 +689,18 @@ int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunc
   int NW = 1;
   if (nnz > 2048 || D.n + D.m > 1024) NW = 4;
   if (nnz > 32768 || D.n + D.m > 8192) NW = 8;
+  {
+    // latency mode: a batch that leaves SMs idle gives each instance a bigger CTA (up to one
+    // thread per ~4 rows / columns), since its solve time is one CTA's per-attempt latency
+    int dev = 0, sms = 0;
+    MPAX_CUDA(cudaGetDevice(&dev));
+    MPAX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (L.batch <= 2 * (int64_t)sms) {
+      const int64_t want = (std::max(D.n, D.m) + 4 * 32 - 1) / (4 * 32);
+      while (NW < 32 && NW < want) NW *= 2;
+    }
+    if (const char *e = getenv("MPAX_INST_NW")) NW = atoi(e);
+  }
   P.gk = pow2_floor(D.avg_row / 4.0);
   P.gkt = pow2_floor(D.avg_col / 4.0);
   const size_t vec_bytes = (size_t)8 * (size_t)(D.n + D.m) * sizeof(double);
@@ -668,8 +709,11 @@ int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunc
   const size_t red_bytes = (size_t)2 * NW * kRedMax * sizeof(double);
   switch (NW) {
     case 1: return launch<1>(P, red_bytes, vec_bytes, mat_bytes, s, work, work_bytes);
+    case 2:
     case 4: return launch<4>(P, red_bytes, vec_bytes, mat_bytes, s, work, work_bytes);
-    default: return launch<8>(P, red_bytes, vec_bytes, mat_bytes, s, work, work_bytes);
+    case 8: return launch<8>(P, red_bytes, vec_bytes, mat_bytes, s, work, work_bytes);
+    case 16: return launch<16>(P, red_bytes, vec_bytes, mat_bytes, s, work, work_bytes);
+    default: return launch<32>(P, red_bytes, vec_bytes, mat_bytes, s, work, work_bytes);
   }
 }
 
