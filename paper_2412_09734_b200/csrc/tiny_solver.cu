@@ -8,6 +8,8 @@
 // gathered by the SpMVs (x' and y', and the average at checks) go through
 // shared memory.  Same arithmetic, in the same order, as the generic
 // instance_kernel (instance_solver.cu) and the grid kernel; DESIGN.md §3.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mpax {
@@ -247,6 +249,9 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       // Branch-free: the commit is computed every attempt and selected by `pending`
       // (theta_p = 0 leaves the average bit-identical), so the attempt is one basic block.
       const double tau = eta * inv_omega, sigma = eta * omega;
+      // raPDHG's averaging weight if this attempt is accepted (depends on eta and W only):
+      // its division runs here, off the post-reduction critical path (same operations)
+      const double W1c = W_ + eta, theta_c = R2 ? 0.0 : eta / W1c;
       const double theta_p = pending ? theta : 0.0;
       double f1 = 0.0, f2 = 0.0;
       if (!CS) step_factors(P.tab, jatt + 1, f1, f2);
@@ -278,9 +283,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         const double d = xp[t] - x[t];
         dx2 += d * d;
       }
-      // the ||dx||^2 butterfly does not depend on phase B: issue it now so it overlaps
       double vdx[1] = {dx2};
-      if (need) wsum<1>(vdx);
       __syncwarp();
       // ================= phase B: [commit m-side] + SpMV #1 + dual step =================
       double dy2 = 0.0, I = 0.0;
@@ -310,7 +313,11 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       }
       pending = false;
       double v3[2] = {dy2, I};
-      if (need) wsum<2>(v3);
+      if (need) {  // ||dx||^2, ||dy||^2, <dy, K dx> in one butterfly (one 5-level dependency chain)
+        double v4[3] = {vdx[0], v3[0], v3[1]};
+        wsum<3>(v4);
+        vdx[0] = v4[0]; v3[0] = v4[1]; v3[1] = v4[2];
+      }
       ++jatt;
       const double M = omega * vdx[0] + v3[0] * inv_omega;
       const double Iv = v3[1];
@@ -325,9 +332,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       rejects = 0;
       double rP = 0.0;
       if (!R2) {
-        const double W1 = W_ + eta_used;
-        theta = eta_used / W1;
-        W_ = W1;
+        theta = theta_c;
+        W_ = W1c;
       } else {
         // r_P is read only as the restart reference (k_in = 0) and as the check metric:
         // skip its division and square root on the other attempts (they sit on the
