@@ -353,7 +353,8 @@ def run_ours(args):
                 "ms_per_step": ms_e2e / args.steps},
         "gpu_launches": int(launches),
         "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp64_peak, "traffic": None,
+                     "frac": achieved / fp64_peak, "traffic": _traffic("tiny_kernel_c2", "bytes_per_launch"),
+                     "traffic_source": "profiles/traffic.json (ncu --set full capture, per launch)",
                      "kernel": "tiny_kernel<0,1,2,4,4> (raPDHG, register-resident warp per LP)", "kernel_ms": kern_ms,
                      "flops_per_launch": flops,
                      "note": "fp64 FMA peak derived (148 SMs x 64 DFMA/clk x 2 x sm_max); per-instance solves "
@@ -384,6 +385,15 @@ def run_ours(args):
     if ws > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def _traffic(key, field):
+    """DRAM bytes (per launch, or per attempt for the grid kernel, like `achieved`) of a kernel from
+    the committed ncu captures (profiles/traffic.json), or None."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[key][field])
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def attempt_bytes(n, m, nnz, alg):
@@ -432,7 +442,9 @@ def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4"
                     "rel_kkt": best["rel_kkt"], "objective_rel_err": abs(best["primal_objective"] - lp.obj_star)
                     / (1 + abs(lp.obj_star)), "us_per_attempt": t * 1e6 / best["attempts"],
                     "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
-                                 "traffic": None, "kernel": "grid_kernel",
+                                 "traffic": _traffic("grid_kernel_c5" if lp.m >= 1_000_000 else "grid_kernel_c4",
+                                                     "bytes_per_attempt"), "kernel": "grid_kernel",
+                                 "traffic_source": "profiles/traffic.json (ncu --set full capture, per attempt)",
                                  "algorithmic_bytes_per_accepted_attempt": acc,
                                  "note": "working set (~70 MB) is L2-resident at C4; achieved may exceed HBM"}}
     return out
@@ -461,7 +473,9 @@ def dense_leg(mp, torch, dev, peaks):
             sm_max = peaks.get("sm_max_mhz", 1965.0)
             peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12
             d["roofline"] = {"bound": "tensor", "achieved": flops / t / 1e12, "peak": peak, "unit": "TFLOP/s",
-                             "frac": flops / t / 1e12 / peak, "traffic": None, "kernel": "dmma_kernel<4>",
+                             "frac": flops / t / 1e12 / peak, "traffic": _traffic("dmma_kernel_c3", "bytes_per_launch"),
+                            "traffic_source": "profiles/traffic.json (ncu --set full capture, per launch)",
+                            "kernel": "dmma_kernel<4>",
                              "note": "fp64 DMMA peak derived = fp64 FMA peak (148 SMs x 64 x 2 x sm_max)"}
         out[name] = d
     out["speedup_dmma_vs_per_instance"] = out["dmma"]["value"] / out["per_instance"]["value"]
