@@ -132,6 +132,10 @@ typedef struct {
   int32_t display_frequency;    /* 10, reserved */
   int32_t path;                 /* lp_path, default LP_PATH_AUTO */
   int32_t step_rule;            /* lp_step_rule, default LP_STEP_ADAPTIVE */
+  double reflection;            /* r2HPDHG reflection rho in [0, 1], default 1: z <- a((1 + rho) PDHG(z)
+                                   - rho z) + b z0; rho = 1 is the full reflection 2 PDHG(z) - z of
+                                   P:64, rho < 1 the partial reflection of SURVEY §8(f) row 4
+                                   (reading 38); unused by raPDHG */
 } lp_options;
 
 /* Feasibility polishing (reading 36).
@@ -164,7 +168,7 @@ typedef struct {
 } lp_result;
 
 /* Fills o with the Appendix defaults: 1e-4, 1e-4, 1e-8, 1e-8, 1e-6,
- * INT64_MAX, 64, LP_R2HPDHG, 0, 0, 0, 10, LP_PATH_AUTO, LP_STEP_ADAPTIVE. */
+ * INT64_MAX, 64, LP_R2HPDHG, 0, 0, 0, 10, LP_PATH_AUTO, LP_STEP_ADAPTIVE, 1.0. */
 void lp_default_options(lp_options *o);
 
 /* Create a single-LP handle: validates, uploads, builds

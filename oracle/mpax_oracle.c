@@ -76,6 +76,7 @@ typedef struct {
   int32_t feasibility_polishing;/* Appendix, default 0 (DESIGN reading 36) */
   int32_t polish_mode;          /* termination test: 0 relative KKT (contract step 5); 1 primal
                                    residual only; 2 dual residual only (the polishing sub-solves) */
+  double reflection;            /* r2HPDHG reflection rho in [0, 1], default 1 (reading 38) */
 } ora_options;
 
 /* Infeasibility certificate test on ORIGINAL-space rays (reading 35;
@@ -346,6 +347,15 @@ void ora_step_size(double eta, double omega, double dx2, double dy2, double I, i
 
 /* Halpern step with reflection, Eq. (hrpdhg):
  * z_{k+1} = (k+1)/(k+2) (2 w - z_k) + 1/(k+2) z_0 with w = PDHG(z_k). */
+/* Partial reflection (DESIGN reading 38): z <- a((1 + rho) w - rho z) + b z0;
+ * rho = 1 is the full reflection above (the same operations: 2 w and 1 z are exact). */
+void ora_halpern_rho(int64_t len, int64_t k, double rho, const double *z, const double *w, const double *z0,
+                     double *out) {
+  double a = (double)(k + 1) / (double)(k + 2);
+  double b = 1.0 / (double)(k + 2);
+  for (int64_t i = 0; i < len; ++i) out[i] = a * ((1.0 + rho) * w[i] - rho * z[i]) + b * z0[i];
+}
+
 void ora_halpern(int64_t len, int64_t k, const double *z, const double *w, const double *z0, double *out) {
   double a = (double)(k + 1) / (double)(k + 2);
   double b = 1.0 / (double)(k + 2);
@@ -671,10 +681,10 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
       /* fixed-point residual ||z - PDHG(z)||_P, P = [[I/tau, -K'], [-K, I/sigma]] */
       rP = sqrt(dmax(0.0, M / eta_used - 2.0 * I));
       if (k_in == 0) { ref = rP; ref_set = 1; }
-      ora_halpern(n, k_in, x, xp, xa, x);
-      ora_halpern(m, k_in, y, yp, ya, y);
-      ora_halpern(m, k_in, Kx, Kxp, Kxa, Kx);
-      ora_halpern(n, k_in, KTy, KTyp, KTya, KTy);
+      ora_halpern_rho(n, k_in, o->reflection, x, xp, xa, x);
+      ora_halpern_rho(m, k_in, o->reflection, y, yp, ya, y);
+      ora_halpern_rho(m, k_in, o->reflection, Kx, Kxp, Kxa, Kx);
+      ora_halpern_rho(n, k_in, o->reflection, KTy, KTyp, KTya, KTy);
     }
     k_in += 1;
 
@@ -847,6 +857,7 @@ void ora_default_options(ora_options *o) {
   o->eps_feas_polish = 1e-6;                     /* Appendix */
   o->feasibility_polishing = 0;                  /* Appendix */
   o->polish_mode = 0;
+  o->reflection = 1.0;
 }
 
 int ora_num_threads(void) {
@@ -868,7 +879,7 @@ static int check_options(const ora_options *o) {
   if (!o || !(o->eps_abs >= 0.0) || !(o->eps_rel >= 0.0) || o->iteration_limit < 1 ||
       o->check_frequency < 1 || (o->algorithm != ORA_RAPDHG && o->algorithm != ORA_R2HPDHG) ||
       o->step_rule < 0 || o->step_rule > 1 || o->power_iters < 1 || !(o->eps_feas_polish >= 0.0) ||
-      o->polish_mode < 0 || o->polish_mode > 2)
+      o->polish_mode < 0 || o->polish_mode > 2 || !(o->reflection >= 0.0 && o->reflection <= 1.0))
     return ORA_ERR_INVALID;
   return ORA_OK;
 }

@@ -45,7 +45,8 @@ class Options(C.Structure):
                 ("ruiz_iters", C.c_int32), ("pock_chambolle", C.c_int32),
                 ("step_rule", C.c_int32), ("power_iters", C.c_int32),
                 ("eps_primal_infeasible", C.c_double), ("eps_dual_infeasible", C.c_double),
-                ("eps_feas_polish", C.c_double), ("feasibility_polishing", C.c_int32), ("polish_mode", C.c_int32)]
+                ("eps_feas_polish", C.c_double), ("feasibility_polishing", C.c_int32), ("polish_mode", C.c_int32),
+                ("reflection", C.c_double)]
 
 
 class Certificate(C.Structure):
@@ -116,6 +117,8 @@ def lib():
             L.ora_num_threads.restype = C.c_int
             L.ora_set_threads.argtypes = [C.c_int]
             L.ora_spectral_norm.argtypes = [P(Problem), C.c_int32, P(C.c_double)]
+            L.ora_halpern_rho.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p]
             L.ora_certificate_test.argtypes = [P(Problem), C.c_void_p, C.c_void_p, C.c_double, C.c_double,
                                                P(Certificate)]
             _lib = L
@@ -146,7 +149,7 @@ class _Bound:
 
 def options(algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, check_frequency=64,
             ruiz_iters=10, pock_chambolle=1, step_rule=0, power_iters=200, eps_primal_infeasible=1e-8,
-            eps_dual_infeasible=1e-8, feasibility_polishing=False, eps_feas_polish=1e-6):
+            eps_dual_infeasible=1e-8, feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0):
     o = Options()
     lib().ora_default_options(C.byref(o))
     o.algorithm = R2HPDHG if algorithm in ("r2", "r2hpdhg", R2HPDHG) else RAPDHG
@@ -159,6 +162,7 @@ def options(algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, ch
     o.power_iters = power_iters
     o.eps_primal_infeasible, o.eps_dual_infeasible = eps_primal_infeasible, eps_dual_infeasible
     o.feasibility_polishing, o.eps_feas_polish = int(bool(feasibility_polishing)), eps_feas_polish
+    o.reflection = reflection
     return o
 
 
@@ -169,14 +173,15 @@ def validate(lp) -> int:
 
 def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, x0=None, y0=None,
           check_frequency=64, log_capacity=0, step_rule=0, eps_primal_infeasible=1e-8, eps_dual_infeasible=1e-8,
-          feasibility_polishing=False, eps_feas_polish=1e-6):
+          feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0):
     """Full solve (contract steps 0-6).  Returns a dict with x, y, lam, the
     result fields, and (if log_capacity) the attempt/check decision logs."""
     b = _Bound(lp)
     m = lp.m1 + lp.m2
     o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule,
                 eps_primal_infeasible=eps_primal_infeasible, eps_dual_infeasible=eps_dual_infeasible,
-                feasibility_polishing=feasibility_polishing, eps_feas_polish=eps_feas_polish)
+                feasibility_polishing=feasibility_polishing, eps_feas_polish=eps_feas_polish,
+                reflection=reflection)
     x = np.zeros(lp.n)
     y = np.zeros(m)
     lam = np.zeros(lp.n)
@@ -203,7 +208,7 @@ def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, 
 
 def solve_batch(lp, C_=None, Q=None, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None,
                 X0=None, Y0=None, check_frequency=64, threads=None, step_rule=0, eps_primal_infeasible=1e-8,
-                eps_dual_infeasible=1e-8, feasibility_polishing=False, eps_feas_polish=1e-6):
+                eps_dual_infeasible=1e-8, feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0):
     """Batch solve sharing K, l, u; one instance per OpenMP thread."""
     b = _Bound(lp)
     m = lp.m1 + lp.m2
@@ -212,7 +217,8 @@ def solve_batch(lp, C_=None, Q=None, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4,
     B = Cm.shape[0] if Cm is not None else Qm.shape[0]
     o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule,
                 eps_primal_infeasible=eps_primal_infeasible, eps_dual_infeasible=eps_dual_infeasible,
-                feasibility_polishing=feasibility_polishing, eps_feas_polish=eps_feas_polish)
+                feasibility_polishing=feasibility_polishing, eps_feas_polish=eps_feas_polish,
+                reflection=reflection)
     X = np.zeros((B, lp.n))
     Y = np.zeros((B, m))
     res = (Result * B)()
@@ -298,6 +304,14 @@ def halpern(k, z, w, z0):
     z, w, z0 = _f64(z), _f64(w), _f64(z0)
     out = np.zeros_like(z)
     lib().ora_halpern(z.size, k, z.ctypes.data, w.ctypes.data, z0.ctypes.data, out.ctypes.data)
+    return out
+
+
+def halpern_rho(k, z, w, z0, rho):
+    """Partial reflection step a((1 + rho) w - rho z) + b z0 (reading 38)."""
+    z, w, z0 = _f64(z), _f64(w), _f64(z0)
+    out = np.zeros_like(z)
+    lib().ora_halpern_rho(z.size, k, rho, z.ctypes.data, w.ctypes.data, z0.ctypes.data, out.ctypes.data)
     return out
 
 

@@ -256,6 +256,7 @@ int check_options(const lp_options *o) {
   if (o->path < LP_PATH_AUTO || o->path > LP_PATH_DMMA) return fail(LP_ERR_INVALID_ARGUMENT, "bad path");
   if (o->step_rule != LP_STEP_ADAPTIVE && o->step_rule != LP_STEP_CONSTANT)
     return fail(LP_ERR_INVALID_ARGUMENT, "bad step_rule");
+  if (!(o->reflection >= 0.0 && o->reflection <= 1.0)) return fail(LP_ERR_INVALID_ARGUMENT, "reflection not in [0, 1]");
   return LP_OK;
 }
 
@@ -500,6 +501,8 @@ void lp_default_options(lp_options *o) {
   o->verbose = 0;
   o->display_frequency = 10;
   o->path = LP_PATH_AUTO;
+  o->step_rule = LP_STEP_ADAPTIVE;
+  o->reflection = 1.0;
 }
 
 int lp_create(const lp_problem_desc *p, void *cuda_stream, lp_handle *out) {

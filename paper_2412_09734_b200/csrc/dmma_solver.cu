@@ -57,7 +57,7 @@ struct DmmaParams {
   const double *C0, *Q0, *X0, *Y0;
   int64_t cstride, qstride;
   const double *kmax, *sigma, *tab;
-  double eps_abs, eps_rel, eps_pi, eps_di, eps_fp;
+  double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
   int32_t check_freq, alg, const_step, polish_mode;
   const lp_result *active;
@@ -287,6 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
   for (int t = tid; t < np * kS; t += kThreads) S.Xc[t] = 0.0;
   const bool cstep = P.const_step != 0;  // constant step rule (reading 34)
   const double eta0 = initial_eta(P.kmax, P.sigma, cstep);
+  // r2HPDHG reflection z <- a((1 + rho) w - rho z) + b z0 (rho = 1: 2 PDHG(z) - z; reading 38)
+  const double rf1 = 1.0 + P.rho, rf0 = P.rho;
   // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
   auto tpass = [&](const K5 &k, double nq, double nc) {
     return P.polish_mode ? polish_pass(P.polish_mode, k.pres, k.dres, nq, nc, P.eps_fp)
@@ -412,8 +414,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
             P.xa[o] += I.theta * (xpv - P.xa[o]);
             xv = xpv; kt = kty;
           } else {
-            xv = I.ha * (2.0 * xpv - xv) + I.hb * P.xa[o];
-            kt = I.ha * (2.0 * kty - kt) + I.hb * P.KTya[o];
+            xv = I.ha * (rf1 * xpv - rf0 * xv) + I.hb * P.xa[o];
+            kt = I.ha * (rf1 * kty - rf0 * kt) + I.hb * P.KTya[o];
           }
           P.x[o] = xv; P.KTy[o] = kt;
         }
@@ -445,8 +447,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
             P.ya[o] += I.theta * (ypv - P.ya[o]);
             yv = ypv; kxv = kxpo;
           } else {
-            yv = I.ha * (2.0 * ypv - yv) + I.hb * P.ya[o];
-            kxv = I.ha * (2.0 * kxpo - kxv) + I.hb * P.Kxa[o];
+            yv = I.ha * (rf1 * ypv - rf0 * yv) + I.hb * P.ya[o];
+            kxv = I.ha * (rf1 * kxpo - rf0 * kxv) + I.hb * P.Kxa[o];
           }
           P.y[o] = yv; P.Kx[o] = kxv;
         }
@@ -539,8 +541,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           }
         } else {
           P.KTyp[o] = kty;
-          P.x[o] = I.ha * (2.0 * xpv - P.x[o]) + I.hb * P.xa[o];
-          P.KTy[o] = I.ha * (2.0 * kty - P.KTy[o]) + I.hb * P.KTya[o];
+          P.x[o] = I.ha * (rf1 * xpv - rf0 * P.x[o]) + I.hb * P.xa[o];
+          P.KTy[o] = I.ha * (rf1 * kty - rf0 * P.KTy[o]) + I.hb * P.KTya[o];
           if (I.check) {
             CertAcc acc;
             cert_col(acc, P.Dc[j], P.x[o], P.xa[o], P.KTy[o], P.KTya[o], P.C0[b * P.cstride + j], P.l0[j], P.u0[j]);
@@ -572,8 +574,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
             vq[s][4] = fmax(vq[s][4], acc.vy); vq[s][5] = fmax(vq[s][5], acc.vx);
           }
         } else {
-          P.y[o] = I.ha * (2.0 * ypv - P.y[o]) + I.hb * P.ya[o];
-          P.Kx[o] = I.ha * (2.0 * kxp - P.Kx[o]) + I.hb * P.Kxa[o];
+          P.y[o] = I.ha * (rf1 * ypv - rf0 * P.y[o]) + I.hb * P.ya[o];
+          P.Kx[o] = I.ha * (rf1 * kxp - rf0 * P.Kx[o]) + I.hb * P.Kxa[o];
           if (I.check) {
             CertAcc acc;
             cert_row(acc, i < m1, P.Dr[i], P.y[o], P.ya[o], P.Kx[o], P.Kxa[o], q0i);
@@ -862,7 +864,7 @@ int dmma_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
     P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
     P.check_freq = o.check_frequency; P.alg = o.algorithm;
     P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
-    P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active;
+    P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active; P.rho = o.reflection;
     P.batch = L.batch; P.queue = queue;
     const size_t BN = (size_t)L.batch * n, BM = (size_t)L.batch * m;
     double *w = work;

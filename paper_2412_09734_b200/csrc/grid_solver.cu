@@ -45,7 +45,7 @@ struct GridParams {
   double *x, *KTy, *xp, *KTyp, *xa, *KTya, *xr;   // n-side
   double *y, *Kx, *yp, *Kxp, *ya, *Kxa, *yr;      // m-side
   double *part;                                   // gridDim.x x kNP
-  double eps_abs, eps_rel, eps_pi, eps_di, eps_fp;
+  double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
   int32_t check_freq, alg, gk, gkt, const_step, polish_mode;
   double *X, *Y, *L;
@@ -258,6 +258,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   if (sqrt(tot4[0]) > 1e-10 && sqrt(tot4[1]) > 1e-10) omega = sqrt(tot4[0]) / sqrt(tot4[1]);
   const bool cstep = P.const_step != 0;  // constant step rule (reading 34)
   double eta = initial_eta(P.kmax, P.sigma, cstep);
+  // r2HPDHG reflection z <- a((1 + rho) w - rho z) + b z0 (rho = 1: 2 PDHG(z) - z; reading 38)
+  const double rf1 = 1.0 + P.rho, rf0 = P.rho;
   // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
   auto tpass = [&](const KktT &k, double nq, double nc) {
     return P.polish_mode ? polish_pass(P.polish_mode, k.pres, k.dres, nq, nc, P.eps_fp)
@@ -345,8 +347,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
             xn = o_xp; kt = s;
             KTyp[j] = s;           // becomes KTy after the pointer swap
           } else {
-            xn = ha * (2.0 * o_xp - o_x) + hb * o_xa;
-            kt = ha * (2.0 * s - o_kt) + hb * o_kta;
+            xn = ha * (rf1 * o_xp - rf0 * o_x) + hb * o_xa;
+            kt = ha * (rf1 * s - rf0 * o_kt) + hb * o_kta;
             x[j] = xn; KTy[j] = kt;
           }
           const double xnew = median3(o_ls, xn - tau * (o_cs - kt), o_us);
@@ -394,8 +396,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
               ya[i] = o_ya + theta * (o_yp - o_ya);
               kxv = o_kxp;
             } else {
-              yv = ha * (2.0 * o_yp - o_y) + hb * o_ya;
-              kxv = ha * (2.0 * o_kxp - o_kx) + hb * o_kxa;
+              yv = ha * (rf1 * o_yp - rf0 * o_y) + hb * o_ya;
+              kxv = ha * (rf1 * o_kxp - rf0 * o_kx) + hb * o_kxa;
               y[i] = yv; Kx[i] = kxv;
             }
           } else {
@@ -468,8 +470,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           if (!r2) {
             xa[j] += theta * (xp[j] - xa[j]);
           } else {
-            x[j] = ha * (2.0 * xp[j] - x[j]) + hb * xa[j];
-            KTy[j] = ha * (2.0 * s - KTy[j]) + hb * KTya[j];
+            x[j] = ha * (rf1 * xp[j] - rf0 * x[j]) + hb * xa[j];
+            KTy[j] = ha * (rf1 * s - rf0 * KTy[j]) + hb * KTya[j];
             const double dc = P.Dc[j];
             kkt_col(v, true, dc, xp[j], s, P.c0[j], cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
             const double d = xp[j] - xr[j];
@@ -483,8 +485,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           ya[i] += theta * (yp[i] - ya[i]);
         } else {
           const double ypi = yp[i], kxp = Kxp[i];
-          y[i] = ha * (2.0 * ypi - y[i]) + hb * ya[i];
-          Kx[i] = ha * (2.0 * kxp - Kx[i]) + hb * Kxa[i];
+          y[i] = ha * (rf1 * ypi - rf0 * y[i]) + hb * ya[i];
+          Kx[i] = ha * (rf1 * kxp - rf0 * Kx[i]) + hb * Kxa[i];
           kkt_row(v, true, i, m1, P.Dr[i], ypi, kxp, P.q0[i], qs[i]);
           const double d = ypi - yr[i];
           v[5] += d * d;
@@ -684,7 +686,7 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   P.part = w;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
   P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
-  P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode;
+  P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.rho = o.reflection;
   P.check_freq = o.check_frequency; P.alg = o.algorithm;
   // thread per row for short rows (all lanes do useful epilogue work), 8 or 32 lanes for long rows
   // G ~ mean row length / 4 (measured on B200 for this persistent kernel: 4 lanes per 20-entry

@@ -45,7 +45,7 @@ struct InstParams {
   const double *C0, *Q0, *X0, *Y0;
   int64_t cstride, qstride;
   const double *kmax, *sigma, *tab;
-  double eps_abs, eps_rel, eps_pi, eps_di, eps_fp;
+  double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
   int32_t check_freq, alg, const_step, polish_mode;
   const lp_result *active;
@@ -255,6 +255,8 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
   const int G = P.gk, Gt = P.gkt;
   const bool cstep = P.const_step != 0;  // constant step rule (reading 34)
   const double eta0 = initial_eta(P.kmax, P.sigma, cstep);
+  // r2HPDHG reflection z <- a((1 + rho) w - rho z) + b z0 (rho = 1: 2 PDHG(z) - z; reading 38)
+  const double rf1 = 1.0 + P.rho, rf0 = P.rho;
   // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
   auto tpass = [&](const Kkt &k, double nq, double nc) {
     return P.polish_mode ? polish_pass(P.polish_mode, k.pres, k.dres, nq, nc, P.eps_fp)
@@ -371,8 +373,8 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
             xn = xv; kt = s;
             KTyp[j] = s;           // becomes K~'y after the pointer swap
           } else {
-            xn = ha * (2.0 * xp[j] - x[j]) + hb * xa[j];
-            kt = ha * (2.0 * s - KTy[j]) + hb * KTya[j];
+            xn = ha * (rf1 * xp[j] - rf0 * x[j]) + hb * xa[j];
+            kt = ha * (rf1 * s - rf0 * KTy[j]) + hb * KTya[j];
             x[j] = xn; KTy[j] = kt;
           }
           const double xnew = median3(ls[j], xn - tau * (cs[j] - kt), us[j]);
@@ -405,8 +407,8 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
             ya[i] += theta * (yv - ya[i]);
             kxv = Kxp[i];
           } else {
-            yv = ha * (2.0 * yp[i] - y[i]) + hb * ya[i];
-            kxv = ha * (2.0 * Kxp[i] - Kx[i]) + hb * Kxa[i];
+            yv = ha * (rf1 * yp[i] - rf0 * y[i]) + hb * ya[i];
+            kxv = ha * (rf1 * Kxp[i] - rf0 * Kx[i]) + hb * Kxa[i];
             y[i] = yv; Kx[i] = kxv;
           }
         } else {
@@ -465,8 +467,8 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
             xa[j] += theta * (xp[j] - xa[j]);
           } else {
             const double xpj = xp[j];
-            x[j] = ha * (2.0 * xpj - x[j]) + hb * xa[j];
-            KTy[j] = ha * (2.0 * s - KTy[j]) + hb * KTya[j];
+            x[j] = ha * (rf1 * xpj - rf0 * x[j]) + hb * xa[j];
+            KTy[j] = ha * (rf1 * s - rf0 * KTy[j]) + hb * KTya[j];
             kkt_col(v, true, Dc[j], xpj, s, c0[j], cs[j], P.l0[j], ls[j], P.u0[j], us[j]);
             const double d = xpj - xr[j];
             v[4] += d * d;
@@ -477,8 +479,8 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
             ya[i] += theta * (yp[i] - ya[i]);
           } else {
             const double ypi = yp[i], kxp = Kxp[i];
-            y[i] = ha * (2.0 * ypi - y[i]) + hb * ya[i];
-            Kx[i] = ha * (2.0 * kxp - Kx[i]) + hb * Kxa[i];
+            y[i] = ha * (rf1 * ypi - rf0 * y[i]) + hb * ya[i];
+            Kx[i] = ha * (rf1 * kxp - rf0 * Kx[i]) + hb * Kxa[i];
             kkt_row(v, true, i, m1, Dr[i], ypi, kxp, q0[i], qs[i]);
             const double d = ypi - yr[i];
             v[5] += d * d;
@@ -680,7 +682,7 @@ int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunc
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
   P.check_freq = o.check_frequency; P.alg = o.algorithm;
   P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
-  P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active;
+  P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active; P.rho = o.reflection;
   P.batch = L.batch; P.queue = queue;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   P.work = nullptr; P.work_stride = 0;

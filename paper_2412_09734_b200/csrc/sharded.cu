@@ -42,6 +42,7 @@ struct ShState {
   // viol_y, viol_x (max); columns replicated, rows reduced across GPUs (sums, then maxima)
   double certc[6], certr[6];
   double ray_ny, ray_nx;
+  double rho;  // r2HPDHG reflection parameter (reading 38)
   unsigned int cnt_cols, cnt_rows;
 };
 
@@ -200,6 +201,7 @@ __global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, con
   if (st->halt && mode != COLS_OUT) return;
   const bool r2 = st->r2, pend = st->pending;
   const double tau = st->eta / st->omega, theta = st->theta, ha = st->ha, hb = st->hb;
+  const double rf1 = 1.0 + st->rho, rf0 = st->rho;  // reflection (reading 38)
   double v[20] = {};
   const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x, st_ = (int64_t)gridDim.x * kB;
   for (int64_t j = gt; j < n; j += st_) {
@@ -214,8 +216,8 @@ __global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, con
           V.xa[j] += theta * (xpv - V.xa[j]);
           xv = xpv; kt = kty;
         } else {
-          xv = ha * (2.0 * xpv - xv) + hb * V.xa[j];
-          kt = ha * (2.0 * kty - kt) + hb * V.KTya[j];
+          xv = ha * (rf1 * xpv - rf0 * xv) + hb * V.xa[j];
+          kt = ha * (rf1 * kty - rf0 * kt) + hb * V.KTya[j];
         }
         V.x[j] = xv; V.KTy[j] = kt;
       }
@@ -292,6 +294,7 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
   if (st->halt && mode != ROWS_OUT) return;
   const bool r2 = st->r2, pend = st->pending;
   const double sigma = st->eta * st->omega, theta = st->theta, ha = st->ha, hb = st->hb;
+  const double rf1 = 1.0 + st->rho, rf0 = st->rho;  // reflection (reading 38)
   double v[20] = {};
   const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x;
   const bool spmv = (mode == ROWS_STEP || mode == ROWS_AVG || mode == ROWS_INIT2);
@@ -317,8 +320,8 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
           V.ya[i] += theta * (ypv - V.ya[i]);
           yv = ypv; kxv = kxp;
         } else {
-          yv = ha * (2.0 * ypv - yv) + hb * V.ya[i];
-          kxv = ha * (2.0 * kxp - kxv) + hb * V.Kxa[i];
+          yv = ha * (rf1 * ypv - rf0 * yv) + hb * V.ya[i];
+          kxv = ha * (rf1 * kxp - rf0 * kxv) + hb * V.Kxa[i];
         }
         V.y[i] = yv; V.Kx[i] = kxv;
       }
@@ -528,8 +531,9 @@ __global__ void k_vreduce(double *const *ptrs, int p, int64_t count, int op_max)
   }
 }
 
-__global__ void k_set_eta0(ShState *st, const double *kmax, const double *sigma, int r2, int cstep) {
+__global__ void k_set_eta0(ShState *st, const double *kmax, const double *sigma, int r2, int cstep, double rho) {
   st->eta0 = initial_eta(kmax, sigma, cstep != 0);
+  st->rho = rho;
   st->r2 = r2;
   st->cstep = cstep;
 }
@@ -787,7 +791,7 @@ int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const dou
     MPAX_CUDA(cudaMemsetAsync(S.st, 0, sizeof(ShState), s));
     S.V.X0 = X0;                                        // full n (replicated)
     S.V.Y0 = Y0 ? Y0 + S.row_offset - (E.virt ? 0 : 0) : nullptr;
-    MPAX_LAUNCH(k_set_eta0, 1, 1, 0, s, S.st, S.P.kmax, S.P.sigma, r2 ? 1 : 0, cstep ? 1 : 0);
+    MPAX_LAUNCH(k_set_eta0, 1, 1, 0, s, S.st, S.P.kmax, S.P.sigma, r2 ? 1 : 0, cstep ? 1 : 0, o.reflection);
   }
   if (!E.virt) for (auto &S : E.sh) S.V.Y0 = Y0;        // a real rank passes its own rows
   // ---- step 2 ----

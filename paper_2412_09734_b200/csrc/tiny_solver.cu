@@ -23,7 +23,7 @@ struct TinyParams {
   const double *C0, *Q0, *X0, *Y0;
   int64_t cstride, qstride;
   const double *kmax, *sigma, *tab;
-  double eps_abs, eps_rel, eps_pi, eps_di, eps_fp;
+  double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
   int32_t check_freq, polish_mode;
   const lp_result *active;
@@ -137,6 +137,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
   for (int t = lane; t < 32 * CPT; t += 32) sx[t] = 0.0;
   for (int t = lane; t < 32 * RPT; t += 32) sy[t] = 0.0;
   const double eta0 = initial_eta(P.kmax, P.sigma, CS);
+  // r2HPDHG reflection z <- a((1 + rho) w - rho z) + b z0 (rho = 1: 2 PDHG(z) - z; reading 38)
+  const double rf1 = 1.0 + P.rho, rf0 = P.rho;
   // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
   auto tpass = [&](const K5 &k, double nq, double nc) {
     return P.polish_mode ? polish_pass(P.polish_mode, k.pres, k.dres, nq, nc, P.eps_fp)
@@ -272,8 +274,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           x[t] = pending ? xp[t] : x[t];
           KTy[t] = pending ? s : KTy[t];
         } else {
-          const double xc = ha * (2.0 * xp[t] - x[t]) + hb * xa[t];
-          const double kc = ha * (2.0 * s - KTy[t]) + hb * KTya[t];
+          const double xc = ha * (rf1 * xp[t] - rf0 * x[t]) + hb * xa[t];
+          const double kc = ha * (rf1 * s - rf0 * KTy[t]) + hb * KTya[t];
           x[t] = pending ? xc : x[t];
           KTy[t] = pending ? kc : KTy[t];
         }
@@ -297,8 +299,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           y[t] = pending ? yp[t] : y[t];
           Kx[t] = pending ? Kxp[t] : Kx[t];
         } else {
-          const double yc = ha * (2.0 * yp[t] - y[t]) + hb * ya[t];
-          const double kc = ha * (2.0 * Kxp[t] - Kx[t]) + hb * Kxa[t];
+          const double yc = ha * (rf1 * yp[t] - rf0 * y[t]) + hb * ya[t];
+          const double kc = ha * (rf1 * Kxp[t] - rf0 * Kx[t]) + hb * Kxa[t];
           y[t] = pending ? yc : y[t];
           Kx[t] = pending ? kc : Kx[t];
         }
@@ -366,8 +368,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           x[t] = xp[t];
           KTy[t] = KTyp[t];
         } else {
-          x[t] = ha * (2.0 * xp[t] - x[t]) + hb * xa[t];
-          KTy[t] = ha * (2.0 * KTyp[t] - KTy[t]) + hb * KTya[t];
+          x[t] = ha * (rf1 * xp[t] - rf0 * x[t]) + hb * xa[t];
+          KTy[t] = ha * (rf1 * KTyp[t] - rf0 * KTy[t]) + hb * KTya[t];
         }
       }
 #pragma unroll
@@ -378,8 +380,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           y[t] = yp[t];
           Kx[t] = Kxp[t];
         } else {
-          y[t] = ha * (2.0 * yp[t] - y[t]) + hb * ya[t];
-          Kx[t] = ha * (2.0 * Kxp[t] - Kx[t]) + hb * Kxa[t];
+          y[t] = ha * (rf1 * yp[t] - rf0 * y[t]) + hb * ya[t];
+          Kx[t] = ha * (rf1 * Kxp[t] - rf0 * Kx[t]) + hb * Kxa[t];
         }
       }
       double metric, dx2c, dy2c;
@@ -607,7 +609,7 @@ int tiny_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
   P.kmax = D.kmax; P.sigma = D.sigma; P.tab = D.tab;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit; P.check_freq = o.check_frequency;
   P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
-  P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active;
+  P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active; P.rho = o.reflection;
   P.batch = L.batch; P.queue = queue;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   const bool r2 = o.algorithm == LP_R2HPDHG, cs = o.step_rule == LP_STEP_CONSTANT;

@@ -48,7 +48,8 @@ class Options(C.Structure):
                 ("eps_dual_infeasible", C.c_double), ("eps_feas_polish", C.c_double),
                 ("iteration_limit", C.c_int64), ("check_frequency", C.c_int32), ("algorithm", C.c_int32),
                 ("warm_start", C.c_int32), ("feasibility_polishing", C.c_int32), ("verbose", C.c_int32),
-                ("display_frequency", C.c_int32), ("path", C.c_int32), ("step_rule", C.c_int32)]
+                ("display_frequency", C.c_int32), ("path", C.c_int32), ("step_rule", C.c_int32),
+                ("reflection", C.c_double)]
 
 
 class Result(C.Structure):

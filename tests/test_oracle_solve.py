@@ -165,3 +165,37 @@ def test_constant_step_variant(alg):
         dp = lpgen.grid_dp_optimum(5, C[b])
         assert res[b]["status"] == oracle.OPTIMAL and abs(res[b]["primal_objective"] - dp) <= 1e-3 * (1 + dp)
         assert res[b]["attempts"] == res[b]["iterations"]
+
+
+# ---- partial reflection (reading 38) ----
+
+def test_partial_reflection_step_pins():
+    rng = np.random.default_rng(5)
+    z, w, z0 = rng.normal(size=(3, 17))
+    for k in (0, 3, 40):
+        # rho = 1 is the full reflection of P:64, the same operations bit for bit
+        assert np.array_equal(oracle.halpern_rho(k, z, w, z0, 1.0), oracle.halpern(k, z, w, z0))
+        # a fixed point of the PDHG map (w = z) anchored at itself stays put for every rho
+        for rho in (0.0, 0.3, 1.0):
+            assert np.allclose(oracle.halpern_rho(k, z, z, z, rho), z, rtol=1e-15, atol=1e-15)
+    # rho = 0, k = 0: plain Halpern on PDHG, (w + z0) / 2 (a = b = 1/2)
+    assert np.allclose(oracle.halpern_rho(0, z, w, z0, 0.0), 0.5 * w + 0.5 * z0, rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("rho", [0.0, 0.5, 0.9])
+def test_partial_reflection_solves(rho):
+    """Partial reflection reaches the same optima (constructed G-RAND optimum, grid DP);
+    rho = 1 is bitwise the default; rho outside [0, 1] is rejected."""
+    lp = lpgen.g_rand(50, 100, 10, seed=1)
+    r = oracle.solve(lp, "r2", reflection=rho)
+    assert r["status"] == oracle.OPTIMAL
+    assert abs(r["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
+    grid, C = lpgen.g_grid(batch=32)
+    _, _, res = oracle.solve_batch(grid, C, None, "r2", reflection=rho)
+    for b in range(32):
+        dp = lpgen.grid_dp_optimum(5, C[b])
+        assert res[b]["status"] == oracle.OPTIMAL and abs(res[b]["primal_objective"] - dp) <= 1e-3 * (1 + dp)
+    a, b_ = oracle.solve(lp, "r2", reflection=1.0), oracle.solve(lp, "r2")
+    assert np.array_equal(a["x"], b_["x"]) and a["attempts"] == b_["attempts"]
+    with pytest.raises(ValueError):
+        oracle.solve(lp, "r2", reflection=1.5)
