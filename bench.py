@@ -235,21 +235,21 @@ def run_ours(args):
     X_d = torch.empty((args.batch, lp.n), dtype=torch.float64, device=dev)
     Y_d = torch.empty((args.batch, lp.m), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
-    def step(prob, Cx, X, Y, mem, alg=args.alg, rule="adaptive"):
+    def step(prob, Cx, X, Y, mem, alg=args.alg, rule="adaptive", rho=1.0):
         bs = mp.BatchSolver(prob, Cx)
         # iteration_limit: safety net; every instance must be OPTIMAL
-        res = bs.solve(algorithm=alg, iteration_limit=200_000, step_rule=rule)
+        res = bs.solve(algorithm=alg, iteration_limit=200_000, step_rule=rule, reflection=rho)
         bs.solutions(memory=mem, X=X, Y=Y)
         bs.close()
         return res
 
-    def timed(prob, Cx, X, Y, mem, steps, collect, alg=args.alg, rule="adaptive"):
+    def timed(prob, Cx, X, Y, mem, steps, collect, alg=args.alg, rule="adaptive", rho=1.0):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         all_res = []
         for s in range(steps):
             flush.zero_()                       # evict L2 between steps (outside the event pair)
             ev[s][0].record(stream)
-            res = step(prob, Cx, X, Y, mem, alg, rule)
+            res = step(prob, Cx, X, Y, mem, alg, rule, rho)
             ev[s][1].record(stream)
             if collect:
                 all_res.append(res)
@@ -293,26 +293,31 @@ def run_ours(args):
     # ---- constant-step variants (reading 34), same workload ----
     log("constant-step variants")
     var_ms, var_res = {}, {}
-    for va in ("r2", "ra"):
-        step(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, va, "constant")
+    # (name, algorithm, step rule, reflection): SURVEY §8(f) row 4, readings 34 and 38
+    VARIANTS = (("r2hpdhg_constant_step", "r2", "constant", 1.0), ("rapdhg_constant_step", "ra", "constant", 1.0),
+                ("r2hpdhg_partial_reflection_0.8", "r2", "adaptive", 0.8))
+    for name, va, rule, rho in VARIANTS:
+        step(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, va, rule, rho)
         barrier()
-        var_ms[va], var_res[va] = timed(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, args.secondary_steps, True, va,
-                                        "constant")
+        var_ms[name], var_res[name] = timed(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, args.secondary_steps, True, va,
+                                            rule, rho)
         barrier()
-    t = torch.tensor([ms, ms_e2e, ms2, var_ms["r2"], var_ms["ra"]], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms, ms_e2e, ms2] + [var_ms[v[0]] for v in VARIANTS], dtype=torch.float64, device=dev)
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms, ms_e2e, ms2 = float(t[0]), float(t[1]), float(t[2])
-    var_ms = {"r2": float(t[3]), "ra": float(t[4])}
+    var_ms = {v[0]: float(t[3 + i]) for i, v in enumerate(VARIANTS)}
     variants = {}
-    for va in ("r2", "ra"):
-        itv = np.array([r["iterations"] for r in var_res[va][-1]])
-        variants[("r2hpdhg" if va == "r2" else "rapdhg") + "_constant_step"] = {
-            "value": args.batch * args.secondary_steps * ws / (var_ms[va] * 1e-3), "unit": UNIT,
-            "ms_per_step": var_ms[va] / args.secondary_steps,
-            "all_optimal": all(r["status"] == mp.LP_OPTIMAL for res in var_res[va] for r in res),
-            "iterations": {"p50": float(np.median(itv)), "p99": float(np.percentile(itv, 99)), "max": int(itv.max())},
-            "step": "eta = 0.998 / sigma_max(K~), 200 power iterations (inside the timed step)"}
+    for name, va, rule, rho in VARIANTS:
+        itv = np.array([r["iterations"] for r in var_res[name][-1]])
+        variants[name] = {
+            "algorithm": "r2hpdhg" if va == "r2" else "rapdhg", "step_rule": rule, "reflection": rho,
+            "value": args.batch * args.secondary_steps * ws / (var_ms[name] * 1e-3), "unit": UNIT,
+            "ms_per_step": var_ms[name] / args.secondary_steps,
+            "all_optimal": all(r["status"] == mp.LP_OPTIMAL for res in var_res[name] for r in res),
+            "iterations": {"p50": float(np.median(itv)), "p99": float(np.percentile(itv, 99)), "max": int(itv.max())}}
+        if rule == "constant":
+            variants[name]["step"] = "eta = 0.998 / sigma_max(K~), 200 power iterations (inside the timed step)"
     it2 = np.array([r["iterations"] for r in res2[-1]])
     secondary = {"algorithm": "r2hpdhg" if alg2 == "r2" else "rapdhg",
                  "value": args.batch * args.secondary_steps * ws / (ms2 * 1e-3), "unit": UNIT,
