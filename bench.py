@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (1e8 nnz) whole-GPU leg")
     ap.add_argument("--no-dense", action="store_true", help="skip the C3 shared-dense-K (DMMA) leg")
     ap.add_argument("--no-spo", action="store_true", help="skip the SPO+ (Warcraft-shaped) leg")
+    ap.add_argument("--c5-sharded", action="store_true",
+                    help="run the C5 leg on the row-sharded NCCL engine even at one rank (it is used for N > 1)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -373,7 +375,12 @@ def run_ours(args):
     if not args.no_large:
         log("large-LP leg (C4)")
         line["large_lp"] = large_lp_leg(mp, torch, dev, stream, peaks, args)
-    if not args.no_c5 and rank == 0:
+    if not args.no_c5 and (ws > 1 or args.c5_sharded):
+        log("large-LP leg (C5, 1e8 nnz), row-sharded over the ranks (NCCL)")
+        c5 = c5_sharded_leg(mp, torch, dev, ws, rank, args)
+        if rank == 0:
+            line["c5_sharded"] = c5
+    elif not args.no_c5 and rank == 0:
         log("large-LP leg (C5, 1e8 nnz)")
         line["c5"] = large_lp_leg(mp, torch, dev, stream, peaks, args, m=5_000_000, seed=5, label="C5", reps=1)
     if not args.no_dense:
@@ -452,6 +459,49 @@ def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4"
                                  "traffic_source": "profiles/traffic.json (ncu --set full capture, per attempt)",
                                  "algorithmic_bytes_per_accepted_attempt": acc,
                                  "note": "working set (~70 MB) is L2-resident at C4; achieved may exceed HBM"}}
+    return out
+
+
+def c5_sharded_leg(mp, torch, dev, ws, rank, args, m=5_000_000, seed=5):
+    """C5 = G-RAND(5e6, 1e7, 20, seed 5) row-sharded over the job's ranks (SURVEY §8(e) variant A):
+    each rank holds an nnz-balanced block of rows, the n-long K~'y partials and the scalar
+    partials are ncclAllReduce'd every attempt.  Time to 1e-4 = max over ranks of the
+    library's device-timed solve (strong scaling: the LP is fixed)."""
+    import torch.distributed as tdist
+    t0 = time.time()
+    lp = lpgen.g_rand(m, 2 * m, 20, seed=seed)
+    gen_s = time.time() - t0
+    cuts = mp.row_partition(lp.row_ptr, ws)
+    r0, r1 = cuts[rank], cuts[rank + 1]
+    loc = mp.local_rows(mp.Problem.from_lp(lp), r0, r1).to(dev)
+    uid = [mp.nccl_unique_id() if rank == 0 else None]
+    if ws > 1:
+        tdist.broadcast_object_list(uid, src=0)
+    comm = mp.nccl_comm_init(ws, uid[0], rank)
+    out = {"workload": f"C5: G-RAND({m}, {2 * m}, 20, seed {seed}), one LP row-sharded over {ws} GPU(s) "
+                       f"(NCCL all-reduce of K~'y partials), to 1e-4",
+           "nnz": lp.nnz, "ranks": ws, "rows_per_rank_max": int(max(np.diff(cuts))), "generate_s": gen_s,
+           "scaling": "strong"}
+    try:
+        with mp.ShardedSolver(loc, global_row_offset=r0, m1_global=lp.m1, m2_global=lp.m2, comm=comm, rank=rank,
+                              nranks=ws) as s:
+            for alg in ("ra",):
+                s.solve(algorithm=alg, iteration_limit=20_000)                 # warm-up
+                if ws > 1:
+                    tdist.barrier()
+                r = s.solve(algorithm=alg, iteration_limit=20_000)
+                t = torch.tensor([r["solve_seconds"]], dtype=torch.float64, device=dev)
+                if ws > 1:
+                    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+                pair, acc = attempt_bytes(lp.n, lp.m, lp.nnz, alg)
+                out[alg] = {"status_optimal": r["status"] == mp.LP_OPTIMAL, "time_ms": float(t[0]) * 1e3,
+                            "iterations": r["iterations"], "attempts": r["attempts"], "restarts": r["restarts"],
+                            "rel_kkt": r["rel_kkt"],
+                            "objective_rel_err": abs(r["primal_objective"] - lp.obj_star) / (1 + abs(lp.obj_star)),
+                            "us_per_attempt": float(t[0]) * 1e6 / r["attempts"],
+                            "algorithmic_gbs_per_gpu": r["iterations"] * acc / ws / float(t[0]) / 1e9}
+    finally:
+        mp.nccl_comm_destroy(comm)
     return out
 
 
