@@ -235,6 +235,81 @@ __device__ __forceinline__ void attempt_partials(double dxe, double dxo, double 
   }
 }
 
+// Check-phase accumulators with the fragment layouts in mind (no per-instance arrays, which
+// would live in local memory): the GEMM1 epilogue of lane l touches instances 2(l%4) and
+// 2(l%4)+1 (ce, co), the row loops instance tid % 8 (r).  MX: bit k = max-reduced value.
+template <int V>
+struct FragAcc {
+  double ce[V], co[V], r[V];
+  __device__ FragAcc() {
+#pragma unroll
+    for (int k = 0; k < V; ++k) { ce[k] = 0.0; co[k] = 0.0; r[k] = 0.0; }
+  }
+};
+template <int V, unsigned MX>
+__device__ __forceinline__ void frag_col(FragAcc<V> &A, int s, const double (&t)[V]) {
+  const bool odd = s & 1;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const bool mx = (MX >> k) & 1u;
+    const double e = odd ? 0.0 : t[k], o = odd ? t[k] : 0.0;   // 0 is neutral for sums and for maxima of values >= 0
+    A.ce[k] = mx ? fmax(A.ce[k], e) : A.ce[k] + e;
+    A.co[k] = mx ? fmax(A.co[k], o) : A.co[k] + o;
+  }
+}
+template <int V, unsigned MX>
+__device__ __forceinline__ void frag_row(FragAcc<V> &A, const double (&t)[V]) {
+#pragma unroll
+  for (int k = 0; k < V; ++k) A.r[k] = ((MX >> k) & 1u) ? fmax(A.r[k], t[k]) : A.r[k] + t[k];
+}
+// FragAcc -> S.part[s][0..V) (fixed order): column parts reduced over lanes with equal l%4,
+// row parts over lanes with equal l%8, combined per instance, then warps in order.
+template <int V, unsigned MX = 0u>
+__device__ __forceinline__ void frag_partials(FragAcc<V> &A, const Smem &S) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const bool mx = (MX >> k) & 1u;
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      const double e = __shfl_xor_sync(FULL, A.ce[k], off), o = __shfl_xor_sync(FULL, A.co[k], off);
+      A.ce[k] = mx ? fmax(A.ce[k], e) : A.ce[k] + e;
+      A.co[k] = mx ? fmax(A.co[k], o) : A.co[k] + o;
+    }
+#pragma unroll
+    for (int off = 8; off < 32; off <<= 1) {
+      const double r = __shfl_xor_sync(FULL, A.r[k], off);
+      A.r[k] = mx ? fmax(A.r[k], r) : A.r[k] + r;
+    }
+  }
+  if (lane < 4) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      S.wpart[(w * kS + 2 * lane) * 24 + k] = A.ce[k];
+      S.wpart[(w * kS + 2 * lane + 1) * 24 + k] = A.co[k];
+    }
+  }
+  __syncwarp();
+  if (lane < kS) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      double *d = &S.wpart[(w * kS + lane) * 24 + k];
+      *d = ((MX >> k) & 1u) ? fmax(*d, A.r[k]) : *d + A.r[k];
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kS * V; t += kThreads) {
+    const int s = t / V, k = t % V;
+    const bool mx = (MX >> k) & 1u;
+    double acc = 0.0;
+    for (int ww = 0; ww < kThreads / 32; ++ww) {
+      const double o = S.wpart[(ww * kS + s) * 24 + k];
+      acc = mx ? fmax(acc, o) : acc + o;
+    }
+    S.part[s * 24 + k] = acc;
+  }
+}
+
 // After a cluster barrier: tot[s][k] = sum over cluster ranks (in rank order) of part.
 template <int CL, int V, unsigned MX = 0u>
 __device__ __forceinline__ void cluster_totals(cg::cluster_group &cl, const Smem &S, double *tot /* kS*24 */) {
@@ -519,8 +594,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       // Infeasibility rays (reading 35) of the checked instances: raPDHG z - (pre-step point),
       // whose pre-step values are parked in xp / KTyp / yp / Kxp (free until the next attempt),
       // r2HPDHG z - (Halpern anchor xa ...).
-      double vc[kS][6] = {};
-      double vq[kS][6] = {};  // |dy|^2, |dx|^2, dual-ray obj, c'dx | viol_y, viol_x (max)
+      FragAcc<6> vc;          // r2HPDHG KKT of w and distances (sums)
+      FragAcc<6> vq;          // |dy|^2, |dx|^2, dual-ray obj, c'dx | viol_y, viol_x (max)
       gemm1(S, np, mp, [&](int jj, int s, double kty) {
         const Inst &I = S.inst[s];
         if (jj >= jn || I.done || !I.pending) return;
@@ -536,8 +611,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           if (I.check) {
             CertAcc acc;
             cert_col(acc, P.Dc[j], xpv, xo, kty, kto, P.C0[b * P.cstride + j], P.l0[j], P.u0[j]);
-            vq[s][0] += acc.sy; vq[s][1] += acc.sx; vq[s][2] += acc.oy; vq[s][3] += acc.ox;
-            vq[s][4] = fmax(vq[s][4], acc.vy); vq[s][5] = fmax(vq[s][5], acc.vx);
+            const double t6[6] = {acc.sy, acc.sx, acc.oy, acc.ox, acc.vy, acc.vx};
+            frag_col<6, (3u << 4)>(vq, s, t6);
           }
         } else {
           P.KTyp[o] = kty;
@@ -546,11 +621,13 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           if (I.check) {
             CertAcc acc;
             cert_col(acc, P.Dc[j], P.x[o], P.xa[o], P.KTy[o], P.KTya[o], P.C0[b * P.cstride + j], P.l0[j], P.u0[j]);
-            vq[s][0] += acc.sy; vq[s][1] += acc.sx; vq[s][2] += acc.oy; vq[s][3] += acc.ox;
-            vq[s][4] = fmax(vq[s][4], acc.vy); vq[s][5] = fmax(vq[s][5], acc.vx);
-            kcol(vc[s], true, P.Dc[j], xpv, kty, P.C0[b * P.cstride + j], P.cs[o], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+            const double t6[6] = {acc.sy, acc.sx, acc.oy, acc.ox, acc.vy, acc.vx};
+            frag_col<6, (3u << 4)>(vq, s, t6);
+            double tc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            kcol(tc, true, P.Dc[j], xpv, kty, P.C0[b * P.cstride + j], P.cs[o], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
             const double d = xpv - P.xr[o];
-            vc[s][4] += d * d;
+            tc[4] = d * d;
+            frag_col<6, 0u>(vc, s, tc);
           }
         }
       });
@@ -567,11 +644,11 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           P.ya[o] += I.theta * (ypv - P.ya[o]);
           P.y[o] = ypv; P.Kx[o] = kxp;
           P.yp[o] = yo; P.Kxp[o] = kxo;
-          if (I.check) {
+          if (I.check) {   // s = tid % 8 in these row loops (kThreads is a multiple of 8)
             CertAcc acc;
             cert_row(acc, i < m1, P.Dr[i], ypv, yo, kxp, kxo, q0i);
-            vq[s][0] += acc.sy; vq[s][2] += acc.oy;
-            vq[s][4] = fmax(vq[s][4], acc.vy); vq[s][5] = fmax(vq[s][5], acc.vx);
+            const double t6[6] = {acc.sy, 0.0, acc.oy, 0.0, acc.vy, acc.vx};
+            frag_row<6, (3u << 4)>(vq, t6);
           }
         } else {
           P.y[o] = I.ha * (rf1 * ypv - rf0 * P.y[o]) + I.hb * P.ya[o];
@@ -579,11 +656,13 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           if (I.check) {
             CertAcc acc;
             cert_row(acc, i < m1, P.Dr[i], P.y[o], P.ya[o], P.Kx[o], P.Kxa[o], q0i);
-            vq[s][0] += acc.sy; vq[s][2] += acc.oy;
-            vq[s][4] = fmax(vq[s][4], acc.vy); vq[s][5] = fmax(vq[s][5], acc.vx);
-            krow(vc[s], true, i < m1, P.Dr[i], ypv, kxp, P.Q0[b * P.qstride + i], P.qs[o]);
+            const double t6[6] = {acc.sy, 0.0, acc.oy, 0.0, acc.vy, acc.vx};
+            frag_row<6, (3u << 4)>(vq, t6);
+            double tr[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            krow(tr, true, i < m1, P.Dr[i], ypv, kxp, P.Q0[b * P.qstride + i], P.qs[o]);
             const double d = ypv - P.yr[o];
-            vc[s][5] += d * d;
+            tr[5] = d * d;
+            frag_row<6, 0u>(vc, tr);
           }
         }
       }
@@ -592,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       cl.sync();  // every rank's commits (global state) visible before they are read across slices
       // certificate totals -> per-instance verdict (applied after the optimality tests)
       S.part = (S.part == S.part_a) ? S.part_b : S.part_a;
-      cta_partials<6, (3u << 4)>(vq, S);
+      frag_partials<6, (3u << 4)>(vq, S);
       cl.sync();
       cluster_totals<CL, 6, (3u << 4)>(cl, S, tot);
       if (tid < kS) {
@@ -607,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       __syncthreads();
       if (r2) {
         S.part = (S.part == S.part_a) ? S.part_b : S.part_a;
-        cta_partials<6>(vc, S);
+        frag_partials<6>(vc, S);
         cl.sync();
         cluster_totals<CL, 6>(cl, S, tot);
         if (tid < kS) {
@@ -635,8 +714,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         __syncthreads();
         gemm2(S, np, mp);
         cl.sync();
-        double v[kS][20] = {};
-        for (int t = tid; t < in_ * kS; t += kThreads) {
+        FragAcc<20> v;
+        for (int t = tid; t < in_ * kS; t += kThreads) {   // s = tid % 8
           const int ii = t / kS, s = t % kS, i = i0 + ii;
           if (!S.inst[s].check) continue;
           double kxa = 0.0;
@@ -647,13 +726,17 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           const double dr = P.Dr[i], yai = P.ya[o], yi = P.y[o], kxi = P.Kx[o], q0 = P.Q0[b * P.qstride + i],
                        qsi = P.qs[o];
           const bool ge = i < m1;
-          krow(v[s] + 0, true, ge, dr, yai, kxa, q0, qsi);
-          krow(v[s] + 4, true, ge, dr, yi, kxi, q0, qsi);
-          krow(v[s] + 8, false, ge, dr, yai, kxa, q0, qsi);
-          krow(v[s] + 12, false, ge, dr, yi, kxi, q0, qsi);
+          double tr[20];
+#pragma unroll
+          for (int k = 0; k < 20; ++k) tr[k] = 0.0;
+          krow(tr + 0, true, ge, dr, yai, kxa, q0, qsi);
+          krow(tr + 4, true, ge, dr, yi, kxi, q0, qsi);
+          krow(tr + 8, false, ge, dr, yai, kxa, q0, qsi);
+          krow(tr + 12, false, ge, dr, yi, kxi, q0, qsi);
           const double da = yai - P.yr[o], dcur = yi - P.yr[o];
-          v[s][17] += da * da;
-          v[s][19] += dcur * dcur;
+          tr[17] = da * da;
+          tr[19] = dcur * dcur;
+          frag_row<20, 0u>(v, tr);
         }
         gemm1(S, np, mp, [&](int jj, int s, double kta) {
           if (jj >= jn || !S.inst[s].check) return;
@@ -664,16 +747,20 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           const double dc = P.Dc[j], xaj = P.xa[o], xj = P.x[o], ktj = P.KTy[o];
           const double c0 = P.C0[b * P.cstride + j], csj = P.cs[o], l0 = P.l0[j], lsj = P.ls[j], u0 = P.u0[j],
                        usj = P.us[j];
-          kcol(v[s] + 0, true, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
-          kcol(v[s] + 4, true, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
-          kcol(v[s] + 8, false, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
-          kcol(v[s] + 12, false, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+          double tc[20];
+#pragma unroll
+          for (int k = 0; k < 20; ++k) tc[k] = 0.0;
+          kcol(tc + 0, true, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
+          kcol(tc + 4, true, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+          kcol(tc + 8, false, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
+          kcol(tc + 12, false, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
           const double da = xaj - P.xr[o], dcur = xj - P.xr[o];
-          v[s][16] += da * da;
-          v[s][18] += dcur * dcur;
+          tc[16] = da * da;
+          tc[18] = dcur * dcur;
+          frag_col<20, 0u>(v, s, tc);
         });
         S.part = (S.part == S.part_a) ? S.part_b : S.part_a;
-        cta_partials<20>(v, S);
+        frag_partials<20>(v, S);
         cl.sync();
         cluster_totals<CL, 20>(cl, S, tot);
         if (tid < kS) {
