@@ -128,8 +128,10 @@ typedef struct {
   int32_t algorithm;            /* lp_algorithm, default LP_R2HPDHG */
   int32_t warm_start;           /* informational; a non-NULL x0 / y0 is what warm-starts */
   int32_t feasibility_polishing;/* 0; 1: polish OPTIMAL results (see below; not on sharded handles) */
-  int32_t verbose;              /* reserved */
-  int32_t display_frequency;    /* 10, reserved */
+  int32_t verbose;              /* 0; 1: one line per display_frequency-th check of every
+                                   instance (device printf, flushed when the solve returns; tiny,
+                                   instance and grid kernels -- the DMMA and sharded engines ignore it) */
+  int32_t display_frequency;    /* 10, in checks */
   int32_t path;                 /* lp_path, default LP_PATH_AUTO */
   int32_t step_rule;            /* lp_step_rule, default LP_STEP_ADAPTIVE */
   double reflection;            /* r2HPDHG reflection rho in [0, 1], default 1: z <- a((1 + rho) PDHG(z)

@@ -47,7 +47,7 @@ struct GridParams {
   double *part;                                   // gridDim.x x kNP
   double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
-  int32_t check_freq, alg, gk, gkt, const_step, polish_mode;
+  int32_t check_freq, alg, gk, gkt, const_step, polish_mode, verbose, display_freq;
   double *X, *Y, *L;
   lp_result *res;
 };
@@ -552,6 +552,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       double t[kNP];
       grid_totals<kNP, (3u << 24)>(t, cur_part(), s_tot);
       const KktT ka = mk(t + 0), kc = mk(t + 4);
+      if (blockIdx.x == 0 && threadIdx.x == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
+        verbose_line(0, k, kc.pobj, kc.dobj, kc.pres, kc.dres, kc.gap, omega, eta);
       if (tpass(ka, nq0, nc0)) { status = LP_OPTIMAL; ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; break; }
       if (tpass(kc, nq0, nc0)) { status = LP_OPTIMAL; ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
       if (certify(t + 20, xp, yp, KTyp)) break;
@@ -570,6 +572,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       double t[12];
       grid_totals<12, (3u << 10)>(t, cur_part(), s_tot);
       const KktT kw = mk(t);
+      if (blockIdx.x == 0 && threadIdx.x == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
+        verbose_line(0, k, kw.pobj, kw.dobj, kw.pres, kw.dres, kw.gap, omega, eta);
       if (tpass(kw, nq0, nc0)) { status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
       if (certify(t + 6, xa, ya, KTya)) break;
       if (k == P.iter_limit) { status = LP_ITERATION_LIMIT; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
@@ -687,6 +691,7 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
   P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
   P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.rho = o.reflection;
+  P.verbose = o.verbose; P.display_freq = o.display_frequency;
   P.check_freq = o.check_frequency; P.alg = o.algorithm;
   // thread per row for short rows (all lanes do useful epilogue work), 8 or 32 lanes for long rows
   // G ~ mean row length / 4 (measured on B200 for this persistent kernel: 4 lanes per 20-entry

@@ -47,7 +47,7 @@ struct InstParams {
   const double *kmax, *sigma, *tab;
   double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
-  int32_t check_freq, alg, const_step, polish_mode;
+  int32_t check_freq, alg, const_step, polish_mode, verbose, display_freq;
   const lp_result *active;
   int64_t batch;
   unsigned long long *queue;
@@ -495,6 +495,8 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
         } else {
           breduce<NW, 6>(v, redbuf());
           const Kkt kw = make_kkt(v);
+          if (tid == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
+            verbose_line(b, k, kw.pobj, kw.dobj, kw.pres, kw.dres, kw.gap, omega, eta);
           if (tpass(kw, nq0, nc0)) {
             status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break;
           }
@@ -533,6 +535,8 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
         });
         breduce<NW, kRedMax>(v, redbuf());
         const Kkt ka = make_kkt(v + 0), kc = make_kkt(v + 4);
+        if (tid == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
+          verbose_line(b, k, kc.pobj, kc.dobj, kc.pres, kc.dres, kc.gap, omega, eta);
         if (tpass(ka, nq0, nc0)) {
           status = LP_OPTIMAL; ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; break;
         }
@@ -683,6 +687,7 @@ int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunc
   P.check_freq = o.check_frequency; P.alg = o.algorithm;
   P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
   P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active; P.rho = o.reflection;
+  P.verbose = o.verbose; P.display_freq = o.display_frequency;
   P.batch = L.batch; P.queue = queue;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   P.work = nullptr; P.work_stride = 0;

@@ -25,7 +25,7 @@ struct TinyParams {
   const double *kmax, *sigma, *tab;
   double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
-  int32_t check_freq, polish_mode;
+  int32_t check_freq, polish_mode, verbose, display_freq;
   const lp_result *active;
   int64_t batch;
   unsigned long long *queue;
@@ -414,6 +414,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         v[6] = cacc.sy; v[7] = cacc.sx; v[8] = cacc.oy; v[9] = cacc.ox;
         wsum<10>(v);
         const K5 kw = mk5(v);
+        if (lane == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
+          verbose_line(b, k, kw.pobj, kw.dobj, kw.pres, kw.dres, kw.gap, omega, eta);
         if (tpass(kw, nq0, nc0)) { status = LP_OPTIMAL; outsel = 1; break; }
         {
           double mv[2] = {cacc.vy, cacc.vx};
@@ -482,6 +484,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         v[20] = cacc.sy; v[21] = cacc.sx; v[22] = cacc.oy; v[23] = cacc.ox;
         wsum<24>(v);
         const K5 ka = mk5(v + 0), kc = mk5(v + 4);
+        if (lane == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
+          verbose_line(b, k, kc.pobj, kc.dobj, kc.pres, kc.dres, kc.gap, omega, eta);
         if (tpass(ka, nq0, nc0)) { status = LP_OPTIMAL; outsel = 1; break; }
         if (tpass(kc, nq0, nc0)) { status = LP_OPTIMAL; outsel = 0; break; }
         {
@@ -610,6 +614,7 @@ int tiny_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit; P.check_freq = o.check_frequency;
   P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
   P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active; P.rho = o.reflection;
+  P.verbose = o.verbose; P.display_freq = o.display_frequency;
   P.batch = L.batch; P.queue = queue;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   const bool r2 = o.algorithm == LP_R2HPDHG, cs = o.step_rule == LP_STEP_CONSTANT;
