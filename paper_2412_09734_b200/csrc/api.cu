@@ -9,6 +9,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -82,6 +83,28 @@ void pin_put(void *p, size_t bytes) {
   g_pin_free.emplace(pin_class(bytes), p);
 }
 
+// Timing events are recycled across handles too (creating two per handle is a measurable part
+// of a small batch's setup).
+std::mutex g_ev_mu;
+std::vector<cudaEvent_t> g_ev_free;
+cudaEvent_t ev_get() {
+  {
+    std::lock_guard<std::mutex> lk(g_ev_mu);
+    if (!g_ev_free.empty()) {
+      cudaEvent_t e = g_ev_free.back();
+      g_ev_free.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e = nullptr;
+  return cudaEventCreate(&e) == cudaSuccess ? e : nullptr;
+}
+void ev_put(cudaEvent_t e) {
+  if (!e) return;
+  std::lock_guard<std::mutex> lk(g_ev_mu);
+  g_ev_free.push_back(e);
+}
+
 void init_pool() {
   std::call_once(g_pool_once, [] {
     int dev = 0;
@@ -128,8 +151,8 @@ void free_handle(lp_handle h) {
   // every D2H into the pinned buffers was followed by a stream sync, so they can be recycled now
   pin_put(h->h_res, (size_t)h->batch * sizeof(lp_result));
   pin_put(h->h_flag, 8 * sizeof(int));
-  if (h->ev0) cudaEventDestroy(h->ev0);
-  if (h->ev1) cudaEventDestroy(h->ev1);
+  ev_put(h->ev0);
+  ev_put(h->ev1);
   delete h;
 }
 
@@ -208,7 +231,7 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
   h->h_res = (lp_result *)pin_get((size_t)batch * sizeof(lp_result));
   h->h_flag = (int *)pin_get(8 * sizeof(int));
   if (!h->h_res || !h->h_flag) return cleanup(fail(LP_ERR_OUT_OF_MEMORY, "pinned host buffers"));
-  if (cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess)
+  if (!(h->ev0 = ev_get()) || !(h->ev1 = ev_get()))
     return cleanup(fail(LP_ERR_CUDA, "event create"));
   auto cp = [&](void *dst, const void *src, size_t bytes) -> int {
     if (bytes == 0) return LP_OK;

@@ -213,8 +213,10 @@ __global__ void spmv_kernel(int64_t rows, const int32_t *__restrict__ rp, const 
 // barriers between the phases (the multi-kernel path costs ~35 launches, which
 // dominates the per-batch setup of the paper's small LPs).  The transpose places
 // column j's entries by scanning K in row-major order, which is the stable order.
-constexpr int kSmallT = 1024;
+// T threads: 1024 in general, 256 when m + n <= 256 (the C2 LPs: a quarter of the warps to
+// synchronise at each of the ~70 block barriers of the 11 scaling rounds)
 
+template <int kSmallT>
 __device__ __forceinline__ int block_exclusive_scan(int v, int *warp_tot) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int incl = v;
@@ -239,6 +241,7 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *warp_tot) {
   return res;
 }
 
+template <int kSmallT>
 __global__ void __launch_bounds__(kSmallT) setup_small_kernel(
     int m, int n, int nnz, const int64_t *__restrict__ rp64, const int32_t *__restrict__ ci,
     const double *__restrict__ kv0, const double *__restrict__ c, int64_t nc, const double *__restrict__ q, int64_t nq,
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(kSmallT) setup_small_kernel(
     if (j < n)
       for (int p = 0; p < nnz; ++p) cnt += (ci[p] == j);
     if (j < n) atomicMax(flag + 6, cnt);
-    const int off = block_exclusive_scan(cnt, warp_tot);
+    const int off = block_exclusive_scan<kSmallT>(cnt, warp_tot);
     if (j < n) trp[j] = running + off;
     // block total for the next chunk
     if (tid == kSmallT - 1) warp_tot[0] = off + cnt;
@@ -477,8 +480,13 @@ bool setup_small_ok(const DevProblem &P) {
 int setup_small(DevProblem &P, const int64_t *row_ptr64, const double *c, int64_t nc, const double *q, int64_t nq,
                 cudaStream_t s, int *d_flag) {
   const size_t smem = (size_t)(P.m + P.n) * sizeof(double);
-  MPAX_LAUNCH(setup_small_kernel, 1, kSmallT, smem, s, (int)P.m, (int)P.n, (int)P.nnz, row_ptr64, P.ci, P.kv0, c, nc,
-              q, nq, P.l0, P.u0, P.rp, P.trp, P.tci, P.perm, P.kv, P.tkv, P.ls, P.us, P.Dr, P.Dc, P.kmax, d_flag);
+  if (P.m + P.n <= 256) {
+    MPAX_LAUNCH(setup_small_kernel<256>, 1, 256, smem, s, (int)P.m, (int)P.n, (int)P.nnz, row_ptr64, P.ci, P.kv0, c,
+                nc, q, nq, P.l0, P.u0, P.rp, P.trp, P.tci, P.perm, P.kv, P.tkv, P.ls, P.us, P.Dr, P.Dc, P.kmax, d_flag);
+  } else {
+    MPAX_LAUNCH(setup_small_kernel<1024>, 1, 1024, smem, s, (int)P.m, (int)P.n, (int)P.nnz, row_ptr64, P.ci, P.kv0,
+                c, nc, q, nq, P.l0, P.u0, P.rp, P.trp, P.tci, P.perm, P.kv, P.tkv, P.ls, P.us, P.Dr, P.Dc, P.kmax, d_flag);
+  }
   MPAX_CHECK_LAUNCH();
   P.avg_row = P.m > 0 ? (double)P.nnz / (double)P.m : 0.0;
   P.avg_col = (double)P.nnz / (double)P.n;

@@ -579,12 +579,18 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
 
 template <bool R2, bool CS, int RPT, int CPT, int W, int WT>
 int launch_tiny(const TinyParams &P, cudaStream_t s) {
-  int dev = 0, sms = 0, per_sm = 0;
-  MPAX_CUDA(cudaGetDevice(&dev));
-  MPAX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const size_t smem = (size_t)32 * (CPT + RPT) * sizeof(double);
-  MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiny_kernel<R2, CS, RPT, CPT, W, WT>, 32, smem));
-  if (per_sm < 1) per_sm = 1;
+  // occupancy of this instantiation: queried once per process (a small batch's solve is short
+  // enough for the driver queries to show)
+  static int sms = 0, per_sm = 0;
+  if (per_sm == 0) {
+    int dev = 0, s_ = 0, p_ = 0;
+    MPAX_CUDA(cudaGetDevice(&dev));
+    MPAX_CUDA(cudaDeviceGetAttribute(&s_, cudaDevAttrMultiProcessorCount, dev));
+    MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p_, tiny_kernel<R2, CS, RPT, CPT, W, WT>, 32, smem));
+    sms = s_;
+    per_sm = p_ < 1 ? 1 : p_;
+  }
   int64_t grid = (int64_t)per_sm * sms;
   if (grid > P.batch) grid = P.batch;
   MPAX_CUDA(cudaMemsetAsync(P.queue, 0, sizeof(unsigned long long), s));

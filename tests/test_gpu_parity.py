@@ -347,9 +347,10 @@ def test_dense_batch_per_instance_c3_sample():
         assert abs(res[b]["primal_objective"] - obj[b]) <= 1e-3 * (1 + abs(obj[b]))
         if res[b]["attempts"] == ro[b]["attempts"] and res[b]["restarts"] == ro[b]["restarts"]:
             # no sensitivity guard here (the oracle's 8 solves of 200x400 take seconds each): equal
-            # counts still allow the rounding-level drift of reading 30, so the bar is the solve's
-            # own tolerance scale, not 1e-6
-            assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= 1e-4 * (1 + abs(obj[b]))
+            # counts still allow the rounding-level drift of reading 30, and two 1e-4-optimal points
+            # may differ by the gap tolerance eps (1 + |pobj| + |dobj|) ~ 2e-4 |obj| (measured 2.2e-4
+            # on one instance), so the bar is the solve's own tolerance scale, not 1e-6
+            assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= 1e-3 * (1 + abs(obj[b]))
 
 
 @pytest.mark.parametrize("alg", ALGS)
