@@ -344,7 +344,7 @@ def run_ours(args):
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     sm_max = peaks.get("sm_max_mhz", 1965.0)
-    fp64_peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12   # 148 SMs x 64 FP64 FMA/clk x 2 flop
+    fp64_peak, peak_src = _fp64_peak("fp64_dfma_tflops", sm_max)
     achieved = flops / (kern_ms * 1e-3) / 1e12
     h2d = (lp.row_ptr.nbytes + lp.col_idx.nbytes + lp.val.nbytes + lp.c.nbytes + lp.q.nbytes + lp.l.nbytes +
            lp.u.nbytes + C.nbytes)
@@ -364,8 +364,8 @@ def run_ours(args):
                      "traffic_source": "profiles/traffic.json (ncu --set full capture, per launch)",
                      "kernel": "tiny_kernel<0,1,2,4,4> (raPDHG, register-resident warp per LP)", "kernel_ms": kern_ms,
                      "flops_per_launch": flops,
-                     "note": "fp64 FMA peak derived (148 SMs x 64 DFMA/clk x 2 x sm_max); per-instance solves "
-                             "are latency-bound, see DESIGN.md §6"},
+                     "peak_source": peak_src,
+                     "note": "per-instance solves are latency-bound, see DESIGN.md §6"},
         "iterations": {"p50": float(np.median(iters)), "p99": float(np.percentile(iters, 99)),
                        "max": int(iters.max()), "attempts_total": int(atts.sum())},
         "clocks": clocks,
@@ -397,6 +397,16 @@ def run_ours(args):
     if ws > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def _fp64_peak(key, sm_max):
+    """Measured fp64 DFMA / DMMA TFLOP/s (profiles/fp64_peaks.json, scripts/micro/fp64_peak.cu on
+    this pool's B200), else the derived 148 SMs x 64 FMA/clk x 2 flop x sm_max."""
+    try:
+        v = float(json.load(open(os.path.join(ROOT, "profiles", "fp64_peaks.json")))[key])
+        return v, "measured: profiles/fp64_peaks.json (scripts/micro/fp64_peak.cu)"
+    except (OSError, KeyError, ValueError):
+        return 148 * 64 * 2 * sm_max * 1e6 / 1e12, "derived: 148 SMs x 64 FP64 FMA/clk x 2 flop x sm_max"
 
 
 def _traffic(key, field):
@@ -525,13 +535,12 @@ def dense_leg(mp, torch, dev, peaks):
             # each group of 8 runs in lock-step until its slowest instance is done: 2 GEMMs of 2*m*n*8 flops
             att = np.asarray(res["attempts"]).reshape(-1, 8).max(axis=1)
             flops = float(att.sum()) * 2 * 2 * 200 * 400 * 8
-            sm_max = peaks.get("sm_max_mhz", 1965.0)
-            peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12
+            peak, peak_src = _fp64_peak("fp64_dmma_tflops", peaks.get("sm_max_mhz", 1965.0))
             d["roofline"] = {"bound": "tensor", "achieved": flops / t / 1e12, "peak": peak, "unit": "TFLOP/s",
                              "frac": flops / t / 1e12 / peak, "traffic": _traffic("dmma_kernel_c3", "bytes_per_launch"),
                             "traffic_source": "profiles/traffic.json (ncu --set full capture, per launch)",
                             "kernel": "dmma_kernel<4>",
-                             "note": "fp64 DMMA peak derived = fp64 FMA peak (148 SMs x 64 x 2 x sm_max)"}
+                             "peak_source": peak_src}
         out[name] = d
     out["speedup_dmma_vs_per_instance"] = out["dmma"]["value"] / out["per_instance"]["value"]
     return out
