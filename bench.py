@@ -399,6 +399,30 @@ def run_ours(args):
     return 0
 
 
+def spmv_pair_leg(mp, torch, dev, prob, lp, hbm, reps=20):
+    """The SpMV pair alone (BASELINE metric "SpMV-pair GB/s vs HBM peak"): K~ v and K~' w with the
+    library's standalone SpMV kernels (lp_spmv_scaled) on device-resident vectors; algorithmic
+    B_pair = 24 nnz + 4(m+1) + 4(n+1) + 8n + 8m bytes per pair."""
+    with mp.Solver(prob) as s:
+        v = torch.rand(lp.n, dtype=torch.float64, device=dev)
+        w = torch.rand(lp.m, dtype=torch.float64, device=dev)
+        outs = (torch.empty(lp.m, dtype=torch.float64, device=dev), torch.empty(lp.n, dtype=torch.float64, device=dev))
+        for _ in range(3):
+            s.spmv_scaled(v, w, out=outs)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(torch.cuda.current_stream())
+        for _ in range(reps):
+            s.spmv_scaled(v, w, out=outs)
+        e1.record(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        t_pair = e0.elapsed_time(e1) / reps * 1e-3
+    b_pair = 24 * lp.nnz + 4 * (lp.m + 1) + 4 * (lp.n + 1) + 8 * lp.n + 8 * lp.m
+    return {"us": t_pair * 1e6, "algorithmic_bytes": b_pair, "gbs": b_pair / t_pair / 1e9,
+            "frac_of_hbm": b_pair / t_pair / 1e9 / hbm, "kernel": "spmv_kernel (standalone, x2)",
+            "note": "random-column gathers move 32-byte sectors for 8 useful bytes (DESIGN.md §6)"}
+
+
 def _fp64_peak(key, sm_max):
     """Measured fp64 DFMA / DMMA TFLOP/s (profiles/fp64_peaks.json, scripts/micro/fp64_peak.cu on
     this pool's B200), else the derived 148 SMs x 64 FMA/clk x 2 flop x sm_max."""
@@ -446,6 +470,8 @@ def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4"
     out = {"workload": f"{label}: G-RAND({m}, {2 * m}, 20, seed {seed}), one LP on the whole GPU (grid path), to 1e-4",
            "nnz": lp.nnz, "generate_s": gen_s, "create_s_wall": setup_s}
     hbm = peaks.get("hbm_gbs", 6546.6)
+    if lp.m >= 1_000_000:   # at C4 a pair is ~10 us of GPU time, below the binding's per-call host cost
+        out["spmv_pair"] = spmv_pair_leg(mp, torch, dev, prob, lp, hbm)
     for alg in ("ra", "r2"):
         with mp.Solver(prob) as s:
             log(f"large leg {alg}: warm-up")

@@ -191,21 +191,43 @@ __global__ void step_table_kernel(double *tab) {
   }
 }
 
-// Plain SpMV with the solver's scaled matrices (diagnostics / tests).
-__global__ void spmv_kernel(int64_t rows, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+// Standalone SpMV with the solver's scaled matrices (lp_spmv_scaled: parity tests and the
+// bench's SpMV-pair bandwidth): G lanes per row (G ~ mean row length / 4, as the grid kernel),
+// each lane with four entries in flight (index and value streamed evict-first, then the four
+// gathers), butterfly over the group.  Fixed order: deterministic.
+__global__ void spmv_kernel(int64_t rows, int G, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                             const double *__restrict__ v, const double *__restrict__ x, double *__restrict__ y) {
-  // one warp per row, lanes stride the row, butterfly sum
-  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = w; r < rows; r += nw) {
-    double s = 0.0;
-    for (int32_t p = rp[r] + lane; p < rp[r + 1]; p += 32) s += v[p] * x[ci[p]];
-    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
-    if (lane == 0) y[r] = s;
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / G;
+  const int gl = (int)(gt % G);
+  const int64_t iters = (rows + ng - 1) / ng;
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t r = it * ng + gt / G;
+    double s0 = 0.0, s1 = 0.0;
+    if (r < rows) {
+      const int32_t e = __ldg(rp + r + 1);
+      for (int32_t p = __ldg(rp + r) + gl; p < e; p += 4 * G) {
+        int32_t c[4];
+        double w[4], xv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int32_t q = p + k * G;
+          c[k] = q < e ? __ldcs(ci + q) : 0;
+          w[k] = q < e ? __ldcs(v + q) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xv[k] = p + k * G < e ? x[c[k]] : 0.0;
+        s0 += w[0] * xv[0];
+        s1 += w[1] * xv[1];
+        s0 += w[2] * xv[2];
+        s1 += w[3] * xv[3];
+      }
+    }
+    double s = s0 + s1;
+    for (int off = G >> 1; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    if (r < rows && gl == 0) y[r] = s;
   }
 }
-
 
 // ---- fused single-CTA setup for small LPs --------------------------------------
 // Same checks and the same arithmetic, in the same order, as validate_kernel +
@@ -494,8 +516,15 @@ int setup_small(DevProblem &P, const int64_t *row_ptr64, const double *c, int64_
 }
 
 int spmv_scaled(const DevProblem &P, const double *v, double *Kv, const double *w, double *KTw, cudaStream_t s) {
-  if (v && Kv && P.m > 0) MPAX_LAUNCH(spmv_kernel, grid_for(P.m * 32), 256, 0, s, P.m, P.rp, P.ci, P.kv, v, Kv);
-  if (w && KTw) MPAX_LAUNCH(spmv_kernel, grid_for(P.n * 32), 256, 0, s, P.n, P.trp, P.tci, P.tkv, w, KTw);
+  auto group = [](double avg) {
+    int g = 1;
+    while (g * 2 <= avg / 4.0 && g < 32) g *= 2;
+    return g;
+  };
+  const int G = group(P.avg_row), GT = group(P.avg_col);
+  const int blocks = 148 * 8;  // grid-stride over row groups: 8 CTAs of 256 threads per SM
+  if (v && Kv && P.m > 0) MPAX_LAUNCH(spmv_kernel, blocks, 256, 0, s, P.m, G, P.rp, P.ci, P.kv, v, Kv);
+  if (w && KTw) MPAX_LAUNCH(spmv_kernel, blocks, 256, 0, s, P.n, GT, P.trp, P.tci, P.tkv, w, KTw);
   MPAX_CHECK_LAUNCH();
   return LP_OK;
 }

@@ -310,13 +310,20 @@ class Solver:
         _check(lib().lp_get_scaling(self._h, Dr.ctypes.data, Dc.ctypes.data, LP_HOST), "lp_get_scaling")
         return Dr[: self.problem.m], Dc
 
-    def spmv_scaled(self, v=None, w=None):
+    def spmv_scaled(self, v=None, w=None, out=None):
+        """K~ v and K~' w with the solver's scaled matrices (lp_spmv_scaled).  Host (numpy) or
+        device (torch) inputs; device calls may pass preallocated outputs (Kv, KTw)."""
         n, m = self.problem.n, self.problem.m
+        mem = _same_mem([v, w])
         va, wa = _Arr(v, np.float64), _Arr(w, np.float64)
-        Kv = np.zeros(max(m, 1)) if v is not None else None
-        KTw = np.zeros(n) if w is not None else None
-        _check(lib().lp_spmv_scaled(self._h, va.ptr, None if Kv is None else Kv.ctypes.data, wa.ptr,
-                                    None if KTw is None else KTw.ctypes.data, LP_HOST), "lp_spmv_scaled")
+        if out is not None:
+            Kv, KTw = out
+        else:
+            dev = (v.device if _is_torch(v) else w.device) if mem == LP_DEVICE else None
+            Kv = _new_out((max(m, 1),), mem, dev) if v is not None else None
+            KTw = _new_out((n,), mem, dev) if w is not None else None
+        p = lambda t: None if t is None else (t.data_ptr() if _is_torch(t) else t.ctypes.data)
+        _check(lib().lp_spmv_scaled(self._h, va.ptr, p(Kv), wa.ptr, p(KTw), mem), "lp_spmv_scaled")
         return (None if Kv is None else Kv[:m]), KTw
 
     def close(self):
