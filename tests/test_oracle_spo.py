@@ -106,3 +106,36 @@ def test_finite_differences():
             assert abs(fd - grad[0, j]) <= 1e-4, (s, j, fd, grad[0, j])
             checked += 1
     assert checked >= 40
+
+
+def test_acceptance_9_training_loop_on_the_oracle():
+    """S:632 on the oracle: plain gradient descent on the mean SPO+ loss of a linear predictor
+    (50 knapsack samples, N = 20, d = 3, noiseless polynomial values, eps 1e-4) cuts the training
+    loss by >= 50% and reaches a normalized test regret < 5% within 30 epochs (the GPU layer is
+    held to the same bar in test_gpu_spo_training.py)."""
+    N, D, P = 20, 3, 5
+    lp = lpgen.knapsack_lp(N, D, seed=7, capacity=30.0, dense=False)
+    B = (np.random.default_rng(8).uniform(size=(N, P)) < 0.5).astype(np.float64)
+
+    def dataset(n, seed):
+        rng = np.random.default_rng(seed)
+        F = rng.normal(size=(n, P))
+        return F, -(((F @ B.T) / np.sqrt(P) + 3.0) ** 4 + 1.0) / 3.5 ** 4
+
+    Ftr, Ctr = dataset(50, 9)
+    Fte, Cte = dataset(50, 10)
+    kw = dict(step_rule=1, eps_abs=1e-4, eps_rel=1e-4)
+    Xtr, _, _ = oracle.solve_batch(lp, Ctr, None, "r2", **kw)
+    Xte, _, _ = oracle.solve_batch(lp, Cte, None, "r2", **kw)
+    otr, ote = (Ctr * Xtr).sum(1), (Cte * Xte).sum(1)
+    W, b = 0.1 * np.random.default_rng(0).normal(size=(N, P)), np.zeros(N)
+    losses = []
+    for _ in range(30):
+        loss, grad, *_ = spo_plus(lp, Ftr @ W.T + b, Ctr, Xtr, otr, "r2", **kw)
+        losses.append(loss.mean())
+        g = grad / 50
+        W -= 0.5 * (g.T @ Ftr)
+        b -= 0.5 * g.sum(0)
+    Xh, _, _ = oracle.solve_batch(lp, Fte @ W.T + b, None, "r2", **kw)
+    regret = ((Cte * Xh).sum(1) - ote).sum() / np.abs(ote).sum()
+    assert losses[-1] <= 0.5 * losses[0] and regret < 0.05, (losses[0], losses[-1], regret)
