@@ -389,6 +389,9 @@ def run_ours(args):
     if not args.no_spo and rank == 0:
         log("SPO+ leg (Warcraft-shaped batches)")
         line["spo"] = spo_leg(mp, torch, dev)
+    if rank == 0:
+        log("batch-size scaling leg (C2 shape)")
+        line["batch_scaling"] = batch_scaling_leg(mp, torch, dev)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         log("cpu baseline")
         line["cpu_baseline"] = cpu_baseline(lp, C, args.alg, args.cpu_seconds)
@@ -569,6 +572,36 @@ def dense_leg(mp, torch, dev, peaks):
                              "peak_source": peak_src}
         out[name] = d
     out["speedup_dmma_vs_per_instance"] = out["dmma"]["value"] / out["per_instance"]["value"]
+    return out
+
+
+def batch_scaling_leg(mp, torch, dev, sizes=(4096, 16384, 65536), reps=3):
+    """Context for serving: the C2 step (create + solve + get + destroy, device-resident) at larger
+    batches of the same LP shape; the headline stays at BASELINE's 1024."""
+    out = {"workload": "C2-shaped batches (5x5 grid LPs, raPDHG, 1e-4), batch size varied", "unit": UNIT}
+    for B in sizes:
+        lp, C = lpgen.g_grid(batch=B, seed=2)
+        prob = mp.Problem.from_lp(lp).to(dev)
+        Cd = torch.as_tensor(C, device=dev)
+        X = torch.empty((B, lp.n), dtype=torch.float64, device=dev)
+        Y = torch.empty((B, lp.m), dtype=torch.float64, device=dev)
+        best, ok = None, True
+        for rep in range(reps + 1):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.current_stream())
+            bs = mp.BatchSolver(prob, Cd)
+            res = bs.solve(algorithm="ra", iteration_limit=200_000)
+            bs.solutions(memory=mp.LP_DEVICE, X=X, Y=Y)
+            bs.close()
+            e1.record(torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            ok &= bool((res["status"] == mp.LP_OPTIMAL).all())
+            if rep:
+                ms = e0.elapsed_time(e1)
+                best = ms if best is None else min(best, ms)
+        out[str(B)] = {"ms_per_step": best, "value": B / (best * 1e-3), "all_optimal": ok,
+                       "max_iterations": int(res["iterations"].max())}
     return out
 
 
