@@ -48,6 +48,7 @@ struct InstParams {
   double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
   int32_t check_freq, alg, const_step, polish_mode, verbose, display_freq;
+  int32_t hyb;  // global-state mode with the SpMV gather vectors (x, x', y, y') in shared memory
   const lp_result *active;
   int64_t batch;
   unsigned long long *queue;
@@ -278,6 +279,9 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
            *xr = KTya + n, *cs = xr + n;
     double *y = cs + n, *Kx = y + m, *yp = Kx + m, *Kxp = yp + m, *ya = Kxp + m, *Kxa = ya + m, *yr = Kxa + m,
            *qs = yr + m;
+    if (!SMEM && P.hyb) {  // the vectors the SpMVs gather from live on chip (random reads hit smem)
+      x = after_red; xp = x + n; y = xp + n; yp = y + m;
+    }
     const double *c0 = P.C0 + b * P.cstride;
     const double *q0 = P.Q0 + b * P.qstride;
     const double *X0 = P.X0 ? P.X0 + b * (int64_t)n : nullptr;
@@ -637,6 +641,12 @@ int launch_cfg(const InstParams &P0, size_t smem, size_t vec_bytes, cudaStream_t
   int dev = 0, sms = 0;
   MPAX_CUDA(cudaGetDevice(&dev));
   MPAX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (!SMEM) {
+    // hybrid: x, x', y, y' (the gather sources of the two SpMVs) in shared memory when they fit
+    const size_t hyb_bytes = smem + (size_t)2 * (size_t)(P.n + P.m) * sizeof(double);
+    P.hyb = hyb_bytes <= 200 * 1024;
+    if (P.hyb) smem = hyb_bytes;
+  }
   MPAX_CUDA(cudaFuncSetAttribute(instance_kernel<NW, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, instance_kernel<NW, SMEM>, NW * 32, smem));
@@ -690,7 +700,7 @@ int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunc
   P.verbose = o.verbose; P.display_freq = o.display_frequency;
   P.batch = L.batch; P.queue = queue;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
-  P.work = nullptr; P.work_stride = 0;
+  P.work = nullptr; P.work_stride = 0; P.hyb = 0;
   // CTA size from the work per SpMV; group size from the mean row length
   const double nnz = (double)D.nnz;
   int NW = 1;
