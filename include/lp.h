@@ -15,8 +15,12 @@
  * (raPDHG) or Halpern reflection Eq. (hrpdhg) (r2HPDHG), checks of
  * termination / restart every 64 iterations, primal-weight
  * update on restart, warm start and batches of same-shape
- * instances.  Everything after argument checks runs in CUDA kernels
- * on the handle's stream; there is no CPU fallback.
+ * instances; plus the SURVEY §8(f) rows: infeasibility detection with
+ * certificate rays (reading 35), feasibility polishing
+ * (reading 36), the SPO+ layer (reading 37, lp_spo_plus),
+ * and the constant-step / partial-reflection variants (readings 34, 38).
+ * Everything after argument checks runs in CUDA kernels on the handle's stream;
+ * there is no CPU fallback.
  *
  * Conventions (all entry points):
  *  - Return value: an lp_error code (LP_OK = 0).  Output parameters are only
@@ -194,7 +198,10 @@ int lp_update_batch(lp_handle h, const double *C, const double *Q, int32_t memor
 
 /* Solve a single-LP handle.  x0 (n) / y0 (m) are an optional warm start in
  * ORIGINAL space; NULL halves start at zero.  `memory`
- * applies to x0, y0.  `out` is a host struct. */
+ * applies to x0, y0.  `out` is a host struct; out->status is OPTIMAL,
+ * PRIMAL_INFEASIBLE / DUAL_INFEASIBLE (then lp_get_solution returns the rays),
+ * ITERATION_LIMIT or NUMERICAL_ERROR.  The kernel is picked by o->path (AUTO: the
+ * persistent grid kernel for large single LPs, else the per-instance kernels). */
 int lp_solve(lp_handle h, const lp_options *o, const double *x0, const double *y0, int32_t memory,
              lp_result *out);
 
