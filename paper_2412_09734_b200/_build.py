@@ -19,9 +19,13 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libmpax_b200.so")
 BUILD = os.path.join(HERE, "build")
 DEBUG = bool(os.environ.get("MPAX_DEBUG_BUILD"))
+TRACE = bool(os.environ.get("MPAX_TRACE_BUILD"))
 if DEBUG:  # a separate library with device-side bounds checks (load it with MPAX_LIB=...)
     LIB = os.path.join(HERE, "libmpax_b200_debug.so")
     BUILD = os.path.join(HERE, "build_debug")
+elif TRACE:  # a separate library whose grid kernel prints per-phase timings (experiments only)
+    LIB = os.path.join(HERE, "libmpax_b200_trace.so")
+    BUILD = os.path.join(HERE, "build_trace")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -65,7 +69,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     nccl_inc, nccl_lib = _nccl_dirs()
-    defs = ["-DMPAX_DEBUG=1"] if DEBUG else []
+    defs = ["-DMPAX_DEBUG=1"] if DEBUG else (["-DMPAX_TRACE=1"] if TRACE else [])
     if nccl_inc:
         inc += ["-I", nccl_inc]
         defs += ["-DMPAX_HAVE_NCCL=1"]

@@ -20,11 +20,15 @@
 // Data layout: CSR of K~ and of K~' (int32 offsets/indices, fp64 values), all
 // vectors fp64 SoA.  The matrices are streamed with evict-first loads; the
 // gathered vector (x' in phase B, y' in phase A) uses the default policy so it
-// can stay L2-resident.  Each row is summed by G lanes (butterfly), G from the
-// mean row length.  Results are bitwise deterministic.
+// can stay L2-resident.  Short rows (mean <= 48, as in C4/C5) use the warp-tile
+// CSR-stream mapping (one warp per 32 consecutive rows, coalesced chunks, each lane
+// sums and finishes its own row); long rows are summed by G lanes (butterfly), G from
+// the mean row length.  Results are bitwise deterministic.
 #include <cooperative_groups.h>
 
 #include <stdlib.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -45,9 +49,10 @@ struct GridParams {
   double *x, *KTy, *xp, *KTyp, *xa, *KTya, *xr;   // n-side
   double *y, *Kx, *yp, *Kxp, *ya, *Kxa, *yr;      // m-side
   double *part;                                   // gridDim.x x kNP
+  double *tpart;                                  // 2 x blocks x ceil(tiles / blocks): per-tile partials
   double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
-  int32_t check_freq, alg, gk, gkt, const_step, polish_mode, verbose, display_freq;
+  int32_t check_freq, alg, gk, gkt, const_step, polish_mode, verbose, display_freq, vpol, tdist, dyn;
   double *X, *Y, *L;
   lp_result *res;
 };
@@ -90,37 +95,38 @@ __device__ __forceinline__ void kkt_col(double *v, bool orig, double dc, double 
   if (u < INFINITY) v[3] -= u * lm;
 }
 
+#ifdef MPAX_TRACE
+// Phase timers (trace build only, MPAX_TRACE_BUILD=1): CTA 0 / the last CTA, thread 0.
+__device__ __forceinline__ unsigned long long tnow() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TR(...) __VA_ARGS__
+#else
+#define TR(...)
+#endif
+
+__device__ __forceinline__ void st_evict_last(double *p, double v) {
+  asm volatile("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+               "st.global.L2::cache_hint.f64 [%0], %1, pol;\n\t}" :: "l"(p), "d"(v) : "memory");
+}
+
 // streamed (evict-first) loads of the matrices
 __device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
 __device__ __forceinline__ int32_t ld_stream(const int32_t *p) { return __ldcs(p); }
 
-// Sum of row r of a CSR matrix times x, G lanes per row (all lanes get the sum).
-// Each lane takes its entries four at a time (index and value loads first, then
-// the four gathers, then the FMAs) so that twelve loads are in flight per lane;
-// two interleaved accumulators.  Fixed order: deterministic.
-__device__ __forceinline__ double row_dot(int64_t r, bool valid, int G, int gl, const int32_t *__restrict__ rp,
-                                          const int32_t *__restrict__ ci, const double *__restrict__ v,
-                                          const double *x) {
+// Sum of row r of a CSR matrix times x (all lanes of the row's group get the sum).
+// G == 1: warp-tile CSR-stream (common.cuh tile_row_dot): the warp's 32 consecutive rows,
+// one per lane, streamed coalesced; no idle lanes in the epilogue.
+// G >= 2: G lanes per row, each taking its entries four at a time (index and value loads
+// first, then the four gathers, then the FMAs) so that twelve loads are in flight per lane;
+// two interleaved accumulators, butterfly over the group.  Fixed order: deterministic.
+__device__ __forceinline__ double row_dot(int64_t r, bool valid, int rows, int G, int gl,
+                                          const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                          const double *__restrict__ v, const double *x, double *tbuf) {
+  if (G == 1) return tile_row_dot((int)r, valid, rows, rp, ci, v, x, tbuf);
   double s0 = 0.0, s1 = 0.0;
-  if (G == 1) {  // thread per row: no idle lanes in the epilogue, four entries per step in flight
-    if (valid) {
-      const int32_t e = __ldg(rp + r + 1);
-      int32_t p = __ldg(rp + r);
-      for (; p + 3 < e; p += 4) {
-        const int32_t c0 = ld_stream(ci + p), c1 = ld_stream(ci + p + 1), c2 = ld_stream(ci + p + 2),
-                      c3 = ld_stream(ci + p + 3);
-        const double w0 = ld_stream(v + p), w1 = ld_stream(v + p + 1), w2 = ld_stream(v + p + 2),
-                     w3 = ld_stream(v + p + 3);
-        const double x0 = x[c0], x1 = x[c1], x2 = x[c2], x3 = x[c3];
-        s0 += w0 * x0;
-        s1 += w1 * x1;
-        s0 += w2 * x2;
-        s1 += w3 * x3;
-      }
-      for (; p < e; ++p) s0 += ld_stream(v + p) * x[ld_stream(ci + p)];
-    }
-    return s0 + s1;
-  }
   if (valid) {
     const int32_t e = __ldg(rp + r + 1);
     for (int32_t p = __ldg(rp + r) + gl; p < e; p += 4 * G) {
@@ -209,6 +215,67 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double s_red[kBS / 32][kNP];
   __shared__ double s_tot[kNP];
+  __shared__ double s_tile[kBS / 32][kTileBuf];   // per-warp product buffer of the G == 1 mapping
+  __shared__ int s_ctr;                             // tile counter of tiles_dynamic
+  double *const tbuf = s_tile[threadIdx.x >> 5];
+  // L2 policy of the attempt's vector traffic (P.vpol): 0 = default; 1 = every
+  // vector access except the stores of the next gather target (x', y') is evict-first, so the
+  // target stays L2-resident for the next phase's SpMV; 2 = 1 + those stores evict-last.
+  const int vpol = P.vpol, tdist = P.tdist, dyn = P.dyn;
+  auto lv = [vpol](const double *p) { return vpol ? __ldcs(p) : *p; };
+  auto sv = [vpol](double *p, double v) { if (vpol) __stcs(p, v); else *p = v; };
+  auto st_tgt = [vpol](double *p, double v) { if (vpol == 2) st_evict_last(p, v); else *p = v; };
+  // Hot-loop driver of the warp-tile mapping (G == 1): CTA b owns the contiguous tiles
+  // [b T, (b + 1) T) of 32 rows; its warps claim them dynamically from a shared counter, so
+  // early warps take more tiles instead of idling at the CTA barrier (the static mapping
+  // left 30% of phase B's warp samples waiting there, ncu C5).  Each tile's V contributions
+  // are summed over its lanes (butterfly) into P.tpart[tile], and the CTA sums its tiles in
+  // tile order: the result does not depend on which warp took which tile (deterministic).
+  // On return, thread 0 holds the CTA totals in tot[] and every other thread zeros.
+  auto tiles_dynamic = [&](int rows, auto &&body, auto &tot) {
+    constexpr int V = sizeof(tot) / sizeof(double);
+    const int ntiles = (rows + 31) >> 5;
+    const int nb = (int)gridDim.x, T = (ntiles + nb - 1) / nb;
+    // k-th tile of this CTA: contiguous range (tdist 0) or interleaved over the CTAs (tdist 1)
+    const int kmax = tdist ? (ntiles - (int)blockIdx.x + nb - 1) / nb : max(0, min(ntiles, ((int)blockIdx.x + 1) * T) - (int)blockIdx.x * T);
+    const int t0 = (int)blockIdx.x * T, t1 = t0 + kmax;   // this CTA's slots in P.tpart
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_ctr = 0;
+    __syncthreads();
+    for (;;) {
+      int kk = 0;
+      if (lane == 0) kk = atomicAdd(&s_ctr, 1);
+      kk = __shfl_sync(FULL, kk, 0);
+      if (kk >= kmax) break;
+      const int t = tdist ? (int)blockIdx.x + kk * nb : t0 + kk;
+      const int r = (t << 5) + lane;
+      double c[V];
+      body(r, r < rows, c);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+#pragma unroll
+        for (int off = 16; off; off >>= 1) c[k] += __shfl_xor_sync(FULL, c[k], off);
+        if (lane == 0) P.tpart[(size_t)(t0 + kk) * 2 + k] = c[k];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < V; ++k) tot[k] = 0.0;
+    if (threadIdx.x < 32) {
+      double a[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) a[k] = 0.0;
+      for (int t = t0 + lane; t < t1; t += 32)
+#pragma unroll
+        for (int k = 0; k < V; ++k) a[k] += __ldcg(P.tpart + (size_t)t * 2 + k);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+#pragma unroll
+        for (int off = 16; off; off >>= 1) a[k] += __shfl_xor_sync(FULL, a[k], off);
+        if (threadIdx.x == 0) tot[k] = a[k];
+      }
+    }
+  };
   const int n = (int)P.n, m = (int)P.m, m1 = (int)P.m1;  // < 2^31 (lp_create checks)
   const int gtid = blockIdx.x * kBS + threadIdx.x, gthreads = gridDim.x * kBS;
   const bool r2 = (P.alg == LP_R2HPDHG);
@@ -271,7 +338,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     for (int it = 0; it < row_iters; ++it) {
       const int i = it * ngrp + grp;
       const bool ok = i < m;
-      const double s = row_dot(i, ok, G, gl, P.rp, P.ci, P.kv, x);
+      const double s = row_dot(i, ok, m, G, gl, P.rp, P.ci, P.kv, x, tbuf);
       if (ok && gl == 0) {
         Kx[i] = s; Kxa[i] = s;
         const double yv = y[i];
@@ -282,7 +349,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     for (int it = 0; it < col_iters; ++it) {
       const int j = it * ngrpt + grpt;
       const bool ok = j < n;
-      const double s = row_dot(j, ok, Gt, glt, P.trp, P.tci, P.tkv, y);
+      const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, y, tbuf);
       if (ok && glt == 0) {
         KTy[j] = s; KTya[j] = s;
         const double xv = x[j];
@@ -325,37 +392,48 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     return true;
   };
 
+  TR(unsigned long long tr_a = 0, tr_aw = 0, tr_b = 0, tr_bw = 0, tr_chk = 0, tr_n = 0, tr_t0 = 0, tr_t1 = 0);
+  TR(const bool tr_on = threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1));
   while (!done) {
+    TR(if (tr_on) tr_t0 = tnow());
     // ================= phase A: [commit n-side] + primal step =================
     const double tau = eta / omega, sigma = eta * omega;
     double v3[3] = {0.0, 0.0, 0.0};
     if (pending) {
-      for (int it = 0; it < col_iters; ++it) {
-        const int j = it * ngrpt + grpt;
-        const bool ok = j < n, lead = ok && glt == 0;
+      // one column j of phase A; returns its ||dx||^2 term
+      auto colA = [&](int j, bool ok, bool lead) -> double {
         // operands of the epilogue, loaded before the dot so they are in flight with it
         double o_xp = 0.0, o_xa = 0.0, o_x = 0.0, o_kt = 0.0, o_kta = 0.0, o_cs = 0.0, o_ls = 0.0, o_us = 0.0;
         if (lead) {
-          o_xp = xp[j]; o_xa = xa[j]; o_cs = cs[j]; o_ls = P.ls[j]; o_us = P.us[j];
-          if (r2) { o_x = x[j]; o_kt = KTy[j]; o_kta = KTya[j]; }
+          o_xp = lv(xp + j); o_xa = lv(xa + j); o_cs = lv(cs + j); o_ls = lv(P.ls + j); o_us = lv(P.us + j);
+          if (r2) { o_x = lv(x + j); o_kt = lv(KTy + j); o_kta = lv(KTya + j); }
         }
-        const double s = row_dot(j, ok, Gt, glt, P.trp, P.tci, P.tkv, yp);
-        if (lead) {
-          double xn, kt;
-          if (!r2) {
-            xa[j] = o_xa + theta * (o_xp - o_xa);
-            xn = o_xp; kt = s;
-            KTyp[j] = s;           // becomes KTy after the pointer swap
-          } else {
-            xn = ha * (rf1 * o_xp - rf0 * o_x) + hb * o_xa;
-            kt = ha * (rf1 * s - rf0 * o_kt) + hb * o_kta;
-            x[j] = xn; KTy[j] = kt;
-          }
-          const double xnew = median3(o_ls, xn - tau * (o_cs - kt), o_us);
-          if (!r2) x[j] = xnew;    // x (old-x buffer) becomes x' after the swap
-          else xp[j] = xnew;
-          const double d = xnew - xn;
-          v3[0] += d * d;
+        const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, yp, tbuf);
+        if (!lead) return 0.0;
+        double xn, kt;
+        if (!r2) {
+          sv(xa + j, o_xa + theta * (o_xp - o_xa));
+          xn = o_xp; kt = s;
+          sv(KTyp + j, s);       // becomes KTy after the pointer swap
+        } else {
+          xn = ha * (rf1 * o_xp - rf0 * o_x) + hb * o_xa;
+          kt = ha * (rf1 * s - rf0 * o_kt) + hb * o_kta;
+          sv(x + j, xn); sv(KTy + j, kt);
+        }
+        const double xnew = median3(o_ls, xn - tau * (o_cs - kt), o_us);
+        st_tgt(r2 ? xp + j : x + j, xnew);   // ra: the old-x buffer becomes x' after the swap
+        const double d = xnew - xn;
+        return d * d;
+      };
+      if (Gt == 1 && (dyn & 1)) {
+        double t1[1];
+        tiles_dynamic(n, [&](int j, bool ok, double (&c)[1]) { c[0] = colA(j, ok, ok); }, t1);
+        v3[0] = t1[0];
+      } else {
+        for (int it = 0; it < col_iters; ++it) {
+          const int j = it * ngrpt + grpt;
+          const bool ok = j < n;
+          v3[0] += colA(j, ok, ok && glt == 0);
         }
       }
       if (!r2) {  // swap: x <-> x', K~'y <-> K~'y'
@@ -364,52 +442,66 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       }
     } else {
       for (int j = gtid; j < n; j += gthreads) {
-        const double xo = x[j];
-        const double xn = median3(P.ls[j], xo - tau * (cs[j] - KTy[j]), P.us[j]);
-        xp[j] = xn;
+        const double xo = lv(x + j);
+        const double xn = median3(lv(P.ls + j), xo - tau * (lv(cs + j) - lv(KTy + j)), lv(P.us + j));
+        st_tgt(xp + j, xn);
         const double d = xn - xo;
         v3[0] += d * d;
       }
     }
+    TR(if (tr_on) { tr_t1 = tnow(); tr_a += tr_t1 - tr_t0; });
     grid.sync();
+    TR(if (tr_on) { tr_t0 = tnow(); tr_aw += tr_t0 - tr_t1; });
     // ================= phase B: [commit m-side] + SpMV #1 + dual step =================
     {
-      for (int it = 0; it < row_iters; ++it) {
-        const int i = it * ngrp + grp;
-        const bool ok = i < m, lead = ok && gl == 0;
+      // one row i of phase B; returns its ||dy||^2 and <dy, K~x' - K~x> terms
+      auto rowB = [&](int i, bool ok, bool lead, double (&c)[2]) {
         double o_y = 0.0, o_kx = 0.0, o_yp = 0.0, o_ya = 0.0, o_kxp = 0.0, o_kxa = 0.0, o_qs = 0.0;
         if (lead) {
-          o_qs = qs[i];
+          o_qs = lv(qs + i);
           if (pending) {
-            o_yp = yp[i]; o_ya = ya[i]; o_kxp = Kxp[i];
-            if (r2) { o_y = y[i]; o_kx = Kx[i]; o_kxa = Kxa[i]; }
+            o_yp = lv(yp + i); o_ya = lv(ya + i); o_kxp = lv(Kxp + i);
+            if (r2) { o_y = lv(y + i); o_kx = lv(Kx + i); o_kxa = lv(Kxa + i); }
           } else {
-            o_y = y[i]; o_kx = Kx[i];
+            o_y = lv(y + i); o_kx = lv(Kx + i);
           }
         }
-        const double s = row_dot(i, ok, G, gl, P.rp, P.ci, P.kv, xp);
-        if (lead) {
-          double yv, kxv;
-          if (pending) {
-            if (!r2) {
-              yv = o_yp;
-              ya[i] = o_ya + theta * (o_yp - o_ya);
-              kxv = o_kxp;
-            } else {
-              yv = ha * (rf1 * o_yp - rf0 * o_y) + hb * o_ya;
-              kxv = ha * (rf1 * o_kxp - rf0 * o_kx) + hb * o_kxa;
-              y[i] = yv; Kx[i] = kxv;
-            }
+        const double s = row_dot(i, ok, m, G, gl, P.rp, P.ci, P.kv, xp, tbuf);
+        c[0] = 0.0; c[1] = 0.0;
+        if (!lead) return;
+        double yv, kxv;
+        if (pending) {
+          if (!r2) {
+            yv = o_yp;
+            sv(ya + i, o_ya + theta * (o_yp - o_ya));
+            kxv = o_kxp;
           } else {
-            yv = o_y; kxv = o_kx;
+            yv = ha * (rf1 * o_yp - rf0 * o_y) + hb * o_ya;
+            kxv = ha * (rf1 * o_kxp - rf0 * o_kx) + hb * o_kxa;
+            sv(y + i, yv); sv(Kx + i, kxv);
           }
-          double yn = yv + sigma * (o_qs - 2.0 * s + kxv);
-          if (i < m1) yn = fmax(yn, 0.0);
-          if (pending && !r2) { y[i] = yn; Kx[i] = s; }   // old buffers become y', K~x' after the swap
-          else { yp[i] = yn; Kxp[i] = s; }
-          const double d = yn - yv;
-          v3[1] += d * d;
-          v3[2] += d * (s - kxv);
+        } else {
+          yv = o_y; kxv = o_kx;
+        }
+        double yn = yv + sigma * (o_qs - 2.0 * s + kxv);
+        if (i < m1) yn = fmax(yn, 0.0);
+        if (pending && !r2) { st_tgt(y + i, yn); sv(Kx + i, s); }   // old buffers become y', K~x' after the swap
+        else { st_tgt(yp + i, yn); sv(Kxp + i, s); }
+        const double d = yn - yv;
+        c[0] = d * d;
+        c[1] = d * (s - kxv);
+      };
+      if (G == 1 && (dyn & 2)) {
+        double t2[2];
+        tiles_dynamic(m, [&](int i, bool ok, double (&c)[2]) { rowB(i, ok, ok, c); }, t2);
+        v3[1] = t2[0]; v3[2] = t2[1];
+      } else {
+        for (int it = 0; it < row_iters; ++it) {
+          const int i = it * ngrp + grp;
+          const bool ok = i < m;
+          double c[2];
+          rowB(i, ok, ok && gl == 0, c);
+          v3[1] += c[0]; v3[2] += c[1];
         }
       }
       if (pending && !r2) {
@@ -419,9 +511,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       pending = false;
       block_partials<3>(v3, next_part(), s_red);
     }
+    TR(if (tr_on) { tr_t1 = tnow(); tr_b += tr_t1 - tr_t0; });
     grid.sync();
     double t3[3];
     grid_totals<3>(t3, cur_part(), s_tot);
+    TR(if (tr_on) { tr_t0 = tnow(); tr_bw += tr_t0 - tr_t1; ++tr_n; });
     ++jatt;
     const double I = t3[2];
     const double M = omega * t3[0] + t3[1] / omega;
@@ -453,6 +547,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     ++k;
     ++k_in;
     if (k % P.check_freq != 0 && k != P.iter_limit) { pending = true; continue; }
+    TR(if (tr_on) tr_t1 = tnow());
 
     // ================= check: commit-only phase (both sides) =================
     // infeasibility rays (reading 35): r2HPDHG z - anchor here, raPDHG z - (pre-step point) below
@@ -464,7 +559,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       for (int it = 0; it < col_iters; ++it) {
         const int j = it * ngrpt + grpt;
         const bool ok = j < n;
-        const double s = row_dot(j, ok, Gt, glt, P.trp, P.tci, P.tkv, yp);
+        const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, yp, tbuf);
         if (ok && glt == 0) {
           KTyp[j] = s;
           if (!r2) {
@@ -514,7 +609,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       for (int it = 0; it < row_iters; ++it) {
         const int i = it * ngrp + grp;
         const bool ok = i < m;
-        const double s = row_dot(i, ok, G, gl, P.rp, P.ci, P.kv, xa);
+        const double s = row_dot(i, ok, m, G, gl, P.rp, P.ci, P.kv, xa, tbuf);
         if (ok && gl == 0) {
           Kxa[i] = s;
           const double dr = P.Dr[i], yai = ya[i], yi = y[i], kxi = Kx[i], q0 = P.q0[i], qsi = qs[i];
@@ -531,7 +626,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       for (int it = 0; it < col_iters; ++it) {
         const int j = it * ngrpt + grpt;
         const bool ok = j < n;
-        const double s = row_dot(j, ok, Gt, glt, P.trp, P.tci, P.tkv, ya);
+        const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, ya, tbuf);
         if (ok && glt == 0) {
           KTya[j] = s;
           const double dc = P.Dc[j], xaj = xa[j], xj = x[j], ktj = KTy[j];
@@ -598,7 +693,12 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       if (!r2) { W = 0.0; ref = metric; }
       grid.sync();
     }
+    TR(if (tr_on) tr_chk += tnow() - tr_t1);
   }
+  TR(if (tr_on && tr_n)
+       printf("[trace] cta %d attempts %llu  per attempt (us): A work %.1f  A barrier %.1f  B work %.1f  "
+              "B barrier+totals %.1f  | checks total %.1f us\n", blockIdx.x, tr_n, tr_a * 1e-3 / tr_n,
+              tr_aw * 1e-3 / tr_n, tr_b * 1e-3 / tr_n, tr_bw * 1e-3 / tr_n, tr_chk * 1e-3));
 
   // ================= step 6: output the candidate =================
   {
@@ -666,7 +766,9 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   // small problems do not need the whole GPU
   const int64_t work_items = (D.nnz + n + m);
   while (blocks > sms && (int64_t)blocks * kBS > 4 * work_items) blocks -= sms;
-  const size_t vec = (size_t)(8 * n + 8 * m) + 2 * (size_t)blocks * kNP;
+  const int64_t ntile = (std::max(n, m) + 31) / 32;
+  const size_t ntp = 2 * (size_t)blocks * (size_t)((ntile + blocks - 1) / blocks);  // P.tpart slots
+  const size_t vec = (size_t)(8 * n + 8 * m) + 2 * (size_t)blocks * kNP + ntp;
   const size_t need = vec * sizeof(double);
   if (*work_bytes < need) {
     if (*work) MPAX_CUDA(cudaFreeAsync(*work, s));
@@ -687,7 +789,8 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   P.qs = w; w += m;
   P.y = w; w += m; P.Kx = w; w += m; P.yp = w; w += m; P.Kxp = w; w += m; P.ya = w; w += m; P.Kxa = w; w += m;
   P.yr = w; w += m;
-  P.part = w;
+  P.part = w; w += 2 * (size_t)blocks * kNP;
+  P.tpart = w;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
   P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
   P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.rho = o.reflection;
@@ -697,11 +800,20 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   // G ~ mean row length / 4 (measured on B200 for this persistent kernel: 4 lanes per 20-entry
   // row beat 1 and 8; each group walks its rows sequentially, so shorter groups mean longer
   // dependent chains; scripts/micro/spmv_bench.cu has the standalone-SpMV comparison)
-  auto group = [](double avg) { return pow2_floor(avg / 4.0); };
-  P.gk = group(D.avg_row);
-  P.gkt = group(D.avg_col);
+  // G = 1: warp-tile CSR-stream for short rows, else G lanes per row (G ~ mean length / 4)
+  auto group = [](double avg, int mx) { return tile_mapping_ok(avg, mx) ? 1 : std::max(2, pow2_floor(avg / 4.0)); };
+  P.gk = group(D.avg_row, D.max_row);
+  P.gkt = group(D.avg_col, D.max_col);
   if (const char *e = getenv("MPAX_GRID_G")) P.gk = atoi(e);     // tuning experiments only
   if (const char *e = getenv("MPAX_GRID_GT")) P.gkt = atoi(e);
+  P.vpol = 0;
+  if (const char *e = getenv("MPAX_GRID_VPOL")) P.vpol = atoi(e);
+  P.tdist = 0;
+  if (const char *e = getenv("MPAX_GRID_TDIST")) P.tdist = atoi(e);
+  // dynamic tile driver per hot phase (bit 0: phase A, bit 1: phase B); measured on C5: phase B
+  // 1.2 -> 0.85 ms, phase A 0.66 -> 0.73 ms, so phase B only by default
+  P.dyn = 2;
+  if (const char *e = getenv("MPAX_GRID_DYN")) P.dyn = atoi(e);
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   void *args[] = {&P};
   MPAX_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(kBS), args, 0, s));

@@ -192,12 +192,24 @@ __global__ void step_table_kernel(double *tab) {
 }
 
 // Standalone SpMV with the solver's scaled matrices (lp_spmv_scaled: parity tests and the
-// bench's SpMV-pair bandwidth): G lanes per row (G ~ mean row length / 4, as the grid kernel),
-// each lane with four entries in flight (index and value streamed evict-first, then the four
+// bench's SpMV-pair bandwidth), with the grid kernel's mappings: G == 1 is the warp-tile
+// CSR-stream (common.cuh tile_row_dot) for short rows; G >= 2 lanes per row otherwise, each
+// lane with four entries in flight (index and value streamed evict-first, then the four
 // gathers), butterfly over the group.  Fixed order: deterministic.
-__global__ void spmv_kernel(int64_t rows, int G, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                            const double *__restrict__ v, const double *__restrict__ x, double *__restrict__ y) {
+__global__ void __launch_bounds__(256) spmv_kernel(int64_t rows, int G, const int32_t *__restrict__ rp,
+                                                   const int32_t *__restrict__ ci, const double *__restrict__ v,
+                                                   const double *__restrict__ x, double *__restrict__ y) {
+  __shared__ double s_tile[256 / 32][kTileBuf];
   const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (G == 1) {
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = gt - (threadIdx.x & 31); base < rows; base += nthr) {
+      const int64_t r = base + (threadIdx.x & 31);
+      const double s = tile_row_dot((int)r, r < rows, (int)rows, rp, ci, v, x, s_tile[threadIdx.x >> 5]);
+      if (r < rows) y[r] = s;
+    }
+    return;
+  }
   const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / G;
   const int gl = (int)(gt % G);
   const int64_t iters = (rows + ng - 1) / ng;
@@ -516,12 +528,13 @@ int setup_small(DevProblem &P, const int64_t *row_ptr64, const double *c, int64_
 }
 
 int spmv_scaled(const DevProblem &P, const double *v, double *Kv, const double *w, double *KTw, cudaStream_t s) {
-  auto group = [](double avg) {
-    int g = 1;
+  auto group = [](double avg, int mx) {  // as grid_solver.cu: 1 = warp-tile mapping
+    if (tile_mapping_ok(avg, mx)) return 1;
+    int g = 2;
     while (g * 2 <= avg / 4.0 && g < 32) g *= 2;
     return g;
   };
-  const int G = group(P.avg_row), GT = group(P.avg_col);
+  const int G = group(P.avg_row, P.max_row), GT = group(P.avg_col, P.max_col);
   const int blocks = 148 * 8;  // grid-stride over row groups: 8 CTAs of 256 threads per SM
   if (v && Kv && P.m > 0) MPAX_LAUNCH(spmv_kernel, blocks, 256, 0, s, P.m, G, P.rp, P.ci, P.kv, v, Kv);
   if (w && KTw) MPAX_LAUNCH(spmv_kernel, blocks, 256, 0, s, P.n, GT, P.trp, P.tci, P.tkv, w, KTw);

@@ -1,0 +1,226 @@
+// Microbenchmark (not product code): CSR SpMV mappings for the C5 shape on B200.
+//
+// A: m = 5e6 rows x n = 1e7 columns, 20 uniformly random columns per row (G-RAND's row
+// pattern), and A' (n rows, ~10 per row).  Compares the product's current
+// mapping (G lanes per row, four entries in flight per lane) with a warp-tile "CSR-stream"
+// mapping: a warp takes 32 consecutive rows, streams their contiguous nonzero range fully
+// coalesced in chunks of CH entries (all index / value loads, then all gathers, in flight),
+// parks the products in shared memory and each lane sums its own row in entry order.
+// Optionally the columns are split in two halves (two passes, gather target half the size).
+//
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o spmv2_bench spmv2_bench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <vector>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
+  printf("CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); exit(1); } } while (0)
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t mix(uint32_t v) {
+  v ^= v >> 16; v *= 0x7feb352dU; v ^= v >> 15; v *= 0x846ca68bU; v ^= v >> 16; return v;
+}
+
+// ---- current product mapping (grid_solver.cu row_dot, G >= 2) ----
+template <int G>
+__global__ void __launch_bounds__(512, 2) k_glanes(int m, const int *__restrict__ rp, const int *__restrict__ ci,
+                                                   const double *__restrict__ v, const double *x, double *y) {
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
+  const int grp = gtid / G, ngrp = gthreads / G, gl = gtid % G;
+  const int iters = (m + ngrp - 1) / ngrp;
+  for (int it = 0; it < iters; ++it) {
+    const int r = it * ngrp + grp;
+    double s0 = 0, s1 = 0;
+    if (r < m) {
+      const int e = __ldg(rp + r + 1);
+      for (int p = __ldg(rp + r) + gl; p < e; p += 4 * G) {
+        int c[4]; double w[4], xv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { const int q = p + k * G; const bool ok = q < e;
+          c[k] = ok ? __ldcs(ci + q) : 0; w[k] = ok ? __ldcs(v + q) : 0.0; }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xv[k] = (p + k * G < e) ? x[c[k]] : 0.0;
+        s0 += w[0] * xv[0]; s1 += w[1] * xv[1]; s0 += w[2] * xv[2]; s1 += w[3] * xv[3];
+      }
+    }
+    double s = s0 + s1;
+    for (int off = G >> 1; off; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+    if (r < m && gl == 0) y[r] = s;
+  }
+}
+
+// ---- warp-tile CSR-stream ----
+// smem index with one pad double per 16 (rows of ~20 entries start 20 apart: no 8-way conflicts)
+__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+
+template <int CH, bool ACC>
+__global__ void __launch_bounds__(512, 2) k_stream(int m, const int *__restrict__ rp, const int *__restrict__ ci,
+                                                   const double *__restrict__ v, const double *x, double *y,
+                                                   int col_lo, int col_hi) {
+  __shared__ double buf[16][CH + CH / 16];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int ntiles = (m + 31) >> 5;
+  double *b = buf[wl];
+  for (int tile = warp; tile < ntiles; tile += nwarps) {
+    const int r0 = tile << 5, r = r0 + lane;
+    const bool rok = r < m;
+    const int rs = rok ? __ldg(rp + r) : 0, re = rok ? __ldg(rp + r + 1) : 0;
+    const int a = __shfl_sync(FULL, rs, 0);
+    const int e = __shfl_sync(FULL, rok ? re : 0, min(31, m - 1 - r0));
+    double acc = ACC && rok ? y[r] : 0.0;
+    for (int cb = a; cb < e; cb += CH) {
+      const int ce = min(cb + CH, e);
+      int c[CH / 32]; double w[CH / 32];
+#pragma unroll
+      for (int k = 0; k < CH / 32; ++k) {
+        const int p = cb + lane + 32 * k;
+        const bool ok = p < ce;
+        c[k] = ok ? __ldcs(ci + p) : col_lo;
+        w[k] = ok ? __ldcs(v + p) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < CH / 32; ++k) {
+        // column split: entries outside [col_lo, col_hi) contribute 0 and gather nothing
+        const bool in = c[k] >= col_lo && c[k] < col_hi;
+        b[pad(lane + 32 * k)] = in ? w[k] * x[c[k]] : 0.0;
+      }
+      __syncwarp();
+      const int s = max(rs, cb) - cb, t = min(re, ce) - cb;
+      for (int q = s; q < t; ++q) acc += b[pad(q)];
+      __syncwarp();
+    }
+    if (rok) y[r] = acc;
+  }
+}
+
+// phase-A stand-in: stream `bytes` of a big buffer (evict-first) and rewrite x (n doubles)
+__global__ void __launch_bounds__(512) k_phaseA(long long nstream, const double *__restrict__ big, int n, double *x,
+                                                double *sink) {
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nt = (long long)gridDim.x * blockDim.x;
+  double acc = 0;
+  for (long long i = tid; i < nstream; i += nt) {
+    acc += __ldcs(big + i);
+    const long long j = i * n / nstream;  // x written progressively as the stream advances
+    if (i % (nstream / n > 0 ? nstream / n : 1) == 0 && j < n) x[j] = 1.0 + (j % 5) * 0.25 + acc * 0.0;
+  }
+  if (acc == 1.2345) sink[0] = acc;
+}
+struct PhaseRun { long long nstream; const double *big; int n; double *x; double *sink; int blocks; };
+static void L_phaseA(void *p) { PhaseRun &R = *(PhaseRun *)p;
+  k_phaseA<<<R.blocks, 512>>>(R.nstream, R.big, R.n, R.x, R.sink); }
+
+static float timeit(void (*launch)(void *), void *arg, int reps = 8) {
+  cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
+  float best = 1e30f;
+  for (int i = 0; i < reps; ++i) {
+    CK(cudaEventRecord(a)); launch(arg); CK(cudaEventRecord(b)); CK(cudaEventSynchronize(b));
+    CK(cudaGetLastError());
+    float ms; CK(cudaEventElapsedTime(&ms, a, b)); if (i > 0 && ms < best) best = ms;
+  }
+  return best;
+}
+
+struct Mat { int rows, cols; long long nnz; int *rp, *ci; double *v; };
+struct Run { Mat A; const double *x; double *y; int blocks; int col_lo, col_hi; };
+
+__global__ void fill_ci(long long nnz, int col_lo, int cols, uint32_t seed, int *ci, double *v) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < nnz; p += (long long)gridDim.x * blockDim.x) {
+    const uint32_t h = mix((uint32_t)p * 0x9e3779b9U + seed);
+    ci[p] = col_lo + (int)(((uint64_t)h * (uint32_t)(cols - col_lo)) >> 32);
+    v[p] = 1.0 + (double)(mix(h) & 1023) / 1024.0;
+  }
+}
+__global__ void fill_vec(int n, double *x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = 1.0 + (i % 7) * 0.125;
+}
+
+static Mat make(int rows, int cols, int mean, bool var, uint32_t seed, int col_lo = 0) {
+  Mat M; M.rows = rows; M.cols = cols;
+  std::vector<int> h(rows + 1);
+  long long s = 0;
+  for (int r = 0; r < rows; ++r) {
+    h[r] = (int)s;
+    int len = mean;
+    if (var) { uint32_t z = (uint32_t)r * 2654435761u + seed; z ^= z >> 13; z *= 0x5bd1e995u; z ^= z >> 15; len = mean / 2 + (int)(z % (uint32_t)(mean + 1)); }
+    s += len;
+  }
+  h[rows] = (int)s; M.nnz = s;
+  CK(cudaMalloc(&M.rp, (rows + 1) * sizeof(int)));
+  CK(cudaMalloc(&M.ci, s * sizeof(int)));
+  CK(cudaMalloc(&M.v, s * sizeof(double)));
+  CK(cudaMemcpy(M.rp, h.data(), (rows + 1) * sizeof(int), cudaMemcpyHostToDevice));
+  fill_ci<<<2048, 256>>>(s, col_lo, cols, seed, M.ci, M.v);
+  CK(cudaDeviceSynchronize());
+  return M;
+}
+
+template <int G> static void L_g(void *p) { Run &R = *(Run *)p;
+  k_glanes<G><<<R.blocks, 512>>>(R.A.rows, R.A.rp, R.A.ci, R.A.v, R.x, R.y); }
+template <int CH> static void L_s(void *p) { Run &R = *(Run *)p;
+  k_stream<CH, false><<<R.blocks, 512>>>(R.A.rows, R.A.rp, R.A.ci, R.A.v, R.x, R.y, 0, R.A.cols); }
+static Mat g_AL, g_AR;  // the column halves (10 per row each) of a 20-per-row matrix
+template <int CH> static void L_split(void *p) { Run &R = *(Run *)p;
+  k_stream<CH, false><<<R.blocks, 512>>>(g_AL.rows, g_AL.rp, g_AL.ci, g_AL.v, R.x, R.y, 0, g_AL.cols);
+  k_stream<CH, true><<<R.blocks, 512>>>(g_AR.rows, g_AR.rp, g_AR.ci, g_AR.v, R.x, R.y, 0, g_AR.cols); }
+
+int main() {
+  int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int m = 5000000, n = 10000000;
+  Mat A = make(m, n, 20, false, 5u);     // G-RAND rows: exactly 20 per row
+  Mat AT = make(n, m, 10, true, 7u);     // transpose-like: 5..15 per row, mean 10
+  g_AL = make(m, n / 2, 10, false, 11u);       // columns [0, n/2)
+  g_AR = make(m, n, 10, false, 13u, n / 2);    // columns [n/2, n)
+  double *x, *yv, *o1, *o2;
+  CK(cudaMalloc(&x, n * 8.0)); CK(cudaMalloc(&yv, m * 8.0));
+  CK(cudaMalloc(&o1, n * 8.0)); CK(cudaMalloc(&o2, n * 8.0));
+  fill_vec<<<1024, 256>>>(n, x); fill_vec<<<1024, 256>>>(m, yv);
+  CK(cudaDeviceSynchronize());
+  struct Case { const char *name; Mat *M; const double *src; void (*f)(void *); };
+  Case cases[] = {
+    {"A x   G=2 lanes/row", &A, x, L_g<2>}, {"A x   G=4 lanes/row", &A, x, L_g<4>}, {"A x   G=8 lanes/row", &A, x, L_g<8>},
+    {"A x   stream CH=128", &A, x, L_s<128>}, {"A x   stream CH=256", &A, x, L_s<256>},
+    {"A x   stream CH=256, 2 column halves (two CSRs)", &A, x, L_split<256>},
+    {"A x   stream CH=128, 2 column halves (two CSRs)", &A, x, L_split<128>},
+    {"A'y   G=2 lanes/row", &AT, yv, L_g<2>}, {"A'y   G=4 lanes/row", &AT, yv, L_g<4>},
+    {"A'y   stream CH=128", &AT, yv, L_s<128>}, {"A'y   stream CH=256", &AT, yv, L_s<256>},
+  };
+  for (auto &cs : cases) {
+    Run R{*cs.M, cs.src, cs.M == &A ? o1 : o2, 2 * sms, 0, cs.M->cols};
+    const float ms = timeit(cs.f, &R);
+    const double bytes = 12.0 * cs.M->nnz + 4.0 * (cs.M->rows + 1) + 8.0 * cs.M->cols + 8.0 * cs.M->rows;
+    printf("{\"case\": \"%s\", \"nnz\": %lld, \"ms\": %.4f, \"alg_GBps\": %.1f}\n", cs.name, cs.M->nnz, ms, bytes / ms / 1e6);
+    fflush(stdout);
+  }
+  // fresh-write experiment: phase-A stand-in (1.2 GB stream + rewrite of x) then A x
+  {
+    const long long nstream = 150000000;  // 1.2 GB of doubles
+    double *big; CK(cudaMalloc(&big, nstream * 8)); CK(cudaMemset(big, 0, nstream * 8));
+    PhaseRun PR{nstream, big, n, x, o2, 2 * sms};
+    const float ta = timeit(L_phaseA, &PR);
+    Run R{A, x, o1, 2 * sms, 0, n};
+    struct Both { PhaseRun *pr; Run *r; void (*f)(void *); };
+    auto both_s = [](void *p) { Both &B = *(Both *)p; L_phaseA(B.pr); B.f(B.r); };
+    for (int mode = 0; mode < 3; ++mode) {
+      Both B{&PR, &R, mode == 0 ? L_g<4> : mode == 1 ? L_s<128> : L_split<128>};
+      const float tb = timeit(both_s, &B);
+      printf("{\"case\": \"phaseA stand-in (%.3f ms) then A x %s\", \"Ax_ms\": %.4f}\n", ta,
+             mode == 0 ? "G=4" : mode == 1 ? "stream CH=128" : "stream CH=128, 2 column halves", tb - ta);
+      fflush(stdout);
+    }
+    CK(cudaFree(big));
+  }
+  // agreement of the mappings (same entry order per row for stream; G lanes reorders the sum)
+  {
+    std::vector<double> h1(m), h2(m);
+    Run R{A, x, o1, 2 * sms, 0, n};
+    L_g<4>(&R); CK(cudaMemcpy(h1.data(), o1, m * 8, cudaMemcpyDeviceToHost));
+    L_s<128>(&R); CK(cudaMemcpy(h2.data(), o1, m * 8, cudaMemcpyDeviceToHost));
+    double md = 0; for (int i = 0; i < m; ++i) { double d = fabs(h1[i] - h2[i]) / (1 + fabs(h1[i])); if (d > md) md = d; }
+    printf("{\"check\": \"G=4 vs split stream\", \"max_rel_diff\": %.3e}\n", md);
+  }
+  return 0;
+}
