@@ -30,6 +30,8 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# NCCL's version banner would land on stdout next to the one JSON line rank 0 prints
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402

@@ -90,10 +90,14 @@ __device__ __forceinline__ double rel5(const K5 &k, double nq, double nc) {
   return fmax(k.pres / (1.0 + nq), fmax(k.dres / (1.0 + nc), k.gap / (1.0 + fabs(k.pobj) + fabs(k.dobj))));
 }
 
-// row r of a CSR matrix times x with G lanes (all lanes get the sum); 4 entries in flight per lane
+// row r of a CSR matrix times x (all lanes of the row's group get the sum): G == 1 is the
+// warp-tile CSR-stream of common.cuh (every lane of the warp calls it, r = tile row + lane;
+// rows = the matrix's row count, buf = the warp's kTileBuf doubles); G >= 2 lanes per row
+// with 4 entries in flight per lane otherwise
 __device__ __forceinline__ double row_dot(int64_t r, bool valid, int G, int gl, const int32_t *__restrict__ rp,
                                           const int32_t *__restrict__ ci, const double *__restrict__ v,
-                                          const double *__restrict__ x) {
+                                          const double *__restrict__ x, int64_t rows, double *buf) {
+  if (G == 1) return tile_row_dot((int)r, valid, (int)rows, rp, ci, v, x, buf);
   double s0 = 0.0, s1 = 0.0;
   if (valid) {
     const int32_t e = __ldg(rp + r + 1);
@@ -184,12 +188,13 @@ inline int blocks_for(int64_t work) {
 __global__ void k_cols_spmv(const ShState *st, int64_t n, int G, const int32_t *trp, const int32_t *tci,
                             const double *tkv, const double *ysrc, double *out) {
   if (st->halt) return;
+  __shared__ double s_tile[kB / 32][kTileBuf];
   const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x, ng = (int64_t)gridDim.x * kB / G;
   const int gl = (int)(gt % G);
   const int64_t iters = (n + ng - 1) / ng;
   for (int64_t it = 0; it < iters; ++it) {
     const int64_t j = it * ng + gt / G;
-    const double s = row_dot(j, j < n, G, gl, trp, tci, tkv, ysrc);
+    const double s = row_dot(j, j < n, G, gl, trp, tci, tkv, ysrc, n, s_tile[threadIdx.x >> 5]);
     if (j < n && gl == 0) out[j] = s;
   }
 }
@@ -296,6 +301,7 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
   const double sigma = st->eta * st->omega, theta = st->theta, ha = st->ha, hb = st->hb;
   const double rf1 = 1.0 + st->rho, rf0 = st->rho;  // reflection (reading 38)
   double v[20] = {};
+  __shared__ double s_tile[kB / 32][kTileBuf];
   const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x;
   const bool spmv = (mode == ROWS_STEP || mode == ROWS_AVG || mode == ROWS_INIT2);
   const int g = spmv ? G : 1;
@@ -307,7 +313,7 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
     const bool ok = i < m;
     const bool lead = ok && gl == 0;
     const double *src = mode == ROWS_AVG ? V.xa : (mode == ROWS_INIT2 ? V.x : V.xp);
-    const double s = spmv ? row_dot(i, ok, g, gl, P.rp, P.ci, P.kv, src) : 0.0;
+    const double s = spmv ? row_dot(i, ok, g, gl, P.rp, P.ci, P.kv, src, m, s_tile[threadIdx.x >> 5]) : 0.0;
     if (!lead) continue;
     const double dr = P.Dr[i];
     const bool ge = i < m1;
@@ -690,6 +696,8 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
     if (f[0] == 3) return LP_ERR_DIMENSION;
     if (f[0] == 2) return LP_ERR_NAN;
     if (f[0] == 1) return LP_ERR_CROSSED_BOUNDS;
+    E.sh[g].P.max_row = f[5];   // longest row of K_g / of K_g' (setup_validate, setup_transpose)
+    E.sh[g].P.max_col = f[6];
   }
   // preconditioning with column norms reduced across shards
   std::vector<double *> rho(p), gam(p);
@@ -723,8 +731,10 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
 
 namespace {
 
-inline int group_of(double avg) {
-  int g = 1;
+// 1 = warp-tile mapping (short rows), else G lanes per row (G ~ mean length / 4)
+inline int group_of(double avg, int mx) {
+  if (tile_mapping_ok(avg, mx)) return 1;
+  int g = 2;
   while (g * 2 <= avg / 4.0 && g < 32) g *= 2;
   return g;
 }
@@ -738,7 +748,7 @@ int launch_cols(ShardedLP &E, int mode) {
 }
 int launch_rows(ShardedLP &E, int mode) {
   for (auto &S : E.sh) {
-    const int G = group_of(S.P.avg_row);
+    const int G = group_of(S.P.avg_row, S.P.max_row);
     const bool spmv = (mode == ROWS_STEP || mode == ROWS_AVG || mode == ROWS_INIT2);
     MPAX_LAUNCH(k_rows, blocks_for(S.P.m * (spmv ? G : 1)), kB, 0, E.s, S.st, mode, S.P.m, S.P.m1, G, S.P, S.V);
   }
@@ -749,7 +759,7 @@ int launch_rows(ShardedLP &E, int mode) {
 int cols_spmv(ShardedLP &E, int which /*0: yp, 1: y, 2: ya*/) {
   std::vector<double *> bufs;
   for (auto &S : E.sh) {
-    const int G = group_of(S.P.avg_col);
+    const int G = group_of(S.P.avg_col, S.P.max_col);
     const double *src = which == 0 ? S.V.yp : (which == 1 ? S.V.y : S.V.ya);
     MPAX_LAUNCH(k_cols_spmv, blocks_for(E.n * G), kB, 0, E.s, S.st, E.n, G, S.P.trp, S.P.tci, S.P.tkv, src, S.V.red);
     bufs.push_back(S.V.red);
