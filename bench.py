@@ -423,7 +423,9 @@ def spmv_pair_leg(mp, torch, dev, prob, lp, hbm, reps=20):
         torch.cuda.synchronize()
         t_pair = e0.elapsed_time(e1) / reps * 1e-3
     b_pair = 24 * lp.nnz + 4 * (lp.m + 1) + 4 * (lp.n + 1) + 8 * lp.n + 8 * lp.m
+    gf = gather_floor_us(lp.n, lp.m, lp.nnz, "ra", hbm)
     return {"us": t_pair * 1e6, "algorithmic_bytes": b_pair, "gbs": b_pair / t_pair / 1e9,
+            "gather_floor_us": gf[1] if gf else None, "frac_of_gather_floor": gf[1] / (t_pair * 1e6) if gf else None,
             "frac_of_hbm": b_pair / t_pair / 1e9 / hbm, "kernel": "spmv_kernel (standalone, x2)",
             "note": "random-column gathers move 32-byte sectors for 8 useful bytes (DESIGN.md §6)"}
 
@@ -445,6 +447,32 @@ def _traffic(key, field):
         return float(json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[key][field])
     except (OSError, KeyError, ValueError):
         return None
+
+
+def gather_floor_us(n, m, nnz, alg, hbm):
+    """Gather-bound floor of one accepted grid-path attempt: every nonzero gathers
+    one fp64 at a random column, and B200 serves random 8-byte gathers at a rate set by the
+    gathered array's size (L2-resident below ~72 MB, then DRAM sectors): the SpMV-like sweep of
+    profiles/gather_rates.json (12 B/nnz stream + gather, measured) gives each SpMV's floor by
+    linear interpolation in the target's size (y': 8m bytes for K~'y', x': 8n bytes for K~x'),
+    plus the fused vector updates at HBM peak.  Returns (floor_us, pair_floor_us) or None."""
+    try:
+        sw = json.load(open(os.path.join(ROOT, "profiles", "gather_rates.json")))["spmv_like_sweep"]
+    except (OSError, KeyError, ValueError):
+        return None
+    pts = sorted((d["array_mb"], d["ms_per_1e8"]) for d in sw)
+
+    def ms_per_1e8(mb):
+        if mb <= pts[0][0]:
+            return pts[0][1]
+        for (a, ta), (b, tb) in zip(pts, pts[1:]):
+            if mb <= b:
+                return ta + (tb - ta) * (mb - a) / (b - a)
+        (a, ta), (b, tb) = pts[-2], pts[-1]
+        return tb + (tb - ta) * (mb - b) / (b - a)
+    pair = nnz / 1e8 * (ms_per_1e8(8 * m / 1e6) + ms_per_1e8(8 * n / 1e6)) * 1e3
+    upd = (64 * n + 56 * m if alg == "ra" else 88 * n + 88 * m) / (hbm * 1e9) * 1e6
+    return pair + upd, pair
 
 
 def attempt_bytes(n, m, nnz, alg):
@@ -500,6 +528,14 @@ def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4"
                                  "traffic_source": "profiles/traffic.json (ncu --set full capture, per attempt)",
                                  "algorithmic_bytes_per_accepted_attempt": acc,
                                  "note": "working set (~70 MB) is L2-resident at C4; achieved may exceed HBM"}}
+        gf = gather_floor_us(lp.n, lp.m, lp.nnz, alg, hbm)
+        if gf is not None:
+            out[alg]["roofline"]["gather_floor"] = {
+                "us_per_attempt": gf[0], "spmv_pair_us": gf[1],
+                "frac": gf[0] / out[alg]["us_per_attempt"],
+                "source": "profiles/gather_rates.json (scripts/micro/gather_bench.cu, measured random-gather rates)",
+                "model": "per SpMV: nnz x measured time per random gather at the target's size (12 B/nnz stream "
+                         "included) + fused vector updates at HBM peak (DESIGN.md section 6)"}
     return out
 
 

@@ -97,6 +97,54 @@ __global__ void __launch_bounds__(512, 2) k_stream(int m, const int *__restrict_
   }
 }
 
+// software-pipelined variant: the next chunk's index / value loads are issued before the
+// current chunk's gathers are consumed
+template <int CH>
+__global__ void __launch_bounds__(512, 2) k_stream_pf(int m, const int *__restrict__ rp, const int *__restrict__ ci,
+                                                      const double *__restrict__ v, const double *x, double *y) {
+  __shared__ double buf[16][CH + CH / 16];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int ntiles = (m + 31) >> 5;
+  double *b = buf[wl];
+  for (int tile = warp; tile < ntiles; tile += nwarps) {
+    const int r0 = tile << 5, r = r0 + lane;
+    const bool rok = r < m;
+    const int rs = rok ? __ldg(rp + r) : 0, re = rok ? __ldg(rp + r + 1) : 0;
+    const int a = __shfl_sync(FULL, rs, 0);
+    const int e = __shfl_sync(FULL, rok ? re : 0, min(31, m - 1 - r0));
+    double acc = 0.0;
+    int c[CH / 32]; double w[CH / 32];
+#pragma unroll
+    for (int k = 0; k < CH / 32; ++k) {
+      const int p = a + lane + 32 * k; const bool ok = p < e;
+      c[k] = ok ? __ldcs(ci + p) : 0; w[k] = ok ? __ldcs(v + p) : 0.0;
+    }
+    for (int cb = a; cb < e; cb += CH) {
+      const int ce = min(cb + CH, e);
+      double g[CH / 32];
+#pragma unroll
+      for (int k = 0; k < CH / 32; ++k) g[k] = (cb + lane + 32 * k < ce) ? x[c[k]] : 0.0;
+      double prod[CH / 32];
+#pragma unroll
+      for (int k = 0; k < CH / 32; ++k) prod[k] = w[k];
+      const int nb = cb + CH;
+#pragma unroll
+      for (int k = 0; k < CH / 32; ++k) {
+        const int p = nb + lane + 32 * k; const bool ok = p < e;
+        c[k] = ok ? __ldcs(ci + p) : 0; w[k] = ok ? __ldcs(v + p) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < CH / 32; ++k) b[pad(lane + 32 * k)] = prod[k] * g[k];
+      __syncwarp();
+      const int s = max(rs, cb) - cb, t = min(re, ce) - cb;
+      for (int q = s; q < t; ++q) acc += b[pad(q)];
+      __syncwarp();
+    }
+    if (rok) y[r] = acc;
+  }
+}
+
 // phase-A stand-in: stream `bytes` of a big buffer (evict-first) and rewrite x (n doubles)
 __global__ void __launch_bounds__(512) k_phaseA(long long nstream, const double *__restrict__ big, int n, double *x,
                                                 double *sink) {
@@ -162,6 +210,8 @@ template <int G> static void L_g(void *p) { Run &R = *(Run *)p;
   k_glanes<G><<<R.blocks, 512>>>(R.A.rows, R.A.rp, R.A.ci, R.A.v, R.x, R.y); }
 template <int CH> static void L_s(void *p) { Run &R = *(Run *)p;
   k_stream<CH, false><<<R.blocks, 512>>>(R.A.rows, R.A.rp, R.A.ci, R.A.v, R.x, R.y, 0, R.A.cols); }
+template <int CH> static void L_spf(void *p) { Run &R = *(Run *)p;
+  k_stream_pf<CH><<<R.blocks, 512>>>(R.A.rows, R.A.rp, R.A.ci, R.A.v, R.x, R.y); }
 static Mat g_AL, g_AR;  // the column halves (10 per row each) of a 20-per-row matrix
 template <int CH> static void L_split(void *p) { Run &R = *(Run *)p;
   k_stream<CH, false><<<R.blocks, 512>>>(g_AL.rows, g_AL.rp, g_AL.ci, g_AL.v, R.x, R.y, 0, g_AL.cols);
@@ -185,6 +235,8 @@ int main() {
     {"A x   stream CH=128", &A, x, L_s<128>}, {"A x   stream CH=256", &A, x, L_s<256>},
     {"A x   stream CH=256, 2 column halves (two CSRs)", &A, x, L_split<256>},
     {"A x   stream CH=128, 2 column halves (two CSRs)", &A, x, L_split<128>},
+    {"A x   stream CH=128 pipelined", &A, x, L_spf<128>}, {"A x   stream CH=64 pipelined", &A, x, L_spf<64>},
+    {"A'y   stream CH=128 pipelined", &AT, yv, L_spf<128>}, {"A'y   stream CH=64 pipelined", &AT, yv, L_spf<64>},
     {"A'y   G=2 lanes/row", &AT, yv, L_g<2>}, {"A'y   G=4 lanes/row", &AT, yv, L_g<4>},
     {"A'y   stream CH=128", &AT, yv, L_s<128>}, {"A'y   stream CH=256", &AT, yv, L_s<256>},
   };
