@@ -146,7 +146,8 @@ void free_handle(lp_handle h) {
     return;
   }
   cudaStream_t s = h->stream;
-  for (void *p : {(void *)h->arena, (void *)h->X0, (void *)h->Y0, (void *)h->work, (void *)h->pol, (void *)h->spo})
+  for (void *p : {(void *)h->arena, (void *)h->X0, (void *)h->Y0, (void *)h->work, (void *)h->pol, (void *)h->spo,
+                 h->P.split_mem})
     if (p) cudaFreeAsync(p, s);
   // every D2H into the pinned buffers was followed by a stream sync, so they can be recycled now
   pin_put(h->h_res, (size_t)h->batch * sizeof(lp_result));
@@ -433,6 +434,7 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
       GridLaunch G;
       G.c0 = L.C0; G.q0 = L.Q0; G.X0 = L.X0; G.Y0 = L.Y0; G.X = L.X; G.Y = L.Y; G.L = L.L; G.res = L.res;
       G.polish_mode = L.polish_mode;
+      if (int rs = grid_split_prepare(h->P, s)) return rs;
       int rc = grid_solve(h->P, oo, G, s, &h->work, &h->work_bytes);
       if (rc == LP_ERR_UNSUPPORTED) return fail(rc, "cooperative launch unavailable");
       return rc;

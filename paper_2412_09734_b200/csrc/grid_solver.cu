@@ -30,6 +30,8 @@
 
 #include <algorithm>
 
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -50,6 +52,11 @@ struct GridParams {
   double *y, *Kx, *yp, *Kxp, *ya, *Kxa, *yr;      // m-side
   double *part;                                   // gridDim.x x kNP
   double *tpart;                                  // 2 x blocks x ceil(tiles / blocks): per-tile partials
+  // two-pass phase B over the column halves of K~ (split != 0): pass 1 parks K~_L x' in tmp
+  const int32_t *rpL, *ciL, *rpR, *ciR;
+  const double *kvL, *kvR;
+  double *tmp;
+  int32_t split;
   double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
   int32_t check_freq, alg, gk, gkt, const_step, polish_mode, verbose, display_freq, vpol, tdist, dyn;
@@ -232,7 +239,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   // are summed over its lanes (butterfly) into P.tpart[tile], and the CTA sums its tiles in
   // tile order: the result does not depend on which warp took which tile (deterministic).
   // On return, thread 0 holds the CTA totals in tot[] and every other thread zeros.
-  auto tiles_dynamic = [&](int rows, auto &&body, auto &tot) {
+  auto tiles_dynamic = [&](int rows, auto &&body, auto &tot, bool reduce) {
     constexpr int V = sizeof(tot) / sizeof(double);
     const int ntiles = (rows + 31) >> 5;
     const int nb = (int)gridDim.x, T = (ntiles + nb - 1) / nb;
@@ -251,6 +258,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       const int r = (t << 5) + lane;
       double c[V];
       body(r, r < rows, c);
+      if (!reduce) continue;
 #pragma unroll
       for (int k = 0; k < V; ++k) {
 #pragma unroll
@@ -261,7 +269,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < V; ++k) tot[k] = 0.0;
-    if (threadIdx.x < 32) {
+    if (reduce && threadIdx.x < 32) {
       double a[V];
 #pragma unroll
       for (int k = 0; k < V; ++k) a[k] = 0.0;
@@ -427,7 +435,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       };
       if (Gt == 1 && (dyn & 1)) {
         double t1[1];
-        tiles_dynamic(n, [&](int j, bool ok, double (&c)[1]) { c[0] = colA(j, ok, ok); }, t1);
+        tiles_dynamic(n, [&](int j, bool ok, double (&c)[1]) { c[0] = colA(j, ok, ok); }, t1, true);
         v3[0] = t1[0];
       } else {
         for (int it = 0; it < col_iters; ++it) {
@@ -455,10 +463,12 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     // ================= phase B: [commit m-side] + SpMV #1 + dual step =================
     {
       // one row i of phase B; returns its ||dy||^2 and <dy, K~x' - K~x> terms
-      auto rowB = [&](int i, bool ok, bool lead, double (&c)[2]) {
-        double o_y = 0.0, o_kx = 0.0, o_yp = 0.0, o_ya = 0.0, o_kxp = 0.0, o_kxa = 0.0, o_qs = 0.0;
+      auto rowB = [&](int i, bool ok, bool lead, double (&c)[2], const int32_t *rp_, const int32_t *ci_,
+                      const double *kv_, const double *addp) {
+        double o_y = 0.0, o_kx = 0.0, o_yp = 0.0, o_ya = 0.0, o_kxp = 0.0, o_kxa = 0.0, o_qs = 0.0, o_add = 0.0;
         if (lead) {
           o_qs = lv(qs + i);
+          if (addp) o_add = addp[i];   // pass 1's K~_L x' (two-pass phase B)
           if (pending) {
             o_yp = lv(yp + i); o_ya = lv(ya + i); o_kxp = lv(Kxp + i);
             if (r2) { o_y = lv(y + i); o_kx = lv(Kx + i); o_kxa = lv(Kxa + i); }
@@ -466,7 +476,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
             o_y = lv(y + i); o_kx = lv(Kx + i);
           }
         }
-        const double s = row_dot(i, ok, m, G, gl, P.rp, P.ci, P.kv, xp, tbuf);
+        const double s = o_add + row_dot(i, ok, m, G, gl, rp_, ci_, kv_, xp, tbuf);
         c[0] = 0.0; c[1] = 0.0;
         if (!lead) return;
         double yv, kxv;
@@ -493,14 +503,28 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       };
       if (G == 1 && (dyn & 2)) {
         double t2[2];
-        tiles_dynamic(m, [&](int i, bool ok, double (&c)[2]) { rowB(i, ok, ok, c); }, t2);
+        if (P.split) {
+          // pass 1: K~_L x' of the CTA's tiles into tmp (gather target: the first column half of
+          // x' only, L2-resident); pass 2: K~_R x' + tmp and the row epilogue
+          double none[1];
+          tiles_dynamic(m, [&](int i, bool ok, double (&c)[1]) {
+            const double sl = tile_row_dot(i, ok, m, P.rpL, P.ciL, P.kvL, xp, tbuf);
+            if (ok) P.tmp[i] = sl;
+            c[0] = 0.0;
+          }, none, false);
+          tiles_dynamic(m, [&](int i, bool ok, double (&c)[2]) { rowB(i, ok, ok, c, P.rpR, P.ciR, P.kvR, P.tmp); },
+                        t2, true);
+        } else {
+          tiles_dynamic(m, [&](int i, bool ok, double (&c)[2]) { rowB(i, ok, ok, c, P.rp, P.ci, P.kv, nullptr); },
+                        t2, true);
+        }
         v3[1] = t2[0]; v3[2] = t2[1];
       } else {
         for (int it = 0; it < row_iters; ++it) {
           const int i = it * ngrp + grp;
           const bool ok = i < m;
           double c[2];
-          rowB(i, ok, ok && gl == 0, c);
+          rowB(i, ok, ok && gl == 0, c, P.rp, P.ci, P.kv, nullptr);
           v3[1] += c[0]; v3[2] += c[1];
         }
       }
@@ -737,6 +761,40 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   }
 }
 
+// ---- column halves of K~ (grid_split_prepare) ----
+__global__ void split_count(int m, int h, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                            int32_t *cntL) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    int c = 0;
+    for (int p = rp[i]; p < rp[i + 1]; ++p) c += ci[p] < h;
+    cntL[i] = c;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cntL[m] = 0;
+}
+// stable partition of every row into its left (column < h) and right entries; rpL from the scan
+__global__ void split_fill(int m, int h, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                           const double *__restrict__ kv, const int32_t *__restrict__ rpL, int32_t *rpR,
+                           int32_t *ciL, double *kvL, int32_t *ciR, double *kvR) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= m; i += gridDim.x * blockDim.x) {
+    rpR[i] = rp[i] - rpL[i];
+    if (i == m) continue;
+    int pl = rpL[i], pr = rp[i] - rpL[i];
+    for (int p = rp[i]; p < rp[i + 1]; ++p) {
+      if (ci[p] < h) { ciL[pl] = ci[p]; kvL[pl++] = kv[p]; }
+      else { ciR[pr] = ci[p]; kvR[pr++] = kv[p]; }
+    }
+  }
+}
+
+// The two-pass phase B pays when x' (8n bytes) is past the L2-resident knee of random gathers
+// (~64-72 MB, profiles/gather_rates.json) and the rows use the warp-tile mapping.
+// MPAX_GRID_SPLIT=1 forces it (tests), =0 disables it.
+bool split_wanted(const DevProblem &D) {
+  const char *e = getenv("MPAX_GRID_SPLIT");
+  if (e) return atoi(e) == 1 && tile_mapping_ok(D.avg_row, D.max_row) && D.n >= 2;
+  return tile_mapping_ok(D.avg_row, D.max_row) && 8.0 * (double)D.n > 64e6;
+}
+
 inline int pow2_floor(double v) {
   int g = 1;
   while (g * 2 <= v && g < 32) g *= 2;
@@ -744,6 +802,37 @@ inline int pow2_floor(double v) {
 }
 
 }  // namespace
+
+int grid_split_prepare(DevProblem &P, cudaStream_t s) {
+  if (P.split_h > 0 || !split_wanted(P) || P.nnz <= 0) return LP_OK;
+  const int m = (int)P.m, h = (int)(P.n / 2);
+  const int64_t nnz = P.nnz;
+  // one allocation: rpL, rpR (m+1 each), ciL/ciR (nnz), kvL/kvR (nnz), scan scratch
+  size_t temp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, temp, (int32_t *)nullptr, (int32_t *)nullptr, m + 1, s);
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t o_rpL = 0, o_rpR = o_rpL + al(4 * (size_t)(m + 1)), o_ci = o_rpR + al(4 * (size_t)(m + 1)),
+               o_kv = o_ci + al(4 * (size_t)nnz), o_cnt = o_kv + al(8 * (size_t)nnz), o_tmp = o_cnt + al(4 * (size_t)(m + 1)),
+               total = o_tmp + al(temp);
+  char *base = nullptr;
+  MPAX_CUDA(cudaMallocAsync((void **)&base, total, s));
+  P.split_mem = base;
+  P.rpL = (int32_t *)(base + o_rpL); P.rpR = (int32_t *)(base + o_rpR);
+  int32_t *cnt = (int32_t *)(base + o_cnt);
+  MPAX_LAUNCH(split_count, 148 * 8, 256, 0, s, m, h, P.rp, P.ci, cnt);
+  MPAX_CUDA(cub::DeviceScan::ExclusiveSum(base + o_tmp, temp, cnt, P.rpL, m + 1, s));
+  // left entries first, right entries after them, in one ci / kv block each
+  int32_t nL = 0;
+  MPAX_CUDA(cudaMemcpyAsync(&nL, P.rpL + m, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  P.ciL = (int32_t *)(base + o_ci); P.ciR = P.ciL + nL;
+  P.kvL = (double *)(base + o_kv); P.kvR = P.kvL + nL;
+  // the right half's row pointers index from the start of ciR / kvR
+  MPAX_LAUNCH(split_fill, 148 * 8, 256, 0, s, m, h, P.rp, P.ci, P.kv, P.rpL, P.rpR, P.ciL, P.kvL, P.ciR, P.kvR);
+  MPAX_CHECK_LAUNCH();
+  P.split_h = h;
+  return LP_OK;
+}
 
 int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cudaStream_t s, double **work,
                size_t *work_bytes) {
@@ -768,7 +857,7 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   while (blocks > sms && (int64_t)blocks * kBS > 4 * work_items) blocks -= sms;
   const int64_t ntile = (std::max(n, m) + 31) / 32;
   const size_t ntp = 2 * (size_t)blocks * (size_t)((ntile + blocks - 1) / blocks);  // P.tpart slots
-  const size_t vec = (size_t)(8 * n + 8 * m) + 2 * (size_t)blocks * kNP + ntp;
+  const size_t vec = (size_t)(8 * n + 9 * m) + 2 * (size_t)blocks * kNP + ntp;   // + tmp (m)
   const size_t need = vec * sizeof(double);
   if (*work_bytes < need) {
     if (*work) MPAX_CUDA(cudaFreeAsync(*work, s));
@@ -790,7 +879,8 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   P.y = w; w += m; P.Kx = w; w += m; P.yp = w; w += m; P.Kxp = w; w += m; P.ya = w; w += m; P.Kxa = w; w += m;
   P.yr = w; w += m;
   P.part = w; w += 2 * (size_t)blocks * kNP;
-  P.tpart = w;
+  P.tpart = w; w += ntp;
+  P.tmp = w;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
   P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
   P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.rho = o.reflection;
@@ -814,6 +904,8 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   // 1.2 -> 0.85 ms, phase A 0.66 -> 0.73 ms, so phase B only by default
   P.dyn = 2;
   if (const char *e = getenv("MPAX_GRID_DYN")) P.dyn = atoi(e);
+  P.split = (D.split_h > 0 && split_wanted(D) && P.gk == 1 && (P.dyn & 2)) ? 1 : 0;
+  P.rpL = D.rpL; P.ciL = D.ciL; P.kvL = D.kvL; P.rpR = D.rpR; P.ciR = D.ciR; P.kvR = D.kvR;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   void *args[] = {&P};
   MPAX_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(kBS), args, 0, s));

@@ -123,3 +123,49 @@ def test_c5_full_size_sampled():
     assert r["status"] == mp.LP_OPTIMAL and r["rel_kkt"] <= 1e-4
     assert abs(r["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
     assert np.all(y[: lp.m1] >= 0) and np.all(x >= lp.l)
+
+
+# ---- SpMV mappings, the dynamic tile driver and the two-pass phase B ----
+# Rows of mean length <= 48 use the warp-tile CSR-stream mapping and phase B claims its tiles
+# dynamically inside each CTA; MPAX_GRID_G / MPAX_GRID_GT / MPAX_GRID_DYN select the other
+# mappings (read at every grid solve).  Every combination is deterministic and computes the same
+# iteration up to summation order.
+MAP_LP = lpgen.g_rand(20000, 40000, 20, seed=11)   # ~625 row tiles: several per CTA, fewer than warps
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_grid_dynamic_tiles_deterministic(alg):
+    a = grid_solve(MAP_LP, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=96)
+    b = grid_solve(MAP_LP, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=96)
+    for key in ("iterations", "attempts", "restarts", "primal_objective", "dual_objective"):
+        assert a[key] == b[key], key
+    assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["y"], b["y"])
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("env", [{"MPAX_GRID_DYN": "0"}, {"MPAX_GRID_DYN": "3"},
+                                 {"MPAX_GRID_G": "4", "MPAX_GRID_GT": "2"}, {"MPAX_GRID_TDIST": "1"},
+                                 {"MPAX_GRID_SPLIT": "1"}, {"MPAX_GRID_SPLIT": "1", "MPAX_GRID_TDIST": "1"}])
+def test_grid_mappings_agree(alg, env, monkeypatch):
+    ref = grid_solve(MAP_LP, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=64)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    other = grid_solve(MAP_LP, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=64)
+    for key in ("status", "iterations", "attempts", "restarts"):
+        assert other[key] == ref[key], key
+    assert rel(other["x"], ref["x"]) <= 1e-9 and rel(other["y"], ref["y"]) <= 1e-9
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("name,lp", [c for c in CASES if c[0] in ("C1", "ragged", "mid", "wide")])
+def test_grid_split_vs_oracle(alg, name, lp, monkeypatch):
+    """The two-pass phase B (column halves of K~, forced on at any size) against the oracle."""
+    monkeypatch.setenv("MPAX_GRID_SPLIT", "1")
+    ro, stable, drift = oracle_stability(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=64)
+    rg = grid_solve(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=64)
+    if not stable:
+        pytest.skip("ill-conditioned at this K")
+    tol = max(1e-9, 100 * drift)
+    for key in ("status", "iterations", "attempts", "restarts"):
+        assert rg[key] == ro[key], (key, rg[key], ro[key])
+    assert rel(rg["x"], ro["x"]) <= tol and rel(rg["y"], ro["y"]) <= tol
