@@ -454,8 +454,9 @@ def gather_floor_us(n, m, nnz, alg, hbm):
     one fp64 at a random column, and B200 serves random 8-byte gathers at a rate set by the
     gathered array's size (L2-resident below ~72 MB, then DRAM sectors): the SpMV-like sweep of
     profiles/gather_rates.json (12 B/nnz stream + gather, measured) gives each SpMV's floor by
-    linear interpolation in the target's size (y': 8m bytes for K~'y', x': 8n bytes for K~x'),
-    plus the fused vector updates at HBM peak.  Returns (floor_us, pair_floor_us) or None."""
+    linear interpolation in the target's size (y': 8m bytes for K~'y', x': 8n bytes for K~x',
+    each optionally split into column parts), plus the fused vector updates at HBM peak.
+    Returns (floor_us, pair_floor_us) or None."""
     try:
         sw = json.load(open(os.path.join(ROOT, "profiles", "gather_rates.json")))["spmv_like_sweep"]
     except (OSError, KeyError, ValueError):
@@ -470,7 +471,16 @@ def gather_floor_us(n, m, nnz, alg, hbm):
                 return ta + (tb - ta) * (mb - a) / (b - a)
         (a, ta), (b, tb) = pts[-2], pts[-1]
         return tb + (tb - ta) * (mb - b) / (b - a)
-    pair = nnz / 1e8 * (ms_per_1e8(8 * m / 1e6) + ms_per_1e8(8 * n / 1e6)) * 1e3
+    def spmv_us(rows, target_elems):
+        # a target past the L2 knee may be split into k column parts (k passes, each gathering
+        # from 1/k of the vector; the row partials cost 16 B per row per extra pass at HBM peak):
+        # the floor takes the best k, as the grid kernel's two-pass phase B does with k = 2
+        best = None
+        for k in (1, 2, 3, 4):
+            t = nnz / 1e8 * ms_per_1e8(8 * target_elems / k / 1e6) * 1e3 + (k - 1) * 16 * rows / (hbm * 1e9) * 1e6
+            best = t if best is None else min(best, t)
+        return best
+    pair = spmv_us(m, n) + spmv_us(n, m)
     upd = (64 * n + 56 * m if alg == "ra" else 88 * n + 88 * m) / (hbm * 1e9) * 1e6
     return pair + upd, pair
 
@@ -535,7 +545,8 @@ def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4"
                 "frac": gf[0] / out[alg]["us_per_attempt"],
                 "source": "profiles/gather_rates.json (scripts/micro/gather_bench.cu, measured random-gather rates)",
                 "model": "per SpMV: nnz x measured time per random gather at the target's size (12 B/nnz stream "
-                         "included) + fused vector updates at HBM peak (DESIGN.md section 6)"}
+                         "included; a target past the L2 knee may be split into column parts, best of 1-4) + "
+                         "fused vector updates at HBM peak (DESIGN.md section 6)"}
     return out
 
 

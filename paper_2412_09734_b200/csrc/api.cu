@@ -674,6 +674,7 @@ int lp_spmv_scaled(lp_handle h, const double *v, double *Kv, const double *w, do
     TRY(dalloc(&dw, m, s)); TRY(dalloc(&dKTw, n, s));
     if (m) MPAX_CUDA(cudaMemcpyAsync(dw, w, (size_t)m * sizeof(double), cudaMemcpyDefault, s));
   }
+  if (!h->is_batch) TRY(grid_split_prepare(h->P, s));   // the layout the grid kernel's K~x' uses
   TRY(spmv_scaled(h->P, dv, dKv, dw, dKTw, s));
   if (dKv && m) MPAX_CUDA(cudaMemcpyAsync(Kv, dKv, (size_t)m * sizeof(double), cudaMemcpyDefault, s));
   if (dKTw) MPAX_CUDA(cudaMemcpyAsync(KTw, dKTw, (size_t)n * sizeof(double), cudaMemcpyDefault, s));

@@ -196,16 +196,20 @@ __global__ void step_table_kernel(double *tab) {
 // CSR-stream (common.cuh tile_row_dot) for short rows; G >= 2 lanes per row otherwise, each
 // lane with four entries in flight (index and value streamed evict-first, then the four
 // gathers), butterfly over the group.  Fixed order: deterministic.
+// accumulate (G == 1 only): y = y + K x, the second pass over the right column half of K~ as
+// in the grid kernel's two-pass phase B (same summation order: left half, then right).
 __global__ void __launch_bounds__(256) spmv_kernel(int64_t rows, int G, const int32_t *__restrict__ rp,
                                                    const int32_t *__restrict__ ci, const double *__restrict__ v,
-                                                   const double *__restrict__ x, double *__restrict__ y) {
+                                                   const double *__restrict__ x, double *__restrict__ y,
+                                                   int accumulate) {
   __shared__ double s_tile[256 / 32][kTileBuf];
   const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (G == 1) {
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = gt - (threadIdx.x & 31); base < rows; base += nthr) {
       const int64_t r = base + (threadIdx.x & 31);
-      const double s = tile_row_dot((int)r, r < rows, (int)rows, rp, ci, v, x, s_tile[threadIdx.x >> 5]);
+      const double a = (accumulate && r < rows) ? y[r] : 0.0;
+      const double s = a + tile_row_dot((int)r, r < rows, (int)rows, rp, ci, v, x, s_tile[threadIdx.x >> 5]);
       if (r < rows) y[r] = s;
     }
     return;
@@ -536,8 +540,15 @@ int spmv_scaled(const DevProblem &P, const double *v, double *Kv, const double *
   };
   const int G = group(P.avg_row, P.max_row), GT = group(P.avg_col, P.max_col);
   const int blocks = 148 * 8;  // grid-stride over row groups: 8 CTAs of 256 threads per SM
-  if (v && Kv && P.m > 0) MPAX_LAUNCH(spmv_kernel, blocks, 256, 0, s, P.m, G, P.rp, P.ci, P.kv, v, Kv);
-  if (w && KTw) MPAX_LAUNCH(spmv_kernel, blocks, 256, 0, s, P.n, GT, P.trp, P.tci, P.tkv, w, KTw);
+  if (v && Kv && P.m > 0) {
+    if (G == 1 && P.split_h > 0) {  // the column halves built for the grid kernel (grid_split_prepare)
+      MPAX_LAUNCH(spmv_kernel, blocks, 256, 0, s, P.m, 1, P.rpL, P.ciL, P.kvL, v, Kv, 0);
+      MPAX_LAUNCH(spmv_kernel, blocks, 256, 0, s, P.m, 1, P.rpR, P.ciR, P.kvR, v, Kv, 1);
+    } else {
+      MPAX_LAUNCH(spmv_kernel, blocks, 256, 0, s, P.m, G, P.rp, P.ci, P.kv, v, Kv, 0);
+    }
+  }
+  if (w && KTw) MPAX_LAUNCH(spmv_kernel, blocks, 256, 0, s, P.n, GT, P.trp, P.tci, P.tkv, w, KTw, 0);
   MPAX_CHECK_LAUNCH();
   return LP_OK;
 }
