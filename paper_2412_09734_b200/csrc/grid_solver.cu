@@ -894,6 +894,10 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   auto group = [](double avg, int mx) { return tile_mapping_ok(avg, mx) ? 1 : std::max(2, pow2_floor(avg / 4.0)); };
   P.gk = group(D.avg_row, D.max_row);
   P.gkt = group(D.avg_col, D.max_col);
+  // phase A keeps the static mapping: with fewer than ~4 column tiles per warp (C4: 1.3) the
+  // tile chunks are a serial latency chain and G lanes per column are faster (C4 phase A
+  // 21 -> 17 us per attempt, trace build); phase B's dynamic tile driver wins at any size
+  if (P.gkt == 1 && (n + 31) / 32 < 4 * (int64_t)blocks * (kBS / 32)) P.gkt = std::max(2, pow2_floor(D.avg_col / 4.0));
   if (const char *e = getenv("MPAX_GRID_G")) P.gk = atoi(e);     // tuning experiments only
   if (const char *e = getenv("MPAX_GRID_GT")) P.gkt = atoi(e);
   P.vpol = 0;
