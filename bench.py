@@ -426,7 +426,7 @@ def spmv_pair_leg(mp, torch, dev, prob, lp, hbm, reps=20):
     gf = gather_floor_us(lp.n, lp.m, lp.nnz, "ra", hbm)
     return {"us": t_pair * 1e6, "algorithmic_bytes": b_pair, "gbs": b_pair / t_pair / 1e9,
             "gather_floor_us": gf[1] if gf else None, "frac_of_gather_floor": gf[1] / (t_pair * 1e6) if gf else None,
-            "frac_of_hbm": b_pair / t_pair / 1e9 / hbm, "kernel": "spmv_kernel (standalone, x2)",
+            "frac_of_hbm": b_pair / t_pair / 1e9 / hbm, "kernel": "spmv_kernel (standalone; K~x over the two column halves when split, K~'w)",
             "note": "random-column gathers move 32-byte sectors for 8 useful bytes (DESIGN.md §6)"}
 
 

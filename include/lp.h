@@ -243,7 +243,10 @@ int lp_get_shape(lp_handle h, int64_t *n, int64_t *m1, int64_t *m2, int64_t *bat
 
 /* Diagnostics used by the parity tests: the diagonal scalings Dr (m), Dc (n)
  * of step 1, and the scaled products K~ v (m) and K~' w (n) computed by the
- * solver's own SpMV kernels.  Any pointer may be NULL. */
+ * solver's own SpMV kernels (bench.py's SpMV-pair leg).  Any pointer may be
+ * NULL.  memory = LP_DEVICE: the buffers are device memory and are read /
+ * written in place; LP_HOST: staged through device copies.  Blocks until the
+ * products are written. */
 int lp_get_scaling(lp_handle h, double *Dr, double *Dc, int32_t memory);
 int lp_spmv_scaled(lp_handle h, const double *v, double *Kv, const double *w, double *KTw,
                    int32_t memory);

@@ -666,6 +666,13 @@ int lp_spmv_scaled(lp_handle h, const double *v, double *Kv, const double *w, do
   cudaStream_t s = h->stream;
   const int64_t n = h->P.n, m = h->P.m;
   double *dv = nullptr, *dKv = nullptr, *dw = nullptr, *dKTw = nullptr;
+  if (memory == LP_DEVICE) {  // device buffers are used in place: no staging copies
+    if (!h->is_batch) TRY(grid_split_prepare(h->P, s));
+    TRY(spmv_scaled(h->P, v && Kv ? v : nullptr, v && Kv ? Kv : nullptr, w && KTw ? w : nullptr,
+                    w && KTw ? KTw : nullptr, s));
+    MPAX_CUDA(cudaStreamSynchronize(s));
+    return LP_OK;
+  }
   if (v && Kv) {
     TRY(dalloc(&dv, n, s)); TRY(dalloc(&dKv, m, s));
     MPAX_CUDA(cudaMemcpyAsync(dv, v, (size_t)n * sizeof(double), cudaMemcpyDefault, s));
