@@ -57,6 +57,8 @@ struct GridParams {
   const double *kvL, *kvR;
   double *tmp;
   int32_t split;
+  double *tpartA;                                 // ceil(n / 32): phase A's per-tile ||dx||^2 (global claims)
+  unsigned long long *gctr;                       // global tile counter of phase A (monotonic)
   double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
   int32_t check_freq, alg, gk, gkt, const_step, polish_mode, verbose, display_freq, vpol, tdist, dyn;
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       y[i] = yv;
     }
     block_partials<4>(v, next_part(), s_red);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.gctr = 0ull;   // before the first grid barrier
   }
   grid.sync();
   double tot4[4];
@@ -400,6 +403,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     return true;
   };
 
+  unsigned long long gbase = 0;   // phase A's global tile counter value at this phase's start
+  bool sliceA = false;            // phase A used global claims: reduce this CTA's slice in phase B
   TR(unsigned long long tr_a = 0, tr_aw = 0, tr_b = 0, tr_bw = 0, tr_chk = 0, tr_n = 0, tr_t0 = 0, tr_t1 = 0);
   TR(const bool tr_on = threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1));
   while (!done) {
@@ -433,7 +438,29 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         const double d = xnew - xn;
         return d * d;
       };
-      if (Gt == 1 && (dyn & 1)) {
+      if (Gt == 1 && (dyn & 4)) {
+        // global dynamic claims: warps of every CTA take column tiles from one monotonic counter,
+        // so CTAs that run ahead take more tiles (no inter-CTA tail at the barrier).  Every warp
+        // makes exactly one failing claim per phase, so each phase consumes ntiles + all warps
+        // counter values and every CTA advances gbase identically.  Tile partials go to
+        // P.tpartA[tile]; CTA b sums its fixed slice in tile order after the barrier (phase B):
+        // deterministic whichever warp took which tile.
+        const int ntA = (n + 31) >> 5, lane = threadIdx.x & 31;
+        for (;;) {
+          unsigned long long c = 0;
+          if (lane == 0) c = atomicAdd(P.gctr, 1ull);
+          c = __shfl_sync(FULL, c, 0);
+          const long long t = (long long)(c - gbase);
+          if (t >= ntA) break;
+          const int j = ((int)t << 5) + lane;
+          double d = colA(j, j < n, j < n);
+#pragma unroll
+          for (int off = 16; off; off >>= 1) d += __shfl_xor_sync(FULL, d, off);
+          if (lane == 0) P.tpartA[t] = d;
+        }
+        gbase += (unsigned long long)ntA + (unsigned long long)gridDim.x * (kBS / 32);
+        sliceA = true;
+      } else if (Gt == 1 && (dyn & 1)) {
         double t1[1];
         tiles_dynamic(n, [&](int j, bool ok, double (&c)[1]) { c[0] = colA(j, ok, ok); }, t1, true);
         v3[0] = t1[0];
@@ -533,6 +560,20 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         t = Kx; Kx = Kxp; Kxp = t;
       }
       pending = false;
+      if (sliceA) {  // phase A's tile partials of this CTA's fixed slice, in tile order
+        sliceA = false;
+        const int ntA = (n + 31) >> 5, nb = (int)gridDim.x, TA = (ntA + nb - 1) / nb;
+        const int a0 = (int)blockIdx.x * TA, a1 = min(ntA, a0 + TA);
+        if (threadIdx.x < 32) {
+          double a = 0.0;
+          for (int t = a0 + (int)threadIdx.x; t < a1; t += 32) a += __ldcg(P.tpartA + t);
+#pragma unroll
+          for (int off = 16; off; off >>= 1) a += __shfl_xor_sync(FULL, a, off);
+          v3[0] = threadIdx.x == 0 ? a : 0.0;
+        } else {
+          v3[0] = 0.0;
+        }
+      }
       block_partials<3>(v3, next_part(), s_red);
     }
     TR(if (tr_on) { tr_t1 = tnow(); tr_b += tr_t1 - tr_t0; });
@@ -857,7 +898,8 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   while (blocks > sms && (int64_t)blocks * kBS > 4 * work_items) blocks -= sms;
   const int64_t ntile = (std::max(n, m) + 31) / 32;
   const size_t ntp = 2 * (size_t)blocks * (size_t)((ntile + blocks - 1) / blocks);  // P.tpart slots
-  const size_t vec = (size_t)(8 * n + 9 * m) + 2 * (size_t)blocks * kNP + ntp;   // + tmp (m)
+  const size_t ntpA = (size_t)((n + 31) / 32) + 1;   // + the counter
+  const size_t vec = (size_t)(8 * n + 9 * m) + 2 * (size_t)blocks * kNP + ntp + ntpA;   // + tmp (m)
   const size_t need = vec * sizeof(double);
   if (*work_bytes < need) {
     if (*work) MPAX_CUDA(cudaFreeAsync(*work, s));
@@ -880,7 +922,9 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   P.yr = w; w += m;
   P.part = w; w += 2 * (size_t)blocks * kNP;
   P.tpart = w; w += ntp;
-  P.tmp = w;
+  P.tmp = w; w += m;
+  P.gctr = (unsigned long long *)w; w += 1;
+  P.tpartA = w;
   P.eps_abs = o.eps_abs; P.eps_rel = o.eps_rel; P.iter_limit = o.iteration_limit;
   P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
   P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.rho = o.reflection;
@@ -904,8 +948,10 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   if (const char *e = getenv("MPAX_GRID_VPOL")) P.vpol = atoi(e);
   P.tdist = 0;
   if (const char *e = getenv("MPAX_GRID_TDIST")) P.tdist = atoi(e);
-  // dynamic tile driver per hot phase (bit 0: phase A, bit 1: phase B); measured on C5: phase B
-  // 1.2 -> 0.85 ms, phase A 0.66 -> 0.73 ms, so phase B only by default
+  // dynamic tile driver per hot phase (bit 0: phase A inside each CTA, bit 1: phase B inside
+  // each CTA, bit 2: phase A from one global counter); measured on C5: phase B 1.2 -> 0.85 ms;
+  // phase A 0.66 -> 0.73 ms (bit 0), barrier wait 60-75 -> 7 us but work +50-75 us (bit 2):
+  // phase B only by default
   P.dyn = 2;
   if (const char *e = getenv("MPAX_GRID_DYN")) P.dyn = atoi(e);
   P.split = (D.split_h > 0 && split_wanted(D) && P.gk == 1 && (P.dyn & 2)) ? 1 : 0;

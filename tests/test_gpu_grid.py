@@ -143,7 +143,8 @@ def test_grid_dynamic_tiles_deterministic(alg):
 
 
 @pytest.mark.parametrize("alg", ALGS)
-@pytest.mark.parametrize("env", [{"MPAX_GRID_DYN": "0"}, {"MPAX_GRID_DYN": "3"},
+@pytest.mark.parametrize("env", [{"MPAX_GRID_DYN": "0"}, {"MPAX_GRID_DYN": "3"}, {"MPAX_GRID_DYN": "6"},
+                                 {"MPAX_GRID_DYN": "6", "MPAX_GRID_GT": "1"},
                                  {"MPAX_GRID_G": "4", "MPAX_GRID_GT": "2"}, {"MPAX_GRID_TDIST": "1"},
                                  {"MPAX_GRID_SPLIT": "1"}, {"MPAX_GRID_SPLIT": "1", "MPAX_GRID_TDIST": "1"}])
 def test_grid_mappings_agree(alg, env, monkeypatch):
