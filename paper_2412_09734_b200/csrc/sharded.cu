@@ -50,6 +50,7 @@ struct Vecs {
   double *x, *KTy, *xp, *KTyp, *xa, *KTya, *xr, *cs, *red;  // n
   double *y, *Kx, *yp, *Kxp, *ya, *Kxa, *yr, *qs;           // m_local
   double *part;                                             // blocks x kV
+  double *tmp;                                              // m_local: K~_L x' (two-pass rows step)
   const double *c0, *q0, *X0, *Y0;
 };
 
@@ -295,6 +296,18 @@ __global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, con
   last_block_sum<20>(v, V.part, &st->cnt_cols, st->colsum);
 }
 
+// pass 1 of the two-pass rows step: V.tmp = K~_L x' (warp-tile mapping, same order as the grid kernel)
+__global__ void k_rows_left(const ShState *st, int64_t m, const DevProblem P, const double *x, double *tmp) {
+  if (st->halt) return;
+  __shared__ double s_tile[kB / 32][kTileBuf];
+  const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x, nthr = (int64_t)gridDim.x * kB;
+  for (int64_t base = gt - (threadIdx.x & 31); base < m; base += nthr) {
+    const int64_t r = base + (threadIdx.x & 31);
+    const double v = tile_row_dot((int)r, r < m, (int)m, P.rpL, P.ciL, P.kvL, x, s_tile[threadIdx.x >> 5]);
+    if (r < m) tmp[r] = v;
+  }
+}
+
 __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, const DevProblem P, const Vecs V) {
   if (st->halt && mode != ROWS_OUT) return;
   const bool r2 = st->r2, pend = st->pending;
@@ -313,7 +326,11 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
     const bool ok = i < m;
     const bool lead = ok && gl == 0;
     const double *src = mode == ROWS_AVG ? V.xa : (mode == ROWS_INIT2 ? V.x : V.xp);
-    const double s = spmv ? row_dot(i, ok, g, gl, P.rp, P.ci, P.kv, src, m, s_tile[threadIdx.x >> 5]) : 0.0;
+    // ROWS_STEP over split K~_g: pass 1 (k_rows_left) parked K~_L x' in V.tmp; add K~_R x'
+    const bool two = mode == ROWS_STEP && P.split_h > 0 && g == 1;
+    const double s = !spmv ? 0.0
+                     : two ? (ok ? V.tmp[i] : 0.0) + row_dot(i, ok, 1, 0, P.rpR, P.ciR, P.kvR, src, m, s_tile[threadIdx.x >> 5])
+                           : row_dot(i, ok, g, gl, P.rp, P.ci, P.kv, src, m, s_tile[threadIdx.x >> 5]);
     if (!lead) continue;
     const double dr = P.Dr[i];
     const bool ge = i < m1;
@@ -676,7 +693,7 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
     double *vec = nullptr;
     S.nb = 148 * 8;
     const size_t nv = 9 * (size_t)n + 8 * (size_t)(m > 0 ? m : 1) + (size_t)S.nb * kV + 3 * (size_t)n +
-                      (size_t)(m > 0 ? m : 1);
+                      2 * (size_t)(m > 0 ? m : 1);
     MPAX_CUDA(cudaMallocAsync((void **)&vec, nv * sizeof(double), s));
     S.vecs = vec;
     Vecs &V = S.V;
@@ -688,6 +705,7 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
     V.Kxa = w; w += mm; V.yr = w; w += mm; V.qs = w; w += mm;
     V.part = w; w += (size_t)S.nb * kV;
     S.X = w; w += n; S.L = w; w += n; w += n; S.Y = w; w += mm;
+    V.tmp = w; w += mm;
     V.c0 = c0; V.q0 = q0;
   }
   MPAX_CUDA(cudaStreamSynchronize(s));
@@ -725,6 +743,9 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
     MPAX_CUDA(cudaFreeAsync(gam[g], s));
   }
   MPAX_CUDA(cudaFreeAsync(noflag, s));
+  // column halves of each K~_g for the two-pass rows step (grid_solver.cu grid_split_prepare:
+  // x' is replicated, so its 8n bytes are the gather target at every p)
+  for (int g = 0; g < p; ++g) STRY(grid_split_prepare(E.sh[g].P, s));
   MPAX_CUDA(cudaStreamSynchronize(s));
   return LP_OK;
 }
@@ -750,6 +771,8 @@ int launch_rows(ShardedLP &E, int mode) {
   for (auto &S : E.sh) {
     const int G = group_of(S.P.avg_row, S.P.max_row);
     const bool spmv = (mode == ROWS_STEP || mode == ROWS_AVG || mode == ROWS_INIT2);
+    if (mode == ROWS_STEP && S.P.split_h > 0 && G == 1 && S.P.m > 0)
+      MPAX_LAUNCH(k_rows_left, blocks_for(S.P.m), kB, 0, E.s, S.st, S.P.m, S.P, S.V.xp, S.V.tmp);
     MPAX_LAUNCH(k_rows, blocks_for(S.P.m * (spmv ? G : 1)), kB, 0, E.s, S.st, mode, S.P.m, S.P.m1, G, S.P, S.V);
   }
   MPAX_CHECK_LAUNCH();
@@ -904,6 +927,7 @@ void sharded_free(ShardedLP *E) {
   for (auto &S : E->sh) {
     if (S.arena) cudaFreeAsync(S.arena, E->s);
     if (S.vecs) cudaFreeAsync(S.vecs, E->s);
+    if (S.P.split_mem) cudaFreeAsync(S.P.split_mem, E->s);
   }
   if (E->d_ptrs) cudaFreeAsync(E->d_ptrs, E->s);
   if (E->d_res) cudaFreeAsync(E->d_res, E->s);

@@ -92,3 +92,20 @@ def test_sharded_local_rows_api_matches_virtual():
     Kl = lpgen.LP(loc.n, loc.m1, loc.m2, np.asarray(loc.row_ptr), np.asarray(loc.col_idx),
                   np.asarray(loc.values), lp.c, np.asarray(loc.q), lp.l, lp.u).dense_K()
     assert np.array_equal(Kl, K[cuts[1]:cuts[2]])
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("shards", [1, 3])
+@pytest.mark.parametrize("name,lp", CASES[:2])
+def test_sharded_two_pass_rows(alg, shards, name, lp, monkeypatch):
+    """The rows step over the column halves of each K~_g (forced on; by default only past the
+    L2 gather knee) against the oracle at fixed K."""
+    monkeypatch.setenv("MPAX_GRID_SPLIT", "1")
+    ro, stable, drift = oracle_stability(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=64)
+    rg = sharded(lp, alg, shards, eps_abs=0.0, eps_rel=0.0, iteration_limit=64)
+    if not stable:
+        pytest.skip("ill-conditioned at this K")
+    tol = max(1e-9, 100 * drift)
+    for key in ("status", "iterations", "attempts", "restarts"):
+        assert rg[key] == ro[key], (key, rg[key], ro[key])
+    assert rel(rg["x"], ro["x"]) <= tol and rel(rg["y"], ro["y"]) <= tol
