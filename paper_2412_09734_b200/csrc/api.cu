@@ -170,6 +170,40 @@ struct Arena {
   }
 };
 
+// Device-to-device uploads of one create in one launch: entry e copies bytes[e] (a multiple of
+// 4) from src[e] to dst[e]; block 0 also writes the validation flags' initial values.
+struct UploadList {
+  static constexpr int kMax = 8;
+  void *dst[kMax];
+  const void *src[kMax];
+  size_t bytes[kMax];
+  int count = 0;
+  int flag_init[8];
+  int *flag = nullptr;
+  void add(void *d, const void *s_, size_t b) {
+    if (b == 0) return;
+    dst[count] = d; src[count] = s_; bytes[count] = b; ++count;
+  }
+};
+__global__ void upload_gather_kernel(const UploadList U) {
+  if (blockIdx.x == 0 && threadIdx.x < 8 && U.flag) U.flag[threadIdx.x] = U.flag_init[threadIdx.x];
+  for (int e = 0; e < U.count; ++e) {
+    const size_t words = U.bytes[e] / 4;
+    const uint32_t *src = (const uint32_t *)U.src[e];
+    uint32_t *dst = (uint32_t *)U.dst[e];
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words; i += (size_t)gridDim.x * blockDim.x)
+      dst[i] = src[i];
+  }
+}
+int upload_gather(const UploadList &U, cudaStream_t s) {
+  size_t words = 0;
+  for (int e = 0; e < U.count; ++e) words = std::max(words, U.bytes[e] / 4);
+  const int blocks = (int)std::min<size_t>(148 * 4, std::max<size_t>(1, (words + 255) / 256));
+  MPAX_LAUNCH(upload_gather_kernel, blocks, 256, 0, s, U);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
 int check_desc(const lp_problem_desc *p) {
   if (!p) return fail(LP_ERR_INVALID_ARGUMENT, "problem descriptor is NULL");
   if (p->memory != LP_HOST && p->memory != LP_DEVICE) return fail(LP_ERR_INVALID_ARGUMENT, "bad memory kind");
@@ -239,17 +273,27 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
     MPAX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
     return LP_OK;
   };
-  CK(cp(h->rp64, p->row_ptr, (size_t)(m + 1) * sizeof(int64_t)));
-  CK(cp(P.ci, p->col_idx, (size_t)nnz * sizeof(int32_t)));
-  CK(cp(P.kv0, p->values, (size_t)nnz * sizeof(double)));
-  CK(cp(P.l0, p->l, (size_t)n * sizeof(double)));
-  CK(cp(P.u0, p->u, (size_t)n * sizeof(double)));
-  CK(cp(h->C0, perC ? (const void *)C : (const void *)p->c, (size_t)(perC ? batch * n : n) * sizeof(double)));
-  if (m > 0) CK(cp(h->Q0, perQ ? (const void *)Q : (const void *)p->q, (size_t)(perQ ? batch * m : m) * sizeof(double)));
   {
     const int init[8] = {0, INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX, 0, 0, 0};
     memcpy(h->h_flag, init, sizeof(init));
-    CK(cp(h->d_flag, h->h_flag, sizeof(init)));
+    UploadList U;
+    U.add(h->rp64, p->row_ptr, (size_t)(m + 1) * sizeof(int64_t));
+    U.add(P.ci, p->col_idx, (size_t)nnz * sizeof(int32_t));
+    U.add(P.kv0, p->values, (size_t)nnz * sizeof(double));
+    U.add(P.l0, p->l, (size_t)n * sizeof(double));
+    U.add(P.u0, p->u, (size_t)n * sizeof(double));
+    U.add(h->C0, perC ? (const void *)C : (const void *)p->c, (size_t)(perC ? batch * n : n) * sizeof(double));
+    if (m > 0) U.add(h->Q0, perQ ? (const void *)Q : (const void *)p->q, (size_t)(perQ ? batch * m : m) * sizeof(double));
+    if (p->memory == LP_DEVICE && memory == LP_DEVICE) {
+      // device inputs: every copy and the flags' initial values in ONE gather kernel (a small
+      // LP's create is bound by per-call overhead, not bytes: C2 8 copy calls -> 1 launch)
+      for (int k = 0; k < 8; ++k) U.flag_init[k] = init[k];
+      U.flag = h->d_flag;
+      CK(upload_gather(U, s));
+    } else {
+      for (int k = 0; k < U.count; ++k) CK(cp(U.dst[k], U.src[k], U.bytes[k]));
+      CK(cp(h->d_flag, h->h_flag, sizeof(init)));
+    }
   }
   if (setup_small_ok(P)) {
     CK(setup_small(P, h->rp64, h->C0, perC ? batch * n : n, h->Q0, perQ ? batch * m : m, s, h->d_flag));
