@@ -367,7 +367,13 @@ def run_ours(args):
                      "kernel": "tiny_kernel<0,1,2,4,4> (raPDHG, register-resident warp per LP)", "kernel_ms": kern_ms,
                      "flops_per_launch": flops,
                      "peak_source": peak_src,
-                     "note": "per-instance solves are latency-bound, see DESIGN.md §6"},
+                     "note": "per-instance solves are latency-bound, see DESIGN.md §6",
+                     # the batch time is the slowest instance's attempts x one warp's attempt latency
+                     "critical_path": {"attempts_slowest": int(atts.max()),
+                                       "us_per_attempt": kern_ms * 1e3 / max(1, int(atts.max())),
+                                       "cycles_per_attempt": kern_ms * 1e-3 / max(1, int(atts.max())) * sm_max * 1e6,
+                                       "attempts_mean": float(atts.mean()),
+                                       "note": "one warp per LP; fp64 ALU issue would allow ~50x more"}},
         "iterations": {"p50": float(np.median(iters)), "p99": float(np.percentile(iters, 99)),
                        "max": int(iters.max()), "attempts_total": int(atts.sum())},
         "clocks": clocks,
