@@ -626,6 +626,9 @@ int tiny_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
   const bool r2 = o.algorithm == LP_R2HPDHG, cs = o.step_rule == LP_STEP_CONSTANT;
   const int64_t n = D.n, m = D.m;
   const int W = D.max_row, WT = D.max_col;
+  // ELL widths as tight as the LP allows: a padded slot is a zero-valued FMA on the attempt's
+  // dependent chain (C2, the 5x5 grid: every column of K has exactly two entries)
+  if (m <= 32 && n <= 64 && W <= 4 && WT <= 2) return launch_alg<1, 2, 4, 2>(P, r2, cs, s);
   if (m <= 32 && n <= 64 && W <= 4 && WT <= 4) return launch_alg<1, 2, 4, 4>(P, r2, cs, s);
   if (m <= 32 && n <= 64 && W <= 8 && WT <= 8) return launch_alg<1, 2, 8, 8>(P, r2, cs, s);
   return LP_ERR_UNSUPPORTED;
