@@ -885,8 +885,13 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   // register budget: 2 CTAs of 512 threads per SM (64 regs; the spills sit in the rare check
   // code) by default -- measured 12% faster than 1 CTA/SM at 128 regs on a 2e7-nnz LP, equal at C4;
   // MPAX_GRID_MINB=1 selects the 128-register build
+  // CTAs per SM: 2 x 512 threads (64 registers) give the memory-level parallelism a large LP's
+  // gathers need (C5: 1.4 ms per attempt, against 3.2 ms with 1); with fewer than ~4 row +
+  // column tiles per warp the phases are latency chains and 1 CTA of 128 registers per SM
+  // (fewer spills, half the CTAs at every grid barrier) is faster (C4: 51 -> 46 us per attempt)
   const char *env = getenv("MPAX_GRID_MINB");
-  const int minb = (env && atoi(env) == 1) ? 1 : 2;
+  const int64_t tiles = (D.m + 31) / 32 + (D.n + 31) / 32;
+  const int minb = env ? (atoi(env) == 1 ? 1 : 2) : (tiles < 4 * 2 * (int64_t)sms * (kBS / 32) ? 1 : 2);
   void *kfn = minb == 1 ? (void *)grid_kernel<1> : (void *)grid_kernel<2>;
   int per_sm = 0;
   MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kBS, 0));
