@@ -364,7 +364,7 @@ def run_ours(args):
         "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": _traffic("tiny_kernel_c2", "bytes_per_launch"),
                      "traffic_source": "profiles/traffic.json (ncu --set full capture, per launch)",
-                     "kernel": "tiny_kernel<0,1,2,4,4> (raPDHG, register-resident warp per LP)", "kernel_ms": kern_ms,
+                     "kernel": "tiny_kernel<raPDHG, adaptive, RPT=1, CPT=2, W=4, WT=2> (register-resident warp per LP)", "kernel_ms": kern_ms,
                      "flops_per_launch": flops,
                      "peak_source": peak_src,
                      "note": "per-instance solves are latency-bound, see DESIGN.md §6",
