@@ -239,21 +239,21 @@ def run_ours(args):
     X_d = torch.empty((args.batch, lp.n), dtype=torch.float64, device=dev)
     Y_d = torch.empty((args.batch, lp.m), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
-    def step(prob, Cx, X, Y, mem, alg=args.alg, rule="adaptive", rho=1.0):
+    def step(prob, Cx, X, Y, mem, alg=args.alg, rule="adaptive", rho=1.0, opts=None):
         bs = mp.BatchSolver(prob, Cx)
         # iteration_limit: safety net; every instance must be OPTIMAL
-        res = bs.solve(algorithm=alg, iteration_limit=200_000, step_rule=rule, reflection=rho)
+        res = bs.solve(algorithm=alg, iteration_limit=200_000, step_rule=rule, reflection=rho, **(opts or {}))
         bs.solutions(memory=mem, X=X, Y=Y)
         bs.close()
         return res
 
-    def timed(prob, Cx, X, Y, mem, steps, collect, alg=args.alg, rule="adaptive", rho=1.0):
+    def timed(prob, Cx, X, Y, mem, steps, collect, alg=args.alg, rule="adaptive", rho=1.0, opts=None):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         all_res = []
         for s in range(steps):
             flush.zero_()                       # evict L2 between steps (outside the event pair)
             ev[s][0].record(stream)
-            res = step(prob, Cx, X, Y, mem, alg, rule, rho)
+            res = step(prob, Cx, X, Y, mem, alg, rule, rho, opts)
             ev[s][1].record(stream)
             if collect:
                 all_res.append(res)
@@ -297,14 +297,18 @@ def run_ours(args):
     # ---- constant-step variants (reading 34), same workload ----
     log("constant-step variants")
     var_ms, var_res = {}, {}
-    # (name, algorithm, step rule, reflection): SURVEY §8(f) row 4, readings 34 and 38
-    VARIANTS = (("r2hpdhg_constant_step", "r2", "constant", 1.0), ("rapdhg_constant_step", "ra", "constant", 1.0),
-                ("r2hpdhg_partial_reflection_0.8", "r2", "adaptive", 0.8))
-    for name, va, rule, rho in VARIANTS:
-        step(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, va, rule, rho)
+    # (name, algorithm, step rule, reflection, options): SURVEY §8(f) rows 2 and 4, DESIGN.md
+    # readings 34, 36 and 38
+    POLISH = {"feasibility_polishing": 1}
+    VARIANTS = (("r2hpdhg_constant_step", "r2", "constant", 1.0, None),
+                ("rapdhg_constant_step", "ra", "constant", 1.0, None),
+                ("r2hpdhg_partial_reflection_0.8", "r2", "adaptive", 0.8, None),
+                ("rapdhg_feasibility_polishing", "ra", "adaptive", 1.0, POLISH))
+    for name, va, rule, rho, opts in VARIANTS:
+        step(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, va, rule, rho, opts)
         barrier()
         var_ms[name], var_res[name] = timed(prob_d, C_d, X_d, Y_d, mp.LP_DEVICE, args.secondary_steps, True, va,
-                                            rule, rho)
+                                            rule, rho, opts)
         barrier()
     t = torch.tensor([ms, ms_e2e, ms2] + [var_ms[v[0]] for v in VARIANTS], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -312,7 +316,7 @@ def run_ours(args):
     ms, ms_e2e, ms2 = float(t[0]), float(t[1]), float(t[2])
     var_ms = {v[0]: float(t[3 + i]) for i, v in enumerate(VARIANTS)}
     variants = {}
-    for name, va, rule, rho in VARIANTS:
+    for name, va, rule, rho, opts in VARIANTS:
         itv = np.array([r["iterations"] for r in var_res[name][-1]])
         variants[name] = {
             "algorithm": "r2hpdhg" if va == "r2" else "rapdhg", "step_rule": rule, "reflection": rho,
@@ -322,6 +326,10 @@ def run_ours(args):
             "iterations": {"p50": float(np.median(itv)), "p99": float(np.percentile(itv, 99)), "max": int(itv.max())}}
         if rule == "constant":
             variants[name]["step"] = "eta = 0.998 / sigma_max(K~), 200 power iterations (inside the timed step)"
+        if opts is POLISH:
+            variants[name]["polished"] = int(sum(r["polish"] == 1 for r in var_res[name][-1]))
+            variants[name]["polish"] = ("after the 1e-4 solve, primal (c = 0) and dual (q = 0) sub-solves to "
+                                        "eps_feas_polish = 1e-6 on the same kernel (inside the timed step)")
     it2 = np.array([r["iterations"] for r in res2[-1]])
     secondary = {"algorithm": "r2hpdhg" if alg2 == "r2" else "rapdhg",
                  "value": args.batch * args.secondary_steps * ws / (ms2 * 1e-3), "unit": UNIT,
@@ -397,6 +405,9 @@ def run_ours(args):
     if not args.no_spo and rank == 0:
         log("SPO+ leg (Warcraft-shaped batches)")
         line["spo"] = spo_leg(mp, torch, dev)
+    if rank == 0:
+        log("infeasibility-detection leg (mixed-status batch)")
+        line["infeasibility"] = infeasibility_leg(mp, torch, dev)
     if rank == 0:
         log("batch-size scaling leg (C2 shape)")
         line["batch_scaling"] = batch_scaling_leg(mp, torch, dev)
@@ -628,6 +639,47 @@ def dense_leg(mp, torch, dev, peaks):
         out[name] = d
     out["speedup_dmma_vs_per_instance"] = out["dmma"]["value"] / out["per_instance"]["value"]
     return out
+
+
+def infeasibility_leg(mp, torch, dev, batch=1024, reps=5):
+    """SURVEY §8(f) row 1 on a batch: 1024 LPs sharing K (lpgen.g_infeasible("dual")), half of
+    the cost vectors bounded (OPTIMAL), half unbounded (DUAL_INFEASIBLE, certified by the primal
+    ray of P:530-531); the C2 step (create + solve + get + destroy, device-resident)."""
+    for seed in range(200):   # the first planted LP whose K fits the register-resident kernel
+        lp = lpgen.g_infeasible("dual", seed, m1=10, m2=3, n=20, density=0.15)
+        if np.diff(lp.row_ptr).max() <= 8 and np.bincount(lp.col_idx, minlength=lp.n).max() <= 8:
+            break
+    j = int(np.nonzero(~np.isfinite(lp.u))[0][0])
+    rng = np.random.default_rng(5)
+    C = lp.c + 0.1 * rng.normal(size=(batch, lp.n))
+    C[::2, j] = np.abs(C[::2, j]) + 1.0
+    C[1::2, j] = -np.abs(C[1::2, j]) - 0.5
+    want = np.where(np.arange(batch) % 2 == 0, mp.LP_OPTIMAL, mp.LP_DUAL_INFEASIBLE)
+    prob = mp.Problem.from_lp(lp).to(dev)
+    Cd = torch.as_tensor(C, device=dev)
+    X = torch.empty((batch, lp.n), dtype=torch.float64, device=dev)
+    Y = torch.empty((batch, lp.m), dtype=torch.float64, device=dev)
+    best, ok = None, True
+    for rep in range(reps + 1):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(torch.cuda.current_stream())
+        bs = mp.BatchSolver(prob, Cd)
+        res = bs.solve(algorithm="ra", iteration_limit=200_000)
+        bs.solutions(memory=mp.LP_DEVICE, X=X, Y=Y)
+        bs.close()
+        e1.record(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        ok &= bool((np.asarray(res["status"]) == want).all())
+        if rep:
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+    it = np.asarray(res["iterations"])
+    return {"workload": f"{batch} sparse LPs sharing K ({lp.m} x {lp.n}), half unbounded, raPDHG, 1e-4 / "
+                        "infeasibility tolerance 1e-8", "unit": UNIT, "ms_per_step": best,
+            "value": batch / (best * 1e-3), "statuses_as_planted": ok,
+            "iterations": {"p50_optimal": float(np.median(it[::2])), "p50_infeasible": float(np.median(it[1::2])),
+                           "max": int(it.max())}}
 
 
 def batch_scaling_leg(mp, torch, dev, sizes=(4096, 16384, 65536), reps=3):
