@@ -641,10 +641,10 @@ def dense_leg(mp, torch, dev, peaks):
     return out
 
 
-def infeasibility_leg(mp, torch, dev, batch=1024, reps=5):
-    """SURVEY §8(f) row 1 on a batch: 1024 LPs sharing K (lpgen.g_infeasible("dual")), half of
-    the cost vectors bounded (OPTIMAL), half unbounded (DUAL_INFEASIBLE, certified by the primal
-    ray of P:530-531); the C2 step (create + solve + get + destroy, device-resident)."""
+def infeasibility_workload(batch):
+    """The infeasibility leg's batch: one planted LP (lpgen.g_infeasible("dual"): column j has
+    G[:, j] >= 0, A[:, j] = 0, u_j = +inf) with perturbed costs; c_j > 0 on even instances
+    (bounded) and c_j < 0 on odd ones (unbounded along e_j).  Returns (lp, C, unbounded mask)."""
     for seed in range(200):   # the first planted LP whose K fits the register-resident kernel
         lp = lpgen.g_infeasible("dual", seed, m1=10, m2=3, n=20, density=0.15)
         if np.diff(lp.row_ptr).max() <= 8 and np.bincount(lp.col_idx, minlength=lp.n).max() <= 8:
@@ -654,7 +654,14 @@ def infeasibility_leg(mp, torch, dev, batch=1024, reps=5):
     C = lp.c + 0.1 * rng.normal(size=(batch, lp.n))
     C[::2, j] = np.abs(C[::2, j]) + 1.0
     C[1::2, j] = -np.abs(C[1::2, j]) - 0.5
-    want = np.where(np.arange(batch) % 2 == 0, mp.LP_OPTIMAL, mp.LP_DUAL_INFEASIBLE)
+    return lp, C, np.arange(batch) % 2 == 1
+
+def infeasibility_leg(mp, torch, dev, batch=1024, reps=5):
+    """SURVEY §8(f) row 1 on a batch: 1024 LPs sharing K (lpgen.g_infeasible("dual")), half of
+    the cost vectors bounded (OPTIMAL), half unbounded (DUAL_INFEASIBLE, certified by the primal
+    ray of P:530-531); the C2 step (create + solve + get + destroy, device-resident)."""
+    lp, C, unbounded = infeasibility_workload(batch)
+    want = np.where(unbounded, mp.LP_DUAL_INFEASIBLE, mp.LP_OPTIMAL)
     prob = mp.Problem.from_lp(lp).to(dev)
     Cd = torch.as_tensor(C, device=dev)
     X = torch.empty((batch, lp.n), dtype=torch.float64, device=dev)

@@ -54,3 +54,17 @@ def test_gather_floor_split_and_monotone():
     assert full2 - full == pytest.approx(((88e7 + 88 * 5e6) - (64e7 + 56 * 5e6)) / (HBM * 1e9) * 1e6, rel=1e-9)
     # more nonzeros, larger floor
     assert bench.gather_floor_us(10_000_000, 5_000_000, 200_000_000, "ra", HBM)[1] > pair
+
+
+def test_infeasibility_leg_statuses_are_as_planted():
+    """The bench's mixed-status batch: the oracle classifies a sample exactly as planted
+    (OPTIMAL for c_j > 0, DUAL_INFEASIBLE for c_j < 0 along the unbounded column)."""
+    import numpy as np
+    import oracle
+    lp, C, unbounded = bench.infeasibility_workload(1024)
+    assert C.shape == (1024, lp.n) and unbounded.sum() == 512
+    assert np.diff(lp.row_ptr).max() <= 8 and np.bincount(lp.col_idx, minlength=lp.n).max() <= 8
+    idx = np.arange(0, 1024, 37)
+    _, _, res = oracle.solve_batch(lp, C[idx], None, "ra", iteration_limit=200_000)
+    got = np.array([r["status"] for r in res])
+    assert (got == np.where(unbounded[idx], oracle.DUAL_INFEASIBLE, oracle.OPTIMAL)).all()
