@@ -27,7 +27,11 @@
  * reductions are sequential, so results do not depend on the thread count.
  *
  * Parity status: every function is pinned by tests in
- * tests/test_oracle_*.py EXCEPT the iteration / attempt / restart COUNTS of a
+ * tests/test_oracle_*.py -- including the readings the paper leaves unquantified
+ * (KKT_omega, omega0 / eta0, the restart candidate, the r2HPDHG epoch reference:
+ * hand-derived values in tests/golden/readings.json) -- and
+ * tests/test_oracle_mutations.py checks that 19 plausible one-line slips in this
+ * file each fail a pin.  NOT pinned: the iteration / attempt / restart COUNTS of a
  * full solve, which are "parity unpinned" externally (the paper prints counts
  * only for datasets we do not have); only GPU == oracle applies to
  * them.
@@ -461,6 +465,34 @@ static double kkt_omega(const scaled_lp *S, double omega, const double *x, const
   return sqrt(omega * r.pres * r.pres + r.dres * r.dres / omega + r.gap * r.gap);
 }
 
+/* Initial primal weight and step (contract step 2; readings c.3 #5 and #7):
+ *   omega0 = ||c~|| / ||q~|| of the SCALED costs and right-hand side if both exceed 1e-10,
+ *            else 1;
+ *   eta0   = 1 / max_ij |K~_ij| (adaptive step; 1 if K~ = 0), or 0.998 / sigma_max(K~) for the
+ *            constant-step variant (reading 34), so tau sigma ||K~||^2 = eta^2 sigma^2 < 1. */
+static void initial_weight_and_step(const scaled_lp *S, const ora_options *o, double *omega, double *eta) {
+  const int64_t n = S->n, m = S->m;
+  *omega = 1.0;
+  double nc = norm2(S->c, n), nq = m ? norm2(S->q, m) : 0.0;
+  if (nc > 1e-10 && nq > 1e-10) *omega = nc / nq;
+  *eta = 1.0;
+  if (o->step_rule != 1) {
+    double mx = 0.0;
+    for (int64_t k = 0; k < S->K.nnz; ++k) mx = dmax(mx, fabs(S->K.v[k]));
+    if (mx > 0.0) *eta = 1.0 / mx;
+  } else {
+    double sg = power_sigma(&S->K, &S->KT, o->power_iters);
+    if (sg > 0.0) *eta = 0.998 / sg;
+  }
+}
+
+/* raPDHG restart candidate (contract step 5, reading c.3 #10): the average if its
+ * KKT_omega is STRICTLY smaller than the current iterate's, else the current iterate
+ * (a tie keeps the current point).  Returns 1 for the average. */
+int32_t ora_restart_candidate(double kkt_omega_avg, double kkt_omega_cur) {
+  return kkt_omega_avg < kkt_omega_cur ? 1 : 0;
+}
+
 /* ---------------------------------------------------------- the solve ---- */
 
 static void log_attempt(ora_log *g, int64_t j, int32_t acc, double eta, double eta_bar) {
@@ -600,22 +632,9 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
   double *xo = malloc(bn), *KTyo = malloc(bn), *yo = malloc(bm), *Kxo = malloc(bm);
 
   /* ---- Step 2: initialise (P:251 zero start; warm start P:249-267) ---- */
-  double omega = 1.0;
-  {
-    double nc = norm2(S->c, n), nq = m ? norm2(S->q, m) : 0.0;
-    if (nc > 1e-10 && nq > 1e-10) omega = nc / nq;
-  }
-  double eta = 1.0;
+  double omega, eta;
   const int const_step = (o->step_rule == 1);
-  if (!const_step) {
-    double mx = 0.0;
-    for (int64_t k = 0; k < S->K.nnz; ++k) mx = dmax(mx, fabs(S->K.v[k]));
-    if (mx > 0.0) eta = 1.0 / mx;
-  } else {
-    /* constant step: eta = 0.998 / sigma_max(K~), so tau sigma ||K~||^2 = eta^2 sigma^2 < 1 */
-    double sg = power_sigma(&S->K, &S->KT, o->power_iters);
-    if (sg > 0.0) eta = 0.998 / sg;
-  }
+  initial_weight_and_step(S, o, &omega, &eta);
   for (int64_t jj = 0; jj < n; ++jj) x[jj] = median3(S->l[jj], x0 ? x0[jj] / S->Dc[jj] : 0.0, S->u[jj]);
   for (int64_t i = 0; i < m; ++i) y[i] = y0 ? y0[i] / S->Dr[i] : 0.0;
   project_dual(y, m1);
@@ -735,7 +754,7 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
       }
       double e_c = kkt_omega(S, omega, x, y, Kx, KTy);
       double e_a = kkt_omega(S, omega, xa, ya, Kxa, KTya);
-      if (e_a < e_c) { cx = xa; cy = ya; cKx = Kxa; cKTy = KTya; metric = e_a; }
+      if (ora_restart_candidate(e_a, e_c)) { cx = xa; cy = ya; cKx = Kxa; cKTy = KTya; metric = e_a; }
       else { cx = x; cy = y; cKx = Kx; cKTy = KTy; metric = e_c; }
     } else {
       ora_kkt kw;
@@ -1034,5 +1053,38 @@ int ora_certificate_test(const ora_problem *p, const double *dx, const double *d
   int e = ora_spmv_pair(p, dx, Kdx, dy, KTdy);
   if (!e) certificate_test(n, m, p->m1, p->c, p->q, p->l, p->u, dx, Kdx, dy, KTdy, eps_p, eps_d, out);
   free(Kdx); free(KTdy);
+  return e;
+}
+
+/* Weighted KKT error of (x, y) on the problem AS GIVEN (no scaling; products with K):
+ * the raPDHG restart metric sqrt(omega pres^2 + dres^2 / omega + gap^2) of contract step 5,
+ * evaluated by the same routine the solve applies to the scaled problem (pins). */
+int ora_kkt_omega(const ora_problem *p, double omega, const double *x, const double *y, double *out) {
+  int64_t n = p->n, m = p->m1 + p->m2;
+  double *Kx = malloc((size_t)(m ? m : 1) * sizeof(double)), *KTy = malloc((size_t)n * sizeof(double));
+  int e = ora_spmv_pair(p, x, Kx, y, KTy);
+  scaled_lp S;
+  memset(&S, 0, sizeof(S));
+  S.n = n; S.m = m; S.m1 = p->m1;
+  S.c = (double *)p->c; S.q = (double *)p->q; S.l = (double *)p->l; S.u = (double *)p->u;
+  if (!e) *out = kkt_omega(&S, omega, x, y, Kx, KTy);
+  free(Kx); free(KTy);
+  return e;
+}
+
+/* omega0 and eta0 of contract step 2 for the problem scaled with the options'
+ * ruiz_iters / pock_chambolle (pins of readings c.3 #5, #7 and 34). */
+int ora_initial_steps(const ora_problem *p, const ora_options *o, double *omega0, double *eta0) {
+  int e = ora_validate(p);
+  if (e) return e;
+  if ((e = check_options(o))) return e;
+  int64_t m = p->m1 + p->m2;
+  double *Dr = (double *)malloc((size_t)(m ? m : 1) * sizeof(double));
+  double *Dc = (double *)malloc((size_t)p->n * sizeof(double));
+  ora_precondition(p, o->ruiz_iters, o->pock_chambolle, Dr, Dc);
+  scaled_lp S;
+  if ((e = build_scaled(p, Dr, Dc, NULL, NULL, &S)) == ORA_OK) initial_weight_and_step(&S, o, omega0, eta0);
+  scaled_free(&S, 1);
+  free(Dr); free(Dc);
   return e;
 }

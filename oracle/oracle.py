@@ -16,6 +16,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "mpax_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# tests/test_oracle_mutations.py points this at a deliberately mutated build
+_LIB_OVERRIDE = os.environ.get("MPAX_ORACLE_LIB")
 _lock = threading.Lock()
 _lib = None
 
@@ -85,7 +87,7 @@ def lib():
     global _lib
     with _lock:
         if _lib is None:
-            L = C.CDLL(build())
+            L = C.CDLL(_LIB_OVERRIDE or build())
             P = C.POINTER
             L.ora_validate.argtypes = [P(Problem)]
             L.ora_solve.argtypes = [P(Problem), P(Options), C.c_void_p, C.c_void_p, C.c_void_p,
@@ -121,6 +123,10 @@ def lib():
                                           C.c_void_p]
             L.ora_certificate_test.argtypes = [P(Problem), C.c_void_p, C.c_void_p, C.c_double, C.c_double,
                                                P(Certificate)]
+            L.ora_kkt_omega.argtypes = [P(Problem), C.c_double, C.c_void_p, C.c_void_p, P(C.c_double)]
+            L.ora_initial_steps.argtypes = [P(Problem), P(Options), P(C.c_double), P(C.c_double)]
+            L.ora_restart_candidate.argtypes = [C.c_double, C.c_double]
+            L.ora_restart_candidate.restype = C.c_int32
             _lib = L
     return _lib
 
@@ -148,8 +154,9 @@ class _Bound:
 
 
 def options(algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, check_frequency=64,
-            ruiz_iters=10, pock_chambolle=1, step_rule=0, power_iters=200, eps_primal_infeasible=1e-8,
-            eps_dual_infeasible=1e-8, feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0):
+            step_rule=0, power_iters=200, eps_primal_infeasible=1e-8,
+            eps_dual_infeasible=1e-8, feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0,
+            ruiz_iters=10, pock_chambolle=1):
     o = Options()
     lib().ora_default_options(C.byref(o))
     o.algorithm = R2HPDHG if algorithm in ("r2", "r2hpdhg", R2HPDHG) else RAPDHG
@@ -173,7 +180,7 @@ def validate(lp) -> int:
 
 def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, x0=None, y0=None,
           check_frequency=64, log_capacity=0, step_rule=0, eps_primal_infeasible=1e-8, eps_dual_infeasible=1e-8,
-          feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0):
+          feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0, ruiz_iters=10, pock_chambolle=1):
     """Full solve (contract steps 0-6).  Returns a dict with x, y, lam, the
     result fields, and (if log_capacity) the attempt/check decision logs."""
     b = _Bound(lp)
@@ -181,7 +188,7 @@ def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, 
     o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule,
                 eps_primal_infeasible=eps_primal_infeasible, eps_dual_infeasible=eps_dual_infeasible,
                 feasibility_polishing=feasibility_polishing, eps_feas_polish=eps_feas_polish,
-                reflection=reflection)
+                reflection=reflection, ruiz_iters=ruiz_iters, pock_chambolle=pock_chambolle)
     x = np.zeros(lp.n)
     y = np.zeros(m)
     lam = np.zeros(lp.n)
@@ -379,3 +386,30 @@ def certificate_test(lp, dx, dy, eps_primal_infeasible=1e-8, eps_dual_infeasible
     if e != 0:
         raise ValueError(f"oracle error {e}")
     return {f: getattr(r, f) for f, _ in r._fields_}
+
+
+def kkt_omega(lp, omega, x, y):
+    """The raPDHG restart metric sqrt(omega pres^2 + dres^2/omega + gap^2) of (x, y) on the
+    problem as given (contract step 5)."""
+    b = _Bound(lp)
+    xa = _f64(x)
+    ya = _f64(y) if (lp.m1 + lp.m2) else np.zeros(1)
+    out = C.c_double()
+    lib().ora_kkt_omega(C.byref(b.s), omega, xa.ctypes.data, ya.ctypes.data, C.byref(out))
+    return out.value
+
+
+def initial_steps(lp, step_rule=0, ruiz_iters=10, pock_chambolle=1):
+    """(omega0, eta0) of contract step 2 on the problem scaled with the given rounds."""
+    b = _Bound(lp)
+    o = options("ra", step_rule=step_rule, ruiz_iters=ruiz_iters, pock_chambolle=pock_chambolle)
+    om, et = C.c_double(), C.c_double()
+    e = lib().ora_initial_steps(C.byref(b.s), C.byref(o), C.byref(om), C.byref(et))
+    if e != 0:
+        raise ValueError(f"oracle error {e}")
+    return om.value, et.value
+
+
+def restart_candidate(kkt_omega_avg, kkt_omega_cur):
+    """'avg' if the average's KKT_omega is strictly smaller, else 'cur' (reading c.3 #10)."""
+    return "avg" if lib().ora_restart_candidate(kkt_omega_avg, kkt_omega_cur) else "cur"
