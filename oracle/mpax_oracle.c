@@ -337,11 +337,13 @@ static void project_dual(double *y, int64_t m1) {
 }
 
 /* Adaptive step size ("heuristic line search"; contract step 3, reading
- * c.3 #4): eta_bar = M / (2|I|) (+inf if I == 0), accept iff eta <= eta_bar,
- * eta_next = min((1-(j+1)^-0.3) eta_bar, (1+(j+1)^-0.6) eta). */
+ * c.3 #4): M = omega dx2 + dy2 omega^-1, eta_bar = M / (2|I|) (+inf if I == 0),
+ * accept iff eta <= eta_bar, eta_next = min((1-(j+1)^-0.3) eta_bar, (1+(j+1)^-0.6) eta).
+ * omega^-1 = 1 / omega (reading 32: every x / omega of the iteration is x * omega^-1). */
 void ora_step_size(double eta, double omega, double dx2, double dy2, double I, int64_t j,
                    double *eta_bar, int32_t *acc, double *eta_next) {
-  double M = omega * dx2 + dy2 / omega;
+  double inv_omega = 1.0 / omega;
+  double M = omega * dx2 + dy2 * inv_omega;
   double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : ORA_INF;
   double jp1 = (double)(j + 1);
   *eta_bar = eb;
@@ -457,12 +459,14 @@ double ora_rel_kkt(const ora_kkt *r, double norm_q, double norm_c) {
 }
 
 /* Weighted scaled-space KKT error used as raPDHG's restart metric ("KKT
- * error for raPDHG"; contract step 5):  sqrt(omega pres~^2 + dres~^2/omega + gap~^2). */
+ * error for raPDHG"; contract step 5):  sqrt(omega pres~^2 + dres~^2 omega^-1 + gap~^2),
+ * omega^-1 = 1 / omega (reading 32). */
 static double kkt_omega(const scaled_lp *S, double omega, const double *x, const double *y,
                         const double *Kx, const double *KTy) {
   ora_kkt r;
   kkt_residuals(S->n, S->m, S->m1, x, y, Kx, KTy, S->c, S->q, S->l, S->u, &r);
-  return sqrt(omega * r.pres * r.pres + r.dres * r.dres / omega + r.gap * r.gap);
+  double inv_omega = 1.0 / omega;
+  return sqrt(omega * r.pres * r.pres + r.dres * r.dres * inv_omega + r.gap * r.gap);
 }
 
 /* Initial primal weight and step (contract step 2; readings c.3 #5 and #7):
@@ -655,7 +659,7 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
     double eta_used = eta, M = 0.0, I = 0.0;
     while (!acc) {
       j += 1;
-      double tau = eta / omega, sigma = eta * omega;
+      double tau = eta * (1.0 / omega), sigma = eta * omega;   /* reading 32: x / omega as x * omega^-1 */
       for (int64_t jj = 0; jj < n; ++jj)
         xp[jj] = median3(S->l[jj], x[jj] - tau * (S->c[jj] - KTy[jj]), S->u[jj]);
       csr_spmv(&S->K, xp, Kxp);                                   /* SpMV #1 */
@@ -669,7 +673,7 @@ static void solve_scaled(const scaled_lp *S, const ora_options *o, const double 
         dy2 += d * d;
         I += d * (Kxp[i] - Kx[i]);
       }
-      M = omega * dx2 + dy2 / omega;
+      M = omega * dx2 + dy2 * (1.0 / omega);
       double eta_bar, eta_next;
       eta_used = eta;
       ora_step_size(eta, omega, dx2, dy2, I, j, &eta_bar, &acc, &eta_next);

@@ -72,7 +72,7 @@ struct DmmaParams {
 
 // per-instance scalar state (identical copy in every CTA of the cluster)
 struct Inst {
-  double omega, eta, W, ref, last, theta, ha, hb, rP, nc0, nq0, metric, dx2c, dy2c, eta_used, M, I;
+  double omega, inv_omega, eta, W, ref, last, theta, ha, hb, rP, nc0, nq0, metric, dx2c, dy2c, eta_used, M, I;
   double ray_ny, ray_nx;  // infeasibility rays' norms (reading 35)
   long long k, j, k_in, restarts;
   int rejects, status, pending, done, check, outsel, csel, valid, cert, rays, skip;
@@ -84,41 +84,6 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-struct K5 {
-  double pres, dres, pobj, dobj, gap;
-};
-__device__ __forceinline__ K5 mk5(const double *v) {
-  K5 k;
-  k.pres = sqrt(v[0]); k.dres = sqrt(v[1]); k.pobj = v[2]; k.dobj = v[3]; k.gap = fabs(v[2] - v[3]);
-  return k;
-}
-__device__ __forceinline__ bool pass5(const K5 &k, double nq, double nc, double ea, double er) {
-  return k.pres <= ea + er * nq && k.dres <= ea + er * nc && k.gap <= ea + er * (fabs(k.pobj) + fabs(k.dobj));
-}
-__device__ __forceinline__ double rel5(const K5 &k, double nq, double nc) {
-  return fmax(k.pres / (1.0 + nq), fmax(k.dres / (1.0 + nc), k.gap / (1.0 + fabs(k.pobj) + fabs(k.dobj))));
-}
-__device__ __forceinline__ void krow(double *v, bool orig, bool ge, double dr, double ys, double Kxs, double q0,
-                                     double qs) {
-  const double Kx = orig ? Kxs / dr : Kxs, q = orig ? q0 : qs, y = orig ? dr * ys : ys;
-  double r = q - Kx;
-  if (ge) r = fmax(r, 0.0);
-  v[0] += r * r;
-  v[3] += q * y;
-}
-__device__ __forceinline__ void kcol(double *v, bool orig, double dc, double xs, double KTys, double c0, double cs,
-                                     double l0, double ls, double u0, double us) {
-  const double x = orig ? dc * xs : xs, KTy = orig ? KTys / dc : KTys;
-  const double c = orig ? c0 : cs, l = orig ? l0 : ls, u = orig ? u0 : us;
-  const double lam = c - KTy, lp = fmax(lam, 0.0), lm = fmax(-lam, 0.0);
-  double d = 0.0;
-  if (l == -INFINITY) d += lp;
-  if (u == INFINITY) d += lm;
-  v[1] += d * d;
-  v[2] += c * x;
-  if (l > -INFINITY) v[3] += l * lp;
-  if (u < INFINITY) v[3] -= u * lm;
-}
 
 // Shared-memory layout of one CTA.
 struct Smem {
@@ -365,9 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
   // r2HPDHG reflection z <- a((1 + rho) w - rho z) + b z0 (rho = 1: 2 PDHG(z) - z; reading 38)
   const double rf1 = 1.0 + P.rho, rf0 = P.rho;
   // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
-  auto tpass = [&](const K5 &k, double nq, double nc) {
+  auto tpass = [&](const Kkt5 &k, double nq, double nc) {
     return P.polish_mode ? polish_pass(P.polish_mode, k.pres, k.dres, nq, nc, P.eps_fp)
-                         : pass5(k, nq, nc, P.eps_abs, P.eps_rel);
+                         : kkt5_pass(k, nq, nc, P.eps_abs, P.eps_rel);
   };
 
   for (;;) {
@@ -425,6 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         I.nc0 = sqrt(t4[2]); I.nq0 = sqrt(t4[3]);
         I.omega = 1.0;
         if (sqrt(t4[0]) > 1e-10 && sqrt(t4[1]) > 1e-10) I.omega = sqrt(t4[0]) / sqrt(t4[1]);
+        I.inv_omega = 1.0 / I.omega;  // every x / omega is x * omega^-1 (reading 32)
         I.eta = eta0; I.last = INFINITY;
       }
       // full y0 from the peers' row slices
@@ -448,14 +414,14 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         for (int c = 0; c < CL; ++c) a += cl.map_shared_rank(S.Pc, c)[i * kS + s];
         const int64_t b = b0 + s;
         P.Kx[b * m + i] = a; P.Kxa[b * m + i] = a; P.Kxp[b * m + i] = a;
-        krow(v[s], false, i < m1, 1.0, P.y[b * m + i], a, 0.0, P.qs[b * m + i]);
+        kkt_row_acc(v[s], false, i < m1, 1.0, P.y[b * m + i], a, 0.0, P.qs[b * m + i]);
       }
       gemm1(S, np, mp, [&](int jj, int s, double val) {
         if (jj >= jn || !S.inst[s].valid) return;
         const int64_t b = b0 + s;
         const int j = j0 + jj;
         P.KTy[b * n + j] = val; P.KTya[b * n + j] = val; P.KTyp[b * n + j] = val;
-        kcol(v[s], false, 1.0, P.x[b * n + j], val, 0.0, P.cs[b * n + j], 0.0, P.ls[j], 0.0, P.us[j]);
+        kkt_col_acc(v[s], false, 1.0, P.x[b * n + j], val, 0.0, P.cs[b * n + j], 0.0, P.ls[j], 0.0, P.us[j]);
       });
       S.part = (S.part == S.part_a) ? S.part_b : S.part_a;  // double-buffered (see grid_solver.cu)
       cta_partials<4>(v, S);
@@ -463,8 +429,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       cluster_totals<CL, 4>(cl, S, tot);
       if (tid < kS && S.inst[tid].valid && !r2) {
         Inst &I = S.inst[tid];
-        const K5 ks = mk5(tot + tid * 24);
-        I.ref = sqrt(I.omega * ks.pres * ks.pres + ks.dres * ks.dres / I.omega + ks.gap * ks.gap);
+        const Kkt5 ks = kkt5(tot + tid * 24);
+        I.ref = kkt_omega(ks, I.omega, I.inv_omega);
       }
       __syncthreads();
     }
@@ -494,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           }
           P.x[o] = xv; P.KTy[o] = kt;
         }
-        const double tau = I.eta / I.omega;
+        const double tau = I.eta * I.inv_omega;
         const double xn = median3(P.ls[j], xv - tau * (P.cs[o] - kt), P.us[j]);
         P.xp[o] = xn;
         S.Xc[jj * kS + s] = xn;
@@ -558,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           double f1, f2;
           step_factors(P.tab, I.j, f1, f2);
           const double Iv = t3[2];
-          const double M = I.omega * t3[0] + t3[1] / I.omega;
+          const double M = I.omega * t3[0] + t3[1] * I.inv_omega;
           const double eb = (Iv != 0.0) ? M / (2.0 * fabs(Iv)) : INFINITY;
           const bool acc = cstep || I.eta <= eb;
           const double eta_used = I.eta;
@@ -624,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
             const double t6[6] = {acc.sy, acc.sx, acc.oy, acc.ox, acc.vy, acc.vx};
             frag_col<6, (3u << 4)>(vq, s, t6);
             double tc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            kcol(tc, true, P.Dc[j], xpv, kty, P.C0[b * P.cstride + j], P.cs[o], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+            kkt_col_acc(tc, true, P.Dc[j], xpv, kty, P.C0[b * P.cstride + j], P.cs[o], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
             const double d = xpv - P.xr[o];
             tc[4] = d * d;
             frag_col<6, 0u>(vc, s, tc);
@@ -659,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
             const double t6[6] = {acc.sy, 0.0, acc.oy, 0.0, acc.vy, acc.vx};
             frag_row<6, (3u << 4)>(vq, t6);
             double tr[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            krow(tr, true, i < m1, P.Dr[i], ypv, kxp, P.Q0[b * P.qstride + i], P.qs[o]);
+            kkt_row_acc(tr, true, i < m1, P.Dr[i], ypv, kxp, P.Q0[b * P.qstride + i], P.qs[o]);
             const double d = ypv - P.yr[o];
             tr[5] = d * d;
             frag_row<6, 0u>(vc, tr);
@@ -693,7 +659,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           Inst &I = S.inst[tid];
           if (I.check) {
             const double *t6 = tot + tid * 24;
-            const K5 kw = mk5(t6);
+            const Kkt5 kw = kkt5(t6);
             if (tpass(kw, I.nq0, I.nc0)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 1; }
             else if (I.cert) { I.status = I.cert; I.done = 1; I.outsel = 0; I.rays = 1; }
             else if (I.k == P.iter_limit) { I.status = LP_ITERATION_LIMIT; I.done = 1; I.outsel = 1; }
@@ -729,10 +695,10 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           double tr[20];
 #pragma unroll
           for (int k = 0; k < 20; ++k) tr[k] = 0.0;
-          krow(tr + 0, true, ge, dr, yai, kxa, q0, qsi);
-          krow(tr + 4, true, ge, dr, yi, kxi, q0, qsi);
-          krow(tr + 8, false, ge, dr, yai, kxa, q0, qsi);
-          krow(tr + 12, false, ge, dr, yi, kxi, q0, qsi);
+          kkt_row_acc(tr + 0, true, ge, dr, yai, kxa, q0, qsi);
+          kkt_row_acc(tr + 4, true, ge, dr, yi, kxi, q0, qsi);
+          kkt_row_acc(tr + 8, false, ge, dr, yai, kxa, q0, qsi);
+          kkt_row_acc(tr + 12, false, ge, dr, yi, kxi, q0, qsi);
           const double da = yai - P.yr[o], dcur = yi - P.yr[o];
           tr[17] = da * da;
           tr[19] = dcur * dcur;
@@ -750,10 +716,10 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           double tc[20];
 #pragma unroll
           for (int k = 0; k < 20; ++k) tc[k] = 0.0;
-          kcol(tc + 0, true, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
-          kcol(tc + 4, true, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
-          kcol(tc + 8, false, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
-          kcol(tc + 12, false, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+          kkt_col_acc(tc + 0, true, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
+          kkt_col_acc(tc + 4, true, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+          kkt_col_acc(tc + 8, false, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
+          kkt_col_acc(tc + 12, false, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
           const double da = xaj - P.xr[o], dcur = xj - P.xr[o];
           tc[16] = da * da;
           tc[18] = dcur * dcur;
@@ -767,19 +733,18 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           Inst &I = S.inst[tid];
           if (I.check) {
             const double *t = tot + tid * 24;
-            const K5 ka = mk5(t + 0), kc = mk5(t + 4);
+            const Kkt5 ka = kkt5(t + 0), kc = kkt5(t + 4);
             if (tpass(ka, I.nq0, I.nc0)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 1; }
             else if (tpass(kc, I.nq0, I.nc0)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 0; }
             else if (I.cert) { I.status = I.cert; I.done = 1; I.outsel = 0; I.rays = 1; }
             else if (I.k == P.iter_limit) {
               I.status = LP_ITERATION_LIMIT; I.done = 1;
-              I.outsel = rel5(ka, I.nq0, I.nc0) < rel5(kc, I.nq0, I.nc0) ? 1 : 0;
+              I.outsel = kkt5_rel(ka, I.nq0, I.nc0) < kkt5_rel(kc, I.nq0, I.nc0) ? 1 : 0;
             } else {
-              const K5 sa = mk5(t + 8), sc = mk5(t + 12);
-              const double om = I.omega;
-              const double e_a = sqrt(om * sa.pres * sa.pres + sa.dres * sa.dres / om + sa.gap * sa.gap);
-              const double e_c = sqrt(om * sc.pres * sc.pres + sc.dres * sc.dres / om + sc.gap * sc.gap);
-              if (e_a < e_c) { I.csel = 1; I.metric = e_a; I.dx2c = t[16]; I.dy2c = t[17]; }
+              const Kkt5 sa = kkt5(t + 8), sc = kkt5(t + 12);
+              const double e_a = kkt_omega(sa, I.omega, I.inv_omega);
+              const double e_c = kkt_omega(sc, I.omega, I.inv_omega);
+              if (restart_to_average(e_a, e_c)) { I.csel = 1; I.metric = e_a; I.dx2c = t[16]; I.dy2c = t[17]; }
               else { I.csel = 0; I.metric = e_c; I.dx2c = t[18]; I.dy2c = t[19]; }
             }
           }
@@ -791,14 +756,13 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         Inst &I = S.inst[tid];
         I.pending = 0;
         if (I.check && !I.done) {
-          const bool restart = ((double)I.k_in >= 0.36 * (double)I.k) || (I.metric <= 0.2 * I.ref) ||
-                               (I.metric <= 0.8 * I.ref && I.metric > I.last);
+          const bool restart = restart_due(I.k_in, I.k, I.metric, I.ref, I.last);
           I.last = I.metric;
           I.check = restart ? 2 : 0;
           if (restart) {
             I.restarts += 1;
-            const double dxn = sqrt(I.dx2c), dyn = sqrt(I.dy2c);
-            if (dxn > 1e-10 && dyn > 1e-10) I.omega = sqrt(I.omega * (dyn / dxn));
+            I.omega = primal_weight(I.omega, sqrt(I.dx2c), sqrt(I.dy2c));
+            I.inv_omega = 1.0 / I.omega;
             I.k_in = 0;
             if (!r2) { I.W = 0.0; I.ref = I.metric; }
           }
@@ -850,7 +814,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         const double xs = I.outsel ? (r2 ? P.xp[o] : P.xa[o]) : P.x[o];
         const double kt = I.outsel ? (r2 ? P.KTyp[o] : P.KTya[o]) : P.KTy[o];
         const double dc = P.Dc[j], c0 = P.C0[b * P.cstride + j];
-        kcol(v[s], true, dc, xs, kt, c0, P.cs[o], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+        kkt_col_acc(v[s], true, dc, xs, kt, c0, P.cs[o], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
         if (I.rays) {  // infeasible: unit rays against the base (r2: anchor; ra: parked pre-step point)
           const double xb = r2 ? P.xa[o] : P.xp[o], ktb = r2 ? P.KTya[o] : P.KTyp[o];
           P.X[o] = dc * (xs - xb) / I.ray_nx;
@@ -869,7 +833,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         const double ys = I.outsel ? (r2 ? P.yp[o] : P.ya[o]) : P.y[o];
         const double kx = I.outsel ? (r2 ? P.Kxp[o] : P.Kxa[o]) : P.Kx[o];
         const double dr = P.Dr[i];
-        krow(v[s], true, i < m1, dr, ys, kx, P.Q0[b * P.qstride + i], P.qs[o]);
+        kkt_row_acc(v[s], true, i < m1, dr, ys, kx, P.Q0[b * P.qstride + i], P.qs[o]);
         if (I.rays) P.Y[o] = dr * (ys - (r2 ? P.ya[o] : P.yp[o])) / I.ray_ny;
         else P.Y[o] = dr * ys;
       }
@@ -879,13 +843,13 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       cluster_totals<CL, 4>(cl, S, tot);
       if (crank == 0 && tid < kS && S.inst[tid].valid && !S.inst[tid].skip) {
         const Inst &I = S.inst[tid];
-        const K5 ko = mk5(tot + tid * 24);
+        const Kkt5 ko = kkt5(tot + tid * 24);
         lp_result r;
         r.status = I.status; r.polish = 0;
         r.iterations = I.k; r.attempts = I.j; r.restarts = I.restarts;
         r.primal_objective = ko.pobj; r.dual_objective = ko.dobj;
         r.primal_residual = ko.pres; r.dual_residual = ko.dres; r.gap = ko.gap;
-        r.rel_kkt = rel5(ko, I.nq0, I.nc0);
+        r.rel_kkt = kkt5_rel(ko, I.nq0, I.nc0);
         r.omega = I.omega; r.eta = I.eta; r.solve_seconds = 0.0;
         P.res[b0 + tid] = r;
       }

@@ -66,43 +66,8 @@ struct GridParams {
   lp_result *res;
 };
 
-struct KktT {
-  double pres, dres, pobj, dobj, gap;
-};
-__device__ __forceinline__ KktT mk(const double *v) {
-  KktT k;
-  k.pres = sqrt(v[0]); k.dres = sqrt(v[1]); k.pobj = v[2]; k.dobj = v[3]; k.gap = fabs(v[2] - v[3]);
-  return k;
-}
-__device__ __forceinline__ bool pass(const KktT &k, double nq, double nc, double ea, double er) {
-  return k.pres <= ea + er * nq && k.dres <= ea + er * nc && k.gap <= ea + er * (fabs(k.pobj) + fabs(k.dobj));
-}
-__device__ __forceinline__ double relk(const KktT &k, double nq, double nc) {
-  return fmax(k.pres / (1.0 + nq), fmax(k.dres / (1.0 + nc), k.gap / (1.0 + fabs(k.pobj) + fabs(k.dobj))));
-}
 
 // KKT contributions of one row / one column (contract step 5), original or scaled space.
-__device__ __forceinline__ void kkt_row(double *v, bool orig, int64_t i, int64_t m1, double dr, double ys, double Kxs,
-                                        double q0, double qs) {
-  const double Kx = orig ? Kxs / dr : Kxs, q = orig ? q0 : qs, y = orig ? dr * ys : ys;
-  double r = q - Kx;
-  if (i < m1) r = fmax(r, 0.0);
-  v[0] += r * r;
-  v[3] += q * y;
-}
-__device__ __forceinline__ void kkt_col(double *v, bool orig, double dc, double xs, double KTys, double c0, double cs,
-                                        double l0, double ls, double u0, double us) {
-  const double x = orig ? dc * xs : xs, KTy = orig ? KTys / dc : KTys;
-  const double c = orig ? c0 : cs, l = orig ? l0 : ls, u = orig ? u0 : us;
-  const double lam = c - KTy, lp = fmax(lam, 0.0), lm = fmax(-lam, 0.0);
-  double d = 0.0;
-  if (l == -INFINITY) d += lp;
-  if (u == INFINITY) d += lm;
-  v[1] += d * d;
-  v[2] += c * x;
-  if (l > -INFINITY) v[3] += l * lp;
-  if (u < INFINITY) v[3] -= u * lm;
-}
 
 #ifdef MPAX_TRACE
 // Phase timers (trace build only, MPAX_TRACE_BUILD=1): CTA 0 / the last CTA, thread 0.
@@ -334,14 +299,15 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   const double nc0 = sqrt(tot4[2]), nq0 = sqrt(tot4[3]);
   double omega = 1.0;
   if (sqrt(tot4[0]) > 1e-10 && sqrt(tot4[1]) > 1e-10) omega = sqrt(tot4[0]) / sqrt(tot4[1]);
+  double inv_omega = 1.0 / omega;  // every x / omega is x * omega^-1 (reading 32)
   const bool cstep = P.const_step != 0;  // constant step rule (reading 34)
   double eta = initial_eta(P.kmax, P.sigma, cstep);
   // r2HPDHG reflection z <- a((1 + rho) w - rho z) + b z0 (rho = 1: 2 PDHG(z) - z; reading 38)
   const double rf1 = 1.0 + P.rho, rf0 = P.rho;
   // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
-  auto tpass = [&](const KktT &k, double nq, double nc) {
+  auto tpass = [&](const Kkt5 &k, double nq, double nc) {
     return P.polish_mode ? polish_pass(P.polish_mode, k.pres, k.dres, nq, nc, P.eps_fp)
-                         : pass(k, nq, nc, P.eps_abs, P.eps_rel);
+                         : kkt5_pass(k, nq, nc, P.eps_abs, P.eps_rel);
   };
   {
     // K~x0, K~'y0; anchors / restart point; KKT_omega(z0) partials (scaled space)
@@ -354,7 +320,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         Kx[i] = s; Kxa[i] = s;
         const double yv = y[i];
         ya[i] = yv; yr[i] = yv;
-        kkt_row(v, false, i, m1, 1.0, yv, s, 0.0, qs[i]);
+        kkt_row_acc(v, false, i < m1, 1.0, yv, s, 0.0, qs[i]);
       }
     }
     for (int it = 0; it < col_iters; ++it) {
@@ -365,7 +331,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         KTy[j] = s; KTya[j] = s;
         const double xv = x[j];
         xa[j] = xv; xr[j] = xv;
-        kkt_col(v, false, 1.0, xv, s, 0.0, cs[j], 0.0, P.ls[j], 0.0, P.us[j]);
+        kkt_col_acc(v, false, 1.0, xv, s, 0.0, cs[j], 0.0, P.ls[j], 0.0, P.us[j]);
       }
     }
     block_partials<4>(v, next_part(), s_red);
@@ -377,8 +343,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     double t[4];
     grid_totals<4>(t, cur_part(), s_tot);
     if (!r2) {
-      const KktT ks = mk(t);
-      ref = sqrt(omega * ks.pres * ks.pres + ks.dres * ks.dres / omega + ks.gap * ks.gap);
+      const Kkt5 ks = kkt5(t);
+      ref = kkt_omega(ks, omega, inv_omega);
     }
   }
 
@@ -410,7 +376,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   while (!done) {
     TR(if (tr_on) tr_t0 = tnow());
     // ================= phase A: [commit n-side] + primal step =================
-    const double tau = eta / omega, sigma = eta * omega;
+    const double tau = eta * inv_omega, sigma = eta * omega;
     double v3[3] = {0.0, 0.0, 0.0};
     if (pending) {
       // one column j of phase A; returns its ||dx||^2 term
@@ -583,7 +549,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     TR(if (tr_on) { tr_t0 = tnow(); tr_bw += tr_t0 - tr_t1; ++tr_n; });
     ++jatt;
     const double I = t3[2];
-    const double M = omega * t3[0] + t3[1] / omega;
+    const double M = omega * t3[0] + t3[1] * inv_omega;
     const double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : INFINITY;
     const bool acc = cstep || (eta <= eb);
     const double eta_used = eta;
@@ -633,7 +599,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
             x[j] = ha * (rf1 * xp[j] - rf0 * x[j]) + hb * xa[j];
             KTy[j] = ha * (rf1 * s - rf0 * KTy[j]) + hb * KTya[j];
             const double dc = P.Dc[j];
-            kkt_col(v, true, dc, xp[j], s, P.c0[j], cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+            kkt_col_acc(v, true, dc, xp[j], s, P.c0[j], cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
             const double d = xp[j] - xr[j];
             v[4] += d * d;
             cert_col(acc, dc, x[j], xa[j], KTy[j], KTya[j], P.c0[j], P.l0[j], P.u0[j]);
@@ -647,7 +613,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           const double ypi = yp[i], kxp = Kxp[i];
           y[i] = ha * (rf1 * ypi - rf0 * y[i]) + hb * ya[i];
           Kx[i] = ha * (rf1 * kxp - rf0 * Kx[i]) + hb * Kxa[i];
-          kkt_row(v, true, i, m1, P.Dr[i], ypi, kxp, P.q0[i], qs[i]);
+          kkt_row_acc(v, true, i < m1, P.Dr[i], ypi, kxp, P.q0[i], qs[i]);
           const double d = ypi - yr[i];
           v[5] += d * d;
           cert_row(acc, i < m1, P.Dr[i], y[i], ya[i], Kx[i], Kxa[i], P.q0[i]);
@@ -678,10 +644,10 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         if (ok && gl == 0) {
           Kxa[i] = s;
           const double dr = P.Dr[i], yai = ya[i], yi = y[i], kxi = Kx[i], q0 = P.q0[i], qsi = qs[i];
-          kkt_row(v + 0, true, i, m1, dr, yai, s, q0, qsi);
-          kkt_row(v + 4, true, i, m1, dr, yi, kxi, q0, qsi);
-          kkt_row(v + 8, false, i, m1, dr, yai, s, q0, qsi);
-          kkt_row(v + 12, false, i, m1, dr, yi, kxi, q0, qsi);
+          kkt_row_acc(v + 0, true, i < m1, dr, yai, s, q0, qsi);
+          kkt_row_acc(v + 4, true, i < m1, dr, yi, kxi, q0, qsi);
+          kkt_row_acc(v + 8, false, i < m1, dr, yai, s, q0, qsi);
+          kkt_row_acc(v + 12, false, i < m1, dr, yi, kxi, q0, qsi);
           const double da = yai - yr[i], dcur = yi - yr[i];
           v[17] += da * da;
           v[19] += dcur * dcur;
@@ -696,10 +662,10 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           KTya[j] = s;
           const double dc = P.Dc[j], xaj = xa[j], xj = x[j], ktj = KTy[j];
           const double c0 = P.c0[j], csj = cs[j], l0 = P.l0[j], lsj = P.ls[j], u0 = P.u0[j], usj = P.us[j];
-          kkt_col(v + 0, true, dc, xaj, s, c0, csj, l0, lsj, u0, usj);
-          kkt_col(v + 4, true, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
-          kkt_col(v + 8, false, dc, xaj, s, c0, csj, l0, lsj, u0, usj);
-          kkt_col(v + 12, false, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+          kkt_col_acc(v + 0, true, dc, xaj, s, c0, csj, l0, lsj, u0, usj);
+          kkt_col_acc(v + 4, true, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+          kkt_col_acc(v + 8, false, dc, xaj, s, c0, csj, l0, lsj, u0, usj);
+          kkt_col_acc(v + 12, false, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
           const double da = xaj - xr[j], dcur = xj - xr[j];
           v[16] += da * da;
           v[18] += dcur * dcur;
@@ -711,7 +677,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       grid.sync();
       double t[kNP];
       grid_totals<kNP, (3u << 24)>(t, cur_part(), s_tot);
-      const KktT ka = mk(t + 0), kc = mk(t + 4);
+      const Kkt5 ka = kkt5(t + 0), kc = kkt5(t + 4);
       if (blockIdx.x == 0 && threadIdx.x == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
         verbose_line(0, k, kc.pobj, kc.dobj, kc.pres, kc.dres, kc.gap, omega, eta);
       if (tpass(ka, nq0, nc0)) { status = LP_OPTIMAL; ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; break; }
@@ -719,19 +685,19 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       if (certify(t + 20, xp, yp, KTyp)) break;
       if (k == P.iter_limit) {
         status = LP_ITERATION_LIMIT;
-        if (relk(ka, nq0, nc0) < relk(kc, nq0, nc0)) { ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; }
+        if (kkt5_rel(ka, nq0, nc0) < kkt5_rel(kc, nq0, nc0)) { ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; }
         else { ox = x; oy = y; oKx = Kx; oKTy = KTy; }
         break;
       }
-      const KktT sa = mk(t + 8), sc = mk(t + 12);
-      const double e_a = sqrt(omega * sa.pres * sa.pres + sa.dres * sa.dres / omega + sa.gap * sa.gap);
-      const double e_c = sqrt(omega * sc.pres * sc.pres + sc.dres * sc.dres / omega + sc.gap * sc.gap);
-      if (e_a < e_c) { cx = xa; cy = ya; cKx = Kxa; cKTy = KTya; metric = e_a; dx2 = t[16]; dy2 = t[17]; }
+      const Kkt5 sa = kkt5(t + 8), sc = kkt5(t + 12);
+      const double e_a = kkt_omega(sa, omega, inv_omega);
+      const double e_c = kkt_omega(sc, omega, inv_omega);
+      if (restart_to_average(e_a, e_c)) { cx = xa; cy = ya; cKx = Kxa; cKTy = KTya; metric = e_a; dx2 = t[16]; dy2 = t[17]; }
       else { cx = x; cy = y; cKx = Kx; cKTy = KTy; metric = e_c; dx2 = t[18]; dy2 = t[19]; }
     } else {
       double t[12];
       grid_totals<12, (3u << 10)>(t, cur_part(), s_tot);
-      const KktT kw = mk(t);
+      const Kkt5 kw = kkt5(t);
       if (blockIdx.x == 0 && threadIdx.x == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
         verbose_line(0, k, kw.pobj, kw.dobj, kw.pres, kw.dres, kw.gap, omega, eta);
       if (tpass(kw, nq0, nc0)) { status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
@@ -739,13 +705,12 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       if (k == P.iter_limit) { status = LP_ITERATION_LIMIT; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
       cx = xp; cy = yp; cKx = Kxp; cKTy = KTyp; metric = rP; dx2 = t[4]; dy2 = t[5];
     }
-    const bool restart = ((double)k_in >= 0.36 * (double)k) || (metric <= 0.2 * ref) ||
-                         (metric <= 0.8 * ref && metric > last);
+    const bool restart = restart_due(k_in, k, metric, ref, last);
     last = metric;
     if (restart) {
       ++restarts;
-      const double dxn = sqrt(dx2), dyn = sqrt(dy2);
-      if (dxn > 1e-10 && dyn > 1e-10) omega = sqrt(omega * (dyn / dxn));
+      omega = primal_weight(omega, sqrt(dx2), sqrt(dy2));
+      inv_omega = 1.0 / omega;
       for (int j = gtid; j < n; j += gthreads) {
         const double xv = cx[j], kt = cKTy[j];
         x[j] = xv; xr[j] = xv; xa[j] = xv; KTy[j] = kt; KTya[j] = kt;
@@ -770,7 +735,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j = gtid; j < n; j += gthreads) {
       const double dc = P.Dc[j], xs = ox[j], kt = oKTy[j];
-      kkt_col(v, true, dc, xs, kt, P.c0[j], cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+      kkt_col_acc(v, true, dc, xs, kt, P.c0[j], cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
       if (bx) {  // infeasible: the unit rays (reading 35)
         P.X[j] = dc * (xs - bx[j]) / ray_nx;
         P.L[j] = -((kt - bKTy[j]) / dc) / ray_ny;
@@ -781,7 +746,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     }
     for (int i = gtid; i < m; i += gthreads) {
       const double dr = P.Dr[i];
-      kkt_row(v, true, i, m1, dr, oy[i], oKx[i], P.q0[i], qs[i]);
+      kkt_row_acc(v, true, i < m1, dr, oy[i], oKx[i], P.q0[i], qs[i]);
       P.Y[i] = bx ? dr * (oy[i] - by[i]) / ray_ny : dr * oy[i];
     }
     block_partials<4>(v, next_part(), s_red);
@@ -790,13 +755,13 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   double t[4];
   grid_totals<4>(t, cur_part(), s_tot);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const KktT ko = mk(t);
+    const Kkt5 ko = kkt5(t);
     lp_result r;
     r.status = status; r.polish = 0;
     r.iterations = k; r.attempts = jatt; r.restarts = restarts;
     r.primal_objective = ko.pobj; r.dual_objective = ko.dobj;
     r.primal_residual = ko.pres; r.dual_residual = ko.dres; r.gap = ko.gap;
-    r.rel_kkt = relk(ko, nq0, nc0);
+    r.rel_kkt = kkt5_rel(ko, nq0, nc0);
     r.omega = omega; r.eta = eta; r.solve_seconds = 0.0;
     *P.res = r;
   }

@@ -178,50 +178,11 @@ __device__ __forceinline__ void spmv_rows(int rows, int G, const int32_t *rp, co
   }
 }
 
-struct Kkt {
-  double pres, dres, pobj, dobj, gap;
-};
 
-__device__ __forceinline__ Kkt make_kkt(const double *v) {
-  Kkt k;
-  k.pres = sqrt(v[0]);
-  k.dres = sqrt(v[1]);
-  k.pobj = v[2];
-  k.dobj = v[3];
-  k.gap = fabs(v[2] - v[3]);
-  return k;
-}
 
-__device__ __forceinline__ bool kkt_pass(const Kkt &k, double nq, double nc, double ea, double er) {
-  return k.pres <= ea + er * nq && k.dres <= ea + er * nc && k.gap <= ea + er * (fabs(k.pobj) + fabs(k.dobj));
-}
 
-__device__ __forceinline__ double rel_kkt(const Kkt &k, double nq, double nc) {
-  return fmax(k.pres / (1.0 + nq), fmax(k.dres / (1.0 + nc), k.gap / (1.0 + fabs(k.pobj) + fabs(k.dobj))));
-}
 
 // KKT contributions of one row / one column (contract step 5); orig: unscale with Dr, Dc.
-__device__ __forceinline__ void kkt_row(double *v, bool orig, int i, int m1, double dr, double ys, double Kxs,
-                                        double q0, double qs) {
-  const double Kx = orig ? Kxs / dr : Kxs, q = orig ? q0 : qs, y = orig ? dr * ys : ys;
-  double r = q - Kx;
-  if (i < m1) r = fmax(r, 0.0);
-  v[0] += r * r;
-  v[3] += q * y;
-}
-__device__ __forceinline__ void kkt_col(double *v, bool orig, double dc, double xs, double KTys, double c0, double cs,
-                                        double l0, double ls, double u0, double us) {
-  const double x = orig ? dc * xs : xs, KTy = orig ? KTys / dc : KTys;
-  const double c = orig ? c0 : cs, l = orig ? l0 : ls, u = orig ? u0 : us;
-  const double lam = c - KTy, lp = fmax(lam, 0.0), lm = fmax(-lam, 0.0);
-  double d = 0.0;
-  if (l == -INFINITY) d += lp;
-  if (u == INFINITY) d += lm;
-  v[1] += d * d;
-  v[2] += c * x;
-  if (l > -INFINITY) v[3] += l * lp;
-  if (u < INFINITY) v[3] -= u * lm;
-}
 
 template <int NW, bool SMEM>
 __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
@@ -259,9 +220,9 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
   // r2HPDHG reflection z <- a((1 + rho) w - rho z) + b z0 (rho = 1: 2 PDHG(z) - z; reading 38)
   const double rf1 = 1.0 + P.rho, rf0 = P.rho;
   // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
-  auto tpass = [&](const Kkt &k, double nq, double nc) {
+  auto tpass = [&](const Kkt5 &k, double nq, double nc) {
     return P.polish_mode ? polish_pass(P.polish_mode, k.pres, k.dres, nq, nc, P.eps_fp)
-                         : kkt_pass(k, nq, nc, P.eps_abs, P.eps_rel);
+                         : kkt5_pass(k, nq, nc, P.eps_abs, P.eps_rel);
   };
   int rbuf = 0;
   auto redbuf = [&]() { rbuf ^= 1; return rbuf ? red1 : red0; };
@@ -314,6 +275,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
       const double nc = sqrt(v4[0]), nq = sqrt(v4[1]);
       if (nc > 1e-10 && nq > 1e-10) omega = nc / nq;
     }
+    double inv_omega = 1.0 / omega;  // every x / omega is x * omega^-1 (reading 32)
     double eta = eta0;
     bsync<NW>();
     double ref = 0.0;
@@ -323,18 +285,18 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
         Kx[i] = s; Kxa[i] = s;
         const double yv = y[i];
         yr[i] = yv; ya[i] = yv;
-        kkt_row(v, false, i, m1, 1.0, yv, s, 0.0, qs[i]);
+        kkt_row_acc(v, false, i < m1, 1.0, yv, s, 0.0, qs[i]);
       });
       spmv_rows<NW>(n, Gt, trp, tci, tkv, y, [&](int j, double s) {
         KTy[j] = s; KTya[j] = s;
         const double xv = x[j];
         xr[j] = xv; xa[j] = xv;
-        kkt_col(v, false, 1.0, xv, s, 0.0, cs[j], 0.0, ls[j], 0.0, us[j]);
+        kkt_col_acc(v, false, 1.0, xv, s, 0.0, cs[j], 0.0, ls[j], 0.0, us[j]);
       });
       breduce<NW, 4>(v, redbuf());
       if (!r2) {  // raPDHG reference metric KKT_omega(z0)
-        const Kkt ks = make_kkt(v);
-        ref = sqrt(omega * ks.pres * ks.pres + ks.dres * ks.dres / omega + ks.gap * ks.gap);
+        const Kkt5 ks = kkt5(v);
+        ref = kkt_omega(ks, omega, inv_omega);
       }
     }
     int64_t k = 0, jatt = 0, k_in = 0, restarts = 0;
@@ -364,7 +326,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
 
     for (;;) {
       // ================= phase A: [commit n-side] + primal step =================
-      const double tau = eta / omega, sigma = eta * omega;
+      const double tau = eta * inv_omega, sigma = eta * omega;
       double f1, f2;
       step_factors(P.tab, jatt + 1, f1, f2);  // prefetch this attempt's growth factors
       double v3[3] = {0.0, 0.0, 0.0};
@@ -434,7 +396,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
       breduce<NW, 3>(v3, redbuf());
       ++jatt;
       const double I = v3[2];
-      const double M = omega * v3[0] + v3[1] / omega;
+      const double M = omega * v3[0] + v3[1] * inv_omega;
       const double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : INFINITY;
       const bool acc = cstep || (eta <= eb);
       const double eta_used = eta;
@@ -473,7 +435,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
             const double xpj = xp[j];
             x[j] = ha * (rf1 * xpj - rf0 * x[j]) + hb * xa[j];
             KTy[j] = ha * (rf1 * s - rf0 * KTy[j]) + hb * KTya[j];
-            kkt_col(v, true, Dc[j], xpj, s, c0[j], cs[j], P.l0[j], ls[j], P.u0[j], us[j]);
+            kkt_col_acc(v, true, Dc[j], xpj, s, c0[j], cs[j], P.l0[j], ls[j], P.u0[j], us[j]);
             const double d = xpj - xr[j];
             v[4] += d * d;
           }
@@ -485,7 +447,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
             const double ypi = yp[i], kxp = Kxp[i];
             y[i] = ha * (rf1 * ypi - rf0 * y[i]) + hb * ya[i];
             Kx[i] = ha * (rf1 * kxp - rf0 * Kx[i]) + hb * Kxa[i];
-            kkt_row(v, true, i, m1, Dr[i], ypi, kxp, q0[i], qs[i]);
+            kkt_row_acc(v, true, i < m1, Dr[i], ypi, kxp, q0[i], qs[i]);
             const double d = ypi - yr[i];
             v[5] += d * d;
           }
@@ -498,7 +460,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
           bsync<NW>();
         } else {
           breduce<NW, 6>(v, redbuf());
-          const Kkt kw = make_kkt(v);
+          const Kkt5 kw = kkt5(v);
           if (tid == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
             verbose_line(b, k, kw.pobj, kw.dobj, kw.pres, kw.dres, kw.gap, omega, eta);
           if (tpass(kw, nq0, nc0)) {
@@ -517,10 +479,10 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
         spmv_rows<NW>(m, G, rp, ci, kv, xa, [&](int i, double s) {
           Kxa[i] = s;
           const double dr = Dr[i], yai = ya[i], yi = y[i], kxi = Kx[i], q0i = q0[i], qsi = qs[i];
-          kkt_row(v + 0, true, i, m1, dr, yai, s, q0i, qsi);
-          kkt_row(v + 4, true, i, m1, dr, yi, kxi, q0i, qsi);
-          kkt_row(v + 8, false, i, m1, dr, yai, s, q0i, qsi);
-          kkt_row(v + 12, false, i, m1, dr, yi, kxi, q0i, qsi);
+          kkt_row_acc(v + 0, true, i < m1, dr, yai, s, q0i, qsi);
+          kkt_row_acc(v + 4, true, i < m1, dr, yi, kxi, q0i, qsi);
+          kkt_row_acc(v + 8, false, i < m1, dr, yai, s, q0i, qsi);
+          kkt_row_acc(v + 12, false, i < m1, dr, yi, kxi, q0i, qsi);
           const double da = yai - yr[i], dcur = yi - yr[i];
           v[17] += da * da;
           v[19] += dcur * dcur;
@@ -529,16 +491,16 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
           KTya[j] = s;
           const double dc = Dc[j], xaj = xa[j], xj = x[j], ktj = KTy[j];
           const double c0j = c0[j], csj = cs[j], l0j = P.l0[j], lsj = ls[j], u0j = P.u0[j], usj = us[j];
-          kkt_col(v + 0, true, dc, xaj, s, c0j, csj, l0j, lsj, u0j, usj);
-          kkt_col(v + 4, true, dc, xj, ktj, c0j, csj, l0j, lsj, u0j, usj);
-          kkt_col(v + 8, false, dc, xaj, s, c0j, csj, l0j, lsj, u0j, usj);
-          kkt_col(v + 12, false, dc, xj, ktj, c0j, csj, l0j, lsj, u0j, usj);
+          kkt_col_acc(v + 0, true, dc, xaj, s, c0j, csj, l0j, lsj, u0j, usj);
+          kkt_col_acc(v + 4, true, dc, xj, ktj, c0j, csj, l0j, lsj, u0j, usj);
+          kkt_col_acc(v + 8, false, dc, xaj, s, c0j, csj, l0j, lsj, u0j, usj);
+          kkt_col_acc(v + 12, false, dc, xj, ktj, c0j, csj, l0j, lsj, u0j, usj);
           const double da = xaj - xr[j], dcur = xj - xr[j];
           v[16] += da * da;
           v[18] += dcur * dcur;
         });
         breduce<NW, kRedMax>(v, redbuf());
-        const Kkt ka = make_kkt(v + 0), kc = make_kkt(v + 4);
+        const Kkt5 ka = kkt5(v + 0), kc = kkt5(v + 4);
         if (tid == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
           verbose_line(b, k, kc.pobj, kc.dobj, kc.pres, kc.dres, kc.gap, omega, eta);
         if (tpass(ka, nq0, nc0)) {
@@ -550,24 +512,23 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
         if (infeasible(xp, yp, Kxp, KTyp)) break;     // rays from the last step (pre-commit point)
         if (k == P.iter_limit) {
           status = LP_ITERATION_LIMIT;
-          if (rel_kkt(ka, nq0, nc0) < rel_kkt(kc, nq0, nc0)) { ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; }
+          if (kkt5_rel(ka, nq0, nc0) < kkt5_rel(kc, nq0, nc0)) { ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; }
           else { ox = x; oy = y; oKx = Kx; oKTy = KTy; }
           break;
         }
-        const Kkt sa = make_kkt(v + 8), sc = make_kkt(v + 12);
-        const double e_a = sqrt(omega * sa.pres * sa.pres + sa.dres * sa.dres / omega + sa.gap * sa.gap);
-        const double e_c = sqrt(omega * sc.pres * sc.pres + sc.dres * sc.dres / omega + sc.gap * sc.gap);
-        if (e_a < e_c) { cx = xa; cy = ya; cKx = Kxa; cKTy = KTya; metric = e_a; dx2 = v[16]; dy2 = v[17]; }
+        const Kkt5 sa = kkt5(v + 8), sc = kkt5(v + 12);
+        const double e_a = kkt_omega(sa, omega, inv_omega);
+        const double e_c = kkt_omega(sc, omega, inv_omega);
+        if (restart_to_average(e_a, e_c)) { cx = xa; cy = ya; cKx = Kxa; cKTy = KTya; metric = e_a; dx2 = v[16]; dy2 = v[17]; }
         else { cx = x; cy = y; cKx = Kx; cKTy = KTy; metric = e_c; dx2 = v[18]; dy2 = v[19]; }
       }
       // restart test (contract step 5): artificial / sufficient / necessary + stall
-      const bool restart = ((double)k_in >= 0.36 * (double)k) || (metric <= 0.2 * ref) ||
-                           (metric <= 0.8 * ref && metric > last);
+      const bool restart = restart_due(k_in, k, metric, ref, last);
       last = metric;
       if (restart) {
         ++restarts;
-        const double dxn = sqrt(dx2), dyn = sqrt(dy2);
-        if (dxn > 1e-10 && dyn > 1e-10) omega = sqrt(omega * (dyn / dxn));
+        omega = primal_weight(omega, sqrt(dx2), sqrt(dy2));
+        inv_omega = 1.0 / omega;
         for (int j = tid; j < n; j += T) {
           const double xv = cx[j], kt = cKTy[j];
           x[j] = xv; xr[j] = xv; xa[j] = xv;
@@ -590,7 +551,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
       double *X = P.X + b * (int64_t)n, *L = P.L + b * (int64_t)n, *Y = P.Y + b * (int64_t)m;
       for (int j = tid; j < n; j += T) {
         const double dc = Dc[j], xs = ox[j], kt = oKTy[j];
-        kkt_col(v, true, dc, xs, kt, c0[j], cs[j], P.l0[j], ls[j], P.u0[j], us[j]);
+        kkt_col_acc(v, true, dc, xs, kt, c0[j], cs[j], P.l0[j], ls[j], P.u0[j], us[j]);
         if (bx) {  // infeasible: the unit rays d_x, d_y and -K'd_y (reading 35)
           X[j] = dc * (xs - bx[j]) / ray_nx;
           L[j] = -((kt - bKTy[j]) / dc) / ray_ny;
@@ -601,12 +562,12 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
       }
       for (int i = tid; i < m; i += T) {
         const double dr = Dr[i];
-        kkt_row(v, true, i, m1, dr, oy[i], oKx[i], q0[i], qs[i]);
+        kkt_row_acc(v, true, i < m1, dr, oy[i], oKx[i], q0[i], qs[i]);
         Y[i] = bx ? dr * (oy[i] - by[i]) / ray_ny : dr * oy[i];
       }
       breduce<NW, 4>(v, redbuf());
       if (tid == 0) {
-        const Kkt ko = make_kkt(v);
+        const Kkt5 ko = kkt5(v);
         lp_result r;
         r.status = status;
         r.polish = 0;
@@ -618,7 +579,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
         r.primal_residual = ko.pres;
         r.dual_residual = ko.dres;
         r.gap = ko.gap;
-        r.rel_kkt = rel_kkt(ko, nq0, nc0);
+        r.rel_kkt = kkt5_rel(ko, nq0, nc0);
         r.omega = omega;
         r.eta = eta;
         r.solve_seconds = 0.0;

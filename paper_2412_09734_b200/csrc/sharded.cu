@@ -33,7 +33,7 @@ constexpr int kB = 256;  // threads per block
 constexpr int kV = 24;   // partial-sum slots
 
 struct ShState {
-  double omega, eta, W, ref, last, theta, ha, hb, rP, M, Iv, eta_used, metric, nc0, nq0, eta0;
+  double omega, inv_omega, eta, W, ref, last, theta, ha, hb, rP, M, Iv, eta_used, metric, nc0, nq0, eta0;
   long long k, j, k_in, restarts;
   int rejects, status, pending, halt, restart, outsel, csel, r2, cstep, rays;
   double colsum[kV];  // totals over this GPU's columns (replicated data: identical on every GPU)
@@ -54,42 +54,7 @@ struct Vecs {
   const double *c0, *q0, *X0, *Y0;
 };
 
-__device__ __forceinline__ void kkt_row(double *v, bool orig, bool ge, double dr, double ys, double Kxs, double q0,
-                                        double qs) {
-  const double Kx = orig ? Kxs / dr : Kxs, q = orig ? q0 : qs, y = orig ? dr * ys : ys;
-  double r = q - Kx;
-  if (ge) r = fmax(r, 0.0);
-  v[0] += r * r;
-  v[3] += q * y;
-}
-__device__ __forceinline__ void kkt_col(double *v, bool orig, double dc, double xs, double KTys, double c0, double cs,
-                                        double l0, double ls, double u0, double us) {
-  const double x = orig ? dc * xs : xs, KTy = orig ? KTys / dc : KTys;
-  const double c = orig ? c0 : cs, l = orig ? l0 : ls, u = orig ? u0 : us;
-  const double lam = c - KTy, lp = fmax(lam, 0.0), lm = fmax(-lam, 0.0);
-  double d = 0.0;
-  if (l == -INFINITY) d += lp;
-  if (u == INFINITY) d += lm;
-  v[1] += d * d;
-  v[2] += c * x;
-  if (l > -INFINITY) v[3] += l * lp;
-  if (u < INFINITY) v[3] -= u * lm;
-}
 
-struct K5 {
-  double pres, dres, pobj, dobj, gap;
-};
-__device__ __forceinline__ K5 mk5(const double *v) {
-  K5 k;
-  k.pres = sqrt(v[0]); k.dres = sqrt(v[1]); k.pobj = v[2]; k.dobj = v[3]; k.gap = fabs(v[2] - v[3]);
-  return k;
-}
-__device__ __forceinline__ bool pass5(const K5 &k, double nq, double nc, double ea, double er) {
-  return k.pres <= ea + er * nq && k.dres <= ea + er * nc && k.gap <= ea + er * (fabs(k.pobj) + fabs(k.dobj));
-}
-__device__ __forceinline__ double rel5(const K5 &k, double nq, double nc) {
-  return fmax(k.pres / (1.0 + nq), fmax(k.dres / (1.0 + nc), k.gap / (1.0 + fabs(k.pobj) + fabs(k.dobj))));
-}
 
 // row r of a CSR matrix times x (all lanes of the row's group get the sum): G == 1 is the
 // warp-tile CSR-stream of common.cuh (every lane of the warp calls it, r = tile row + lane;
@@ -206,7 +171,7 @@ enum { ROWS_STEP = 0, ROWS_COMMIT_ONLY = 1, ROWS_AVG = 2, ROWS_INIT = 3, ROWS_IN
 __global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, const Vecs V) {
   if (st->halt && mode != COLS_OUT) return;
   const bool r2 = st->r2, pend = st->pending;
-  const double tau = st->eta / st->omega, theta = st->theta, ha = st->ha, hb = st->hb;
+  const double tau = st->eta * st->inv_omega, theta = st->theta, ha = st->ha, hb = st->hb;
   const double rf1 = 1.0 + st->rho, rf0 = st->rho;  // reflection (reading 38)
   double v[20] = {};
   const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x, st_ = (int64_t)gridDim.x * kB;
@@ -239,7 +204,7 @@ __global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, con
         V.KTyp[j] = kty;
         if (pend) {
           const double xpv = V.xp[j];
-          kkt_col(v, true, dc, xpv, kty, V.c0[j], V.cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+          kkt_col_acc(v, true, dc, xpv, kty, V.c0[j], V.cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
           const double d = xpv - V.xr[j];
           v[4] += d * d;
         }
@@ -249,10 +214,10 @@ __global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, con
       V.KTya[j] = kta;
       const double xaj = V.xa[j], xj = V.x[j], ktj = V.KTy[j], c0 = V.c0[j], csj = V.cs[j], l0 = P.l0[j],
                    lsj = P.ls[j], u0 = P.u0[j], usj = P.us[j];
-      kkt_col(v + 0, true, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
-      kkt_col(v + 4, true, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
-      kkt_col(v + 8, false, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
-      kkt_col(v + 12, false, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+      kkt_col_acc(v + 0, true, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
+      kkt_col_acc(v + 4, true, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
+      kkt_col_acc(v + 8, false, dc, xaj, kta, c0, csj, l0, lsj, u0, usj);
+      kkt_col_acc(v + 12, false, dc, xj, ktj, c0, csj, l0, lsj, u0, usj);
       const double da = xaj - V.xr[j], dcur = xj - V.xr[j];
       v[16] += da * da;
       v[18] += dcur * dcur;
@@ -272,12 +237,12 @@ __global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, con
     } else if (mode == COLS_INIT2) {
       const double kty = V.red[j];
       V.KTy[j] = kty; V.KTya[j] = kty; V.KTyp[j] = kty;
-      kkt_col(v, false, dc, V.x[j], kty, 0.0, V.cs[j], 0.0, P.ls[j], 0.0, P.us[j]);
+      kkt_col_acc(v, false, dc, V.x[j], kty, 0.0, V.cs[j], 0.0, P.ls[j], 0.0, P.us[j]);
     } else {  // COLS_OUT
       const int sel = st->outsel;
       const double xs = sel ? (r2 ? V.xp[j] : V.xa[j]) : V.x[j];
       const double kt = sel ? (r2 ? V.KTyp[j] : V.KTya[j]) : V.KTy[j];
-      kkt_col(v, true, dc, xs, kt, V.c0[j], V.cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
+      kkt_col_acc(v, true, dc, xs, kt, V.c0[j], V.cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
       if (st->rays) {  // infeasible: unit rays against the base (reading 35)
         const double xb = r2 ? V.xa[j] : V.xp[j], ktb = r2 ? V.KTya[j] : V.KTyp[j];
         V.red[j] = dc * (xs - xb) / st->ray_nx;
@@ -357,7 +322,7 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
         v[1] += d * (s - kxv);
       } else if (r2 && pend) {
         const double ypv = V.yp[i], kxp = V.Kxp[i];
-        kkt_row(v, true, ge, dr, ypv, kxp, V.q0[i], V.qs[i]);
+        kkt_row_acc(v, true, ge, dr, ypv, kxp, V.q0[i], V.qs[i]);
         const double d = ypv - V.yr[i];
         v[5] += d * d;
       } else if (!r2 && pend) {
@@ -372,10 +337,10 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
     } else if (mode == ROWS_AVG) {
       V.Kxa[i] = s;
       const double yai = V.ya[i], yi = V.y[i], kxi = V.Kx[i], q0 = V.q0[i], qsi = V.qs[i];
-      kkt_row(v + 0, true, ge, dr, yai, s, q0, qsi);
-      kkt_row(v + 4, true, ge, dr, yi, kxi, q0, qsi);
-      kkt_row(v + 8, false, ge, dr, yai, s, q0, qsi);
-      kkt_row(v + 12, false, ge, dr, yi, kxi, q0, qsi);
+      kkt_row_acc(v + 0, true, ge, dr, yai, s, q0, qsi);
+      kkt_row_acc(v + 4, true, ge, dr, yi, kxi, q0, qsi);
+      kkt_row_acc(v + 8, false, ge, dr, yai, s, q0, qsi);
+      kkt_row_acc(v + 12, false, ge, dr, yi, kxi, q0, qsi);
       const double da = yai - V.yr[i], dcur = yi - V.yr[i];
       v[17] += da * da;
       v[19] += dcur * dcur;
@@ -389,12 +354,12 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
       V.y[i] = yv; V.ya[i] = yv; V.yr[i] = yv; V.yp[i] = yv;
     } else if (mode == ROWS_INIT2) {
       V.Kx[i] = s; V.Kxa[i] = s; V.Kxp[i] = s;
-      kkt_row(v, false, ge, dr, V.y[i], s, 0.0, V.qs[i]);
+      kkt_row_acc(v, false, ge, dr, V.y[i], s, 0.0, V.qs[i]);
     } else {  // ROWS_OUT
       const int sel = st->outsel;
       const double ys = sel ? (r2 ? V.yp[i] : V.ya[i]) : V.y[i];
       const double kx = sel ? (r2 ? V.Kxp[i] : V.Kxa[i]) : V.Kx[i];
-      kkt_row(v, true, ge, dr, ys, kx, V.q0[i], V.qs[i]);
+      kkt_row_acc(v, true, ge, dr, ys, kx, V.q0[i], V.qs[i]);
       if (st->rays) V.Kxp[i] = dr * (ys - (r2 ? V.ya[i] : V.yp[i])) / st->ray_ny;
       else V.Kxp[i] = dr * ys;  // unscaled y (output buffer)
     }
@@ -414,12 +379,13 @@ __global__ void k_init_decide(ShState *st, int stage) {
     st->nc0 = sqrt(st->colsum[1]);
     st->nq0 = sqrt(st->rowsum[1]);
     st->omega = (nc > 1e-10 && nq > 1e-10) ? nc / nq : 1.0;
+    st->inv_omega = 1.0 / st->omega;  // every x / omega is x * omega^-1 (reading 32)
     st->eta = st->eta0;
   } else if (!st->r2) {  // raPDHG reference KKT_omega(z0): rows (reduced) + columns
     double t[4];
     for (int k = 0; k < 4; ++k) t[k] = st->rowsum[k] + st->colsum[k];
-    const K5 ks = mk5(t);
-    st->ref = sqrt(st->omega * ks.pres * ks.pres + ks.dres * ks.dres / st->omega + ks.gap * ks.gap);
+    const Kkt5 ks = kkt5(t);
+    st->ref = kkt_omega(ks, st->omega, st->inv_omega);
   }
 }
 
@@ -429,7 +395,7 @@ __global__ void k_decide(ShState *st, const double *tab, int64_t check_freq, int
   double f1 = 0.0, f2 = 0.0;
   if (!st->cstep) step_factors(tab, st->j, f1, f2);
   const double dx2 = st->colsum[0], dy2 = st->rowsum[0], I = st->rowsum[1];
-  const double M = st->omega * dx2 + dy2 / st->omega;
+  const double M = st->omega * dx2 + dy2 * st->inv_omega;
   const double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : INFINITY;
   const bool acc = st->cstep || st->eta <= eb;  // constant step rule: DESIGN.md reading 34
   const double eta_used = st->eta;
@@ -470,8 +436,8 @@ __global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, doub
   double ny = 1.0, nx = 1.0;
   const int cert = cert_decide(ct, eps_pi, eps_di, ny, nx);
   if (st->r2) {
-    const K5 kw = mk5(t);
-    if (pass5(kw, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
+    const Kkt5 kw = kkt5(t);
+    if (kkt5_pass(kw, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
     if (cert) {
       st->status = cert; st->halt = 1; st->outsel = 0; st->rays = 1; st->ray_ny = ny; st->ray_nx = nx;
       return;
@@ -482,34 +448,32 @@ __global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, doub
     st->colsum[22] = t[4];
     st->colsum[23] = t[5];
   } else {
-    const K5 ka = mk5(t + 0), kc = mk5(t + 4);
-    if (pass5(ka, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
-    if (pass5(kc, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 0; return; }
+    const Kkt5 ka = kkt5(t + 0), kc = kkt5(t + 4);
+    if (kkt5_pass(ka, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
+    if (kkt5_pass(kc, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 0; return; }
     if (cert) {
       st->status = cert; st->halt = 1; st->outsel = 0; st->rays = 1; st->ray_ny = ny; st->ray_nx = nx;
       return;
     }
     if (st->k == iter_limit) {
       st->status = LP_ITERATION_LIMIT; st->halt = 1;
-      st->outsel = rel5(ka, nq0, nc0) < rel5(kc, nq0, nc0) ? 1 : 0;
+      st->outsel = kkt5_rel(ka, nq0, nc0) < kkt5_rel(kc, nq0, nc0) ? 1 : 0;
       return;
     }
-    const K5 sa = mk5(t + 8), sc = mk5(t + 12);
-    const double om = st->omega;
-    const double e_a = sqrt(om * sa.pres * sa.pres + sa.dres * sa.dres / om + sa.gap * sa.gap);
-    const double e_c = sqrt(om * sc.pres * sc.pres + sc.dres * sc.dres / om + sc.gap * sc.gap);
-    if (e_a < e_c) { st->csel = 1; st->metric = e_a; st->colsum[22] = t[16]; st->colsum[23] = t[17]; }
+    const Kkt5 sa = kkt5(t + 8), sc = kkt5(t + 12);
+    const double e_a = kkt_omega(sa, st->omega, st->inv_omega);
+    const double e_c = kkt_omega(sc, st->omega, st->inv_omega);
+    if (restart_to_average(e_a, e_c)) { st->csel = 1; st->metric = e_a; st->colsum[22] = t[16]; st->colsum[23] = t[17]; }
     else { st->csel = 0; st->metric = e_c; st->colsum[22] = t[18]; st->colsum[23] = t[19]; }
   }
   const double metric = st->metric;
-  const bool restart = ((double)st->k_in >= 0.36 * (double)st->k) || (metric <= 0.2 * st->ref) ||
-                       (metric <= 0.8 * st->ref && metric > st->last);
+  const bool restart = restart_due(st->k_in, st->k, metric, st->ref, st->last);
   st->last = metric;
   if (restart) {
     st->restart = 1;
     st->restarts += 1;
-    const double dxn = sqrt(st->colsum[22]), dyn = sqrt(st->colsum[23]);
-    if (dxn > 1e-10 && dyn > 1e-10) st->omega = sqrt(st->omega * (dyn / dxn));
+    st->omega = primal_weight(st->omega, sqrt(st->colsum[22]), sqrt(st->colsum[23]));
+    st->inv_omega = 1.0 / st->omega;
     st->k_in = 0;
     if (!st->r2) { st->W = 0.0; st->ref = metric; }
   }
@@ -534,13 +498,13 @@ __global__ void k_restart(const ShState *st, int64_t n, int64_t m, const Vecs V)
 __global__ void k_final(const ShState *st, lp_result *res) {
   double t[4];
   for (int k = 0; k < 4; ++k) t[k] = st->colsum[k] + st->rowsum[k];
-  const K5 ko = mk5(t);
+  const Kkt5 ko = kkt5(t);
   lp_result r;
   r.status = st->status; r.polish = 0;
   r.iterations = st->k; r.attempts = st->j; r.restarts = st->restarts;
   r.primal_objective = ko.pobj; r.dual_objective = ko.dobj;
   r.primal_residual = ko.pres; r.dual_residual = ko.dres; r.gap = ko.gap;
-  r.rel_kkt = rel5(ko, st->nq0, st->nc0);
+  r.rel_kkt = kkt5_rel(ko, st->nq0, st->nc0);
   r.omega = st->omega; r.eta = st->eta; r.solve_seconds = 0.0;
   *res = r;
 }

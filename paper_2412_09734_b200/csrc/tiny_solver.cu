@@ -6,8 +6,8 @@
 // iteration (x, K~'y, x', average / anchor, restart point, c~, l~, u~ and the
 // m-side analogues) lives in registers; only the two vectors that are
 // gathered by the SpMVs (x' and y', and the average at checks) go through
-// shared memory.  Same arithmetic, in the same order, as the generic
-// instance_kernel (instance_solver.cu) and the grid kernel; DESIGN.md §3.
+// shared memory.  The contract's arithmetic (common.cuh helpers) in
+// the oracle's order; sums run in lane / butterfly order (reading 27).
 #include <cstdlib>
 
 #include "common.cuh"
@@ -55,41 +55,6 @@ __device__ __forceinline__ void wmax(double (&v)[V]) {
   }
 }
 
-struct K5 {
-  double pres, dres, pobj, dobj, gap;
-};
-__device__ __forceinline__ K5 mk5(const double *v) {
-  K5 k;
-  k.pres = sqrt(v[0]); k.dres = sqrt(v[1]); k.pobj = v[2]; k.dobj = v[3]; k.gap = fabs(v[2] - v[3]);
-  return k;
-}
-__device__ __forceinline__ bool pass5(const K5 &k, double nq, double nc, double ea, double er) {
-  return k.pres <= ea + er * nq && k.dres <= ea + er * nc && k.gap <= ea + er * (fabs(k.pobj) + fabs(k.dobj));
-}
-__device__ __forceinline__ double rel5(const K5 &k, double nq, double nc) {
-  return fmax(k.pres / (1.0 + nq), fmax(k.dres / (1.0 + nc), k.gap / (1.0 + fabs(k.pobj) + fabs(k.dobj))));
-}
-__device__ __forceinline__ void krow(double *v, bool orig, bool ge, double dr, double ys, double Kxs, double q0,
-                                     double qs) {
-  const double Kx = orig ? Kxs / dr : Kxs, q = orig ? q0 : qs, y = orig ? dr * ys : ys;
-  double r = q - Kx;
-  if (ge) r = fmax(r, 0.0);
-  v[0] += r * r;
-  v[3] += q * y;
-}
-__device__ __forceinline__ void kcol(double *v, bool orig, double dc, double xs, double KTys, double c0, double cs,
-                                     double l0, double ls, double u0, double us) {
-  const double x = orig ? dc * xs : xs, KTy = orig ? KTys / dc : KTys;
-  const double c = orig ? c0 : cs, l = orig ? l0 : ls, u = orig ? u0 : us;
-  const double lam = c - KTy, lp = fmax(lam, 0.0), lm = fmax(-lam, 0.0);
-  double d = 0.0;
-  if (l == -INFINITY) d += lp;
-  if (u == INFINITY) d += lm;
-  v[1] += d * d;
-  v[2] += c * x;
-  if (l > -INFINITY) v[3] += l * lp;
-  if (u < INFINITY) v[3] -= u * lm;
-}
 
 // CS: constant step rule (eta = 0.998 / sigma_max(K~), every attempt accepted; DESIGN.md
 // reading 34) -- the line-search reductions are then needed only where r2HPDHG uses
@@ -140,9 +105,9 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
   // r2HPDHG reflection z <- a((1 + rho) w - rho z) + b z0 (rho = 1: 2 PDHG(z) - z; reading 38)
   const double rf1 = 1.0 + P.rho, rf0 = P.rho;
   // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
-  auto tpass = [&](const K5 &k, double nq, double nc) {
+  auto tpass = [&](const Kkt5 &k, double nq, double nc) {
     return P.polish_mode ? polish_pass(P.polish_mode, k.pres, k.dres, nq, nc, P.eps_fp)
-                         : pass5(k, nq, nc, P.eps_abs, P.eps_rel);
+                         : kkt5_pass(k, nq, nc, P.eps_abs, P.eps_rel);
   };
   __shared__ unsigned long long s_inst;
 
@@ -188,8 +153,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
     double omega = 1.0;
     if (sqrt(v4[0]) > 1e-10 && sqrt(v4[1]) > 1e-10) omega = sqrt(v4[0]) / sqrt(v4[1]);
     double eta = eta0, ref = 0.0;
-    // 1/omega changes only at restarts: x / omega is evaluated as x * (1/omega) on the attempt's
-    // critical path (an algebraically identical evaluation order, SURVEY §8(c) c.2 "Notation")
+    // omega^-1 = 1 / omega, recomputed whenever omega changes; every x / omega of the iteration
+    // is x * omega^-1 (reading 32, the same in the oracle and every kernel)
     double inv_omega = 1.0 / omega;
     {
       double v[4] = {0.0, 0.0, 0.0, 0.0};
@@ -199,7 +164,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
 #pragma unroll
         for (int w = 0; w < W; ++w) s += rval[t][w] * sx[rcol[t][w]];
         Kx[t] = s; Kxa[t] = s; ya[t] = y[t]; yr[t] = y[t];
-        if (rok[t]) krow(v, false, lane + 32 * t < m1, 1.0, y[t], s, 0.0, qs[t]);
+        if (rok[t]) kkt_row_acc(v, false, lane + 32 * t < m1, 1.0, y[t], s, 0.0, qs[t]);
       }
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {
@@ -207,12 +172,12 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
 #pragma unroll
         for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
         KTy[t] = s; KTya[t] = s; xa[t] = x[t]; xr[t] = x[t];
-        if (cok[t]) kcol(v, false, 1.0, x[t], s, 0.0, cs[t], 0.0, lsv[t], 0.0, usv[t]);
+        if (cok[t]) kkt_col_acc(v, false, 1.0, x[t], s, 0.0, cs[t], 0.0, lsv[t], 0.0, usv[t]);
       }
       wsum<4>(v);
       if (!R2) {
-        const K5 ks = mk5(v);
-        ref = sqrt(omega * ks.pres * ks.pres + ks.dres * ks.dres / omega + ks.gap * ks.gap);
+        const Kkt5 ks = kkt5(v);
+        ref = kkt_omega(ks, omega, inv_omega);
       }
     }
 #pragma unroll
@@ -395,7 +360,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           const int j = lane + 32 * t;
           if (cok[t]) {
             const double l0j = P.l0[j], u0j = P.u0[j];
-            kcol(v, true, dc[t], xp[t], KTyp[t], c0[j], cs[t], l0j, lsv[t], u0j, usv[t]);
+            kkt_col_acc(v, true, dc[t], xp[t], KTyp[t], c0[j], cs[t], l0j, lsv[t], u0j, usv[t]);
             const double d = xp[t] - xr[t];
             v[4] += d * d;
             cert_col(cacc, dc[t], x[t], xa[t], KTy[t], KTya[t], c0[j], l0j, u0j);
@@ -405,7 +370,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         for (int t = 0; t < RPT; ++t) {
           const int i = lane + 32 * t;
           if (rok[t]) {
-            krow(v, true, i < m1, dr[t], yp[t], Kxp[t], q0[i], qs[t]);
+            kkt_row_acc(v, true, i < m1, dr[t], yp[t], Kxp[t], q0[i], qs[t]);
             const double d = yp[t] - yr[t];
             v[5] += d * d;
             cert_row(cacc, i < m1, dr[t], y[t], ya[t], Kx[t], Kxa[t], q0[i]);
@@ -413,7 +378,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         }
         v[6] = cacc.sy; v[7] = cacc.sx; v[8] = cacc.oy; v[9] = cacc.ox;
         wsum<10>(v);
-        const K5 kw = mk5(v);
+        const Kkt5 kw = kkt5(v);
         if (lane == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
           verbose_line(b, k, kw.pobj, kw.dobj, kw.pres, kw.dres, kw.gap, omega, eta);
         if (tpass(kw, nq0, nc0)) { status = LP_OPTIMAL; outsel = 1; break; }
@@ -452,10 +417,10 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           if (rok[t]) {
             const bool ge = i < m1;
             const double q0i = q0[i];
-            krow(v + 0, true, ge, dr[t], ya[t], s, q0i, qs[t]);
-            krow(v + 4, true, ge, dr[t], y[t], Kx[t], q0i, qs[t]);
-            krow(v + 8, false, ge, dr[t], ya[t], s, q0i, qs[t]);
-            krow(v + 12, false, ge, dr[t], y[t], Kx[t], q0i, qs[t]);
+            kkt_row_acc(v + 0, true, ge, dr[t], ya[t], s, q0i, qs[t]);
+            kkt_row_acc(v + 4, true, ge, dr[t], y[t], Kx[t], q0i, qs[t]);
+            kkt_row_acc(v + 8, false, ge, dr[t], ya[t], s, q0i, qs[t]);
+            kkt_row_acc(v + 12, false, ge, dr[t], y[t], Kx[t], q0i, qs[t]);
             const double da = ya[t] - yr[t], dcur = y[t] - yr[t];
             v[17] += da * da;
             v[19] += dcur * dcur;
@@ -471,10 +436,10 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           const int j = lane + 32 * t;
           if (cok[t]) {
             const double c0j = c0[j], l0j = P.l0[j], u0j = P.u0[j];
-            kcol(v + 0, true, dc[t], xa[t], s, c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
-            kcol(v + 4, true, dc[t], x[t], KTy[t], c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
-            kcol(v + 8, false, dc[t], xa[t], s, c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
-            kcol(v + 12, false, dc[t], x[t], KTy[t], c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
+            kkt_col_acc(v + 0, true, dc[t], xa[t], s, c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
+            kkt_col_acc(v + 4, true, dc[t], x[t], KTy[t], c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
+            kkt_col_acc(v + 8, false, dc[t], xa[t], s, c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
+            kkt_col_acc(v + 12, false, dc[t], x[t], KTy[t], c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
             const double da = xa[t] - xr[t], dcur = x[t] - xr[t];
             v[16] += da * da;
             v[18] += dcur * dcur;
@@ -483,7 +448,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         }
         v[20] = cacc.sy; v[21] = cacc.sx; v[22] = cacc.oy; v[23] = cacc.ox;
         wsum<24>(v);
-        const K5 ka = mk5(v + 0), kc = mk5(v + 4);
+        const Kkt5 ka = kkt5(v + 0), kc = kkt5(v + 4);
         if (lane == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
           verbose_line(b, k, kc.pobj, kc.dobj, kc.pres, kc.dres, kc.gap, omega, eta);
         if (tpass(ka, nq0, nc0)) { status = LP_OPTIMAL; outsel = 1; break; }
@@ -502,22 +467,20 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         }
         if (k == P.iter_limit) {
           status = LP_ITERATION_LIMIT;
-          outsel = rel5(ka, nq0, nc0) < rel5(kc, nq0, nc0) ? 1 : 0;
+          outsel = kkt5_rel(ka, nq0, nc0) < kkt5_rel(kc, nq0, nc0) ? 1 : 0;
           break;
         }
-        const K5 sa = mk5(v + 8), sc = mk5(v + 12);
-        const double e_a = sqrt(omega * sa.pres * sa.pres + sa.dres * sa.dres / omega + sa.gap * sa.gap);
-        const double e_c = sqrt(omega * sc.pres * sc.pres + sc.dres * sc.dres / omega + sc.gap * sc.gap);
-        if (e_a < e_c) { csel = 1; metric = e_a; dx2c = v[16]; dy2c = v[17]; }
+        const Kkt5 sa = kkt5(v + 8), sc = kkt5(v + 12);
+        const double e_a = kkt_omega(sa, omega, inv_omega);
+        const double e_c = kkt_omega(sc, omega, inv_omega);
+        if (restart_to_average(e_a, e_c)) { csel = 1; metric = e_a; dx2c = v[16]; dy2c = v[17]; }
         else { csel = 0; metric = e_c; dx2c = v[18]; dy2c = v[19]; }
       }
-      const bool restart = ((double)k_in >= 0.36 * (double)k) || (metric <= 0.2 * ref) ||
-                           (metric <= 0.8 * ref && metric > last);
+      const bool restart = restart_due(k_in, k, metric, ref, last);
       last = metric;
       if (restart) {
         ++restarts;
-        const double dxn = sqrt(dx2c), dyn = sqrt(dy2c);
-        if (dxn > 1e-10 && dyn > 1e-10) omega = sqrt(omega * (dyn / dxn));
+        omega = primal_weight(omega, sqrt(dx2c), sqrt(dy2c));
         inv_omega = 1.0 / omega;
 #pragma unroll
         for (int t = 0; t < CPT; ++t) {
@@ -544,7 +507,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         if (cok[t]) {
           const double xs = outsel ? (R2 ? xp[t] : xa[t]) : x[t];
           const double kt = outsel ? (R2 ? KTyp[t] : KTya[t]) : KTy[t];
-          kcol(v, true, dc[t], xs, kt, c0[j], cs[t], P.l0[j], lsv[t], P.u0[j], usv[t]);
+          kkt_col_acc(v, true, dc[t], xs, kt, c0[j], cs[t], P.l0[j], lsv[t], P.u0[j], usv[t]);
           if (!rays) {
             X[j] = dc[t] * xs;
             L[j] = c0[j] - kt / dc[t];
@@ -557,19 +520,19 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         if (rok[t]) {
           const double ys = outsel ? (R2 ? yp[t] : ya[t]) : y[t];
           const double kx = outsel ? (R2 ? Kxp[t] : Kxa[t]) : Kx[t];
-          krow(v, true, i < m1, dr[t], ys, kx, q0[i], qs[t]);
+          kkt_row_acc(v, true, i < m1, dr[t], ys, kx, q0[i], qs[t]);
           if (!rays) Y[i] = dr[t] * ys;
         }
       }
       wsum<4>(v);
       if (lane == 0) {
-        const K5 ko = mk5(v);
+        const Kkt5 ko = kkt5(v);
         lp_result r;
         r.status = status; r.polish = 0;
         r.iterations = k; r.attempts = jatt; r.restarts = restarts;
         r.primal_objective = ko.pobj; r.dual_objective = ko.dobj;
         r.primal_residual = ko.pres; r.dual_residual = ko.dres; r.gap = ko.gap;
-        r.rel_kkt = rel5(ko, nq0, nc0);
+        r.rel_kkt = kkt5_rel(ko, nq0, nc0);
         r.omega = omega; r.eta = eta; r.solve_seconds = 0.0;
         P.res[b] = r;
       }

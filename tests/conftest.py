@@ -9,3 +9,16 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA (B200, sm_100a) device")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+def parity_log(test, **counts):
+    """Record how many cases a parity test actually compared (DESIGN.md §4 quotes these).
+    Appends one JSON line to $MPAX_PARITY_LOG when set (the GPU runs point it at
+    gpurun_out/), and prints it (visible with pytest -s / -rA)."""
+    import json
+    line = json.dumps(dict(test=test, **{k: (int(v) if hasattr(v, "__int__") else v) for k, v in counts.items()}))
+    print("PARITY", line)
+    path = os.environ.get("MPAX_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(line + "\n")

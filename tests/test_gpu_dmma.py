@@ -13,7 +13,8 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs CUDA", allow_module_level=True)
 
 import paper_2412_09734_b200 as mp  # noqa: E402
-from tests.test_gpu_parity import batch_drift, rel  # noqa: E402
+from tests.conftest import parity_log  # noqa: E402
+from tests.test_gpu_parity import batch_drift, close, maxrel, rel  # noqa: E402
 
 ALGS = ["ra", "r2"]
 
@@ -37,28 +38,15 @@ def test_dmma_fixed_K(alg, K, name, m, n, B, seed):
     kw = dict(eps_abs=1e-13, eps_rel=1e-13, iteration_limit=K)
     res, X, Y = dmma_batch(lp, C, Q, alg, **kw)
     Xo, Yo, ro = oracle.solve_batch(lp, C, Q, alg, **kw)
-    stable, dx = batch_drift_q(lp, C, Q, alg, ro, Xo, **kw)
+    stable, dx, _ = batch_drift(lp, C, alg, ro, Xo, Q=Q, seeds=(1, 2), **kw)
+    parity_log(f"dmma_fixed_K{K}[{name},{alg}]", compared=stable.sum(), total=B)
     assert stable.sum() >= 0.75 * B, stable.sum()
     for b in np.nonzero(stable)[0]:
         for k in ("status", "iterations", "attempts", "restarts"):
             assert res[b][k] == ro[b][k], (b, k, res[b][k], ro[b][k])
         tol = max(1e-9, 100 * dx[b])
-        assert rel(X[b], Xo[b]) <= tol, (b, rel(X[b], Xo[b]), dx[b])
-        assert rel(Y[b], Yo[b]) <= max(tol, 1e-8)
-
-
-def batch_drift_q(lp, C, Q, alg, ro, X, **kw):
-    keys = ("status", "iterations", "attempts", "restarts")
-    from tests.test_gpu_parity import ulp_perturb
-    B = C.shape[0]
-    stable = np.ones(B, bool)
-    dx = np.zeros(B)
-    for seed in (1, 2):
-        Xp, _, rp = oracle.solve_batch(lp, ulp_perturb(C, seed), Q, alg, **kw)
-        for b in range(B):
-            stable[b] &= all(rp[b][k] == ro[b][k] for k in keys)
-            dx[b] = max(dx[b], rel(Xp[b], X[b]))
-    return stable, dx
+        assert close(X[b], Xo[b], tol), (b, rel(X[b], Xo[b]), maxrel(X[b], Xo[b]), dx[b])
+        assert close(Y[b], Yo[b], max(tol, 1e-8)), (b, rel(Y[b], Yo[b]), maxrel(Y[b], Yo[b]))
 
 
 @pytest.mark.parametrize("alg", ALGS)
@@ -67,7 +55,12 @@ def test_dmma_full_solve(alg, name, m, n, B, seed):
     lp, C, Q, obj = lpgen.g_dense(m, n, batch=B, seed=seed)
     res, X, Y = dmma_batch(lp, C, Q, alg)
     Xo, Yo, ro = oracle.solve_batch(lp, C, Q, alg)
-    same = 0
+    # four perturbed oracle runs: a full solve of these dense LPs is chaotic (reading 30), and
+    # the guard is a sample -- an instance it calls stable can still be moved by the GPU's
+    # summation order; such misses are counted and bounded (<= 10% of the stable instances)
+    stable, dx, dobj = batch_drift(lp, C, alg, ro, Xo, Q=Q, seeds=(1, 2, 3, 4))
+    keys = ("status", "iterations", "attempts", "restarts")
+    same = compared = missed = 0
     for b in range(B):
         assert res[b]["status"] == mp.LP_OPTIMAL and res[b]["rel_kkt"] <= 1e-4, (b, res[b])
         assert abs(res[b]["primal_objective"] - obj[b]) <= 1e-3 * (1 + abs(obj[b]))
@@ -75,7 +68,18 @@ def test_dmma_full_solve(alg, name, m, n, B, seed):
         assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(Q[b]))
         assert k["dres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(C[b]))
         same += res[b]["attempts"] == ro[b]["attempts"]
-    assert same >= B // 2, same
+        if stable[b]:
+            if not all(res[b][kk] == ro[b][kk] for kk in keys):
+                missed += 1
+                continue
+            # well-posed trajectory: the oracle's counts, its objective to 1e-6 (or 100x its own drift)
+            tol = max(1e-6, 100 * dobj[b])
+            assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= tol * (1 + abs(ro[b]["primal_objective"]))
+            compared += 1
+    parity_log(f"dmma_full[{name},{alg}]", compared=compared, missed=missed, stable=stable.sum(), same_counts=same,
+               total=B)
+    assert missed <= max(1, stable.sum() // 10), (missed, stable.sum())
+    assert compared >= 1, compared
 
 
 def test_dmma_matches_per_instance_path():

@@ -13,6 +13,7 @@ import pytest
 
 import lpgen
 import oracle
+from tests.conftest import parity_log
 
 pytestmark = pytest.mark.gpu
 
@@ -30,6 +31,19 @@ def rel(a, b):
     a, b = np.asarray(a), np.asarray(b)
     den = max(np.linalg.norm(b), 1e-300)
     return np.linalg.norm(a - b) / den
+
+
+def maxrel(a, b):
+    """Elementwise error max |a - b| relative to max |b| (beside the l2 `rel`)."""
+    a, b = np.asarray(a), np.asarray(b)
+    if b.size == 0:
+        return 0.0
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def close(a, b, tol):
+    """Iterate parity: both the l2-relative and the elementwise error within tol."""
+    return rel(a, b) <= tol and maxrel(a, b) <= tol
 
 
 def min_margin(r):
@@ -167,9 +181,9 @@ def test_fixed_K_iterates(alg, K, name, lp):
     tol = max(1e-9, 100 * drift)
     for key in ("status", "iterations", "attempts", "restarts"):
         assert rg[key] == ro[key], (key, rg[key], ro[key])
-    assert rel(rg["x"], ro["x"]) <= tol
+    assert close(rg["x"], ro["x"], tol), (rel(rg["x"], ro["x"]), maxrel(rg["x"], ro["x"]))
     if lp.m:
-        assert rel(rg["y"], ro["y"]) <= tol
+        assert close(rg["y"], ro["y"], tol), (rel(rg["y"], ro["y"]), maxrel(rg["y"], ro["y"]))
     assert abs(rg["primal_objective"] - ro["primal_objective"]) <= tol * (1 + abs(ro["primal_objective"]))
 
 
@@ -181,10 +195,6 @@ def test_full_solve(alg, name, lp):
     ro, stable, drift = oracle_stability(lp, alg)
     rg = gpu_solve(lp, alg)
     assert rg["status"] == mp.LP_OPTIMAL and ro["status"] == oracle.OPTIMAL
-    if stable:
-        for key in ("iterations", "attempts", "restarts"):
-            assert rg[key] == ro[key], (key, rg[key], ro[key])
-        assert abs(rg["primal_objective"] - ro["primal_objective"]) <= obj_tol(ro) * (1 + abs(ro["primal_objective"]))
     assert rg["rel_kkt"] <= 1e-4
     # self-certification on original data with the oracle's independent KKT routine
     k = oracle.kkt_original(lp, rg["x"], rg["y"])
@@ -196,6 +206,15 @@ def test_full_solve(alg, name, lp):
     assert np.all(rg["x"] >= lp.l - slack) and np.all(rg["x"] <= lp.u + slack) and np.all(rg["y"][: lp.m1] >= 0)
     if lp.obj_star is not None:
         assert abs(rg["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
+    # oracle parity (counts identical, objective within 1e-6) where the trajectory is well-posed
+    if not stable:
+        pytest.skip("counts unstable: the oracle's own counts move under a 1-ulp perturbation of c, q "
+                    "(checked above: OPTIMAL, self-certified, at the known optimum)")
+    for key in ("iterations", "attempts", "restarts"):
+        assert rg[key] == ro[key], (key, rg[key], ro[key])
+    # the objective, not x: a full solve stops anywhere in a 1e-4 neighbourhood of a possibly
+    # non-unique optimal face (reading 26); iterates are compared in the fixed-K tests
+    assert abs(rg["primal_objective"] - ro["primal_objective"]) <= obj_tol(ro) * (1 + abs(ro["primal_objective"]))
 
 
 @pytest.mark.parametrize("alg", ALGS)
@@ -213,11 +232,16 @@ def test_warm_start_parity(alg):
     lp = lpgen.g_rand(50, 100, 10, seed=1)
     rng = np.random.default_rng(3)
     x0, y0 = rng.normal(size=lp.n), rng.normal(size=lp.m)
-    ro = oracle.solve(lp, alg, x0=x0, y0=y0, iteration_limit=128, eps_abs=0, eps_rel=0)
+    ro, stable, drift = oracle_stability(lp, alg, x0=x0, y0=y0, iteration_limit=128, eps_abs=0, eps_rel=0)
     with mp.Solver(mp.Problem.from_lp(lp)) as s:
         rg = s.solve(x0, y0, algorithm=alg, iteration_limit=128, eps_abs=0.0, eps_rel=0.0)
         x, y, _ = s.solution()
-    assert rg["attempts"] == ro["attempts"] and rel(x, ro["x"]) <= 1e-9 and rel(y, ro["y"]) <= 1e-9
+    if not stable:
+        pytest.skip("ill-conditioned at this K: the oracle's own counts move under a 1-ulp perturbation")
+    tol = max(1e-9, 100 * drift)
+    assert rg["attempts"] == ro["attempts"] and rg["restarts"] == ro["restarts"]
+    assert close(x, ro["x"], tol), (rel(x, ro["x"]), maxrel(x, ro["x"]), drift)
+    assert close(y, ro["y"], tol), (rel(y, ro["y"]), maxrel(y, ro["y"]), drift)
 
 
 @pytest.mark.parametrize("alg", ALGS)
@@ -244,16 +268,17 @@ def test_device_memory_path_equals_host_path():
 
 # ------------------------------------------------------------- batches -----
 
-def batch_drift(lp, C, alg, ro, X, **kw):
-    """Per-instance sensitivity of the oracle's batch solve under three entrywise
-    1-ulp perturbations of C: (counts stable?, iterate drift, objective drift)."""
+def batch_drift(lp, C, alg, ro, X, Q=None, seeds=(1, 2, 3), **kw):
+    """Per-instance sensitivity of the oracle's batch solve under entrywise 1-ulp
+    perturbations of C (and Q when given): (counts stable?, iterate drift, objective drift)."""
     keys = ("status", "iterations", "attempts", "restarts")
     B = C.shape[0]
     stable = np.ones(B, bool)
     dx = np.zeros(B)
     dobj = np.zeros(B)
-    for seed in (1, 2, 3):
-        Xp, _, rp = oracle.solve_batch(lp, ulp_perturb(C, seed), None, alg, **kw)
+    for seed in seeds:
+        Qp = None if Q is None else ulp_perturb(Q, seed + 100)
+        Xp, _, rp = oracle.solve_batch(lp, ulp_perturb(C, seed), Qp, alg, **kw)
         for b in range(B):
             stable[b] &= all(rp[b][k] == ro[b][k] for k in keys)
             dx[b] = max(dx[b], rel(Xp[b], X[b]))
@@ -277,11 +302,13 @@ def test_grid_batch_c2_fixed_K(alg):
     Xo, Yo, ro = oracle.solve_batch(lp, C, None, alg, **kw)
     stable, dx, _ = batch_drift(lp, C, alg, ro, Xo, **kw)
     assert stable.sum() >= 0.9 * 1024, stable.sum()
+    parity_log(f"c2_fixed_K[{alg}]", compared=stable.sum(), total=1024)
     for b in np.nonzero(stable)[0]:
         for k in ("status", "iterations", "attempts", "restarts"):
             assert res[b][k] == ro[b][k], (b, k, res[b][k], ro[b][k])
-        assert rel(X[b], Xo[b]) <= max(1e-9, 100 * dx[b]), (b, rel(X[b], Xo[b]), dx[b])
-        assert rel(Y[b], Yo[b]) <= max(1e-9, 100 * dx[b]) or rel(Y[b], Yo[b]) <= 1e-8
+        tol = max(1e-9, 100 * dx[b])
+        assert close(X[b], Xo[b], tol), (b, rel(X[b], Xo[b]), maxrel(X[b], Xo[b]), dx[b])
+        assert close(Y[b], Yo[b], max(tol, 1e-8)), (b, rel(Y[b], Yo[b]), maxrel(Y[b], Yo[b]))
 
 
 @pytest.mark.parametrize("alg", ALGS)
@@ -291,7 +318,8 @@ def test_grid_batch_c2(alg):
     changes move the oracle's own counts on ~2% (ra) / ~14% (r2) of instances), so
     full-solve count identity is only checked loosely; every instance must be
     OPTIMAL, self-certified and at the DP optimum, and instances with identical
-    counts must agree on the objective (1e-6, or 100x the oracle's own drift)."""
+    counts must agree on the objective (1e-6, or 100x the oracle's own drift).
+    Instances whose counts are unstable, or differ, are counted and reported, not compared."""
     lp, C = lpgen.g_grid(batch=1024)
     bs = mp.BatchSolver(mp.Problem.from_lp(lp), C)
     res = bs.solve(algorithm=alg)
@@ -302,17 +330,17 @@ def test_grid_batch_c2(alg):
     keys = ("status", "iterations", "attempts", "restarts")
     same = np.array([all(res[b][k] == ro[b][k] for k in keys) for b in range(1024)])
     assert same.sum() >= (0.9 if alg == "ra" else 0.6) * 1024, same.sum()
+    compared = same & stable
+    parity_log(f"c2_full[{alg}]", compared=compared.sum(), same_counts=same.sum(), stable=stable.sum(), total=1024)
+    assert compared.sum() >= (0.85 if alg == "ra" else 0.5) * 1024, compared.sum()
     for b in range(1024):
         assert res[b]["status"] == mp.LP_OPTIMAL
         assert res[b]["rel_kkt"] <= 1e-4
         dp = lpgen.grid_dp_optimum(5, C[b])
         assert abs(res[b]["primal_objective"] - dp) <= 1e-3 * (1 + dp)
-        if same[b]:
-            # two eps-optimal points may differ by ~2 eps (1 + 2|obj|) when the trajectory is unstable;
-            # stable ones to 1e-5 (not the fixed-K 1e-9): the full solve stops at a 1e-4 KKT tolerance
-            # on degenerate grid LPs, where a rounding-level difference in the step (e.g. x * (1/omega)
-            # vs x / omega) moves the final point along the optimal face
-            tol = max(1e-5, 100 * dobj[b]) if stable[b] else 1e-3
+        if compared[b]:
+            tol = max(1e-6, 100 * dobj[b])
+            # objective only: grid LPs are degenerate, the 1e-4 point moves along the optimal face (reading 26)
             assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= tol * (1 + dp), (b, dobj[b])
         k = oracle.kkt_original(lp.with_costs(c=C[b]), X[b], Y[b])
         assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.q))
@@ -342,15 +370,21 @@ def test_dense_batch_per_instance_c3_sample():
     X, _ = bs.solutions()
     bs.close()
     Xo, _, ro = oracle.solve_batch(lp, Cs, Qs, "r2")
+    stable, dx, dobj = batch_drift(lp, Cs, "r2", ro, Xo, Q=Qs, seeds=(1, 2))
+    keys = ("status", "iterations", "attempts", "restarts")
+    compared = 0
     for b in range(8):
         assert res[b]["status"] == mp.LP_OPTIMAL and res[b]["rel_kkt"] <= 1e-4
         assert abs(res[b]["primal_objective"] - obj[b]) <= 1e-3 * (1 + abs(obj[b]))
-        if res[b]["attempts"] == ro[b]["attempts"] and res[b]["restarts"] == ro[b]["restarts"]:
-            # no sensitivity guard here (the oracle's 8 solves of 200x400 take seconds each): equal
-            # counts still allow the rounding-level drift of reading 30, and two 1e-4-optimal points
-            # may differ by the gap tolerance eps (1 + |pobj| + |dobj|) ~ 2e-4 |obj| (measured 2.2e-4
-            # on one instance), so the bar is the solve's own tolerance scale, not 1e-6
-            assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= 1e-3 * (1 + abs(obj[b]))
+        if stable[b]:
+            # sensitivity guard: well-posed trajectories match the oracle exactly
+            for k in keys:
+                assert res[b][k] == ro[b][k], (b, k, res[b][k], ro[b][k])
+            tol = max(1e-6, 100 * dobj[b])
+            assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= tol * (1 + abs(obj[b])), (b, dobj[b])
+            compared += 1
+    parity_log("c3_instance_path", compared=compared, total=8)
+    assert compared >= 4, compared
 
 
 @pytest.mark.parametrize("alg", ALGS)
@@ -368,10 +402,13 @@ def test_tiny_register_path_matches_generic_kernel(alg):
     (ra_, Xa, Ya), (rb_, Xb, Yb) = out[mp.PATH_AUTO], out[mp.PATH_INSTANCE]
     same = [ra_[b]["attempts"] == rb_[b]["attempts"] and ra_[b]["restarts"] == rb_[b]["restarts"]
             for b in range(256)]
+    parity_log(f"tiny_vs_generic[{alg}]", same_counts=sum(same), total=256)
     assert sum(same) >= (0.9 if alg == "ra" else 0.6) * 256, sum(same)
     for b in range(256):
         assert ra_[b]["status"] == mp.LP_OPTIMAL and rb_[b]["status"] == mp.LP_OPTIMAL
-        assert abs(ra_[b]["primal_objective"] - rb_[b]["primal_objective"]) <= 1e-3 * (1 + abs(rb_[b]["primal_objective"]))
+        # same arithmetic (common.cuh), different summation order: identical counts -> same point
+        tol = 1e-6 if same[b] else 1e-3
+        assert abs(ra_[b]["primal_objective"] - rb_[b]["primal_objective"]) <= tol * (1 + abs(rb_[b]["primal_objective"]))
     # before the long-run chaos: one check interval, identical counts and iterates
     bsA = mp.BatchSolver(mp.Problem.from_lp(lp), C)
     rA = bsA.solve(algorithm=alg, path=mp.PATH_AUTO, iteration_limit=64, eps_abs=0.0, eps_rel=0.0)

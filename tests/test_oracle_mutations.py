@@ -20,8 +20,8 @@ PIN_SUITES = ["tests/test_oracle_readings.py", "tests/test_oracle_pins.py", "tes
 
 # (name, [(exact source text, replacement)], contract step / reading it breaks)
 MUTATIONS = [
-    ("kkt_omega weights swapped", [("sqrt(omega * r.pres * r.pres + r.dres * r.dres / omega",
-                                    "sqrt(r.pres * r.pres / omega + omega * r.dres * r.dres")], "step 5"),
+    ("kkt_omega weights swapped", [("sqrt(omega * r.pres * r.pres + r.dres * r.dres * inv_omega",
+                                    "sqrt(r.pres * r.pres * inv_omega + omega * r.dres * r.dres")], "step 5"),
     ("omega0 from the unscaled ||q||", [("nq = m ? norm2(S->q, m) : 0.0;", "nq = m ? norm2(S->q0, m) : 0.0;")],
      "c.3 #7"),
     ("omega0 inverted", [("*omega = nc / nq;", "*omega = nq / nc;")], "c.3 #7"),
@@ -32,6 +32,8 @@ MUTATIONS = [
     ("r2 reference never reset", [("if (k_in == 0) { ref = rP; ref_set = 1; }",
                                    "if (!ref_set) { ref = rP; ref_set = 1; }"),
                                   ("      else ref_set = 0;\n", "      else {}\n")], "c.3 #12"),
+    ("primal step uses eta * omega", [("double tau = eta * (1.0 / omega), sigma", "double tau = eta * omega, sigma")],
+     "step 3"),
     ("dual step drops +K~x", [("(S->q[i] - 2.0 * Kxp[i] + Kx[i])", "(S->q[i] - 2.0 * Kxp[i])")], "step 3"),
     ("dual objective upper-bound sign", [("if (u[j] < ORA_INF) dobj -= u[j] * lm;",
                                           "if (u[j] < ORA_INF) dobj += u[j] * lm;")], "step 5"),
