@@ -193,7 +193,10 @@ int lp_create_batch(const lp_problem_desc *shared, int64_t batch, const double *
 
 /* Replace the per-instance costs / right-hand sides of a batch handle (same
  * shapes; NULL leaves that side unchanged).  Used for SPO+-style loops where K
- * is fixed and c changes every step. */
+ * is fixed and c changes every step.  The new values are validated
+ * like lp_create's (LP_ERR_NAN for a NaN or infinity; the handle then holds the
+ * rejected values and no solution until the next successful update).  Synchronous:
+ * the caller's buffers may be freed on return.  LP_ERR_UNSUPPORTED on a sharded handle. */
 int lp_update_batch(lp_handle h, const double *C, const double *Q, int32_t memory);
 
 /* Solve a single-LP handle.  x0 (n) / y0 (m) are an optional warm start in
@@ -275,6 +278,16 @@ int lp_create_sharded_virtual(const lp_problem_desc *p, int32_t shards, void *cu
 int lp_nccl_unique_id(void *out_id128);
 int lp_nccl_comm_init(void **comm, int nranks, const void *id128, int rank);
 int lp_nccl_comm_destroy(void *comm);
+
+/* Self-test of the division with a deferred slow path that the latency-bound kernels use for
+ * the line-search ratio eta_bar = M / (2|I|) and the averaging weight eta / (W + eta)
+ * (contract step 3-4): `count` operand pairs drawn on the device from a
+ * counter-based hash of `seed` (random signs, exponents over the whole double range, and
+ * zeros, infinities, NaNs, subnormals mixed in) are divided both ways.  *mismatches = pairs
+ * where the fast path claimed success (ok) but its quotient is not bit-identical to the
+ * IEEE quotient a / b; *slow = pairs that took the slow path.  Synchronous on the default
+ * stream.  Returns LP_ERR_CUDA without a GPU. */
+int lp_selftest_division(int64_t count, uint64_t seed, int64_t *mismatches, int64_t *slow);
 
 /* Number of kernels this library has launched in the calling process so far
  * (bench.py reports the difference across its timed region). */

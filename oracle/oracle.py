@@ -16,23 +16,33 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "mpax_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# The same source compiled with FMA contraction (-ffp-contract=fast): an equally valid evaluation
+# order of the same arithmetic (reading 27), used by the GPU parity tests only as a
+# rounding-sensitivity probe -- how far the oracle's own trajectory moves when every step rounds
+# differently.  Never a reference value.
+_LIB_FMA = os.path.join(_HERE, "liboracle_fma.so")
 # tests/test_oracle_mutations.py points this at a deliberately mutated build
 _LIB_OVERRIDE = os.environ.get("MPAX_ORACLE_LIB")
 _lock = threading.Lock()
 _lib = None
+_lib_fma = None
 
 OPTIMAL, ITERATION_LIMIT, NUMERICAL_ERROR, PRIMAL_INFEASIBLE, DUAL_INFEASIBLE = 1, 2, 3, 4, 5
 RAPDHG, R2HPDHG = 0, 1
 
 
-def build(force: bool = False) -> str:
-    """Compile the oracle shared library (plain C, no FMA contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-ffp-contract=off",
+def build(force: bool = False, fma: bool = False) -> str:
+    """Compile the oracle shared library (plain C, no FMA contraction; `fma`: the contracted
+    rounding-sensitivity build)."""
+    out = _LIB_FMA if fma else _LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        tmp = out + f".tmp{os.getpid()}"
+        contract = "-ffp-contract=fast" if fma else "-ffp-contract=off"
+        flags = ["-march=x86-64-v3"] if fma else []   # hardware FMA so contraction really happens
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", contract, *flags,
                                "-fno-fast-math", "-fPIC", "-shared", _SRC, "-o", tmp, "-lm"])
-        os.replace(tmp, _LIB)
-    return _LIB
+        os.replace(tmp, out)
+    return out
 
 
 class Problem(C.Structure):
@@ -83,11 +93,13 @@ class Kkt(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
-def lib():
-    global _lib
+def lib(fma: bool = False):
+    global _lib, _lib_fma
     with _lock:
-        if _lib is None:
-            L = C.CDLL(_LIB_OVERRIDE or build())
+        if fma and _lib_fma is not None:
+            return _lib_fma
+        if (fma and _lib_fma is None) or (not fma and _lib is None):
+            L = C.CDLL(build(fma=True) if fma else (_LIB_OVERRIDE or build()))
             P = C.POINTER
             L.ora_validate.argtypes = [P(Problem)]
             L.ora_solve.argtypes = [P(Problem), P(Options), C.c_void_p, C.c_void_p, C.c_void_p,
@@ -127,6 +139,9 @@ def lib():
             L.ora_initial_steps.argtypes = [P(Problem), P(Options), P(C.c_double), P(C.c_double)]
             L.ora_restart_candidate.argtypes = [C.c_double, C.c_double]
             L.ora_restart_candidate.restype = C.c_int32
+            if fma:
+                _lib_fma = L
+                return L
             _lib = L
     return _lib
 
@@ -180,7 +195,8 @@ def validate(lp) -> int:
 
 def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, x0=None, y0=None,
           check_frequency=64, log_capacity=0, step_rule=0, eps_primal_infeasible=1e-8, eps_dual_infeasible=1e-8,
-          feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0, ruiz_iters=10, pock_chambolle=1):
+          feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0, ruiz_iters=10, pock_chambolle=1,
+          fma=False):
     """Full solve (contract steps 0-6).  Returns a dict with x, y, lam, the
     result fields, and (if log_capacity) the attempt/check decision logs."""
     b = _Bound(lp)
@@ -200,7 +216,7 @@ def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, 
         g = Log(log_capacity, 0, att.ctypes.data, log_capacity, 0, chk.ctypes.data)
     x0a = None if x0 is None else _f64(x0)
     y0a = None if y0 is None else _f64(y0)
-    e = lib().ora_solve(C.byref(b.s), C.byref(o), _ptr(x0a), _ptr(y0a), x.ctypes.data,
+    e = lib(fma).ora_solve(C.byref(b.s), C.byref(o), _ptr(x0a), _ptr(y0a), x.ctypes.data,
                         y.ctypes.data if m else None, lam.ctypes.data, C.byref(r),
                         C.byref(g) if g is not None else None)
     if e != 0:
@@ -215,7 +231,8 @@ def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, 
 
 def solve_batch(lp, C_=None, Q=None, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None,
                 X0=None, Y0=None, check_frequency=64, threads=None, step_rule=0, eps_primal_infeasible=1e-8,
-                eps_dual_infeasible=1e-8, feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0):
+                eps_dual_infeasible=1e-8, feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0,
+                fma=False):
     """Batch solve sharing K, l, u; one instance per OpenMP thread."""
     b = _Bound(lp)
     m = lp.m1 + lp.m2
@@ -233,7 +250,7 @@ def solve_batch(lp, C_=None, Q=None, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4,
         lib().ora_set_threads(int(threads))
     X0a = None if X0 is None else _f64(X0)
     Y0a = None if Y0 is None else _f64(Y0)
-    e = lib().ora_solve_batch(C.byref(b.s), B, _ptr(Cm), _ptr(Qm), C.byref(o), _ptr(X0a), _ptr(Y0a),
+    e = lib(fma).ora_solve_batch(C.byref(b.s), B, _ptr(Cm), _ptr(Qm), C.byref(o), _ptr(X0a), _ptr(Y0a),
                               X.ctypes.data, Y.ctypes.data if m else None, res)
     if e != 0:
         raise ValueError(f"oracle error {e}")

@@ -38,10 +38,11 @@ struct lp_handle_s {
   double *spo = nullptr;                // SPO+ staging for host inputs / outputs (lazily allocated)
   lp_result *d_res = nullptr, *h_res = nullptr;
   unsigned long long *queue = nullptr;
+  unsigned long long qbase = kQueueUnknown;  // the queue counter's value when known (tiny_solve)
   double *work = nullptr;
   size_t work_bytes = 0;
   int64_t *rp64 = nullptr;
-  int *d_flag = nullptr, *h_flag = nullptr;
+  int *d_flag = nullptr, *h_flag = nullptr;  // validation flags (8 ints; the fused small setup: 8 per CTA)
   void *arena = nullptr;  // one allocation holding every per-handle array
   ShardedLP *sharded = nullptr;  // row-sharded handle (lp_create_sharded / _virtual)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -151,7 +152,7 @@ void free_handle(lp_handle h) {
     if (p) cudaFreeAsync(p, s);
   // every D2H into the pinned buffers was followed by a stream sync, so they can be recycled now
   pin_put(h->h_res, (size_t)h->batch * sizeof(lp_result));
-  pin_put(h->h_flag, 8 * sizeof(int));
+  pin_put(h->h_flag, 8 * kMaxSetupBlocks * sizeof(int));
   ev_put(h->ev0);
   ev_put(h->ev1);
   delete h;
@@ -251,7 +252,7 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
     A.take(&P.l0, n); A.take(&P.u0, n); A.take(&P.ls, n); A.take(&P.us, n); A.take(&P.Dr, m); A.take(&P.Dc, n);
     A.take(&P.kmax, 1); A.take(&P.sigma, 1); A.take(&h->C0, perC ? batch * n : n); A.take(&h->Q0, perQ ? batch * m : m);
     A.take(&h->X, batch * n); A.take(&h->Y, batch * m); A.take(&h->L, batch * n);
-    A.take(&h->d_res, batch); A.take(&h->queue, 1); A.take(&h->d_flag, 8);
+    A.take(&h->d_res, batch); A.take(&h->queue, 1); A.take(&h->d_flag, 8 * kMaxSetupBlocks);
   };
   {
     Arena sizing;
@@ -264,7 +265,7 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
   P.tab = const_cast<double *>(step_table(s));
   if (!P.tab) return cleanup(fail(LP_ERR_CUDA, "line-search table"));
   h->h_res = (lp_result *)pin_get((size_t)batch * sizeof(lp_result));
-  h->h_flag = (int *)pin_get(8 * sizeof(int));
+  h->h_flag = (int *)pin_get(8 * kMaxSetupBlocks * sizeof(int));
   if (!h->h_res || !h->h_flag) return cleanup(fail(LP_ERR_OUT_OF_MEMORY, "pinned host buffers"));
   if (!(h->ev0 = ev_get()) || !(h->ev1 = ev_get()))
     return cleanup(fail(LP_ERR_CUDA, "event create"));
@@ -273,7 +274,40 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
     MPAX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
     return LP_OK;
   };
-  {
+  const int64_t nC = perC ? batch * n : n, nQ = m > 0 ? (perQ ? batch * m : m) : 0;
+  const double *srcC = perC ? C : p->c, *srcQ = perQ ? Q : p->q;
+  if (setup_tiny_ok(P)) {
+    // one launch: K, l, u, c / q copied into the handle, validated, transposed and scaled
+    // (device inputs are read in place; host inputs are copied in first)
+    const int blocks = setup_tiny_blocks(nC, nQ);
+    TinySetupSources S;
+    if (p->memory == LP_DEVICE && memory == LP_DEVICE) {
+      S.rp64 = p->row_ptr; S.ci = p->col_idx; S.kv0 = p->values; S.l = p->l; S.u = p->u; S.c = srcC; S.q = srcQ;
+    } else {
+      CK(cp(P.ci, p->col_idx, (size_t)nnz * sizeof(int32_t)));
+      CK(cp(P.kv0, p->values, (size_t)nnz * sizeof(double)));
+      CK(cp(h->rp64, p->row_ptr, (size_t)(m + 1) * sizeof(int64_t)));
+      CK(cp(P.l0, p->l, (size_t)n * sizeof(double)));
+      CK(cp(P.u0, p->u, (size_t)n * sizeof(double)));
+      CK(cp(h->C0, srcC, (size_t)nC * sizeof(double)));
+      if (nQ) CK(cp(h->Q0, srcQ, (size_t)nQ * sizeof(double)));
+      S.rp64 = h->rp64; S.ci = P.ci; S.kv0 = P.kv0; S.l = P.l0; S.u = P.u0; S.c = h->C0; S.q = h->Q0;
+    }
+    CK(setup_tiny(P, S, h->rp64, h->C0, nC, h->Q0, nQ, h->d_flag, blocks, s, h->queue));
+    h->qbase = 0;  // zeroed by the setup kernel
+    CK(cp(h->h_flag, h->d_flag, (size_t)blocks * 8 * sizeof(int)));
+    if (cudaStreamSynchronize(s) != cudaSuccess) return cleanup(fail(LP_ERR_CUDA, "setup"));
+    // combine the per-CTA validation records (severity max, first index min, lengths max)
+    int f[8] = {0, INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX, 0, 0, 0};
+    for (int b = 0; b < blocks; ++b) {
+      const int *r = h->h_flag + 8 * b;
+      f[0] = std::max(f[0], r[0]);
+      for (int k = 1; k <= 4; ++k) f[k] = std::min(f[k], r[k]);
+      f[5] = std::max(f[5], r[5]);
+      f[6] = std::max(f[6], r[6]);
+    }
+    memcpy(h->h_flag, f, sizeof(f));
+  } else {
     const int init[8] = {0, INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX, 0, 0, 0};
     memcpy(h->h_flag, init, sizeof(init));
     UploadList U;
@@ -294,15 +328,15 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
       for (int k = 0; k < U.count; ++k) CK(cp(U.dst[k], U.src[k], U.bytes[k]));
       CK(cp(h->d_flag, h->h_flag, sizeof(init)));
     }
+    if (setup_small_ok(P)) {
+      CK(setup_small(P, h->rp64, h->C0, perC ? batch * n : n, h->Q0, perQ ? batch * m : m, s, h->d_flag));
+    } else {
+      CK(setup_validate(P, h->rp64, h->C0, perC ? batch * n : n, h->Q0, perQ ? batch * m : m, s, h->d_flag));
+      CK(setup_build(P, h->rp64, s, h->d_flag));
+    }
+    CK(cp(h->h_flag, h->d_flag, 8 * sizeof(int)));
+    if (cudaStreamSynchronize(s) != cudaSuccess) return cleanup(fail(LP_ERR_CUDA, "setup"));
   }
-  if (setup_small_ok(P)) {
-    CK(setup_small(P, h->rp64, h->C0, perC ? batch * n : n, h->Q0, perQ ? batch * m : m, s, h->d_flag));
-  } else {
-    CK(setup_validate(P, h->rp64, h->C0, perC ? batch * n : n, h->Q0, perQ ? batch * m : m, s, h->d_flag));
-    CK(setup_build(P, h->rp64, s, h->d_flag));
-  }
-  CK(cp(h->h_flag, h->d_flag, 8 * sizeof(int)));
-  if (cudaStreamSynchronize(s) != cudaSuccess) return cleanup(fail(LP_ERR_CUDA, "setup"));
   const int *flag = h->h_flag;
   if (flag[0] == 3) return cleanup(fail(LP_ERR_DIMENSION, "CSR structure invalid at row " + std::to_string(flag[4])));
   if (flag[0] == 2) return cleanup(fail(LP_ERR_NAN, "NaN or infinity in K, c or q (or NaN in l/u) near index " + std::to_string(flag[3])));
@@ -486,10 +520,14 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
     int rc = LP_ERR_UNSUPPORTED;
     if (dmma) {
       rc = dmma_solve(h->P, oo, L, s, h->queue, h->work);
+      h->qbase = kQueueUnknown;
       if (rc == LP_ERR_UNSUPPORTED && oo.path == LP_PATH_DMMA) return fail(rc, "dense K too large for the DMMA path");
     }
-    if (rc == LP_ERR_UNSUPPORTED && oo.path == LP_PATH_AUTO) rc = tiny_solve(h->P, oo, L, s, h->queue);
-    if (rc == LP_ERR_UNSUPPORTED) rc = instance_solve(h->P, oo, L, s, h->queue, &h->work, &h->work_bytes);
+    if (rc == LP_ERR_UNSUPPORTED && oo.path == LP_PATH_AUTO) rc = tiny_solve(h->P, oo, L, s, h->queue, &h->qbase);
+    if (rc == LP_ERR_UNSUPPORTED) {
+      rc = instance_solve(h->P, oo, L, s, h->queue, &h->work, &h->work_bytes);
+      h->qbase = kQueueUnknown;  // (the generic kernels reset the counter themselves)
+    }
     return rc;
   };
   MPAX_CUDA(cudaEventRecord(h->ev0, s));
@@ -585,18 +623,25 @@ int lp_create_batch(const lp_problem_desc *shared, int64_t batch, const double *
 
 int lp_update_batch(lp_handle h, const double *C, const double *Q, int32_t memory) {
   if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  if (h->sharded) return fail(LP_ERR_UNSUPPORTED, "lp_update_batch on a sharded handle");
   if (memory != LP_HOST && memory != LP_DEVICE) return fail(LP_ERR_INVALID_ARGUMENT, "bad memory kind");
   cudaStream_t s = h->stream;
   const int64_t n = h->P.n, m = h->P.m, B = h->batch;
-  if (C) {
-    if (h->cstride == 0 && B > 1) return fail(LP_ERR_BATCH_SHAPE, "handle was created with a shared c");
-    MPAX_CUDA(cudaMemcpyAsync(h->C0, C, (size_t)(B * n) * sizeof(double), cudaMemcpyDefault, s));
-  }
-  if (Q && m > 0) {
-    if (h->qstride == 0 && B > 1) return fail(LP_ERR_BATCH_SHAPE, "handle was created with a shared q");
-    MPAX_CUDA(cudaMemcpyAsync(h->Q0, Q, (size_t)(B * m) * sizeof(double), cudaMemcpyDefault, s));
-  }
+  if (C && h->cstride == 0 && B > 1) return fail(LP_ERR_BATCH_SHAPE, "handle was created with a shared c");
+  if (Q && m > 0 && h->qstride == 0 && B > 1) return fail(LP_ERR_BATCH_SHAPE, "handle was created with a shared q");
+  const int64_t nc = C ? (h->cstride ? B * n : n) : 0, nq = (Q && m > 0) ? (h->qstride ? B * m : m) : 0;
+  if (C) MPAX_CUDA(cudaMemcpyAsync(h->C0, C, (size_t)nc * sizeof(double), cudaMemcpyDefault, s));
+  if (nq) MPAX_CUDA(cudaMemcpyAsync(h->Q0, Q, (size_t)nq * sizeof(double), cudaMemcpyDefault, s));
+  // the new costs are validated like lp_create's (NaN / infinity -> LP_ERR_NAN, the handle keeps
+  // no solution); synchronous, so the caller's (possibly temporary) buffers are free on return
   h->solved = false;
+  if (nc + nq > 0) {
+    TRY(validate_costs(h->C0, nc, h->Q0, nq, h->d_flag, s));
+    MPAX_CUDA(cudaMemcpyAsync(h->h_flag, h->d_flag, 8 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  }
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  if (nc + nq > 0 && h->h_flag[0] == 2)
+    return fail(LP_ERR_NAN, "NaN or infinity in the updated c or q near index " + std::to_string(h->h_flag[3]));
   return LP_OK;
 }
 
@@ -671,6 +716,7 @@ int lp_get_solution(lp_handle h, int64_t instance, double *x, double *y, double 
 
 int lp_get_solutions(lp_handle h, double *X, double *Y, int32_t memory) {
   if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  if (h->sharded) return fail(LP_ERR_UNSUPPORTED, "lp_get_solutions on a sharded handle (use lp_get_solution)");
   if (!h->solved) return fail(LP_ERR_NOT_SOLVED, "no solve yet");
   cudaStream_t s = h->stream;
   const int64_t n = h->P.n, m = h->P.m, B = h->batch;
@@ -698,6 +744,7 @@ int lp_get_shape(lp_handle h, int64_t *n, int64_t *m1, int64_t *m2, int64_t *bat
 
 int lp_get_scaling(lp_handle h, double *Dr, double *Dc, int32_t memory) {
   if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  if (h->sharded) return fail(LP_ERR_UNSUPPORTED, "lp_get_scaling on a sharded handle");
   cudaStream_t s = h->stream;
   if (Dr && h->P.m) MPAX_CUDA(cudaMemcpyAsync(Dr, h->P.Dr, (size_t)h->P.m * sizeof(double), cudaMemcpyDefault, s));
   if (Dc) MPAX_CUDA(cudaMemcpyAsync(Dc, h->P.Dc, (size_t)h->P.n * sizeof(double), cudaMemcpyDefault, s));
@@ -707,6 +754,7 @@ int lp_get_scaling(lp_handle h, double *Dr, double *Dc, int32_t memory) {
 
 int lp_spmv_scaled(lp_handle h, const double *v, double *Kv, const double *w, double *KTw, int32_t memory) {
   if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  if (h->sharded) return fail(LP_ERR_UNSUPPORTED, "lp_spmv_scaled on a sharded handle");
   cudaStream_t s = h->stream;
   const int64_t n = h->P.n, m = h->P.m;
   double *dv = nullptr, *dKv = nullptr, *dw = nullptr, *dKTw = nullptr;

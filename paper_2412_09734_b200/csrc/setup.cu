@@ -395,6 +395,193 @@ __global__ void __launch_bounds__(kSmallT) setup_small_kernel(
   if (tid == 0) *kmax = __longlong_as_double((long long)s_kmax);
 }
 
+// ---- fused multi-CTA setup for LPs whose K fits in shared memory (the C2 batches) ----------
+// One launch does the whole create of a small LP batch: CTA 0 copies the shared K, l, u into the
+// handle, validates them, transposes K and runs the 11 scaling rounds with every array in shared
+// memory (no L2 round trips on the rounds' dependent loads); CTAs 1.. copy and check the
+// per-instance costs c / q in parallel.  Same checks, same arithmetic in the same order as
+// validate_kernel + transpose + precond_norms/update + scale_kernel (Dr, Dc bitwise equal).
+// Each CTA writes its own 8 validation ints (vflag[blockIdx.x * 8 ..]; the flag layout of
+// `report`) so no initialisation launch is needed; the host combines them (max / min).
+struct TinySetupArgs {
+  int m, n, nnz;
+  const int64_t *rp64_src;
+  const int32_t *ci_src;
+  const double *kv0_src, *l_src, *u_src, *c_src, *q_src;
+  int64_t nc, nq;
+  int32_t *rp, *ci, *trp, *tci, *perm;
+  double *kv0, *l0, *u0, *c_dst, *q_dst, *kv, *tkv, *ls, *us, *Dr, *Dc, *kmax;
+  int *vflag;
+  unsigned long long *queue;  // the handle's work-queue counter, zeroed here
+};
+constexpr int kTinySetupT = 256;
+
+__device__ __forceinline__ void sreport(int *f, int sev, int idx) {
+  atomicMax(f, sev);
+  atomicMin(f + 1 + sev, idx);
+}
+
+__global__ void __launch_bounds__(kTinySetupT) setup_tiny_kernel(const TinySetupArgs A) {
+  __shared__ int f[8];
+  __shared__ int warp_tot[kTinySetupT / 32];
+  __shared__ unsigned long long s_kmax;
+  const int tid = threadIdx.x;
+  if (tid < 8) f[tid] = (tid >= 1 && tid <= 4) ? INT32_MAX : 0;
+  if (tid == 0) s_kmax = 0ull;
+  if (tid == 0 && blockIdx.x == 0 && A.queue) *A.queue = 0ull;
+  __syncthreads();
+  if (blockIdx.x > 0) {  // per-instance costs: copy into the handle and check finiteness
+    const int64_t st = (int64_t)(gridDim.x - 1) * kTinySetupT;
+    for (int64_t t = (int64_t)(blockIdx.x - 1) * kTinySetupT + tid; t < A.nc + A.nq; t += st) {
+      if (t < A.nc) {
+        const double v = A.c_src[t];
+        if (A.c_dst != A.c_src) A.c_dst[t] = v;
+        if (!isfinite(v)) sreport(f, 2, (int)t);
+      } else {
+        const double v = A.q_src[t - A.nc];
+        if (A.q_dst != A.q_src) A.q_dst[t - A.nc] = v;
+        if (!isfinite(v)) sreport(f, 2, (int)(t - A.nc));
+      }
+    }
+    __syncthreads();
+    if (tid < 8) A.vflag[blockIdx.x * 8 + tid] = f[tid];
+    return;
+  }
+  const int m = A.m, n = A.n, nnz = A.nnz;
+  extern __shared__ double sh[];
+  double *kvs = sh, *Dr = kvs + nnz, *Dc = Dr + m, *rho = Dc + n, *gam = rho + m;
+  int *rp = (int *)(gam + n), *ci = rp + m + 1, *trp = ci + nnz, *tci = trp + n + 1, *perm = tci + nnz;
+  // phase 0: copy K, l, u into the handle (and shared memory), validation (validate_kernel's checks)
+  for (int i = tid; i <= m; i += kTinySetupT) {
+    const int64_t a = A.rp64_src[i];
+    rp[i] = (int32_t)a;
+    A.rp[i] = (int32_t)a;
+  }
+  for (int p = tid; p < nnz; p += kTinySetupT) {
+    const int32_t j = A.ci_src[p];
+    const double v = A.kv0_src[p];
+    ci[p] = j; kvs[p] = v;
+    A.ci[p] = j; A.kv0[p] = v;
+    if (!isfinite(v)) sreport(f, 2, p);
+  }
+  for (int j = tid; j < n; j += kTinySetupT) {
+    const double lj = A.l_src[j], uj = A.u_src[j];
+    if (A.l0 != A.l_src) A.l0[j] = lj;
+    if (A.u0 != A.u_src) A.u0[j] = uj;
+    if (isnan(lj) || isnan(uj)) sreport(f, 2, j);
+    else if (lj == INFINITY || uj == -INFINITY || lj > uj) sreport(f, 1, j);
+  }
+  __syncthreads();
+  for (int i = tid; i < m; i += kTinySetupT) {
+    const int64_t a = A.rp64_src[i], b = A.rp64_src[i + 1];
+    if ((i == 0 && a != 0) || (i == m - 1 && b != nnz) || b < a || a < 0 || b > nnz) { sreport(f, 3, i); continue; }
+    atomicMax(f + 5, (int)(b - a));
+    for (int p = (int)a; p < (int)b; ++p) {
+      const int32_t j = ci[p];
+      if (j < 0 || j >= n || (p > a && j <= ci[p - 1])) { sreport(f, 3, i); break; }
+    }
+  }
+  __syncthreads();
+  if (f[0] != 0) {
+    if (tid < 8) A.vflag[tid] = f[tid];
+    return;
+  }
+  // phase 1: column counts, K' row pointers (block scan), stable placement (row-major scan)
+  for (int j = tid; j <= n; j += kTinySetupT) trp[j] = 0;
+  __syncthreads();
+  for (int p = tid; p < nnz; p += kTinySetupT) atomicAdd(trp + ci[p], 1);
+  __syncthreads();
+  int running = 0;
+  for (int j0 = 0; j0 < n; j0 += kTinySetupT) {
+    const int j = j0 + tid;
+    const int cnt = j < n ? trp[j] : 0;
+    if (j < n) atomicMax(f + 6, cnt);
+    const int off = block_exclusive_scan<kTinySetupT>(cnt, warp_tot);  // (synchronises)
+    if (j < n) trp[j] = running + off;
+    if (tid == kTinySetupT - 1) warp_tot[0] = off + cnt;
+    __syncthreads();
+    running += warp_tot[0];
+    __syncthreads();
+  }
+  if (tid == 0) trp[n] = nnz;
+  __syncthreads();
+  for (int j = tid; j < n; j += kTinySetupT) {
+    int d = trp[j], row = 0;
+    for (int p = 0; p < nnz; ++p) {
+      while (rp[row + 1] <= p) ++row;
+      if (ci[p] == j) { tci[d] = row; perm[d] = p; ++d; }
+    }
+  }
+  for (int i = tid; i < m; i += kTinySetupT) Dr[i] = 1.0;
+  for (int j = tid; j < n; j += kTinySetupT) Dc[j] = 1.0;
+  __syncthreads();
+  // phase 2: Ruiz x10 + Pock-Chambolle (alpha = 1), a_ij = (|K_ij| Dr_i) Dc_j in stored order
+  for (int r = 0; r < 11; ++r) {
+    const bool use_sum = (r == 10);
+    for (int t = tid; t < m + n; t += kTinySetupT) {
+      double acc = 0.0;
+      if (t < m) {
+        const double dr = Dr[t];
+        for (int p = rp[t]; p < rp[t + 1]; ++p) {
+          const double a = (fabs(kvs[p]) * dr) * Dc[ci[p]];
+          acc = use_sum ? acc + a : fmax(acc, a);
+        }
+        rho[t] = acc;
+      } else {
+        const int j = t - m;
+        const double dc = Dc[j];
+        for (int d = trp[j]; d < trp[j + 1]; ++d) {
+          const double a = (fabs(kvs[perm[d]]) * Dr[tci[d]]) * dc;
+          acc = use_sum ? acc + a : fmax(acc, a);
+        }
+        gam[j] = acc;
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < m + n; t += kTinySetupT) {
+      if (t < m) { const double rr = rho[t]; Dr[t] *= (rr > 0.0 ? 1.0 / sqrt(rr) : 1.0); }
+      else { const double g = gam[t - m]; Dc[t - m] *= (g > 0.0 ? 1.0 / sqrt(g) : 1.0); }
+    }
+    __syncthreads();
+  }
+  // phase 3: scaled values, K' structure, bounds, max |K~| into the handle
+  double mx = 0.0;
+  for (int t = tid; t < m + n; t += kTinySetupT) {
+    if (t < m) {
+      const double dr = Dr[t];
+      A.Dr[t] = dr;
+      for (int p = rp[t]; p < rp[t + 1]; ++p) {
+        const double sv = (kvs[p] * dr) * Dc[ci[p]];
+        A.kv[p] = sv;
+        mx = fmax(mx, fabs(sv));
+      }
+    } else {
+      const int j = t - m;
+      const double dc = Dc[j];
+      A.Dc[j] = dc;
+      A.trp[j] = trp[j];
+      for (int d = trp[j]; d < trp[j + 1]; ++d) {
+        A.tci[d] = tci[d];
+        A.perm[d] = perm[d];
+        A.tkv[d] = (kvs[perm[d]] * Dr[tci[d]]) * dc;
+      }
+      A.ls[j] = A.l_src[j] / dc;
+      A.us[j] = A.u_src[j] / dc;
+    }
+  }
+  if (mx > 0.0) atomicMax(&s_kmax, (unsigned long long)__double_as_longlong(mx));
+  __syncthreads();
+  if (tid == 0) {
+    A.trp[n] = nnz;
+    *A.kmax = __longlong_as_double((long long)s_kmax);
+  }
+  if (tid < 8) A.vflag[tid] = f[tid];
+}
+
+size_t tiny_setup_smem(int64_t m, int64_t n, int64_t nnz) {
+  return (size_t)(nnz + 2 * (m + n)) * sizeof(double) + (size_t)(m + 1 + n + 1 + 3 * nnz) * sizeof(int);
+}
+
 inline int grid_for(int64_t work, int block = 256) {
   int64_t g = (work + block - 1) / block;
   if (g < 1) g = 1;
@@ -403,6 +590,27 @@ inline int grid_for(int64_t work, int block = 256) {
 }
 
 }  // namespace
+
+// Finiteness of replaced costs / right-hand sides (lp_update_batch): flags as validate_kernel's.
+__global__ void validate_costs_kernel(const double *__restrict__ c, int64_t nc, const double *__restrict__ q,
+                                      int64_t nq, int *flag) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nc + nq; t += st) {
+    if (t < nc) { if (!isfinite(c[t])) report(flag, 2, (int)t); }
+    else if (!isfinite(q[t - nc])) report(flag, 2, (int)(t - nc));
+  }
+}
+
+__global__ void flag_init_kernel(int *flag) {
+  if (threadIdx.x < 8) flag[threadIdx.x] = (threadIdx.x >= 1 && threadIdx.x <= 4) ? INT32_MAX : 0;
+}
+
+int validate_costs(const double *c, int64_t nc, const double *q, int64_t nq, int *d_flag, cudaStream_t s) {
+  MPAX_LAUNCH(flag_init_kernel, 1, 32, 0, s, d_flag);
+  MPAX_LAUNCH(validate_costs_kernel, grid_for(nc + nq), 256, 0, s, c, nc, q, nq, d_flag);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
 
 int setup_validate(DevProblem &P, const int64_t *row_ptr64, const double *c, int64_t nc, const double *q, int64_t nq,
                    cudaStream_t s, int *d_flag) {
@@ -508,6 +716,44 @@ int setup_build(DevProblem &P, const int64_t *row_ptr64, cudaStream_t s, int *d_
   if ((rc = setup_scale(P, s, d_flag))) return rc;
   MPAX_CUDA(cudaFreeAsync(rho, s));
   MPAX_CUDA(cudaFreeAsync(gam, s));
+  return LP_OK;
+}
+
+// The fused multi-CTA launch applies when K, the scalings and the transpose fit in shared memory.
+constexpr size_t kTinySetupSmem = 160 * 1024;
+bool setup_tiny_ok(const DevProblem &P) {
+  return P.m + P.n <= 8192 && tiny_setup_smem(P.m, P.n, P.nnz) <= kTinySetupSmem;
+}
+
+int setup_tiny_blocks(int64_t nc, int64_t nq) {
+  const int64_t per = (int64_t)kTinySetupT * 4;  // about 4 cost entries per thread
+  int64_t g = (nc + nq + per - 1) / per;
+  if (g > 147) g = 147;
+  if (g < 1) g = 1;
+  return (int)(1 + g);
+}
+
+int setup_tiny(DevProblem &P, const TinySetupSources &S, int64_t *rp64_dst, double *c_dst, int64_t nc,
+               double *q_dst, int64_t nq, int *vflag, int blocks, cudaStream_t s, unsigned long long *queue) {
+  static bool attr_set = false;  // one opt-in per process for the large dynamic shared memory
+  if (!attr_set) {
+    MPAX_CUDA(cudaFuncSetAttribute(setup_tiny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kTinySetupSmem));
+    attr_set = true;
+  }
+  (void)rp64_dst;
+  TinySetupArgs A;
+  A.m = (int)P.m; A.n = (int)P.n; A.nnz = (int)P.nnz;
+  A.rp64_src = S.rp64; A.ci_src = S.ci; A.kv0_src = S.kv0; A.l_src = S.l; A.u_src = S.u;
+  A.c_src = S.c; A.q_src = S.q; A.nc = nc; A.nq = nq;
+  A.rp = P.rp; A.ci = P.ci; A.trp = P.trp; A.tci = P.tci; A.perm = P.perm;
+  A.kv0 = P.kv0; A.l0 = P.l0; A.u0 = P.u0; A.c_dst = c_dst; A.q_dst = q_dst;
+  A.kv = P.kv; A.tkv = P.tkv; A.ls = P.ls; A.us = P.us; A.Dr = P.Dr; A.Dc = P.Dc; A.kmax = P.kmax;
+  A.vflag = vflag;
+  A.queue = queue;
+  const size_t smem = tiny_setup_smem(P.m, P.n, P.nnz);
+  MPAX_LAUNCH(setup_tiny_kernel, blocks, kTinySetupT, smem, s, A);
+  MPAX_CHECK_LAUNCH();
   return LP_OK;
 }
 

@@ -28,7 +28,7 @@ struct TinyParams {
   int32_t check_freq, polish_mode, verbose, display_freq;
   const lp_result *active;
   int64_t batch;
-  unsigned long long *queue;
+  unsigned long long *queue, qbase;
   double *X, *Y, *L;
   lp_result *res;
 };
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
 
   for (;;) {
     __syncwarp();
-    if (lane == 0) s_inst = atomicAdd(P.queue, 1ull);
+    if (lane == 0) s_inst = atomicAdd(P.queue, 1ull) - P.qbase;
     __syncwarp();
     const int64_t b = (int64_t)s_inst;
     if (b >= P.batch) return;
@@ -186,6 +186,15 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
     for (int t = 0; t < RPT; ++t) { yp[t] = y[t]; Kxp[t] = Kx[t]; }
     int64_t k = 0, jatt = 0, k_in = 0, restarts = 0;
     int64_t next_check = P.check_freq < P.iter_limit ? P.check_freq : P.iter_limit;  // k % F == 0 || k == limit
+    // K~'y' of the latest candidate, gathered at the end of each attempt (off the next attempt's
+    // critical path): the n-side commit of an accepted step uses it
+    double KTyn[CPT];
+#pragma unroll
+    for (int t = 0; t < CPT; ++t) KTyn[t] = KTy[t];
+    // line-search factors of the NEXT attempt, loaded one attempt ahead
+    double f1n = 0.0, f2n = 0.0;
+    if (!CS) step_factors(P.tab, 1, f1n, f2n);
+    const double *ftab = P.tab + 2 * 2;  // the table entry of attempt jatt + 2 (loop-carried pointer)
     double W_ = 0.0, last = INFINITY, theta = 0.0, ha = 0.0, hb = 0.0;
     int status = 0, rejects = 0;
     bool pending = false;
@@ -210,18 +219,37 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       }
     };
 
+    // Shared-memory hazards of the attempt loop: every write of sx (phase A) / sy (phase B) is
+    // separated from the previous reads of that buffer by one of the loop's two __syncwarp()s
+    // (after phase A, after phase B); the check path ends with its own.
+    __syncwarp();
     for (;;) {
-      __syncwarp();
       // ================= phase A: [commit n-side] + primal step =================
       // Branch-free: the commit is computed every attempt and selected by `pending`
       // (theta_p = 0 leaves the average bit-identical), so the attempt is one basic block.
       const double tau = eta * inv_omega, sigma = eta * omega;
-      // raPDHG's averaging weight if this attempt is accepted (depends on eta and W only):
-      // its division runs here, off the post-reduction critical path (same operations)
-      const double W1c = W_ + eta, theta_c = R2 ? 0.0 : eta / W1c;
+      // raPDHG's averaging weight eta / (W + eta) if this attempt is accepted: the division's
+      // fast path here, its (rare) slow path only at acceptance (div_rn_fast, bit-identical to /)
+      const double W1c = W_ + eta;
+      bool theta_ok = true;
+      const double theta_f = R2 ? 0.0 : div_rn_fast(eta, W1c, theta_ok);
+      if (!R2) pin(theta_f);
       const double theta_p = pending ? theta : 0.0;
-      double f1 = 0.0, f2 = 0.0;
-      if (!CS) step_factors(P.tab, jatt + 1, f1, f2);
+      const double f1 = f1n, f2 = f2n;
+      if (!CS) {
+        // the table entry of attempt jatt + 2 (clamped; past the table the factors come from
+        // the out-of-line pow, a rarely taken call)
+        const bool in_tab = jatt + 2 < kStepTab;
+        const double *fp = in_tab ? ftab : P.tab;
+        f1n = __ldg(fp);
+        f2n = __ldg(fp + 1);
+        if (__builtin_expect(!in_tab, 0)) {
+          const double2 f = step_factors_far(jatt + 2);
+          f1n = f.x;
+          f2n = f.y;
+        }
+        ftab += 2;
+      }
       // r2HPDHG: the Halpern coefficients this attempt commits with if accepted (index k_in),
       // loaded now so the table latency overlaps the attempt instead of the next commit
       double ha_n = 0.0, hb_n = 0.0;
@@ -231,9 +259,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       double dx2 = 0.0;
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {
-        double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
+        const double s = KTyn[t];
         if (!R2) {
           xa[t] += theta_p * (xp[t] - xa[t]);
           x[t] = pending ? xp[t] : x[t];
@@ -251,6 +277,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         dx2 += d * d;
       }
       double vdx[1] = {dx2};
+      if (need) wsum<1>(vdx);  // ||dx||^2: its butterfly overlaps phase B
       __syncwarp();
       // ================= phase B: [commit m-side] + SpMV #1 + dual step =================
       double dy2 = 0.0, I = 0.0;
@@ -280,26 +307,35 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       }
       pending = false;
       double v3[2] = {dy2, I};
-      if (need) {  // ||dx||^2, ||dy||^2, <dy, K dx> in one butterfly (one 5-level dependency chain)
-        double v4[3] = {vdx[0], v3[0], v3[1]};
-        wsum<3>(v4);
-        vdx[0] = v4[0]; v3[0] = v4[1]; v3[1] = v4[2];
+      if (need) wsum<2>(v3);  // ||dy||^2, <dy, K dx>
+      // K~'y' for the next attempt's commit (and this one's check), overlapping the butterfly
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < CPT; ++t) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
+        KTyn[t] = cok[t] ? s : 0.0;
       }
       ++jatt;
       const double M = omega * vdx[0] + v3[0] * inv_omega;
       const double Iv = v3[1];
-      const double eb = (Iv != 0.0) ? M / (2.0 * fabs(Iv)) : INFINITY;
+      bool eb_ok = true;
+      double eb = div_rn_fast(M, 2.0 * fabs(Iv), eb_ok);
+      if (Iv == 0.0) eb = INFINITY;
+      else if (__builtin_expect(!eb_ok, 0)) eb = div_rn_slow(M, 2.0 * fabs(Iv));
       const bool acc = CS || (eta <= eb);
       const double eta_used = eta;
       if (!CS) eta = fmin(f1 * eb, f2 * eta);
-      if (!acc) {
+      if (__builtin_expect(!acc, 0)) {
         if (++rejects >= 100) { status = LP_NUMERICAL_ERROR; outsel = 0; break; }
         continue;
       }
       rejects = 0;
       double rP = 0.0;
       if (!R2) {
-        theta = theta_c;
+        theta = theta_f;
+        if (__builtin_expect(!theta_ok, 0)) theta = div_rn_slow(eta_used, W1c);
         W_ = W1c;
       } else {
         // r_P is read only as the restart reference (k_in = 0) and as the check metric:
@@ -312,7 +348,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       }
       ++k;
       ++k_in;
-      if (k != next_check) { pending = true; continue; }
+      if (__builtin_expect(k != next_check, 1)) { pending = true; continue; }
       next_check = (next_check + P.check_freq < P.iter_limit) ? next_check + P.check_freq : P.iter_limit;
 
       // ================= step 5: check =================
@@ -323,10 +359,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       double xo[CPT], KTyo[CPT], yo[RPT], Kxo[RPT];
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {  // commit-only, n side (K~'y' into KTyp)
-        double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
-        KTyp[t] = cok[t] ? s : 0.0;
+        KTyp[t] = KTyn[t];
         if (!R2) {
           xo[t] = x[t]; KTyo[t] = KTy[t];
           xa[t] += theta * (xp[t] - xa[t]);
@@ -495,6 +528,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         k_in = 0;
         if (!R2) { W_ = 0.0; ref = metric; }
       }
+      __syncwarp();  // the check's gathers of sx / sy before the next phase A writes sx
     }
 
     // ---- step 6: output (candidate selected by outsel) ----
@@ -541,7 +575,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
 }
 
 template <bool R2, bool CS, int RPT, int CPT, int W, int WT>
-int launch_tiny(const TinyParams &P, cudaStream_t s) {
+int launch_tiny(TinyParams P, cudaStream_t s, unsigned long long *qbase) {
   const size_t smem = (size_t)32 * (CPT + RPT) * sizeof(double);
   // occupancy of this instantiation: queried once per process (a small batch's solve is short
   // enough for the driver queries to show)
@@ -556,23 +590,30 @@ int launch_tiny(const TinyParams &P, cudaStream_t s) {
   }
   int64_t grid = (int64_t)per_sm * sms;
   if (grid > P.batch) grid = P.batch;
-  MPAX_CUDA(cudaMemsetAsync(P.queue, 0, sizeof(unsigned long long), s));
+  if (!qbase || *qbase == kQueueUnknown) {
+    MPAX_CUDA(cudaMemsetAsync(P.queue, 0, sizeof(unsigned long long), s));
+    P.qbase = 0;
+  } else {
+    P.qbase = *qbase;
+  }
   MPAX_LAUNCH((tiny_kernel<R2, CS, RPT, CPT, W, WT>), (int)grid, 32, smem, s, P);
   MPAX_CHECK_LAUNCH();
+  // every warp ends on one ticket past the batch: the launch consumes batch + grid tickets
+  if (qbase) *qbase = P.qbase + (unsigned long long)P.batch + (unsigned long long)grid;
   return LP_OK;
 }
 
 template <int RPT, int CPT, int W, int WT>
-int launch_alg(const TinyParams &P, bool r2, bool cs, cudaStream_t s) {
-  if (cs) return r2 ? launch_tiny<true, true, RPT, CPT, W, WT>(P, s) : launch_tiny<false, true, RPT, CPT, W, WT>(P, s);
-  return r2 ? launch_tiny<true, false, RPT, CPT, W, WT>(P, s) : launch_tiny<false, false, RPT, CPT, W, WT>(P, s);
+int launch_alg(const TinyParams &P, bool r2, bool cs, cudaStream_t s, unsigned long long *qb) {
+  if (cs) return r2 ? launch_tiny<true, true, RPT, CPT, W, WT>(P, s, qb) : launch_tiny<false, true, RPT, CPT, W, WT>(P, s, qb);
+  return r2 ? launch_tiny<true, false, RPT, CPT, W, WT>(P, s, qb) : launch_tiny<false, false, RPT, CPT, W, WT>(P, s, qb);
 }
 
 }  // namespace
 
 // Returns LP_ERR_UNSUPPORTED when the LP does not fit one of the register layouts.
 int tiny_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L, cudaStream_t s,
-               unsigned long long *queue) {
+               unsigned long long *queue, unsigned long long *qbase) {
   if (D.max_row < 0 || D.max_col < 0) return LP_ERR_UNSUPPORTED;
   TinyParams P;
   P.n = (int32_t)D.n; P.m = (int32_t)D.m; P.m1 = (int32_t)D.m1;
@@ -591,9 +632,9 @@ int tiny_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
   const int W = D.max_row, WT = D.max_col;
   // ELL widths as tight as the LP allows: a padded slot is a zero-valued FMA on the attempt's
   // dependent chain (C2, the 5x5 grid: every column of K has exactly two entries)
-  if (m <= 32 && n <= 64 && W <= 4 && WT <= 2) return launch_alg<1, 2, 4, 2>(P, r2, cs, s);
-  if (m <= 32 && n <= 64 && W <= 4 && WT <= 4) return launch_alg<1, 2, 4, 4>(P, r2, cs, s);
-  if (m <= 32 && n <= 64 && W <= 8 && WT <= 8) return launch_alg<1, 2, 8, 8>(P, r2, cs, s);
+  if (m <= 32 && n <= 64 && W <= 4 && WT <= 2) return launch_alg<1, 2, 4, 2>(P, r2, cs, s, qbase);
+  if (m <= 32 && n <= 64 && W <= 4 && WT <= 4) return launch_alg<1, 2, 4, 4>(P, r2, cs, s, qbase);
+  if (m <= 32 && n <= 64 && W <= 8 && WT <= 8) return launch_alg<1, 2, 8, 8>(P, r2, cs, s, qbase);
   return LP_ERR_UNSUPPORTED;
 }
 

@@ -23,7 +23,7 @@ EXPORTED_SYMBOLS = [
     "lp_get_solution", "lp_get_solutions", "lp_get_shape", "lp_get_scaling", "lp_spmv_scaled",
     "lp_kernel_launch_count", "lp_error_string", "lp_last_error_detail", "lp_destroy",
     "lp_create_sharded", "lp_create_sharded_virtual", "lp_nccl_unique_id", "lp_nccl_comm_init",
-    "lp_nccl_comm_destroy", "lp_spo_plus",
+    "lp_nccl_comm_destroy", "lp_spo_plus", "lp_selftest_division",
 ]
 
 
@@ -101,12 +101,22 @@ def lib():
             L.lp_nccl_unique_id.argtypes = [V]
             L.lp_nccl_comm_init.argtypes = [P(V), C.c_int, V, C.c_int]
             L.lp_nccl_comm_destroy.argtypes = [V]
+            if hasattr(L, "lp_selftest_division"):  # (older builds, loaded for A/B timing, lack it)
+                L.lp_selftest_division.argtypes = [C.c_int64, C.c_uint64, P(C.c_int64), P(C.c_int64)]
             L.lp_error_string.argtypes = [C.c_int]
             L.lp_error_string.restype = C.c_char_p
             L.lp_last_error_detail.restype = C.c_char_p
             L.lp_destroy.argtypes = [V]
             _lib = L
     return _lib
+
+
+def selftest_division(count: int, seed: int = 1):
+    """(mismatches, slow_path) of lp_selftest_division: the kernels' division fast path against
+    IEEE a / b on `count` device-generated operand pairs."""
+    m, sl = C.c_int64(), C.c_int64()
+    _check(lib().lp_selftest_division(int(count), int(seed), C.byref(m), C.byref(sl)), "lp_selftest_division")
+    return m.value, sl.value
 
 
 def launch_count() -> int:
@@ -132,17 +142,29 @@ def _mem_of(a):
     return LP_HOST
 
 
+_TORCH_DT = {}
+
+
+def _torch_dtype(dtype):
+    if not _TORCH_DT:
+        import torch
+        _TORCH_DT.update({np.float64: torch.float64, np.int64: torch.int64, np.int32: torch.int32})
+    return _TORCH_DT[dtype]
+
+
 class _Arr:
     """A contiguous array of a given dtype on host (numpy) or device (torch)."""
+
+    __slots__ = ("src", "obj", "ptr")
 
     def __init__(self, a, dtype):
         self.src = a
         if a is None:
             self.obj, self.ptr = None, None
         elif _is_torch(a):
-            import torch
-            tdt = {np.float64: torch.float64, np.int64: torch.int64, np.int32: torch.int32}[dtype]
-            t = a.to(dtype=tdt).contiguous()
+            tdt = _torch_dtype(dtype)
+            # already the right dtype and contiguous (the common case): no torch op, just the pointer
+            t = a if (a.dtype == tdt and a.is_contiguous()) else a.to(dtype=tdt).contiguous()
             self.obj, self.ptr = t, t.data_ptr()
         else:
             arr = np.ascontiguousarray(a, dtype=dtype)
@@ -201,12 +223,20 @@ class Problem:
                        f(self.l, torch.float64), f(self.u, torch.float64), self.dense)
 
     def _desc(self):
+        """The lp_problem_desc of this problem (and the arrays it points into, kept alive).  Cached
+        while the problem's arrays are the same objects (a batch loop creates handles on one
+        problem many times; the descriptor is pure marshalling)."""
+        key = tuple(id(a) for a in (self.row_ptr, self.col_idx, self.values, self.c, self.q, self.l, self.u))
+        cached = getattr(self, "_desc_cache", None)
+        if cached is not None and cached[0] == key:
+            return cached[1], cached[2]
         arrs = [_Arr(self.row_ptr, np.int64), _Arr(self.col_idx, np.int32), _Arr(self.values, np.float64),
                 _Arr(self.c, np.float64), _Arr(self.q, np.float64), _Arr(self.l, np.float64),
                 _Arr(self.u, np.float64)]
         mem = _same_mem([a.src for a in arrs])
         nnz = int(arrs[2].obj.numel() if _is_torch(arrs[2].obj) else arrs[2].obj.size)
         d = ProblemDesc(self.n, self.m1, self.m2, nnz, int(self.dense), mem, *[a.ptr for a in arrs])
+        self._desc_cache = (key, d, arrs)
         return d, arrs
 
 
@@ -251,9 +281,15 @@ def create_lp(c, A=None, b=None, G=None, h=None, l=None, u=None, use_sparse_matr
     return Problem(n, Gm.shape[0], Am.shape[0], rp, ci, v, c, np.concatenate([hq, bq]), l, u, dense)
 
 
+_DEFAULTS = None
+
+
 def default_options(**kw) -> Options:
-    o = Options()
-    lib().lp_default_options(C.byref(o))
+    global _DEFAULTS
+    if _DEFAULTS is None:
+        _DEFAULTS = Options()
+        lib().lp_default_options(C.byref(_DEFAULTS))
+    o = Options.from_buffer_copy(_DEFAULTS)
     rule = kw.pop("step_rule", None)
     if rule is not None:
         o.step_rule = STEP_CONSTANT if rule in ("constant", STEP_CONSTANT) else STEP_ADAPTIVE

@@ -1,5 +1,6 @@
 """C2 step timing only (bench.py's step: create + batch solve + solutions + close), for A/B runs
-of the library (MPAX_LIB)."""
+of the library (MPAX_LIB).  Prints the median step, the median solve (the library's own event
+time around the solver launch) and the slowest instance's attempts (the critical path)."""
 import os
 import sys
 
@@ -10,25 +11,34 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_2412_09734_b200 as mp  # noqa: E402
 
-lp, C = bench.make_workload(1024, seed=2)
+lp, C = bench.make_workload(int(os.environ.get("C2_BATCH", 1024)), seed=2)
+B = C.shape[0]
 dev = torch.device("cuda", 0)
 prob = mp.Problem.from_lp(lp).to(dev)
 Cd = torch.as_tensor(C, device=dev)
-X = torch.empty((1024, lp.n), dtype=torch.float64, device=dev)
-Y = torch.empty((1024, lp.m), dtype=torch.float64, device=dev)
+X = torch.empty((B, lp.n), dtype=torch.float64, device=dev)
+Y = torch.empty((B, lp.m), dtype=torch.float64, device=dev)
 alg = os.environ.get("C2_ALG", "ra")
+rule = os.environ.get("C2_RULE", "adaptive")
+
+
 def step():
     bs = mp.BatchSolver(prob, Cd)
-    r = bs.solve(algorithm=alg, iteration_limit=200_000)
+    r = bs.solve(algorithm=alg, iteration_limit=200_000, step_rule=rule)
     bs.solutions(memory=mp.LP_DEVICE, X=X, Y=Y)
     bs.close()
     return r
+
+
 for _ in range(10):
     step()
 st = torch.cuda.current_stream()
-ts = []
-for _ in range(300):
+ts, ss = [], []
+for _ in range(int(os.environ.get("C2_REPS", 300))):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(st); r = step(); b.record(st); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
-print(f"{os.environ.get('MPAX_LIB', 'default')}: median {np.median(ts):.4f} ms  min {np.min(ts):.4f}  "
-      f"LPs/s {1024 / np.median(ts) * 1e3:.0f}  max it {r['iterations'].max()}  sum att {r['attempts'].sum()}")
+    a.record(st); r = step(); b.record(st); torch.cuda.synchronize()
+    ts.append(a.elapsed_time(b)); ss.append(float(r["solve_seconds"][0]) * 1e3)
+att = int(r["attempts"].max())
+print(f"{os.path.basename(os.environ.get('MPAX_LIB', 'default')):12s} {alg} step {np.median(ts):.4f} ms (min {np.min(ts):.4f})  "
+      f"solve {np.median(ss):.4f} ms  LPs/s {B / np.median(ts) * 1e3:.0f}  max it {r['iterations'].max()}  "
+      f"max att {att} (instance {int(np.argmax(r['attempts']))})  us/att {np.median(ss) * 1e3 / att:.3f}  sum att {r['attempts'].sum()}", flush=True)

@@ -38,7 +38,7 @@ def test_dmma_fixed_K(alg, K, name, m, n, B, seed):
     kw = dict(eps_abs=1e-13, eps_rel=1e-13, iteration_limit=K)
     res, X, Y = dmma_batch(lp, C, Q, alg, **kw)
     Xo, Yo, ro = oracle.solve_batch(lp, C, Q, alg, **kw)
-    stable, dx, _ = batch_drift(lp, C, alg, ro, Xo, Q=Q, seeds=(1, 2), **kw)
+    stable, dx, _ = batch_drift(lp, C, alg, ro, Xo, Q=Q, seeds=(1, 2), Y=Yo, **kw)
     parity_log(f"dmma_fixed_K{K}[{name},{alg}]", compared=stable.sum(), total=B)
     assert stable.sum() >= 0.75 * B, stable.sum()
     for b in np.nonzero(stable)[0]:
@@ -58,7 +58,8 @@ def test_dmma_full_solve(alg, name, m, n, B, seed):
     # four perturbed oracle runs: a full solve of these dense LPs is chaotic (reading 30), and
     # the guard is a sample -- an instance it calls stable can still be moved by the GPU's
     # summation order; such misses are counted and bounded (<= 10% of the stable instances)
-    stable, dx, dobj = batch_drift(lp, C, alg, ro, Xo, Q=Q, seeds=(1, 2, 3, 4))
+    stable, dz, dobj = batch_drift(lp, C, alg, ro, Xo, Q=Q, seeds=(1, 2, 3, 4), Y=Yo)
+    stable &= dz <= 1e-6   # well-posed final point (tests/test_gpu_parity.py::test_grid_batch_c2)
     keys = ("status", "iterations", "attempts", "restarts")
     same = compared = missed = 0
     for b in range(B):

@@ -132,3 +132,38 @@ def test_invalid_batch_shapes():
     with pytest.raises(mp.LpError):
         bs.update(C)                                             # the handle shares one c
     bs.close()
+
+
+def test_division_fast_path_is_bitwise_ieee():
+    """div_rn_fast (common.cuh), used for eta_bar = M / (2|I|) and eta / (W + eta) in the
+    latency-bound kernels, is bit-identical to IEEE a / b whenever its range test passes."""
+    for seed in (1, 2):
+        mism, slow = mp.selftest_division(1 << 26, seed)
+        assert mism == 0, mism
+        assert 0 < slow < (1 << 26) // 2, slow      # the special / extreme operands take the slow path
+
+
+def test_update_batch_validates_and_sharded_handles_refuse_batch_calls():
+    """lp_update_batch checks the new costs like lp_create (LP_ERR_NAN) and is synchronous;
+    calls that have no meaning on a row-sharded handle return LP_ERR_UNSUPPORTED instead of
+    silently doing nothing."""
+    lp, C = lpgen.g_grid(batch=8)
+    bs = mp.BatchSolver(mp.Problem.from_lp(lp), C)
+    bs.solve(algorithm="ra")
+    bad = C.copy()
+    bad[3, 5] = np.nan
+    with pytest.raises(mp.LpError) as e:
+        bs.update(bad)
+    assert e.value.code == -3
+    with pytest.raises(mp.LpError) as e:          # no solution is kept after a rejected update
+        bs.solutions()
+    assert e.value.code == -9
+    bs.update(C)
+    res = bs.solve(algorithm="ra")
+    assert all(r["status"] == mp.LP_OPTIMAL for r in res)
+    bs.close()
+    with mp.ShardedSolver(mp.Problem.from_lp(lpgen.g_rand(50, 100, 10, seed=1)), virtual_shards=2) as s:
+        for call in (lambda: mp.lib().lp_get_solutions(s._h, None, None, 0),
+                     lambda: mp.lib().lp_get_scaling(s._h, None, None, 0),
+                     lambda: mp.lib().lp_update_batch(s._h, None, None, 0)):
+            assert call() == -10

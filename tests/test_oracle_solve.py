@@ -199,3 +199,42 @@ def test_partial_reflection_solves(rho):
     assert np.array_equal(a["x"], b_["x"]) and a["attempts"] == b_["attempts"]
     with pytest.raises(ValueError):
         oracle.solve(lp, "r2", reflection=1.5)
+
+
+def _restart_kinds(chk):
+    """Classify each logged restart by the first criterion of reading 12 it meets."""
+    kinds, last_k = [], 0
+    for k, metric, ref, last, rs, ps in chk[:, :6]:
+        if rs == 1:
+            kinds.append("artificial" if k - last_k >= 0.36 * k else "sufficient" if metric <= 0.2 * ref else "necessary")
+            last_k = k
+    return kinds
+
+
+def test_r2_adaptive_tail_mechanism():
+    """DESIGN.md reading 31: why adaptive-step r2HPDHG has a heavy tail on C2 (the oracle's
+    slowest instance of the 1024-LP batch, 6976 iterations vs a median of 192).  After a
+    sufficient restart at an excellent point the epoch's reference r_P(first step) is tiny, the
+    fixed-point residual then GROWS by >100x under the adaptive step (the line search bounds
+    <dy, K dx> only, which does not keep the reflected Halpern map nonexpansive), so neither the
+    sufficient nor the necessary test can fire and the epoch ends only at the artificial
+    k_in >= 0.36 k: epochs grow geometrically (x1.56).  With the constant step (reading 34) the
+    same LP takes <= 576 iterations."""
+    lp, C = lpgen.g_grid(batch=1024, seed=2)
+    lpb = lp.with_costs(c=C[764])
+    r = oracle.solve(lpb, "r2", log_capacity=1 << 16)
+    assert r["status"] == oracle.OPTIMAL and r["iterations"] >= 4000
+    chk = r["chk_log"]
+    kinds = _restart_kinds(chk)
+    assert "necessary" not in kinds and kinds.count("artificial") >= 6
+    # the long epochs: each starts right after a sufficient restart and ends artificially
+    ks = [int(k) for k, rs in zip(chk[:, 0], chk[:, 4]) if rs == 1]
+    long_epochs = [(a, b) for a, b, t in zip(ks, ks[1:], kinds[1:]) if b - a > 256]
+    assert len(long_epochs) >= 3 and all(kinds[ks.index(b)] == "artificial" for _, b in long_epochs)
+    assert all(kinds[ks.index(a)] == "sufficient" for a, _ in long_epochs)
+    ratio = chk[:, 1] / chk[:, 2]
+    assert ratio.max() > 100.0                      # the residual grows far above the epoch's reference
+    lens = [b - a for a, b in long_epochs]
+    assert all(l2 > 1.4 * l1 for l1, l2 in zip(lens, lens[1:]))   # geometric epoch growth
+    rc = oracle.solve(lpb, "r2", step_rule="constant")
+    assert rc["status"] == oracle.OPTIMAL and rc["iterations"] <= 576
