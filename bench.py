@@ -388,9 +388,12 @@ def run_ours(args):
         "secondary": secondary,
         "variants": variants,
     }
+    if rank == 0:
+        log("C1 leg (one small LP, r2HPDHG)")
+        line["c1"] = c1_leg(mp, torch, dev)
     if not args.no_large:
         log("large-LP leg (C4)")
-        line["large_lp"] = large_lp_leg(mp, torch, dev, stream, peaks, args)
+        line["large_lp"] = large_lp_leg(mp, torch, dev, stream, peaks, args, cpu=rank == 0 and not args.no_cpu_baseline)
     if not args.no_c5 and (ws > 1 or args.c5_sharded):
         log("large-LP leg (C5, 1e8 nnz), row-sharded over the ranks (NCCL)")
         c5 = c5_sharded_leg(mp, torch, dev, ws, rank, args)
@@ -398,10 +401,11 @@ def run_ours(args):
             line["c5_sharded"] = c5
     elif not args.no_c5 and rank == 0:
         log("large-LP leg (C5, 1e8 nnz)")
-        line["c5"] = large_lp_leg(mp, torch, dev, stream, peaks, args, m=5_000_000, seed=5, label="C5", reps=1)
+        line["c5"] = large_lp_leg(mp, torch, dev, stream, peaks, args, m=5_000_000, seed=5, label="C5", reps=1,
+                                  cpu=not args.no_cpu_baseline)
     if not args.no_dense:
         log("dense shared-K leg (C3)")
-        line["dense_batch"] = dense_leg(mp, torch, dev, peaks)
+        line["dense_batch"] = dense_leg(mp, torch, dev, peaks, args.no_cpu_baseline or rank != 0)
     if not args.no_spo and rank == 0:
         log("SPO+ leg (Warcraft-shaped batches)")
         line["spo"] = spo_leg(mp, torch, dev)
@@ -512,7 +516,81 @@ def attempt_bytes(n, m, nnz, alg):
     return pair, pair + upd
 
 
-def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4", reps=3):
+def oracle_cores():
+    return len(os.sched_getaffinity(0))
+
+
+def c1_leg(mp, torch, dev, reps=200, oracle_reps=20):
+    """C1 (BASELINE configs[0]): one random sparse LP G-RAND(50, 100, 10, seed 1), r2HPDHG to 1e-4
+    relative KKT.  Time of the whole path for one LP through the C ABI with device-resident
+    inputs (lp_create: validate, transpose, precondition; lp_solve; lp_get_solution; lp_destroy),
+    CUDA events on the solve stream, median of `reps`; the solve's own kernel time; the counts.
+    Beside it the CPU oracle on one host core (a single LP: the oracle's OpenMP loops only split
+    SpMV rows, so one thread is its natural setting here)."""
+    import oracle
+    lp = lpgen.g_rand(50, 100, 10, seed=1)
+    prob = mp.Problem.from_lp(lp).to(dev)
+    st = torch.cuda.current_stream()
+    ts, ks = [], []
+    for rep in range(reps + 5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        with mp.Solver(prob) as s:
+            r = s.solve(algorithm="r2")
+            x, y, lam = s.solution(memory=mp.LP_DEVICE)
+        e1.record(st)
+        torch.cuda.synchronize()
+        if rep >= 5:
+            ts.append(e0.elapsed_time(e1) * 1e3)
+            ks.append(r["solve_seconds"] * 1e6)
+    oracle.set_threads(1)
+    to = []
+    for _ in range(oracle_reps):
+        t0 = time.perf_counter()
+        ro = oracle.solve(lp, "r2")
+        to.append((time.perf_counter() - t0) * 1e6)
+    oracle.set_threads(oracle_cores())
+    return {"workload": "C1: G-RAND(50, 100, 10, seed 1), one LP, r2HPDHG to 1e-4 relative KKT",
+            "metric": "time to 1e-4 KKT (one LP, whole path)", "unit": "us", "higher_is_better": False,
+            "time_us": float(np.median(ts)), "solve_kernel_us": float(np.median(ks)),
+            "status_optimal": r["status"] == mp.LP_OPTIMAL, "iterations": int(r["iterations"]),
+            "attempts": int(r["attempts"]), "restarts": int(r["restarts"]), "rel_kkt": float(r["rel_kkt"]),
+            "objective_rel_err": abs(r["primal_objective"] - lp.obj_star) / (1 + abs(lp.obj_star)),
+            "path": "create + solve + get_solution + destroy, device inputs; the solve runs the CTA-per-LP kernel",
+            "cpu_baseline": {"value": float(np.median(to)), "unit": "us", "cores": 1, "kind": "oracle",
+                             "sample": f"median of {oracle_reps} full oracle solves of the same LP (one thread)",
+                             "iterations": int(ro["iterations"]), "cpu_model": _cpu_model()}}
+
+
+def oracle_large_baseline(lp, alg, full, label):
+    """The CPU oracle beside a large-LP leg, on every host core: a full solve (C4) or, for C5, the
+    per-attempt time from two short solves (3 and 1 accepted steps; the setup cancels) times the
+    GPU's attempt count -- labelled extrapolated."""
+    import oracle
+    cores = oracle_cores()
+    oracle.set_threads(cores)
+    if full:
+        t0 = time.perf_counter()
+        r = oracle.solve(lp, alg, iteration_limit=20_000)
+        t = time.perf_counter() - t0
+        return {"kind": "oracle", "cores": cores, "unit": "ms", "value": t * 1e3, "cpu_model": _cpu_model(),
+                "sample": f"one full {label} solve ({r['iterations']} iterations, {r['attempts']} attempts), "
+                          f"setup included", "iterations": int(r["iterations"]), "attempts": int(r["attempts"]),
+                "us_per_attempt_incl_setup": t * 1e6 / max(1, r["attempts"])}
+    t0 = time.perf_counter()
+    r1 = oracle.solve(lp, alg, iteration_limit=1, eps_abs=0.0, eps_rel=0.0)
+    t1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    r3 = oracle.solve(lp, alg, iteration_limit=3, eps_abs=0.0, eps_rel=0.0)
+    t3 = time.perf_counter() - t0
+    per = (t3 - t1) / max(1, r3["attempts"] - r1["attempts"])
+    return {"kind": "oracle", "cores": cores, "unit": "us_per_attempt", "value": per * 1e6,
+            "setup_s": t1 - per * r1["attempts"], "cpu_model": _cpu_model(),
+            "sample": f"{label}: oracle solves of 1 and 3 accepted steps; per-attempt time = difference / "
+                      "attempt difference (setup cancels)"}
+
+
+def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4", reps=3, cpu=False):
     """One large random sparse LP (C4 = G-RAND(1e5, 2e5, 20, seed 4); C5 = G-RAND(5e6, 1e7,
     20, seed 5)) solved to 1e-4 on the whole-GPU grid path: time to tolerance and the
     achieved algorithmic GB/s of the fused SpMV-pair + update loop."""
@@ -555,6 +633,16 @@ def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4"
                                  "traffic_source": "profiles/traffic.json (ncu --set full capture, per attempt)",
                                  "algorithmic_bytes_per_accepted_attempt": acc,
                                  "note": "working set (~70 MB) is L2-resident at C4; achieved may exceed HBM"}}
+        if cpu:
+            log(f"large leg {alg}: CPU oracle beside it")
+            cb = oracle_large_baseline(lp, alg, full=lp.m < 1_000_000, label=label)
+            if cb["unit"] == "us_per_attempt":   # C5: extrapolated to the GPU's attempts
+                cb["extrapolated_ms"] = cb["value"] * best["attempts"] * 1e-3 + cb["setup_s"] * 1e3
+                cb["note"] = "extrapolated: oracle per-attempt time x the GPU solve's attempts + the oracle's setup"
+                cb["gpu_speedup_extrapolated"] = cb["extrapolated_ms"] / (t * 1e3)
+            else:
+                cb["gpu_speedup"] = cb["value"] / (t * 1e3)
+            out[alg]["cpu_baseline"] = cb
         gf = gather_floor_us(lp.n, lp.m, lp.nnz, alg, hbm)
         if gf is not None:
             out[alg]["roofline"]["gather_floor"] = {
@@ -610,7 +698,7 @@ def c5_sharded_leg(mp, torch, dev, ws, rank, args, m=5_000_000, seed=5):
     return out
 
 
-def dense_leg(mp, torch, dev, peaks):
+def dense_leg(mp, torch, dev, peaks, no_cpu_baseline=False):
     """C3: 256 dense 200x400 LPs sharing K: LPs/s on the fp64 tensor-core (DMMA)
     path and on the per-instance path, with the DMMA path's achieved fp64 rate."""
     lp, C, Q, obj = lpgen.g_dense(200, 400, batch=256, seed=3)
@@ -638,6 +726,18 @@ def dense_leg(mp, torch, dev, peaks):
                              "peak_source": peak_src}
         out[name] = d
     out["speedup_dmma_vs_per_instance"] = out["dmma"]["value"] / out["per_instance"]["value"]
+    if not no_cpu_baseline:
+        import oracle
+        cores = oracle_cores()
+        oracle.set_threads(cores)
+        k = 32
+        t0 = time.perf_counter()
+        _, _, ro = oracle.solve_batch(lp, C[:k], Q[:k], "ra", iteration_limit=100_000, threads=cores)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": k / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+                               "sample": f"the first {k} of the 256 C3 instances, oracle solve_batch (one LP per "
+                                         "thread)", "cpu_model": _cpu_model(),
+                               "all_optimal": all(r["status"] == 1 for r in ro)}
     return out
 
 

@@ -234,11 +234,15 @@ int lp_spo_plus(lp_handle h, const lp_options *o, const double *C_pred, const do
                 double *grad, lp_result *out);
 
 /* Copy out instance `instance`'s solution of the last solve, in original space:
- * x (n), y (m), reduced costs lambda = c - K'y (n).  Any pointer may be NULL. */
+ * x (n), y (m), reduced costs lambda = c - K'y (n).  Any pointer may be NULL.
+ * memory = LP_HOST: synchronous (the data is in place on return).  memory = LP_DEVICE:
+ * stream-ordered on the handle's stream (no host synchronisation; work queued on that
+ * stream afterwards sees the data). */
 int lp_get_solution(lp_handle h, int64_t instance, double *x, double *y, double *reduced_costs,
                     int32_t memory);
 
-/* Copy out every instance: X (batch x n), Y (batch x m); either may be NULL. */
+/* Copy out every instance: X (batch x n), Y (batch x m); either may be NULL.
+ * Synchronous for LP_HOST, stream-ordered on the handle's stream for LP_DEVICE. */
 int lp_get_solutions(lp_handle h, double *X, double *Y, int32_t memory);
 
 /* Shapes of a handle: n, m1, m2, batch (any pointer may be NULL). */

@@ -6,6 +6,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -50,6 +52,27 @@ struct lp_handle_s {
 };
 
 namespace {
+
+// Host-side phase timer of the API calls (MPAX_HOST_TRACE=1: one stderr line per call with the
+// microseconds since the call started at each mark; diagnostics only, off by default).
+struct HostTrace {
+  bool on;
+  const char *what;
+  std::chrono::steady_clock::time_point t0;
+  char buf[512];
+  int len = 0;
+  explicit HostTrace(const char *w) : on(getenv("MPAX_HOST_TRACE") != nullptr), what(w) {
+    if (on) t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char *label) {
+    if (!on || len > 400) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    len += snprintf(buf + len, sizeof(buf) - len, " %s %.1f", label, us);
+  }
+  ~HostTrace() {
+    if (on) fprintf(stderr, "[host] %s:%s\n", what, buf);
+  }
+};
 
 std::once_flag g_pool_once;
 
@@ -223,6 +246,7 @@ int check_desc(const lp_problem_desc *p) {
 
 int create_common(const lp_problem_desc *p, int64_t batch, const double *C, const double *Q, int32_t memory,
                   void *stream, lp_handle *out, bool is_batch) {
+  HostTrace tr("create");
   TRY(check_desc(p));
   if (!out) return fail(LP_ERR_INVALID_ARGUMENT, "out is NULL");
   if (batch < 1) return fail(LP_ERR_BATCH_SHAPE, "batch must be >= 1");
@@ -258,6 +282,7 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
     Arena sizing;
     carve(sizing);
     CK(dalloc((char **)&h->arena, sizing.off, s));
+    tr.mark("arena");
     Arena real;
     real.base = (char *)h->arena;
     carve(real);
@@ -269,6 +294,7 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
   if (!h->h_res || !h->h_flag) return cleanup(fail(LP_ERR_OUT_OF_MEMORY, "pinned host buffers"));
   if (!(h->ev0 = ev_get()) || !(h->ev1 = ev_get()))
     return cleanup(fail(LP_ERR_CUDA, "event create"));
+  tr.mark("bufs");
   auto cp = [&](void *dst, const void *src, size_t bytes) -> int {
     if (bytes == 0) return LP_OK;
     MPAX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
@@ -295,8 +321,11 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
     }
     CK(setup_tiny(P, S, h->rp64, h->C0, nC, h->Q0, nQ, h->d_flag, blocks, s, h->queue));
     h->qbase = 0;  // zeroed by the setup kernel
+    tr.mark("launch");
     CK(cp(h->h_flag, h->d_flag, (size_t)blocks * 8 * sizeof(int)));
+    tr.mark("d2h");
     if (cudaStreamSynchronize(s) != cudaSuccess) return cleanup(fail(LP_ERR_CUDA, "setup"));
+    tr.mark("sync");
     // combine the per-CTA validation records (severity max, first index min, lengths max)
     int f[8] = {0, INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX, 0, 0, 0};
     for (int b = 0; b < blocks; ++b) {
@@ -343,6 +372,7 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
   if (flag[0] == 1) return cleanup(fail(LP_ERR_CROSSED_BOUNDS, "crossed bounds at index " + std::to_string(flag[2])));
   P.max_row = flag[5];
   P.max_col = flag[6];
+  tr.mark("done");
   *out = h;
   return LP_OK;
 #undef CK
@@ -471,6 +501,7 @@ __global__ void spo_loss_kernel(int64_t n, const double *__restrict__ Cp, const 
 int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *Y0, int32_t memory,
               lp_result *out) {
   if (!h || !out) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle or result");
+  HostTrace tr("solve");
   TRY(check_options(o));
   if (memory != LP_HOST && memory != LP_DEVICE) return fail(LP_ERR_INVALID_ARGUMENT, "bad memory kind");
   if (h->sharded) {
@@ -576,14 +607,17 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
     }
   }
   MPAX_CUDA(cudaEventRecord(h->ev1, s));
+  tr.mark("launched");
   MPAX_CUDA(cudaMemcpyAsync(h->h_res, h->d_res, (size_t)B * sizeof(lp_result), cudaMemcpyDeviceToHost, s));
   MPAX_CUDA(cudaStreamSynchronize(s));
+  tr.mark("sync");
   float ms = 0.0f;
   MPAX_CUDA(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   for (int64_t b = 0; b < B; ++b) {
     out[b] = h->h_res[b];
     out[b].solve_seconds = ms * 1e-3;
   }
+  tr.mark("copied");
   h->solved = true;
   return LP_OK;
 }
@@ -710,7 +744,7 @@ int lp_get_solution(lp_handle h, int64_t instance, double *x, double *y, double 
   if (x) MPAX_CUDA(cudaMemcpyAsync(x, h->X + instance * n, (size_t)n * sizeof(double), cudaMemcpyDefault, s));
   if (y && m) MPAX_CUDA(cudaMemcpyAsync(y, h->Y + instance * m, (size_t)m * sizeof(double), cudaMemcpyDefault, s));
   if (rc) MPAX_CUDA(cudaMemcpyAsync(rc, h->L + instance * n, (size_t)n * sizeof(double), cudaMemcpyDefault, s));
-  MPAX_CUDA(cudaStreamSynchronize(s));
+  if (memory != LP_DEVICE) MPAX_CUDA(cudaStreamSynchronize(s));  // device destinations: stream-ordered
   return LP_OK;
 }
 
@@ -722,7 +756,7 @@ int lp_get_solutions(lp_handle h, double *X, double *Y, int32_t memory) {
   const int64_t n = h->P.n, m = h->P.m, B = h->batch;
   if (X) MPAX_CUDA(cudaMemcpyAsync(X, h->X, (size_t)(B * n) * sizeof(double), cudaMemcpyDefault, s));
   if (Y && m) MPAX_CUDA(cudaMemcpyAsync(Y, h->Y, (size_t)(B * m) * sizeof(double), cudaMemcpyDefault, s));
-  MPAX_CUDA(cudaStreamSynchronize(s));
+  if (memory != LP_DEVICE) MPAX_CUDA(cudaStreamSynchronize(s));  // device destinations: stream-ordered
   return LP_OK;
 }
 

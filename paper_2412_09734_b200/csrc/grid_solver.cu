@@ -62,6 +62,7 @@ struct GridParams {
   double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
   int32_t check_freq, alg, gk, gkt, const_step, polish_mode, verbose, display_freq, vpol, tdist, dyn;
+  int32_t lean;   // bit 0 / 1: phase A / B through the lean out-of-line sweeps (phase_tiles)
   double *X, *Y, *L;
   lp_result *res;
 };
@@ -184,6 +185,116 @@ __device__ __forceinline__ void grid_totals(double (&t)[V], const double *part, 
   for (int k = 0; k < V; ++k) t[k] = s_tot[k];
 }
 
+// ---- lean hot phases (warp-tile mapping) -------------------------------------------------
+// The fused attempt's two SpMV sweeps run in out-of-line functions that read their pointers
+// and scalars from a per-CTA context in shared memory right where they are used (volatile:
+// not hoisted into registers).  Inlined into the kernel body, the sweeps shared the 64-register
+// budget of 2 CTAs x 512 threads per SM with the whole solve's state and spilled in the tile
+// loop (round 1: 648 B of stack per thread, ~1.2 GB of local-memory loads per C5 attempt,
+// profiles/r01g_summary.md); here the tile loop owns the registers.
+enum PhaseMode : int {
+  kA_RA = 0,   // phase A, raPDHG, commit pending: average + swap, primal step
+  kA_R2 = 1,   // phase A, r2HPDHG, commit pending: Halpern reflection, primal step
+  kB_PARK = 2, // phase B pass 1: park K~_L x' (no epilogue)
+  kB_RA = 3,   // phase B, raPDHG, commit pending: average + swap, dual step
+  kB_R2 = 4,   // phase B, r2HPDHG, commit pending
+  kB_NOP = 5,  // phase B, no pending commit (after a rejected attempt or a check)
+};
+struct PhaseCtx {
+  const int32_t *rp, *ci;
+  const double *kv, *tgt;         // the sweep's matrix and gathered vector
+  const double *add;              // + add[row] (two-pass phase B pass 2), or null
+  double *park;                   // pass 1 output
+  // epilogue vectors (meaning per mode, see phase_tiles)
+  double *e0, *e1, *e2, *e3, *e4;
+  const double *r0, *r1, *r2, *r3, *r4;
+  double tau_sigma, theta, ha, hb, rf1, rf0;
+  int rows, m1;
+  double *tpart;                  // per-tile partials (2 per tile)
+  int t0, kmax;                   // this CTA's tile range [t0, t0 + kmax) (contiguous slots)
+};
+
+template <int MODE>
+__device__ __noinline__ void phase_tiles(const volatile PhaseCtx *cx, int *s_ctr, double *tbuf) {
+  const int lane = threadIdx.x & 31;
+  const int rows = cx->rows, t0 = cx->t0, kmax = cx->kmax;
+  for (;;) {
+    int kk = 0;
+    if (lane == 0) kk = atomicAdd(s_ctr, 1);
+    kk = __shfl_sync(FULL, kk, 0);
+    if (kk >= kmax) break;
+    const int r = ((t0 + kk) << 5) + lane;
+    const bool ok = r < rows;
+    double c0 = 0.0, c1 = 0.0;
+    if (MODE == kB_PARK) {
+      const double sl = tile_row_dot(r, ok, rows, (const int32_t *)cx->rp, (const int32_t *)cx->ci,
+                                     (const double *)cx->kv, (const double *)cx->tgt, tbuf);
+      if (ok) cx->park[r] = sl;
+      continue;
+    }
+    double s = tile_row_dot(r, ok, rows, (const int32_t *)cx->rp, (const int32_t *)cx->ci, (const double *)cx->kv,
+                            (const double *)cx->tgt, tbuf);
+    if (ok) {
+      if (MODE == kA_RA) {
+        // r0 = xp, r1 = cs, r2 = ls, r3 = us; e0 = xa (rw), e1 = KTy' (w), e2 = the old x buffer (w: x')
+        const double o_xp = cx->r0[r], o_xa = cx->e0[r];
+        cx->e0[r] = o_xa + cx->theta * (o_xp - o_xa);
+        cx->e1[r] = s;
+        const double xnew = median3(cx->r2[r], o_xp - cx->tau_sigma * (cx->r1[r] - s), cx->r3[r]);
+        cx->e2[r] = xnew;
+        const double d = xnew - o_xp;
+        c0 = d * d;
+      } else if (MODE == kA_R2) {
+        // r0 = xp, r1 = cs, r2 = ls, r3 = us, r4 = KTya, e0 = xa (r), e1 = x (rw), e2 = KTy (rw), e3 = x' (w)
+        const double xn = cx->ha * (cx->rf1 * cx->r0[r] - cx->rf0 * cx->e1[r]) + cx->hb * cx->e0[r];
+        const double kt = cx->ha * (cx->rf1 * s - cx->rf0 * cx->e2[r]) + cx->hb * cx->r4[r];
+        cx->e1[r] = xn;
+        cx->e2[r] = kt;
+        const double xnew = median3(cx->r2[r], xn - cx->tau_sigma * (cx->r1[r] - kt), cx->r3[r]);
+        cx->e3[r] = xnew;
+        const double d = xnew - xn;
+        c0 = d * d;
+      } else {
+        if (cx->add) s += cx->add[r];
+        double yv, kxv;
+        if (MODE == kB_RA) {
+          // r0 = qs, r1 = yp, r2 = Kxp; e0 = ya (rw), e1 = the old y buffer (w: y'), e2 = the old Kx buffer (w)
+          yv = cx->r1[r];
+          kxv = cx->r2[r];
+          const double o_ya = cx->e0[r];
+          cx->e0[r] = o_ya + cx->theta * (yv - o_ya);
+        } else if (MODE == kB_R2) {
+          // r0 = qs, r1 = yp, r2 = Kxp, r3 = ya, r4 = Kxa; e0 = y (rw), e1 = Kx (rw), e2 = y' (w), e3 = K~x' (w)
+          yv = cx->ha * (cx->rf1 * cx->r1[r] - cx->rf0 * cx->e0[r]) + cx->hb * cx->r3[r];
+          kxv = cx->ha * (cx->rf1 * cx->r2[r] - cx->rf0 * cx->e1[r]) + cx->hb * cx->r4[r];
+          cx->e0[r] = yv;
+          cx->e1[r] = kxv;
+        } else {
+          // r0 = qs, r1 = y, r2 = Kx; e2 = y' (w), e3 = K~x' (w)
+          yv = cx->r1[r];
+          kxv = cx->r2[r];
+        }
+        double yn = yv + cx->tau_sigma * (cx->r0[r] - 2.0 * s + kxv);
+        if (r < cx->m1) yn = fmax(yn, 0.0);
+        if (MODE == kB_RA) { cx->e1[r] = yn; cx->e2[r] = s; }
+        else { cx->e2[r] = yn; cx->e3[r] = s; }
+        const double d = yn - yv;
+        c0 = d * d;
+        c1 = d * (s - kxv);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      c0 += __shfl_xor_sync(FULL, c0, off);
+      c1 += __shfl_xor_sync(FULL, c1, off);
+    }
+    if (lane == 0) {
+      cx->tpart[(size_t)(t0 + kk) * 2] = c0;
+      cx->tpart[(size_t)(t0 + kk) * 2 + 1] = c1;
+    }
+  }
+}
+
 template <int MINB>
 __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   cg::grid_group grid = cg::this_grid();
@@ -191,6 +302,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   __shared__ double s_tot[kNP];
   __shared__ double s_tile[kBS / 32][kTileBuf];   // per-warp product buffer of the G == 1 mapping
   __shared__ int s_ctr;                             // tile counter of tiles_dynamic
+  __shared__ PhaseCtx s_cx;                         // context of the lean hot phases (phase_tiles)
   double *const tbuf = s_tile[threadIdx.x >> 5];
   // L2 policy of the attempt's vector traffic (P.vpol): 0 = default; 1 = every
   // vector access except the stores of the next gather target (x', y') is evict-first, so the
@@ -251,6 +363,36 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       }
     }
   };
+  // Lean phase driver: thread 0 writes the context (fill), the CTA runs phase_tiles<MODE> over its
+  // contiguous tile range with dynamic claims, then (reduce) warp 0 sums the tile partials in tile
+  // order: on return thread 0 holds the CTA totals in tot[0..1], every other thread zeros.
+  auto lean_range = [&](int rows) {
+    const int ntiles = (rows + 31) >> 5, nb = (int)gridDim.x, T = (ntiles + nb - 1) / nb;
+    const int t0 = (int)blockIdx.x * T;
+    s_cx.rows = rows;
+    s_cx.t0 = t0;
+    s_cx.kmax = max(0, min(ntiles, t0 + T) - t0);
+    s_cx.tpart = P.tpart;
+    s_ctr = 0;
+  };
+  auto lean_reduce = [&](double (&tot)[2]) {
+    tot[0] = 0.0; tot[1] = 0.0;
+    if (threadIdx.x < 32) {
+      const int t0 = s_cx.t0, t1 = t0 + s_cx.kmax;
+      double a0 = 0.0, a1 = 0.0;
+      for (int t = t0 + (int)threadIdx.x; t < t1; t += 32) {
+        a0 += __ldcg(P.tpart + (size_t)t * 2);
+        a1 += __ldcg(P.tpart + (size_t)t * 2 + 1);
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        a0 += __shfl_xor_sync(FULL, a0, off);
+        a1 += __shfl_xor_sync(FULL, a1, off);
+      }
+      if (threadIdx.x == 0) { tot[0] = a0; tot[1] = a1; }
+    }
+  };
+  const bool leanA = P.lean & 1, leanB = P.lean & 2;
   const int n = (int)P.n, m = (int)P.m, m1 = (int)P.m1;  // < 2^31 (lp_create checks)
   const int gtid = blockIdx.x * kBS + threadIdx.x, gthreads = gridDim.x * kBS;
   const bool r2 = (P.alg == LP_R2HPDHG);
@@ -404,7 +546,24 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         const double d = xnew - xn;
         return d * d;
       };
-      if (Gt == 1 && (dyn & 4)) {
+      if (Gt == 1 && leanA) {
+        if (threadIdx.x == 0) {
+          lean_range(n);
+          s_cx.rp = P.trp; s_cx.ci = P.tci; s_cx.kv = P.tkv; s_cx.tgt = yp; s_cx.add = nullptr;
+          s_cx.r0 = xp; s_cx.r1 = cs; s_cx.r2 = P.ls; s_cx.r3 = P.us; s_cx.r4 = KTya;
+          s_cx.e0 = xa;
+          if (!r2) { s_cx.e1 = KTyp; s_cx.e2 = x; }
+          else { s_cx.e1 = x; s_cx.e2 = KTy; s_cx.e3 = xp; }
+          s_cx.tau_sigma = tau; s_cx.theta = theta; s_cx.ha = ha; s_cx.hb = hb; s_cx.rf1 = rf1; s_cx.rf0 = rf0;
+        }
+        __syncthreads();
+        if (!r2) phase_tiles<kA_RA>(&s_cx, &s_ctr, tbuf);
+        else phase_tiles<kA_R2>(&s_cx, &s_ctr, tbuf);
+        __syncthreads();
+        double t2[2];
+        lean_reduce(t2);
+        v3[0] = t2[0];
+      } else if (Gt == 1 && (dyn & 4)) {
         // global dynamic claims: warps of every CTA take column tiles from one monotonic counter,
         // so CTAs that run ahead take more tiles (no inter-CTA tail at the barrier).  Every warp
         // makes exactly one failing claim per phase, so each phase consumes ntiles + all warps
@@ -494,7 +653,38 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         c[0] = d * d;
         c[1] = d * (s - kxv);
       };
-      if (G == 1 && (dyn & 2)) {
+      if (G == 1 && leanB) {
+        // pass 1 (two-pass split): K~_L x' of this CTA's row tiles parked in tmp; pass 2 (or the
+        // only pass): K~_R x' (+ tmp) or K~x' with the row epilogue
+        if (P.split) {
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            lean_range(m);
+            s_cx.rp = P.rpL; s_cx.ci = P.ciL; s_cx.kv = P.kvL; s_cx.tgt = xp; s_cx.park = P.tmp;
+          }
+          __syncthreads();
+          phase_tiles<kB_PARK>(&s_cx, &s_ctr, tbuf);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          lean_range(m);
+          if (P.split) { s_cx.rp = P.rpR; s_cx.ci = P.ciR; s_cx.kv = P.kvR; s_cx.add = P.tmp; }
+          else { s_cx.rp = P.rp; s_cx.ci = P.ci; s_cx.kv = P.kv; s_cx.add = nullptr; }
+          s_cx.tgt = xp; s_cx.m1 = m1; s_cx.r0 = qs;
+          s_cx.tau_sigma = sigma; s_cx.theta = theta; s_cx.ha = ha; s_cx.hb = hb; s_cx.rf1 = rf1; s_cx.rf0 = rf0;
+          if (pending && !r2) { s_cx.r1 = yp; s_cx.r2 = Kxp; s_cx.e0 = ya; s_cx.e1 = y; s_cx.e2 = Kx; }
+          else if (pending) { s_cx.r1 = yp; s_cx.r2 = Kxp; s_cx.r3 = ya; s_cx.r4 = Kxa; s_cx.e0 = y; s_cx.e1 = Kx; s_cx.e2 = yp; s_cx.e3 = Kxp; }
+          else { s_cx.r1 = y; s_cx.r2 = Kx; s_cx.e2 = yp; s_cx.e3 = Kxp; }
+        }
+        __syncthreads();
+        if (pending && !r2) phase_tiles<kB_RA>(&s_cx, &s_ctr, tbuf);
+        else if (pending) phase_tiles<kB_R2>(&s_cx, &s_ctr, tbuf);
+        else phase_tiles<kB_NOP>(&s_cx, &s_ctr, tbuf);
+        __syncthreads();
+        double t2[2];
+        lean_reduce(t2);
+        v3[1] = t2[0]; v3[2] = t2[1];
+      } else if (G == 1 && (dyn & 2)) {
         double t2[2];
         if (P.split) {
           // pass 1: K~_L x' of the CTA's tiles into tmp (gather target: the first column half of
@@ -924,6 +1114,8 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   // phase B only by default
   P.dyn = 2;
   if (const char *e = getenv("MPAX_GRID_DYN")) P.dyn = atoi(e);
+  P.lean = 3;
+  if (const char *e = getenv("MPAX_GRID_LEAN")) P.lean = atoi(e);   // experiments: 0 = the inlined sweeps
   P.split = (D.split_h > 0 && split_wanted(D) && P.gk == 1 && (P.dyn & 2)) ? 1 : 0;
   P.rpL = D.rpL; P.ciL = D.ciL; P.kvL = D.kvL; P.rpR = D.rpR; P.ciR = D.ciR; P.kvR = D.kvR;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;

@@ -415,6 +415,7 @@ struct TinySetupArgs {
   unsigned long long *queue;  // the handle's work-queue counter, zeroed here
 };
 constexpr int kTinySetupT = 256;
+constexpr int kCostPer = 8;    // cost values per thread of the cost CTAs
 
 __device__ __forceinline__ void sreport(int *f, int sev, int idx) {
   atomicMax(f, sev);
@@ -431,16 +432,29 @@ __global__ void __launch_bounds__(kTinySetupT) setup_tiny_kernel(const TinySetup
   if (tid == 0 && blockIdx.x == 0 && A.queue) *A.queue = 0ull;
   __syncthreads();
   if (blockIdx.x > 0) {  // per-instance costs: copy into the handle and check finiteness
-    const int64_t st = (int64_t)(gridDim.x - 1) * kTinySetupT;
-    for (int64_t t = (int64_t)(blockIdx.x - 1) * kTinySetupT + tid; t < A.nc + A.nq; t += st) {
-      if (t < A.nc) {
-        const double v = A.c_src[t];
-        if (A.c_dst != A.c_src) A.c_dst[t] = v;
-        if (!isfinite(v)) sreport(f, 2, (int)t);
-      } else {
-        const double v = A.q_src[t - A.nc];
-        if (A.q_dst != A.q_src) A.q_dst[t - A.nc] = v;
-        if (!isfinite(v)) sreport(f, 2, (int)(t - A.nc));
+    // kCostPer consecutive values per thread, every load issued before any use (one memory
+    // round trip per CTA instead of one per grid-stride iteration)
+    const int64_t total = A.nc + A.nq;
+    const int64_t base = ((int64_t)(blockIdx.x - 1) * kTinySetupT + tid) * kCostPer;
+    const int64_t stride = (int64_t)(gridDim.x - 1) * kTinySetupT * kCostPer;
+    for (int64_t t0 = base; t0 < total; t0 += stride) {
+      double v[kCostPer];
+#pragma unroll
+      for (int u = 0; u < kCostPer; ++u) {
+        const int64_t t = t0 + u;
+        v[u] = t < A.nc ? A.c_src[t] : (t < total ? A.q_src[t - A.nc] : 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kCostPer; ++u) {
+        const int64_t t = t0 + u;
+        if (t >= total) break;
+        if (t < A.nc) {
+          if (A.c_dst != A.c_src) A.c_dst[t] = v[u];
+          if (!isfinite(v[u])) sreport(f, 2, (int)t);
+        } else {
+          if (A.q_dst != A.q_src) A.q_dst[t - A.nc] = v[u];
+          if (!isfinite(v[u])) sreport(f, 2, (int)(t - A.nc));
+        }
       }
     }
     __syncthreads();
@@ -449,36 +463,46 @@ __global__ void __launch_bounds__(kTinySetupT) setup_tiny_kernel(const TinySetup
   }
   const int m = A.m, n = A.n, nnz = A.nnz;
   extern __shared__ double sh[];
-  double *kvs = sh, *Dr = kvs + nnz, *Dc = Dr + m, *rho = Dc + n, *gam = rho + m;
-  int *rp = (int *)(gam + n), *ci = rp + m + 1, *trp = ci + nnz, *tci = trp + n + 1, *perm = tci + nnz;
-  // phase 0: copy K, l, u into the handle (and shared memory), validation (validate_kernel's checks)
-  for (int i = tid; i <= m; i += kTinySetupT) {
-    const int64_t a = A.rp64_src[i];
-    rp[i] = (int32_t)a;
-    A.rp[i] = (int32_t)a;
+  double *kvs = sh, *Dr = kvs + nnz, *Dc = Dr + m, *rho = Dc + n, *gam = rho + m, *ls = gam + n, *us = ls + n;
+  int *rp = (int *)(us + n), *ci = rp + m + 1, *trp = ci + nnz, *tci = trp + n + 1, *perm = tci + nnz,
+      *rowof = perm + nnz, *rank = rowof + nnz;
+  // phase 0: every input load in flight at once (one memory round trip): K, l, u into shared
+  // memory and the handle; value / bound checks (validate_kernel's)
+  const int span = max(max(m + 1, nnz), n);
+  for (int t = tid; t < span; t += kTinySetupT) {
+    if (t <= m) {
+      const int64_t a = A.rp64_src[t];
+      rp[t] = (int32_t)a;
+      A.rp[t] = (int32_t)a;
+      if (t < m && a != (int32_t)a) sreport(f, 3, t);
+    }
+    if (t < nnz) {
+      const int32_t j = A.ci_src[t];
+      const double v = A.kv0_src[t];
+      ci[t] = j; kvs[t] = v;
+      A.ci[t] = j; A.kv0[t] = v;
+      if (!isfinite(v)) sreport(f, 2, t);
+    }
+    if (t < n) {
+      const double lj = A.l_src[t], uj = A.u_src[t];
+      ls[t] = lj; us[t] = uj;
+      if (A.l0 != A.l_src) A.l0[t] = lj;
+      if (A.u0 != A.u_src) A.u0[t] = uj;
+      if (isnan(lj) || isnan(uj)) sreport(f, 2, t);
+      else if (lj == INFINITY || uj == -INFINITY || lj > uj) sreport(f, 1, t);
+    }
   }
-  for (int p = tid; p < nnz; p += kTinySetupT) {
-    const int32_t j = A.ci_src[p];
-    const double v = A.kv0_src[p];
-    ci[p] = j; kvs[p] = v;
-    A.ci[p] = j; A.kv0[p] = v;
-    if (!isfinite(v)) sreport(f, 2, p);
-  }
-  for (int j = tid; j < n; j += kTinySetupT) {
-    const double lj = A.l_src[j], uj = A.u_src[j];
-    if (A.l0 != A.l_src) A.l0[j] = lj;
-    if (A.u0 != A.u_src) A.u0[j] = uj;
-    if (isnan(lj) || isnan(uj)) sreport(f, 2, j);
-    else if (lj == INFINITY || uj == -INFINITY || lj > uj) sreport(f, 1, j);
-  }
+  for (int j = tid; j <= n; j += kTinySetupT) trp[j] = 0;
   __syncthreads();
+  // row structure (offsets, ranges, sorted in-range columns) and each entry's row
   for (int i = tid; i < m; i += kTinySetupT) {
-    const int64_t a = A.rp64_src[i], b = A.rp64_src[i + 1];
+    const int a = rp[i], b = rp[i + 1];
     if ((i == 0 && a != 0) || (i == m - 1 && b != nnz) || b < a || a < 0 || b > nnz) { sreport(f, 3, i); continue; }
-    atomicMax(f + 5, (int)(b - a));
-    for (int p = (int)a; p < (int)b; ++p) {
+    atomicMax(f + 5, b - a);
+    for (int p = a; p < b; ++p) {
       const int32_t j = ci[p];
       if (j < 0 || j >= n || (p > a && j <= ci[p - 1])) { sreport(f, 3, i); break; }
+      rowof[p] = i;
     }
   }
   __syncthreads();
@@ -486,10 +510,15 @@ __global__ void __launch_bounds__(kTinySetupT) setup_tiny_kernel(const TinySetup
     if (tid < 8) A.vflag[tid] = f[tid];
     return;
   }
-  // phase 1: column counts, K' row pointers (block scan), stable placement (row-major scan)
-  for (int j = tid; j <= n; j += kTinySetupT) trp[j] = 0;
-  __syncthreads();
-  for (int p = tid; p < nnz; p += kTinySetupT) atomicAdd(trp + ci[p], 1);
+  // phase 1: the stable transpose, every entry in parallel.  Entries are in row-major order, so
+  // an entry's position within its column is the number of earlier entries in that column.
+  for (int p = tid; p < nnz; p += kTinySetupT) {
+    const int j = ci[p];
+    atomicAdd(trp + j, 1);
+    int r = 0;
+    for (int q = 0; q < p; ++q) r += (ci[q] == j);
+    rank[p] = r;
+  }
   __syncthreads();
   int running = 0;
   for (int j0 = 0; j0 < n; j0 += kTinySetupT) {
@@ -504,13 +533,10 @@ __global__ void __launch_bounds__(kTinySetupT) setup_tiny_kernel(const TinySetup
     __syncthreads();
   }
   if (tid == 0) trp[n] = nnz;
-  __syncthreads();
-  for (int j = tid; j < n; j += kTinySetupT) {
-    int d = trp[j], row = 0;
-    for (int p = 0; p < nnz; ++p) {
-      while (rp[row + 1] <= p) ++row;
-      if (ci[p] == j) { tci[d] = row; perm[d] = p; ++d; }
-    }
+  for (int p = tid; p < nnz; p += kTinySetupT) {
+    const int d = trp[ci[p]] + rank[p];
+    tci[d] = rowof[p];
+    perm[d] = p;
   }
   for (int i = tid; i < m; i += kTinySetupT) Dr[i] = 1.0;
   for (int j = tid; j < n; j += kTinySetupT) Dc[j] = 1.0;
@@ -565,8 +591,8 @@ __global__ void __launch_bounds__(kTinySetupT) setup_tiny_kernel(const TinySetup
         A.perm[d] = perm[d];
         A.tkv[d] = (kvs[perm[d]] * Dr[tci[d]]) * dc;
       }
-      A.ls[j] = A.l_src[j] / dc;
-      A.us[j] = A.u_src[j] / dc;
+      A.ls[j] = ls[j] / dc;
+      A.us[j] = us[j] / dc;
     }
   }
   if (mx > 0.0) atomicMax(&s_kmax, (unsigned long long)__double_as_longlong(mx));
@@ -579,7 +605,7 @@ __global__ void __launch_bounds__(kTinySetupT) setup_tiny_kernel(const TinySetup
 }
 
 size_t tiny_setup_smem(int64_t m, int64_t n, int64_t nnz) {
-  return (size_t)(nnz + 2 * (m + n)) * sizeof(double) + (size_t)(m + 1 + n + 1 + 3 * nnz) * sizeof(int);
+  return (size_t)(nnz + 2 * (m + n) + 2 * n) * sizeof(double) + (size_t)(m + 1 + n + 1 + 5 * nnz) * sizeof(int);
 }
 
 inline int grid_for(int64_t work, int block = 256) {
@@ -722,11 +748,12 @@ int setup_build(DevProblem &P, const int64_t *row_ptr64, cudaStream_t s, int *d_
 // The fused multi-CTA launch applies when K, the scalings and the transpose fit in shared memory.
 constexpr size_t kTinySetupSmem = 160 * 1024;
 bool setup_tiny_ok(const DevProblem &P) {
-  return P.m + P.n <= 8192 && tiny_setup_smem(P.m, P.n, P.nnz) <= kTinySetupSmem;
+  // the per-entry rank scan of the transpose is O(nnz^2 / threads): small K only
+  return P.m + P.n <= 8192 && P.nnz <= 2048 && tiny_setup_smem(P.m, P.n, P.nnz) <= kTinySetupSmem;
 }
 
 int setup_tiny_blocks(int64_t nc, int64_t nq) {
-  const int64_t per = (int64_t)kTinySetupT * 4;  // about 4 cost entries per thread
+  const int64_t per = (int64_t)kTinySetupT * kCostPer;
   int64_t g = (nc + nq + per - 1) / per;
   if (g > 147) g = 147;
   if (g < 1) g = 1;
@@ -735,8 +762,9 @@ int setup_tiny_blocks(int64_t nc, int64_t nq) {
 
 int setup_tiny(DevProblem &P, const TinySetupSources &S, int64_t *rp64_dst, double *c_dst, int64_t nc,
                double *q_dst, int64_t nq, int *vflag, int blocks, cudaStream_t s, unsigned long long *queue) {
-  static bool attr_set = false;  // one opt-in per process for the large dynamic shared memory
-  if (!attr_set) {
+  const size_t need = tiny_setup_smem(P.m, P.n, P.nnz);
+  static bool attr_set = false;  // opt in to large dynamic shared memory once, only when needed
+  if (need > 48 * 1024 && !attr_set) {
     MPAX_CUDA(cudaFuncSetAttribute(setup_tiny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)kTinySetupSmem));
     attr_set = true;

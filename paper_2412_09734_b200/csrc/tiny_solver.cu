@@ -296,7 +296,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           y[t] = pending ? yc : y[t];
           Kx[t] = pending ? kc : Kx[t];
         }
-        double yn = y[t] + sigma * (qs[t] - 2.0 * s + Kx[t]);
+        // q~ - 2 K~x' as one fma: 2 s is exact, so this is the oracle's q~ - 2.0 * s, one op shorter
+        double yn = y[t] + sigma * (fma(-2.0, s, qs[t]) + Kx[t]);
         if (lane + 32 * t < m1) yn = fmax(yn, 0.0);
         yp[t] = rok[t] ? yn : 0.0;
         Kxp[t] = rok[t] ? s : 0.0;
