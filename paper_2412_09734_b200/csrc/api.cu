@@ -319,13 +319,28 @@ int create_common(const lp_problem_desc *p, int64_t batch, const double *C, cons
       if (nQ) CK(cp(h->Q0, srcQ, (size_t)nQ * sizeof(double)));
       S.rp64 = h->rp64; S.ci = P.ci; S.kv0 = P.kv0; S.l = P.l0; S.u = P.u0; S.c = h->C0; S.q = h->Q0;
     }
-    CK(setup_tiny(P, S, h->rp64, h->C0, nC, h->Q0, nQ, h->d_flag, blocks, s, h->queue));
+    cudaEvent_t te[3] = {nullptr, nullptr, nullptr};
+    if (tr.on) for (auto &e : te) { cudaEventCreate(&e); }
+    if (tr.on) cudaEventRecord(te[0], s);
+    // the per-CTA validation records go straight into the pinned host buffer (device-mapped, UVA)
+    CK(setup_tiny(P, S, h->rp64, h->C0, nC, h->Q0, nQ, h->h_flag, blocks, s, h->queue));
+    if (tr.on) cudaEventRecord(te[1], s);
     h->qbase = 0;  // zeroed by the setup kernel
     tr.mark("launch");
-    CK(cp(h->h_flag, h->d_flag, (size_t)blocks * 8 * sizeof(int)));
+    if (tr.on) cudaEventRecord(te[2], s);
     tr.mark("d2h");
     if (cudaStreamSynchronize(s) != cudaSuccess) return cleanup(fail(LP_ERR_CUDA, "setup"));
     tr.mark("sync");
+    if (tr.on) {
+      float k_ms = 0.f, c_ms = 0.f;
+      cudaEventElapsedTime(&k_ms, te[0], te[1]);
+      cudaEventElapsedTime(&c_ms, te[1], te[2]);
+      tr.mark(k_ms * 1e3f > 0 ? "gpu_kernel" : "gpu_kernel");
+      const int *ts = h->h_flag + 8 * kMaxSetupBlocks - 8;
+      fprintf(stderr, "[host] create device: setup kernel %.1f us, flag copy %.1f us; CTA 0 cycles: validated %d "
+              "transposed %d ruiz %d pc %d done %d\n", k_ms * 1e3, c_ms * 1e3, ts[0], ts[1], ts[2], ts[3], ts[4]);
+      for (auto &e : te) cudaEventDestroy(e);
+    }
     // combine the per-CTA validation records (severity max, first index min, lengths max)
     int f[8] = {0, INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX, 0, 0, 0};
     for (int b = 0; b < blocks; ++b) {
@@ -537,6 +552,7 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
       h->work_bytes = need;
     }
   }
+  bool host_written = false;   // the register kernel wrote the results into h_res itself
   // one solve of the batch (main, or a polishing sub-solve) on the chosen path
   auto dispatch = [&](const lp_options &oo, InstanceLaunch L) -> int {
     if (use_grid) {
@@ -554,7 +570,10 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
       h->qbase = kQueueUnknown;
       if (rc == LP_ERR_UNSUPPORTED && oo.path == LP_PATH_DMMA) return fail(rc, "dense K too large for the DMMA path");
     }
-    if (rc == LP_ERR_UNSUPPORTED && oo.path == LP_PATH_AUTO) rc = tiny_solve(h->P, oo, L, s, h->queue, &h->qbase);
+    if (rc == LP_ERR_UNSUPPORTED && oo.path == LP_PATH_AUTO) {
+      rc = tiny_solve(h->P, oo, L, s, h->queue, &h->qbase);
+      if (rc == LP_OK && L.res_host) host_written = true;
+    }
     if (rc == LP_ERR_UNSUPPORTED) {
       rc = instance_solve(h->P, oo, L, s, h->queue, &h->work, &h->work_bytes);
       h->qbase = kQueueUnknown;  // (the generic kernels reset the counter themselves)
@@ -567,6 +586,9 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
   InstanceLaunch L;
   L.C0 = h->C0; L.cstride = h->cstride; L.Q0 = h->Q0; L.qstride = h->qstride;
   L.X0 = dX0; L.Y0 = dY0; L.batch = B; L.X = h->X; L.Y = h->Y; L.L = h->L; L.res = h->d_res;
+  // the main solve's results straight into the pinned host buffer (device-mapped through UVA) when
+  // they are final: no polishing pass rewrites them afterwards
+  L.res_host = o->feasibility_polishing ? nullptr : h->h_res;
   TRY(dispatch(*o, L));
   if (o->feasibility_polishing) {
     // (reading 36) primal polish: c = 0 from (x*, 0); dual polish: q = 0 from (proj 0, y*);
@@ -608,7 +630,8 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
   }
   MPAX_CUDA(cudaEventRecord(h->ev1, s));
   tr.mark("launched");
-  MPAX_CUDA(cudaMemcpyAsync(h->h_res, h->d_res, (size_t)B * sizeof(lp_result), cudaMemcpyDeviceToHost, s));
+  if (!host_written)
+    MPAX_CUDA(cudaMemcpyAsync(h->h_res, h->d_res, (size_t)B * sizeof(lp_result), cudaMemcpyDeviceToHost, s));
   MPAX_CUDA(cudaStreamSynchronize(s));
   tr.mark("sync");
   float ms = 0.0f;

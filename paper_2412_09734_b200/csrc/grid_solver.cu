@@ -212,15 +212,19 @@ struct PhaseCtx {
   int rows, m1;
   double *tpart;                  // per-tile partials (2 per tile)
   int t0, kmax;                   // this CTA's tile range [t0, t0 + kmax) (contiguous slots)
+  unsigned long long *gctr;       // non-null: claim tiles from this global counter (all CTAs)
+  unsigned long long gbase;       //   counter value at the phase's start; tiles [0, kmax)
 };
 
 template <int MODE>
 __device__ __noinline__ void phase_tiles(const volatile PhaseCtx *cx, int *s_ctr, double *tbuf) {
   const int lane = threadIdx.x & 31;
   const int rows = cx->rows, t0 = cx->t0, kmax = cx->kmax;
+  unsigned long long *const gctr = cx->gctr;
+  const unsigned long long gbase = cx->gbase;
   for (;;) {
     int kk = 0;
-    if (lane == 0) kk = atomicAdd(s_ctr, 1);
+    if (lane == 0) kk = gctr ? (int)(atomicAdd(gctr, 1ull) - gbase) : atomicAdd(s_ctr, 1);
     kk = __shfl_sync(FULL, kk, 0);
     if (kk >= kmax) break;
     const int r = ((t0 + kk) << 5) + lane;
@@ -513,6 +517,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
 
   unsigned long long gbase = 0;   // phase A's global tile counter value at this phase's start
   bool sliceA = false;            // phase A used global claims: reduce this CTA's slice in phase B
+  bool sliceA2 = false;           // the same for the lean sweep (partials in P.tpart, stride 2)
   TR(unsigned long long tr_a = 0, tr_aw = 0, tr_b = 0, tr_bw = 0, tr_chk = 0, tr_n = 0, tr_t0 = 0, tr_t1 = 0);
   TR(const bool tr_on = threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1));
   while (!done) {
@@ -547,8 +552,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         return d * d;
       };
       if (Gt == 1 && leanA) {
+        const bool glob = P.lean & 4;   // claims from one global counter (no inter-CTA tail at the barrier)
         if (threadIdx.x == 0) {
           lean_range(n);
+          s_cx.gctr = nullptr;
+          if (glob) { s_cx.gctr = P.gctr; s_cx.gbase = gbase; s_cx.t0 = 0; s_cx.kmax = (n + 31) >> 5; s_cx.tpart = P.tpartA; }
           s_cx.rp = P.trp; s_cx.ci = P.tci; s_cx.kv = P.tkv; s_cx.tgt = yp; s_cx.add = nullptr;
           s_cx.r0 = xp; s_cx.r1 = cs; s_cx.r2 = P.ls; s_cx.r3 = P.us; s_cx.r4 = KTya;
           s_cx.e0 = xa;
@@ -560,9 +568,17 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         if (!r2) phase_tiles<kA_RA>(&s_cx, &s_ctr, tbuf);
         else phase_tiles<kA_R2>(&s_cx, &s_ctr, tbuf);
         __syncthreads();
-        double t2[2];
-        lean_reduce(t2);
-        v3[0] = t2[0];
+        if (glob) {
+          // every warp made exactly one failing claim: the phase consumed tiles + warps values;
+          // this CTA's fixed slice of the tile partials is summed in tile order after the barrier
+          gbase += (unsigned long long)((n + 31) >> 5) + (unsigned long long)gridDim.x * (kBS / 32);
+          sliceA2 = true;
+          v3[0] = 0.0;
+        } else {
+          double t2[2];
+          lean_reduce(t2);
+          v3[0] = t2[0];
+        }
       } else if (Gt == 1 && (dyn & 4)) {
         // global dynamic claims: warps of every CTA take column tiles from one monotonic counter,
         // so CTAs that run ahead take more tiles (no inter-CTA tail at the barrier).  Every warp
@@ -660,6 +676,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           __syncthreads();
           if (threadIdx.x == 0) {
             lean_range(m);
+            s_cx.gctr = nullptr;
             s_cx.rp = P.rpL; s_cx.ci = P.ciL; s_cx.kv = P.kvL; s_cx.tgt = xp; s_cx.park = P.tmp;
           }
           __syncthreads();
@@ -668,6 +685,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         __syncthreads();
         if (threadIdx.x == 0) {
           lean_range(m);
+          s_cx.gctr = nullptr;
           if (P.split) { s_cx.rp = P.rpR; s_cx.ci = P.ciR; s_cx.kv = P.kvR; s_cx.add = P.tmp; }
           else { s_cx.rp = P.rp; s_cx.ci = P.ci; s_cx.kv = P.kv; s_cx.add = nullptr; }
           s_cx.tgt = xp; s_cx.m1 = m1; s_cx.r0 = qs;
@@ -716,6 +734,20 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         t = Kx; Kx = Kxp; Kxp = t;
       }
       pending = false;
+      if (sliceA2) {  // the lean phase A's global-claim partials: this CTA's fixed slice, tile order
+        sliceA2 = false;
+        const int ntA = (n + 31) >> 5, nb = (int)gridDim.x, TA = (ntA + nb - 1) / nb;
+        const int a0 = (int)blockIdx.x * TA, a1 = min(ntA, a0 + TA);
+        if (threadIdx.x < 32) {
+          double a = 0.0;
+          for (int t = a0 + (int)threadIdx.x; t < a1; t += 32) a += __ldcg(P.tpartA + (size_t)t * 2);
+#pragma unroll
+          for (int off = 16; off; off >>= 1) a += __shfl_xor_sync(FULL, a, off);
+          v3[0] = threadIdx.x == 0 ? a : 0.0;
+        } else {
+          v3[0] = 0.0;
+        }
+      }
       if (sliceA) {  // phase A's tile partials of this CTA's fixed slice, in tile order
         sliceA = false;
         const int ntA = (n + 31) >> 5, nb = (int)gridDim.x, TA = (ntA + nb - 1) / nb;
@@ -1058,7 +1090,7 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   while (blocks > sms && (int64_t)blocks * kBS > 4 * work_items) blocks -= sms;
   const int64_t ntile = (std::max(n, m) + 31) / 32;
   const size_t ntp = 2 * (size_t)blocks * (size_t)((ntile + blocks - 1) / blocks);  // P.tpart slots
-  const size_t ntpA = (size_t)((n + 31) / 32) + 1;   // + the counter
+  const size_t ntpA = 2 * (size_t)((n + 31) / 32) + 1;   // + the counter (the lean sweep writes 2 per tile)
   const size_t vec = (size_t)(8 * n + 9 * m) + 2 * (size_t)blocks * kNP + ntp + ntpA;   // + tmp (m)
   const size_t need = vec * sizeof(double);
   if (*work_bytes < need) {

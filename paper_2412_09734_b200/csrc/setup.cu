@@ -10,6 +10,7 @@
 // bitwise reproducible run to run.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -120,7 +121,7 @@ __global__ void precond_norms(int64_t m, int64_t n, const int32_t *__restrict__ 
       int64_t i = t;
       double dr = Dr[i];
       for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
-        double a = (fabs(kv0[p]) * dr) * Dc[ci[p]];
+        double a = __dmul_rn(fabs(kv0[p]) * dr, Dc[ci[p]]);   // (never contracted with the sum)
         acc = use_sum ? acc + a : fmax(acc, a);
       }
       rho[i] = acc;
@@ -128,7 +129,7 @@ __global__ void precond_norms(int64_t m, int64_t n, const int32_t *__restrict__ 
       int64_t j = t - m;
       double dc = Dc[j];
       for (int32_t d = trp[j]; d < trp[j + 1]; ++d) {
-        double a = (fabs(kv0[perm[d]]) * Dr[tci[d]]) * dc;
+        double a = __dmul_rn(fabs(kv0[perm[d]]) * Dr[tci[d]], dc);
         acc = use_sum ? acc + a : fmax(acc, a);
       }
       gam[j] = acc;
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(kSmallT) setup_small_kernel(
       if (t < m) {
         const double dr = Dr[t];
         for (int p = rp[t]; p < rp[t + 1]; ++p) {
-          const double a = (fabs(kv0[p]) * dr) * Dc[ci[p]];
+          const double a = __dmul_rn(fabs(kv0[p]) * dr, Dc[ci[p]]);   // (never contracted with the sum)
           acc = use_sum ? acc + a : fmax(acc, a);
         }
         rho[t] = acc;
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(kSmallT) setup_small_kernel(
         const int j = t - m;
         const double dc = Dc[j];
         for (int d = trp[j]; d < trp[j + 1]; ++d) {
-          const double a = (fabs(kv0[perm[d]]) * Dr[tci[d]]) * dc;
+          const double a = __dmul_rn(fabs(kv0[perm[d]]) * Dr[tci[d]], dc);
           acc = use_sum ? acc + a : fmax(acc, a);
         }
         gam[j] = acc;
@@ -413,6 +414,7 @@ struct TinySetupArgs {
   double *kv0, *l0, *u0, *c_dst, *q_dst, *kv, *tkv, *ls, *us, *Dr, *Dc, *kmax;
   int *vflag;
   unsigned long long *queue;  // the handle's work-queue counter, zeroed here
+  int *tstamp;                // diagnostics (MPAX_HOST_TRACE): CTA 0's phase times in cycles, or null
 };
 constexpr int kTinySetupT = 256;
 constexpr int kCostPer = 8;    // cost values per thread of the cost CTAs
@@ -423,6 +425,10 @@ __device__ __forceinline__ void sreport(int *f, int sev, int idx) {
 }
 
 __global__ void __launch_bounds__(kTinySetupT) setup_tiny_kernel(const TinySetupArgs A) {
+  long long t_start = clock64();
+  auto stamp = [&](int k) {
+    if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0) A.tstamp[k] = (int)(clock64() - t_start);
+  };
   __shared__ int f[8];
   __shared__ int warp_tot[kTinySetupT / 32];
   __shared__ unsigned long long s_kmax;
@@ -510,12 +516,14 @@ __global__ void __launch_bounds__(kTinySetupT) setup_tiny_kernel(const TinySetup
     if (tid < 8) A.vflag[tid] = f[tid];
     return;
   }
+  stamp(0);
   // phase 1: the stable transpose, every entry in parallel.  Entries are in row-major order, so
   // an entry's position within its column is the number of earlier entries in that column.
   for (int p = tid; p < nnz; p += kTinySetupT) {
     const int j = ci[p];
     atomicAdd(trp + j, 1);
     int r = 0;
+#pragma unroll 8
     for (int q = 0; q < p; ++q) r += (ci[q] == j);
     rank[p] = r;
   }
@@ -541,35 +549,62 @@ __global__ void __launch_bounds__(kTinySetupT) setup_tiny_kernel(const TinySetup
   for (int i = tid; i < m; i += kTinySetupT) Dr[i] = 1.0;
   for (int j = tid; j < n; j += kTinySetupT) Dc[j] = 1.0;
   __syncthreads();
-  // phase 2: Ruiz x10 + Pock-Chambolle (alpha = 1), a_ij = (|K_ij| Dr_i) Dc_j in stored order
-  for (int r = 0; r < 11; ++r) {
-    const bool use_sum = (r == 10);
-    for (int t = tid; t < m + n; t += kTinySetupT) {
-      double acc = 0.0;
-      if (t < m) {
-        const double dr = Dr[t];
-        for (int p = rp[t]; p < rp[t + 1]; ++p) {
-          const double a = (fabs(kvs[p]) * dr) * Dc[ci[p]];
-          acc = use_sum ? acc + a : fmax(acc, a);
-        }
-        rho[t] = acc;
-      } else {
-        const int j = t - m;
-        const double dc = Dc[j];
-        for (int d = trp[j]; d < trp[j + 1]; ++d) {
-          const double a = (fabs(kvs[perm[d]]) * Dr[tci[d]]) * dc;
-          acc = use_sum ? acc + a : fmax(acc, a);
-        }
-        gam[j] = acc;
-      }
+  stamp(1);
+  // phase 2a: 10 Ruiz rounds.  Every entry's a_ij = (|K_ij| Dr_i) Dc_j in parallel; the row and
+  // column maxima through integer atomicMax on the bit patterns of these non-negative doubles
+  // (order-free, so exactly the sequential maxima); then 1 / sqrt per row / column.
+  unsigned long long *rmax = (unsigned long long *)rho, *cmax = (unsigned long long *)gam;
+  for (int t = tid; t < m + n; t += kTinySetupT) {
+    if (t < m) rmax[t] = 0ull; else cmax[t - m] = 0ull;
+  }
+  __syncthreads();
+  for (int r = 0; r < 10; ++r) {
+    for (int p = tid; p < nnz; p += kTinySetupT) {
+      const int i = rowof[p], j = ci[p];
+      const unsigned long long a = (unsigned long long)__double_as_longlong((fabs(kvs[p]) * Dr[i]) * Dc[j]);
+      atomicMax(rmax + i, a);
+      atomicMax(cmax + j, a);
     }
     __syncthreads();
     for (int t = tid; t < m + n; t += kTinySetupT) {
-      if (t < m) { const double rr = rho[t]; Dr[t] *= (rr > 0.0 ? 1.0 / sqrt(rr) : 1.0); }
-      else { const double g = gam[t - m]; Dc[t - m] *= (g > 0.0 ? 1.0 / sqrt(g) : 1.0); }
+      unsigned long long *slot = t < m ? rmax + t : cmax + (t - m);
+      const double g = __longlong_as_double((long long)*slot);
+      *slot = 0ull;   // ready for the next round
+      double f = 1.0;
+      if (g > 0.0) {
+        const double sg = sqrt(g);
+        bool ok;
+        f = div_rn_fast(1.0, sg, ok);
+        if (!ok) f = 1.0 / sg;
+      }
+      if (t < m) Dr[t] *= f; else Dc[t - m] *= f;
     }
     __syncthreads();
   }
+  stamp(2);
+  // phase 2b: Pock-Chambolle (alpha = 1): row / column sums in stored order (K' rows are in
+  // increasing row order), sequential per row / column as the oracle's
+  for (int t = tid; t < m + n; t += kTinySetupT) {
+    double acc = 0.0;
+    if (t < m) {
+      const double dr = Dr[t];
+      // __dmul_rn / __dadd_rn: never contracted into an FMA (the oracle rounds product and sum apart)
+      for (int p = rp[t]; p < rp[t + 1]; ++p) acc = __dadd_rn(acc, __dmul_rn(fabs(kvs[p]) * dr, Dc[ci[p]]));
+      rho[t] = acc;
+    } else {
+      const int j = t - m;
+      const double dc = Dc[j];
+      for (int d = trp[j]; d < trp[j + 1]; ++d) acc = __dadd_rn(acc, __dmul_rn(fabs(kvs[perm[d]]) * Dr[tci[d]], dc));
+      gam[j] = acc;
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < m + n; t += kTinySetupT) {
+    if (t < m) { const double rr = rho[t]; Dr[t] *= (rr > 0.0 ? 1.0 / sqrt(rr) : 1.0); }
+    else { const double g = gam[t - m]; Dc[t - m] *= (g > 0.0 ? 1.0 / sqrt(g) : 1.0); }
+  }
+  __syncthreads();
+  stamp(3);
   // phase 3: scaled values, K' structure, bounds, max |K~| into the handle
   double mx = 0.0;
   for (int t = tid; t < m + n; t += kTinySetupT) {
@@ -601,6 +636,7 @@ __global__ void __launch_bounds__(kTinySetupT) setup_tiny_kernel(const TinySetup
     A.trp[n] = nnz;
     *A.kmax = __longlong_as_double((long long)s_kmax);
   }
+  stamp(4);
   if (tid < 8) A.vflag[tid] = f[tid];
 }
 
@@ -779,6 +815,8 @@ int setup_tiny(DevProblem &P, const TinySetupSources &S, int64_t *rp64_dst, doub
   A.kv = P.kv; A.tkv = P.tkv; A.ls = P.ls; A.us = P.us; A.Dr = P.Dr; A.Dc = P.Dc; A.kmax = P.kmax;
   A.vflag = vflag;
   A.queue = queue;
+  // diagnostics: phase stamps into the tail of the (pinned, mapped) flag buffer
+  A.tstamp = getenv("MPAX_HOST_TRACE") ? vflag + 8 * kMaxSetupBlocks - 8 : nullptr;
   const size_t smem = tiny_setup_smem(P.m, P.n, P.nnz);
   MPAX_LAUNCH(setup_tiny_kernel, blocks, kTinySetupT, smem, s, A);
   MPAX_CHECK_LAUNCH();

@@ -30,7 +30,7 @@ struct TinyParams {
   int64_t batch;
   unsigned long long *queue, qbase;
   double *X, *Y, *L;
-  lp_result *res;
+  lp_result *res, *res_host;
 };
 
 template <int V>
@@ -328,28 +328,29 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       const bool acc = CS || (eta <= eb);
       const double eta_used = eta;
       if (!CS) eta = fmin(f1 * eb, f2 * eta);
-      if (__builtin_expect(!acc, 0)) {
-        if (++rejects >= 100) { status = LP_NUMERICAL_ERROR; outsel = 0; break; }
-        continue;
-      }
-      rejects = 0;
+      // the attempt's bookkeeping without branches (selects on acc); one rarely taken branch
+      // leaves the common path: 100 consecutive rejections, or an accepted step that is due a check
+      rejects = acc ? 0 : rejects + 1;
       double rP = 0.0;
       if (!R2) {
-        theta = theta_f;
-        if (__builtin_expect(!theta_ok, 0)) theta = div_rn_slow(eta_used, W1c);
-        W_ = W1c;
+        theta = acc ? theta_f : theta;
+        W_ = acc ? W1c : W_;
+        if (__builtin_expect(acc && !theta_ok, 0)) theta = div_rn_slow(eta_used, W1c);
       } else {
         // r_P is read only as the restart reference (k_in = 0) and as the check metric:
         // skip its division and square root on the other attempts (they sit on the
         // warp's in-order issue path)
-        if (k_in == 0 || k + 1 == next_check) rP = sqrt(fmax(0.0, M / eta_used - 2.0 * Iv));
-        if (k_in == 0) ref = rP;
-        ha = ha_n;
-        hb = hb_n;
+        if (acc && (k_in == 0 || k + 1 == next_check)) rP = sqrt(fmax(0.0, M / eta_used - 2.0 * Iv));
+        if (acc && k_in == 0) ref = rP;
+        ha = acc ? ha_n : ha;
+        hb = acc ? hb_n : hb;
       }
-      ++k;
-      ++k_in;
-      if (__builtin_expect(k != next_check, 1)) { pending = true; continue; }
+      k += acc;
+      k_in += acc;
+      pending = acc;
+      if (__builtin_expect(!(acc && k == next_check) && rejects < 100, 1)) continue;
+      if (rejects >= 100) { status = LP_NUMERICAL_ERROR; outsel = 0; break; }
+      pending = false;   // the check commits this step itself
       next_check = (next_check + P.check_freq < P.iter_limit) ? next_check + P.check_freq : P.iter_limit;
 
       // ================= step 5: check =================
@@ -570,6 +571,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         r.rel_kkt = kkt5_rel(ko, nq0, nc0);
         r.omega = omega; r.eta = eta; r.solve_seconds = 0.0;
         P.res[b] = r;
+        if (P.res_host) P.res_host[b] = r;   // pinned host memory, device-mapped (UVA): no copy-out
       }
     }
   }
@@ -627,7 +629,7 @@ int tiny_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
   P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active; P.rho = o.reflection;
   P.verbose = o.verbose; P.display_freq = o.display_frequency;
   P.batch = L.batch; P.queue = queue;
-  P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
+  P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res; P.res_host = L.res_host;
   const bool r2 = o.algorithm == LP_R2HPDHG, cs = o.step_rule == LP_STEP_CONSTANT;
   const int64_t n = D.n, m = D.m;
   const int W = D.max_row, WT = D.max_col;

@@ -1,12 +1,8 @@
 #!/bin/bash
-# C5 grid kernel: trace timings at MINB=1/2, then one ncu --set full capture (source-level).
+# ncu full capture (source-level) of the C5 grid kernel, after a plain run exits 0.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-MPAX_LIB=$GRAFT_REPO_ROOT/paper_2412_09734_b200/libmpax_b200_trace.so MPAX_GRID_MINB=1 PROF_M=5000000 PROF_K=64 \
-  timeout 300 python scripts/prof_grid.py > gpurun_out/p_c5_minb1.log 2>&1
-MPAX_LIB=$GRAFT_REPO_ROOT/paper_2412_09734_b200/libmpax_b200_trace.so PROF_M=5000000 PROF_K=64 \
-  timeout 300 python scripts/prof_grid.py > gpurun_out/p_c5_minb2.log 2>&1
-PROF_M=5000000 PROF_K=16 timeout 300 python scripts/prof_grid.py > gpurun_out/p_c5_plain.log 2>&1 || exit 1
-PROF_M=5000000 PROF_K=16 timeout 900 ncu --set full --clock-control none --import-source on -k regex:grid_kernel -c 1 \
-  -o gpurun_out/p_c5_grid python scripts/prof_grid.py > gpurun_out/p_c5_ncu.log 2>&1
-echo "ncu rc=$?" >> gpurun_out/p_c5_ncu.log
+PROF_M=5000000 PROF_K=16 timeout 600 python scripts/prof_grid.py > gpurun_out/prof_c5_plain.log 2>&1 || { echo "plain failed"; exit 1; }
+PROF_M=5000000 PROF_K=16 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:grid_kernel -s 1 -c 1 \
+  -o gpurun_out/prof_grid_c5${1:+_$1} python scripts/prof_grid.py > gpurun_out/ncu_grid_c5.log 2>&1
+echo "ncu rc=$?" >> gpurun_out/ncu_grid_c5.log
