@@ -107,7 +107,19 @@ __device__ __forceinline__ void gemm1(const Smem &S, int np, int mp, F &&f) {
     double d0 = 0.0, d1 = 0.0;
     const int j = jt * 8 + r;
     DCHK(j < np);
-    for (int kt = 0; kt < mp; kt += 4) {
+    int kt = 0;
+    // four k-steps' operands in flight before their DMMAs (the accumulation order is unchanged)
+    for (; kt + 16 <= mp; kt += 16) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = S.Ks[(kt + 4 * u + q) * np + j];     // A(j, i=kt+4u+q)
+        b[u] = S.Yf[(kt + 4 * u + q) * kS + r];     // B(i=kt+4u+q, s=r)
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma(d0, d1, a[u], b[u]);
+    }
+    for (; kt < mp; kt += 4) {
       DCHK(kt + q < mp);
       const double a = S.Ks[(kt + q) * np + j];        // A(j, i=kt+q)
       const double b = S.Yf[(kt + q) * kS + r];        // B(i=kt+q, s=r)
@@ -115,6 +127,38 @@ __device__ __forceinline__ void gemm1(const Smem &S, int np, int mp, F &&f) {
     }
     f(j, 2 * q, d0);
     f(j, 2 * q + 1, d1);
+  }
+}
+
+// GEMM1 whose epilogue operands are loaded before the k-loop (in flight during the DMMA chain):
+// pre(j, s) returns them, f(j, s, value, ops) consumes them.
+template <class Pre, class F>
+__device__ __forceinline__ void gemm1_pre(const Smem &S, int np, int mp, Pre &&pre, F &&f) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  for (int jt = w; jt * 8 < np; jt += kThreads / 32) {
+    double d0 = 0.0, d1 = 0.0;
+    const int j = jt * 8 + r;
+    auto o0 = pre(j, 2 * q);
+    auto o1 = pre(j, 2 * q + 1);
+    int kt = 0;
+    for (; kt + 16 <= mp; kt += 16) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = S.Ks[(kt + 4 * u + q) * np + j];
+        b[u] = S.Yf[(kt + 4 * u + q) * kS + r];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma(d0, d1, a[u], b[u]);
+    }
+    for (; kt < mp; kt += 4) {
+      const double a = S.Ks[(kt + q) * np + j];
+      const double b = S.Yf[(kt + q) * kS + r];
+      dmma(d0, d1, a, b);
+    }
+    f(j, 2 * q, d0, o0);
+    f(j, 2 * q + 1, d1, o1);
   }
 }
 
@@ -126,7 +170,18 @@ __device__ __forceinline__ void gemm2(const Smem &S, int np, int mp) {
     double d0 = 0.0, d1 = 0.0;
     const int i = it * 8 + r;
     DCHK(i < mp);
-    for (int kt = 0; kt < np; kt += 4) {
+    int kt = 0;
+    for (; kt + 16 <= np; kt += 16) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = S.Ks[i * np + kt + 4 * u + q];       // A(i, j=kt+4u+q)
+        b[u] = S.Xc[(kt + 4 * u + q) * kS + r];     // B(j=kt+4u+q, s=r)
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma(d0, d1, a[u], b[u]);
+    }
+    for (; kt < np; kt += 4) {
       DCHK(kt + q < np);
       const double a = S.Ks[i * np + kt + q];          // A(i, j=kt+q)
       const double b = S.Xc[(kt + q) * kS + r];        // B(j=kt+q, s=r)
@@ -442,66 +497,111 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
       if (all_done) break;
       // ---- phase A: GEMM1 = K~_c' Y' ; [commit n-side] ; primal step ; X'_c ----
       double dx_even = 0.0, dx_odd = 0.0;  // this lane's instances 2q and 2q+1 (GEMM1 fragment layout)
-      gemm1(S, np, mp, [&](int jj, int s, double kty) {
+      struct OpsA {
+        double x, kt, xp, xa, cs, ls, us, kta;
+      };
+      gemm1_pre(S, np, mp, [&](int jj, int s) {
+        OpsA o = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        const Inst &I = S.inst[s];
+        if (jj >= jn || I.done) return o;
+        const int j = j0 + jj;
+        const int64_t off = (b0 + s) * n + j;
+        o.x = P.x[off]; o.kt = P.KTy[off]; o.cs = P.cs[off]; o.ls = P.ls[j]; o.us = P.us[j];
+        if (I.pending) {
+          o.xp = P.xp[off]; o.xa = P.xa[off];
+          if (r2) o.kta = P.KTya[off];
+        }
+        return o;
+      }, [&](int jj, int s, double kty, const OpsA &op) {
         const Inst &I = S.inst[s];
         if (jj >= jn || I.done) { if (jj < np) S.Xc[jj * kS + s] = 0.0; return; }
         const int64_t b = b0 + s;
         const int j = j0 + jj;
         const int64_t o = b * n + j;
-        double xv = P.x[o], kt = P.KTy[o];
+        double xv = op.x, kt = op.kt;
         if (I.pending) {
-          const double xpv = P.xp[o];
+          const double xpv = op.xp;
           if (!r2) {
-            P.xa[o] += I.theta * (xpv - P.xa[o]);
+            P.xa[o] = op.xa + I.theta * (xpv - op.xa);
             xv = xpv; kt = kty;
           } else {
-            xv = I.ha * (rf1 * xpv - rf0 * xv) + I.hb * P.xa[o];
-            kt = I.ha * (rf1 * kty - rf0 * kt) + I.hb * P.KTya[o];
+            xv = I.ha * (rf1 * xpv - rf0 * xv) + I.hb * op.xa;
+            kt = I.ha * (rf1 * kty - rf0 * kt) + I.hb * op.kta;
           }
           P.x[o] = xv; P.KTy[o] = kt;
         }
         const double tau = I.eta * I.inv_omega;
-        const double xn = median3(P.ls[j], xv - tau * (P.cs[o] - kt), P.us[j]);
+        const double xn = median3(op.ls, xv - tau * (op.cs - kt), op.us);
         P.xp[o] = xn;
         S.Xc[jj * kS + s] = xn;
         const double d = xn - xv;
         if (s & 1) dx_odd += d * d; else dx_even += d * d;
       });
       __syncthreads();
+      // ---- phase B operands of this thread's first two row items, loaded before GEMM2 (in flight
+      // during it and the cluster barrier) ----
+      struct OpsB {
+        double y, kx, yp, kxp, ya, kxa, qs;
+      };
+      OpsB pb[2];
+      auto load_b = [&](int t) {
+        OpsB o = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        const int ii = t / kS, s = t % kS, i = i0 + ii;
+        const Inst &I = S.inst[s];
+        if (I.done) return o;
+        const int64_t off = (b0 + s) * m + i;
+        o.y = P.y[off]; o.kx = P.Kx[off]; o.qs = P.qs[off];
+        if (I.pending) {
+          o.yp = P.yp[off]; o.kxp = P.Kxp[off]; o.ya = P.ya[off];
+          if (r2) o.kxa = P.Kxa[off];
+        }
+        return o;
+      };
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int t = tid + u * kThreads;
+        if (t < in_ * kS) pb[u] = load_b(t);
+      }
       // ---- GEMM2: partial K~_c X'_c ----
       gemm2(S, np, mp);
       cl.sync();
       // ---- phase B: reduce K~x' for own rows; [commit m-side]; dual step ----
       double dy_own = 0.0, I_own = 0.0;  // instance tid % 8 (kThreads is a multiple of kS)
-      for (int t = tid; t < in_ * kS; t += kThreads) {
+      auto row_b = [&](int t, const OpsB &op) {
         const int ii = t / kS, s = t % kS, i = i0 + ii;
         const Inst &I = S.inst[s];
-        if (I.done) continue;
+        if (I.done) return;
         double kxp = 0.0;
         for (int c = 0; c < CL; ++c) kxp += cl.map_shared_rank(S.Pc, c)[i * kS + s];
         const int64_t b = b0 + s;
         const int64_t o = b * m + i;
-        double yv = P.y[o], kxv = P.Kx[o];
+        double yv = op.y, kxv = op.kx;
         if (I.pending) {
-          const double ypv = P.yp[o], kxpo = P.Kxp[o];
+          const double ypv = op.yp, kxpo = op.kxp;
           if (!r2) {
-            P.ya[o] += I.theta * (ypv - P.ya[o]);
+            P.ya[o] = op.ya + I.theta * (ypv - op.ya);
             yv = ypv; kxv = kxpo;
           } else {
-            yv = I.ha * (rf1 * ypv - rf0 * yv) + I.hb * P.ya[o];
-            kxv = I.ha * (rf1 * kxpo - rf0 * kxv) + I.hb * P.Kxa[o];
+            yv = I.ha * (rf1 * ypv - rf0 * yv) + I.hb * op.ya;
+            kxv = I.ha * (rf1 * kxpo - rf0 * kxv) + I.hb * op.kxa;
           }
           P.y[o] = yv; P.Kx[o] = kxv;
         }
         const double sigma = I.eta * I.omega;
-        double yn = yv + sigma * (P.qs[o] - 2.0 * kxp + kxv);
+        double yn = yv + sigma * (op.qs - 2.0 * kxp + kxv);
         if (i < m1) yn = fmax(yn, 0.0);
         P.yp[o] = yn; P.Kxp[o] = kxp;
         S.Yf[i * kS + s] = yn;
         const double d = yn - yv;
         dy_own += d * d;
         I_own += d * (kxp - kxv);
+      };
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int t = tid + u * kThreads;
+        if (t < in_ * kS) row_b(t, pb[u]);
       }
+      for (int t = tid + 2 * kThreads; t < in_ * kS; t += kThreads) row_b(t, load_b(t));
       S.part = (S.part == S.part_a) ? S.part_b : S.part_a;
       attempt_partials(dx_even, dx_odd, dy_own, I_own, S);
       cl.sync();
