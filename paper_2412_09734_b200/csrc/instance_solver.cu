@@ -678,6 +678,8 @@ int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunc
       while (NW < 32 && NW < want) NW *= 2;
     }
     if (const char *e = getenv("MPAX_INST_NW")) NW = atoi(e);
+    if (NW == 2) NW = 4;              // the instantiated CTA sizes: 1, 4, 8, 16, 32 warps
+    if (NW > 16 && NW != 32) NW = 32;
   }
   P.gk = pow2_floor(D.avg_row / 4.0);
   P.gkt = pow2_floor(D.avg_col / 4.0);

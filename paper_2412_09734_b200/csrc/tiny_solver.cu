@@ -1,8 +1,9 @@
 // tiny_solver.cu -- register-resident per-instance PDHG for very small LPs
 // (the paper's batched shortest-path LPs, P:334,
-// P:156-157).  One warp owns one instance; lane l owns rows i = l + 32t
-// (t < RPT) and columns j = l + 32t (t < CPT) together with their ELL rows of
-// K~ (width W) and K~' (width WT).  Every per-row / per-column quantity of the
+// P:156-157; and C1-sized single LPs).  NT threads own one instance (NT = 32: one warp, the
+// C2 batches; NT = 64..256: a CTA, for LPs up to NT*RPT rows / NT*CPT columns); thread l
+// owns rows i = l + NT t (t < RPT) and columns j = l + NT t (t < CPT) together with their
+// ELL rows of K~ (width W) and K~' (width WT).  Every per-row / per-column quantity of the
 // iteration (x, K~'y, x', average / anchor, restart point, c~, l~, u~ and the
 // m-side analogues) lives in registers; only the two vectors that are
 // gathered by the SpMVs (x' and y', and the average at checks) go through
@@ -33,6 +34,15 @@ struct TinyParams {
   lp_result *res, *res_host;
 };
 
+// Barrier of the instance's threads: the warp, or the CTA.
+template <int NT>
+__device__ __forceinline__ void isync() {
+  if (NT == 32) __syncwarp();
+  else __syncthreads();
+}
+
+constexpr int kRedV = 24;  // the largest reduction (raPDHG check)
+
 template <int V>
 __device__ __forceinline__ void wsum(double (&v)[V]) {
 #pragma unroll
@@ -55,16 +65,42 @@ __device__ __forceinline__ void wmax(double (&v)[V]) {
   }
 }
 
+// Sum (MX = false) or max over the instance's NT threads, every thread getting the total: the
+// warp butterfly, then (NT > 32) the warps' partials through shared memory in warp order --
+// fixed order, deterministic.  `red` holds 2 x (NT / 32) x kRedV doubles; `rb` alternates
+// between its halves, so a buffer is rewritten only after an intervening barrier.
+template <int NT, bool MX, int V>
+__device__ __forceinline__ void ired(double (&v)[V], double *red, int &rb) {
+  if (MX) wmax<V>(v); else wsum<V>(v);
+  if (NT == 32) return;
+  double *buf = red + rb * (NT / 32) * kRedV;
+  rb ^= 1;
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) buf[w * kRedV + k] = v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    double s = buf[k];
+    for (int ww = 1; ww < NT / 32; ++ww) s = MX ? fmax(s, buf[ww * kRedV + k]) : s + buf[ww * kRedV + k];
+    v[k] = s;
+  }
+}
+
 
 // CS: constant step rule (eta = 0.998 / sigma_max(K~), every attempt accepted; DESIGN.md
 // reading 34) -- the line-search reductions are then needed only where r2HPDHG uses
 // r_P (restart reference at k_in = 0 and the check), and never for raPDHG.
-template <bool R2, bool CS, int RPT, int CPT, int W, int WT>
-__global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
+template <bool R2, bool CS, int NT, int RPT, int CPT, int W, int WT>
+__global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
   extern __shared__ __align__(16) double sm[];
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x;   // the thread's index within its instance (0 .. NT-1)
   const int n = P.n, m = P.m, m1 = P.m1;
-  double *sx = sm, *sy = sm + 32 * CPT;  // gather buffers: x' (or average) and y' (or average)
+  double *sx = sm, *sy = sm + NT * CPT;  // gather buffers: x' (or average) and y' (or average)
+  double *red = sy + NT * RPT;           // cross-warp reduction scratch (NT > 32)
+  int rb = 0;
   // ---- static per-lane structure: ELL rows of K~ and K~' in registers ----
   int rcol[RPT][W], ccol[CPT][WT];
   double rval[RPT][W], cval[CPT][WT];
@@ -72,7 +108,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
   double dr[RPT], lsv[CPT], usv[CPT], dc[CPT];
 #pragma unroll
   for (int t = 0; t < RPT; ++t) {
-    const int i = lane + 32 * t;
+    const int i = lane + NT * t;
     rok[t] = i < m;
     const int a = rok[t] ? P.rp[i] : 0, e = rok[t] ? P.rp[i + 1] : 0;
 #pragma unroll
@@ -85,7 +121,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
   }
 #pragma unroll
   for (int t = 0; t < CPT; ++t) {
-    const int j = lane + 32 * t;
+    const int j = lane + NT * t;
     cok[t] = j < n;
     const int a = cok[t] ? P.trp[j] : 0, e = cok[t] ? P.trp[j + 1] : 0;
 #pragma unroll
@@ -99,8 +135,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
     usv[t] = cok[t] ? P.us[j] : 0.0;
   }
   // padding entries point at element 0 with value 0; keep the gather buffers finite
-  for (int t = lane; t < 32 * CPT; t += 32) sx[t] = 0.0;
-  for (int t = lane; t < 32 * RPT; t += 32) sy[t] = 0.0;
+  for (int t = lane; t < NT * CPT; t += NT) sx[t] = 0.0;
+  for (int t = lane; t < NT * RPT; t += NT) sy[t] = 0.0;
   const double eta0 = initial_eta(P.kmax, P.sigma, CS);
   // r2HPDHG reflection z <- a((1 + rho) w - rho z) + b z0 (rho = 1: 2 PDHG(z) - z; reading 38)
   const double rf1 = 1.0 + P.rho, rf0 = P.rho;
@@ -112,9 +148,9 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
   __shared__ unsigned long long s_inst;
 
   for (;;) {
-    __syncwarp();
+    isync<NT>();
     if (lane == 0) s_inst = atomicAdd(P.queue, 1ull) - P.qbase;
-    __syncwarp();
+    isync<NT>();
     const int64_t b = (int64_t)s_inst;
     if (b >= P.batch) return;
     if (P.active && P.active[b].status != LP_OPTIMAL) continue;  // polishing: main solve not OPTIMAL
@@ -126,7 +162,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
     double v4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int t = 0; t < CPT; ++t) {
-      const int j = lane + 32 * t;
+      const int j = lane + NT * t;
       const double c = cok[t] ? c0[j] : 0.0;
       cs[t] = c * dc[t];
       v4[0] += cs[t] * cs[t];
@@ -137,7 +173,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
     }
 #pragma unroll
     for (int t = 0; t < RPT; ++t) {
-      const int i = lane + 32 * t;
+      const int i = lane + NT * t;
       const double q = rok[t] ? q0[i] : 0.0;
       qs[t] = q * dr[t];
       v4[1] += qs[t] * qs[t];
@@ -147,8 +183,8 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       y[t] = rok[t] ? yv : 0.0;
       sy[i] = y[t];
     }
-    wsum<4>(v4);
-    __syncwarp();
+    ired<NT, false>(v4, red, rb);
+    isync<NT>();
     const double nc0 = sqrt(v4[2]), nq0 = sqrt(v4[3]);
     double omega = 1.0;
     if (sqrt(v4[0]) > 1e-10 && sqrt(v4[1]) > 1e-10) omega = sqrt(v4[0]) / sqrt(v4[1]);
@@ -164,7 +200,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
 #pragma unroll
         for (int w = 0; w < W; ++w) s += rval[t][w] * sx[rcol[t][w]];
         Kx[t] = s; Kxa[t] = s; ya[t] = y[t]; yr[t] = y[t];
-        if (rok[t]) kkt_row_acc(v, false, lane + 32 * t < m1, 1.0, y[t], s, 0.0, qs[t]);
+        if (rok[t]) kkt_row_acc(v, false, lane + NT * t < m1, 1.0, y[t], s, 0.0, qs[t]);
       }
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {
@@ -174,7 +210,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         KTy[t] = s; KTya[t] = s; xa[t] = x[t]; xr[t] = x[t];
         if (cok[t]) kkt_col_acc(v, false, 1.0, x[t], s, 0.0, cs[t], 0.0, lsv[t], 0.0, usv[t]);
       }
-      wsum<4>(v);
+      ired<NT, false>(v, red, rb);
       if (!R2) {
         const Kkt5 ks = kkt5(v);
         ref = kkt_omega(ks, omega, inv_omega);
@@ -206,7 +242,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       double *X = P.X + bi * (int64_t)n, *L = P.L + bi * (int64_t)n, *Y = P.Y + bi * (int64_t)m;
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {
-        const int j = lane + 32 * t;
+        const int j = lane + NT * t;
         if (cok[t]) {
           X[j] = dc[t] * (x[t] - xb[t]) / nx;
           L[j] = -((KTy[t] - KTyb[t]) / dc[t]) / ny;
@@ -214,15 +250,15 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       }
 #pragma unroll
       for (int t = 0; t < RPT; ++t) {
-        const int i = lane + 32 * t;
+        const int i = lane + NT * t;
         if (rok[t]) Y[i] = dr[t] * (y[t] - yb[t]) / ny;
       }
     };
 
     // Shared-memory hazards of the attempt loop: every write of sx (phase A) / sy (phase B) is
-    // separated from the previous reads of that buffer by one of the loop's two __syncwarp()s
+    // separated from the previous reads of that buffer by one of the loop's two instance barriers (isync)
     // (after phase A, after phase B); the check path ends with its own.
-    __syncwarp();
+    isync<NT>();
     for (;;) {
       // ================= phase A: [commit n-side] + primal step =================
       // Branch-free: the commit is computed every attempt and selected by `pending`
@@ -272,13 +308,13 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         }
         const double xn = median3(lsv[t], x[t] - tau * (cs[t] - KTy[t]), usv[t]);
         xp[t] = cok[t] ? xn : 0.0;
-        sx[lane + 32 * t] = xp[t];
+        sx[lane + NT * t] = xp[t];
         const double d = xp[t] - x[t];
         dx2 += d * d;
       }
       double vdx[1] = {dx2};
-      if (need) wsum<1>(vdx);  // ||dx||^2: its butterfly overlaps phase B
-      __syncwarp();
+      if (NT == 32 && need) wsum<1>(vdx);  // ||dx||^2: its butterfly overlaps phase B (one warp)
+      isync<NT>();
       // ================= phase B: [commit m-side] + SpMV #1 + dual step =================
       double dy2 = 0.0, I = 0.0;
 #pragma unroll
@@ -298,19 +334,27 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         }
         // q~ - 2 K~x' as one fma: 2 s is exact, so this is the oracle's q~ - 2.0 * s, one op shorter
         double yn = y[t] + sigma * (fma(-2.0, s, qs[t]) + Kx[t]);
-        if (lane + 32 * t < m1) yn = fmax(yn, 0.0);
+        if (lane + NT * t < m1) yn = fmax(yn, 0.0);
         yp[t] = rok[t] ? yn : 0.0;
         Kxp[t] = rok[t] ? s : 0.0;
-        sy[lane + 32 * t] = yp[t];
+        sy[lane + NT * t] = yp[t];
         const double d = yp[t] - y[t];
         dy2 += d * d;
         I += d * (Kxp[t] - Kx[t]);
       }
       pending = false;
       double v3[2] = {dy2, I};
-      if (need) wsum<2>(v3);  // ||dy||^2, <dy, K dx>
+      if (need) {  // ||dy||^2, <dy, K dx> (and ||dx||^2 for a CTA instance)
+        if (NT == 32) {
+          wsum<2>(v3);
+        } else {
+          double v3x[3] = {vdx[0], v3[0], v3[1]};
+          ired<NT, false>(v3x, red, rb);
+          vdx[0] = v3x[0]; v3[0] = v3x[1]; v3[1] = v3x[2];
+        }
+      }
       // K~'y' for the next attempt's commit (and this one's check), overlapping the butterfly
-      __syncwarp();
+      isync<NT>();
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {
         double s = 0.0;
@@ -354,7 +398,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       next_check = (next_check + P.check_freq < P.iter_limit) ? next_check + P.check_freq : P.iter_limit;
 
       // ================= step 5: check =================
-      __syncwarp();
+      isync<NT>();
       // infeasibility rays (reading 35): raPDHG from the point before this step (xo ...),
       // r2HPDHG from the epoch's Halpern anchor (xa ...)
       CertAcc cacc;
@@ -392,7 +436,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         for (int q = 0; q < 10; ++q) v[q] = 0.0;
 #pragma unroll
         for (int t = 0; t < CPT; ++t) {
-          const int j = lane + 32 * t;
+          const int j = lane + NT * t;
           if (cok[t]) {
             const double l0j = P.l0[j], u0j = P.u0[j];
             kkt_col_acc(v, true, dc[t], xp[t], KTyp[t], c0[j], cs[t], l0j, lsv[t], u0j, usv[t]);
@@ -403,7 +447,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         }
 #pragma unroll
         for (int t = 0; t < RPT; ++t) {
-          const int i = lane + 32 * t;
+          const int i = lane + NT * t;
           if (rok[t]) {
             kkt_row_acc(v, true, i < m1, dr[t], yp[t], Kxp[t], q0[i], qs[t]);
             const double d = yp[t] - yr[t];
@@ -412,14 +456,14 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           }
         }
         v[6] = cacc.sy; v[7] = cacc.sx; v[8] = cacc.oy; v[9] = cacc.ox;
-        wsum<10>(v);
+        ired<NT, false>(v, red, rb);
         const Kkt5 kw = kkt5(v);
         if (lane == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
           verbose_line(b, k, kw.pobj, kw.dobj, kw.pres, kw.dres, kw.gap, omega, eta);
         if (tpass(kw, nq0, nc0)) { status = LP_OPTIMAL; outsel = 1; break; }
         {
           double mv[2] = {cacc.vy, cacc.vx};
-          wmax<2>(mv);
+          ired<NT, true>(mv, red, rb);
           CertAcc tot;
           tot.sy = v[6]; tot.sx = v[7]; tot.oy = v[8]; tot.ox = v[9]; tot.vy = mv[0]; tot.vx = mv[1];
           double ny, nx;
@@ -433,12 +477,12 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         metric = rP; dx2c = v[4]; dy2c = v[5]; csel = 1;
       } else {
         // the average's products: K~ x-bar and K~' y-bar through the gather buffers
-        __syncwarp();
+        isync<NT>();
 #pragma unroll
-        for (int t = 0; t < CPT; ++t) sx[lane + 32 * t] = cok[t] ? xa[t] : 0.0;
+        for (int t = 0; t < CPT; ++t) sx[lane + NT * t] = cok[t] ? xa[t] : 0.0;
 #pragma unroll
-        for (int t = 0; t < RPT; ++t) sy[lane + 32 * t] = rok[t] ? ya[t] : 0.0;
-        __syncwarp();
+        for (int t = 0; t < RPT; ++t) sy[lane + NT * t] = rok[t] ? ya[t] : 0.0;
+        isync<NT>();
         double v[24];
 #pragma unroll
         for (int q = 0; q < 24; ++q) v[q] = 0.0;
@@ -448,7 +492,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
 #pragma unroll
           for (int w = 0; w < W; ++w) s += rval[t][w] * sx[rcol[t][w]];
           Kxa[t] = rok[t] ? s : 0.0;
-          const int i = lane + 32 * t;
+          const int i = lane + NT * t;
           if (rok[t]) {
             const bool ge = i < m1;
             const double q0i = q0[i];
@@ -468,7 +512,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
 #pragma unroll
           for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
           KTya[t] = cok[t] ? s : 0.0;
-          const int j = lane + 32 * t;
+          const int j = lane + NT * t;
           if (cok[t]) {
             const double c0j = c0[j], l0j = P.l0[j], u0j = P.u0[j];
             kkt_col_acc(v + 0, true, dc[t], xa[t], s, c0j, cs[t], l0j, lsv[t], u0j, usv[t]);
@@ -482,7 +526,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           }
         }
         v[20] = cacc.sy; v[21] = cacc.sx; v[22] = cacc.oy; v[23] = cacc.ox;
-        wsum<24>(v);
+        ired<NT, false>(v, red, rb);
         const Kkt5 ka = kkt5(v + 0), kc = kkt5(v + 4);
         if (lane == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
           verbose_line(b, k, kc.pobj, kc.dobj, kc.pres, kc.dres, kc.gap, omega, eta);
@@ -490,7 +534,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         if (tpass(kc, nq0, nc0)) { status = LP_OPTIMAL; outsel = 0; break; }
         {
           double mv[2] = {cacc.vy, cacc.vx};
-          wmax<2>(mv);
+          ired<NT, true>(mv, red, rb);
           CertAcc tot;
           tot.sy = v[20]; tot.sx = v[21]; tot.oy = v[22]; tot.ox = v[23]; tot.vy = mv[0]; tot.vx = mv[1];
           double ny, nx;
@@ -530,7 +574,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
         k_in = 0;
         if (!R2) { W_ = 0.0; ref = metric; }
       }
-      __syncwarp();  // the check's gathers of sx / sy before the next phase A writes sx
+      isync<NT>();  // the check's gathers of sx / sy before the next phase A writes sx
     }
 
     // ---- step 6: output (candidate selected by outsel) ----
@@ -539,7 +583,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       double *X = P.X + b * (int64_t)n, *L = P.L + b * (int64_t)n, *Y = P.Y + b * (int64_t)m;
 #pragma unroll
       for (int t = 0; t < CPT; ++t) {
-        const int j = lane + 32 * t;
+        const int j = lane + NT * t;
         if (cok[t]) {
           const double xs = outsel ? (R2 ? xp[t] : xa[t]) : x[t];
           const double kt = outsel ? (R2 ? KTyp[t] : KTya[t]) : KTy[t];
@@ -552,7 +596,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
       }
 #pragma unroll
       for (int t = 0; t < RPT; ++t) {
-        const int i = lane + 32 * t;
+        const int i = lane + NT * t;
         if (rok[t]) {
           const double ys = outsel ? (R2 ? yp[t] : ya[t]) : y[t];
           const double kx = outsel ? (R2 ? Kxp[t] : Kxa[t]) : Kx[t];
@@ -560,7 +604,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
           if (!rays) Y[i] = dr[t] * ys;
         }
       }
-      wsum<4>(v);
+      ired<NT, false>(v, red, rb);
       if (lane == 0) {
         const Kkt5 ko = kkt5(v);
         lp_result r;
@@ -577,9 +621,10 @@ __global__ void __launch_bounds__(32) tiny_kernel(const TinyParams P) {
   }
 }
 
-template <bool R2, bool CS, int RPT, int CPT, int W, int WT>
+template <bool R2, bool CS, int NT, int RPT, int CPT, int W, int WT>
 int launch_tiny(TinyParams P, cudaStream_t s, unsigned long long *qbase) {
-  const size_t smem = (size_t)32 * (CPT + RPT) * sizeof(double);
+  const size_t smem = (size_t)NT * (CPT + RPT) * sizeof(double) +
+                      (NT > 32 ? (size_t)2 * (NT / 32) * kRedV * sizeof(double) : 0);
   // occupancy of this instantiation: queried once per process (a small batch's solve is short
   // enough for the driver queries to show)
   static int sms = 0, per_sm = 0;
@@ -587,7 +632,7 @@ int launch_tiny(TinyParams P, cudaStream_t s, unsigned long long *qbase) {
     int dev = 0, s_ = 0, p_ = 0;
     MPAX_CUDA(cudaGetDevice(&dev));
     MPAX_CUDA(cudaDeviceGetAttribute(&s_, cudaDevAttrMultiProcessorCount, dev));
-    MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p_, tiny_kernel<R2, CS, RPT, CPT, W, WT>, 32, smem));
+    MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p_, tiny_kernel<R2, CS, NT, RPT, CPT, W, WT>, NT, smem));
     sms = s_;
     per_sm = p_ < 1 ? 1 : p_;
   }
@@ -599,17 +644,19 @@ int launch_tiny(TinyParams P, cudaStream_t s, unsigned long long *qbase) {
   } else {
     P.qbase = *qbase;
   }
-  MPAX_LAUNCH((tiny_kernel<R2, CS, RPT, CPT, W, WT>), (int)grid, 32, smem, s, P);
+  MPAX_LAUNCH((tiny_kernel<R2, CS, NT, RPT, CPT, W, WT>), (int)grid, NT, smem, s, P);
   MPAX_CHECK_LAUNCH();
-  // every warp ends on one ticket past the batch: the launch consumes batch + grid tickets
+  // every CTA ends on one ticket past the batch: the launch consumes batch + grid tickets
   if (qbase) *qbase = P.qbase + (unsigned long long)P.batch + (unsigned long long)grid;
   return LP_OK;
 }
 
-template <int RPT, int CPT, int W, int WT>
+template <int NT, int RPT, int CPT, int W, int WT>
 int launch_alg(const TinyParams &P, bool r2, bool cs, cudaStream_t s, unsigned long long *qb) {
-  if (cs) return r2 ? launch_tiny<true, true, RPT, CPT, W, WT>(P, s, qb) : launch_tiny<false, true, RPT, CPT, W, WT>(P, s, qb);
-  return r2 ? launch_tiny<true, false, RPT, CPT, W, WT>(P, s, qb) : launch_tiny<false, false, RPT, CPT, W, WT>(P, s, qb);
+  if (cs) return r2 ? launch_tiny<true, true, NT, RPT, CPT, W, WT>(P, s, qb)
+                    : launch_tiny<false, true, NT, RPT, CPT, W, WT>(P, s, qb);
+  return r2 ? launch_tiny<true, false, NT, RPT, CPT, W, WT>(P, s, qb)
+            : launch_tiny<false, false, NT, RPT, CPT, W, WT>(P, s, qb);
 }
 
 }  // namespace
@@ -635,9 +682,14 @@ int tiny_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
   const int W = D.max_row, WT = D.max_col;
   // ELL widths as tight as the LP allows: a padded slot is a zero-valued FMA on the attempt's
   // dependent chain (C2, the 5x5 grid: every column of K has exactly two entries)
-  if (m <= 32 && n <= 64 && W <= 4 && WT <= 2) return launch_alg<1, 2, 4, 2>(P, r2, cs, s, qbase);
-  if (m <= 32 && n <= 64 && W <= 4 && WT <= 4) return launch_alg<1, 2, 4, 4>(P, r2, cs, s, qbase);
-  if (m <= 32 && n <= 64 && W <= 8 && WT <= 8) return launch_alg<1, 2, 8, 8>(P, r2, cs, s, qbase);
+  if (m <= 32 && n <= 64 && W <= 4 && WT <= 2) return launch_alg<32, 1, 2, 4, 2>(P, r2, cs, s, qbase);
+  if (m <= 32 && n <= 64 && W <= 4 && WT <= 4) return launch_alg<32, 1, 2, 4, 4>(P, r2, cs, s, qbase);
+  if (m <= 32 && n <= 64 && W <= 8 && WT <= 8) return launch_alg<32, 1, 2, 8, 8>(P, r2, cs, s, qbase);
+  // a CTA per instance for larger small LPs (C1: 50 x 100, rows <= 11, columns <= 12 entries)
+  if (m <= 128 && n <= 128 && W <= 12 && WT <= 12) return launch_alg<128, 1, 1, 12, 12>(P, r2, cs, s, qbase);
+  if (m <= 128 && n <= 128 && W <= 16 && WT <= 16) return launch_alg<128, 1, 1, 16, 16>(P, r2, cs, s, qbase);
+  // Warcraft-shaped SPO+ LPs (k = 12: 144 x 1012, rows <= 16, columns <= 2 entries)
+  if (m <= 256 && n <= 1024 && W <= 16 && WT <= 2) return launch_alg<256, 1, 4, 16, 2>(P, r2, cs, s, qbase);
   return LP_ERR_UNSUPPORTED;
 }
 

@@ -33,12 +33,16 @@ def step():
 for _ in range(10):
     step()
 st = torch.cuda.current_stream()
+# C2_FLUSH=1: evict L2 between steps (outside the event pair), as bench.py's timed region does
+flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev) if os.environ.get("C2_FLUSH") else None
 ts, ss = [], []
 for _ in range(int(os.environ.get("C2_REPS", 300))):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if flush is not None:
+        flush.zero_()
     a.record(st); r = step(); b.record(st); torch.cuda.synchronize()
     ts.append(a.elapsed_time(b)); ss.append(float(r["solve_seconds"][0]) * 1e3)
 att = int(r["attempts"].max())
-print(f"{os.path.basename(os.environ.get('MPAX_LIB', 'default')):12s} {alg} step {np.median(ts):.4f} ms (min {np.min(ts):.4f})  "
+print(f"{os.path.basename(os.environ.get('MPAX_LIB', 'default')):12s} {'cold' if flush is not None else 'warm'} {alg} step {np.median(ts):.4f} ms (min {np.min(ts):.4f})  "
       f"solve {np.median(ss):.4f} ms  LPs/s {B / np.median(ts) * 1e3:.0f}  max it {r['iterations'].max()}  "
       f"max att {att} (instance {int(np.argmax(r['attempts']))})  us/att {np.median(ss) * 1e3 / att:.3f}  sum att {r['attempts'].sum()}", flush=True)
