@@ -445,10 +445,46 @@ def spmv_pair_leg(mp, torch, dev, prob, lp, hbm, reps=20):
         t_pair = e0.elapsed_time(e1) / reps * 1e-3
     b_pair = 24 * lp.nnz + 4 * (lp.m + 1) + 4 * (lp.n + 1) + 8 * lp.n + 8 * lp.m
     gf = gather_floor_us(lp.n, lp.m, lp.nnz, "ra", hbm)
+    cus = cusparse_pair_us(torch, dev, lp, reps)
     return {"us": t_pair * 1e6, "algorithmic_bytes": b_pair, "gbs": b_pair / t_pair / 1e9,
+            "cusparse_yardstick": cus,
             "gather_floor_us": gf[1] if gf else None, "frac_of_gather_floor": gf[1] / (t_pair * 1e6) if gf else None,
             "frac_of_hbm": b_pair / t_pair / 1e9 / hbm, "kernel": "spmv_kernel (standalone; K~x over the two column halves when split, K~'w)",
             "note": "random-column gathers move 32-byte sectors for 8 useful bytes (DESIGN.md §6)"}
+
+
+def cusparse_pair_us(torch, dev, lp, reps=20):
+    """Library yardstick for the SpMV pair: the same sparsity pattern as
+    two fp64 CSR matrices (K and its explicit transpose, int32 indices) multiplied by torch's
+    sparse CSR matvec, which calls cuSPARSE SpMV. Not on the product path; None if torch's
+    sparse build refuses."""
+    try:
+        rp = torch.from_numpy(lp.row_ptr.astype(np.int32)).to(dev)
+        ci = torch.from_numpy(lp.col_idx.astype(np.int32)).to(dev)
+        va = torch.from_numpy(lp.val).to(dev)
+        K = torch.sparse_csr_tensor(rp, ci, va, size=(lp.m, lp.n))
+        Kt = K.to_sparse_csc()   # CSC of K = CSR of K'
+        Kt = torch.sparse_csr_tensor(Kt.ccol_indices().to(torch.int32), Kt.row_indices().to(torch.int32),
+                                     Kt.values(), size=(lp.n, lp.m))
+        v = torch.rand(lp.n, 1, dtype=torch.float64, device=dev)
+        w = torch.rand(lp.m, 1, dtype=torch.float64, device=dev)
+        for _ in range(3):
+            K @ v, Kt @ w
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            K @ v
+            Kt @ w
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / reps * 1e3
+        del K, Kt, rp, ci, va
+        torch.cuda.empty_cache()
+        return {"us": us, "library": "cuSPARSE SpMV via torch.sparse_csr_tensor @ dense (fp64, int32 CSR, "
+                "unscaled K and an explicit K' CSR; output allocation included)"}
+    except (RuntimeError, TypeError) as e:
+        return {"us": None, "error": str(e).splitlines()[0][:160]}
 
 
 def _fp64_peak(key, sm_max):
@@ -506,13 +542,14 @@ def gather_floor_us(n, m, nnz, alg, hbm):
     return pair + upd, pair
 
 
-def attempt_bytes(n, m, nnz, alg):
+def attempt_bytes(n, m, nnz, alg, elem=8):
     """Algorithmic bytes of one accepted attempt of the grid path (DESIGN.md §6,
-    SURVEY §8(d) d.2): the SpMV pair streams K~ and K~' once (12 B per entry each)
-    plus their int32 row pointers and gathers x' and y' once; the fused updates
-    move 64n + 56m (raPDHG) or 88n + 88m (r2HPDHG) bytes."""
-    pair = 24 * nnz + 4 * (m + 1) + 4 * (n + 1) + 8 * n + 8 * m
-    upd = 64 * n + 56 * m if alg == "ra" else 88 * n + 88 * m
+    SURVEY §8(d) d.2): the SpMV pair streams K~ and K~' once (4-byte index + elem-byte value
+    per entry each) plus their int32 row pointers and gathers x' and y' once; the fused updates
+    move 8n + 7m (raPDHG) or 11n + 11m (r2HPDHG) vector elements.  elem = 8 (fp64) or 4 (fp32
+    storage, reading 39)."""
+    pair = 2 * (4 + elem) * nnz + 4 * (m + 1) + 4 * (n + 1) + elem * (n + m)
+    upd = elem * (8 * n + 7 * m if alg == "ra" else 11 * n + 11 * m)
     return pair, pair + upd
 
 
@@ -577,20 +614,16 @@ def oracle_large_baseline(lp, alg, full, label):
                 "sample": f"one full {label} solve ({r['iterations']} iterations, {r['attempts']} attempts), "
                           f"setup included", "iterations": int(r["iterations"]), "attempts": int(r["attempts"]),
                 "us_per_attempt_incl_setup": t * 1e6 / max(1, r["attempts"])}
-    t0 = time.perf_counter()
-    r1 = oracle.solve(lp, alg, iteration_limit=1, eps_abs=0.0, eps_rel=0.0)
-    t1 = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    r3 = oracle.solve(lp, alg, iteration_limit=3, eps_abs=0.0, eps_rel=0.0)
-    t3 = time.perf_counter() - t0
-    per = (t3 - t1) / max(1, r3["attempts"] - r1["attempts"])
+    r = oracle.solve(lp, alg, iteration_limit=3, eps_abs=0.0, eps_rel=0.0)
+    setup_s, solve_s = oracle.last_timing()
+    per = solve_s / max(1, r["attempts"])
     return {"kind": "oracle", "cores": cores, "unit": "us_per_attempt", "value": per * 1e6,
-            "setup_s": t1 - per * r1["attempts"], "cpu_model": _cpu_model(),
-            "sample": f"{label}: oracle solves of 1 and 3 accepted steps; per-attempt time = difference / "
-                      "attempt difference (setup cancels)"}
+            "setup_s": setup_s, "cpu_model": _cpu_model(),
+            "sample": f"{label}: one oracle solve of 3 accepted steps ({r['attempts']} attempts); per-attempt time = "
+                      "its iteration phase / attempts (the oracle's setup timed apart)"}
 
 
-def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4", reps=3, cpu=False):
+def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4", reps=3, cpu=False, fp32=True):
     """One large random sparse LP (C4 = G-RAND(1e5, 2e5, 20, seed 4); C5 = G-RAND(5e6, 1e7,
     20, seed 5)) solved to 1e-4 on the whole-GPU grid path: time to tolerance and the
     achieved algorithmic GB/s of the fused SpMV-pair + update loop."""
@@ -610,30 +643,39 @@ def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4"
     hbm = peaks.get("hbm_gbs", 6546.6)
     if lp.m >= 1_000_000:   # at C4 a pair is ~10 us of GPU time, below the binding's per-call host cost
         out["spmv_pair"] = spmv_pair_leg(mp, torch, dev, prob, lp, hbm)
-    for alg in ("ra", "r2"):
+    runs = [(a, "fp64") for a in ("ra", "r2")] + ([(a, "fp32") for a in ("ra", "r2")] if fp32 else [])
+    for alg, prec in runs:
+        key = alg if prec == "fp64" else f"{alg}_fp32"
         with mp.Solver(prob) as s:
-            log(f"large leg {alg}: warm-up")
-            s.solve(algorithm=alg, path=mp.PATH_GRID, iteration_limit=20_000)   # warm-up
+            log(f"large leg {key}: warm-up")
+            s.solve(algorithm=alg, path=mp.PATH_GRID, iteration_limit=20_000, precision=prec)   # warm-up
             best = None
             for _ in range(reps):
-                r = s.solve(algorithm=alg, path=mp.PATH_GRID, iteration_limit=20_000)
+                r = s.solve(algorithm=alg, path=mp.PATH_GRID, iteration_limit=20_000, precision=prec)
                 best = r if best is None or r["solve_seconds"] < best["solve_seconds"] else best
-        pair, acc = attempt_bytes(lp.n, lp.m, lp.nnz, alg)
+        pair, acc = attempt_bytes(lp.n, lp.m, lp.nnz, alg, 8 if prec == "fp64" else 4)
         rej = best["attempts"] - best["iterations"]
         byts = best["iterations"] * acc + rej * (pair // 2)
         t = best["solve_seconds"]
         gbs = byts / t / 1e9
-        out[alg] = {"status_optimal": best["status"] == mp.LP_OPTIMAL, "time_ms": t * 1e3,
+        out[key] = {"status_optimal": best["status"] == mp.LP_OPTIMAL, "time_ms": t * 1e3,
                     "iterations": best["iterations"], "attempts": best["attempts"], "restarts": best["restarts"],
                     "rel_kkt": best["rel_kkt"], "objective_rel_err": abs(best["primal_objective"] - lp.obj_star)
                     / (1 + abs(lp.obj_star)), "us_per_attempt": t * 1e6 / best["attempts"],
                     "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
-                                 "traffic": _traffic("grid_kernel_c5" if lp.m >= 1_000_000 else "grid_kernel_c4",
-                                                     "bytes_per_attempt"), "kernel": "grid_kernel",
+                                 "traffic": _traffic(("grid_kernel_c5" if lp.m >= 1_000_000 else "grid_kernel_c4")
+                                                     + ("" if prec == "fp64" else "_fp32"), "bytes_per_attempt"),
+                                 "kernel": "grid_kernel", "storage": prec,
                                  "traffic_source": "profiles/traffic.json (ncu --set full capture, per attempt)",
                                  "algorithmic_bytes_per_accepted_attempt": acc,
                                  "note": "working set (~70 MB) is L2-resident at C4; achieved may exceed HBM"}}
-        if cpu:
+        if prec == "fp32":
+            out[key]["objective_rel_err_vs_fp64"] = abs(best["primal_objective"] - out[alg]["objective"]) / (
+                1 + abs(out[alg]["objective"]))
+            out[key]["speedup_vs_fp64"] = out[alg]["time_ms"] / (t * 1e3)
+            continue
+        out[key]["objective"] = best["primal_objective"]
+        if cpu and (lp.m < 1_000_000 or alg == "ra"):   # C5: one oracle solve (its setup is ~50 s)
             log(f"large leg {alg}: CPU oracle beside it")
             cb = oracle_large_baseline(lp, alg, full=lp.m < 1_000_000, label=label)
             if cb["unit"] == "us_per_attempt":   # C5: extrapolated to the GPU's attempts

@@ -93,6 +93,15 @@ enum lp_algorithm { LP_RAPDHG = 0, LP_R2HPDHG = 1 };
  * attempt accepted -- the constant-step r2HPDHG of the cited Halpern work (SURVEY
  * §8(f) row 4; reading 34). */
 enum lp_step_rule { LP_STEP_ADAPTIVE = 0, LP_STEP_CONSTANT = 1 };
+
+/* Storage precision of the solve (lp_options.precision; MPAX runs in fp32 by
+ * default, fp64 with jax_enable_x64; every LP experiment of the paper is fp64).
+ * LP_FP64: everything fp64.  LP_FP32 (grid path only, DESIGN.md
+ * reading 39): K~, K~' and every iterate vector are STORED in fp32 -- half the bytes per
+ * attempt -- while each element's arithmetic, every dot product and every reduction runs in
+ * fp64 registers; inputs, setup (scaling) and the returned solution stay fp64.  Any other
+ * path with LP_FP32 returns LP_ERR_UNSUPPORTED. */
+enum lp_precision { LP_FP64 = 0, LP_FP32 = 1 };
 enum lp_memory { LP_HOST = 0, LP_DEVICE = 1 };
 
 /* Solve path selection (lp_options.path). */
@@ -142,6 +151,8 @@ typedef struct {
                                    - rho z) + b z0; rho = 1 is the full reflection 2 PDHG(z) - z of
                                    P:64, rho < 1 the partial reflection of SURVEY §8(f) row 4
                                    (reading 38); unused by raPDHG */
+  int32_t precision;            /* lp_precision, default LP_FP64 */
+  int32_t reserved;             /* 0 */
 } lp_options;
 
 /* Feasibility polishing (reading 36).
@@ -174,7 +185,7 @@ typedef struct {
 } lp_result;
 
 /* Fills o with the Appendix defaults: 1e-4, 1e-4, 1e-8, 1e-8, 1e-6,
- * INT64_MAX, 64, LP_R2HPDHG, 0, 0, 0, 10, LP_PATH_AUTO, LP_STEP_ADAPTIVE, 1.0. */
+ * INT64_MAX, 64, LP_R2HPDHG, 0, 0, 0, 10, LP_PATH_AUTO, LP_STEP_ADAPTIVE, 1.0, LP_FP64. */
 void lp_default_options(lp_options *o);
 
 /* Create a single-LP handle: validates, uploads, builds

@@ -38,13 +38,35 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <time.h>
 #include <stdlib.h>
 #include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
 
+typedef double ora_time_t;   /* wall-clock seconds (timing only; fp64 in both builds) */
+
+/* The fp32 build (liboracle_f32.so; reading 39).  MPAX's default precision is
+ * single ("MPAX uses single-precision (FP32) by default, consistent with JAX's
+ * standard setting"): in JAX every array and every operation of the solve is then float32, and
+ * Python literals adopt the array dtype (weak typing).  This file compiled with -DORA_FP32 and
+ * -fsingle-precision-constant is that program: every real (inputs, scaling, iterates,
+ * reductions, step sizes, tolerances) is an IEEE single, every literal is rounded to single,
+ * and the math library calls are their single-precision versions.  Integers (indices, counts)
+ * are unchanged.  Defined after the system headers so their prototypes keep their types. */
+#ifdef ORA_FP32
+#define double float
+#define sqrt sqrtf
+#define fabs fabsf
+#define fmin fminf
+#define fmax fmaxf
+#define pow powf
+#define ORA_INF HUGE_VALF
+#else
 #define ORA_INF HUGE_VAL
+#endif
+
 #define ORA_POLISH_LIMIT 100000   /* accepted steps per polishing sub-solve (reading 36) */
 
 enum { ORA_OK = 0, ORA_ERR_INVALID = -1, ORA_ERR_DIMENSION = -2, ORA_ERR_NAN = -3,
@@ -907,10 +929,24 @@ static int check_options(const ora_options *o) {
   return ORA_OK;
 }
 
+/* Wall-clock split of the calling thread's last ora_solve (bench.py's CPU baseline beside C5):
+ * setup = validation + preconditioning + scaled copies, solve = steps 2-6.  Timing only. */
+static _Thread_local ora_time_t g_t_setup = 0, g_t_solve = 0;
+static ora_time_t wall(void) {
+  struct timespec t;
+  clock_gettime(CLOCK_MONOTONIC, &t);
+  return (ora_time_t)t.tv_sec + (ora_time_t)t.tv_nsec / (ora_time_t)1000000000;
+}
+void ora_last_timing(ora_time_t *setup_s, ora_time_t *solve_s) {
+  if (setup_s) *setup_s = g_t_setup;
+  if (solve_s) *solve_s = g_t_solve;
+}
+
 /* Full single solve (contract steps 0-6).  x0/y0 (original space) may be NULL;
  * x_out (n), y_out (m), lam_out (n) may be NULL; log may be NULL. */
 int ora_solve(const ora_problem *p, const ora_options *o, const double *x0, const double *y0,
               double *x_out, double *y_out, double *lam_out, ora_result *res, ora_log *g) {
+  const ora_time_t t0 = wall();
   int e = ora_validate(p);
   if (e) return e;
   if ((e = check_options(o))) return e;
@@ -923,7 +959,10 @@ int ora_solve(const ora_problem *p, const ora_options *o, const double *x0, cons
   if ((e = build_scaled(p, Dr, Dc, NULL, NULL, &S))) { free(Dr); free(Dc); return e; }
   if (g) { g->att_len = 0; g->chk_len = 0; }
   memset(res, 0, sizeof(*res));
+  const ora_time_t t1 = wall();
   solve_polished(p, &S, o, x0, y0, x_out, y_out, lam_out, res, g);
+  g_t_setup = t1 - t0;
+  g_t_solve = wall() - t1;
   scaled_free(&S, 1);
   free(Dr); free(Dc);
   return ORA_OK;

@@ -21,24 +21,30 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 # rounding-sensitivity probe -- how far the oracle's own trajectory moves when every step rounds
 # differently.  Never a reference value.
 _LIB_FMA = os.path.join(_HERE, "liboracle_fma.so")
+# The same source compiled as the fp32 program (-DORA_FP32 -fsingle-precision-constant; DESIGN.md
+# reading 39): MPAX's default single precision.  The reference of the fp32 GPU paths.
+_LIB_F32 = os.path.join(_HERE, "liboracle_f32.so")
 # tests/test_oracle_mutations.py points this at a deliberately mutated build
 _LIB_OVERRIDE = os.environ.get("MPAX_ORACLE_LIB")
 _lock = threading.Lock()
 _lib = None
 _lib_fma = None
+_lib_f32 = None
 
 OPTIMAL, ITERATION_LIMIT, NUMERICAL_ERROR, PRIMAL_INFEASIBLE, DUAL_INFEASIBLE = 1, 2, 3, 4, 5
 RAPDHG, R2HPDHG = 0, 1
 
 
-def build(force: bool = False, fma: bool = False) -> str:
+def build(force: bool = False, fma: bool = False, f32: bool = False) -> str:
     """Compile the oracle shared library (plain C, no FMA contraction; `fma`: the contracted
-    rounding-sensitivity build)."""
-    out = _LIB_FMA if fma else _LIB
+    rounding-sensitivity build; `f32`: the fp32 program, reading 39)."""
+    out = _LIB_F32 if f32 else _LIB_FMA if fma else _LIB
     if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
         tmp = out + f".tmp{os.getpid()}"
         contract = "-ffp-contract=fast" if fma else "-ffp-contract=off"
         flags = ["-march=x86-64-v3"] if fma else []   # hardware FMA so contraction really happens
+        if f32:
+            flags = ["-DORA_FP32", "-fsingle-precision-constant"]
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", contract, *flags,
                                "-fno-fast-math", "-fPIC", "-shared", _SRC, "-o", tmp, "-lm"])
         os.replace(tmp, out)
@@ -61,6 +67,11 @@ class Options(C.Structure):
                 ("reflection", C.c_double)]
 
 
+class Options32(C.Structure):
+    """ora_options of the fp32 build (every double field is a float there)."""
+    _fields_ = [(f, C.c_float if t is C.c_double else t) for f, t in Options._fields_]
+
+
 class Certificate(C.Structure):
     _fields_ = [("primal_infeasible", C.c_int32), ("dual_infeasible", C.c_int32),
                 ("norm_dy", C.c_double), ("dual_ray_objective", C.c_double), ("dual_ray_violation", C.c_double),
@@ -78,6 +89,13 @@ class Result(C.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class Result32(C.Structure):
+    _fields_ = [(f, C.c_float if t is C.c_double else t) for f, t in Result._fields_]
+
+    def as_dict(self):
+        return {f: float(getattr(self, f)) if t is C.c_float else getattr(self, f) for f, t in self._fields_}
 
 
 class Log(C.Structure):
@@ -139,11 +157,29 @@ def lib(fma: bool = False):
             L.ora_initial_steps.argtypes = [P(Problem), P(Options), P(C.c_double), P(C.c_double)]
             L.ora_restart_candidate.argtypes = [C.c_double, C.c_double]
             L.ora_restart_candidate.restype = C.c_int32
+            L.ora_last_timing.argtypes = [P(C.c_double), P(C.c_double)]
             if fma:
                 _lib_fma = L
                 return L
             _lib = L
     return _lib
+
+
+def lib32():
+    """The fp32 build (reading 39): solve / solve_batch / default options only."""
+    global _lib_f32
+    with _lock:
+        if _lib_f32 is None:
+            L = C.CDLL(build(f32=True))
+            P = C.POINTER
+            L.ora_solve.argtypes = [P(Problem), P(Options32), C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, P(Result32), C.c_void_p]
+            L.ora_solve_batch.argtypes = [P(Problem), C.c_int64, C.c_void_p, C.c_void_p, P(Options32),
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, P(Result32)]
+            L.ora_default_options.argtypes = [P(Options32)]
+            L.ora_set_threads.argtypes = [C.c_int]
+            _lib_f32 = L
+    return _lib_f32
 
 
 def _f64(a):
@@ -157,11 +193,12 @@ def _ptr(a):
 class _Bound:
     """Keeps the numpy buffers a Problem struct points into alive."""
 
-    def __init__(self, lp):
+    def __init__(self, lp, dtype=np.float64):
         self.row_ptr = np.ascontiguousarray(lp.row_ptr, dtype=np.int64)
         self.col_idx = np.ascontiguousarray(lp.col_idx, dtype=np.int32)
-        self.val = _f64(lp.val)
-        self.c, self.q, self.l, self.u = _f64(lp.c), _f64(lp.q), _f64(lp.l), _f64(lp.u)
+        f = lambda a: np.ascontiguousarray(a, dtype=dtype)  # noqa: E731
+        self.val = f(lp.val)
+        self.c, self.q, self.l, self.u = f(lp.c), f(lp.q), f(lp.l), f(lp.u)
         self.s = Problem(int(lp.n), int(lp.m1), int(lp.m2), int(self.val.size),
                          self.row_ptr.ctypes.data, self.col_idx.ctypes.data, self.val.ctypes.data,
                          self.c.ctypes.data, self.q.ctypes.data if self.q.size else None,
@@ -196,9 +233,15 @@ def validate(lp) -> int:
 def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, x0=None, y0=None,
           check_frequency=64, log_capacity=0, step_rule=0, eps_primal_infeasible=1e-8, eps_dual_infeasible=1e-8,
           feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0, ruiz_iters=10, pock_chambolle=1,
-          fma=False):
+          fma=False, precision="fp64"):
     """Full solve (contract steps 0-6).  Returns a dict with x, y, lam, the
-    result fields, and (if log_capacity) the attempt/check decision logs."""
+    result fields, and (if log_capacity) the attempt/check decision logs.
+    precision="fp32": the fp32 build (reading 39); inputs rounded to single, outputs as float64
+    arrays holding the single-precision results."""
+    if precision == "fp32":
+        return _solve32(lp, algorithm, eps_abs, eps_rel, iteration_limit, x0, y0, check_frequency, step_rule,
+                        eps_primal_infeasible, eps_dual_infeasible, feasibility_polishing, eps_feas_polish,
+                        reflection, ruiz_iters, pock_chambolle)
     b = _Bound(lp)
     m = lp.m1 + lp.m2
     o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule,
@@ -229,32 +272,64 @@ def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, 
     return out
 
 
+def _options32(o):
+    return Options32(*[getattr(o, f) for f, _ in Options._fields_])
+
+
+def _solve32(lp, algorithm, eps_abs, eps_rel, iteration_limit, x0, y0, check_frequency, step_rule,
+             eps_primal_infeasible, eps_dual_infeasible, feasibility_polishing, eps_feas_polish, reflection,
+             ruiz_iters, pock_chambolle):
+    b = _Bound(lp, np.float32)
+    m = lp.m1 + lp.m2
+    o = _options32(options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule,
+                           eps_primal_infeasible=eps_primal_infeasible, eps_dual_infeasible=eps_dual_infeasible,
+                           feasibility_polishing=feasibility_polishing, eps_feas_polish=eps_feas_polish,
+                           reflection=reflection, ruiz_iters=ruiz_iters, pock_chambolle=pock_chambolle))
+    x, y, lam = np.zeros(lp.n, np.float32), np.zeros(max(m, 1), np.float32), np.zeros(lp.n, np.float32)
+    x0a = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float32)
+    y0a = None if y0 is None else np.ascontiguousarray(y0, dtype=np.float32)
+    r = Result32()
+    e = lib32().ora_solve(C.byref(b.s), C.byref(o), _ptr(x0a), _ptr(y0a), x.ctypes.data,
+                          y.ctypes.data if m else None, lam.ctypes.data, C.byref(r), None)
+    if e != 0:
+        raise ValueError(f"oracle error {e}")
+    out = r.as_dict()
+    out.update(x=x.astype(np.float64), y=y[:m].astype(np.float64), lam=lam.astype(np.float64))
+    return out
+
+
 def solve_batch(lp, C_=None, Q=None, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None,
                 X0=None, Y0=None, check_frequency=64, threads=None, step_rule=0, eps_primal_infeasible=1e-8,
                 eps_dual_infeasible=1e-8, feasibility_polishing=False, eps_feas_polish=1e-6, reflection=1.0,
-                fma=False):
-    """Batch solve sharing K, l, u; one instance per OpenMP thread."""
-    b = _Bound(lp)
+                fma=False, precision="fp64"):
+    """Batch solve sharing K, l, u; one instance per OpenMP thread.  precision="fp32": the fp32
+    build (reading 39)."""
+    f32 = precision == "fp32"
+    dt = np.float32 if f32 else np.float64
+    b = _Bound(lp, dt)
     m = lp.m1 + lp.m2
-    Cm = None if C_ is None else _f64(C_)
-    Qm = None if Q is None else _f64(Q)
+    Cm = None if C_ is None else np.ascontiguousarray(C_, dtype=dt)
+    Qm = None if Q is None else np.ascontiguousarray(Q, dtype=dt)
     B = Cm.shape[0] if Cm is not None else Qm.shape[0]
     o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule,
                 eps_primal_infeasible=eps_primal_infeasible, eps_dual_infeasible=eps_dual_infeasible,
                 feasibility_polishing=feasibility_polishing, eps_feas_polish=eps_feas_polish,
                 reflection=reflection)
-    X = np.zeros((B, lp.n))
-    Y = np.zeros((B, m))
-    res = (Result * B)()
+    X = np.zeros((B, lp.n), dt)
+    Y = np.zeros((B, m), dt)
+    res = ((Result32 if f32 else Result) * B)()
+    L = lib32() if f32 else lib(fma)
+    if f32:
+        o = _options32(o)
     if threads:
-        lib().ora_set_threads(int(threads))
-    X0a = None if X0 is None else _f64(X0)
-    Y0a = None if Y0 is None else _f64(Y0)
-    e = lib(fma).ora_solve_batch(C.byref(b.s), B, _ptr(Cm), _ptr(Qm), C.byref(o), _ptr(X0a), _ptr(Y0a),
-                              X.ctypes.data, Y.ctypes.data if m else None, res)
+        L.ora_set_threads(int(threads))
+    X0a = None if X0 is None else np.ascontiguousarray(X0, dtype=dt)
+    Y0a = None if Y0 is None else np.ascontiguousarray(Y0, dtype=dt)
+    e = L.ora_solve_batch(C.byref(b.s), B, _ptr(Cm), _ptr(Qm), C.byref(o), _ptr(X0a), _ptr(Y0a),
+                          X.ctypes.data, Y.ctypes.data if m else None, res)
     if e != 0:
         raise ValueError(f"oracle error {e}")
-    return X, Y, [r.as_dict() for r in res]
+    return X.astype(np.float64), Y.astype(np.float64), [r.as_dict() for r in res]
 
 
 def num_threads() -> int:
@@ -430,3 +505,11 @@ def initial_steps(lp, step_rule=0, ruiz_iters=10, pock_chambolle=1):
 def restart_candidate(kkt_omega_avg, kkt_omega_cur):
     """'avg' if the average's KKT_omega is strictly smaller, else 'cur' (reading c.3 #10)."""
     return "avg" if lib().ora_restart_candidate(kkt_omega_avg, kkt_omega_cur) else "cur"
+
+
+def last_timing():
+    """(setup_s, solve_s) of this thread's last oracle.solve: validation + preconditioning +
+    scaled copies, then steps 2-6 (wall clock; timing only)."""
+    a, b = C.c_double(), C.c_double()
+    lib().ora_last_timing(C.byref(a), C.byref(b))
+    return a.value, b.value

@@ -8,7 +8,7 @@ symbols can be inspected), but any solve raises if CUDA is unavailable.
 from .lp import (  # noqa: F401
     LP_DEVICE, LP_HOST, LP_OPTIMAL, LP_ITERATION_LIMIT, LP_NUMERICAL_ERROR, LP_PRIMAL_INFEASIBLE, LP_DUAL_INFEASIBLE,
     RAPDHG, R2HPDHG,
-    PATH_AUTO, PATH_INSTANCE, PATH_GRID, PATH_DMMA, STEP_ADAPTIVE, STEP_CONSTANT, LpError, Problem, Options, Result, Solver, BatchSolver,
+    PATH_AUTO, PATH_INSTANCE, PATH_GRID, PATH_DMMA, STEP_ADAPTIVE, STEP_CONSTANT, FP64, FP32, LpError, Problem, Options, Result, Solver, BatchSolver,
     create_lp, default_options, lib, library_path, launch_count, selftest_division, EXPORTED_SYMBOLS, RESULT_DTYPE,
     ShardedSolver, row_partition, local_rows, nccl_unique_id, nccl_comm_init, nccl_comm_destroy,
 )

@@ -171,7 +171,7 @@ void free_handle(lp_handle h) {
   }
   cudaStream_t s = h->stream;
   for (void *p : {(void *)h->arena, (void *)h->X0, (void *)h->Y0, (void *)h->work, (void *)h->pol, (void *)h->spo,
-                 h->P.split_mem})
+                 h->P.split_mem, h->P.f32_mem})
     if (p) cudaFreeAsync(p, s);
   // every D2H into the pinned buffers was followed by a stream sync, so they can be recycled now
   pin_put(h->h_res, (size_t)h->batch * sizeof(lp_result));
@@ -404,6 +404,7 @@ int check_options(const lp_options *o) {
   if (o->step_rule != LP_STEP_ADAPTIVE && o->step_rule != LP_STEP_CONSTANT)
     return fail(LP_ERR_INVALID_ARGUMENT, "bad step_rule");
   if (!(o->reflection >= 0.0 && o->reflection <= 1.0)) return fail(LP_ERR_INVALID_ARGUMENT, "reflection not in [0, 1]");
+  if (o->precision != LP_FP64 && o->precision != LP_FP32) return fail(LP_ERR_INVALID_ARGUMENT, "bad precision");
   return LP_OK;
 }
 
@@ -520,6 +521,7 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
   TRY(check_options(o));
   if (memory != LP_HOST && memory != LP_DEVICE) return fail(LP_ERR_INVALID_ARGUMENT, "bad memory kind");
   if (h->sharded) {
+    if (o->precision == LP_FP32) return fail(LP_ERR_UNSUPPORTED, "fp32 storage is a grid-path option");
     if (o->feasibility_polishing) return fail(LP_ERR_UNSUPPORTED, "feasibility polishing on a sharded handle");
     return run_sharded(h, o, X0, Y0, out);
   }
@@ -541,6 +543,8 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
   const bool big = h->P.nnz >= 32768 || h->P.n + h->P.m >= 4096;
   const bool use_grid = (B == 1) && (o->path == LP_PATH_GRID || (o->path == LP_PATH_AUTO && big));
   if (o->path == LP_PATH_GRID && B != 1) return fail(LP_ERR_UNSUPPORTED, "the grid path solves one LP");
+  if (o->precision == LP_FP32 && !use_grid)
+    return fail(LP_ERR_UNSUPPORTED, "fp32 storage is a grid-path option (one large LP; DESIGN.md reading 39)");
   // a batch sharing a dense K: fp64 tensor-core path (auto from 8 instances on)
   const bool dmma = !use_grid && h->P.dense && (o->path == LP_PATH_DMMA || (o->path == LP_PATH_AUTO && B >= 8));
   if (dmma) {
@@ -559,7 +563,9 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
       GridLaunch G;
       G.c0 = L.C0; G.q0 = L.Q0; G.X0 = L.X0; G.Y0 = L.Y0; G.X = L.X; G.Y = L.Y; G.L = L.L; G.res = L.res;
       G.polish_mode = L.polish_mode;
-      if (int rs = grid_split_prepare(h->P, s)) return rs;
+      if (int rs = grid_split_prepare(h->P, s, oo.precision == LP_FP32 ? 4 : 8)) return rs;
+      if (oo.precision == LP_FP32)
+        if (int rs = grid_f32_prepare(h->P, s)) return rs;
       int rc = grid_solve(h->P, oo, G, s, &h->work, &h->work_bytes);
       if (rc == LP_ERR_UNSUPPORTED) return fail(rc, "cooperative launch unavailable");
       return rc;
@@ -667,6 +673,8 @@ void lp_default_options(lp_options *o) {
   o->path = LP_PATH_AUTO;
   o->step_rule = LP_STEP_ADAPTIVE;
   o->reflection = 1.0;
+  o->precision = LP_FP64;
+  o->reserved = 0;
 }
 
 int lp_create(const lp_problem_desc *p, void *cuda_stream, lp_handle *out) {

@@ -43,18 +43,23 @@ namespace {
 constexpr int kNP = 26;      // max partial values per phase (raPDHG check: 20 KKT / distance + 6 certificate)
 constexpr int kBS = 512;     // threads per CTA
 
+// T: storage type of K~'s values and of every iterate vector (double; float for fp32 storage,
+// DESIGN.md reading 39).  Arithmetic and reductions are fp64 in both: loads widen, stores round.
+template <typename T>
 struct GridParams {
   int64_t n, m, m1;
   const int32_t *rp, *ci, *trp, *tci;
-  const double *kv, *tkv, *Dr, *Dc, *ls, *us, *l0, *u0, *c0, *q0, *X0, *Y0, *kmax, *sigma, *tab;
-  double *cs, *qs;
-  double *x, *KTy, *xp, *KTyp, *xa, *KTya, *xr;   // n-side
-  double *y, *Kx, *yp, *Kxp, *ya, *Kxa, *yr;      // m-side
+  const T *kv, *tkv;
+  const double *Dr, *Dc, *ls, *us, *l0, *u0, *c0, *q0, *X0, *Y0, *kmax, *sigma, *tab;
+  T *lsw, *usw;                                   // float: l~, u~ rounded (the attempt's projection)
+  T *cs, *qs;
+  T *x, *KTy, *xp, *KTyp, *xa, *KTya, *xr;        // n-side
+  T *y, *Kx, *yp, *Kxp, *ya, *Kxa, *yr;           // m-side
   double *part;                                   // gridDim.x x kNP
   double *tpart;                                  // 2 x blocks x ceil(tiles / blocks): per-tile partials
   // two-pass phase B over the column halves of K~ (split != 0): pass 1 parks K~_L x' in tmp
   const int32_t *rpL, *ciL, *rpR, *ciR;
-  const double *kvL, *kvR;
+  const T *kvL, *kvR;
   double *tmp;
   int32_t split;
   double *tpartA;                                 // ceil(n / 32): phase A's per-tile ||dx||^2 (global claims)
@@ -86,9 +91,14 @@ __device__ __forceinline__ void st_evict_last(double *p, double v) {
   asm volatile("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
                "st.global.L2::cache_hint.f64 [%0], %1, pol;\n\t}" :: "l"(p), "d"(v) : "memory");
 }
+__device__ __forceinline__ void st_evict_last(float *p, double v) {
+  asm volatile("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+               "st.global.L2::cache_hint.f32 [%0], %1, pol;\n\t}" :: "l"(p), "f"((float)v) : "memory");
+}
 
 // streamed (evict-first) loads of the matrices
 __device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
+__device__ __forceinline__ double ld_stream(const float *p) { return (double)__ldcs(p); }
 __device__ __forceinline__ int32_t ld_stream(const int32_t *p) { return __ldcs(p); }
 
 // Sum of row r of a CSR matrix times x (all lanes of the row's group get the sum).
@@ -97,9 +107,10 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t *p) { return __ldcs(p
 // G >= 2: G lanes per row, each taking its entries four at a time (index and value loads
 // first, then the four gathers, then the FMAs) so that twelve loads are in flight per lane;
 // two interleaved accumulators, butterfly over the group.  Fixed order: deterministic.
+template <typename V, typename X>
 __device__ __forceinline__ double row_dot(int64_t r, bool valid, int rows, int G, int gl,
                                           const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                                          const double *__restrict__ v, const double *x, double *tbuf) {
+                                          const V *__restrict__ v, const X *x, double *tbuf) {
   if (G == 1) return tile_row_dot((int)r, valid, rows, rp, ci, v, x, tbuf);
   double s0 = 0.0, s1 = 0.0;
   if (valid) {
@@ -115,7 +126,7 @@ __device__ __forceinline__ double row_dot(int64_t r, bool valid, int rows, int G
         w[k] = ok ? ld_stream(v + q) : 0.0;
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) xv[k] = (p + k * G < e) ? x[c[k]] : 0.0;
+      for (int k = 0; k < 4; ++k) xv[k] = (p + k * G < e) ? (double)x[c[k]] : 0.0;
       s0 += w[0] * xv[0];
       s1 += w[1] * xv[1];
       s0 += w[2] * xv[2];
@@ -200,14 +211,15 @@ enum PhaseMode : int {
   kB_R2 = 4,   // phase B, r2HPDHG, commit pending
   kB_NOP = 5,  // phase B, no pending commit (after a rejected attempt or a check)
 };
+template <typename T>
 struct PhaseCtx {
   const int32_t *rp, *ci;
-  const double *kv, *tgt;         // the sweep's matrix and gathered vector
+  const T *kv, *tgt;              // the sweep's matrix and gathered vector
   const double *add;              // + add[row] (two-pass phase B pass 2), or null
   double *park;                   // pass 1 output
   // epilogue vectors (meaning per mode, see phase_tiles)
-  double *e0, *e1, *e2, *e3, *e4;
-  const double *r0, *r1, *r2, *r3, *r4;
+  T *e0, *e1, *e2, *e3, *e4;
+  const T *r0, *r1, *r2, *r3, *r4;
   double tau_sigma, theta, ha, hb, rf1, rf0;
   int rows, m1;
   double *tpart;                  // per-tile partials (2 per tile)
@@ -216,8 +228,8 @@ struct PhaseCtx {
   unsigned long long gbase;       //   counter value at the phase's start; tiles [0, kmax)
 };
 
-template <int MODE>
-__device__ __noinline__ void phase_tiles(const volatile PhaseCtx *cx, int *s_ctr, double *tbuf) {
+template <int MODE, typename T>
+__device__ __noinline__ void phase_tiles(const volatile PhaseCtx<T> *cx, int *s_ctr, double *tbuf) {
   const int lane = threadIdx.x & 31;
   const int rows = cx->rows, t0 = cx->t0, kmax = cx->kmax;
   unsigned long long *const gctr = cx->gctr;
@@ -232,29 +244,29 @@ __device__ __noinline__ void phase_tiles(const volatile PhaseCtx *cx, int *s_ctr
     double c0 = 0.0, c1 = 0.0;
     if (MODE == kB_PARK) {
       const double sl = tile_row_dot(r, ok, rows, (const int32_t *)cx->rp, (const int32_t *)cx->ci,
-                                     (const double *)cx->kv, (const double *)cx->tgt, tbuf);
+                                     (const T *)cx->kv, (const T *)cx->tgt, tbuf);
       if (ok) cx->park[r] = sl;
       continue;
     }
-    double s = tile_row_dot(r, ok, rows, (const int32_t *)cx->rp, (const int32_t *)cx->ci, (const double *)cx->kv,
-                            (const double *)cx->tgt, tbuf);
+    double s = tile_row_dot(r, ok, rows, (const int32_t *)cx->rp, (const int32_t *)cx->ci, (const T *)cx->kv,
+                            (const T *)cx->tgt, tbuf);
     if (ok) {
       if (MODE == kA_RA) {
         // r0 = xp, r1 = cs, r2 = ls, r3 = us; e0 = xa (rw), e1 = KTy' (w), e2 = the old x buffer (w: x')
         const double o_xp = cx->r0[r], o_xa = cx->e0[r];
         cx->e0[r] = o_xa + cx->theta * (o_xp - o_xa);
         cx->e1[r] = s;
-        const double xnew = median3(cx->r2[r], o_xp - cx->tau_sigma * (cx->r1[r] - s), cx->r3[r]);
+        const double xnew = median3((double)cx->r2[r], o_xp - cx->tau_sigma * ((double)cx->r1[r] - s), (double)cx->r3[r]);
         cx->e2[r] = xnew;
         const double d = xnew - o_xp;
         c0 = d * d;
       } else if (MODE == kA_R2) {
         // r0 = xp, r1 = cs, r2 = ls, r3 = us, r4 = KTya, e0 = xa (r), e1 = x (rw), e2 = KTy (rw), e3 = x' (w)
-        const double xn = cx->ha * (cx->rf1 * cx->r0[r] - cx->rf0 * cx->e1[r]) + cx->hb * cx->e0[r];
-        const double kt = cx->ha * (cx->rf1 * s - cx->rf0 * cx->e2[r]) + cx->hb * cx->r4[r];
+        const double xn = cx->ha * (cx->rf1 * (double)cx->r0[r] - cx->rf0 * (double)cx->e1[r]) + cx->hb * (double)cx->e0[r];
+        const double kt = cx->ha * (cx->rf1 * s - cx->rf0 * (double)cx->e2[r]) + cx->hb * (double)cx->r4[r];
         cx->e1[r] = xn;
         cx->e2[r] = kt;
-        const double xnew = median3(cx->r2[r], xn - cx->tau_sigma * (cx->r1[r] - kt), cx->r3[r]);
+        const double xnew = median3((double)cx->r2[r], xn - cx->tau_sigma * ((double)cx->r1[r] - kt), (double)cx->r3[r]);
         cx->e3[r] = xnew;
         const double d = xnew - xn;
         c0 = d * d;
@@ -269,8 +281,8 @@ __device__ __noinline__ void phase_tiles(const volatile PhaseCtx *cx, int *s_ctr
           cx->e0[r] = o_ya + cx->theta * (yv - o_ya);
         } else if (MODE == kB_R2) {
           // r0 = qs, r1 = yp, r2 = Kxp, r3 = ya, r4 = Kxa; e0 = y (rw), e1 = Kx (rw), e2 = y' (w), e3 = K~x' (w)
-          yv = cx->ha * (cx->rf1 * cx->r1[r] - cx->rf0 * cx->e0[r]) + cx->hb * cx->r3[r];
-          kxv = cx->ha * (cx->rf1 * cx->r2[r] - cx->rf0 * cx->e1[r]) + cx->hb * cx->r4[r];
+          yv = cx->ha * (cx->rf1 * (double)cx->r1[r] - cx->rf0 * (double)cx->e0[r]) + cx->hb * (double)cx->r3[r];
+          kxv = cx->ha * (cx->rf1 * (double)cx->r2[r] - cx->rf0 * (double)cx->e1[r]) + cx->hb * (double)cx->r4[r];
           cx->e0[r] = yv;
           cx->e1[r] = kxv;
         } else {
@@ -278,7 +290,7 @@ __device__ __noinline__ void phase_tiles(const volatile PhaseCtx *cx, int *s_ctr
           yv = cx->r1[r];
           kxv = cx->r2[r];
         }
-        double yn = yv + cx->tau_sigma * (cx->r0[r] - 2.0 * s + kxv);
+        double yn = yv + cx->tau_sigma * ((double)cx->r0[r] - 2.0 * s + kxv);
         if (r < cx->m1) yn = fmax(yn, 0.0);
         if (MODE == kB_RA) { cx->e1[r] = yn; cx->e2[r] = s; }
         else { cx->e2[r] = yn; cx->e3[r] = s; }
@@ -299,22 +311,22 @@ __device__ __noinline__ void phase_tiles(const volatile PhaseCtx *cx, int *s_ctr
   }
 }
 
-template <int MINB>
-__global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
+template <int MINB, typename T>
+__global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double s_red[kBS / 32][kNP];
   __shared__ double s_tot[kNP];
   __shared__ double s_tile[kBS / 32][kTileBuf];   // per-warp product buffer of the G == 1 mapping
   __shared__ int s_ctr;                             // tile counter of tiles_dynamic
-  __shared__ PhaseCtx s_cx;                         // context of the lean hot phases (phase_tiles)
+  __shared__ PhaseCtx<T> s_cx;                      // context of the lean hot phases (phase_tiles)
   double *const tbuf = s_tile[threadIdx.x >> 5];
   // L2 policy of the attempt's vector traffic (P.vpol): 0 = default; 1 = every
   // vector access except the stores of the next gather target (x', y') is evict-first, so the
   // target stays L2-resident for the next phase's SpMV; 2 = 1 + those stores evict-last.
   const int vpol = P.vpol, tdist = P.tdist, dyn = P.dyn;
-  auto lv = [vpol](const double *p) { return vpol ? __ldcs(p) : *p; };
-  auto sv = [vpol](double *p, double v) { if (vpol) __stcs(p, v); else *p = v; };
-  auto st_tgt = [vpol](double *p, double v) { if (vpol == 2) st_evict_last(p, v); else *p = v; };
+  auto lv = [vpol](const auto *p) -> double { return vpol ? (double)__ldcs(p) : (double)*p; };
+  auto sv = [vpol](T *p, double v) { if (vpol) __stcs(p, (T)v); else *p = (T)v; };
+  auto st_tgt = [vpol](T *p, double v) { if (vpol == 2) st_evict_last(p, v); else *p = (T)v; };
   // Hot-loop driver of the warp-tile mapping (G == 1): CTA b owns the contiguous tiles
   // [b T, (b + 1) T) of 32 rows; its warps claim them dynamically from a shared counter, so
   // early warps take more tiles instead of idling at the CTA barrier (the static mapping
@@ -325,10 +337,10 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   auto tiles_dynamic = [&](int rows, auto &&body, auto &tot, bool reduce) {
     constexpr int V = sizeof(tot) / sizeof(double);
     const int ntiles = (rows + 31) >> 5;
-    const int nb = (int)gridDim.x, T = (ntiles + nb - 1) / nb;
+    const int nb = (int)gridDim.x, per = (ntiles + nb - 1) / nb;
     // k-th tile of this CTA: contiguous range (tdist 0) or interleaved over the CTAs (tdist 1)
-    const int kmax = tdist ? (ntiles - (int)blockIdx.x + nb - 1) / nb : max(0, min(ntiles, ((int)blockIdx.x + 1) * T) - (int)blockIdx.x * T);
-    const int t0 = (int)blockIdx.x * T, t1 = t0 + kmax;   // this CTA's slots in P.tpart
+    const int kmax = tdist ? (ntiles - (int)blockIdx.x + nb - 1) / nb : max(0, min(ntiles, ((int)blockIdx.x + 1) * per) - (int)blockIdx.x * per);
+    const int t0 = (int)blockIdx.x * per, t1 = t0 + kmax;   // this CTA's slots in P.tpart
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) s_ctr = 0;
     __syncthreads();
@@ -371,11 +383,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   // contiguous tile range with dynamic claims, then (reduce) warp 0 sums the tile partials in tile
   // order: on return thread 0 holds the CTA totals in tot[0..1], every other thread zeros.
   auto lean_range = [&](int rows) {
-    const int ntiles = (rows + 31) >> 5, nb = (int)gridDim.x, T = (ntiles + nb - 1) / nb;
-    const int t0 = (int)blockIdx.x * T;
+    const int ntiles = (rows + 31) >> 5, nb = (int)gridDim.x, per = (ntiles + nb - 1) / nb;
+    const int t0 = (int)blockIdx.x * per;
     s_cx.rows = rows;
     s_cx.t0 = t0;
-    s_cx.kmax = max(0, min(ntiles, t0 + T) - t0);
+    s_cx.kmax = max(0, min(ntiles, t0 + per) - t0);
     s_cx.tpart = P.tpart;
     s_ctr = 0;
   };
@@ -407,9 +419,13 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   const int grpt = gtid / Gt, ngrpt = gthreads / Gt;
   const int glt = (int)(gtid % Gt);
   const int row_iters = (m + ngrp - 1) / ngrp, col_iters = (n + ngrpt - 1) / ngrpt;
-  double *x = P.x, *KTy = P.KTy, *xp = P.xp, *KTyp = P.KTyp, *xa = P.xa, *KTya = P.KTya, *xr = P.xr;
-  double *y = P.y, *Kx = P.Kx, *yp = P.yp, *Kxp = P.Kxp, *ya = P.ya, *Kxa = P.Kxa, *yr = P.yr;
-  const double *cs = P.cs, *qs = P.qs;
+  T *x = P.x, *KTy = P.KTy, *xp = P.xp, *KTyp = P.KTyp, *xa = P.xa, *KTya = P.KTya, *xr = P.xr;
+  T *y = P.y, *Kx = P.Kx, *yp = P.yp, *Kxp = P.Kxp, *ya = P.ya, *Kxa = P.Kxa, *yr = P.yr;
+  const T *cs = P.cs, *qs = P.qs;
+  // the attempt's bounds: l~, u~ themselves (fp64), or their fp32 copies (written below)
+  const T *lsT, *usT;
+  if constexpr (sizeof(T) == sizeof(double)) { lsT = (const T *)P.ls; usT = (const T *)P.us; }
+  else { lsT = P.lsw; usT = P.usw; }
   // Per-CTA partials are double-buffered: reduction r writes buffer r % 2, so a CTA that has
   // moved on can never overwrite partials a slower CTA is still summing (that would let CTAs
   // take different decisions and then wait at different grid barriers).
@@ -422,19 +438,20 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j = gtid; j < n; j += gthreads) {
       const double dc = P.Dc[j], c = P.c0[j], cj = c * dc;
-      P.cs[j] = cj;
+      P.cs[j] = (T)cj;
       v[0] += cj * cj;
       v[2] += c * c;
-      x[j] = median3(P.ls[j], P.X0 ? P.X0[j] / dc : 0.0, P.us[j]);
+      x[j] = (T)median3(P.ls[j], P.X0 ? P.X0[j] / dc : 0.0, P.us[j]);
+      if constexpr (sizeof(T) != sizeof(double)) { P.lsw[j] = (T)P.ls[j]; P.usw[j] = (T)P.us[j]; }
     }
     for (int i = gtid; i < m; i += gthreads) {
       const double dr = P.Dr[i], q = P.q0[i], qi = q * dr;
-      P.qs[i] = qi;
+      P.qs[i] = (T)qi;
       v[1] += qi * qi;
       v[3] += q * q;
       double yv = P.Y0 ? P.Y0[i] / dr : 0.0;
       if (i < m1) yv = fmax(yv, 0.0);
-      y[i] = yv;
+      y[i] = (T)yv;
     }
     block_partials<4>(v, next_part(), s_red);
     if (blockIdx.x == 0 && threadIdx.x == 0) *P.gctr = 0ull;   // before the first grid barrier
@@ -463,9 +480,9 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       const bool ok = i < m;
       const double s = row_dot(i, ok, m, G, gl, P.rp, P.ci, P.kv, x, tbuf);
       if (ok && gl == 0) {
-        Kx[i] = s; Kxa[i] = s;
+        Kx[i] = (T)s; Kxa[i] = (T)s;
         const double yv = y[i];
-        ya[i] = yv; yr[i] = yv;
+        ya[i] = (T)yv; yr[i] = (T)yv;
         kkt_row_acc(v, false, i < m1, 1.0, yv, s, 0.0, qs[i]);
       }
     }
@@ -474,10 +491,10 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       const bool ok = j < n;
       const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, y, tbuf);
       if (ok && glt == 0) {
-        KTy[j] = s; KTya[j] = s;
+        KTy[j] = (T)s; KTya[j] = (T)s;
         const double xv = x[j];
-        xa[j] = xv; xr[j] = xv;
-        kkt_col_acc(v, false, 1.0, xv, s, 0.0, cs[j], 0.0, P.ls[j], 0.0, P.us[j]);
+        xa[j] = (T)xv; xr[j] = (T)xv;
+        kkt_col_acc(v, false, 1.0, xv, s, 0.0, (double)cs[j], 0.0, (double)lsT[j], 0.0, (double)usT[j]);
       }
     }
     block_partials<4>(v, next_part(), s_red);
@@ -499,13 +516,13 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
   double theta = 0.0, ha = 0.0, hb = 0.0;  // raPDHG average weight / r2HPDHG Halpern coefficients
   int rejects = 0;
   // returned candidate (pointers)
-  const double *ox = x, *oy = y, *oKx = Kx, *oKTy = KTy;
+  const T *ox = x, *oy = y, *oKx = Kx, *oKTy = KTy;
   bool done = false;
   // infeasibility (reading 35): t = reduced (|dy|^2, |dx|^2, dual-ray obj, c'dx, viol_y, viol_x);
   // on a certificate the status is set and the output writes the rays against (bx, by, bKTy)
-  const double *bx = nullptr, *by = nullptr, *bKTy = nullptr;
+  const T *bx = nullptr, *by = nullptr, *bKTy = nullptr;
   double ray_ny = 1.0, ray_nx = 1.0;
-  auto certify = [&](const double *t, const double *xb, const double *yb, const double *KTyb) {
+  auto certify = [&](const double *t, const T *xb, const T *yb, const T *KTyb) {
     CertAcc tot;
     tot.sy = t[0]; tot.sx = t[1]; tot.oy = t[2]; tot.ox = t[3]; tot.vy = t[4]; tot.vx = t[5];
     const int st = cert_decide(tot, P.eps_pi, P.eps_di, ray_ny, ray_nx);
@@ -531,7 +548,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         // operands of the epilogue, loaded before the dot so they are in flight with it
         double o_xp = 0.0, o_xa = 0.0, o_x = 0.0, o_kt = 0.0, o_kta = 0.0, o_cs = 0.0, o_ls = 0.0, o_us = 0.0;
         if (lead) {
-          o_xp = lv(xp + j); o_xa = lv(xa + j); o_cs = lv(cs + j); o_ls = lv(P.ls + j); o_us = lv(P.us + j);
+          o_xp = lv(xp + j); o_xa = lv(xa + j); o_cs = lv(cs + j); o_ls = lv(lsT + j); o_us = lv(usT + j);
           if (r2) { o_x = lv(x + j); o_kt = lv(KTy + j); o_kta = lv(KTya + j); }
         }
         const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, yp, tbuf);
@@ -558,15 +575,15 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           s_cx.gctr = nullptr;
           if (glob) { s_cx.gctr = P.gctr; s_cx.gbase = gbase; s_cx.t0 = 0; s_cx.kmax = (n + 31) >> 5; s_cx.tpart = P.tpartA; }
           s_cx.rp = P.trp; s_cx.ci = P.tci; s_cx.kv = P.tkv; s_cx.tgt = yp; s_cx.add = nullptr;
-          s_cx.r0 = xp; s_cx.r1 = cs; s_cx.r2 = P.ls; s_cx.r3 = P.us; s_cx.r4 = KTya;
+          s_cx.r0 = xp; s_cx.r1 = cs; s_cx.r2 = lsT; s_cx.r3 = usT; s_cx.r4 = KTya;
           s_cx.e0 = xa;
           if (!r2) { s_cx.e1 = KTyp; s_cx.e2 = x; }
           else { s_cx.e1 = x; s_cx.e2 = KTy; s_cx.e3 = xp; }
           s_cx.tau_sigma = tau; s_cx.theta = theta; s_cx.ha = ha; s_cx.hb = hb; s_cx.rf1 = rf1; s_cx.rf0 = rf0;
         }
         __syncthreads();
-        if (!r2) phase_tiles<kA_RA>(&s_cx, &s_ctr, tbuf);
-        else phase_tiles<kA_R2>(&s_cx, &s_ctr, tbuf);
+        if (!r2) phase_tiles<kA_RA, T>(&s_cx, &s_ctr, tbuf);
+        else phase_tiles<kA_R2, T>(&s_cx, &s_ctr, tbuf);
         __syncthreads();
         if (glob) {
           // every warp made exactly one failing claim: the phase consumed tiles + warps values;
@@ -613,13 +630,13 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         }
       }
       if (!r2) {  // swap: x <-> x', K~'y <-> K~'y'
-        double *t = x; x = xp; xp = t;
+        T *t = x; x = xp; xp = t;
         t = KTy; KTy = KTyp; KTyp = t;
       }
     } else {
       for (int j = gtid; j < n; j += gthreads) {
         const double xo = lv(x + j);
-        const double xn = median3(lv(P.ls + j), xo - tau * (lv(cs + j) - lv(KTy + j)), lv(P.us + j));
+        const double xn = median3(lv(lsT + j), xo - tau * (lv(cs + j) - lv(KTy + j)), lv(usT + j));
         st_tgt(xp + j, xn);
         const double d = xn - xo;
         v3[0] += d * d;
@@ -632,7 +649,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
     {
       // one row i of phase B; returns its ||dy||^2 and <dy, K~x' - K~x> terms
       auto rowB = [&](int i, bool ok, bool lead, double (&c)[2], const int32_t *rp_, const int32_t *ci_,
-                      const double *kv_, const double *addp) {
+                      const T *kv_, const double *addp) {
         double o_y = 0.0, o_kx = 0.0, o_yp = 0.0, o_ya = 0.0, o_kxp = 0.0, o_kxa = 0.0, o_qs = 0.0, o_add = 0.0;
         if (lead) {
           o_qs = lv(qs + i);
@@ -680,7 +697,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
             s_cx.rp = P.rpL; s_cx.ci = P.ciL; s_cx.kv = P.kvL; s_cx.tgt = xp; s_cx.park = P.tmp;
           }
           __syncthreads();
-          phase_tiles<kB_PARK>(&s_cx, &s_ctr, tbuf);
+          phase_tiles<kB_PARK, T>(&s_cx, &s_ctr, tbuf);
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -695,9 +712,9 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
           else { s_cx.r1 = y; s_cx.r2 = Kx; s_cx.e2 = yp; s_cx.e3 = Kxp; }
         }
         __syncthreads();
-        if (pending && !r2) phase_tiles<kB_RA>(&s_cx, &s_ctr, tbuf);
-        else if (pending) phase_tiles<kB_R2>(&s_cx, &s_ctr, tbuf);
-        else phase_tiles<kB_NOP>(&s_cx, &s_ctr, tbuf);
+        if (pending && !r2) phase_tiles<kB_RA, T>(&s_cx, &s_ctr, tbuf);
+        else if (pending) phase_tiles<kB_R2, T>(&s_cx, &s_ctr, tbuf);
+        else phase_tiles<kB_NOP, T>(&s_cx, &s_ctr, tbuf);
         __syncthreads();
         double t2[2];
         lean_reduce(t2);
@@ -730,7 +747,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         }
       }
       if (pending && !r2) {
-        double *t = y; y = yp; yp = t;
+        T *t = y; y = yp; yp = t;
         t = Kx; Kx = Kxp; Kxp = t;
       }
       pending = false;
@@ -814,12 +831,12 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         const bool ok = j < n;
         const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, yp, tbuf);
         if (ok && glt == 0) {
-          KTyp[j] = s;
+          KTyp[j] = (T)s;
           if (!r2) {
-            xa[j] += theta * (xp[j] - xa[j]);
+            xa[j] = (T)((double)xa[j] + theta * ((double)xp[j] - (double)xa[j]));
           } else {
-            x[j] = ha * (rf1 * xp[j] - rf0 * x[j]) + hb * xa[j];
-            KTy[j] = ha * (rf1 * s - rf0 * KTy[j]) + hb * KTya[j];
+            x[j] = (T)(ha * (rf1 * (double)xp[j] - rf0 * (double)x[j]) + hb * (double)xa[j]);
+            KTy[j] = (T)(ha * (rf1 * s - rf0 * (double)KTy[j]) + hb * (double)KTya[j]);
             const double dc = P.Dc[j];
             kkt_col_acc(v, true, dc, xp[j], s, P.c0[j], cs[j], P.l0[j], P.ls[j], P.u0[j], P.us[j]);
             const double d = xp[j] - xr[j];
@@ -830,11 +847,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       }
       for (int i = gtid; i < m; i += gthreads) {
         if (!r2) {
-          ya[i] += theta * (yp[i] - ya[i]);
+          ya[i] = (T)((double)ya[i] + theta * ((double)yp[i] - (double)ya[i]));
         } else {
           const double ypi = yp[i], kxp = Kxp[i];
-          y[i] = ha * (rf1 * ypi - rf0 * y[i]) + hb * ya[i];
-          Kx[i] = ha * (rf1 * kxp - rf0 * Kx[i]) + hb * Kxa[i];
+          y[i] = (T)(ha * (rf1 * ypi - rf0 * (double)y[i]) + hb * (double)ya[i]);
+          Kx[i] = (T)(ha * (rf1 * kxp - rf0 * (double)Kx[i]) + hb * (double)Kxa[i]);
           kkt_row_acc(v, true, i < m1, P.Dr[i], ypi, kxp, P.q0[i], qs[i]);
           const double d = ypi - yr[i];
           v[5] += d * d;
@@ -842,7 +859,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         }
       }
       if (!r2) {
-        double *t = x; x = xp; xp = t;
+        T *t = x; x = xp; xp = t;
         t = KTy; KTy = KTyp; KTyp = t;
         t = y; y = yp; yp = t;
         t = Kx; Kx = Kxp; Kxp = t;
@@ -851,7 +868,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       if (r2) block_partials<12, (3u << 10)>(v, next_part(), s_red);
     }
     grid.sync();
-    const double *cx, *cy, *cKx, *cKTy;
+    const T *cx, *cy, *cKx, *cKTy;
     double metric, dx2, dy2;
     if (!r2) {
       // average's products (2 SpMVs) fused with all KKT / distance partials
@@ -864,7 +881,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         const bool ok = i < m;
         const double s = row_dot(i, ok, m, G, gl, P.rp, P.ci, P.kv, xa, tbuf);
         if (ok && gl == 0) {
-          Kxa[i] = s;
+          Kxa[i] = (T)s;
           const double dr = P.Dr[i], yai = ya[i], yi = y[i], kxi = Kx[i], q0 = P.q0[i], qsi = qs[i];
           kkt_row_acc(v + 0, true, i < m1, dr, yai, s, q0, qsi);
           kkt_row_acc(v + 4, true, i < m1, dr, yi, kxi, q0, qsi);
@@ -881,7 +898,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
         const bool ok = j < n;
         const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, ya, tbuf);
         if (ok && glt == 0) {
-          KTya[j] = s;
+          KTya[j] = (T)s;
           const double dc = P.Dc[j], xaj = xa[j], xj = x[j], ktj = KTy[j];
           const double c0 = P.c0[j], csj = cs[j], l0 = P.l0[j], lsj = P.ls[j], u0 = P.u0[j], usj = P.us[j];
           kkt_col_acc(v + 0, true, dc, xaj, s, c0, csj, l0, lsj, u0, usj);
@@ -934,11 +951,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams P) {
       omega = primal_weight(omega, sqrt(dx2), sqrt(dy2));
       inv_omega = 1.0 / omega;
       for (int j = gtid; j < n; j += gthreads) {
-        const double xv = cx[j], kt = cKTy[j];
+        const T xv = cx[j], kt = cKTy[j];
         x[j] = xv; xr[j] = xv; xa[j] = xv; KTy[j] = kt; KTya[j] = kt;
       }
       for (int i = gtid; i < m; i += gthreads) {
-        const double yv = cy[i], kx = cKx[i];
+        const T yv = cy[i], kx = cKx[i];
         y[i] = yv; yr[i] = yv; ya[i] = yv; Kx[i] = kx; Kxa[i] = kx;
       }
       k_in = 0;
@@ -1014,13 +1031,18 @@ __global__ void split_fill(int m, int h, const int32_t *__restrict__ rp, const i
   }
 }
 
-// The two-pass phase B pays when x' (8n bytes) is past the L2-resident knee of random gathers
-// (~64-72 MB, profiles/gather_rates.json) and the rows use the warp-tile mapping.
-// MPAX_GRID_SPLIT=1 forces it (tests), =0 disables it.
-bool split_wanted(const DevProblem &D) {
+// The two-pass phase B pays when x' (elem x n bytes: 8 fp64, 4 fp32 storage) is past the
+// L2-resident knee of random gathers (~64-72 MB, profiles/gather_rates.json) and the rows use the
+// warp-tile mapping.  MPAX_GRID_SPLIT=1 forces it (tests), =0 disables it.
+bool split_wanted(const DevProblem &D, int elem) {
   const char *e = getenv("MPAX_GRID_SPLIT");
   if (e) return atoi(e) == 1 && tile_mapping_ok(D.avg_row, D.max_row) && D.n >= 2;
-  return tile_mapping_ok(D.avg_row, D.max_row) && 8.0 * (double)D.n > 64e6;
+  return tile_mapping_ok(D.avg_row, D.max_row) && (double)elem * (double)D.n > 64e6;
+}
+
+__global__ void round_f32(int64_t n, const double *__restrict__ a, float *__restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = __double2float_rn(a[i]);
 }
 
 inline int pow2_floor(double v) {
@@ -1031,8 +1053,8 @@ inline int pow2_floor(double v) {
 
 }  // namespace
 
-int grid_split_prepare(DevProblem &P, cudaStream_t s) {
-  if (P.split_h > 0 || !split_wanted(P) || P.nnz <= 0) return LP_OK;
+int grid_split_prepare(DevProblem &P, cudaStream_t s, int elem) {
+  if (P.split_h > 0 || !split_wanted(P, elem) || P.nnz <= 0) return LP_OK;
   const int m = (int)P.m, h = (int)(P.n / 2);
   const int64_t nnz = P.nnz;
   // one allocation: rpL, rpR (m+1 each), ciL/ciR (nnz), kvL/kvR (nnz), scan scratch
@@ -1062,8 +1084,35 @@ int grid_split_prepare(DevProblem &P, cudaStream_t s) {
   return LP_OK;
 }
 
-int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cudaStream_t s, double **work,
-               size_t *work_bytes) {
+int grid_f32_prepare(DevProblem &P, cudaStream_t s) {
+  const int64_t nnz = P.nnz;
+  if (nnz <= 0) return LP_OK;
+  const bool halves = P.split_h > 0;
+  if (P.f32_mem && P.f32_split_h == (halves ? P.split_h : 0)) return LP_OK;
+  if (P.f32_mem) MPAX_CUDA(cudaFreeAsync(P.f32_mem, s));
+  P.f32_mem = nullptr;
+  float *b = nullptr;
+  MPAX_CUDA(cudaMallocAsync((void **)&b, (size_t)(halves ? 3 : 2) * (size_t)nnz * sizeof(float), s));
+  P.f32_mem = b;
+  P.kv32 = b; P.tkv32 = b + nnz;
+  MPAX_LAUNCH(round_f32, 148 * 8, 256, 0, s, nnz, P.kv, P.kv32);
+  MPAX_LAUNCH(round_f32, 148 * 8, 256, 0, s, nnz, P.tkv, P.tkv32);
+  if (halves) {   // kvL, kvR are one contiguous block of nnz values (grid_split_prepare)
+    P.kvL32 = b + 2 * nnz;
+    P.kvR32 = P.kvL32 + (P.kvR - P.kvL);
+    MPAX_LAUNCH(round_f32, 148 * 8, 256, 0, s, nnz, P.kvL, P.kvL32);
+  }
+  MPAX_CHECK_LAUNCH();
+  P.f32_split_h = halves ? P.split_h : 0;
+  return LP_OK;
+}
+
+namespace {
+
+template <typename T>
+int grid_launch(const DevProblem &D, const lp_options &o, const GridLaunch &L, cudaStream_t s, double **work,
+                size_t *work_bytes) {
+  constexpr bool f32 = sizeof(T) == sizeof(float);
   int dev = 0, sms = 0, coop = 0;
   MPAX_CUDA(cudaGetDevice(&dev));
   MPAX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1079,7 +1128,7 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   const char *env = getenv("MPAX_GRID_MINB");
   const int64_t tiles = (D.m + 31) / 32 + (D.n + 31) / 32;
   const int minb = env ? (atoi(env) == 1 ? 1 : 2) : (tiles < 4 * 2 * (int64_t)sms * (kBS / 32) ? 1 : 2);
-  void *kfn = minb == 1 ? (void *)grid_kernel<1> : (void *)grid_kernel<2>;
+  void *kfn = minb == 1 ? (void *)grid_kernel<1, T> : (void *)grid_kernel<2, T>;
   int per_sm = 0;
   MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kBS, 0));
   if (per_sm < 1) return LP_ERR_UNSUPPORTED;
@@ -1091,8 +1140,11 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   const int64_t ntile = (std::max(n, m) + 31) / 32;
   const size_t ntp = 2 * (size_t)blocks * (size_t)((ntile + blocks - 1) / blocks);  // P.tpart slots
   const size_t ntpA = 2 * (size_t)((n + 31) / 32) + 1;   // + the counter (the lean sweep writes 2 per tile)
-  const size_t vec = (size_t)(8 * n + 9 * m) + 2 * (size_t)blocks * kNP + ntp + ntpA;   // + tmp (m)
-  const size_t need = vec * sizeof(double);
+  // fp64 block: per-CTA / per-tile partials, tmp (m), the counter; then the T block: 8n + 8m
+  // iterate vectors (+ l~, u~ copies for fp32 storage)
+  const size_t dbl = (size_t)m + 2 * (size_t)blocks * kNP + ntp + ntpA;
+  const size_t tvec = (size_t)(8 * n + 8 * m) + (f32 ? 2 * (size_t)n : 0);
+  const size_t need = dbl * sizeof(double) + tvec * sizeof(T);
   if (*work_bytes < need) {
     if (*work) MPAX_CUDA(cudaFreeAsync(*work, s));
     *work = nullptr;
@@ -1100,18 +1152,23 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
     *work_bytes = need;
   }
   double *w = *work;
-  GridParams P;
+  T *wt = (T *)(w + dbl);
+  GridParams<T> P;
   P.n = n; P.m = m; P.m1 = D.m1;
   P.rp = D.rp; P.ci = D.ci; P.trp = D.trp; P.tci = D.tci;
-  P.kv = D.kv; P.tkv = D.tkv; P.Dr = D.Dr; P.Dc = D.Dc; P.ls = D.ls; P.us = D.us; P.l0 = D.l0; P.u0 = D.u0;
+  if constexpr (f32) { P.kv = D.kv32; P.tkv = D.tkv32; }
+  else { P.kv = D.kv; P.tkv = D.tkv; }
+  P.Dr = D.Dr; P.Dc = D.Dc; P.ls = D.ls; P.us = D.us; P.l0 = D.l0; P.u0 = D.u0;
   P.c0 = L.c0; P.q0 = L.q0; P.X0 = L.X0; P.Y0 = L.Y0; P.kmax = D.kmax; P.sigma = D.sigma; P.tab = D.tab;
   P.const_step = o.step_rule == LP_STEP_CONSTANT;
-  P.cs = w; w += n;
-  P.x = w; w += n; P.KTy = w; w += n; P.xp = w; w += n; P.KTyp = w; w += n; P.xa = w; w += n; P.KTya = w; w += n;
-  P.xr = w; w += n;
-  P.qs = w; w += m;
-  P.y = w; w += m; P.Kx = w; w += m; P.yp = w; w += m; P.Kxp = w; w += m; P.ya = w; w += m; P.Kxa = w; w += m;
-  P.yr = w; w += m;
+  P.cs = wt; wt += n;
+  P.x = wt; wt += n; P.KTy = wt; wt += n; P.xp = wt; wt += n; P.KTyp = wt; wt += n; P.xa = wt; wt += n;
+  P.KTya = wt; wt += n; P.xr = wt; wt += n;
+  P.qs = wt; wt += m;
+  P.y = wt; wt += m; P.Kx = wt; wt += m; P.yp = wt; wt += m; P.Kxp = wt; wt += m; P.ya = wt; wt += m;
+  P.Kxa = wt; wt += m; P.yr = wt; wt += m;
+  P.lsw = nullptr; P.usw = nullptr;
+  if constexpr (f32) { P.lsw = wt; wt += n; P.usw = wt; wt += n; }
   P.part = w; w += 2 * (size_t)blocks * kNP;
   P.tpart = w; w += ntp;
   P.tmp = w; w += m;
@@ -1148,14 +1205,28 @@ int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cu
   if (const char *e = getenv("MPAX_GRID_DYN")) P.dyn = atoi(e);
   P.lean = 3;
   if (const char *e = getenv("MPAX_GRID_LEAN")) P.lean = atoi(e);   // experiments: 0 = the inlined sweeps
-  P.split = (D.split_h > 0 && split_wanted(D) && P.gk == 1 && (P.dyn & 2)) ? 1 : 0;
-  P.rpL = D.rpL; P.ciL = D.ciL; P.kvL = D.kvL; P.rpR = D.rpR; P.ciR = D.ciR; P.kvR = D.kvR;
+  P.split = (D.split_h > 0 && split_wanted(D, (int)sizeof(T)) && P.gk == 1 && (P.dyn & 2) &&
+             (!f32 || D.f32_split_h == D.split_h)) ? 1 : 0;
+  P.rpL = D.rpL; P.ciL = D.ciL; P.rpR = D.rpR; P.ciR = D.ciR;
+  if constexpr (f32) { P.kvL = D.kvL32; P.kvR = D.kvR32; }
+  else { P.kvL = D.kvL; P.kvR = D.kvR; }
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
   void *args[] = {&P};
   MPAX_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(kBS), args, 0, s));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   MPAX_CHECK_LAUNCH();
   return LP_OK;
+}
+
+}  // namespace
+
+int grid_solve(const DevProblem &D, const lp_options &o, const GridLaunch &L, cudaStream_t s, double **work,
+               size_t *work_bytes) {
+  if (o.precision == LP_FP32) {
+    if (D.nnz > 0 && !D.f32_mem) return LP_ERR_INVALID_ARGUMENT;   // grid_f32_prepare first
+    return grid_launch<float>(D, o, L, s, work, work_bytes);
+  }
+  return grid_launch<double>(D, o, L, s, work, work_bytes);
 }
 
 }  // namespace mpax

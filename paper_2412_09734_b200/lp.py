@@ -17,6 +17,7 @@ LP_OPTIMAL, LP_ITERATION_LIMIT, LP_NUMERICAL_ERROR, LP_PRIMAL_INFEASIBLE, LP_DUA
 RAPDHG, R2HPDHG = 0, 1
 PATH_AUTO, PATH_INSTANCE, PATH_GRID, PATH_DMMA = 0, 1, 2, 3
 STEP_ADAPTIVE, STEP_CONSTANT = 0, 1
+FP64, FP32 = 0, 1
 
 EXPORTED_SYMBOLS = [
     "lp_default_options", "lp_create", "lp_create_batch", "lp_update_batch", "lp_solve", "lp_solve_batch",
@@ -49,7 +50,7 @@ class Options(C.Structure):
                 ("iteration_limit", C.c_int64), ("check_frequency", C.c_int32), ("algorithm", C.c_int32),
                 ("warm_start", C.c_int32), ("feasibility_polishing", C.c_int32), ("verbose", C.c_int32),
                 ("display_frequency", C.c_int32), ("path", C.c_int32), ("step_rule", C.c_int32),
-                ("reflection", C.c_double)]
+                ("reflection", C.c_double), ("precision", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Result(C.Structure):
@@ -293,6 +294,9 @@ def default_options(**kw) -> Options:
     rule = kw.pop("step_rule", None)
     if rule is not None:
         o.step_rule = STEP_CONSTANT if rule in ("constant", STEP_CONSTANT) else STEP_ADAPTIVE
+    prec = kw.pop("precision", None)
+    if prec is not None:
+        o.precision = FP32 if prec in ("fp32", FP32) else FP64
     alg = kw.pop("algorithm", None)
     if alg is not None:
         o.algorithm = R2HPDHG if alg in ("r2", "r2hpdhg", "r2HPDHG", R2HPDHG) else RAPDHG

@@ -22,16 +22,22 @@ s = mp.Solver(prob)
 torch.cuda.synchronize()
 print(f"create (validate+transpose+precondition) {time.time() - t0:.3f}s", flush=True)
 res = {}
+precs = os.environ.get("C5_PREC", "fp64").split(",")
 for alg in ("ra", "r2"):
-    r = s.solve(algorithm=alg, path=mp.PATH_GRID, iteration_limit=int(os.environ.get("C5_LIMIT", "4000")))
-    pair = 24 * lp.nnz + 4 * (lp.m + 1) + 4 * (lp.n + 1) + 8 * lp.n + 8 * lp.m
-    upd = 64 * lp.n + 56 * lp.m if alg == "ra" else 88 * lp.n + 88 * lp.m
-    gbs = r["iterations"] * (pair + upd) / r["solve_seconds"] / 1e9
-    res[alg] = r
-    print(f"{alg}: status {r['status']} it {r['iterations']} att {r['attempts']} restarts {r['restarts']} "
-          f"time {r['solve_seconds']:.3f}s  {r['solve_seconds'] * 1e6 / r['attempts']:.0f} us/attempt  "
-          f"{gbs:.0f} GB/s  rel_kkt {r['rel_kkt']:.2e}  obj err {abs(r['primal_objective'] - lp.obj_star) / (1 + abs(lp.obj_star)):.2e}",
-          flush=True)
+    for prec in precs:
+        e = 8 if prec == "fp64" else 4
+        for _ in range(int(os.environ.get("C5_REPS", "1"))):   # > 1: the last solve is reported (warm)
+            r = s.solve(algorithm=alg, path=mp.PATH_GRID, iteration_limit=int(os.environ.get("C5_LIMIT", "4000")),
+                        precision=prec)
+        pair = 2 * (4 + e) * lp.nnz + 4 * (lp.m + 1) + 4 * (lp.n + 1) + e * lp.n + e * lp.m
+        upd = e * (8 * lp.n + 7 * lp.m if alg == "ra" else 11 * lp.n + 11 * lp.m)
+        gbs = r["iterations"] * (pair + upd) / r["solve_seconds"] / 1e9
+        if prec == "fp64" or alg not in res:
+            res[alg] = r
+        print(f"{alg} {prec}: status {r['status']} it {r['iterations']} att {r['attempts']} restarts {r['restarts']} "
+              f"time {r['solve_seconds']:.3f}s  {r['solve_seconds'] * 1e6 / r['attempts']:.0f} us/attempt  "
+              f"{gbs:.0f} GB/s  rel_kkt {r['rel_kkt']:.2e}  obj err {abs(r['primal_objective'] - lp.obj_star) / (1 + abs(lp.obj_star)):.2e}",
+              flush=True)
 if os.environ.get("C5_ORACLE"):
     import oracle
     oracle.set_threads(len(os.sched_getaffinity(0)))

@@ -16,7 +16,8 @@ def parity_log(test, **counts):
     Appends one JSON line to $MPAX_PARITY_LOG when set (the GPU runs point it at
     gpurun_out/), and prints it (visible with pytest -s / -rA)."""
     import json
-    line = json.dumps(dict(test=test, **{k: (int(v) if hasattr(v, "__int__") else v) for k, v in counts.items()}))
+    conv = lambda v: int(v) if hasattr(v, "__index__") else float(v) if hasattr(v, "__float__") else v  # noqa: E731
+    line = json.dumps(dict(test=test, **{k: conv(v) for k, v in counts.items()}))
     print("PARITY", line)
     path = os.environ.get("MPAX_PARITY_LOG")
     if path:

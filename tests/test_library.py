@@ -62,3 +62,32 @@ def test_no_oracle_import_in_product():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle/", ""), f
+
+
+def test_abi_struct_layouts(tmp_path):
+    """The binding's ctypes structs match include/lp.h byte for byte (sizes and every field
+    offset, from a C program compiled against the header)."""
+    import ctypes as C
+
+    import paper_2412_09734_b200 as mp
+    from paper_2412_09734_b200 import lp as mlp
+    structs = {"lp_options": mlp.Options, "lp_result": mlp.Result, "lp_problem_desc": mlp.ProblemDesc}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "lp.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'  printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                        check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[cname]) == C.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert int(got[f"{cname}.{f}"]) == getattr(py, f).offset, (cname, f)
+    o = mp.default_options()
+    assert o.precision == mp.FP64 and o.reflection == 1.0 and o.step_rule == mp.STEP_ADAPTIVE
+    assert mp.default_options(precision="fp32").precision == mp.FP32
