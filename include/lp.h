@@ -140,10 +140,10 @@ typedef struct {
   int32_t check_frequency;      /* 64 */
   int32_t algorithm;            /* lp_algorithm, default LP_R2HPDHG */
   int32_t warm_start;           /* informational; a non-NULL x0 / y0 is what warm-starts */
-  int32_t feasibility_polishing;/* 0; 1: polish OPTIMAL results (see below; not on sharded handles) */
+  int32_t feasibility_polishing;/* 0; 1: polish OPTIMAL results (see below; every engine) */
   int32_t verbose;              /* 0; 1: one line per display_frequency-th check of every
-                                   instance (device printf, flushed when the solve returns; tiny,
-                                   instance and grid kernels -- the DMMA and sharded engines ignore it) */
+                                   instance (device printf, flushed when the solve returns; every
+                                   engine -- the sharded one prints from rank 0's first shard) */
   int32_t display_frequency;    /* 10, in checks */
   int32_t path;                 /* lp_path, default LP_PATH_AUTO */
   int32_t step_rule;            /* lp_step_rule, default LP_STEP_ADAPTIVE */
@@ -152,7 +152,11 @@ typedef struct {
                                    P:64, rho < 1 the partial reflection of SURVEY §8(f) row 4
                                    (reading 38); unused by raPDHG */
   int32_t precision;            /* lp_precision, default LP_FP64 */
-  int32_t reserved;             /* 0 */
+  int32_t sharded_exchange;     /* row-sharded engine: 0 = variant A, all-reduce of the
+                                   K~'y partials, n-side update replicated on every GPU (default);
+                                   1 = variant B, reduce-scatter of the partials, n-side update on
+                                   each GPU's slice of n/p columns, all-gather of x' (and of the
+                                   average before a check); other engines ignore it */
 } lp_options;
 
 /* Feasibility polishing (reading 36).
@@ -185,7 +189,7 @@ typedef struct {
 } lp_result;
 
 /* Fills o with the Appendix defaults: 1e-4, 1e-4, 1e-8, 1e-8, 1e-6,
- * INT64_MAX, 64, LP_R2HPDHG, 0, 0, 0, 10, LP_PATH_AUTO, LP_STEP_ADAPTIVE, 1.0, LP_FP64. */
+ * INT64_MAX, 64, LP_R2HPDHG, 0, 0, 0, 10, LP_PATH_AUTO, LP_STEP_ADAPTIVE, 1.0, LP_FP64, 0. */
 void lp_default_options(lp_options *o);
 
 /* Create a single-LP handle: validates, uploads, builds
@@ -266,6 +270,21 @@ int lp_get_shape(lp_handle h, int64_t *n, int64_t *m1, int64_t *m2, int64_t *bat
  * written in place; LP_HOST: staged through device copies.  Blocks until the
  * products are written. */
 int lp_get_scaling(lp_handle h, double *Dr, double *Dc, int32_t memory);
+
+/* Decision log of the grid path (the parity tests' tool for finding the
+ * first decision where the GPU and the oracle part ways).  att: att_cap x 4
+ * doubles, one row per line-search attempt j = 1, 2, ... : (j, accepted, eta, eta_bar) with
+ * eta the step tried and eta_bar = M / (2|I|) (contract step 3); chk: chk_cap x 6 doubles, one
+ * row per check: (k, metric, ref, last, restart, outcome) with outcome 0 = no termination,
+ * 1 = optimal (raPDHG: the average; r2HPDHG: the candidate), 2 = optimal (raPDHG: the current
+ * iterate), 3 = infeasibility certificate; metric = 0 where the oracle logs 0 -- the same
+ * records as the oracle's ora_log.  Rows past the capacity are dropped; rows not reached are
+ * left untouched.  The buffers must be device-accessible (device or mapped pinned memory) and
+ * stay valid through every later lp_solve on the handle; NULL / capacity 0 switches a log off.
+ * Single-LP handles only; a solve that does not take the grid path returns
+ * LP_ERR_UNSUPPORTED while a log is set.  Polishing sub-solves are not logged. */
+int lp_set_decision_log(lp_handle h, double *att, int64_t att_cap, double *chk, int64_t chk_cap);
+
 int lp_spmv_scaled(lp_handle h, const double *v, double *Kv, const double *w, double *KTw,
                    int32_t memory);
 
@@ -286,6 +305,26 @@ int lp_create_sharded(const lp_problem_desc *local_rows, int64_t global_row_offs
  * CURRENT device and a fixed-order device sum in place of NCCL: the partitioned
  * arithmetic of lp_create_sharded, testable on one GPU.  y covers all m rows. */
 int lp_create_sharded_virtual(const lp_problem_desc *p, int32_t shards, void *cuda_stream, lp_handle *out);
+
+/* ---- the sharding axis (reading 33) ----
+ * Row sharding exchanges the n-long K~'y partials every attempt, column sharding the m-long
+ * K~x' partials: the shorter vector should travel.  lp_shard_axis(m, n) = LP_SHARD_COLS iff
+ * m < n, else LP_SHARD_ROWS.
+ * Column-sharded engine: process `rank` passes ITS block of columns, columns
+ * [global_col_offset, global_col_offset + n_local) of K as an m x n_local CSR with LOCAL
+ * column indices (every row, m1 / m2 global), the FULL q (m) and its c, l, u (n_local).  Row
+ * norms of the preconditioner and every cross-shard sum go through ncclAllReduce.  lp_solve
+ * takes x0 (this rank's n_local columns) and y0 (m); lp_get_solution returns this rank's
+ * columns of x and of the reduced costs and the full y.  The constant step rule is not built
+ * for column sharding (LP_ERR_UNSUPPORTED).  lp_create_sharded_virtual_axis: `shards` blocks
+ * of rows or columns (balanced by nnz; LP_SHARD_AUTO picks lp_shard_axis) on the current
+ * device with the fixed-order device sum; x, y and the reduced costs then cover the whole LP. */
+enum lp_shard_axis { LP_SHARD_ROWS = 0, LP_SHARD_COLS = 1, LP_SHARD_AUTO = 2 };
+int lp_shard_axis(int64_t m, int64_t n);
+int lp_create_sharded_cols(const lp_problem_desc *local_cols, int64_t global_col_offset, int64_t n_global,
+                           void *nccl_comm, int rank, int nranks, void *cuda_stream, lp_handle *out);
+int lp_create_sharded_virtual_axis(const lp_problem_desc *p, int32_t shards, int32_t axis, void *cuda_stream,
+                                   lp_handle *out);
 
 /* NCCL communicator helpers (so callers need no NCCL headers): rank 0 calls
  * lp_nccl_unique_id (128 bytes) and broadcasts it (e.g. torch.distributed),

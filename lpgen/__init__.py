@@ -205,6 +205,45 @@ def g_rand(m: int, n: int, r: int, seed: int, m1: Optional[int] = None) -> LP:
     return lp
 
 
+def g_powerlaw(m: int, n: int, r_mean: float, seed: int, alpha: float = 1.6, r_max: Optional[int] = None,
+               m1: Optional[int] = None) -> LP:
+    """G-POWERLAW: G-RAND's construction (known optimum) with skewed row lengths -- lengths drawn
+    from a Pareto tail with exponent `alpha`, scaled to mean ~r_mean and clipped at r_max (default
+    n // 2): a few rows hold thousands of entries, most a handful (SURVEY north star (1):
+    "warp-per-row / merge-path" load balancing; the scale-free degree mixes of real LPs).
+    Columns per row are distinct and uniform; every column gets at least one entry."""
+    rng = np.random.default_rng(seed)
+    m1 = m // 2 if m1 is None else m1
+    m2 = m - m1
+    r_max = n // 2 if r_max is None else r_max
+    raw = rng.pareto(alpha, size=m) + 1.0
+    lens = np.clip(np.round(raw * (r_mean / raw.mean())), 1, r_max).astype(np.int64)
+    rows = []
+    for i in range(m):
+        rows.append(np.sort(rng.choice(n, size=int(lens[i]), replace=False)))
+    cover = np.zeros(n, bool)
+    for c in rows:
+        cover[c] = True
+    for j in np.nonzero(~cover)[0]:
+        i = int(rng.integers(0, m))
+        rows[i] = np.sort(np.append(rows[i], j))
+    lens = np.array([c.size for c in rows], np.int64)
+    row_ptr = np.zeros(m + 1, np.int64)
+    np.cumsum(lens, out=row_ptr[1:])
+    col_idx = np.concatenate(rows).astype(np.int32)
+    val = rng.normal(size=col_idx.size)
+    l, u, xs, lam = _bounds_and_primal(rng, n)
+    Kx = _csr_matvec(row_ptr, col_idx, val, xs)
+    ys, q = _duals_and_rhs(rng, Kx, m1, m2)
+    c = _csr_rmatvec(row_ptr, col_idx, val, ys, n) + lam
+    lp = LP(n, m1, m2, row_ptr, col_idx, val, c, q, l, u)
+    lp.obj_star = float(c @ xs)
+    lp.x_star, lp.y_star, lp.lam_star = xs, ys, lam
+    lp.meta = dict(generator="G-POWERLAW", m=m, n=n, r_mean=r_mean, alpha=alpha, seed=seed,
+                   max_row=int(lens.max()))
+    return lp
+
+
 # ----------------------------------------------------------------- G-GRID --
 
 def grid_arcs(k: int = 5):

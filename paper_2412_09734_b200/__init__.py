@@ -10,5 +10,5 @@ from .lp import (  # noqa: F401
     RAPDHG, R2HPDHG,
     PATH_AUTO, PATH_INSTANCE, PATH_GRID, PATH_DMMA, STEP_ADAPTIVE, STEP_CONSTANT, FP64, FP32, LpError, Problem, Options, Result, Solver, BatchSolver,
     create_lp, default_options, lib, library_path, launch_count, selftest_division, EXPORTED_SYMBOLS, RESULT_DTYPE,
-    ShardedSolver, row_partition, local_rows, nccl_unique_id, nccl_comm_init, nccl_comm_destroy,
+    ShardedSolver, row_partition, local_rows, col_partition, local_cols, shard_axis, SHARD_ROWS, SHARD_COLS, SHARD_AUTO, nccl_unique_id, nccl_comm_init, nccl_comm_destroy,
 )

@@ -49,6 +49,9 @@ struct lp_handle_s {
   ShardedLP *sharded = nullptr;  // row-sharded handle (lp_create_sharded / _virtual)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool solved = false;
+  // decision log of the grid path (lp_set_decision_log): device-visible buffers, or null
+  double *alog = nullptr, *clog = nullptr;
+  int64_t acap = 0, ccap = 0;
 };
 
 namespace {
@@ -405,12 +408,13 @@ int check_options(const lp_options *o) {
     return fail(LP_ERR_INVALID_ARGUMENT, "bad step_rule");
   if (!(o->reflection >= 0.0 && o->reflection <= 1.0)) return fail(LP_ERR_INVALID_ARGUMENT, "reflection not in [0, 1]");
   if (o->precision != LP_FP64 && o->precision != LP_FP32) return fail(LP_ERR_INVALID_ARGUMENT, "bad precision");
+  if (o->sharded_exchange != 0 && o->sharded_exchange != 1) return fail(LP_ERR_INVALID_ARGUMENT, "bad sharded_exchange");
   return LP_OK;
 }
 
 int run_sharded(lp_handle h, const lp_options *o, const double *X0, const double *Y0, lp_result *out) {
   cudaStream_t s = h->stream;
-  const int64_t n = sharded_n(h->sharded), ml = sharded_m_local(h->sharded);
+  const int64_t n = sharded_n_local(h->sharded), ml = sharded_m_local(h->sharded);
   const double *dX0 = nullptr, *dY0 = nullptr;
   if (X0) {
     if (!h->X0) TRY(dalloc(&h->X0, n, s));
@@ -422,7 +426,7 @@ int run_sharded(lp_handle h, const lp_options *o, const double *X0, const double
     MPAX_CUDA(cudaMemcpyAsync(h->Y0, Y0, (size_t)ml * sizeof(double), cudaMemcpyDefault, s));
     dY0 = h->Y0;
   }
-  const int rc = sharded_solve(*h->sharded, *o, dX0, dY0, out);
+  const int rc = sharded_solve_polished(*h->sharded, *o, dX0, dY0, out);
   if (rc == LP_OK) h->solved = true;
   return rc;
 }
@@ -522,7 +526,6 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
   if (memory != LP_HOST && memory != LP_DEVICE) return fail(LP_ERR_INVALID_ARGUMENT, "bad memory kind");
   if (h->sharded) {
     if (o->precision == LP_FP32) return fail(LP_ERR_UNSUPPORTED, "fp32 storage is a grid-path option");
-    if (o->feasibility_polishing) return fail(LP_ERR_UNSUPPORTED, "feasibility polishing on a sharded handle");
     return run_sharded(h, o, X0, Y0, out);
   }
   cudaStream_t s = h->stream;
@@ -545,6 +548,8 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
   if (o->path == LP_PATH_GRID && B != 1) return fail(LP_ERR_UNSUPPORTED, "the grid path solves one LP");
   if (o->precision == LP_FP32 && !use_grid)
     return fail(LP_ERR_UNSUPPORTED, "fp32 storage is a grid-path option (one large LP; DESIGN.md reading 39)");
+  if ((h->alog || h->clog) && !use_grid)
+    return fail(LP_ERR_UNSUPPORTED, "the decision log is recorded by the grid path only");
   // a batch sharing a dense K: fp64 tensor-core path (auto from 8 instances on)
   const bool dmma = !use_grid && h->P.dense && (o->path == LP_PATH_DMMA || (o->path == LP_PATH_AUTO && B >= 8));
   if (dmma) {
@@ -563,6 +568,7 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
       GridLaunch G;
       G.c0 = L.C0; G.q0 = L.Q0; G.X0 = L.X0; G.Y0 = L.Y0; G.X = L.X; G.Y = L.Y; G.L = L.L; G.res = L.res;
       G.polish_mode = L.polish_mode;
+      if (L.polish_mode == 0) { G.alog = h->alog; G.clog = h->clog; G.acap = h->acap; G.ccap = h->ccap; }
       if (int rs = grid_split_prepare(h->P, s, oo.precision == LP_FP32 ? 4 : 8)) return rs;
       if (oo.precision == LP_FP32)
         if (int rs = grid_f32_prepare(h->P, s)) return rs;
@@ -674,7 +680,7 @@ void lp_default_options(lp_options *o) {
   o->step_rule = LP_STEP_ADAPTIVE;
   o->reflection = 1.0;
   o->precision = LP_FP64;
-  o->reserved = 0;
+  o->sharded_exchange = 0;
 }
 
 int lp_create(const lp_problem_desc *p, void *cuda_stream, lp_handle *out) {
@@ -794,7 +800,7 @@ int lp_get_solutions(lp_handle h, double *X, double *Y, int32_t memory) {
 int lp_get_shape(lp_handle h, int64_t *n, int64_t *m1, int64_t *m2, int64_t *batch) {
   if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
   if (h->sharded) {
-    if (n) *n = sharded_n(h->sharded);
+    if (n) *n = sharded_n_local(h->sharded);
     if (m1) *m1 = 0;
     if (m2) *m2 = sharded_m_local(h->sharded);
     if (batch) *batch = 1;
@@ -804,6 +810,17 @@ int lp_get_shape(lp_handle h, int64_t *n, int64_t *m1, int64_t *m2, int64_t *bat
   if (m1) *m1 = h->P.m1;
   if (m2) *m2 = h->P.m2;
   if (batch) *batch = h->batch;
+  return LP_OK;
+}
+
+int lp_set_decision_log(lp_handle h, double *att, int64_t att_cap, double *chk, int64_t chk_cap) {
+  if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  if (h->sharded || h->is_batch) return fail(LP_ERR_UNSUPPORTED, "the decision log is recorded by the grid path only");
+  if ((att && att_cap < 0) || (chk && chk_cap < 0)) return fail(LP_ERR_INVALID_ARGUMENT, "negative capacity");
+  h->alog = att_cap > 0 ? att : nullptr;
+  h->acap = att_cap > 0 ? att_cap : 0;
+  h->clog = chk_cap > 0 ? chk : nullptr;
+  h->ccap = chk_cap > 0 ? chk_cap : 0;
   return LP_OK;
 }
 
@@ -866,6 +883,106 @@ int lp_create_sharded(const lp_problem_desc *local_rows, int64_t global_row_offs
   std::vector<int64_t> off{global_row_offset};
   const int rc = sharded_create(h->sharded, d, off, local_rows->n, m1_global, m2_global, nccl_comm, rank, nranks,
                                 false);
+  if (rc != LP_OK) {
+    free_handle(h);
+    return fail(rc, "sharded setup failed");
+  }
+  *out = h;
+  return LP_OK;
+}
+
+// Column split of an LP into `shards` blocks balanced by nnz (host-side CSR extraction: setup only).
+static int create_virtual_cols(const lp_problem_desc *p, int32_t shards, void *cuda_stream, lp_handle *out) {
+  const int64_t m = p->m1 + p->m2, n = p->n, nnz = p->nnz;
+  std::vector<int64_t> rp(m + 1);
+  std::vector<int32_t> ci(nnz > 0 ? nnz : 1);
+  std::vector<double> v(nnz > 0 ? nnz : 1);
+  if (cudaMemcpy(rp.data(), p->row_ptr, (m + 1) * sizeof(int64_t), cudaMemcpyDefault) != cudaSuccess ||
+      (nnz && cudaMemcpy(ci.data(), p->col_idx, nnz * sizeof(int32_t), cudaMemcpyDefault) != cudaSuccess) ||
+      (nnz && cudaMemcpy(v.data(), p->values, nnz * sizeof(double), cudaMemcpyDefault) != cudaSuccess))
+    return fail(LP_ERR_CUDA, "CSR read");
+  // column cut balanced by nnz: prefix of the column counts
+  std::vector<int64_t> cc(n + 1, 0);
+  for (int64_t k = 0; k < nnz; ++k) {
+    if (ci[k] < 0 || ci[k] >= n) return fail(LP_ERR_DIMENSION, "column index out of range");
+    cc[ci[k] + 1] += 1;
+  }
+  for (int64_t j = 0; j < n; ++j) cc[j + 1] += cc[j];
+  std::vector<int64_t> cut(shards + 1, 0);
+  cut[shards] = n;
+  for (int g = 1; g < shards; ++g) {
+    cut[g] = std::lower_bound(cc.begin(), cc.end(), nnz * g / shards) - cc.begin();
+    cut[g] = std::min<int64_t>(std::max<int64_t>(cut[g], cut[g - 1]), n);
+  }
+  std::vector<std::vector<int64_t>> lrp(shards);
+  std::vector<std::vector<int32_t>> lci(shards);
+  std::vector<std::vector<double>> lv(shards);
+  std::vector<lp_problem_desc> d(shards);
+  std::vector<int64_t> off(shards);
+  for (int g = 0; g < shards; ++g) {
+    const int64_t c0 = cut[g], c1 = cut[g + 1];
+    lrp[g].assign(m + 1, 0);
+    for (int64_t i = 0; i < m; ++i) {
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+        if (ci[k] >= c0 && ci[k] < c1) { lci[g].push_back((int32_t)(ci[k] - c0)); lv[g].push_back(v[k]); }
+      lrp[g][i + 1] = (int64_t)lci[g].size();
+    }
+    d[g] = *p;
+    d[g].n = c1 - c0;
+    d[g].nnz = (int64_t)lci[g].size();
+    d[g].row_ptr = lrp[g].data();
+    d[g].col_idx = lci[g].empty() ? nullptr : lci[g].data();
+    d[g].values = lv[g].empty() ? nullptr : lv[g].data();
+    d[g].c = p->c + c0;
+    d[g].l = p->l + c0;
+    d[g].u = p->u + c0;
+    d[g].dense = 0;
+    d[g].memory = LP_HOST;   // (sharded setup copies every array with cudaMemcpyDefault)
+    off[g] = c0;
+  }
+  init_pool();
+  lp_handle h = new lp_handle_s();
+  h->stream = (cudaStream_t)cuda_stream;
+  h->sharded = sharded_new(h->stream);
+  const int rc = sharded_create(h->sharded, d, off, n, p->m1, p->m2, nullptr, 0, 1, true, true);
+  if (rc != LP_OK) {
+    free_handle(h);
+    return fail(rc, "sharded setup failed");
+  }
+  *out = h;
+  return LP_OK;
+}
+
+int lp_shard_axis(int64_t m, int64_t n) { return m < n ? LP_SHARD_COLS : LP_SHARD_ROWS; }
+
+int lp_create_sharded_virtual_axis(const lp_problem_desc *p, int32_t shards, int32_t axis, void *cuda_stream,
+                                   lp_handle *out) {
+  TRY(check_desc(p));
+  if (!out || shards < 1 || shards > 64) return fail(LP_ERR_INVALID_ARGUMENT, "shards must be in [1, 64]");
+  if (axis == LP_SHARD_AUTO) axis = lp_shard_axis(p->m1 + p->m2, p->n);
+  if (axis == LP_SHARD_COLS) {
+    if (shards > p->n) return fail(LP_ERR_INVALID_ARGUMENT, "more shards than columns");
+    return create_virtual_cols(p, shards, cuda_stream, out);
+  }
+  if (axis != LP_SHARD_ROWS) return fail(LP_ERR_INVALID_ARGUMENT, "bad axis");
+  return lp_create_sharded_virtual(p, shards, cuda_stream, out);
+}
+
+int lp_create_sharded_cols(const lp_problem_desc *local_cols, int64_t global_col_offset, int64_t n_global,
+                           void *nccl_comm, int rank, int nranks, void *cuda_stream, lp_handle *out) {
+  TRY(check_desc(local_cols));
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks || global_col_offset < 0 ||
+      global_col_offset + local_cols->n > n_global)
+    return fail(LP_ERR_INVALID_ARGUMENT, "bad sharding arguments");
+  if (nranks > 1 && !nccl_comm) return fail(LP_ERR_INVALID_ARGUMENT, "nccl_comm needed for nranks > 1");
+  init_pool();
+  lp_handle h = new lp_handle_s();
+  h->stream = (cudaStream_t)cuda_stream;
+  h->sharded = sharded_new(h->stream);
+  std::vector<lp_problem_desc> d{*local_cols};
+  std::vector<int64_t> off{global_col_offset};
+  const int rc = sharded_create(h->sharded, d, off, n_global, local_cols->m1, local_cols->m2, nccl_comm, rank,
+                                nranks, false, true);
   if (rc != LP_OK) {
     free_handle(h);
     return fail(rc, "sharded setup failed");

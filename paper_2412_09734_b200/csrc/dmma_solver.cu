@@ -59,7 +59,7 @@ struct DmmaParams {
   const double *kmax, *sigma, *tab;
   double eps_abs, eps_rel, eps_pi, eps_di, eps_fp, rho;
   int64_t iter_limit;
-  int32_t check_freq, alg, const_step, polish_mode;
+  int32_t check_freq, alg, const_step, polish_mode, verbose, display_freq;
   const lp_result *active;
   int64_t batch;
   unsigned long long *queue;
@@ -760,6 +760,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           if (I.check) {
             const double *t6 = tot + tid * 24;
             const Kkt5 kw = kkt5(t6);
+            if (cl.block_rank() == 0 && verbose_due(P.verbose, P.display_freq, I.k, P.check_freq))
+              verbose_line(b0 + tid, I.k, kw.pobj, kw.dobj, kw.pres, kw.dres, kw.gap, I.omega, I.eta);
             if (tpass(kw, I.nq0, I.nc0)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 1; }
             else if (I.cert) { I.status = I.cert; I.done = 1; I.outsel = 0; I.rays = 1; }
             else if (I.k == P.iter_limit) { I.status = LP_ITERATION_LIMIT; I.done = 1; I.outsel = 1; }
@@ -834,6 +836,8 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
           if (I.check) {
             const double *t = tot + tid * 24;
             const Kkt5 ka = kkt5(t + 0), kc = kkt5(t + 4);
+            if (cl.block_rank() == 0 && verbose_due(P.verbose, P.display_freq, I.k, P.check_freq))
+              verbose_line(b0 + tid, I.k, kc.pobj, kc.dobj, kc.pres, kc.dres, kc.gap, I.omega, I.eta);
             if (tpass(ka, I.nq0, I.nc0)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 1; }
             else if (tpass(kc, I.nq0, I.nc0)) { I.status = LP_OPTIMAL; I.done = 1; I.outsel = 0; }
             else if (I.cert) { I.status = I.cert; I.done = 1; I.outsel = 0; I.rays = 1; }
@@ -1016,6 +1020,7 @@ int dmma_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
     P.check_freq = o.check_frequency; P.alg = o.algorithm;
     P.eps_pi = o.eps_primal_infeasible; P.eps_di = o.eps_dual_infeasible;
     P.eps_fp = o.eps_feas_polish; P.polish_mode = L.polish_mode; P.active = L.active; P.rho = o.reflection;
+    P.verbose = o.verbose; P.display_freq = o.display_frequency;
     P.batch = L.batch; P.queue = queue;
     const size_t BN = (size_t)L.batch * n, BM = (size_t)L.batch * m;
     double *w = work;

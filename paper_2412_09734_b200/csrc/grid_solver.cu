@@ -68,8 +68,13 @@ struct GridParams {
   int64_t iter_limit;
   int32_t check_freq, alg, gk, gkt, const_step, polish_mode, verbose, display_freq, vpol, tdist, dyn;
   int32_t lean;   // bit 0 / 1: phase A / B through the lean out-of-line sweeps (phase_tiles)
+  int32_t lrA, lrB;   // K~' / K~ has a row of kTileCH entries or more (tile_row_dot's long-row test)
   double *X, *Y, *L;
   lp_result *res;
+  // decision log (CTA 0, thread 0): per attempt (j, accepted, eta, eta_bar), per check
+  // (k, metric, ref, last, restart, outcome) -- the oracle's ora_log records, same meaning
+  double *alog, *clog;
+  int64_t acap, ccap;
 };
 
 
@@ -110,8 +115,8 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t *p) { return __ldcs(p
 template <typename V, typename X>
 __device__ __forceinline__ double row_dot(int64_t r, bool valid, int rows, int G, int gl,
                                           const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                                          const V *__restrict__ v, const X *x, double *tbuf) {
-  if (G == 1) return tile_row_dot((int)r, valid, rows, rp, ci, v, x, tbuf);
+                                          const V *__restrict__ v, const X *x, double *tbuf, bool lr = true) {
+  if (G == 1) return tile_row_dot((int)r, valid, rows, rp, ci, v, x, tbuf, lr);
   double s0 = 0.0, s1 = 0.0;
   if (valid) {
     const int32_t e = __ldg(rp + r + 1);
@@ -222,6 +227,7 @@ struct PhaseCtx {
   const T *r0, *r1, *r2, *r3, *r4;
   double tau_sigma, theta, ha, hb, rf1, rf0;
   int rows, m1;
+  int lr;                         // the swept matrix has long rows (tile_row_dot)
   double *tpart;                  // per-tile partials (2 per tile)
   int t0, kmax;                   // this CTA's tile range [t0, t0 + kmax) (contiguous slots)
   unsigned long long *gctr;       // non-null: claim tiles from this global counter (all CTAs)
@@ -244,12 +250,12 @@ __device__ __noinline__ void phase_tiles(const volatile PhaseCtx<T> *cx, int *s_
     double c0 = 0.0, c1 = 0.0;
     if (MODE == kB_PARK) {
       const double sl = tile_row_dot(r, ok, rows, (const int32_t *)cx->rp, (const int32_t *)cx->ci,
-                                     (const T *)cx->kv, (const T *)cx->tgt, tbuf);
+                                     (const T *)cx->kv, (const T *)cx->tgt, tbuf, cx->lr != 0);
       if (ok) cx->park[r] = sl;
       continue;
     }
     double s = tile_row_dot(r, ok, rows, (const int32_t *)cx->rp, (const int32_t *)cx->ci, (const T *)cx->kv,
-                            (const T *)cx->tgt, tbuf);
+                            (const T *)cx->tgt, tbuf, cx->lr != 0);
     if (ok) {
       if (MODE == kA_RA) {
         // r0 = xp, r1 = cs, r2 = ls, r3 = us; e0 = xa (rw), e1 = KTy' (w), e2 = the old x buffer (w: x')
@@ -478,7 +484,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
     for (int it = 0; it < row_iters; ++it) {
       const int i = it * ngrp + grp;
       const bool ok = i < m;
-      const double s = row_dot(i, ok, m, G, gl, P.rp, P.ci, P.kv, x, tbuf);
+      const double s = row_dot(i, ok, m, G, gl, P.rp, P.ci, P.kv, x, tbuf, P.lrB);
       if (ok && gl == 0) {
         Kx[i] = (T)s; Kxa[i] = (T)s;
         const double yv = y[i];
@@ -489,7 +495,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
     for (int it = 0; it < col_iters; ++it) {
       const int j = it * ngrpt + grpt;
       const bool ok = j < n;
-      const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, y, tbuf);
+      const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, y, tbuf, P.lrA);
       if (ok && glt == 0) {
         KTy[j] = (T)s; KTya[j] = (T)s;
         const double xv = x[j];
@@ -532,6 +538,14 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
     return true;
   };
 
+  int64_t nchk = 0;   // checks logged
+  auto log_check = [&](double metric_, int restart_, int outcome) {
+    if (P.clog && blockIdx.x == 0 && threadIdx.x == 0 && nchk < P.ccap) {
+      double *r = P.clog + 6 * nchk;
+      r[0] = (double)k; r[1] = metric_; r[2] = ref; r[3] = last; r[4] = restart_; r[5] = outcome;
+    }
+    ++nchk;
+  };
   unsigned long long gbase = 0;   // phase A's global tile counter value at this phase's start
   bool sliceA = false;            // phase A used global claims: reduce this CTA's slice in phase B
   bool sliceA2 = false;           // the same for the lean sweep (partials in P.tpart, stride 2)
@@ -551,7 +565,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
           o_xp = lv(xp + j); o_xa = lv(xa + j); o_cs = lv(cs + j); o_ls = lv(lsT + j); o_us = lv(usT + j);
           if (r2) { o_x = lv(x + j); o_kt = lv(KTy + j); o_kta = lv(KTya + j); }
         }
-        const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, yp, tbuf);
+        const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, yp, tbuf, P.lrA);
         if (!lead) return 0.0;
         double xn, kt;
         if (!r2) {
@@ -574,7 +588,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
           lean_range(n);
           s_cx.gctr = nullptr;
           if (glob) { s_cx.gctr = P.gctr; s_cx.gbase = gbase; s_cx.t0 = 0; s_cx.kmax = (n + 31) >> 5; s_cx.tpart = P.tpartA; }
-          s_cx.rp = P.trp; s_cx.ci = P.tci; s_cx.kv = P.tkv; s_cx.tgt = yp; s_cx.add = nullptr;
+          s_cx.rp = P.trp; s_cx.ci = P.tci; s_cx.kv = P.tkv; s_cx.tgt = yp; s_cx.add = nullptr; s_cx.lr = P.lrA;
           s_cx.r0 = xp; s_cx.r1 = cs; s_cx.r2 = lsT; s_cx.r3 = usT; s_cx.r4 = KTya;
           s_cx.e0 = xa;
           if (!r2) { s_cx.e1 = KTyp; s_cx.e2 = x; }
@@ -661,7 +675,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
             o_y = lv(y + i); o_kx = lv(Kx + i);
           }
         }
-        const double s = o_add + row_dot(i, ok, m, G, gl, rp_, ci_, kv_, xp, tbuf);
+        const double s = o_add + row_dot(i, ok, m, G, gl, rp_, ci_, kv_, xp, tbuf, P.lrB);
         c[0] = 0.0; c[1] = 0.0;
         if (!lead) return;
         double yv, kxv;
@@ -694,7 +708,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
           if (threadIdx.x == 0) {
             lean_range(m);
             s_cx.gctr = nullptr;
-            s_cx.rp = P.rpL; s_cx.ci = P.ciL; s_cx.kv = P.kvL; s_cx.tgt = xp; s_cx.park = P.tmp;
+            s_cx.rp = P.rpL; s_cx.ci = P.ciL; s_cx.kv = P.kvL; s_cx.tgt = xp; s_cx.park = P.tmp; s_cx.lr = P.lrB;
           }
           __syncthreads();
           phase_tiles<kB_PARK, T>(&s_cx, &s_ctr, tbuf);
@@ -705,7 +719,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
           s_cx.gctr = nullptr;
           if (P.split) { s_cx.rp = P.rpR; s_cx.ci = P.ciR; s_cx.kv = P.kvR; s_cx.add = P.tmp; }
           else { s_cx.rp = P.rp; s_cx.ci = P.ci; s_cx.kv = P.kv; s_cx.add = nullptr; }
-          s_cx.tgt = xp; s_cx.m1 = m1; s_cx.r0 = qs;
+          s_cx.tgt = xp; s_cx.m1 = m1; s_cx.r0 = qs; s_cx.lr = P.lrB;
           s_cx.tau_sigma = sigma; s_cx.theta = theta; s_cx.ha = ha; s_cx.hb = hb; s_cx.rf1 = rf1; s_cx.rf0 = rf0;
           if (pending && !r2) { s_cx.r1 = yp; s_cx.r2 = Kxp; s_cx.e0 = ya; s_cx.e1 = y; s_cx.e2 = Kx; }
           else if (pending) { s_cx.r1 = yp; s_cx.r2 = Kxp; s_cx.r3 = ya; s_cx.r4 = Kxa; s_cx.e0 = y; s_cx.e1 = Kx; s_cx.e2 = yp; s_cx.e3 = Kxp; }
@@ -726,7 +740,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
           // x' only, L2-resident); pass 2: K~_R x' + tmp and the row epilogue
           double none[1];
           tiles_dynamic(m, [&](int i, bool ok, double (&c)[1]) {
-            const double sl = tile_row_dot(i, ok, m, P.rpL, P.ciL, P.kvL, xp, tbuf);
+            const double sl = tile_row_dot(i, ok, m, P.rpL, P.ciL, P.kvL, xp, tbuf, P.lrB);
             if (ok) P.tmp[i] = sl;
             c[0] = 0.0;
           }, none, false);
@@ -792,6 +806,10 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
     const double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : INFINITY;
     const bool acc = cstep || (eta <= eb);
     const double eta_used = eta;
+    if (P.alog && blockIdx.x == 0 && threadIdx.x == 0 && jatt <= P.acap) {
+      double *r = P.alog + 4 * (jatt - 1);
+      r[0] = (double)jatt; r[1] = acc ? 1.0 : 0.0; r[2] = eta_used; r[3] = eb;
+    }
     if (!cstep) {
       double f1, f2;
       step_factors(P.tab, jatt, f1, f2);
@@ -829,7 +847,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
       for (int it = 0; it < col_iters; ++it) {
         const int j = it * ngrpt + grpt;
         const bool ok = j < n;
-        const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, yp, tbuf);
+        const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, yp, tbuf, P.lrA);
         if (ok && glt == 0) {
           KTyp[j] = (T)s;
           if (!r2) {
@@ -879,7 +897,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
       for (int it = 0; it < row_iters; ++it) {
         const int i = it * ngrp + grp;
         const bool ok = i < m;
-        const double s = row_dot(i, ok, m, G, gl, P.rp, P.ci, P.kv, xa, tbuf);
+        const double s = row_dot(i, ok, m, G, gl, P.rp, P.ci, P.kv, xa, tbuf, P.lrB);
         if (ok && gl == 0) {
           Kxa[i] = (T)s;
           const double dr = P.Dr[i], yai = ya[i], yi = y[i], kxi = Kx[i], q0 = P.q0[i], qsi = qs[i];
@@ -896,7 +914,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
       for (int it = 0; it < col_iters; ++it) {
         const int j = it * ngrpt + grpt;
         const bool ok = j < n;
-        const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, ya, tbuf);
+        const double s = row_dot(j, ok, n, Gt, glt, P.trp, P.tci, P.tkv, ya, tbuf, P.lrA);
         if (ok && glt == 0) {
           KTya[j] = (T)s;
           const double dc = P.Dc[j], xaj = xa[j], xj = x[j], ktj = KTy[j];
@@ -919,10 +937,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
       const Kkt5 ka = kkt5(t + 0), kc = kkt5(t + 4);
       if (blockIdx.x == 0 && threadIdx.x == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
         verbose_line(0, k, kc.pobj, kc.dobj, kc.pres, kc.dres, kc.gap, omega, eta);
-      if (tpass(ka, nq0, nc0)) { status = LP_OPTIMAL; ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; break; }
-      if (tpass(kc, nq0, nc0)) { status = LP_OPTIMAL; ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
-      if (certify(t + 20, xp, yp, KTyp)) break;
+      if (tpass(ka, nq0, nc0)) { log_check(0.0, 0, 1); status = LP_OPTIMAL; ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; break; }
+      if (tpass(kc, nq0, nc0)) { log_check(0.0, 0, 2); status = LP_OPTIMAL; ox = x; oy = y; oKx = Kx; oKTy = KTy; break; }
+      if (certify(t + 20, xp, yp, KTyp)) { log_check(0.0, 0, 3); break; }
       if (k == P.iter_limit) {
+        log_check(0.0, 0, 0);
         status = LP_ITERATION_LIMIT;
         if (kkt5_rel(ka, nq0, nc0) < kkt5_rel(kc, nq0, nc0)) { ox = xa; oy = ya; oKx = Kxa; oKTy = KTya; }
         else { ox = x; oy = y; oKx = Kx; oKTy = KTy; }
@@ -939,12 +958,13 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
       const Kkt5 kw = kkt5(t);
       if (blockIdx.x == 0 && threadIdx.x == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
         verbose_line(0, k, kw.pobj, kw.dobj, kw.pres, kw.dres, kw.gap, omega, eta);
-      if (tpass(kw, nq0, nc0)) { status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
-      if (certify(t + 6, xa, ya, KTya)) break;
-      if (k == P.iter_limit) { status = LP_ITERATION_LIMIT; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
+      if (tpass(kw, nq0, nc0)) { log_check(rP, 0, 1); status = LP_OPTIMAL; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
+      if (certify(t + 6, xa, ya, KTya)) { log_check(0.0, 0, 3); break; }
+      if (k == P.iter_limit) { log_check(rP, 0, 0); status = LP_ITERATION_LIMIT; ox = xp; oy = yp; oKx = Kxp; oKTy = KTyp; break; }
       cx = xp; cy = yp; cKx = Kxp; cKTy = KTyp; metric = rP; dx2 = t[4]; dy2 = t[5];
     }
     const bool restart = restart_due(k_in, k, metric, ref, last);
+    log_check(metric, restart ? 1 : 0, 0);
     last = metric;
     if (restart) {
       ++restarts;
@@ -1187,6 +1207,8 @@ int grid_launch(const DevProblem &D, const lp_options &o, const GridLaunch &L, c
   auto group = [](double avg, int mx) { return tile_mapping_ok(avg, mx) ? 1 : std::max(2, pow2_floor(avg / 4.0)); };
   P.gk = group(D.avg_row, D.max_row);
   P.gkt = group(D.avg_col, D.max_col);
+  P.lrB = (D.max_row < 0 || D.max_row >= kTileCH) ? 1 : 0;   // unknown lengths: keep the test
+  P.lrA = (D.max_col < 0 || D.max_col >= kTileCH) ? 1 : 0;
   // phase A keeps the static mapping: with fewer than ~4 column tiles per warp (C4: 1.3) the
   // tile chunks are a serial latency chain and G lanes per column are faster (C4 phase A
   // 21 -> 17 us per attempt, trace build); phase B's dynamic tile driver wins at any size
@@ -1211,6 +1233,7 @@ int grid_launch(const DevProblem &D, const lp_options &o, const GridLaunch &L, c
   if constexpr (f32) { P.kvL = D.kvL32; P.kvR = D.kvR32; }
   else { P.kvL = D.kvL; P.kvR = D.kvR; }
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res;
+  P.alog = L.alog; P.clog = L.clog; P.acap = L.acap; P.ccap = L.ccap;
   void *args[] = {&P};
   MPAX_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(kBS), args, 0, s));
   g_launches.fetch_add(1, std::memory_order_relaxed);

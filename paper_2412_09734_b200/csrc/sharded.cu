@@ -15,8 +15,27 @@
 // Pock-Chambolle).  With one GPU this is a multi-kernel single-GPU path; the
 // "virtual" mode runs p row shards on ONE GPU with a fixed-order device sum in
 // place of NCCL, which is how the partitioned arithmetic is tested here.
+//
+// Column sharding (the axis chosen by min(m, n); reading 33):
+// GPU g holds the columns [c_g, c_g + n_g) of K (K~_{:,g}, m x n_g, and its transpose), the
+// matching c, l, u and primal iterate, and a replicated copy of every m-long vector.  Per attempt
+//   K~'_g y'  (local: y' is replicated)             commit n-side + primal step x'_g  (local)
+//   K~_{:,g} x'_g (partial, m) --ncclAllReduce(sum)--> K~x'                           [SpMV #1]
+//   commit m-side + dual step y' (replicated), ||dx||^2 partials reduced across GPUs
+// so the exchanged vector is the m-long one: with m < n (C5: 40 MB instead of 80 MB) the
+// collective moves the shorter vector.  Row norms of the preconditioner are reduced instead of
+// column norms.  The same kernels serve both modes; `cols` selects the data each reads.
+//
+// Exchange variant B of the row engine (lp_options.sharded_exchange = 1): the
+// K~_g' y'_g partials are REDUCE-SCATTERED, so GPU g receives only its slice J_g of K~'y' (n/p
+// columns) and runs the n-side commit and primal step on that slice alone; x' is then
+// ALL-GATHERED for the rows step.  Same bytes on the wire as the all-reduce (which is a
+// reduce-scatter + all-gather), but the n-side elementwise work is split p ways instead of
+// replicated; the column-side scalar partials are then reduced like the row-side ones.
 #include <stdio.h>
+#include <stdlib.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -51,6 +70,7 @@ struct Vecs {
   double *y, *Kx, *yp, *Kxp, *ya, *Kxa, *yr, *qs;           // m_local
   double *part;                                             // blocks x kV
   double *tmp;                                              // m_local: K~_L x' (two-pass rows step)
+  const double *pre;                                        // column mode: K~x' summed across shards (m)
   const double *c0, *q0, *X0, *Y0;
 };
 
@@ -168,14 +188,14 @@ __global__ void k_cols_spmv(const ShState *st, int64_t n, int G, const int32_t *
 enum { COLS_STEP = 0, COLS_COMMIT_ONLY = 1, COLS_AVG = 2, COLS_INIT = 3, COLS_INIT2 = 4, COLS_OUT = 5, COLS_CERT = 6 };
 enum { ROWS_STEP = 0, ROWS_COMMIT_ONLY = 1, ROWS_AVG = 2, ROWS_INIT = 3, ROWS_INIT2 = 4, ROWS_OUT = 5, ROWS_CERT = 6 };
 
-__global__ void k_cols(ShState *st, int mode, int64_t n, const DevProblem P, const Vecs V) {
+__global__ void k_cols(ShState *st, int mode, int64_t j0, int64_t n, const DevProblem P, const Vecs V) {
   if (st->halt && mode != COLS_OUT) return;
   const bool r2 = st->r2, pend = st->pending;
   const double tau = st->eta * st->inv_omega, theta = st->theta, ha = st->ha, hb = st->hb;
   const double rf1 = 1.0 + st->rho, rf0 = st->rho;  // reflection (reading 38)
   double v[20] = {};
   const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x, st_ = (int64_t)gridDim.x * kB;
-  for (int64_t j = gt; j < n; j += st_) {
+  for (int64_t j = j0 + gt; j < n; j += st_) {   // columns [j0, n): all, or this shard's slice (variant B)
     const double dc = P.Dc[j];
     if (mode == COLS_STEP || mode == COLS_COMMIT_ONLY) {
       double xv = V.x[j], kt = V.KTy[j];
@@ -294,6 +314,7 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
     // ROWS_STEP over split K~_g: pass 1 (k_rows_left) parked K~_L x' in V.tmp; add K~_R x'
     const bool two = mode == ROWS_STEP && P.split_h > 0 && g == 1;
     const double s = !spmv ? 0.0
+                     : V.pre ? (ok ? V.pre[i] : 0.0)   // column mode: the cross-shard sum, computed before
                      : two ? (ok ? V.tmp[i] : 0.0) + row_dot(i, ok, 1, 0, P.rpR, P.ciR, P.kvR, src, m, s_tile[threadIdx.x >> 5])
                            : row_dot(i, ok, g, gl, P.rp, P.ci, P.kv, src, m, s_tile[threadIdx.x >> 5]);
     if (!lead) continue;
@@ -422,7 +443,13 @@ __global__ void k_decide(ShState *st, const double *tab, int64_t check_freq, int
 }
 
 __global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, double eps_pi, double eps_di,
-                               int64_t iter_limit) {
+                               int64_t iter_limit, int verbose, int display_freq, int64_t check_freq,
+                               int polish_mode, double eps_fp) {
+  // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
+  auto tpass = [&](const Kkt5 &k) {
+    return polish_mode ? polish_pass(polish_mode, k.pres, k.dres, st->nq0, st->nc0, eps_fp)
+                       : kkt5_pass(k, st->nq0, st->nc0, eps_abs, eps_rel);
+  };
   double t[20];
   for (int k = 0; k < 20; ++k) t[k] = st->colsum[k] + st->rowsum[k];
   st->pending = 0;
@@ -437,7 +464,9 @@ __global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, doub
   const int cert = cert_decide(ct, eps_pi, eps_di, ny, nx);
   if (st->r2) {
     const Kkt5 kw = kkt5(t);
-    if (kkt5_pass(kw, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
+    if (verbose_due(verbose, display_freq, st->k, check_freq))
+      verbose_line(0, st->k, kw.pobj, kw.dobj, kw.pres, kw.dres, kw.gap, st->omega, st->eta);
+    if (tpass(kw)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
     if (cert) {
       st->status = cert; st->halt = 1; st->outsel = 0; st->rays = 1; st->ray_ny = ny; st->ray_nx = nx;
       return;
@@ -449,8 +478,10 @@ __global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, doub
     st->colsum[23] = t[5];
   } else {
     const Kkt5 ka = kkt5(t + 0), kc = kkt5(t + 4);
-    if (kkt5_pass(ka, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
-    if (kkt5_pass(kc, nq0, nc0, eps_abs, eps_rel)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 0; return; }
+    if (verbose_due(verbose, display_freq, st->k, check_freq))
+      verbose_line(0, st->k, kc.pobj, kc.dobj, kc.pres, kc.dres, kc.gap, st->omega, st->eta);
+    if (tpass(ka)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
+    if (tpass(kc)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 0; return; }
     if (cert) {
       st->status = cert; st->halt = 1; st->outsel = 0; st->rays = 1; st->ray_ny = ny; st->ray_nx = nx;
       return;
@@ -479,11 +510,11 @@ __global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, doub
   }
 }
 
-__global__ void k_restart(const ShState *st, int64_t n, int64_t m, const Vecs V) {
+__global__ void k_restart(const ShState *st, int64_t j0, int64_t n, int64_t m, const Vecs V) {
   if (!st->restart) return;
   const bool r2 = st->r2, csel = st->csel;
   const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x, s = (int64_t)gridDim.x * kB;
-  for (int64_t j = gt; j < n; j += s) {
+  for (int64_t j = j0 + gt; j < n; j += s) {
     double xv = V.x[j], kt = V.KTy[j];
     if (csel) { xv = r2 ? V.xp[j] : V.xa[j]; kt = r2 ? V.KTyp[j] : V.KTya[j]; }
     V.x[j] = xv; V.xr[j] = xv; V.xa[j] = xv; V.KTy[j] = kt; V.KTya[j] = kt;
@@ -531,7 +562,7 @@ __global__ void k_set_eta0(ShState *st, const double *kmax, const double *sigma,
 
 struct ShardData {
   DevProblem P;
-  int64_t row_offset = 0;
+  int64_t row_offset = 0;   // row mode: first global row of the shard; column mode: first global column
   int64_t *rp64 = nullptr;
   Vecs V{};
   ShState *st = nullptr;
@@ -539,6 +570,9 @@ struct ShardData {
   void *arena = nullptr;
   void *vecs = nullptr;
   int nb = 0;
+  double *pol = nullptr;   // feasibility polishing: x* (n), x_p (n), zeros (n), y* (m), zeros (m), 8 partials
+  const double *c0 = nullptr, *q0 = nullptr;   // the shard's own costs (V.c0 / V.q0 swap to zeros while polishing)
+  int64_t j0 = 0, j1 = 0;   // the n-side range this shard updates: all of [0, n) except under variant B
 };
 
 struct ShardedLP {
@@ -548,22 +582,40 @@ struct ShardedLP {
   void *comm = nullptr;  // ncclComm_t (borrowed)
   int64_t n = 0, m_global = 0, m1_global = 0;
   std::vector<ShardData> sh;
-  double **d_ptrs = nullptr;  // virtual mode: per-shard pointer tables
+  double **d_ptrs = nullptr;  // virtual mode: per-shard pointer tables (kSlots x 64)
+  std::vector<std::vector<double *>> tab_cache;   // the pointers each slot's table holds (uploaded once)
   ShState *h_st = nullptr;
   lp_result *d_res = nullptr, *h_res = nullptr;
   int *d_flags = nullptr, *h_flags = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool solved = false;
   bool sigma_ready = false;  // sigma_max(K~) computed into every shard's P.sigma
+  int polish_mode = 0;       // the running solve is a polishing sub-solve (reading 36): 1 primal, 2 dual
+  bool cols = false;         // column-sharded (every m-long vector replicated) instead of row-sharded
+  bool vb = false;           // this solve uses exchange variant B (row engine): n-side work on slices
+  int64_t ns = 0;            // variant B: columns per slice, ceil(n / p) (p = shards or ranks)
 };
 
 namespace {
+
+int upload_table(ShardedLP &E, int slot, double *const *bufs_host) {
+  double **tab = E.d_ptrs + slot * 64;
+  std::vector<double *> want(bufs_host, bufs_host + E.sh.size());
+  if (E.tab_cache.size() <= (size_t)slot) E.tab_cache.resize(slot + 1);
+  if (E.tab_cache[slot] != want) {
+    MPAX_CUDA(cudaMemcpyAsync(tab, bufs_host, E.sh.size() * sizeof(double *), cudaMemcpyHostToDevice, E.s));
+    E.tab_cache[slot] = want;
+  }
+  return LP_OK;
+}
 
 int reduce_across(ShardedLP &E, int slot, int64_t count, bool op_max, double *const *bufs_host) {
   if (E.virt) {
     if (E.sh.size() < 2) return LP_OK;
     double **tab = E.d_ptrs + slot * 64;
-    MPAX_CUDA(cudaMemcpyAsync(tab, bufs_host, E.sh.size() * sizeof(double *), cudaMemcpyHostToDevice, E.s));
+    // the table is uploaded only when its pointers change: the attempt loop then issues no host
+    // copies, so it can be captured into a CUDA graph (sharded_solve)
+    if (int r = upload_table(E, slot, bufs_host)) return r;
     MPAX_LAUNCH(k_vreduce, blocks_for(count), kB, 0, E.s, tab, (int)E.sh.size(), count, op_max ? 1 : 0);
     MPAX_CHECK_LAUNCH();
     return LP_OK;
@@ -593,10 +645,68 @@ int reduce_vec(ShardedLP &E, int slot, std::vector<double *> bufs, int64_t count
   return reduce_across(E, slot, count, op_max, bufs.data());
 }
 
+// the scalar partials of the sharded side: row sums (row mode) or column sums (column mode)
 int reduce_rowsum(ShardedLP &E, int slot) {
   std::vector<double *> b;
-  for (auto &d : E.sh) b.push_back(d.st->rowsum);
-  return reduce_vec(E, slot, b, kV, false);
+  for (auto &d : E.sh) b.push_back(E.cols ? d.st->colsum : d.st->rowsum);
+  STRY(reduce_vec(E, slot, b, 20, false));   // the 20 partials k_cols / k_rows write ([20..23]: decision scratch)
+  if (!E.vb) return LP_OK;
+  b.clear();   // variant B: the column side is sliced as well
+  for (auto &d : E.sh) b.push_back(d.st->colsum);
+  return reduce_vec(E, slot + 6, b, 20, false);
+}
+
+// Variant B collectives on n-long buffers padded to p x ns: the reduce-scatter leaves shard g
+// the sum of its slice [g ns, (g + 1) ns) (virtual mode: the whole sum, of which only the slice
+// is read); the all-gather copies every shard's slice into every other shard's buffer.
+__global__ void k_vgather(double *const *ptrs, int p, int64_t ns) {
+  for (int64_t t = blockIdx.x * (int64_t)kB + threadIdx.x; t < (int64_t)p * ns; t += (int64_t)gridDim.x * kB) {
+    const int owner = (int)(t / ns);
+    const double v = ptrs[owner][t];
+    for (int q = 0; q < p; ++q)
+      if (q != owner) ptrs[q][t] = v;
+  }
+}
+
+int table_for(ShardedLP &E, int slot, std::vector<double *> &bufs) { return upload_table(E, slot, bufs.data()); }
+
+int reduce_scatter_vec(ShardedLP &E, int slot, std::vector<double *> bufs) {
+  if (E.virt) return reduce_vec(E, slot, bufs, (int64_t)E.sh.size() * E.ns, false);
+  if (E.nranks <= 1) return LP_OK;
+#ifdef MPAX_HAVE_NCCL
+  ncclResult_t r = ncclReduceScatter(bufs[0], bufs[0] + (int64_t)E.rank * E.ns, (size_t)E.ns, ncclDouble, ncclSum,
+                                     (ncclComm_t)E.comm, E.s);
+  if (r != ncclSuccess) {
+    set_error_detail(std::string("ncclReduceScatter: ") + ncclGetErrorString(r));
+    return LP_ERR_NCCL;
+  }
+  return LP_OK;
+#else
+  return LP_ERR_UNSUPPORTED;
+#endif
+}
+
+int allgather_vec(ShardedLP &E, int slot, std::vector<double *> bufs) {
+  if (E.virt) {
+    if (E.sh.size() < 2) return LP_OK;
+    STRY(table_for(E, slot, bufs));
+    MPAX_LAUNCH(k_vgather, blocks_for((int64_t)E.sh.size() * E.ns), kB, 0, E.s, E.d_ptrs + slot * 64,
+                (int)E.sh.size(), E.ns);
+    MPAX_CHECK_LAUNCH();
+    return LP_OK;
+  }
+  if (E.nranks <= 1) return LP_OK;
+#ifdef MPAX_HAVE_NCCL
+  ncclResult_t r = ncclAllGather(bufs[0] + (int64_t)E.rank * E.ns, bufs[0], (size_t)E.ns, ncclDouble,
+                                 (ncclComm_t)E.comm, E.s);
+  if (r != ncclSuccess) {
+    set_error_detail(std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    return LP_ERR_NCCL;
+  }
+  return LP_OK;
+#else
+  return LP_ERR_UNSUPPORTED;
+#endif
 }
 
 }  // namespace
@@ -606,7 +716,7 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
   cudaStream_t s = E.s;
   const int p = (int)descs.size();
   E.sh.resize(p);
-  MPAX_CUDA(cudaMallocAsync((void **)&E.d_ptrs, 8 * 64 * sizeof(double *), s));
+  MPAX_CUDA(cudaMallocAsync((void **)&E.d_ptrs, 32 * 64 * sizeof(double *), s));   // slots 0..31
   for (int g = 0; g < p; ++g) {
     const lp_problem_desc &d = descs[g];
     ShardData &S = E.sh[g];
@@ -656,21 +766,26 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
     // vectors
     double *vec = nullptr;
     S.nb = 148 * 8;
-    const size_t nv = 9 * (size_t)n + 8 * (size_t)(m > 0 ? m : 1) + (size_t)S.nb * kV + 3 * (size_t)n +
+    const size_t nv = 9 * (size_t)(n + 64) + 8 * (size_t)(m > 0 ? m : 1) + (size_t)S.nb * kV + 3 * (size_t)(n + 64) +
                       2 * (size_t)(m > 0 ? m : 1);
     MPAX_CUDA(cudaMallocAsync((void **)&vec, nv * sizeof(double), s));
+    MPAX_CUDA(cudaMemsetAsync(vec, 0, nv * sizeof(double), s));
     S.vecs = vec;
     Vecs &V = S.V;
     double *w = vec;
-    V.x = w; w += n; V.KTy = w; w += n; V.xp = w; w += n; V.KTyp = w; w += n; V.xa = w; w += n; V.KTya = w; w += n;
-    V.xr = w; w += n; V.cs = w; w += n; V.red = w; w += n;
+    // n-vectors padded by 64 (variant B slices of ceil(n / p) columns, p <= 64; pads stay zero)
+    const int64_t na = n + 64;
+    V.x = w; w += na; V.KTy = w; w += na; V.xp = w; w += na; V.KTyp = w; w += na; V.xa = w; w += na;
+    V.KTya = w; w += na; V.xr = w; w += na; V.cs = w; w += na; V.red = w; w += na;
     const int64_t mm = m > 0 ? m : 1;
     V.y = w; w += mm; V.Kx = w; w += mm; V.yp = w; w += mm; V.Kxp = w; w += mm; V.ya = w; w += mm;
     V.Kxa = w; w += mm; V.yr = w; w += mm; V.qs = w; w += mm;
     V.part = w; w += (size_t)S.nb * kV;
-    S.X = w; w += n; S.L = w; w += n; w += n; S.Y = w; w += mm;
+    S.X = w; w += na; S.L = w; w += na; w += na; S.Y = w; w += mm;
     V.tmp = w; w += mm;
     V.c0 = c0; V.q0 = q0;
+    S.c0 = c0; S.q0 = q0;
+    V.pre = E.cols ? V.tmp : nullptr;
   }
   MPAX_CUDA(cudaStreamSynchronize(s));
   for (int g = 0; g < p; ++g) {
@@ -685,7 +800,7 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
   std::vector<double *> rho(p), gam(p);
   for (int g = 0; g < p; ++g) {
     MPAX_CUDA(cudaMallocAsync((void **)&rho[g], (size_t)(E.sh[g].P.m + 1) * sizeof(double), s));
-    MPAX_CUDA(cudaMallocAsync((void **)&gam[g], (size_t)E.n * sizeof(double), s));
+    MPAX_CUDA(cudaMallocAsync((void **)&gam[g], (size_t)E.sh[g].P.n * sizeof(double), s));
     STRY(setup_precond_init(E.sh[g].P, s));
   }
   int *noflag = nullptr;
@@ -693,7 +808,8 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
   MPAX_CUDA(cudaMemsetAsync(noflag, 0, sizeof(int), s));
   for (int r = 0; r < 11; ++r) {
     for (int g = 0; g < p; ++g) STRY(setup_precond_norms(E.sh[g].P, rho[g], gam[g], r == 10, s, noflag));
-    STRY(reduce_vec(E, 1, gam, E.n, r < 10));
+    if (E.cols) STRY(reduce_vec(E, 1, rho, E.m_global, r < 10));   // row norms over every shard's columns
+    else STRY(reduce_vec(E, 1, gam, E.n, r < 10));
     for (int g = 0; g < p; ++g) STRY(setup_precond_update(E.sh[g].P, rho[g], gam[g], s, noflag));
   }
   std::vector<double *> km(p);
@@ -709,7 +825,7 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
   MPAX_CUDA(cudaFreeAsync(noflag, s));
   // column halves of each K~_g for the two-pass rows step (grid_solver.cu grid_split_prepare:
   // x' is replicated, so its 8n bytes are the gather target at every p)
-  for (int g = 0; g < p; ++g) STRY(grid_split_prepare(E.sh[g].P, s));
+  if (!E.cols) for (int g = 0; g < p; ++g) STRY(grid_split_prepare(E.sh[g].P, s));
   MPAX_CUDA(cudaStreamSynchronize(s));
   return LP_OK;
 }
@@ -726,12 +842,36 @@ inline int group_of(double avg, int mx) {
 
 int launch_cols(ShardedLP &E, int mode) {
   for (auto &S : E.sh) {
-    MPAX_LAUNCH(k_cols, blocks_for(E.n), kB, 0, E.s, S.st, mode, E.n, S.P, S.V);
+    MPAX_LAUNCH(k_cols, blocks_for(S.j1 - S.j0), kB, 0, E.s, S.st, mode, S.j0, S.j1, S.P, S.V);
   }
   MPAX_CHECK_LAUNCH();
   return LP_OK;
 }
 int launch_rows(ShardedLP &E, int mode) {
+  const bool spmv_mode = (mode == ROWS_STEP || mode == ROWS_AVG || mode == ROWS_INIT2);
+  if (E.vb && spmv_mode) {   // variant B: the rows' SpMV gathers the full vector the slices updated
+    std::vector<double *> bufs;
+    for (auto &S : E.sh) bufs.push_back(mode == ROWS_AVG ? S.V.xa : (mode == ROWS_INIT2 ? S.V.x : S.V.xp));
+    STRY(allgather_vec(E, mode == ROWS_AVG ? 10 : (mode == ROWS_INIT2 ? 11 : 12), bufs));
+  }
+  if (E.cols && spmv_mode) {
+    // column mode: K~_{:,g} src_g (partial over this shard's columns) into V.pre, summed across
+    // shards; k_rows then reads the sum (G = 1: one thread per row)
+    std::vector<double *> bufs;
+    for (auto &S : E.sh) {
+      const int G = group_of(S.P.avg_row, S.P.max_row);
+      const double *src = mode == ROWS_AVG ? S.V.xa : (mode == ROWS_INIT2 ? S.V.x : S.V.xp);
+      MPAX_LAUNCH(k_cols_spmv, blocks_for(S.P.m * G), kB, 0, E.s, S.st, S.P.m, G, S.P.rp, S.P.ci, S.P.kv, src,
+                  S.V.tmp);
+      bufs.push_back(S.V.tmp);
+    }
+    MPAX_CHECK_LAUNCH();
+    STRY(reduce_vec(E, 8, bufs, E.m_global, false));
+    for (auto &S : E.sh)
+      MPAX_LAUNCH(k_rows, blocks_for(S.P.m), kB, 0, E.s, S.st, mode, S.P.m, S.P.m1, 1, S.P, S.V);
+    MPAX_CHECK_LAUNCH();
+    return LP_OK;
+  }
   for (auto &S : E.sh) {
     const int G = group_of(S.P.avg_row, S.P.max_row);
     const bool spmv = (mode == ROWS_STEP || mode == ROWS_AVG || mode == ROWS_INIT2);
@@ -748,10 +888,13 @@ int cols_spmv(ShardedLP &E, int which /*0: yp, 1: y, 2: ya*/) {
   for (auto &S : E.sh) {
     const int G = group_of(S.P.avg_col, S.P.max_col);
     const double *src = which == 0 ? S.V.yp : (which == 1 ? S.V.y : S.V.ya);
-    MPAX_LAUNCH(k_cols_spmv, blocks_for(E.n * G), kB, 0, E.s, S.st, E.n, G, S.P.trp, S.P.tci, S.P.tkv, src, S.V.red);
+    MPAX_LAUNCH(k_cols_spmv, blocks_for(S.P.n * G), kB, 0, E.s, S.st, S.P.n, G, S.P.trp, S.P.tci, S.P.tkv, src,
+                S.V.red);
     bufs.push_back(S.V.red);
   }
   MPAX_CHECK_LAUNCH();
+  if (E.cols) return LP_OK;   // column mode: y' is replicated, the shard's K~'_g y' is complete
+  if (E.vb) return reduce_scatter_vec(E, 0, bufs);   // variant B: each shard needs its slice only
   return reduce_vec(E, 0, bufs, E.n, false);
 }
 
@@ -763,6 +906,10 @@ namespace {
 // w = sum_g K~_g' u_g reduced across shards, then the replicated normalisation.
 int sharded_power(ShardedLP &E) {
   cudaStream_t s = E.s;
+  if (E.cols) {
+    set_error_detail("the constant step rule is not built for column-sharded LPs");
+    return LP_ERR_UNSUPPORTED;
+  }
   std::vector<PowerState> ps(E.sh.size());
   for (size_t g = 0; g < E.sh.size(); ++g) STRY(power_begin(ps[g], E.n, E.sh[g].P.m, s));
   std::vector<double *> ws;
@@ -784,13 +931,32 @@ int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const dou
   const bool r2 = o.algorithm == LP_R2HPDHG, cstep = o.step_rule == LP_STEP_CONSTANT;
   MPAX_CUDA(cudaEventRecord(E.ev0, s));
   if (cstep && !E.sigma_ready) STRY(sharded_power(E));
+  // exchange variant (row engine): B slices the n-side work, A replicates it
+  const int pp = E.virt ? (int)E.sh.size() : E.nranks;
+  E.vb = !E.cols && o.sharded_exchange == 1 && pp > 1;
+  E.ns = (E.n + pp - 1) / pp;
+  for (size_t g = 0; g < E.sh.size(); ++g) {
+    ShardData &S = E.sh[g];
+    S.j0 = 0;
+    S.j1 = S.P.n;
+    if (E.vb) {
+      const int64_t q = E.virt ? (int64_t)g : E.rank;
+      S.j0 = std::min<int64_t>(E.n, q * E.ns);
+      S.j1 = std::min<int64_t>(E.n, (q + 1) * E.ns);
+    }
+  }
   for (auto &S : E.sh) {
     MPAX_CUDA(cudaMemsetAsync(S.st, 0, sizeof(ShState), s));
-    S.V.X0 = X0;                                        // full n (replicated)
-    S.V.Y0 = Y0 ? Y0 + S.row_offset - (E.virt ? 0 : 0) : nullptr;
+    if (!E.cols) {
+      S.V.X0 = X0;                                        // full n (replicated)
+      S.V.Y0 = Y0 ? Y0 + S.row_offset : nullptr;          // virtual: the full m; a real rank: fixed below
+    } else {
+      S.V.X0 = X0 ? X0 + (E.virt ? S.row_offset : 0) : nullptr;   // this process's columns
+      S.V.Y0 = Y0;                                        // full m (replicated)
+    }
     MPAX_LAUNCH(k_set_eta0, 1, 1, 0, s, S.st, S.P.kmax, S.P.sigma, r2 ? 1 : 0, cstep ? 1 : 0, o.reflection);
   }
-  if (!E.virt) for (auto &S : E.sh) S.V.Y0 = Y0;        // a real rank passes its own rows
+  if (!E.virt && !E.cols) for (auto &S : E.sh) S.V.Y0 = Y0;   // a real rank passes its own rows
   // ---- step 2 ----
   STRY(launch_cols(E, COLS_INIT));
   STRY(launch_rows(E, ROWS_INIT));
@@ -804,12 +970,8 @@ int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const dou
   MPAX_CHECK_LAUNCH();
   // ---- attempts, checks ----
   const int64_t F = o.check_frequency, LIM = o.iteration_limit;
-  int64_t k = 0;
-  for (;;) {
-    int64_t next = ((k / F) + 1) * F;
-    if (next > LIM) next = LIM;
-    const int64_t chunk = next - k;
-    for (int64_t a = 0; a < chunk; ++a) {
+  auto attempts = [&](int64_t cnt) -> int {
+    for (int64_t a = 0; a < cnt; ++a) {
       STRY(cols_spmv(E, 0));
       STRY(launch_cols(E, COLS_STEP));
       STRY(launch_rows(E, ROWS_STEP));
@@ -817,6 +979,62 @@ int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const dou
       for (auto &S : E.sh) MPAX_LAUNCH(k_decide, 1, 1, 0, s, S.st, S.P.tab, F, LIM);
     }
     MPAX_CHECK_LAUNCH();
+    return LP_OK;
+  };
+  // A chunk of F attempts that starts at a check boundary is replayed from a CUDA graph captured
+  // once per solve (every kernel argument and collective buffer is fixed within a solve; the
+  // virtual pointer tables were uploaded by step 2): one launch per F attempts instead of
+  // F x (4 p + collectives).  Chunks after rejections (fewer than F attempts left) are enqueued
+  // directly.  MPAX_SHARDED_GRAPH=0 switches the graph off; a failed capture falls back.
+  const char *genv = getenv("MPAX_SHARDED_GRAPH");
+  bool use_graph = !(genv && atoi(genv) == 0);
+  struct GraphGuard {
+    cudaGraphExec_t x = nullptr;
+    ~GraphGuard() { if (x) cudaGraphExecDestroy(x); }
+  } gexec;
+  int64_t glaunches = 0;
+  int64_t k = 0;
+  for (;;) {
+    int64_t next = ((k / F) + 1) * F;
+    if (next > LIM) next = LIM;
+    const int64_t chunk = next - k;
+    if (use_graph && chunk == F) {
+      if (!gexec.x) {
+        // captured on a private stream (the handle's may be the legacy default stream, which
+        // cannot capture); the graph is then launched on the handle's stream, in its order
+        const int64_t c0 = g_launches.load();
+        cudaGraph_t graph = nullptr;
+        cudaStream_t cs = nullptr, s0 = s;
+        int rc = LP_ERR_CUDA;
+        cudaError_t ec = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+        if (ec == cudaSuccess) ec = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+        if (ec == cudaSuccess) {
+          E.s = cs;
+          s = cs;
+          rc = attempts(F);
+          ec = cudaStreamEndCapture(cs, &graph);
+          E.s = s0;
+          s = s0;
+        }
+        if (cs) cudaStreamDestroy(cs);
+        glaunches = g_launches.load() - c0;   // launches recorded at capture: counted per replay
+        g_launches.fetch_sub(glaunches);
+        if (rc != LP_OK || ec != cudaSuccess || !graph || cudaGraphInstantiate(&gexec.x, graph, 0) != cudaSuccess) {
+          gexec.x = nullptr;
+          use_graph = false;
+          (void)cudaGetLastError();
+        }
+        if (graph) cudaGraphDestroy(graph);
+      }
+      if (gexec.x) {
+        MPAX_CUDA(cudaGraphLaunch(gexec.x, s));
+        g_launches.fetch_add(glaunches);
+      } else {
+        STRY(attempts(chunk));
+      }
+    } else {
+      STRY(attempts(chunk));
+    }
     MPAX_CUDA(cudaMemcpyAsync(E.h_st, E.sh[0].st, sizeof(ShState), cudaMemcpyDeviceToHost, s));
     MPAX_CUDA(cudaStreamSynchronize(s));
     if (E.h_st->halt) break;
@@ -837,15 +1055,29 @@ int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const dou
     STRY(launch_rows(E, ROWS_CERT));
     {
       std::vector<double *> sums, maxs;
-      for (auto &S : E.sh) { sums.push_back(S.st->certr); maxs.push_back(S.st->certr + 4); }
+      for (auto &S : E.sh) {
+        double *c = E.cols ? S.st->certc : S.st->certr;   // the sharded side's certificate partials
+        sums.push_back(c);
+        maxs.push_back(c + 4);
+      }
       STRY(reduce_vec(E, 5, sums, 4, false));
       STRY(reduce_vec(E, 6, maxs, 2, true));
+      if (E.vb) {   // variant B: the column side is sliced too
+        sums.clear();
+        maxs.clear();
+        for (auto &S : E.sh) { sums.push_back(S.st->certc); maxs.push_back(S.st->certc + 4); }
+        STRY(reduce_vec(E, 16, sums, 4, false));
+        STRY(reduce_vec(E, 17, maxs, 2, true));
+      }
     }
+    // verbose lines from one shard of rank 0 only (every shard takes the same decisions)
+    for (size_t g = 0; g < E.sh.size(); ++g)
+      MPAX_LAUNCH(k_check_decide, 1, 1, 0, s, E.sh[g].st, o.eps_abs, o.eps_rel, o.eps_primal_infeasible,
+                  o.eps_dual_infeasible, LIM, (g == 0 && E.rank == 0) ? o.verbose : 0, o.display_frequency,
+                  (int64_t)o.check_frequency, E.polish_mode, o.eps_feas_polish);
     for (auto &S : E.sh)
-      MPAX_LAUNCH(k_check_decide, 1, 1, 0, s, S.st, o.eps_abs, o.eps_rel, o.eps_primal_infeasible,
-                  o.eps_dual_infeasible, LIM);
-    for (auto &S : E.sh)
-      MPAX_LAUNCH(k_restart, blocks_for(E.n > S.P.m ? E.n : S.P.m), kB, 0, s, S.st, E.n, S.P.m, S.V);
+      MPAX_LAUNCH(k_restart, blocks_for(S.j1 - S.j0 > S.P.m ? S.j1 - S.j0 : S.P.m), kB, 0, s, S.st, S.j0, S.j1, S.P.m,
+                  S.V);
     MPAX_CHECK_LAUNCH();
     MPAX_CUDA(cudaMemcpyAsync(E.h_st, E.sh[0].st, sizeof(ShState), cudaMemcpyDeviceToHost, s));
     MPAX_CUDA(cudaStreamSynchronize(s));
@@ -855,11 +1087,17 @@ int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const dou
   STRY(launch_cols(E, COLS_OUT));
   STRY(launch_rows(E, ROWS_OUT));
   STRY(reduce_rowsum(E, 3));
+  if (E.vb) {   // variant B: the unscaled x and the reduced costs were written slice by slice
+    std::vector<double *> xr, lr;
+    for (auto &S : E.sh) { xr.push_back(S.V.red); lr.push_back(S.V.KTyp); }
+    STRY(allgather_vec(E, 13, xr));
+    STRY(allgather_vec(E, 14, lr));
+  }
   MPAX_LAUNCH(k_final, 1, 1, 0, s, E.sh[0].st, E.d_res);
   MPAX_CHECK_LAUNCH();
   for (auto &S : E.sh) {
-    MPAX_CUDA(cudaMemcpyAsync(S.X, S.V.red, E.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    MPAX_CUDA(cudaMemcpyAsync(S.L, S.V.KTyp, E.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    MPAX_CUDA(cudaMemcpyAsync(S.X, S.V.red, S.P.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    MPAX_CUDA(cudaMemcpyAsync(S.L, S.V.KTyp, S.P.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     if (S.P.m) MPAX_CUDA(cudaMemcpyAsync(S.Y, S.V.Kxp, S.P.m * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
   MPAX_CUDA(cudaEventRecord(E.ev1, s));
@@ -870,6 +1108,156 @@ int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const dou
   *out = *E.h_res;
   out->solve_seconds = ms * 1e-3;
   E.solved = true;
+  return LP_OK;
+}
+
+namespace {
+
+// Feasibility polishing on a sharded LP (reading 36; the single-GPU path's polish_combine_kernel):
+// per-shard partials of the combined point's objectives -- the n-side terms are replicated, so
+// only the first shard of rank 0 contributes them; q'y and |q|^2 are summed across shards.
+__global__ void k_polish_partials(int64_t n, int64_t m, const double *c0, const double *q0, const double *l0,
+                                  const double *u0, const double *x, const double *lam, const double *y,
+                                  int own_cols, int own_rows, double *out) {
+  __shared__ double red[4][kB / 32];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};  // c'x + l/u dual terms split below: [c'x, dual obj, |c|^2, |q|^2]
+  if (own_cols) {
+    for (int64_t j = threadIdx.x; j < n; j += kB) {
+      const double lm = lam[j], lp = fmax(lm, 0.0), ln = fmax(-lm, 0.0);
+      v[0] += c0[j] * x[j];
+      v[2] += c0[j] * c0[j];
+      if (l0[j] > -INFINITY) v[1] += l0[j] * lp;
+      if (u0[j] < INFINITY) v[1] -= u0[j] * ln;
+    }
+  }
+  if (own_rows) {
+    for (int64_t i = threadIdx.x; i < m; i += kB) {
+      v[1] += q0[i] * y[i];
+      v[3] += q0[i] * q0[i];
+    }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = 0; k < 4; ++k) {
+    double t = v[k];
+    for (int off = 16; off; off >>= 1) t += __shfl_xor_sync(FULL, t, off);
+    if (lane == 0) red[k][w] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double t = 0.0;
+    for (int ww = 0; ww < kB / 32; ++ww) t += red[threadIdx.x][ww];
+    out[threadIdx.x] = t;
+  }
+}
+
+__global__ void k_polish_final(const double *t, const lp_result *r1, const lp_result *r2, lp_result *res) {
+  lp_result r = *res;
+  const double pres = r1->primal_residual, dres = r2->dual_residual;
+  const double nc = sqrt(t[2]), nq = sqrt(t[3]), gap = fabs(t[0] - t[1]);
+  r.primal_objective = t[0]; r.dual_objective = t[1];
+  r.primal_residual = pres; r.dual_residual = dres; r.gap = gap;
+  r.rel_kkt = fmax(pres / (1.0 + nq), fmax(dres / (1.0 + nc), gap / (1.0 + fabs(t[0]) + fabs(t[1]))));
+  r.iterations += r1->iterations + r2->iterations;
+  r.attempts += r1->attempts + r2->attempts;
+  r.restarts += r1->restarts + r2->restarts;
+  r.polish = (r1->status == LP_OPTIMAL && r2->status == LP_OPTIMAL) ? 1 : 2;
+  *res = r;
+}
+
+}  // namespace
+
+// lp_solve on a sharded handle with feasibility polishing (reading 36): the main solve, then -- if
+// it ended OPTIMAL -- a primal polish (c = 0 from (x*, 0)) and a dual polish (q = 0 from
+// (proj 0, y*)) on the same sharded engine with residual-only tests, infeasibility detection off
+// and at most min(iteration_limit, 100000) accepted steps each; x from the primal polish, y and
+// the reduced costs from the dual polish, objectives recomputed on the original c, q, l, u.
+int sharded_solve_polished(ShardedLP &E, const lp_options &o, const double *X0, const double *Y0, lp_result *out) {
+  lp_options om = o;
+  om.feasibility_polishing = 0;
+  STRY(sharded_solve(E, om, X0, Y0, out));
+  if (!o.feasibility_polishing || out->status != LP_OPTIMAL) return LP_OK;
+  cudaStream_t s = E.s;
+  const int64_t n = E.n;
+  int64_t mtot = 0;
+  for (auto &S : E.sh) mtot += S.P.m;
+  for (auto &S : E.sh) {
+    if (!S.pol) {
+      const int64_t mm = S.P.m > 0 ? S.P.m : 1;
+      MPAX_CUDA(cudaMallocAsync((void **)&S.pol, (size_t)(3 * n + 2 * mm + 8) * sizeof(double), s));
+      MPAX_CUDA(cudaMemsetAsync(S.pol, 0, (size_t)(3 * n + 2 * mm + 8) * sizeof(double), s));
+    }
+  }
+  // the main solve's (x*, y*) in sharded_solve's warm-start layout: the replicated side from the
+  // first shard, the sharded side concatenated in this process's shard order
+  int64_t ntot = 0;
+  for (auto &S : E.sh) ntot += S.P.n;
+  const int64_t nx = E.cols ? ntot : n, ny = E.cols ? E.sh[0].P.m : mtot;
+  double *xstar = nullptr, *ystar = nullptr;
+  lp_result *res_d = nullptr;
+  MPAX_CUDA(cudaMallocAsync((void **)&xstar, (size_t)(nx > 0 ? nx : 1) * sizeof(double), s));
+  MPAX_CUDA(cudaMallocAsync((void **)&ystar, (size_t)(ny > 0 ? ny : 1) * sizeof(double), s));
+  MPAX_CUDA(cudaMallocAsync((void **)&res_d, 3 * sizeof(lp_result), s));
+  MPAX_CUDA(cudaMemcpyAsync(res_d, E.d_res, sizeof(lp_result), cudaMemcpyDeviceToDevice, s));
+  {
+    int64_t ox = 0, oy = 0;
+    for (size_t g = 0; g < E.sh.size(); ++g) {
+      auto &S = E.sh[g];
+      if (E.cols || g == 0) MPAX_CUDA(cudaMemcpyAsync(xstar + ox, S.X, S.P.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      if ((!E.cols || g == 0) && S.P.m)
+        MPAX_CUDA(cudaMemcpyAsync(ystar + oy, S.Y, S.P.m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      if (E.cols) ox += S.P.n; else oy += S.P.m;
+    }
+  }
+  lp_options op = o;
+  op.feasibility_polishing = 0;
+  op.eps_primal_infeasible = -1.0;
+  op.eps_dual_infeasible = -1.0;
+  if (op.iteration_limit > 100000) op.iteration_limit = 100000;
+  lp_result r1, r2;
+  // primal polish: c = 0 (zeros at pol + 2n), from (x*, 0)
+  for (auto &S : E.sh) S.V.c0 = S.pol + 2 * n;
+  E.polish_mode = 1;
+  int rc = sharded_solve(E, op, xstar, nullptr, &r1);
+  for (auto &S : E.sh) S.V.c0 = S.c0;
+  if (rc != LP_OK) { E.polish_mode = 0; return rc; }
+  MPAX_CUDA(cudaMemcpyAsync(res_d + 1, E.d_res, sizeof(lp_result), cudaMemcpyDeviceToDevice, s));
+  for (auto &S : E.sh) MPAX_CUDA(cudaMemcpyAsync(S.pol + n, S.X, S.P.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  // dual polish: q = 0 (zeros at pol + 3n + m), from (proj 0, y*)
+  for (auto &S : E.sh) S.V.q0 = S.pol + 3 * n + (S.P.m > 0 ? S.P.m : 1);
+  E.polish_mode = 2;
+  rc = sharded_solve(E, op, nullptr, ny > 0 ? ystar : nullptr, &r2);
+  for (auto &S : E.sh) S.V.q0 = S.q0;
+  E.polish_mode = 0;
+  if (rc != LP_OK) return rc;
+  MPAX_CUDA(cudaMemcpyAsync(res_d + 2, E.d_res, sizeof(lp_result), cudaMemcpyDeviceToDevice, s));
+  // combine: X <- x_p; Y, L stay the dual polish's; objectives on the original data
+  std::vector<double *> parts;
+  for (size_t g = 0; g < E.sh.size(); ++g) {
+    auto &S = E.sh[g];
+    MPAX_CUDA(cudaMemcpyAsync(S.X, S.pol + n, S.P.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    double *pt = S.pol + 3 * n + 2 * (S.P.m > 0 ? S.P.m : 1);
+    const int first = (g == 0 && E.rank == 0) ? 1 : 0;   // the replicated side is counted once
+    if (E.vb)   // variant B: every shard sums its own slice of the n-side terms
+      MPAX_LAUNCH(k_polish_partials, 1, kB, 0, s, S.j1 - S.j0, S.P.m, S.V.c0 + S.j0, S.V.q0, S.P.l0 + S.j0,
+                  S.P.u0 + S.j0, S.X + S.j0, S.L + S.j0, S.Y, 1, 1, pt);
+    else
+      MPAX_LAUNCH(k_polish_partials, 1, kB, 0, s, S.P.n, S.P.m, S.V.c0, S.V.q0, S.P.l0, S.P.u0, S.X, S.L, S.Y,
+                  E.cols ? 1 : first, E.cols ? first : 1, pt);
+    parts.push_back(pt);
+  }
+  MPAX_CHECK_LAUNCH();
+  STRY(reduce_vec(E, 7, parts, 4, false));
+  MPAX_LAUNCH(k_polish_final, 1, 1, 0, s, parts[0], res_d + 1, res_d + 2, res_d);
+  MPAX_CHECK_LAUNCH();
+  MPAX_CUDA(cudaMemcpyAsync(E.d_res, res_d, sizeof(lp_result), cudaMemcpyDeviceToDevice, s));
+  MPAX_CUDA(cudaMemcpyAsync(E.h_res, res_d, sizeof(lp_result), cudaMemcpyDeviceToHost, s));
+  MPAX_CUDA(cudaStreamSynchronize(s));
+  const double secs = out->solve_seconds + r1.solve_seconds + r2.solve_seconds;
+  *out = *E.h_res;
+  out->solve_seconds = secs;
+  cudaFreeAsync(xstar, s);
+  cudaFreeAsync(ystar, s);
+  cudaFreeAsync(res_d, s);
   return LP_OK;
 }
 
@@ -892,6 +1280,7 @@ void sharded_free(ShardedLP *E) {
     if (S.arena) cudaFreeAsync(S.arena, E->s);
     if (S.vecs) cudaFreeAsync(S.vecs, E->s);
     if (S.P.split_mem) cudaFreeAsync(S.P.split_mem, E->s);
+    if (S.pol) cudaFreeAsync(S.pol, E->s);
   }
   if (E->d_ptrs) cudaFreeAsync(E->d_ptrs, E->s);
   if (E->d_res) cudaFreeAsync(E->d_res, E->s);
@@ -907,6 +1296,18 @@ void sharded_free(ShardedLP *E) {
 int sharded_get(ShardedLP *E, double *x, double *y, double *rc) {
   if (!E->solved) return LP_ERR_NOT_SOLVED;
   cudaStream_t s = E->s;
+  if (E->cols) {   // x, rc: this process's columns in shard order; y replicated
+    int64_t off = 0;
+    for (auto &S : E->sh) {
+      if (x) MPAX_CUDA(cudaMemcpyAsync(x + off, S.X, S.P.n * sizeof(double), cudaMemcpyDefault, s));
+      if (rc) MPAX_CUDA(cudaMemcpyAsync(rc + off, S.L, S.P.n * sizeof(double), cudaMemcpyDefault, s));
+      off += S.P.n;
+    }
+    if (y && E->sh[0].P.m)
+      MPAX_CUDA(cudaMemcpyAsync(y, E->sh[0].Y, E->sh[0].P.m * sizeof(double), cudaMemcpyDefault, s));
+    MPAX_CUDA(cudaStreamSynchronize(s));
+    return LP_OK;
+  }
   if (x) MPAX_CUDA(cudaMemcpyAsync(x, E->sh[0].X, E->n * sizeof(double), cudaMemcpyDefault, s));
   if (rc) MPAX_CUDA(cudaMemcpyAsync(rc, E->sh[0].L, E->n * sizeof(double), cudaMemcpyDefault, s));
   if (y) {
@@ -921,7 +1322,15 @@ int sharded_get(ShardedLP *E, double *x, double *y, double *rc) {
 }
 
 int64_t sharded_n(const ShardedLP *E) { return E->n; }
+// this process's share: columns (column mode; all n in row mode) and rows (all m in column mode)
+int64_t sharded_n_local(const ShardedLP *E) {
+  if (!E->cols) return E->n;
+  int64_t n = 0;
+  for (auto &S : E->sh) n += S.P.n;
+  return n;
+}
 int64_t sharded_m_local(const ShardedLP *E) {
+  if (E->cols) return E->sh.empty() ? 0 : E->sh[0].P.m;
   int64_t m = 0;
   for (auto &S : E->sh) m += S.P.m;
   return m;
@@ -929,9 +1338,9 @@ int64_t sharded_m_local(const ShardedLP *E) {
 
 // Create: `descs` are this process's row shards (one per GPU rank, p for virtual mode).
 int sharded_create(ShardedLP *E, const std::vector<lp_problem_desc> &descs, const std::vector<int64_t> &offsets,
-                   int64_t n, int64_t m1g, int64_t m2g, void *comm, int rank, int nranks, bool virt) {
+                   int64_t n, int64_t m1g, int64_t m2g, void *comm, int rank, int nranks, bool virt, bool cols) {
   E->n = n; E->m1_global = m1g; E->m_global = m1g + m2g;
-  E->comm = comm; E->rank = rank; E->nranks = nranks; E->virt = virt;
+  E->comm = comm; E->rank = rank; E->nranks = nranks; E->virt = virt; E->cols = cols;
   if (!E->h_st || !E->d_res) return LP_ERR_OUT_OF_MEMORY;
   return sharded_setup(*E, descs, offsets);
 }

@@ -18,13 +18,15 @@ RAPDHG, R2HPDHG = 0, 1
 PATH_AUTO, PATH_INSTANCE, PATH_GRID, PATH_DMMA = 0, 1, 2, 3
 STEP_ADAPTIVE, STEP_CONSTANT = 0, 1
 FP64, FP32 = 0, 1
+SHARD_ROWS, SHARD_COLS, SHARD_AUTO = 0, 1, 2
 
 EXPORTED_SYMBOLS = [
     "lp_default_options", "lp_create", "lp_create_batch", "lp_update_batch", "lp_solve", "lp_solve_batch",
     "lp_get_solution", "lp_get_solutions", "lp_get_shape", "lp_get_scaling", "lp_spmv_scaled",
     "lp_kernel_launch_count", "lp_error_string", "lp_last_error_detail", "lp_destroy",
     "lp_create_sharded", "lp_create_sharded_virtual", "lp_nccl_unique_id", "lp_nccl_comm_init",
-    "lp_nccl_comm_destroy", "lp_spo_plus", "lp_selftest_division",
+    "lp_nccl_comm_destroy", "lp_spo_plus", "lp_selftest_division", "lp_set_decision_log",
+    "lp_shard_axis", "lp_create_sharded_cols", "lp_create_sharded_virtual_axis",
 ]
 
 
@@ -50,7 +52,7 @@ class Options(C.Structure):
                 ("iteration_limit", C.c_int64), ("check_frequency", C.c_int32), ("algorithm", C.c_int32),
                 ("warm_start", C.c_int32), ("feasibility_polishing", C.c_int32), ("verbose", C.c_int32),
                 ("display_frequency", C.c_int32), ("path", C.c_int32), ("step_rule", C.c_int32),
-                ("reflection", C.c_double), ("precision", C.c_int32), ("reserved", C.c_int32)]
+                ("reflection", C.c_double), ("precision", C.c_int32), ("sharded_exchange", C.c_int32)]
 
 
 class Result(C.Structure):
@@ -94,11 +96,18 @@ def lib():
             L.lp_get_solutions.argtypes = [V, V, V, C.c_int32]
             L.lp_get_shape.argtypes = [V, P(C.c_int64), P(C.c_int64), P(C.c_int64), P(C.c_int64)]
             L.lp_get_scaling.argtypes = [V, V, V, C.c_int32]
+            if hasattr(L, "lp_set_decision_log"):
+                L.lp_set_decision_log.argtypes = [V, V, C.c_int64, V, C.c_int64]
             L.lp_spmv_scaled.argtypes = [V, V, V, V, V, C.c_int32]
             L.lp_kernel_launch_count.restype = C.c_int64
             L.lp_create_sharded.argtypes = [P(ProblemDesc), C.c_int64, C.c_int64, C.c_int64, V, C.c_int, C.c_int,
                                             V, P(V)]
             L.lp_create_sharded_virtual.argtypes = [P(ProblemDesc), C.c_int32, V, P(V)]
+            if hasattr(L, "lp_create_sharded_cols"):
+                L.lp_shard_axis.argtypes = [C.c_int64, C.c_int64]
+                L.lp_create_sharded_cols.argtypes = [P(ProblemDesc), C.c_int64, C.c_int64, V, C.c_int, C.c_int, V,
+                                                     P(V)]
+                L.lp_create_sharded_virtual_axis.argtypes = [P(ProblemDesc), C.c_int32, C.c_int32, V, P(V)]
             L.lp_nccl_unique_id.argtypes = [V]
             L.lp_nccl_comm_init.argtypes = [P(V), C.c_int, V, C.c_int]
             L.lp_nccl_comm_destroy.argtypes = [V]
@@ -333,6 +342,11 @@ class Solver:
         o = default_options(**opts)
         a, b = _Arr(x0, np.float64), _Arr(y0, np.float64)
         mem = _same_mem([x0, y0])
+        if getattr(self, "_alog", None) is not None:   # the decision log's rows start unwritten
+            self._alog.fill_(float("nan"))
+            self._clog.fill_(float("nan"))
+            import torch
+            torch.cuda.current_stream().synchronize()
         r = Result()
         _check(lib().lp_solve(self._h, C.byref(o), a.ptr, b.ptr, mem, C.byref(r)), "lp_solve")
         return r.as_dict()
@@ -344,6 +358,26 @@ class Solver:
         p = lambda t: t.data_ptr() if _is_torch(t) else (t.ctypes.data if t.size else None)
         _check(lib().lp_get_solution(self._h, 0, p(x), p(y) if m else None, p(lam), memory), "lp_get_solution")
         return x, y, lam
+
+    def set_decision_log(self, att_cap=4096, chk_cap=256, device=None):
+        """Record the grid path's decisions (lp_set_decision_log) into device buffers of the given
+        capacities (NaN-filled before every solve); decision_log() returns the rows written.
+        att_cap = 0 and chk_cap = 0 switch it off."""
+        import torch
+        dev = device or (self._device if self._device is not None else "cuda")
+        self._alog = torch.full((max(att_cap, 1), 4), float("nan"), dtype=torch.float64, device=dev)
+        self._clog = torch.full((max(chk_cap, 1), 6), float("nan"), dtype=torch.float64, device=dev)
+        _check(lib().lp_set_decision_log(self._h, self._alog.data_ptr() if att_cap else None, att_cap,
+                                         self._clog.data_ptr() if chk_cap else None, chk_cap),
+               "lp_set_decision_log")
+        if not att_cap and not chk_cap:
+            self._alog = self._clog = None
+
+    def decision_log(self):
+        """(attempts, checks): numpy arrays of the rows the last solve wrote (the row layout of ora_log, include/lp.h)."""
+        a = self._alog.cpu().numpy()
+        c = self._clog.cpu().numpy()
+        return a[~np.isnan(a[:, 0])], c[~np.isnan(c[:, 0])]
 
     def scaling(self):
         Dr, Dc = np.zeros(max(self.problem.m, 1)), np.zeros(self.problem.n)
@@ -484,6 +518,43 @@ def local_rows(problem: Problem, r0: int, r1: int) -> Problem:
                    np.asarray(problem.values)[sl], problem.c, np.asarray(problem.q)[r0:r1], problem.l, problem.u)
 
 
+def shard_axis(m: int, n: int) -> int:
+    """The axis whose exchanged vector is shorter (lp_shard_axis): columns iff m < n."""
+    return int(lib().lp_shard_axis(int(m), int(n)))
+
+
+def col_partition(problem: Problem, parts: int):
+    """Contiguous column blocks balanced by nnz (a cut on the prefix of the column counts);
+    returns parts+1 cut points.  Same rule as the library's virtual column shards."""
+    n = problem.n
+    cc = np.zeros(n + 1, np.int64)
+    np.add.at(cc, np.asarray(problem.col_idx, np.int64) + 1, 1)
+    cc = np.cumsum(cc)
+    nnz = int(cc[-1])
+    cuts = [0]
+    for g in range(1, parts):
+        c = int(np.searchsorted(cc, nnz * g // parts, side="left"))
+        cuts.append(min(max(c, cuts[-1]), n))
+    cuts.append(n)
+    return cuts
+
+
+def local_cols(problem: Problem, c0: int, c1: int) -> Problem:
+    """Columns [c0, c1) of K as a local problem for lp_create_sharded_cols: every row (global m1,
+    m2), local column indices, the full q, and c, l, u of those columns."""
+    rp = np.asarray(problem.row_ptr, dtype=np.int64)
+    ci = np.asarray(problem.col_idx, dtype=np.int64)
+    v = np.asarray(problem.values, dtype=np.float64)
+    keep = (ci >= c0) & (ci < c1)
+    rows = np.repeat(np.arange(rp.size - 1), np.diff(rp))[keep]
+    lrp = np.zeros(rp.size, np.int64)
+    np.add.at(lrp, rows + 1, 1)
+    lrp = np.cumsum(lrp)
+    sl = slice(c0, c1)
+    return Problem(c1 - c0, problem.m1, problem.m2, lrp, (ci[keep] - c0).astype(np.int32), v[keep],
+                   np.asarray(problem.c)[sl], problem.q, np.asarray(problem.l)[sl], np.asarray(problem.u)[sl])
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().lp_nccl_unique_id(buf), "lp_nccl_unique_id")
@@ -502,18 +573,31 @@ def nccl_comm_destroy(comm: int):
 
 
 class ShardedSolver(Solver):
-    """One LP row-sharded across GPUs (lp_create_sharded), or across `virtual_shards`
-    row blocks on one GPU (lp_create_sharded_virtual)."""
+    """One LP sharded across GPUs by rows (lp_create_sharded) or, axis="cols", by columns
+    (lp_create_sharded_cols: `problem` is this rank's local_cols block), or across
+    `virtual_shards` blocks on one GPU (lp_create_sharded_virtual_axis; axis "rows", "cols" or
+    "auto" = the axis whose exchanged vector is shorter)."""
 
     def __init__(self, problem: Problem, global_row_offset=0, m1_global=None, m2_global=None, comm=None,
-                 rank=0, nranks=1, virtual_shards=None, stream=None):
+                 rank=0, nranks=1, virtual_shards=None, stream=None, axis="rows", global_col_offset=0,
+                 n_global=None):
         self.problem = problem
         d, keep = problem._desc()
         self._device = problem.c.device if _is_torch(problem.c) else None
         h = C.c_void_p()
-        if virtual_shards is not None:
+        ax = {"rows": SHARD_ROWS, "cols": SHARD_COLS, "auto": SHARD_AUTO}.get(axis, axis)
+        if virtual_shards is not None and ax == SHARD_ROWS:
             _check(lib().lp_create_sharded_virtual(C.byref(d), int(virtual_shards), _stream_handle(stream),
                                                    C.byref(h)), "lp_create_sharded_virtual")
+        elif virtual_shards is not None:
+            _check(lib().lp_create_sharded_virtual_axis(C.byref(d), int(virtual_shards), int(ax),
+                                                        _stream_handle(stream), C.byref(h)),
+                   "lp_create_sharded_virtual_axis")
+        elif ax == SHARD_COLS:
+            ng = problem.n if n_global is None else n_global
+            _check(lib().lp_create_sharded_cols(C.byref(d), int(global_col_offset), int(ng), comm, int(rank),
+                                                int(nranks), _stream_handle(stream), C.byref(h)),
+                   "lp_create_sharded_cols")
         else:
             m1g = problem.m1 if m1_global is None else m1_global
             m2g = problem.m2 if m2_global is None else m2_global

@@ -18,6 +18,9 @@ PROF_K=64 python scripts/prof_grid.py > gpurun_out/${T}_c4_plain.log 2>&1 && \
 PROF_M=5000000 PROF_K=16 python scripts/prof_grid.py > gpurun_out/${T}_c5_plain.log 2>&1 && \
   PROF_M=5000000 PROF_K=16 ncu --set full --clock-control none --import-source on -k regex:grid_kernel -s 1 -c 1 \
   -o gpurun_out/${T}_grid_c5 python scripts/prof_grid.py > gpurun_out/${T}_ncu_c5.log 2>&1
+PROF_PREC=fp32 PROF_M=5000000 PROF_K=16 python scripts/prof_grid.py > gpurun_out/${T}_c5f_plain.log 2>&1 && \
+  PROF_PREC=fp32 PROF_M=5000000 PROF_K=16 ncu --set full --clock-control none --import-source on -k regex:grid_kernel \
+  -s 1 -c 1 -o gpurun_out/${T}_grid_c5f python scripts/prof_grid.py > gpurun_out/${T}_ncu_c5f.log 2>&1
 C3_PATHS=3 python scripts/c3_bench.py > gpurun_out/${T}_c3_plain.log 2>&1 && \
   C3_PATHS=3 ncu --set full --clock-control none --import-source on -k regex:dmma_kernel -c 1 \
   -o gpurun_out/${T}_dmma python scripts/c3_bench.py > gpurun_out/${T}_ncu_dmma.log 2>&1

@@ -3,7 +3,8 @@
 DMMA kernel, per attempt of the grid kernel (C4, C5: the capture's solve is limited to PROF_K
 accepted steps; the per-attempt figure divides the whole launch -- init, the check at the limit and
 the output included -- by its attempts, an upper bound).
-usage: python scripts/traffic_from_ncu.py TAG tiny.ncu-rep grid_c4.ncu-rep:ATT grid_c5.ncu-rep:ATT dmma.ncu-rep"""
+usage: python scripts/traffic_from_ncu.py TAG tiny.ncu-rep grid_c4.ncu-rep:ATT grid_c5.ncu-rep:ATT dmma.ncu-rep
+       [grid_c5_fp32.ncu-rep:ATT]"""
 import csv
 import io
 import json
@@ -41,6 +42,10 @@ def main():
                               "algorithmic_bytes_per_attempt": 3.50e9, "capture": os.path.basename(c5r)},
            "dmma_kernel_c3": {"bytes_per_launch": dram(dm), "launch": "one C3 DMMA batch solve",
                               "capture": os.path.basename(dm)}}
+    if len(sys.argv) > 6:
+        fr, fa = sys.argv[6].split(":")
+        out["grid_kernel_c5_fp32"] = {"bytes_per_attempt": dram(fr) / float(fa), "attempts": int(fa),
+                                      "algorithmic_bytes_per_attempt": 2.18e9, "capture": os.path.basename(fr)}
     json.dump(out, open(os.path.join(root, "profiles", "traffic.json"), "w"), indent=1)
     print(json.dumps(out, indent=1))
 

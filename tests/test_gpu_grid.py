@@ -29,7 +29,9 @@ def grid_solve(lp, alg, path=mp.PATH_GRID, x0=None, y0=None, **kw):
 
 CASES = [("tiny", lpgen.tiny_spec()), ("C1", lpgen.g_rand(50, 100, 10, seed=1)),
          ("ragged", lpgen.g_rand(37, 61, 5, seed=7)), ("mid", lpgen.g_rand(3000, 5000, 12, seed=3)),
-         ("wide", lpgen.g_rand(700, 9000, 30, seed=8)), ("dense", lpgen.g_dense(60, 90, batch=1, seed=5)[0])]
+         ("wide", lpgen.g_rand(700, 9000, 30, seed=8)), ("dense", lpgen.g_dense(60, 90, batch=1, seed=5)[0]),
+         # skewed row lengths (Pareto tail; longest rows 300 and 5 366 entries, median 12)
+         ("powerlaw", lpgen.g_powerlaw(300, 600, 12, seed=9)), ("powerlaw-big", lpgen.g_powerlaw(20000, 40000, 20, seed=9))]
 
 
 @pytest.mark.parametrize("alg", ALGS)

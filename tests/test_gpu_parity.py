@@ -435,19 +435,26 @@ def test_tiny_register_path_matches_generic_kernel(alg):
     assert agree >= 0.95 * 256, agree
 
 
-def test_verbose_lines():
-    """verbose = 1: one device printf line per display_frequency-th check; off by default."""
+@pytest.mark.parametrize("engine,expect", [("single", 4), ("dmma", 32), ("sharded", 4)])
+def test_verbose_lines(engine, expect):
+    """verbose = 1: one device printf line per display_frequency-th check of every
+    instance, on every engine; off by default."""
     import subprocess
     import sys
+    mk = {"single": "mp.Solver(mp.Problem.from_lp(lpgen.g_rand(50, 100, 10, seed=1)))",
+          "dmma": "mp.BatchSolver(mp.Problem.from_lp(d[0]), d[1], d[2])",
+          "sharded": "mp.ShardedSolver(mp.Problem.from_lp(lpgen.g_rand(50, 100, 10, seed=1)), virtual_shards=2)"}[engine]
+    path = ", path=mp.PATH_DMMA" if engine == "dmma" else ""
     code = ("import lpgen, paper_2412_09734_b200 as mp\n"
-            "lp = lpgen.g_rand(50, 100, 10, seed=1)\n"
+            "d = lpgen.g_dense(60, 90, batch=8, seed=5)\n"
             "for v in (0, 1):\n"
-            "    with mp.Solver(mp.Problem.from_lp(lp)) as s:\n"
-            "        s.solve(algorithm='ra', verbose=v, display_frequency=1, iteration_limit=256, eps_abs=0.0, eps_rel=0.0)\n"
+            f"    s = {mk}\n"
+            f"    s.solve(algorithm='ra', verbose=v, display_frequency=1, iteration_limit=256, eps_abs=0.0, eps_rel=0.0{path})\n"
+            "    s.close()\n"
             "    print('END', v, flush=True)\n")
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
                          cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__))).stdout
     first, second = out.split("END 0")
     assert "[mpax]" not in first
     lines = [l for l in second.splitlines() if l.startswith("[mpax]")]
-    assert len(lines) == 4 and "iter      256" in lines[-1], out
+    assert len(lines) == expect and "iter      256" in lines[-1], out

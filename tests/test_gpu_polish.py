@@ -137,15 +137,42 @@ def test_dmma_dense_batch(alg):
         assert abs(res[b]["primal_objective"] - ro[b]["primal_objective"]) <= 1e-2 * (1 + abs(obj[b]))
 
 
-def test_unfinished_polish_flag_and_sharded_rejection():
+def test_unfinished_polish_flag():
     lp = lpgen.g_rand(50, 100, 10, seed=1)
     r = gpu_single(lp, "ra", eps_abs=1e-2, eps_rel=1e-2, iteration_limit=192, eps_feas_polish=1e-14, **POL)
     ro = oracle.solve(lp, "ra", eps_abs=1e-2, eps_rel=1e-2, iteration_limit=192, feasibility_polishing=True,
                       eps_feas_polish=1e-14)
     assert r["status"] == ro["status"] == mp.LP_OPTIMAL and r["polish"] == ro["polish"] == 2
     with mp.ShardedSolver(mp.Problem.from_lp(lp), virtual_shards=2) as s:
-        with pytest.raises(mp.LpError):
-            s.solve(algorithm="ra", **POL)
+        r = s.solve(algorithm="ra", eps_abs=1e-2, eps_rel=1e-2, iteration_limit=192, eps_feas_polish=1e-14, **POL)
+    assert r["status"] == mp.LP_OPTIMAL and r["polish"] == 2
+
+
+@pytest.mark.parametrize("rule", ["adaptive", "constant"])
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("shards", [1, 2, 3])
+def test_sharded(shards, alg, rule):
+    """Polishing on the row-sharded engine (virtual shards on one GPU): the same two sub-solves
+    and the same combination as every other path."""
+    lp = lpgen.g_rand(50, 100, 10, seed=1)
+    kw = dict(eps_abs=1e-2, eps_rel=1e-2, step_rule=rule)
+    ro = oracle.solve(lp, alg, feasibility_polishing=True, **kw)
+    with mp.ShardedSolver(mp.Problem.from_lp(lp), virtual_shards=shards) as s:
+        rg = s.solve(algorithm=alg, **POL, **kw)
+        x, y, lam = s.solution()
+    assert rg["status"] == ro["status"] == mp.LP_OPTIMAL
+    assert rg["polish"] == ro["polish"] == 1
+    assert polished_ok(lp, x, y)
+    assert np.allclose(lam, lp.c - lp.dense_K().T @ y, atol=1e-9)
+    k = oracle.kkt_original(lp, x, y)
+    assert rg["primal_residual"] == pytest.approx(k["pres"], rel=1e-6, abs=1e-14)
+    assert rg["dual_residual"] == pytest.approx(k["dres"], rel=1e-6, abs=1e-14)
+    assert rg["primal_objective"] == pytest.approx(float(lp.c @ x), rel=1e-12)
+    assert rg["dual_objective"] == pytest.approx(k["dobj"], rel=1e-9, abs=1e-12)
+    if rule == "constant":  # well-posed trajectories: the same polished pair as the oracle
+        assert rg["iterations"] == ro["iterations"]
+        assert rel(x, ro["x"]) <= 1e-7 and rel(y, ro["y"]) <= 1e-7
+    parity_log(f"sharded_polish[{shards},{alg},{rule}]", compared=1, total=1)
 
 
 def test_no_polish_when_not_optimal():

@@ -109,3 +109,147 @@ def test_sharded_two_pass_rows(alg, shards, name, lp, monkeypatch):
     for key in ("status", "iterations", "attempts", "restarts"):
         assert rg[key] == ro[key], (key, rg[key], ro[key])
     assert rel(rg["x"], ro["x"]) <= tol and rel(rg["y"], ro["y"]) <= tol
+
+
+# ---- column sharding (the axis chosen by min(m, n); reading 33) ----
+COL_CASES = [("C1", lpgen.g_rand(50, 100, 10, seed=1)), ("wide", lpgen.g_rand(700, 9000, 30, seed=8)),
+             ("tiny", lpgen.tiny_spec())]
+
+
+def sharded_cols(lp, alg, shards, axis="cols", **kw):
+    with mp.ShardedSolver(mp.Problem.from_lp(lp), virtual_shards=shards, axis=axis) as s:
+        r = s.solve(algorithm=alg, **kw)
+        x, y, lam = s.solution()
+    r.update(x=x, y=y, lam=lam)
+    return r
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("K", [1, 2, 64])
+@pytest.mark.parametrize("shards", [1, 2, 3])
+@pytest.mark.parametrize("name,lp", COL_CASES)
+def test_cols_fixed_K(alg, K, shards, name, lp):
+    if shards > lp.n:
+        pytest.skip("more shards than columns")
+    ro, stable, drift = oracle_stability(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=K)
+    rg = sharded_cols(lp, alg, shards, eps_abs=0.0, eps_rel=0.0, iteration_limit=K)
+    if not stable:
+        pytest.skip("ill-conditioned at this K: the oracle's own counts move under a 1-ulp perturbation")
+    tol = max(1e-9, 100 * drift)
+    for key in ("status", "iterations", "attempts", "restarts"):
+        assert rg[key] == ro[key], (key, rg[key], ro[key])
+    assert rel(rg["x"], ro["x"]) <= tol
+    assert rel(rg["lam"], ro["lam"]) <= max(1e-8, 1e3 * drift)
+    if lp.m:
+        assert rel(rg["y"], ro["y"]) <= tol
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("shards", [1, 4])
+@pytest.mark.parametrize("name,lp", COL_CASES[:2])
+def test_cols_full_solve(alg, shards, name, lp):
+    ro, stable, drift = oracle_stability(lp, alg)
+    rg = sharded_cols(lp, alg, shards)
+    assert rg["status"] == mp.LP_OPTIMAL and rg["rel_kkt"] <= 1e-4
+    if stable:
+        assert rg["iterations"] == ro["iterations"] and rg["restarts"] == ro["restarts"]
+        assert abs(rg["primal_objective"] - ro["primal_objective"]) <= obj_tol(ro) * (1 + abs(ro["primal_objective"]))
+    k = oracle.kkt_original(lp, rg["x"], rg["y"])
+    assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.q))
+    assert k["dres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.c))
+    assert abs(rg["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
+
+
+def test_axis_auto_and_refusals():
+    wide = lpgen.g_rand(50, 100, 10, seed=1)          # m < n: columns
+    a = sharded_cols(wide, "r2", 2, axis="auto", iteration_limit=128, eps_abs=0.0, eps_rel=0.0)
+    b = sharded_cols(wide, "r2", 2, axis="cols", iteration_limit=128, eps_abs=0.0, eps_rel=0.0)
+    assert a["attempts"] == b["attempts"] and np.array_equal(a["x"], b["x"]) and np.array_equal(a["y"], b["y"])
+    tall = lpgen.g_rand(100, 60, 8, seed=2)           # m >= n: rows
+    a = sharded_cols(tall, "r2", 2, axis="auto", iteration_limit=128, eps_abs=0.0, eps_rel=0.0)
+    b = sharded(tall, "r2", 2, iteration_limit=128, eps_abs=0.0, eps_rel=0.0)
+    assert a["attempts"] == b["attempts"] and np.array_equal(a["x"], b["x"]) and np.array_equal(a["y"], b["y"])
+    with pytest.raises(mp.LpError) as e:
+        sharded_cols(wide, "r2", 2, step_rule="constant")
+    assert e.value.code == -10
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_cols_polish_and_warm_start(alg):
+    lp = lpgen.g_rand(50, 100, 10, seed=1)
+    ro = oracle.solve(lp, alg, eps_abs=1e-2, eps_rel=1e-2, feasibility_polishing=True)
+    rg = sharded_cols(lp, alg, 3, eps_abs=1e-2, eps_rel=1e-2, feasibility_polishing=1)
+    assert rg["status"] == ro["status"] == mp.LP_OPTIMAL and rg["polish"] == ro["polish"] == 1
+    k = oracle.kkt_original(lp, rg["x"], rg["y"])
+    assert k["pres"] <= (1 + 1e-9) * 1e-6 * (1 + np.linalg.norm(lp.q))
+    assert k["dres"] <= (1 + 1e-9) * 1e-6 * (1 + np.linalg.norm(lp.c))
+    assert rg["primal_objective"] == pytest.approx(float(lp.c @ rg["x"]), rel=1e-12)
+    rng = np.random.default_rng(2)
+    x0, y0 = rng.normal(size=lp.n), rng.normal(size=lp.m)
+    ro = oracle.solve(lp, alg, x0=x0, y0=y0, iteration_limit=64, eps_abs=0, eps_rel=0)
+    with mp.ShardedSolver(mp.Problem.from_lp(lp), virtual_shards=2, axis="cols") as s:
+        rg = s.solve(x0, y0, algorithm=alg, iteration_limit=64, eps_abs=0.0, eps_rel=0.0)
+        x, y, _ = s.solution()
+    assert rg["attempts"] == ro["attempts"] and rel(x, ro["x"]) <= 1e-9 and rel(y, ro["y"]) <= 1e-9
+
+
+@pytest.mark.parametrize("axis", ["rows", "cols"])
+def test_graph_replay_matches_direct(axis, monkeypatch):
+    """The attempt chunks replayed from the CUDA graph (default) and enqueued kernel by kernel
+    (MPAX_SHARDED_GRAPH=0) are the same computation: identical results and kernel counts."""
+    lp = lpgen.g_rand(3000, 5000, 12, seed=3)
+
+    def run():
+        before = mp.launch_count()
+        with mp.ShardedSolver(mp.Problem.from_lp(lp), virtual_shards=2, axis=axis) as s:
+            r = s.solve(algorithm="r2", iteration_limit=300, eps_abs=0.0, eps_rel=0.0)
+            x, y, _ = s.solution()
+        return r, x, y, mp.launch_count() - before
+
+    a = run()
+    monkeypatch.setenv("MPAX_SHARDED_GRAPH", "0")
+    b = run()
+    assert a[0]["attempts"] == b[0]["attempts"] and a[0]["restarts"] == b[0]["restarts"]
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    assert a[3] == b[3]
+
+
+# ---- exchange variant B of the row engine (reduce-scatter + all-gather; SURVEY §8(e)) ----
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("K", [1, 64])
+@pytest.mark.parametrize("shards", [1, 2, 3])
+@pytest.mark.parametrize("name,lp", CASES)
+def test_variant_b_fixed_K(alg, K, shards, name, lp):
+    if shards > lp.m:
+        pytest.skip("more shards than rows")
+    ro, stable, drift = oracle_stability(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=K)
+    rb = sharded(lp, alg, shards, eps_abs=0.0, eps_rel=0.0, iteration_limit=K, sharded_exchange=1)
+    ra = sharded(lp, alg, shards, eps_abs=0.0, eps_rel=0.0, iteration_limit=K)
+    if not stable:
+        pytest.skip("ill-conditioned at this K: the oracle's own counts move under a 1-ulp perturbation")
+    tol = max(1e-9, 100 * drift)
+    for key in ("status", "iterations", "attempts", "restarts"):
+        assert rb[key] == ro[key] == ra[key], (key, rb[key], ro[key], ra[key])
+    for v in ("x", "y", "lam"):
+        if v == "y" and not lp.m:
+            continue
+        assert rel(rb[v], ro[v]) <= (tol if v != "lam" else max(1e-8, 1e3 * drift))
+        assert rel(rb[v], ra[v]) <= max(1e-10, 100 * drift)   # A, B differ in the order of the column sums
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_variant_b_full_solve_and_polish(alg):
+    lp = lpgen.g_rand(3000, 5000, 12, seed=3)
+    rb = sharded(lp, alg, 3, sharded_exchange=1)
+    assert rb["status"] == mp.LP_OPTIMAL and rb["rel_kkt"] <= 1e-4
+    k = oracle.kkt_original(lp, rb["x"], rb["y"])
+    assert k["pres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.q))
+    assert k["dres"] <= (1 + 1e-6) * (1e-4 + 1e-4 * np.linalg.norm(lp.c))
+    assert abs(rb["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
+    small = lpgen.g_rand(50, 100, 10, seed=1)
+    rp = sharded(small, alg, 2, eps_abs=1e-2, eps_rel=1e-2, feasibility_polishing=1, sharded_exchange=1)
+    assert rp["status"] == mp.LP_OPTIMAL and rp["polish"] == 1
+    k = oracle.kkt_original(small, rp["x"], rp["y"])
+    assert k["pres"] <= (1 + 1e-9) * 1e-6 * (1 + np.linalg.norm(small.q))
+    assert k["dres"] <= (1 + 1e-9) * 1e-6 * (1 + np.linalg.norm(small.c))
+    assert rp["primal_objective"] == pytest.approx(float(small.c @ rp["x"]), rel=1e-12)

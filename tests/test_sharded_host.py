@@ -63,3 +63,49 @@ def test_two_rank_row_sharding_gloo():
     assert res[0][0] and res[1][0], res
     assert res[0][1] == res[1][1] == 128
     assert res[0][2] + res[1][2] == 301
+
+
+def _worker_cols(rank, world, port, out):
+    """Column sharding (m < n, reading 33): each rank's K_{:,g} x_g partial, summed over the ranks,
+    is K x; with y replicated, each rank's K_g' y is its columns of K' y; the exchanged vector
+    is the m-long one."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2412_09734_b200 as mp
+        lp = lpgen.g_rand(211, 640, 9, seed=13)
+        prob = mp.Problem.from_lp(lp)
+        ok = mp.shard_axis(lp.m, lp.n) == mp.SHARD_COLS and mp.shard_axis(lp.n, lp.m) == mp.SHARD_ROWS
+        ok &= mp.shard_axis(lp.n, lp.n) == mp.SHARD_ROWS
+        cuts = mp.col_partition(prob, world)
+        c0, c1 = cuts[rank], cuts[rank + 1]
+        loc = mp.local_cols(prob, c0, c1)
+        rng = np.random.default_rng(4)
+        x, y = rng.normal(size=lp.n), rng.normal(size=lp.m)
+        Kl = lpgen.LP(loc.n, loc.m1, loc.m2, np.asarray(loc.row_ptr), np.asarray(loc.col_idx),
+                      np.asarray(loc.values), np.asarray(loc.c), lp.q, np.asarray(loc.l), np.asarray(loc.u)).dense_K()
+        K = lp.dense_K()
+        part = torch.from_numpy(Kl @ x[c0:c1])            # this rank's K_{:,g} x_g (m-long)
+        dist.all_reduce(part, op=dist.ReduceOp.SUM)
+        ok &= bool(np.allclose(part.numpy(), K @ x, rtol=1e-12, atol=1e-12))
+        ok &= bool(np.allclose(Kl.T @ y, (K.T @ y)[c0:c1], rtol=1e-13, atol=1e-13))
+        ok &= bool(np.array_equal(Kl, K[:, c0:c1])) and loc.m1 == lp.m1 and loc.m2 == lp.m2
+        ok &= bool(np.array_equal(np.asarray(loc.c), lp.c[c0:c1])) and bool(np.array_equal(np.asarray(loc.q), lp.q))
+        nnz = torch.tensor([int(np.asarray(loc.row_ptr)[-1])])
+        dist.all_reduce(nnz)
+        ok &= int(nnz) == lp.nnz
+        out[rank] = (ok, c1 - c0, int(np.asarray(loc.row_ptr)[-1]), part.numel())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_column_sharding_gloo():
+    port = _free_port()
+    with tmp.Manager() as mgr:
+        out = mgr.dict()
+        tmp.spawn(_worker_cols, args=(2, port, out), nprocs=2, join=True)
+        res = dict(out)
+    assert res[0][0] and res[1][0], res
+    assert res[0][1] + res[1][1] == 640
+    assert abs(res[0][2] - res[1][2]) <= 0.1 * (res[0][2] + res[1][2])   # nnz-balanced
+    assert res[0][3] == 211                                             # the exchange is m-long
