@@ -1162,8 +1162,12 @@ int grid_launch(const DevProblem &D, const lp_options &o, const GridLaunch &L, c
   const size_t ntpA = 2 * (size_t)((n + 31) / 32) + 1;   // + the counter (the lean sweep writes 2 per tile)
   // fp64 block: per-CTA / per-tile partials, tmp (m), the counter; then the T block: 8n + 8m
   // iterate vectors (+ l~, u~ copies for fp32 storage)
-  const size_t dbl = (size_t)m + 2 * (size_t)blocks * kNP + ntp + ntpA;
-  const size_t tvec = (size_t)(8 * n + 8 * m) + (f32 ? 2 * (size_t)n : 0);
+  // every vector starts on a 256-byte boundary (a warp's 32 consecutive fp64 elements = 8 sectors;
+  // one element off and every warp access touches 9)
+  auto up = [](size_t v, size_t a) { return (v + a - 1) / a * a; };
+  const size_t dbl = up((size_t)m + 2 * (size_t)blocks * kNP + ntp + ntpA, 32);
+  const size_t ne = up((size_t)n, 256 / sizeof(T)), me = up((size_t)m, 256 / sizeof(T));
+  const size_t tvec = 8 * ne + 8 * me + (f32 ? 2 * ne : 0);
   const size_t need = dbl * sizeof(double) + tvec * sizeof(T);
   if (*work_bytes < need) {
     if (*work) MPAX_CUDA(cudaFreeAsync(*work, s));
@@ -1181,14 +1185,14 @@ int grid_launch(const DevProblem &D, const lp_options &o, const GridLaunch &L, c
   P.Dr = D.Dr; P.Dc = D.Dc; P.ls = D.ls; P.us = D.us; P.l0 = D.l0; P.u0 = D.u0;
   P.c0 = L.c0; P.q0 = L.q0; P.X0 = L.X0; P.Y0 = L.Y0; P.kmax = D.kmax; P.sigma = D.sigma; P.tab = D.tab;
   P.const_step = o.step_rule == LP_STEP_CONSTANT;
-  P.cs = wt; wt += n;
-  P.x = wt; wt += n; P.KTy = wt; wt += n; P.xp = wt; wt += n; P.KTyp = wt; wt += n; P.xa = wt; wt += n;
-  P.KTya = wt; wt += n; P.xr = wt; wt += n;
-  P.qs = wt; wt += m;
-  P.y = wt; wt += m; P.Kx = wt; wt += m; P.yp = wt; wt += m; P.Kxp = wt; wt += m; P.ya = wt; wt += m;
-  P.Kxa = wt; wt += m; P.yr = wt; wt += m;
+  P.cs = wt; wt += ne;
+  P.x = wt; wt += ne; P.KTy = wt; wt += ne; P.xp = wt; wt += ne; P.KTyp = wt; wt += ne; P.xa = wt; wt += ne;
+  P.KTya = wt; wt += ne; P.xr = wt; wt += ne;
+  P.qs = wt; wt += me;
+  P.y = wt; wt += me; P.Kx = wt; wt += me; P.yp = wt; wt += me; P.Kxp = wt; wt += me; P.ya = wt; wt += me;
+  P.Kxa = wt; wt += me; P.yr = wt; wt += me;
   P.lsw = nullptr; P.usw = nullptr;
-  if constexpr (f32) { P.lsw = wt; wt += n; P.usw = wt; wt += n; }
+  if constexpr (f32) { P.lsw = wt; wt += ne; P.usw = wt; wt += ne; }
   P.part = w; w += 2 * (size_t)blocks * kNP;
   P.tpart = w; w += ntp;
   P.tmp = w; w += m;

@@ -603,6 +603,13 @@ int upload_table(ShardedLP &E, int slot, double *const *bufs_host) {
   std::vector<double *> want(bufs_host, bufs_host + E.sh.size());
   if (E.tab_cache.size() <= (size_t)slot) E.tab_cache.resize(slot + 1);
   if (E.tab_cache[slot] != want) {
+    // never inside a graph capture: the copy would be recorded from this temporary host array
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    MPAX_CUDA(cudaStreamIsCapturing(E.s, &cap));
+    if (cap != cudaStreamCaptureStatusNone) {
+      set_error_detail("sharded pointer table uploaded during a graph capture");
+      return LP_ERR_UNSUPPORTED;
+    }
     MPAX_CUDA(cudaMemcpyAsync(tab, bufs_host, E.sh.size() * sizeof(double *), cudaMemcpyHostToDevice, E.s));
     E.tab_cache[slot] = want;
   }
@@ -766,23 +773,22 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
     // vectors
     double *vec = nullptr;
     S.nb = 148 * 8;
-    const size_t nv = 9 * (size_t)(n + 64) + 8 * (size_t)(m > 0 ? m : 1) + (size_t)S.nb * kV + 3 * (size_t)(n + 64) +
-                      2 * (size_t)(m > 0 ? m : 1);
+    // n-vectors padded by 64 (variant B slices of ceil(n / p) columns, p <= 64; pads stay zero) and
+    // every vector on a 256-byte boundary
+    const int64_t na = (n + 64 + 31) / 32 * 32, ma = ((m > 0 ? m : 1) + 31) / 32 * 32;
+    const size_t nv = 12 * (size_t)na + 10 * (size_t)ma + (size_t)S.nb * kV;
     MPAX_CUDA(cudaMallocAsync((void **)&vec, nv * sizeof(double), s));
     MPAX_CUDA(cudaMemsetAsync(vec, 0, nv * sizeof(double), s));
     S.vecs = vec;
     Vecs &V = S.V;
     double *w = vec;
-    // n-vectors padded by 64 (variant B slices of ceil(n / p) columns, p <= 64; pads stay zero)
-    const int64_t na = n + 64;
     V.x = w; w += na; V.KTy = w; w += na; V.xp = w; w += na; V.KTyp = w; w += na; V.xa = w; w += na;
     V.KTya = w; w += na; V.xr = w; w += na; V.cs = w; w += na; V.red = w; w += na;
-    const int64_t mm = m > 0 ? m : 1;
-    V.y = w; w += mm; V.Kx = w; w += mm; V.yp = w; w += mm; V.Kxp = w; w += mm; V.ya = w; w += mm;
-    V.Kxa = w; w += mm; V.yr = w; w += mm; V.qs = w; w += mm;
+    V.y = w; w += ma; V.Kx = w; w += ma; V.yp = w; w += ma; V.Kxp = w; w += ma; V.ya = w; w += ma;
+    V.Kxa = w; w += ma; V.yr = w; w += ma; V.qs = w; w += ma;
+    S.X = w; w += na; S.L = w; w += na; w += na; S.Y = w; w += ma;
+    V.tmp = w; w += ma;
     V.part = w; w += (size_t)S.nb * kV;
-    S.X = w; w += na; S.L = w; w += na; w += na; S.Y = w; w += mm;
-    V.tmp = w; w += mm;
     V.c0 = c0; V.q0 = q0;
     S.c0 = c0; S.q0 = q0;
     V.pre = E.cols ? V.tmp : nullptr;
@@ -981,6 +987,11 @@ int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const dou
     MPAX_CHECK_LAUNCH();
     return LP_OK;
   };
+  if (E.vb && E.virt) {   // the x' all-gather's pointer table, before any capture of the attempt loop
+    std::vector<double *> b;
+    for (auto &S : E.sh) b.push_back(S.V.xp);
+    STRY(table_for(E, 12, b));
+  }
   // A chunk of F attempts that starts at a check boundary is replayed from a CUDA graph captured
   // once per solve (every kernel argument and collective buffer is fixed within a solve; the
   // virtual pointer tables were uploaded by step 2): one launch per F attempts instead of
