@@ -116,7 +116,10 @@ template <typename V, typename X>
 __device__ __forceinline__ double row_dot(int64_t r, bool valid, int rows, int G, int gl,
                                           const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                                           const V *__restrict__ v, const X *x, double *tbuf, bool lr = true) {
-  if (G == 1) return tile_row_dot((int)r, valid, rows, rp, ci, v, x, tbuf, lr);
+  // (the kernel body's own tile sweeps -- step 2, the checks, the experimental drivers -- keep the
+  // serial per-lane sum: the full-chunk warp sum inlined here costs the whole kernel's register
+  // allocation 7% at C4; the hot sweeps of long-row matrices run in phase_tiles<.., LR = true>)
+  if (G == 1) return tile_row_dot<V, X, false>((int)r, valid, rows, rp, ci, v, x, tbuf, lr);
   double s0 = 0.0, s1 = 0.0;
   if (valid) {
     const int32_t e = __ldg(rp + r + 1);
@@ -227,14 +230,13 @@ struct PhaseCtx {
   const T *r0, *r1, *r2, *r3, *r4;
   double tau_sigma, theta, ha, hb, rf1, rf0;
   int rows, m1;
-  int lr;                         // the swept matrix has long rows (tile_row_dot)
   double *tpart;                  // per-tile partials (2 per tile)
   int t0, kmax;                   // this CTA's tile range [t0, t0 + kmax) (contiguous slots)
   unsigned long long *gctr;       // non-null: claim tiles from this global counter (all CTAs)
   unsigned long long gbase;       //   counter value at the phase's start; tiles [0, kmax)
 };
 
-template <int MODE, typename T>
+template <int MODE, typename T, bool LR>
 __device__ __noinline__ void phase_tiles(const volatile PhaseCtx<T> *cx, int *s_ctr, double *tbuf) {
   const int lane = threadIdx.x & 31;
   const int rows = cx->rows, t0 = cx->t0, kmax = cx->kmax;
@@ -249,13 +251,13 @@ __device__ __noinline__ void phase_tiles(const volatile PhaseCtx<T> *cx, int *s_
     const bool ok = r < rows;
     double c0 = 0.0, c1 = 0.0;
     if (MODE == kB_PARK) {
-      const double sl = tile_row_dot(r, ok, rows, (const int32_t *)cx->rp, (const int32_t *)cx->ci,
-                                     (const T *)cx->kv, (const T *)cx->tgt, tbuf, cx->lr != 0);
+      const double sl = tile_row_dot<T, T, LR>(r, ok, rows, (const int32_t *)cx->rp, (const int32_t *)cx->ci,
+                                               (const T *)cx->kv, (const T *)cx->tgt, tbuf);
       if (ok) cx->park[r] = sl;
       continue;
     }
-    double s = tile_row_dot(r, ok, rows, (const int32_t *)cx->rp, (const int32_t *)cx->ci, (const T *)cx->kv,
-                            (const T *)cx->tgt, tbuf, cx->lr != 0);
+    double s = tile_row_dot<T, T, LR>(r, ok, rows, (const int32_t *)cx->rp, (const int32_t *)cx->ci,
+                                      (const T *)cx->kv, (const T *)cx->tgt, tbuf);
     if (ok) {
       if (MODE == kA_RA) {
         // r0 = xp, r1 = cs, r2 = ls, r3 = us; e0 = xa (rw), e1 = KTy' (w), e2 = the old x buffer (w: x')
@@ -588,7 +590,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
           lean_range(n);
           s_cx.gctr = nullptr;
           if (glob) { s_cx.gctr = P.gctr; s_cx.gbase = gbase; s_cx.t0 = 0; s_cx.kmax = (n + 31) >> 5; s_cx.tpart = P.tpartA; }
-          s_cx.rp = P.trp; s_cx.ci = P.tci; s_cx.kv = P.tkv; s_cx.tgt = yp; s_cx.add = nullptr; s_cx.lr = P.lrA;
+          s_cx.rp = P.trp; s_cx.ci = P.tci; s_cx.kv = P.tkv; s_cx.tgt = yp; s_cx.add = nullptr;
           s_cx.r0 = xp; s_cx.r1 = cs; s_cx.r2 = lsT; s_cx.r3 = usT; s_cx.r4 = KTya;
           s_cx.e0 = xa;
           if (!r2) { s_cx.e1 = KTyp; s_cx.e2 = x; }
@@ -596,8 +598,8 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
           s_cx.tau_sigma = tau; s_cx.theta = theta; s_cx.ha = ha; s_cx.hb = hb; s_cx.rf1 = rf1; s_cx.rf0 = rf0;
         }
         __syncthreads();
-        if (!r2) phase_tiles<kA_RA, T>(&s_cx, &s_ctr, tbuf);
-        else phase_tiles<kA_R2, T>(&s_cx, &s_ctr, tbuf);
+        if (!r2) { if (P.lrA) phase_tiles<kA_RA, T, true>(&s_cx, &s_ctr, tbuf); else phase_tiles<kA_RA, T, false>(&s_cx, &s_ctr, tbuf); }
+        else { if (P.lrA) phase_tiles<kA_R2, T, true>(&s_cx, &s_ctr, tbuf); else phase_tiles<kA_R2, T, false>(&s_cx, &s_ctr, tbuf); }
         __syncthreads();
         if (glob) {
           // every warp made exactly one failing claim: the phase consumed tiles + warps values;
@@ -708,10 +710,11 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
           if (threadIdx.x == 0) {
             lean_range(m);
             s_cx.gctr = nullptr;
-            s_cx.rp = P.rpL; s_cx.ci = P.ciL; s_cx.kv = P.kvL; s_cx.tgt = xp; s_cx.park = P.tmp; s_cx.lr = P.lrB;
+            s_cx.rp = P.rpL; s_cx.ci = P.ciL; s_cx.kv = P.kvL; s_cx.tgt = xp; s_cx.park = P.tmp;
           }
           __syncthreads();
-          phase_tiles<kB_PARK, T>(&s_cx, &s_ctr, tbuf);
+          if (P.lrB) phase_tiles<kB_PARK, T, true>(&s_cx, &s_ctr, tbuf);
+          else phase_tiles<kB_PARK, T, false>(&s_cx, &s_ctr, tbuf);
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -719,16 +722,22 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
           s_cx.gctr = nullptr;
           if (P.split) { s_cx.rp = P.rpR; s_cx.ci = P.ciR; s_cx.kv = P.kvR; s_cx.add = P.tmp; }
           else { s_cx.rp = P.rp; s_cx.ci = P.ci; s_cx.kv = P.kv; s_cx.add = nullptr; }
-          s_cx.tgt = xp; s_cx.m1 = m1; s_cx.r0 = qs; s_cx.lr = P.lrB;
+          s_cx.tgt = xp; s_cx.m1 = m1; s_cx.r0 = qs;
           s_cx.tau_sigma = sigma; s_cx.theta = theta; s_cx.ha = ha; s_cx.hb = hb; s_cx.rf1 = rf1; s_cx.rf0 = rf0;
           if (pending && !r2) { s_cx.r1 = yp; s_cx.r2 = Kxp; s_cx.e0 = ya; s_cx.e1 = y; s_cx.e2 = Kx; }
           else if (pending) { s_cx.r1 = yp; s_cx.r2 = Kxp; s_cx.r3 = ya; s_cx.r4 = Kxa; s_cx.e0 = y; s_cx.e1 = Kx; s_cx.e2 = yp; s_cx.e3 = Kxp; }
           else { s_cx.r1 = y; s_cx.r2 = Kx; s_cx.e2 = yp; s_cx.e3 = Kxp; }
         }
         __syncthreads();
-        if (pending && !r2) phase_tiles<kB_RA, T>(&s_cx, &s_ctr, tbuf);
-        else if (pending) phase_tiles<kB_R2, T>(&s_cx, &s_ctr, tbuf);
-        else phase_tiles<kB_NOP, T>(&s_cx, &s_ctr, tbuf);
+        if (P.lrB) {
+          if (pending && !r2) phase_tiles<kB_RA, T, true>(&s_cx, &s_ctr, tbuf);
+          else if (pending) phase_tiles<kB_R2, T, true>(&s_cx, &s_ctr, tbuf);
+          else phase_tiles<kB_NOP, T, true>(&s_cx, &s_ctr, tbuf);
+        } else {
+          if (pending && !r2) phase_tiles<kB_RA, T, false>(&s_cx, &s_ctr, tbuf);
+          else if (pending) phase_tiles<kB_R2, T, false>(&s_cx, &s_ctr, tbuf);
+          else phase_tiles<kB_NOP, T, false>(&s_cx, &s_ctr, tbuf);
+        }
         __syncthreads();
         double t2[2];
         lean_reduce(t2);
@@ -740,7 +749,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
           // x' only, L2-resident); pass 2: K~_R x' + tmp and the row epilogue
           double none[1];
           tiles_dynamic(m, [&](int i, bool ok, double (&c)[1]) {
-            const double sl = tile_row_dot(i, ok, m, P.rpL, P.ciL, P.kvL, xp, tbuf, P.lrB);
+            const double sl = tile_row_dot<T, T, false>(i, ok, m, P.rpL, P.ciL, P.kvL, xp, tbuf);
             if (ok) P.tmp[i] = sl;
             c[0] = 0.0;
           }, none, false);

@@ -10,8 +10,11 @@ import lpgen  # noqa: E402
 import paper_2412_09734_b200 as mp  # noqa: E402
 
 m = int(os.environ.get("SK_M", "100000"))
+ONLY = os.environ.get("SK_ONLY")
 for name, lp in (("uniform", lpgen.g_rand(m, 2 * m, 20, seed=4)),
                  ("powerlaw", lpgen.g_powerlaw(m, 2 * m, 20, seed=9))):
+    if ONLY and name != ONLY:
+        continue
     lens = np.diff(lp.row_ptr)
     with mp.Solver(mp.Problem.from_lp(lp)) as s:
         s.solve(algorithm="ra", path=mp.PATH_GRID, iteration_limit=64, eps_abs=0.0, eps_rel=0.0)
