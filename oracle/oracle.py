@@ -173,7 +173,7 @@ def lib32():
             L = C.CDLL(build(f32=True))
             P = C.POINTER
             L.ora_solve.argtypes = [P(Problem), P(Options32), C.c_void_p, C.c_void_p, C.c_void_p,
-                                    C.c_void_p, C.c_void_p, P(Result32), C.c_void_p]
+                                    C.c_void_p, C.c_void_p, P(Result32), P(Log)]
             L.ora_solve_batch.argtypes = [P(Problem), C.c_int64, C.c_void_p, C.c_void_p, P(Options32),
                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, P(Result32)]
             L.ora_default_options.argtypes = [P(Options32)]
@@ -241,7 +241,7 @@ def solve(lp, algorithm="r2", eps_abs=1e-4, eps_rel=1e-4, iteration_limit=None, 
     if precision == "fp32":
         return _solve32(lp, algorithm, eps_abs, eps_rel, iteration_limit, x0, y0, check_frequency, step_rule,
                         eps_primal_infeasible, eps_dual_infeasible, feasibility_polishing, eps_feas_polish,
-                        reflection, ruiz_iters, pock_chambolle)
+                        reflection, ruiz_iters, pock_chambolle, log_capacity)
     b = _Bound(lp)
     m = lp.m1 + lp.m2
     o = options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule,
@@ -278,7 +278,7 @@ def _options32(o):
 
 def _solve32(lp, algorithm, eps_abs, eps_rel, iteration_limit, x0, y0, check_frequency, step_rule,
              eps_primal_infeasible, eps_dual_infeasible, feasibility_polishing, eps_feas_polish, reflection,
-             ruiz_iters, pock_chambolle):
+             ruiz_iters, pock_chambolle, log_capacity=0):
     b = _Bound(lp, np.float32)
     m = lp.m1 + lp.m2
     o = _options32(options(algorithm, eps_abs, eps_rel, iteration_limit, check_frequency, step_rule=step_rule,
@@ -289,12 +289,21 @@ def _solve32(lp, algorithm, eps_abs, eps_rel, iteration_limit, x0, y0, check_fre
     x0a = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float32)
     y0a = None if y0 is None else np.ascontiguousarray(y0, dtype=np.float32)
     r = Result32()
+    g = None
+    if log_capacity:   # the decision logs, in the build's precision (float32 records)
+        att = np.zeros((log_capacity, 4), np.float32)
+        chk = np.zeros((log_capacity, 6), np.float32)
+        g = Log(log_capacity, 0, att.ctypes.data, log_capacity, 0, chk.ctypes.data)
     e = lib32().ora_solve(C.byref(b.s), C.byref(o), _ptr(x0a), _ptr(y0a), x.ctypes.data,
-                          y.ctypes.data if m else None, lam.ctypes.data, C.byref(r), None)
+                          y.ctypes.data if m else None, lam.ctypes.data, C.byref(r),
+                          C.byref(g) if g is not None else None)
     if e != 0:
         raise ValueError(f"oracle error {e}")
     out = r.as_dict()
     out.update(x=x.astype(np.float64), y=y[:m].astype(np.float64), lam=lam.astype(np.float64))
+    if g is not None:
+        out["att_log"] = att[: g.att_len].astype(np.float64)
+        out["chk_log"] = chk[: g.chk_len].astype(np.float64)
     return out
 
 
