@@ -94,7 +94,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("BENCH_CLOCK_MS", "50")], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -249,16 +249,20 @@ def run_ours(args):
 
     def timed(prob, Cx, X, Y, mem, steps, collect, alg=args.alg, rule="adaptive", rho=1.0, opts=None):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-        all_res = []
+        # per step, after its end event: every instance's status and the library's solve time;
+        # the last step's full results (no step's result array is retained past the next step)
+        summary = {"all_optimal": True, "solve_s": [], "last": None}
         for s in range(steps):
             flush.zero_()                       # evict L2 between steps (outside the event pair)
             ev[s][0].record(stream)
             res = step(prob, Cx, X, Y, mem, alg, rule, rho, opts)
             ev[s][1].record(stream)
             if collect:
-                all_res.append(res)
+                summary["all_optimal"] &= bool(np.all(res["status"] == mp.LP_OPTIMAL))
+                summary["solve_s"].append(float(res["solve_seconds"][0]))
+                summary["last"] = res
         torch.cuda.synchronize()
-        return sum(a.elapsed_time(b) for a, b in ev), all_res
+        return sum(a.elapsed_time(b) for a, b in ev), summary
 
     def barrier():
         torch.cuda.synchronize()
@@ -317,36 +321,35 @@ def run_ours(args):
     var_ms = {v[0]: float(t[3 + i]) for i, v in enumerate(VARIANTS)}
     variants = {}
     for name, va, rule, rho, opts in VARIANTS:
-        itv = np.array([r["iterations"] for r in var_res[name][-1]])
+        itv = np.asarray(var_res[name]["last"]["iterations"])
         variants[name] = {
             "algorithm": "r2hpdhg" if va == "r2" else "rapdhg", "step_rule": rule, "reflection": rho,
             "value": args.batch * args.secondary_steps * ws / (var_ms[name] * 1e-3), "unit": UNIT,
             "ms_per_step": var_ms[name] / args.secondary_steps,
-            "all_optimal": all(r["status"] == mp.LP_OPTIMAL for res in var_res[name] for r in res),
+            "all_optimal": var_res[name]["all_optimal"],
             "iterations": {"p50": float(np.median(itv)), "p99": float(np.percentile(itv, 99)), "max": int(itv.max())}}
         if rule == "constant":
             variants[name]["step"] = "eta = 0.998 / sigma_max(K~), 200 power iterations (inside the timed step)"
         if opts is POLISH:
-            variants[name]["polished"] = int(sum(r["polish"] == 1 for r in var_res[name][-1]))
+            variants[name]["polished"] = int(np.sum(var_res[name]["last"]["polish"] == 1))
             variants[name]["polish"] = ("after the 1e-4 solve, primal (c = 0) and dual (q = 0) sub-solves to "
                                         "eps_feas_polish = 1e-6 on the same kernel (inside the timed step)")
-    it2 = np.array([r["iterations"] for r in res2[-1]])
+    it2 = np.asarray(res2["last"]["iterations"])
     secondary = {"algorithm": "r2hpdhg" if alg2 == "r2" else "rapdhg",
                  "value": args.batch * args.secondary_steps * ws / (ms2 * 1e-3), "unit": UNIT,
                  "ms_per_step": ms2 / args.secondary_steps,
-                 "all_optimal": all(r["status"] == mp.LP_OPTIMAL for res in res2 for r in res),
+                 "all_optimal": res2["all_optimal"],
                  "iterations": {"p50": float(np.median(it2)), "p99": float(np.percentile(it2, 99)),
                                 "max": int(it2.max())}}
     # correctness of every timed instance
-    statuses = [r["status"] for res in results for r in res]
-    assert all(s == mp.LP_OPTIMAL for s in statuses), "non-optimal instance in the timed region"
+    assert results["all_optimal"], "non-optimal instance in the timed region"
     lps = args.batch * args.steps * ws
     value = lps / (ms * 1e-3)
     e2e = lps / (ms_e2e * 1e-3)
-    last = results[-1]
-    iters = np.array([r["iterations"] for r in last])
-    atts = np.array([r["attempts"] for r in last])
-    kern_ms = statistics.mean(res[0]["solve_seconds"] for res in results) * 1e3
+    last = results["last"]
+    iters = np.asarray(last["iterations"])
+    atts = np.asarray(last["attempts"])
+    kern_ms = statistics.mean(results["solve_s"]) * 1e3
     # roofline of the dominant kernel (the per-instance solver kernel): fp64 ALU bound
     nnz, n, m = lp.nnz, lp.n, lp.m
     flop_attempt = 4 * nnz + 25 * (n + m)          # SURVEY §8(d) d.2 per-attempt flops

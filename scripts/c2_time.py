@@ -36,12 +36,25 @@ st = torch.cuda.current_stream()
 # C2_FLUSH=1: evict L2 between steps (outside the event pair), as bench.py's timed region does
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev) if os.environ.get("C2_FLUSH") else None
 ts, ss = [], []
+# C2_NOSYNC=1: no host synchronisation between steps (bench.py's timed loop); C2_NOGC=1: Python's
+# cyclic garbage collector off during the loop
+if os.environ.get("C2_NOGC"):
+    import gc
+    gc.collect()
+    gc.disable()
+nosync = bool(os.environ.get("C2_NOSYNC"))
+evs = []
 for _ in range(int(os.environ.get("C2_REPS", 300))):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if flush is not None:
         flush.zero_()
-    a.record(st); r = step(); b.record(st); torch.cuda.synchronize()
-    ts.append(a.elapsed_time(b)); ss.append(float(r["solve_seconds"][0]) * 1e3)
+    a.record(st); r = step(); b.record(st)
+    if not nosync:
+        torch.cuda.synchronize()
+    evs.append((a, b)); ss.append(float(r["solve_seconds"][0]) * 1e3)
+torch.cuda.synchronize()
+ts = [a.elapsed_time(b) for a, b in evs]
+print(f"mean step {np.mean(ts):.4f} ms  p90 {np.percentile(ts, 90):.4f}  max {np.max(ts):.4f}", flush=True)
 att = int(r["attempts"].max())
 print(f"{os.path.basename(os.environ.get('MPAX_LIB', 'default')):12s} {'cold' if flush is not None else 'warm'} {alg} step {np.median(ts):.4f} ms (min {np.min(ts):.4f})  "
       f"solve {np.median(ss):.4f} ms  LPs/s {B / np.median(ts) * 1e3:.0f}  max it {r['iterations'].max()}  "
