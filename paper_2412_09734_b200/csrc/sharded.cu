@@ -541,8 +541,8 @@ __global__ void k_final(const ShState *st, lp_result *res) {
 }
 
 // fixed-order reduction over p same-device shard buffers (virtual mode)
-__global__ void k_vreduce(double *const *ptrs, int p, int64_t count, int op_max) {
-  for (int64_t t = blockIdx.x * (int64_t)kB + threadIdx.x; t < count; t += (int64_t)gridDim.x * kB) {
+__global__ void k_vreduce(double *const *ptrs, int p, int64_t off, int64_t count, int op_max) {
+  for (int64_t t = off + blockIdx.x * (int64_t)kB + threadIdx.x; t < off + count; t += (int64_t)gridDim.x * kB) {
     double a = ptrs[0][t];
     for (int s = 1; s < p; ++s) a = op_max ? fmax(a, ptrs[s][t]) : a + ptrs[s][t];
     for (int s = 0; s < p; ++s) ptrs[s][t] = a;
@@ -594,6 +594,12 @@ struct ShardedLP {
   bool cols = false;         // column-sharded (every m-long vector replicated) instead of row-sharded
   bool vb = false;           // this solve uses exchange variant B (row engine): n-side work on slices
   int64_t ns = 0;            // variant B: columns per slice, ceil(n / p) (p = shards or ranks)
+  // chunked overlap of the K~_g'y partials with their all-reduce (variant A): chunk c's reduction
+  // runs on the comm stream while the compute stream sums chunk c + 1
+  int chunks = 1;
+  cudaStream_t comm_s = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+  cudaEvent_t join_ev = nullptr;
 };
 
 namespace {
@@ -616,21 +622,23 @@ int upload_table(ShardedLP &E, int slot, double *const *bufs_host) {
   return LP_OK;
 }
 
-int reduce_across(ShardedLP &E, int slot, int64_t count, bool op_max, double *const *bufs_host) {
+int reduce_across(ShardedLP &E, int slot, int64_t count, bool op_max, double *const *bufs_host, int64_t off = 0,
+                  cudaStream_t st = nullptr) {
+  if (!st) st = E.s;
   if (E.virt) {
     if (E.sh.size() < 2) return LP_OK;
     double **tab = E.d_ptrs + slot * 64;
     // the table is uploaded only when its pointers change: the attempt loop then issues no host
     // copies, so it can be captured into a CUDA graph (sharded_solve)
     if (int r = upload_table(E, slot, bufs_host)) return r;
-    MPAX_LAUNCH(k_vreduce, blocks_for(count), kB, 0, E.s, tab, (int)E.sh.size(), count, op_max ? 1 : 0);
+    MPAX_LAUNCH(k_vreduce, blocks_for(count), kB, 0, st, tab, (int)E.sh.size(), off, count, op_max ? 1 : 0);
     MPAX_CHECK_LAUNCH();
     return LP_OK;
   }
   if (E.nranks <= 1) return LP_OK;
 #ifdef MPAX_HAVE_NCCL
-  ncclResult_t r = ncclAllReduce(bufs_host[0], bufs_host[0], (size_t)count, ncclDouble, op_max ? ncclMax : ncclSum,
-                                 (ncclComm_t)E.comm, E.s);
+  ncclResult_t r = ncclAllReduce(bufs_host[0] + off, bufs_host[0] + off, (size_t)count, ncclDouble,
+                                 op_max ? ncclMax : ncclSum, (ncclComm_t)E.comm, st);
   if (r != ncclSuccess) {
     set_error_detail(std::string("ncclAllReduce: ") + ncclGetErrorString(r));
     return LP_ERR_NCCL;
@@ -890,6 +898,32 @@ int launch_rows(ShardedLP &E, int mode) {
 }
 // K~_g' src_g into red (every shard), then the cross-shard sum
 int cols_spmv(ShardedLP &E, int which /*0: yp, 1: y, 2: ya*/) {
+  const int pp = E.virt ? (int)E.sh.size() : E.nranks;
+  if (E.chunks > 1 && !E.cols && !E.vb && pp > 1 && E.n >= 64 * E.chunks) {
+    // chunked: rows [c0, c1) of every K~_g' summed on the compute stream, then all-reduced on the
+    // comm stream while the next chunk is summed (same sums per element, in the same shard order)
+    std::vector<double *> bufs;
+    for (auto &S : E.sh) bufs.push_back(S.V.red);
+    STRY(upload_table(E, 0, bufs.data()));
+    const int64_t per = (E.n + E.chunks - 1) / E.chunks;
+    for (int c = 0; c < E.chunks; ++c) {
+      const int64_t c0 = c * per, c1 = std::min<int64_t>(E.n, c0 + per);
+      if (c0 >= c1) break;
+      for (auto &S : E.sh) {
+        const int G = group_of(S.P.avg_col, S.P.max_col);
+        const double *src = which == 0 ? S.V.yp : (which == 1 ? S.V.y : S.V.ya);
+        MPAX_LAUNCH(k_cols_spmv, blocks_for((c1 - c0) * G), kB, 0, E.s, S.st, c1 - c0, G, S.P.trp + c0, S.P.tci,
+                    S.P.tkv, src, S.V.red + c0);
+      }
+      MPAX_CHECK_LAUNCH();
+      MPAX_CUDA(cudaEventRecord(E.chunk_ev[c], E.s));
+      MPAX_CUDA(cudaStreamWaitEvent(E.comm_s, E.chunk_ev[c], 0));
+      STRY(reduce_across(E, 0, c1 - c0, false, bufs.data(), c0, E.comm_s));
+    }
+    MPAX_CUDA(cudaEventRecord(E.join_ev, E.comm_s));
+    MPAX_CUDA(cudaStreamWaitEvent(E.s, E.join_ev, 0));
+    return LP_OK;
+  }
   std::vector<double *> bufs;
   for (auto &S : E.sh) {
     const int G = group_of(S.P.avg_col, S.P.max_col);
@@ -1282,6 +1316,14 @@ ShardedLP *sharded_new(cudaStream_t s) {
       cudaEventCreate(&E->ev0) != cudaSuccess || cudaEventCreate(&E->ev1) != cudaSuccess) {
     return E;  // caller checks h_st
   }
+  // chunked exchange (variant A): MPAX_SHARDED_CHUNKS, default 4 chunks when ranks exchange
+  if (const char *e = getenv("MPAX_SHARDED_CHUNKS")) E->chunks = std::max(1, std::min(16, atoi(e)));
+  else E->chunks = -1;   // resolved at create: 4 with NCCL ranks, 1 otherwise
+  if (cudaStreamCreateWithFlags(&E->comm_s, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&E->join_ev, cudaEventDisableTiming) != cudaSuccess)
+    return E;
+  E->chunk_ev.resize(16);
+  for (auto &ev : E->chunk_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   return E;
 }
 
@@ -1301,6 +1343,9 @@ void sharded_free(ShardedLP *E) {
   if (E->h_flags) cudaFreeHost(E->h_flags);
   if (E->ev0) cudaEventDestroy(E->ev0);
   if (E->ev1) cudaEventDestroy(E->ev1);
+  for (auto ev : E->chunk_ev) if (ev) cudaEventDestroy(ev);
+  if (E->join_ev) cudaEventDestroy(E->join_ev);
+  if (E->comm_s) cudaStreamDestroy(E->comm_s);
   delete E;
 }
 
@@ -1352,6 +1397,7 @@ int sharded_create(ShardedLP *E, const std::vector<lp_problem_desc> &descs, cons
                    int64_t n, int64_t m1g, int64_t m2g, void *comm, int rank, int nranks, bool virt, bool cols) {
   E->n = n; E->m1_global = m1g; E->m_global = m1g + m2g;
   E->comm = comm; E->rank = rank; E->nranks = nranks; E->virt = virt; E->cols = cols;
+  if (E->chunks < 0) E->chunks = (!virt && nranks > 1) ? 4 : 1;
   if (!E->h_st || !E->d_res) return LP_ERR_OUT_OF_MEMORY;
   return sharded_setup(*E, descs, offsets);
 }

@@ -253,3 +253,17 @@ def test_variant_b_full_solve_and_polish(alg):
     assert k["pres"] <= (1 + 1e-9) * 1e-6 * (1 + np.linalg.norm(small.q))
     assert k["dres"] <= (1 + 1e-9) * 1e-6 * (1 + np.linalg.norm(small.c))
     assert rp["primal_objective"] == pytest.approx(float(small.c @ rp["x"]), rel=1e-12)
+
+
+@pytest.mark.parametrize("shards", [2, 3])
+def test_chunked_exchange_matches_unchunked(shards, monkeypatch):
+    """Variant A with the K~_g'y partials summed and all-reduced chunk by chunk on a second stream
+    (MPAX_SHARDED_CHUNKS): every element is the same sum in the same shard order, so the solve is
+    bitwise the unchunked one (graph replay included)."""
+    lp = lpgen.g_rand(3000, 5000, 12, seed=3)
+    monkeypatch.setenv("MPAX_SHARDED_CHUNKS", "1")
+    a = sharded(lp, "r2", shards, iteration_limit=300, eps_abs=0.0, eps_rel=0.0)
+    monkeypatch.setenv("MPAX_SHARDED_CHUNKS", "4")
+    b = sharded(lp, "r2", shards, iteration_limit=300, eps_abs=0.0, eps_rel=0.0)
+    assert a["attempts"] == b["attempts"] and a["restarts"] == b["restarts"]
+    assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["y"], b["y"])
