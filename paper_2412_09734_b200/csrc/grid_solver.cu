@@ -1226,8 +1226,10 @@ int grid_launch(const DevProblem &D, const lp_options &o, const GridLaunch &L, c
   // tile chunks are a serial latency chain and G lanes per column are faster (C4 phase A
   // 21 -> 17 us per attempt, trace build); phase B's dynamic tile driver wins at any size
   if (P.gkt == 1 && (n + 31) / 32 < 4 * (int64_t)blocks * (kBS / 32)) P.gkt = std::max(2, pow2_floor(D.avg_col / 4.0));
-  if (const char *e = getenv("MPAX_GRID_G")) P.gk = atoi(e);     // tuning experiments only
-  if (const char *e = getenv("MPAX_GRID_GT")) P.gkt = atoi(e);
+  // tuning experiments only; anything but a power of two in [1, 32] is ignored
+  auto gsize = [](const char *e, int d) { const int v = atoi(e); return (v >= 1 && v <= 32 && !(v & (v - 1))) ? v : d; };
+  if (const char *e = getenv("MPAX_GRID_G")) P.gk = gsize(e, P.gk);
+  if (const char *e = getenv("MPAX_GRID_GT")) P.gkt = gsize(e, P.gkt);
   P.vpol = 0;
   if (const char *e = getenv("MPAX_GRID_VPOL")) P.vpol = atoi(e);
   P.tdist = 0;

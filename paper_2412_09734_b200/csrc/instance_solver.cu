@@ -677,7 +677,10 @@ int instance_solve(const DevProblem &D, const lp_options &o, const InstanceLaunc
       const int64_t want = (std::max(D.n, D.m) + 4 * 32 - 1) / (4 * 32);
       while (NW < 32 && NW < want) NW *= 2;
     }
-    if (const char *e = getenv("MPAX_INST_NW")) NW = atoi(e);
+    if (const char *e = getenv("MPAX_INST_NW")) {   // experiments; anything but a CTA size is ignored
+      const int v = atoi(e);
+      if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) NW = v;
+    }
     if (NW == 2) NW = 4;              // the instantiated CTA sizes: 1, 4, 8, 16, 32 warps
     if (NW > 16 && NW != 32) NW = 32;
   }
