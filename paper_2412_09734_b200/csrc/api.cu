@@ -52,6 +52,7 @@ struct lp_handle_s {
   // decision log of the grid path (lp_set_decision_log): device-visible buffers, or null
   double *alog = nullptr, *clog = nullptr;
   int64_t acap = 0, ccap = 0;
+  int64_t log_inst = 0;   // the batch instance the register kernel logs
 };
 
 namespace {
@@ -548,8 +549,9 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
   if (o->path == LP_PATH_GRID && B != 1) return fail(LP_ERR_UNSUPPORTED, "the grid path solves one LP");
   if (o->precision == LP_FP32 && !use_grid)
     return fail(LP_ERR_UNSUPPORTED, "fp32 storage is a grid-path option (one large LP; DESIGN.md reading 39)");
-  if ((h->alog || h->clog) && !use_grid)
-    return fail(LP_ERR_UNSUPPORTED, "the decision log is recorded by the grid path only");
+  const bool want_log = h->alog || h->clog;
+  if (want_log && !use_grid && o->path != LP_PATH_AUTO)
+    return fail(LP_ERR_UNSUPPORTED, "the decision log is recorded by the grid path and the register kernel only");
   // a batch sharing a dense K: fp64 tensor-core path (auto from 8 instances on)
   const bool dmma = !use_grid && h->P.dense && (o->path == LP_PATH_DMMA || (o->path == LP_PATH_AUTO && B >= 8));
   if (dmma) {
@@ -585,6 +587,8 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
     if (rc == LP_ERR_UNSUPPORTED && oo.path == LP_PATH_AUTO) {
       rc = tiny_solve(h->P, oo, L, s, h->queue, &h->qbase);
       if (rc == LP_OK && L.res_host) host_written = true;
+      if (rc == LP_ERR_UNSUPPORTED && (L.alog || L.clog))
+        return fail(rc, "the register kernel logs decisions for the C2 shapes only");
     }
     if (rc == LP_ERR_UNSUPPORTED) {
       rc = instance_solve(h->P, oo, L, s, h->queue, &h->work, &h->work_bytes);
@@ -601,6 +605,10 @@ int run_solve(lp_handle h, const lp_options *o, const double *X0, const double *
   // the main solve's results straight into the pinned host buffer (device-mapped through UVA) when
   // they are final: no polishing pass rewrites them afterwards
   L.res_host = o->feasibility_polishing ? nullptr : h->h_res;
+  if (want_log && !use_grid) {   // the register kernel's one-instance log (main solve only)
+    if (dmma) return fail(LP_ERR_UNSUPPORTED, "the DMMA path does not log decisions");
+    L.alog = h->alog; L.clog = h->clog; L.acap = h->acap; L.ccap = h->ccap; L.log_inst = h->log_inst;
+  }
   TRY(dispatch(*o, L));
   if (o->feasibility_polishing) {
     // (reading 36) primal polish: c = 0 from (x*, 0); dual polish: q = 0 from (proj 0, y*);
@@ -813,9 +821,16 @@ int lp_get_shape(lp_handle h, int64_t *n, int64_t *m1, int64_t *m2, int64_t *bat
   return LP_OK;
 }
 
+int lp_set_decision_log_instance(lp_handle h, int64_t instance) {
+  if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
+  if (instance < 0 || instance >= h->batch) return fail(LP_ERR_BATCH_SHAPE, "instance out of range");
+  h->log_inst = instance;
+  return LP_OK;
+}
+
 int lp_set_decision_log(lp_handle h, double *att, int64_t att_cap, double *chk, int64_t chk_cap) {
   if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
-  if (h->sharded || h->is_batch) return fail(LP_ERR_UNSUPPORTED, "the decision log is recorded by the grid path only");
+  if (h->sharded) return fail(LP_ERR_UNSUPPORTED, "the decision log is not recorded by the sharded engine");
   if ((att && att_cap < 0) || (chk && chk_cap < 0)) return fail(LP_ERR_INVALID_ARGUMENT, "negative capacity");
   h->alog = att_cap > 0 ? att : nullptr;
   h->acap = att_cap > 0 ? att_cap : 0;

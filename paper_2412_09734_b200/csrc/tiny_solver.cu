@@ -32,6 +32,10 @@ struct TinyParams {
   unsigned long long *queue, qbase;
   double *X, *Y, *L;
   lp_result *res, *res_host;
+  // decision log of instance log_inst (LG instantiations only): per attempt (j, accepted, eta,
+  // eta_bar), per check (k, metric, ref, last, restart, outcome) -- the oracle's ora_log records
+  double *alog, *clog;
+  int64_t acap, ccap, log_inst;
 };
 
 // Barrier of the instance's threads: the warp, or the CTA.
@@ -93,7 +97,7 @@ __device__ __forceinline__ void ired(double (&v)[V], double *red, int &rb) {
 // CS: constant step rule (eta = 0.998 / sigma_max(K~), every attempt accepted; DESIGN.md
 // reading 34) -- the line-search reductions are then needed only where r2HPDHG uses
 // r_P (restart reference at k_in = 0 and the check), and never for raPDHG.
-template <bool R2, bool CS, int NT, int RPT, int CPT, int W, int WT>
+template <bool R2, bool CS, int NT, int RPT, int CPT, int W, int WT, bool LG = false>
 __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x;   // the thread's index within its instance (0 .. NT-1)
@@ -233,6 +237,14 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
     const double *ftab = P.tab + 2 * 2;  // the table entry of attempt jatt + 2 (loop-carried pointer)
     double W_ = 0.0, last = INFINITY, theta = 0.0, ha = 0.0, hb = 0.0;
     int status = 0, rejects = 0;
+    int64_t nchk = 0;   // checks logged (LG)
+    auto log_check = [&](double metric_, int restart_, int outcome) {
+      if (LG && b == P.log_inst && lane == 0 && nchk < P.ccap) {
+        double *r = P.clog + 6 * nchk;
+        r[0] = (double)k; r[1] = metric_; r[2] = ref; r[3] = last; r[4] = restart_; r[5] = outcome;
+      }
+      ++nchk;
+    };
     bool pending = false;
     int outsel = 0;  // 0 current, 1 candidate w / average, as set at termination
     bool rays = false;  // infeasible: the certificate rays are already written (reading 35)
@@ -371,6 +383,10 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
       else if (__builtin_expect(!eb_ok, 0)) eb = div_rn_slow(M, 2.0 * fabs(Iv));
       const bool acc = CS || (eta <= eb);
       const double eta_used = eta;
+      if (LG && b == P.log_inst && lane == 0 && jatt <= P.acap) {
+        double *r = P.alog + 4 * (jatt - 1);
+        r[0] = (double)jatt; r[1] = acc ? 1.0 : 0.0; r[2] = eta_used; r[3] = eb;
+      }
       if (!CS) eta = fmin(f1 * eb, f2 * eta);
       // the attempt's bookkeeping without branches (selects on acc); one rarely taken branch
       // leaves the common path: 100 consecutive rejections, or an accepted step that is due a check
@@ -460,7 +476,7 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
         const Kkt5 kw = kkt5(v);
         if (lane == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
           verbose_line(b, k, kw.pobj, kw.dobj, kw.pres, kw.dres, kw.gap, omega, eta);
-        if (tpass(kw, nq0, nc0)) { status = LP_OPTIMAL; outsel = 1; break; }
+        if (tpass(kw, nq0, nc0)) { log_check(rP, 0, 1); status = LP_OPTIMAL; outsel = 1; break; }
         {
           double mv[2] = {cacc.vy, cacc.vx};
           ired<NT, true>(mv, red, rb);
@@ -470,10 +486,11 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
           const int st = cert_decide(tot, P.eps_pi, P.eps_di, ny, nx);
           if (st) {
             write_rays(b, ny, nx, xa, KTya, ya);
+            log_check(0.0, 0, 3);
             status = st; outsel = 0; rays = true; break;
           }
         }
-        if (k == P.iter_limit) { status = LP_ITERATION_LIMIT; outsel = 1; break; }
+        if (k == P.iter_limit) { log_check(rP, 0, 0); status = LP_ITERATION_LIMIT; outsel = 1; break; }
         metric = rP; dx2c = v[4]; dy2c = v[5]; csel = 1;
       } else {
         // the average's products: K~ x-bar and K~' y-bar through the gather buffers
@@ -530,8 +547,8 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
         const Kkt5 ka = kkt5(v + 0), kc = kkt5(v + 4);
         if (lane == 0 && verbose_due(P.verbose, P.display_freq, k, P.check_freq))
           verbose_line(b, k, kc.pobj, kc.dobj, kc.pres, kc.dres, kc.gap, omega, eta);
-        if (tpass(ka, nq0, nc0)) { status = LP_OPTIMAL; outsel = 1; break; }
-        if (tpass(kc, nq0, nc0)) { status = LP_OPTIMAL; outsel = 0; break; }
+        if (tpass(ka, nq0, nc0)) { log_check(0.0, 0, 1); status = LP_OPTIMAL; outsel = 1; break; }
+        if (tpass(kc, nq0, nc0)) { log_check(0.0, 0, 2); status = LP_OPTIMAL; outsel = 0; break; }
         {
           double mv[2] = {cacc.vy, cacc.vx};
           ired<NT, true>(mv, red, rb);
@@ -541,10 +558,12 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
           const int st = cert_decide(tot, P.eps_pi, P.eps_di, ny, nx);
           if (st) {
             write_rays(b, ny, nx, xo, KTyo, yo);
+            log_check(0.0, 0, 3);
             status = st; outsel = 0; rays = true; break;
           }
         }
         if (k == P.iter_limit) {
+          log_check(0.0, 0, 0);
           status = LP_ITERATION_LIMIT;
           outsel = kkt5_rel(ka, nq0, nc0) < kkt5_rel(kc, nq0, nc0) ? 1 : 0;
           break;
@@ -556,6 +575,7 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
         else { csel = 0; metric = e_c; dx2c = v[18]; dy2c = v[19]; }
       }
       const bool restart = restart_due(k_in, k, metric, ref, last);
+      log_check(metric, restart ? 1 : 0, 0);
       last = metric;
       if (restart) {
         ++restarts;
@@ -621,7 +641,7 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
   }
 }
 
-template <bool R2, bool CS, int NT, int RPT, int CPT, int W, int WT>
+template <bool R2, bool CS, int NT, int RPT, int CPT, int W, int WT, bool LG = false>
 int launch_tiny(TinyParams P, cudaStream_t s, unsigned long long *qbase) {
   const size_t smem = (size_t)NT * (CPT + RPT) * sizeof(double) +
                       (NT > 32 ? (size_t)2 * (NT / 32) * kRedV * sizeof(double) : 0);
@@ -632,7 +652,7 @@ int launch_tiny(TinyParams P, cudaStream_t s, unsigned long long *qbase) {
     int dev = 0, s_ = 0, p_ = 0;
     MPAX_CUDA(cudaGetDevice(&dev));
     MPAX_CUDA(cudaDeviceGetAttribute(&s_, cudaDevAttrMultiProcessorCount, dev));
-    MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p_, tiny_kernel<R2, CS, NT, RPT, CPT, W, WT>, NT, smem));
+    MPAX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p_, tiny_kernel<R2, CS, NT, RPT, CPT, W, WT, LG>, NT, smem));
     sms = s_;
     per_sm = p_ < 1 ? 1 : p_;
   }
@@ -644,19 +664,19 @@ int launch_tiny(TinyParams P, cudaStream_t s, unsigned long long *qbase) {
   } else {
     P.qbase = *qbase;
   }
-  MPAX_LAUNCH((tiny_kernel<R2, CS, NT, RPT, CPT, W, WT>), (int)grid, NT, smem, s, P);
+  MPAX_LAUNCH((tiny_kernel<R2, CS, NT, RPT, CPT, W, WT, LG>), (int)grid, NT, smem, s, P);
   MPAX_CHECK_LAUNCH();
   // every CTA ends on one ticket past the batch: the launch consumes batch + grid tickets
   if (qbase) *qbase = P.qbase + (unsigned long long)P.batch + (unsigned long long)grid;
   return LP_OK;
 }
 
-template <int NT, int RPT, int CPT, int W, int WT>
+template <int NT, int RPT, int CPT, int W, int WT, bool LG = false>
 int launch_alg(const TinyParams &P, bool r2, bool cs, cudaStream_t s, unsigned long long *qb) {
-  if (cs) return r2 ? launch_tiny<true, true, NT, RPT, CPT, W, WT>(P, s, qb)
-                    : launch_tiny<false, true, NT, RPT, CPT, W, WT>(P, s, qb);
-  return r2 ? launch_tiny<true, false, NT, RPT, CPT, W, WT>(P, s, qb)
-            : launch_tiny<false, false, NT, RPT, CPT, W, WT>(P, s, qb);
+  if (cs) return r2 ? launch_tiny<true, true, NT, RPT, CPT, W, WT, LG>(P, s, qb)
+                    : launch_tiny<false, true, NT, RPT, CPT, W, WT, LG>(P, s, qb);
+  return r2 ? launch_tiny<true, false, NT, RPT, CPT, W, WT, LG>(P, s, qb)
+            : launch_tiny<false, false, NT, RPT, CPT, W, WT, LG>(P, s, qb);
 }
 
 }  // namespace
@@ -677,11 +697,19 @@ int tiny_solve(const DevProblem &D, const lp_options &o, const InstanceLaunch &L
   P.verbose = o.verbose; P.display_freq = o.display_frequency;
   P.batch = L.batch; P.queue = queue;
   P.X = L.X; P.Y = L.Y; P.L = L.L; P.res = L.res; P.res_host = L.res_host;
+  P.alog = L.alog; P.clog = L.clog; P.acap = L.acap; P.ccap = L.ccap; P.log_inst = L.log_inst;
+  const bool lg = L.alog || L.clog;
   const bool r2 = o.algorithm == LP_R2HPDHG, cs = o.step_rule == LP_STEP_CONSTANT;
   const int64_t n = D.n, m = D.m;
   const int W = D.max_row, WT = D.max_col;
   // ELL widths as tight as the LP allows: a padded slot is a zero-valued FMA on the attempt's
   // dependent chain (C2, the 5x5 grid: every column of K has exactly two entries)
+  // a decision log (one instance's records): the C2 shapes only
+  if (lg) {
+    if (m <= 32 && n <= 64 && W <= 4 && WT <= 2) return launch_alg<32, 1, 2, 4, 2, true>(P, r2, cs, s, qbase);
+    if (m <= 32 && n <= 64 && W <= 4 && WT <= 4) return launch_alg<32, 1, 2, 4, 4, true>(P, r2, cs, s, qbase);
+    return LP_ERR_UNSUPPORTED;
+  }
   if (m <= 32 && n <= 64 && W <= 4 && WT <= 2) return launch_alg<32, 1, 2, 4, 2>(P, r2, cs, s, qbase);
   if (m <= 32 && n <= 64 && W <= 4 && WT <= 4) return launch_alg<32, 1, 2, 4, 4>(P, r2, cs, s, qbase);
   if (m <= 32 && n <= 64 && W <= 8 && WT <= 8) return launch_alg<32, 1, 2, 8, 8>(P, r2, cs, s, qbase);

@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = [
     "lp_kernel_launch_count", "lp_error_string", "lp_last_error_detail", "lp_destroy",
     "lp_create_sharded", "lp_create_sharded_virtual", "lp_nccl_unique_id", "lp_nccl_comm_init",
     "lp_nccl_comm_destroy", "lp_spo_plus", "lp_selftest_division", "lp_set_decision_log",
-    "lp_shard_axis", "lp_create_sharded_cols", "lp_create_sharded_virtual_axis",
+    "lp_shard_axis", "lp_create_sharded_cols", "lp_create_sharded_virtual_axis", "lp_set_decision_log_instance",
 ]
 
 
@@ -98,6 +98,8 @@ def lib():
             L.lp_get_scaling.argtypes = [V, V, V, C.c_int32]
             if hasattr(L, "lp_set_decision_log"):
                 L.lp_set_decision_log.argtypes = [V, V, C.c_int64, V, C.c_int64]
+            if hasattr(L, "lp_set_decision_log_instance"):
+                L.lp_set_decision_log_instance.argtypes = [V, C.c_int64]
             L.lp_spmv_scaled.argtypes = [V, V, V, V, V, C.c_int32]
             L.lp_kernel_launch_count.restype = C.c_int64
             L.lp_create_sharded.argtypes = [P(ProblemDesc), C.c_int64, C.c_int64, C.c_int64, V, C.c_int, C.c_int,
@@ -443,10 +445,23 @@ class BatchSolver:
         ca, qa = _Arr(C_, np.float64), _Arr(Q, np.float64)
         _check(lib().lp_update_batch(self._h, ca.ptr, qa.ptr, _same_mem([C_, Q])), "lp_update_batch")
 
+    def set_decision_log(self, att_cap=4096, chk_cap=256, instance=0, device=None):
+        """Record the line-search and restart decisions of batch instance `instance` (register
+        kernel, C2 shapes; lp_set_decision_log / lp_set_decision_log_instance)."""
+        _check(lib().lp_set_decision_log_instance(self._h, int(instance)), "lp_set_decision_log_instance")
+        Solver.set_decision_log(self, att_cap, chk_cap, device)
+
+    decision_log = Solver.decision_log
+
     def solve(self, X0=None, Y0=None, **opts):
         """Returns a numpy structured array of `batch` results (fields as lp_result);
         res[b]["status"], res["iterations"], ... (no per-instance Python objects)."""
         o = default_options(**opts)
+        if getattr(self, "_alog", None) is not None:   # the decision log's rows start unwritten
+            self._alog.fill_(float("nan"))
+            self._clog.fill_(float("nan"))
+            import torch
+            torch.cuda.current_stream().synchronize()
         a, b = _Arr(X0, np.float64), _Arr(Y0, np.float64)
         res = np.zeros(self.batch, dtype=RESULT_DTYPE)
         _check(lib().lp_solve_batch(self._h, C.byref(o), a.ptr, b.ptr, _same_mem([X0, Y0]), res.ctypes.data),
