@@ -23,7 +23,7 @@ torch.cuda.synchronize()
 print(f"create (validate+transpose+precondition) {time.time() - t0:.3f}s", flush=True)
 res = {}
 precs = os.environ.get("C5_PREC", "fp64").split(",")
-for alg in ("ra", "r2"):
+for alg in os.environ.get("C5_ALGS", "ra,r2").split(","):
     for prec in precs:
         e = 8 if prec == "fp64" else 4
         for _ in range(int(os.environ.get("C5_REPS", "1"))):   # > 1: the last solve is reported (warm)
@@ -41,7 +41,7 @@ for alg in ("ra", "r2"):
 if os.environ.get("C5_ORACLE"):
     import oracle
     oracle.set_threads(len(os.sched_getaffinity(0)))
-    for alg in ("ra", "r2"):
+    for alg in os.environ.get("C5_ALGS", "ra,r2").split(","):
         t0 = time.time()
         ro = oracle.solve(lp, alg, iteration_limit=2, eps_abs=0.0, eps_rel=0.0)
         t1 = time.time()
