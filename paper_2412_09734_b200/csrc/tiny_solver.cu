@@ -276,12 +276,11 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
       // Branch-free: the commit is computed every attempt and selected by `pending`
       // (theta_p = 0 leaves the average bit-identical), so the attempt is one basic block.
       const double tau = eta * inv_omega, sigma = eta * omega;
-      // raPDHG's averaging weight eta / (W + eta) if this attempt is accepted: the division's
-      // fast path here, its (rare) slow path only at acceptance (div_rn_fast, bit-identical to /)
+      // raPDHG's averaging weight eta / (W + eta) if this attempt is accepted: its division's fast
+      // path is issued beside the (dy2, I) butterfly below, whose shuffle chain hides the Newton
+      // chain (issued here, the in-order warp stalled on it before the primal step: 9% of the
+      // attempt, ncu source page); its (rare) slow path only at acceptance (bit-identical to /)
       const double W1c = W_ + eta;
-      bool theta_ok = true;
-      const double theta_f = R2 ? 0.0 : div_rn_fast(eta, W1c, theta_ok);
-      if (!R2) pin(theta_f);
       const double theta_p = pending ? theta : 0.0;
       const double f1 = f1n, f2 = f2n;
       if (!CS) {
@@ -356,6 +355,8 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
       }
       pending = false;
       double v3[2] = {dy2, I};
+      bool theta_ok = true;
+      const double theta_f = R2 ? 0.0 : div_rn_fast(eta, W1c, theta_ok);
       if (need) {  // ||dy||^2, <dy, K dx> (and ||dx||^2 for a CTA instance)
         if (NT == 32) {
           wsum<2>(v3);
@@ -374,6 +375,7 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
         for (int w = 0; w < WT; ++w) s += cval[t][w] * sy[ccol[t][w]];
         KTyn[t] = cok[t] ? s : 0.0;
       }
+      if (!R2) pin(theta_f);   // complete before the decision's own chain starts
       ++jatt;
       const double M = omega * vdx[0] + v3[0] * inv_omega;
       const double Iv = v3[1];
