@@ -284,18 +284,12 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
       const double theta_p = pending ? theta : 0.0;
       const double f1 = f1n, f2 = f2n;
       if (!CS) {
-        // the table entry of attempt jatt + 2 (clamped; past the table the factors come from
-        // the out-of-line pow, a rarely taken call)
-        const bool in_tab = jatt + 2 < kStepTab;
-        const double *fp = in_tab ? ftab : P.tab;
-        f1n = __ldg(fp);
-        f2n = __ldg(fp + 1);
-        if (__builtin_expect(!in_tab, 0)) {
-          const double2 f = step_factors_far(jatt + 2);
-          f1n = f.x;
-          f2n = f.y;
-        }
-        ftab += 2;
+        // the table entry of attempt jatt + 2, without a branch: the pointer stops on the table's
+        // last entry, and past the table the factors are replaced at the end of the previous
+        // attempt (the out-of-line pow, in the loop's rarely taken tail)
+        f1n = __ldg(ftab);
+        f2n = __ldg(ftab + 1);
+        ftab += (jatt + 3 < kStepTab) ? 2 : 0;
       }
       // r2HPDHG: the Halpern coefficients this attempt commits with if accepted (index k_in),
       // loaded now so the table latency overlaps the attempt instead of the next commit
@@ -410,7 +404,13 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
       k += acc;
       k_in += acc;
       pending = acc;
-      if (__builtin_expect(!(acc && k == next_check) && rejects < 100, 1)) continue;
+      if (__builtin_expect(!(acc && k == next_check) && rejects < 100 && (CS || jatt + 1 < kStepTab), 1)) continue;
+      if (!CS && jatt + 1 >= kStepTab) {   // past the factor table: the next attempt's factors
+        const double2 f = step_factors_far(jatt + 1);
+        f1n = f.x;
+        f2n = f.y;
+        if (!(acc && k == next_check) && rejects < 100) continue;
+      }
       if (rejects >= 100) { status = LP_NUMERICAL_ERROR; outsel = 0; break; }
       pending = false;   // the check commits this step itself
       next_check = (next_check + P.check_freq < P.iter_limit) ? next_check + P.check_freq : P.iter_limit;

@@ -205,3 +205,29 @@ def test_decision_log_off_and_unsupported():
         assert len(att) == min(100, r["attempts"]) and chk[-1, 5] == 1   # capacity respected; optimal
         s.set_decision_log(att_cap=0, chk_cap=0)
         assert s.solve(algorithm="r2")["status"] == mp.LP_OPTIMAL         # log off: any path again
+
+
+def test_step_factors_past_the_table():
+    """The line-search factors of attempt j, 1 - (j+1)^-0.3 and 1 + (j+1)^-0.6 (contract step 3),
+    come from a 65 536-entry table and, past it, from pow: the register kernel's logged step sizes
+    obey eta_{j+1} = min(f1(j) eta_bar_j, f2(j) eta_j) on both sides of the table's end."""
+    lp, C = lpgen.g_grid(batch=1, seed=2)
+    # no flow can leave the source with every arc fixed at 0: a primal-infeasible grid LP that,
+    # with infeasibility detection off, keeps iterating to the limit (a feasible one converges to
+    # rounding and stops on 100 rejections long before 65 536 attempts)
+    lp = lpgen.LP(lp.n, lp.m1, lp.m2, lp.row_ptr, lp.col_idx, lp.val, C[0], lp.q, lp.l, np.zeros(lp.n))
+    bs = mp.BatchSolver(mp.Problem.from_lp(lp).to("cuda"), torch.as_tensor(C[:1], device="cuda"))
+    bs.set_decision_log(att_cap=66500, chk_cap=2000, instance=0)
+    r = bs.solve(algorithm="ra", iteration_limit=66100, eps_abs=0.0, eps_rel=0.0, eps_primal_infeasible=-1.0,
+                 eps_dual_infeasible=-1.0)
+    att, _ = bs.decision_log()
+    bs.close()
+    assert r[0]["attempts"] >= 66100 and len(att) >= 66000, (r[0]["status"], r[0]["attempts"])
+    j = att[:-1, 0]
+    f1 = 1.0 - np.power(j + 1.0, -0.3)
+    f2 = 1.0 + np.power(j + 1.0, -0.6)
+    want = np.minimum(f1 * att[:-1, 3], f2 * att[:-1, 2])
+    np.testing.assert_allclose(att[1:, 2], want, rtol=1e-13)
+    sel = (j >= 65520) & (j <= 65560)   # across the table's end
+    assert sel.sum() >= 40
+    np.testing.assert_allclose(att[1:, 2][sel], want[sel], rtol=1e-14)
