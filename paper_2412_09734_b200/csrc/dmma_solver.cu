@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1) dmma_kernel(const DmmaParams P) {
         }
         const double sigma = I.eta * I.omega;
         double yn = yv + sigma * (op.qs - 2.0 * kxp + kxv);
-        if (i < m1) yn = fmax(yn, 0.0);
+        if (i < m1) yn = pos_part(yn);
         P.yp[o] = yn; P.Kxp[o] = kxp;
         S.Yf[i * kS + s] = yn;
         const double d = yn - yv;

@@ -299,7 +299,7 @@ __device__ __noinline__ void phase_tiles(const volatile PhaseCtx<T> *cx, int *s_
           kxv = cx->r2[r];
         }
         double yn = yv + cx->tau_sigma * ((double)cx->r0[r] - 2.0 * s + kxv);
-        if (r < cx->m1) yn = fmax(yn, 0.0);
+        if (r < cx->m1) yn = pos_part(yn);
         if (MODE == kB_RA) { cx->e1[r] = yn; cx->e2[r] = s; }
         else { cx->e2[r] = yn; cx->e3[r] = s; }
         const double d = yn - yv;
@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(kBS, MINB) grid_kernel(GridParams<T> P) {
           yv = o_y; kxv = o_kx;
         }
         double yn = yv + sigma * (o_qs - 2.0 * s + kxv);
-        if (i < m1) yn = fmax(yn, 0.0);
+        if (i < m1) yn = pos_part(yn);
         if (pending && !r2) { st_tgt(y + i, yn); sv(Kx + i, s); }   // old buffers become y', K~x' after the swap
         else { st_tgt(yp + i, yn); sv(Kxp + i, s); }
         const double d = yn - yv;

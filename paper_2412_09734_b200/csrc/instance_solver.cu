@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(NW * 32) instance_kernel(const InstParams P) {
           yv = y[i]; kxv = Kx[i];
         }
         double yn = yv + sigma * (qs[i] - 2.0 * s + kxv);
-        if (i < m1) yn = fmax(yn, 0.0);
+        if (i < m1) yn = pos_part(yn);
         if (pend && !r2) { y[i] = yn; Kx[i] = s; }   // old buffers become y', K~x' after the swap
         else { yp[i] = yn; Kxp[i] = s; }
         const double d = yn - yv;

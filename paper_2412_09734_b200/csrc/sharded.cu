@@ -336,7 +336,7 @@ __global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, cons
       }
       if (mode == ROWS_STEP) {
         double yn = yv + sigma * (V.qs[i] - 2.0 * s + kxv);
-        if (ge) yn = fmax(yn, 0.0);
+        if (ge) yn = pos_part(yn);
         V.yp[i] = yn; V.Kxp[i] = s;
         const double d = yn - yv;
         v[0] += d * d;

@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
         }
         // q~ - 2 K~x' as one fma: 2 s is exact, so this is the oracle's q~ - 2.0 * s, one op shorter
         double yn = y[t] + sigma * (fma(-2.0, s, qs[t]) + Kx[t]);
-        if (lane + NT * t < m1) yn = fmax(yn, 0.0);
+        if (lane + NT * t < m1) yn = pos_part(yn);
         yp[t] = rok[t] ? yn : 0.0;
         Kxp[t] = rok[t] ? s : 0.0;
         sy[lane + NT * t] = yp[t];
