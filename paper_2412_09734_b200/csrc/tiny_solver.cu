@@ -373,38 +373,64 @@ __global__ void __launch_bounds__(NT) tiny_kernel(const TinyParams P) {
       ++jatt;
       const double M = omega * vdx[0] + v3[0] * inv_omega;
       const double Iv = v3[1];
+      // eta_bar = M / 2|I| by the division's fast path, taken as exact here; its rare slow path
+      // (operands near the exponent limits) is taken in the loop's tail, which redoes the
+      // decision from the saved pre-decision state -- so no branch waits on the quotient
       bool eb_ok = true;
       double eb = div_rn_fast(M, 2.0 * fabs(Iv), eb_ok);
-      if (Iv == 0.0) eb = INFINITY;
-      else if (__builtin_expect(!eb_ok, 0)) eb = div_rn_slow(M, 2.0 * fabs(Iv));
-      const bool acc = CS || (eta <= eb);
+      eb_ok = eb_ok || Iv == 0.0;
+      eb = Iv == 0.0 ? INFINITY : eb;
       const double eta_used = eta;
+      const double theta0 = theta, W0 = W_, ref0 = ref, ha0 = ha, hb0 = hb;
+      const int rej0 = rejects;
+      bool acc = false;
+      double rP = 0.0;
+      // the attempt's bookkeeping without branches (selects on acc); one rarely taken branch
+      // leaves the common path: 100 consecutive rejections, an accepted step that is due a check,
+      // or a slow-path division
+      auto decide = [&](double ebv) {
+        acc = CS || (eta_used <= ebv);
+        if (!CS) eta = fmin(f1 * ebv, f2 * eta_used);
+        rejects = acc ? 0 : rej0 + 1;
+        if (!R2) {
+          theta = acc ? theta_f : theta0;
+          W_ = acc ? W1c : W0;
+        } else {
+          // r_P is read only as the restart reference (k_in = 0) and as the check metric:
+          // skip its division and square root on the other attempts (they sit on the
+          // warp's in-order issue path)
+          rP = 0.0;
+          if (acc && (k_in == 0 || k + 1 == next_check)) rP = sqrt(fmax(0.0, M / eta_used - 2.0 * Iv));
+          ref = (acc && k_in == 0) ? rP : ref0;
+          ha = acc ? ha_n : ha0;
+          hb = acc ? hb_n : hb0;
+        }
+      };
+      decide(eb);
+      if (__builtin_expect(!(acc && k + 1 == next_check) && rejects < 100 && (CS || jatt + 1 < kStepTab) && eb_ok &&
+                               (R2 || theta_ok || !acc), 1)) {
+        if (LG && b == P.log_inst && lane == 0 && jatt <= P.acap) {
+          double *r = P.alog + 4 * (jatt - 1);
+          r[0] = (double)jatt; r[1] = acc ? 1.0 : 0.0; r[2] = eta_used; r[3] = eb;
+        }
+        k += acc;
+        k_in += acc;
+        pending = acc;
+        continue;
+      }
+      if (!eb_ok) {   // the exact quotient; the decision again from the saved state
+        eb = div_rn_slow(M, 2.0 * fabs(Iv));
+        decide(eb);
+      }
+      if (!R2 && acc && !theta_ok) theta = div_rn_slow(eta_used, W1c);
       if (LG && b == P.log_inst && lane == 0 && jatt <= P.acap) {
         double *r = P.alog + 4 * (jatt - 1);
         r[0] = (double)jatt; r[1] = acc ? 1.0 : 0.0; r[2] = eta_used; r[3] = eb;
       }
-      if (!CS) eta = fmin(f1 * eb, f2 * eta);
-      // the attempt's bookkeeping without branches (selects on acc); one rarely taken branch
-      // leaves the common path: 100 consecutive rejections, or an accepted step that is due a check
-      rejects = acc ? 0 : rejects + 1;
-      double rP = 0.0;
-      if (!R2) {
-        theta = acc ? theta_f : theta;
-        W_ = acc ? W1c : W_;
-        if (__builtin_expect(acc && !theta_ok, 0)) theta = div_rn_slow(eta_used, W1c);
-      } else {
-        // r_P is read only as the restart reference (k_in = 0) and as the check metric:
-        // skip its division and square root on the other attempts (they sit on the
-        // warp's in-order issue path)
-        if (acc && (k_in == 0 || k + 1 == next_check)) rP = sqrt(fmax(0.0, M / eta_used - 2.0 * Iv));
-        if (acc && k_in == 0) ref = rP;
-        ha = acc ? ha_n : ha;
-        hb = acc ? hb_n : hb;
-      }
       k += acc;
       k_in += acc;
       pending = acc;
-      if (__builtin_expect(!(acc && k == next_check) && rejects < 100 && (CS || jatt + 1 < kStepTab), 1)) continue;
+      if (!(acc && k == next_check) && rejects < 100 && (CS || jatt + 1 < kStepTab)) continue;
       if (!CS && jatt + 1 >= kStepTab) {   // past the factor table: the next attempt's factors
         const double2 f = step_factors_far(jatt + 1);
         f1n = f.x;
