@@ -1240,7 +1240,10 @@ int grid_launch(const DevProblem &D, const lp_options &o, const GridLaunch &L, c
   // phase B only by default
   P.dyn = 2;
   if (const char *e = getenv("MPAX_GRID_DYN")) P.dyn = atoi(e);
-  P.lean = 3;
+  // lean out-of-line sweeps where the 64-register budget of 2 CTAs per SM needs them (C5); with
+  // 1 CTA of 128 registers per SM the inlined sweeps are 1.5% faster (C4: 44.6 -> 44.0 us per
+  // attempt, scripts/gpu_c4_knobs.sh)
+  P.lean = minb == 1 ? 0 : 3;
   if (const char *e = getenv("MPAX_GRID_LEAN")) P.lean = atoi(e);   // experiments: 0 = the inlined sweeps
   P.split = (D.split_h > 0 && split_wanted(D, (int)sizeof(T)) && P.gk == 1 && (P.dyn & 2) &&
              (!f32 || D.f32_split_h == D.split_h)) ? 1 : 0;
