@@ -267,3 +267,23 @@ def test_chunked_exchange_matches_unchunked(shards, monkeypatch):
     b = sharded(lp, "r2", shards, iteration_limit=300, eps_abs=0.0, eps_rel=0.0)
     assert a["attempts"] == b["attempts"] and a["restarts"] == b["restarts"]
     assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["y"], b["y"])
+
+
+def test_nccl_one_rank_columns_equals_virtual():
+    """lp_create_sharded_cols through a real 1-rank NCCL communicator (the multi-process entry
+    point, its local block being the whole LP) against the virtual 1-shard column engine."""
+    lp = lpgen.g_rand(700, 9000, 30, seed=8)
+    prob = mp.Problem.from_lp(lp)
+    loc = mp.local_cols(prob, 0, lp.n)
+    uid = mp.nccl_unique_id()
+    comm = mp.nccl_comm_init(1, uid, 0)
+    try:
+        with mp.ShardedSolver(loc, comm=comm, rank=0, nranks=1, axis="cols", global_col_offset=0,
+                              n_global=lp.n) as s:
+            a = s.solve(algorithm="r2", iteration_limit=200, eps_abs=0.0, eps_rel=0.0)
+            xa, ya, la = s.solution()
+    finally:
+        mp.nccl_comm_destroy(comm)
+    b = sharded_cols(lp, "r2", 1, iteration_limit=200, eps_abs=0.0, eps_rel=0.0)
+    assert a["attempts"] == b["attempts"]
+    assert np.array_equal(xa, b["x"]) and np.array_equal(ya, b["y"]) and np.array_equal(la, b["lam"])
