@@ -106,3 +106,55 @@ def test_fp32_deterministic():
     a = grid_solve(lp, "r2", precision="fp32", iteration_limit=300, eps_abs=0.0, eps_rel=0.0)
     b = grid_solve(lp, "r2", precision="fp32", iteration_limit=300, eps_abs=0.0, eps_rel=0.0)
     assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["y"], b["y"]) and a["attempts"] == b["attempts"]
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("kind", ["primal", "dual"])
+def test_fp32_infeasibility_certificates(kind, alg):
+    """fp32 storage with infeasibility detection (reading 35) at tolerances a single-precision
+    ray can meet (1e-5: the default 1e-8 lies below fp32's rounding of a unit ray).  A ray is the
+    difference of two nearly equal fp32 points, so whether it meets the tolerance within the
+    limit depends on the trajectory's rounding: the GPU must certify at least as many of the
+    four planted LPs as the fp32 oracle less one, never the wrong kind, and every GPU certificate
+    must be a Farkas certificate of the fp64 problem to the fp32 level (1e-4)."""
+    from tests.test_oracle_infeasibility import farkas_dual_ok, farkas_primal_ok
+    want = mp.LP_PRIMAL_INFEASIBLE if kind == "primal" else mp.LP_DUAL_INFEASIBLE
+    certified = certified_o = 0
+    for seed in range(4):
+        lp = lpgen.g_infeasible(kind, seed)
+        tol = dict(eps_primal_infeasible=1e-5, eps_dual_infeasible=1e-5)
+        o32 = oracle.solve(lp, alg, iteration_limit=10000, precision="fp32", **tol)
+        with mp.Solver(mp.Problem.from_lp(lp)) as s:
+            r = s.solve(algorithm=alg, path=mp.PATH_GRID, precision="fp32", iteration_limit=10000, **tol)
+            x, y, _ = s.solution()
+        assert r["status"] in (want, mp.LP_ITERATION_LIMIT, mp.LP_NUMERICAL_ERROR), (seed, r["status"])
+        certified_o += o32["status"] == want
+        if r["status"] == want:
+            certified += 1
+            # unit rays to the fp32 level (the norm is taken before the stored iterate rounds)
+            if want == mp.LP_PRIMAL_INFEASIBLE:
+                assert abs(np.linalg.norm(y) - 1) <= 1e-6 and farkas_primal_ok(lp, y, tol=1e-4)
+            else:
+                assert abs(np.linalg.norm(x) - 1) <= 1e-6 and farkas_dual_ok(lp, x, tol=1e-4)
+    assert certified >= max(1, certified_o - 1), (certified, certified_o)
+    parity_log(f"fp32_infeasibility[{kind},{alg}]", certified=certified, oracle32_certified=certified_o, total=4)
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_fp32_polishing_and_warm_start(alg):
+    lp = lpgen.g_rand(3000, 5000, 12, seed=3)
+    with mp.Solver(mp.Problem.from_lp(lp)) as s:
+        r = s.solve(algorithm=alg, path=mp.PATH_GRID, precision="fp32", eps_abs=1e-3, eps_rel=1e-3,
+                    feasibility_polishing=1)
+        x, y, lam = s.solution()
+        assert r["status"] == mp.LP_OPTIMAL and r["polish"] in (1, 2)
+        k = oracle.kkt_original(lp, x, y)
+        if r["polish"] == 1:   # the polished residuals, recomputed in fp64 on the returned point
+            assert k["pres"] <= 1.05 * 1e-6 * (1 + np.linalg.norm(lp.q))
+            assert k["dres"] <= 1.05 * 1e-6 * (1 + np.linalg.norm(lp.c))
+        # warm start from the (unpolished) fp32 solution: no more accepted steps to 1e-4 than cold
+        cold = s.solve(algorithm=alg, path=mp.PATH_GRID, precision="fp32")
+        xc, yc, _ = s.solution()
+        warm = s.solve(xc, yc, algorithm=alg, path=mp.PATH_GRID, precision="fp32")
+        assert warm["status"] == cold["status"] == mp.LP_OPTIMAL
+        assert warm["iterations"] <= cold["iterations"]
