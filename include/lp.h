@@ -18,7 +18,9 @@
  * instances; plus the SURVEY §8(f) rows: infeasibility detection with
  * certificate rays (reading 35), feasibility polishing
  * (reading 36), the SPO+ layer (reading 37, lp_spo_plus),
- * and the constant-step / partial-reflection variants (readings 34, 38).
+ * the constant-step / partial-reflection variants (readings 34, 38), fp32 storage on the
+ * grid path (reading 39), row- or column-sharded LPs with the axis chosen by
+ * min(m, n) (reading 33), and per-decision logs for the parity tests.
  * Everything after argument checks runs in CUDA kernels on the handle's stream;
  * there is no CPU fallback.
  *
