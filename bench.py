@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--no-spo", action="store_true", help="skip the SPO+ (Warcraft-shaped) leg")
     ap.add_argument("--c5-sharded", action="store_true",
                     help="run the C5 leg on the row-sharded NCCL engine even at one rank (it is used for N > 1)")
+    ap.add_argument("--c5-axis", default="auto", choices=["rows", "cols", "auto"],
+                    help="sharding axis of the C5 sharded leg; auto = the axis whose exchanged vector is "
+                         "shorter (lp_shard_axis, DESIGN reading 33): columns for C5 (m < n)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -398,7 +401,7 @@ def run_ours(args):
         log("large-LP leg (C4)")
         line["large_lp"] = large_lp_leg(mp, torch, dev, stream, peaks, args, cpu=rank == 0 and not args.no_cpu_baseline)
     if not args.no_c5 and (ws > 1 or args.c5_sharded):
-        log("large-LP leg (C5, 1e8 nnz), row-sharded over the ranks (NCCL)")
+        log(f"large-LP leg (C5, 1e8 nnz), sharded over the ranks (NCCL, axis {args.c5_axis})")
         c5 = c5_sharded_leg(mp, torch, dev, ws, rank, args)
         if rank == 0:
             line["c5_sharded"] = c5
@@ -701,28 +704,42 @@ def large_lp_leg(mp, torch, dev, stream, peaks, args, m=None, seed=4, label="C4"
 
 
 def c5_sharded_leg(mp, torch, dev, ws, rank, args, m=5_000_000, seed=5):
-    """C5 = G-RAND(5e6, 1e7, 20, seed 5) row-sharded over the job's ranks (SURVEY §8(e) variant A):
-    each rank holds an nnz-balanced block of rows, the n-long K~'y partials and the scalar
-    partials are ncclAllReduce'd every attempt.  Time to 1e-4 = max over ranks of the
+    """C5 = G-RAND(5e6, 1e7, 20, seed 5) sharded over the job's ranks: by rows
+    (each rank an nnz-balanced row block, the n-long K~'y partials all-reduced every attempt) or
+    by columns (reading 33: column blocks, the m-long K~x' partials all-reduced) -- `--c5-axis`,
+    default the axis whose exchanged vector is shorter.  Time to 1e-4 = max over ranks of the
     library's device-timed solve (strong scaling: the LP is fixed)."""
     import torch.distributed as tdist
     t0 = time.time()
     lp = lpgen.g_rand(m, 2 * m, 20, seed=seed)
     gen_s = time.time() - t0
-    cuts = mp.row_partition(lp.row_ptr, ws)
-    r0, r1 = cuts[rank], cuts[rank + 1]
-    loc = mp.local_rows(mp.Problem.from_lp(lp), r0, r1).to(dev)
+    axis = args.c5_axis
+    if axis == "auto":
+        axis = "cols" if mp.shard_axis(lp.m, lp.n) == mp.SHARD_COLS else "rows"
+    full = mp.Problem.from_lp(lp)
+    if axis == "cols":
+        cuts = mp.col_partition(full, ws)
+        c0, c1 = cuts[rank], cuts[rank + 1]
+        loc = mp.local_cols(full, c0, c1).to(dev)
+        kw = dict(axis="cols", global_col_offset=c0, n_global=lp.n)
+        what = "column-sharded", "K~x' partials (m-long)"
+    else:
+        cuts = mp.row_partition(lp.row_ptr, ws)
+        r0, r1 = cuts[rank], cuts[rank + 1]
+        loc = mp.local_rows(full, r0, r1).to(dev)
+        kw = dict(global_row_offset=r0, m1_global=lp.m1, m2_global=lp.m2)
+        what = "row-sharded", "K~'y partials (n-long)"
+    del full
     uid = [mp.nccl_unique_id() if rank == 0 else None]
     if ws > 1:
         tdist.broadcast_object_list(uid, src=0)
     comm = mp.nccl_comm_init(ws, uid[0], rank)
-    out = {"workload": f"C5: G-RAND({m}, {2 * m}, 20, seed {seed}), one LP row-sharded over {ws} GPU(s) "
-                       f"(NCCL all-reduce of K~'y partials), to 1e-4",
-           "nnz": lp.nnz, "ranks": ws, "rows_per_rank_max": int(max(np.diff(cuts))), "generate_s": gen_s,
+    out = {"workload": f"C5: G-RAND({m}, {2 * m}, 20, seed {seed}), one LP {what[0]} over {ws} GPU(s) "
+                       f"(NCCL all-reduce of the {what[1]}), to 1e-4",
+           "nnz": lp.nnz, "ranks": ws, "axis": axis, "block_max": int(max(np.diff(cuts))), "generate_s": gen_s,
            "scaling": "strong"}
     try:
-        with mp.ShardedSolver(loc, global_row_offset=r0, m1_global=lp.m1, m2_global=lp.m2, comm=comm, rank=rank,
-                              nranks=ws) as s:
+        with mp.ShardedSolver(loc, comm=comm, rank=rank, nranks=ws, **kw) as s:
             for alg in ("ra",):
                 s.solve(algorithm=alg, iteration_limit=20_000)                 # warm-up
                 if ws > 1:

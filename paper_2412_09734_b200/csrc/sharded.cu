@@ -188,7 +188,11 @@ __global__ void k_cols_spmv(const ShState *st, int64_t n, int G, const int32_t *
 enum { COLS_STEP = 0, COLS_COMMIT_ONLY = 1, COLS_AVG = 2, COLS_INIT = 3, COLS_INIT2 = 4, COLS_OUT = 5, COLS_CERT = 6 };
 enum { ROWS_STEP = 0, ROWS_COMMIT_ONLY = 1, ROWS_AVG = 2, ROWS_INIT = 3, ROWS_INIT2 = 4, ROWS_OUT = 5, ROWS_CERT = 6 };
 
-__global__ void k_cols(ShState *st, int mode, int64_t j0, int64_t n, const DevProblem P, const Vecs V) {
+// MODE is a template parameter: each instantiation keeps only its own branch (fewer registers,
+// no per-element mode tests), the per-element arithmetic is unchanged.
+template <int MODE>
+__global__ void k_cols(ShState *st, int64_t j0, int64_t n, const DevProblem P, const Vecs V) {
+  constexpr int mode = MODE;
   if (st->halt && mode != COLS_OUT) return;
   const bool r2 = st->r2, pend = st->pending;
   const double tau = st->eta * st->inv_omega, theta = st->theta, ha = st->ha, hb = st->hb;
@@ -293,7 +297,9 @@ __global__ void k_rows_left(const ShState *st, int64_t m, const DevProblem P, co
   }
 }
 
-__global__ void k_rows(ShState *st, int mode, int64_t m, int64_t m1, int G, const DevProblem P, const Vecs V) {
+template <int MODE>
+__global__ void k_rows(ShState *st, int64_t m, int64_t m1, int G, const DevProblem P, const Vecs V) {
+  constexpr int mode = MODE;
   if (st->halt && mode != ROWS_OUT) return;
   const bool r2 = st->r2, pend = st->pending;
   const double sigma = st->eta * st->omega, theta = st->theta, ha = st->ha, hb = st->hb;
@@ -854,9 +860,21 @@ inline int group_of(double avg, int mx) {
   return g;
 }
 
+// launch KERNEL<mode> (mode 0..6, the COLS_* / ROWS_* enums)
+#define SH_MODE_LAUNCH(KERNEL, mode, ...)                                              \
+  switch (mode) {                                                                      \
+    case 0: MPAX_LAUNCH(KERNEL<0>, __VA_ARGS__); break;                                \
+    case 1: MPAX_LAUNCH(KERNEL<1>, __VA_ARGS__); break;                                \
+    case 2: MPAX_LAUNCH(KERNEL<2>, __VA_ARGS__); break;                                \
+    case 3: MPAX_LAUNCH(KERNEL<3>, __VA_ARGS__); break;                                \
+    case 4: MPAX_LAUNCH(KERNEL<4>, __VA_ARGS__); break;                                \
+    case 5: MPAX_LAUNCH(KERNEL<5>, __VA_ARGS__); break;                                \
+    default: MPAX_LAUNCH(KERNEL<6>, __VA_ARGS__); break;                               \
+  }
+
 int launch_cols(ShardedLP &E, int mode) {
   for (auto &S : E.sh) {
-    MPAX_LAUNCH(k_cols, blocks_for(S.j1 - S.j0), kB, 0, E.s, S.st, mode, S.j0, S.j1, S.P, S.V);
+    SH_MODE_LAUNCH(k_cols, mode, blocks_for(S.j1 - S.j0), kB, 0, E.s, S.st, S.j0, S.j1, S.P, S.V);
   }
   MPAX_CHECK_LAUNCH();
   return LP_OK;
@@ -882,7 +900,7 @@ int launch_rows(ShardedLP &E, int mode) {
     MPAX_CHECK_LAUNCH();
     STRY(reduce_vec(E, 8, bufs, E.m_global, false));
     for (auto &S : E.sh)
-      MPAX_LAUNCH(k_rows, blocks_for(S.P.m), kB, 0, E.s, S.st, mode, S.P.m, S.P.m1, 1, S.P, S.V);
+      SH_MODE_LAUNCH(k_rows, mode, blocks_for(S.P.m), kB, 0, E.s, S.st, S.P.m, S.P.m1, 1, S.P, S.V);
     MPAX_CHECK_LAUNCH();
     return LP_OK;
   }
@@ -891,7 +909,8 @@ int launch_rows(ShardedLP &E, int mode) {
     const bool spmv = (mode == ROWS_STEP || mode == ROWS_AVG || mode == ROWS_INIT2);
     if (mode == ROWS_STEP && S.P.split_h > 0 && G == 1 && S.P.m > 0)
       MPAX_LAUNCH(k_rows_left, blocks_for(S.P.m), kB, 0, E.s, S.st, S.P.m, S.P, S.V.xp, S.V.tmp);
-    MPAX_LAUNCH(k_rows, blocks_for(S.P.m * (spmv ? G : 1)), kB, 0, E.s, S.st, mode, S.P.m, S.P.m1, G, S.P, S.V);
+    SH_MODE_LAUNCH(k_rows, mode, blocks_for(S.P.m * (spmv ? G : 1)), kB, 0, E.s, S.st, S.P.m, S.P.m1, G, S.P,
+                   S.V);
   }
   MPAX_CHECK_LAUNCH();
   return LP_OK;

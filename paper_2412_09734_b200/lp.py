@@ -543,7 +543,7 @@ def col_partition(problem: Problem, parts: int):
     returns parts+1 cut points.  Same rule as the library's virtual column shards."""
     n = problem.n
     cc = np.zeros(n + 1, np.int64)
-    np.add.at(cc, np.asarray(problem.col_idx, np.int64) + 1, 1)
+    cc[1:] = np.bincount(np.asarray(problem.col_idx, np.int64), minlength=n)
     cc = np.cumsum(cc)
     nnz = int(cc[-1])
     cuts = [0]
@@ -563,7 +563,7 @@ def local_cols(problem: Problem, c0: int, c1: int) -> Problem:
     keep = (ci >= c0) & (ci < c1)
     rows = np.repeat(np.arange(rp.size - 1), np.diff(rp))[keep]
     lrp = np.zeros(rp.size, np.int64)
-    np.add.at(lrp, rows + 1, 1)
+    lrp[1:] = np.bincount(rows, minlength=rp.size - 1)
     lrp = np.cumsum(lrp)
     sl = slice(c0, c1)
     return Problem(c1 - c0, problem.m1, problem.m2, lrp, (ci[keep] - c0).astype(np.int32), v[keep],
