@@ -80,10 +80,13 @@ struct Vecs {
 // warp-tile CSR-stream of common.cuh (every lane of the warp calls it, r = tile row + lane;
 // rows = the matrix's row count, buf = the warp's kTileBuf doubles); G >= 2 lanes per row
 // with 4 entries in flight per lane otherwise
+// LR: compile the full-chunk (long-row) path of tile_row_dot in (the matrix has a row of kTileCH
+// entries or more; common.cuh)
+template <bool LR>
 __device__ __forceinline__ double row_dot(int64_t r, bool valid, int G, int gl, const int32_t *__restrict__ rp,
                                           const int32_t *__restrict__ ci, const double *__restrict__ v,
                                           const double *__restrict__ x, int64_t rows, double *buf) {
-  if (G == 1) return tile_row_dot((int)r, valid, (int)rows, rp, ci, v, x, buf);
+  if (G == 1) return tile_row_dot<double, double, LR>((int)r, valid, (int)rows, rp, ci, v, x, buf);
   double s0 = 0.0, s1 = 0.0;
   if (valid) {
     const int32_t e = __ldg(rp + r + 1);
@@ -171,6 +174,7 @@ inline int blocks_for(int64_t work) {
 
 // ------------------------------------------------------------------ kernels --
 
+template <bool LR>
 __global__ void k_cols_spmv(const ShState *st, int64_t n, int G, const int32_t *trp, const int32_t *tci,
                             const double *tkv, const double *ysrc, double *out) {
   if (st->halt) return;
@@ -180,7 +184,7 @@ __global__ void k_cols_spmv(const ShState *st, int64_t n, int G, const int32_t *
   const int64_t iters = (n + ng - 1) / ng;
   for (int64_t it = 0; it < iters; ++it) {
     const int64_t j = it * ng + gt / G;
-    const double s = row_dot(j, j < n, G, gl, trp, tci, tkv, ysrc, n, s_tile[threadIdx.x >> 5]);
+    const double s = row_dot<LR>(j, j < n, G, gl, trp, tci, tkv, ysrc, n, s_tile[threadIdx.x >> 5]);
     if (j < n && gl == 0) out[j] = s;
   }
 }
@@ -286,18 +290,20 @@ __global__ void k_cols(ShState *st, int64_t j0, int64_t n, const DevProblem P, c
 }
 
 // pass 1 of the two-pass rows step: V.tmp = K~_L x' (warp-tile mapping, same order as the grid kernel)
+template <bool LR>
 __global__ void k_rows_left(const ShState *st, int64_t m, const DevProblem P, const double *x, double *tmp) {
   if (st->halt) return;
   __shared__ double s_tile[kB / 32][kTileBuf];
   const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x, nthr = (int64_t)gridDim.x * kB;
   for (int64_t base = gt - (threadIdx.x & 31); base < m; base += nthr) {
     const int64_t r = base + (threadIdx.x & 31);
-    const double v = tile_row_dot((int)r, r < m, (int)m, P.rpL, P.ciL, P.kvL, x, s_tile[threadIdx.x >> 5]);
+    const double v = tile_row_dot<double, double, LR>((int)r, r < m, (int)m, P.rpL, P.ciL, P.kvL, x,
+                                                       s_tile[threadIdx.x >> 5]);
     if (r < m) tmp[r] = v;
   }
 }
 
-template <int MODE>
+template <int MODE, bool LR>
 __global__ void k_rows(ShState *st, int64_t m, int64_t m1, int G, const DevProblem P, const Vecs V) {
   constexpr int mode = MODE;
   if (st->halt && mode != ROWS_OUT) return;
@@ -321,8 +327,8 @@ __global__ void k_rows(ShState *st, int64_t m, int64_t m1, int G, const DevProbl
     const bool two = mode == ROWS_STEP && P.split_h > 0 && g == 1;
     const double s = !spmv ? 0.0
                      : V.pre ? (ok ? V.pre[i] : 0.0)   // column mode: the cross-shard sum, computed before
-                     : two ? (ok ? V.tmp[i] : 0.0) + row_dot(i, ok, 1, 0, P.rpR, P.ciR, P.kvR, src, m, s_tile[threadIdx.x >> 5])
-                           : row_dot(i, ok, g, gl, P.rp, P.ci, P.kv, src, m, s_tile[threadIdx.x >> 5]);
+                     : two ? (ok ? V.tmp[i] : 0.0) + row_dot<LR>(i, ok, 1, 0, P.rpR, P.ciR, P.kvR, src, m, s_tile[threadIdx.x >> 5])
+                           : row_dot<LR>(i, ok, g, gl, P.rp, P.ci, P.kv, src, m, s_tile[threadIdx.x >> 5]);
     if (!lead) continue;
     const double dr = P.Dr[i];
     const bool ge = i < m1;
@@ -872,6 +878,25 @@ inline int group_of(double avg, int mx) {
     default: MPAX_LAUNCH(KERNEL<6>, __VA_ARGS__); break;                               \
   }
 
+// KERNEL<mode, lr> for the row-side kernels (lr: the matrix has long rows)
+#define SH_ONE_LR(KERNEL, M, LRV, ...)                                                 \
+  { auto kfn = KERNEL<M, LRV>; MPAX_LAUNCH(kfn, __VA_ARGS__); }
+#define SH_MODE_LR(KERNEL, M, lr, ...)                                                 \
+  if (lr) SH_ONE_LR(KERNEL, M, true, __VA_ARGS__) else SH_ONE_LR(KERNEL, M, false, __VA_ARGS__)
+#define SH_MODE_LAUNCH_LR(KERNEL, mode, lr, ...)                                       \
+  switch (mode) {                                                                      \
+    case 0: SH_MODE_LR(KERNEL, 0, lr, __VA_ARGS__) break;                              \
+    case 1: SH_MODE_LR(KERNEL, 1, lr, __VA_ARGS__) break;                              \
+    case 2: SH_MODE_LR(KERNEL, 2, lr, __VA_ARGS__) break;                              \
+    case 3: SH_MODE_LR(KERNEL, 3, lr, __VA_ARGS__) break;                              \
+    case 4: SH_MODE_LR(KERNEL, 4, lr, __VA_ARGS__) break;                              \
+    case 5: SH_MODE_LR(KERNEL, 5, lr, __VA_ARGS__) break;                              \
+    default: SH_MODE_LR(KERNEL, 6, lr, __VA_ARGS__) break;                             \
+  }
+#define SH_LR(KERNEL, lr, ...)                                                         \
+  if (lr) MPAX_LAUNCH(KERNEL<true>, __VA_ARGS__); else MPAX_LAUNCH(KERNEL<false>, __VA_ARGS__)
+inline bool long_rows(int max_len) { return max_len < 0 || max_len >= kTileCH; }   // unknown: keep the path
+
 int launch_cols(ShardedLP &E, int mode) {
   for (auto &S : E.sh) {
     SH_MODE_LAUNCH(k_cols, mode, blocks_for(S.j1 - S.j0), kB, 0, E.s, S.st, S.j0, S.j1, S.P, S.V);
@@ -893,14 +918,15 @@ int launch_rows(ShardedLP &E, int mode) {
     for (auto &S : E.sh) {
       const int G = group_of(S.P.avg_row, S.P.max_row);
       const double *src = mode == ROWS_AVG ? S.V.xa : (mode == ROWS_INIT2 ? S.V.x : S.V.xp);
-      MPAX_LAUNCH(k_cols_spmv, blocks_for(S.P.m * G), kB, 0, E.s, S.st, S.P.m, G, S.P.rp, S.P.ci, S.P.kv, src,
-                  S.V.tmp);
+      SH_LR(k_cols_spmv, long_rows(S.P.max_row), blocks_for(S.P.m * G), kB, 0, E.s, S.st, S.P.m, G, S.P.rp,
+            S.P.ci, S.P.kv, src, S.V.tmp);
       bufs.push_back(S.V.tmp);
     }
     MPAX_CHECK_LAUNCH();
     STRY(reduce_vec(E, 8, bufs, E.m_global, false));
     for (auto &S : E.sh)
-      SH_MODE_LAUNCH(k_rows, mode, blocks_for(S.P.m), kB, 0, E.s, S.st, S.P.m, S.P.m1, 1, S.P, S.V);
+      SH_MODE_LAUNCH_LR(k_rows, mode, long_rows(S.P.max_row), blocks_for(S.P.m), kB, 0, E.s, S.st, S.P.m, S.P.m1,
+                        1, S.P, S.V);
     MPAX_CHECK_LAUNCH();
     return LP_OK;
   }
@@ -908,9 +934,10 @@ int launch_rows(ShardedLP &E, int mode) {
     const int G = group_of(S.P.avg_row, S.P.max_row);
     const bool spmv = (mode == ROWS_STEP || mode == ROWS_AVG || mode == ROWS_INIT2);
     if (mode == ROWS_STEP && S.P.split_h > 0 && G == 1 && S.P.m > 0)
-      MPAX_LAUNCH(k_rows_left, blocks_for(S.P.m), kB, 0, E.s, S.st, S.P.m, S.P, S.V.xp, S.V.tmp);
-    SH_MODE_LAUNCH(k_rows, mode, blocks_for(S.P.m * (spmv ? G : 1)), kB, 0, E.s, S.st, S.P.m, S.P.m1, G, S.P,
-                   S.V);
+      SH_LR(k_rows_left, long_rows(S.P.max_row), blocks_for(S.P.m), kB, 0, E.s, S.st, S.P.m, S.P, S.V.xp,
+            S.V.tmp);
+    SH_MODE_LAUNCH_LR(k_rows, mode, long_rows(S.P.max_row), blocks_for(S.P.m * (spmv ? G : 1)), kB, 0, E.s, S.st,
+                      S.P.m, S.P.m1, G, S.P, S.V);
   }
   MPAX_CHECK_LAUNCH();
   return LP_OK;
@@ -931,8 +958,8 @@ int cols_spmv(ShardedLP &E, int which /*0: yp, 1: y, 2: ya*/) {
       for (auto &S : E.sh) {
         const int G = group_of(S.P.avg_col, S.P.max_col);
         const double *src = which == 0 ? S.V.yp : (which == 1 ? S.V.y : S.V.ya);
-        MPAX_LAUNCH(k_cols_spmv, blocks_for((c1 - c0) * G), kB, 0, E.s, S.st, c1 - c0, G, S.P.trp + c0, S.P.tci,
-                    S.P.tkv, src, S.V.red + c0);
+        SH_LR(k_cols_spmv, long_rows(S.P.max_col), blocks_for((c1 - c0) * G), kB, 0, E.s, S.st, c1 - c0, G,
+              S.P.trp + c0, S.P.tci, S.P.tkv, src, S.V.red + c0);
       }
       MPAX_CHECK_LAUNCH();
       MPAX_CUDA(cudaEventRecord(E.chunk_ev[c], E.s));
@@ -947,8 +974,8 @@ int cols_spmv(ShardedLP &E, int which /*0: yp, 1: y, 2: ya*/) {
   for (auto &S : E.sh) {
     const int G = group_of(S.P.avg_col, S.P.max_col);
     const double *src = which == 0 ? S.V.yp : (which == 1 ? S.V.y : S.V.ya);
-    MPAX_LAUNCH(k_cols_spmv, blocks_for(S.P.n * G), kB, 0, E.s, S.st, S.P.n, G, S.P.trp, S.P.tci, S.P.tkv, src,
-                S.V.red);
+    SH_LR(k_cols_spmv, long_rows(S.P.max_col), blocks_for(S.P.n * G), kB, 0, E.s, S.st, S.P.n, G, S.P.trp,
+          S.P.tci, S.P.tkv, src, S.V.red);
     bufs.push_back(S.V.red);
   }
   MPAX_CHECK_LAUNCH();

@@ -18,8 +18,28 @@ import paper_2412_09734_b200 as mp  # noqa: E402
 from tests.test_gpu_parity import obj_tol, oracle_stability, rel  # noqa: E402
 
 ALGS = ["ra", "r2"]
+
+
+def _long_cols(seed=9):
+    """K' of a G-POWERLAW pattern: columns of up to ~400 entries (the long-row path of the K~'y
+    SpMV), rows short; a box keeps every fixed-K trajectory bounded."""
+    p = lpgen.g_powerlaw(400, 800, 12, seed=seed)
+    K = np.zeros((p.m, p.n))
+    rows = np.repeat(np.arange(p.m), np.diff(p.row_ptr))
+    K[rows, p.col_idx] = p.val
+    KT = K.T                                                   # 800 x 400
+    rng = np.random.default_rng(seed)
+    x0 = rng.uniform(-1, 1, KT.shape[1])
+    q = KT @ x0
+    return lpgen.stack(rng.normal(size=KT.shape[1]), G=KT[:400], h=q[:400] - 1.0, A=KT[400:], b=q[400:],
+                       l=np.full(KT.shape[1], -5.0), u=np.full(KT.shape[1], 5.0))
+
+
+# "powerlaw": rows of up to 421 entries, "longcols": columns of up to ~400 -- the full-chunk
+# (long-row) path of the warp-tile SpMV on each side (the kernels' LR instantiations)
+LONG = [("powerlaw", lpgen.g_powerlaw(2000, 4000, 12, seed=9)), ("longcols", _long_cols())]
 CASES = [("C1", lpgen.g_rand(50, 100, 10, seed=1)), ("mid", lpgen.g_rand(3000, 5000, 12, seed=3)),
-         ("tiny", lpgen.tiny_spec())]
+         ("tiny", lpgen.tiny_spec())] + LONG
 
 
 def sharded(lp, alg, shards, **kw):
@@ -113,7 +133,7 @@ def test_sharded_two_pass_rows(alg, shards, name, lp, monkeypatch):
 
 # ---- column sharding (the axis chosen by min(m, n); reading 33) ----
 COL_CASES = [("C1", lpgen.g_rand(50, 100, 10, seed=1)), ("wide", lpgen.g_rand(700, 9000, 30, seed=8)),
-             ("tiny", lpgen.tiny_spec())]
+             ("tiny", lpgen.tiny_spec())] + LONG
 
 
 def sharded_cols(lp, alg, shards, axis="cols", **kw):
