@@ -307,3 +307,35 @@ def test_nccl_one_rank_columns_equals_virtual():
     b = sharded_cols(lp, "r2", 1, iteration_limit=200, eps_abs=0.0, eps_rel=0.0)
     assert a["attempts"] == b["attempts"]
     assert np.array_equal(xa, b["x"]) and np.array_equal(ya, b["y"]) and np.array_equal(la, b["lam"])
+
+
+@pytest.mark.slow
+def test_c5_sharded_full_size_sampled():
+    """C5 = G-RAND(5e6, 1e7, 20, seed 5) at its BASELINE size on the sharded engine in the launch
+    configuration `bench.py --c5-sharded` (and every N > 1 run) times: a 1-rank NCCL
+    communicator, by rows and by columns.  Iterates after K = 2 accepted r2HPDHG steps against the
+    oracle (~30 s on the host), then a full raPDHG solve to 1e-4 checked by properties."""
+    lp = lpgen.g_rand(5_000_000, 10_000_000, 20, seed=5)
+    oracle.set_threads(0)
+    ro = oracle.solve(lp, "r2", iteration_limit=2, eps_abs=0.0, eps_rel=0.0)
+    full = mp.Problem.from_lp(lp)
+    for axis in ("rows", "cols"):
+        if axis == "cols":
+            loc, kw = mp.local_cols(full, 0, lp.n).to("cuda:0"), dict(axis="cols", n_global=lp.n)
+        else:
+            loc, kw = full.to("cuda:0"), dict(m1_global=lp.m1, m2_global=lp.m2)
+        comm = mp.nccl_comm_init(1, mp.nccl_unique_id(), 0)
+        try:
+            with mp.ShardedSolver(loc, comm=comm, rank=0, nranks=1, **kw) as s:
+                rg = s.solve(algorithm="r2", iteration_limit=2, eps_abs=0.0, eps_rel=0.0)
+                x, y, _ = s.solution()
+                assert rg["attempts"] == ro["attempts"], axis
+                assert rel(x, ro["x"]) <= 1e-12 and rel(y, ro["y"]) <= 1e-12, axis
+                r = s.solve(algorithm="ra", iteration_limit=5000)
+                x, y, _ = s.solution()
+        finally:
+            mp.nccl_comm_destroy(comm)
+        del loc
+        assert r["status"] == mp.LP_OPTIMAL and r["rel_kkt"] <= 1e-4, axis
+        assert abs(r["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star)), axis
+        assert np.all(y[: lp.m1] >= 0) and np.all(x >= lp.l), axis
