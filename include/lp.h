@@ -321,8 +321,9 @@ int lp_create_sharded_virtual(const lp_problem_desc *p, int32_t shards, void *cu
  * column indices (every row, m1 / m2 global), the FULL q (m) and its c, l, u (n_local).  Row
  * norms of the preconditioner and every cross-shard sum go through ncclAllReduce.  lp_solve
  * takes x0 (this rank's n_local columns) and y0 (m); lp_get_solution returns this rank's
- * columns of x and of the reduced costs and the full y.  The constant step rule is not built
- * for column sharding (LP_ERR_UNSUPPORTED).  lp_create_sharded_virtual_axis: `shards` blocks
+ * columns of x and of the reduced costs and the full y.  The constant step rule's power
+ * iteration all-reduces K~x partials and squared norms across the column shards.
+ * lp_create_sharded_virtual_axis: `shards` blocks
  * of rows or columns (balanced by nnz; LP_SHARD_AUTO picks lp_shard_axis) on the current
  * device with the fixed-order device sum; x, y and the reduced costs then cover the whole LP. */
 enum lp_shard_axis { LP_SHARD_ROWS = 0, LP_SHARD_COLS = 1, LP_SHARD_AUTO = 2 };

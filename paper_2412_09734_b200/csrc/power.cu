@@ -281,6 +281,7 @@ int launch_power_reg(const DevProblem &P, cudaStream_t s) {
 struct PowerWs {
   double part[kPBlocks];
   double norm;      // ||.|| of the last reduced vector
+  double ss;        // column shards: this shard's sum of squares, then (reduced) the total
   int done;         // a zero w was met: sigma fixed at 0
   unsigned count;   // last-block counter
 };
@@ -316,6 +317,47 @@ __global__ void __launch_bounds__(kPT) pw_norm(int64_t n, const double *__restri
       if (nrm > 0.0) *sigma_out = sqrt(nrm);
       else { *sigma_out = 0.0; ws->done = 1; }
     }
+  }
+}
+
+// ---- column shards (sharded.cu): v_g = columns [off, off + n) of v, u = sum_g K~_{:,g} v_g is
+// reduced across shards, w_g = K~_{:,g}' u, and ||w||^2 = sum_g ||w_g||^2 ----
+__global__ void pw_start_off(int64_t n, int64_t off, double *__restrict__ v) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    v[j] = start_entry(off + j);   // the unsharded start vector's entries
+}
+
+// ws->ss = sum_j a_j^2 over this shard (per block, then the blocks in order: fixed order)
+__global__ void __launch_bounds__(kPT) pw_sumsq(int64_t n, const double *__restrict__ a, PowerWs *ws) {
+  __shared__ double red[33];
+  __shared__ bool last;
+  if (ws->done) return;
+  double ss = 0.0;
+  for (int64_t j = blockIdx.x * (int64_t)kPT + threadIdx.x; j < n; j += (int64_t)kPBlocks * kPT) ss += a[j] * a[j];
+  ss = block_sum(ss, red);
+  if (threadIdx.x == 0) {
+    ws->part[blockIdx.x] = ss;
+    __threadfence();
+    last = atomicInc(&ws->count, kPBlocks - 1) == kPBlocks - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < kPBlocks; ++b) t += ((volatile double *)ws->part)[b];
+    ws->ss = t;
+  }
+}
+
+// after the cross-shard sum of ws->ss: ||.|| and, with sigma_out, the iteration step (as pw_norm)
+__global__ void pw_finish(PowerWs *ws, double *sigma_out) {
+  if (ws->done) return;
+  const double nrm = sqrt(ws->ss);
+  ws->norm = nrm;
+  if (sigma_out) {
+    if (nrm > 0.0) *sigma_out = sqrt(nrm);
+    else { *sigma_out = 0.0; ws->done = 1; }
   }
 }
 
@@ -376,6 +418,46 @@ int power_normalize(PowerState &S, double *sigma_out, cudaStream_t s) {
   PowerWs *ws = (PowerWs *)S.ws;
   MPAX_LAUNCH(pw_norm, kPBlocks, kPT, 0, s, S.n, S.w, ws, sigma_out);
   MPAX_LAUNCH(pw_scale, blocks_for(S.n), 256, 0, s, S.n, S.v, S.w, ws);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+int power_begin_cols(PowerState &S, int64_t n, int64_t m, int64_t off, cudaStream_t s) {
+  S.n = n; S.m = m;
+  const size_t vb = (size_t)(2 * n + (m > 0 ? m : 1)) * sizeof(double);
+  MPAX_CUDA(cudaMallocAsync((void **)&S.buf, vb + sizeof(PowerWs), s));
+  S.v = (double *)S.buf; S.w = S.v + n; S.u = S.w + n;
+  S.ws = S.buf + vb;
+  MPAX_CUDA(cudaMemsetAsync(S.ws, 0, sizeof(PowerWs), s));
+  MPAX_LAUNCH(pw_start_off, blocks_for(n), 256, 0, s, n, off, S.v);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+int power_kv(const DevProblem &P, PowerState &S, cudaStream_t s) {
+  MPAX_LAUNCH(pw_spmv, blocks_for(S.m * 32), 256, 0, s, S.m, P.rp, P.ci, P.kv, S.v, S.u, (const PowerWs *)S.ws);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+int power_ktu(const DevProblem &P, PowerState &S, cudaStream_t s) {
+  MPAX_LAUNCH(pw_spmv, blocks_for(S.n * 32), 256, 0, s, S.n, P.trp, P.tci, P.tkv, S.u, S.w, (const PowerWs *)S.ws);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+int power_sumsq(PowerState &S, const double *a, cudaStream_t s) {
+  MPAX_LAUNCH(pw_sumsq, kPBlocks, kPT, 0, s, S.n, a, (PowerWs *)S.ws);
+  MPAX_CHECK_LAUNCH();
+  return LP_OK;
+}
+
+double *power_ss(PowerState &S) { return &((PowerWs *)S.ws)->ss; }
+
+int power_finish(PowerState &S, const double *a, double *sigma_out, cudaStream_t s) {
+  PowerWs *ws = (PowerWs *)S.ws;
+  MPAX_LAUNCH(pw_finish, 1, 1, 0, s, ws, sigma_out);
+  MPAX_LAUNCH(pw_scale, blocks_for(S.n), 256, 0, s, S.n, S.v, a, ws);
   MPAX_CHECK_LAUNCH();
   return LP_OK;
 }

@@ -988,14 +988,44 @@ int cols_spmv(ShardedLP &E, int which /*0: yp, 1: y, 2: ya*/) {
 
 namespace {
 
+// sigma_max(K~) of the column-sharded K~ (power.cu): v_g holds this shard's columns of the
+// unsharded start vector; u = sum_g K~_{:,g} v_g reduced across shards (m-long), w_g = K~_{:,g}' u
+// local, ||w||^2 = sum_g ||w_g||^2 reduced across shards, v_g = w_g / ||w||.
+int sharded_power_cols(ShardedLP &E) {
+  cudaStream_t s = E.s;
+  std::vector<PowerState> ps(E.sh.size());
+  for (size_t g = 0; g < E.sh.size(); ++g)
+    STRY(power_begin_cols(ps[g], E.sh[g].P.n, E.sh[g].P.m, E.sh[g].row_offset, s));
+  auto normalise = [&](bool from_w, bool sigma) -> int {
+    std::vector<double *> ss;
+    for (size_t g = 0; g < E.sh.size(); ++g) {
+      STRY(power_sumsq(ps[g], from_w ? ps[g].w : ps[g].v, s));
+      ss.push_back(power_ss(ps[g]));
+    }
+    STRY(reduce_vec(E, 19, ss, 1, false));
+    for (size_t g = 0; g < E.sh.size(); ++g)
+      STRY(power_finish(ps[g], from_w ? ps[g].w : ps[g].v, sigma ? E.sh[g].P.sigma : nullptr, s));
+    return LP_OK;
+  };
+  STRY(normalise(false, false));
+  std::vector<double *> us;
+  for (auto &p : ps) us.push_back(p.u);
+  for (int t = 0; t < kPowerIters; ++t) {
+    for (size_t g = 0; g < E.sh.size(); ++g) STRY(power_kv(E.sh[g].P, ps[g], s));
+    STRY(reduce_vec(E, 18, us, E.sh[0].P.m, false));
+    for (size_t g = 0; g < E.sh.size(); ++g) STRY(power_ktu(E.sh[g].P, ps[g], s));
+    STRY(normalise(true, true));
+  }
+  for (auto &p : ps) STRY(power_end(p, s));
+  E.sigma_ready = true;
+  return LP_OK;
+}
+
 // sigma_max(K~) of the row-sharded K~ (power.cu): u_g = K~_g v on each shard's rows,
 // w = sum_g K~_g' u_g reduced across shards, then the replicated normalisation.
 int sharded_power(ShardedLP &E) {
   cudaStream_t s = E.s;
-  if (E.cols) {
-    set_error_detail("the constant step rule is not built for column-sharded LPs");
-    return LP_ERR_UNSUPPORTED;
-  }
+  if (E.cols) return sharded_power_cols(E);
   std::vector<PowerState> ps(E.sh.size());
   for (size_t g = 0; g < E.sh.size(); ++g) STRY(power_begin(ps[g], E.n, E.sh[g].P.m, s));
   std::vector<double *> ws;

@@ -179,6 +179,45 @@ def test_constant_step_dmma_path(alg):
 
 
 @pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("shards", [1, 2, 4])
+def test_constant_step_column_shards(alg, shards):
+    """Column shards (reading 33): the power iteration on K~ split by columns -- each shard's
+    slice of the unsharded start vector, K~x partials summed across shards, ||w||^2 summed across
+    shards -- gives the oracle's step size to 1e-12 and its fixed-K trajectory."""
+    lp = lpgen.g_rand(700, 9000, 30, seed=8)
+    kw = dict(eps_abs=0.0, eps_rel=0.0, iteration_limit=64, **CONST)
+    ro, stable, drift = oracle_stability(lp, alg, **kw)
+    with mp.ShardedSolver(mp.Problem.from_lp(lp), virtual_shards=shards, axis="cols") as s:
+        r = s.solve(algorithm=alg, **kw)
+        x, y, _ = s.solution()
+        assert abs(r["eta"] - oracle_eta(lp)) <= 1e-12 * oracle_eta(lp)
+        if not stable:
+            pytest.skip("ill-conditioned at this K: the oracle's own counts move under a 1-ulp perturbation")
+        assert r["attempts"] == ro["attempts"] and r["restarts"] == ro["restarts"]
+        tol = max(1e-9, 100 * drift)
+        assert rel(x, ro["x"]) <= tol and rel(y, ro["y"]) <= tol
+        r = s.solve(algorithm=alg, **CONST)
+        assert r["status"] == mp.LP_OPTIMAL and r["rel_kkt"] <= 1e-4
+        assert abs(r["primal_objective"] - lp.obj_star) <= 1e-3 * (1 + abs(lp.obj_star))
+
+
+def test_constant_step_column_shards_nccl_one_rank():
+    lp = lpgen.g_rand(700, 9000, 30, seed=8)
+    comm = mp.nccl_comm_init(1, mp.nccl_unique_id(), 0)
+    try:
+        with mp.ShardedSolver(mp.local_cols(mp.Problem.from_lp(lp), 0, lp.n), axis="cols", n_global=lp.n,
+                              comm=comm, rank=0, nranks=1) as s:
+            a = s.solve(algorithm="r2", eps_abs=0.0, eps_rel=0.0, iteration_limit=64, **CONST)
+            xa, _, _ = s.solution()
+    finally:
+        mp.nccl_comm_destroy(comm)
+    with mp.ShardedSolver(mp.Problem.from_lp(lp), virtual_shards=1, axis="cols") as s:
+        b = s.solve(algorithm="r2", eps_abs=0.0, eps_rel=0.0, iteration_limit=64, **CONST)
+        xb, _, _ = s.solution()
+    assert a["eta"] == b["eta"] and a["attempts"] == b["attempts"] and np.array_equal(xa, xb)
+
+
+@pytest.mark.parametrize("alg", ALGS)
 @pytest.mark.parametrize("shards", [1, 3])
 def test_constant_step_sharded(alg, shards):
     lp = lpgen.g_rand(3000, 5000, 12, seed=3)
