@@ -283,11 +283,11 @@ int lp_get_scaling(lp_handle h, double *Dr, double *Dc, int32_t memory);
  * records as the oracle's ora_log.  Rows past the capacity are dropped; rows not reached are
  * left untouched.  The buffers must be device-accessible (device or mapped pinned memory) and
  * stay valid through every later lp_solve on the handle; NULL / capacity 0 switches a log off.
- * Recorded by the grid path (one LP) and by the register kernel of the small-LP batches (the C2
- * shapes: m <= 32, n <= 64, rows <= 4 and columns <= 4 entries), which logs ONE instance,
- * `instance` of lp_set_decision_log_instance (default 0); any other path returns
- * LP_ERR_UNSUPPORTED while a log is set (sharded handles: always).  Polishing sub-solves are not
- * logged.  Logging does not change any result. */
+ * Recorded by the grid path (one LP), by the sharded engines (every rank records the same,
+ * replicated decisions) and by the register kernel of the small-LP batches (the C2 shapes:
+ * m <= 32, n <= 64, rows <= 4 and columns <= 4 entries), which logs ONE instance, `instance` of
+ * lp_set_decision_log_instance (default 0); any other path returns LP_ERR_UNSUPPORTED while a
+ * log is set.  Polishing sub-solves are not logged.  Logging does not change any result. */
 int lp_set_decision_log(lp_handle h, double *att, int64_t att_cap, double *chk, int64_t chk_cap);
 int lp_set_decision_log_instance(lp_handle h, int64_t instance);
 

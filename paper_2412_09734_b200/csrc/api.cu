@@ -830,12 +830,12 @@ int lp_set_decision_log_instance(lp_handle h, int64_t instance) {
 
 int lp_set_decision_log(lp_handle h, double *att, int64_t att_cap, double *chk, int64_t chk_cap) {
   if (!h) return fail(LP_ERR_INVALID_ARGUMENT, "NULL handle");
-  if (h->sharded) return fail(LP_ERR_UNSUPPORTED, "the decision log is not recorded by the sharded engine");
   if ((att && att_cap < 0) || (chk && chk_cap < 0)) return fail(LP_ERR_INVALID_ARGUMENT, "negative capacity");
   h->alog = att_cap > 0 ? att : nullptr;
   h->acap = att_cap > 0 ? att_cap : 0;
   h->clog = chk_cap > 0 ? chk : nullptr;
   h->ccap = chk_cap > 0 ? chk_cap : 0;
+  if (h->sharded) sharded_set_log(h->sharded, h->alog, h->acap, h->clog, h->ccap);
   return LP_OK;
 }
 

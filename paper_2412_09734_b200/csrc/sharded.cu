@@ -62,6 +62,7 @@ struct ShState {
   double certc[6], certr[6];
   double ray_ny, ray_nx;
   double rho;  // r2HPDHG reflection parameter (reading 38)
+  long long nchk;  // checks taken (the decision log's row index)
   unsigned int cnt_cols, cnt_rows;
 };
 
@@ -422,7 +423,9 @@ __global__ void k_init_decide(ShState *st, int stage) {
   }
 }
 
-__global__ void k_decide(ShState *st, const double *tab, int64_t check_freq, int64_t iter_limit) {
+// alog (one shard, or null): the decision log's attempt rows (j, accepted, eta, eta_bar), lp.h
+__global__ void k_decide(ShState *st, const double *tab, int64_t check_freq, int64_t iter_limit, double *alog,
+                         int64_t acap) {
   if (st->halt) return;
   st->j += 1;
   double f1 = 0.0, f2 = 0.0;
@@ -432,6 +435,10 @@ __global__ void k_decide(ShState *st, const double *tab, int64_t check_freq, int
   const double eb = (I != 0.0) ? M / (2.0 * fabs(I)) : INFINITY;
   const bool acc = st->cstep || st->eta <= eb;  // constant step rule: DESIGN.md reading 34
   const double eta_used = st->eta;
+  if (alog && st->j <= acap) {
+    double *r = alog + 4 * (st->j - 1);
+    r[0] = (double)st->j; r[1] = acc ? 1.0 : 0.0; r[2] = eta_used; r[3] = eb;
+  }
   if (!st->cstep) st->eta = fmin(f1 * eb, f2 * st->eta);
   if (!acc) {
     st->pending = 0;
@@ -456,7 +463,15 @@ __global__ void k_decide(ShState *st, const double *tab, int64_t check_freq, int
 
 __global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, double eps_pi, double eps_di,
                                int64_t iter_limit, int verbose, int display_freq, int64_t check_freq,
-                               int polish_mode, double eps_fp) {
+                               int polish_mode, double eps_fp, double *clog, int64_t ccap) {
+  // the decision log's check rows (k, metric, ref, last, restart, outcome), lp.h
+  auto log_check = [&](double metric_, int restart_, int outcome) {
+    if (clog && st->nchk < ccap) {
+      double *r = clog + 6 * st->nchk;
+      r[0] = (double)st->k; r[1] = metric_; r[2] = st->ref; r[3] = st->last; r[4] = restart_; r[5] = outcome;
+    }
+    st->nchk += 1;
+  };
   // the check's pass test: relative KKT, or a polishing sub-solve's single residual (reading 36)
   auto tpass = [&](const Kkt5 &k) {
     return polish_mode ? polish_pass(polish_mode, k.pres, k.dres, st->nq0, st->nc0, eps_fp)
@@ -478,12 +493,17 @@ __global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, doub
     const Kkt5 kw = kkt5(t);
     if (verbose_due(verbose, display_freq, st->k, check_freq))
       verbose_line(0, st->k, kw.pobj, kw.dobj, kw.pres, kw.dres, kw.gap, st->omega, st->eta);
-    if (tpass(kw)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
+    if (tpass(kw)) { log_check(st->rP, 0, 1); st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
     if (cert) {
+      log_check(0.0, 0, 3);
       st->status = cert; st->halt = 1; st->outsel = 0; st->rays = 1; st->ray_ny = ny; st->ray_nx = nx;
       return;
     }
-    if (st->k == iter_limit) { st->status = LP_ITERATION_LIMIT; st->halt = 1; st->outsel = 1; return; }
+    if (st->k == iter_limit) {
+      log_check(st->rP, 0, 0);
+      st->status = LP_ITERATION_LIMIT; st->halt = 1; st->outsel = 1;
+      return;
+    }
     st->metric = st->rP;
     st->csel = 1;
     st->colsum[22] = t[4];
@@ -492,13 +512,15 @@ __global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, doub
     const Kkt5 ka = kkt5(t + 0), kc = kkt5(t + 4);
     if (verbose_due(verbose, display_freq, st->k, check_freq))
       verbose_line(0, st->k, kc.pobj, kc.dobj, kc.pres, kc.dres, kc.gap, st->omega, st->eta);
-    if (tpass(ka)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
-    if (tpass(kc)) { st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 0; return; }
+    if (tpass(ka)) { log_check(0.0, 0, 1); st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 1; return; }
+    if (tpass(kc)) { log_check(0.0, 0, 2); st->status = LP_OPTIMAL; st->halt = 1; st->outsel = 0; return; }
     if (cert) {
+      log_check(0.0, 0, 3);
       st->status = cert; st->halt = 1; st->outsel = 0; st->rays = 1; st->ray_ny = ny; st->ray_nx = nx;
       return;
     }
     if (st->k == iter_limit) {
+      log_check(0.0, 0, 0);
       st->status = LP_ITERATION_LIMIT; st->halt = 1;
       st->outsel = kkt5_rel(ka, nq0, nc0) < kkt5_rel(kc, nq0, nc0) ? 1 : 0;
       return;
@@ -511,6 +533,7 @@ __global__ void k_check_decide(ShState *st, double eps_abs, double eps_rel, doub
   }
   const double metric = st->metric;
   const bool restart = restart_due(st->k_in, st->k, metric, st->ref, st->last);
+  log_check(metric, restart ? 1 : 0, 0);
   st->last = metric;
   if (restart) {
     st->restart = 1;
@@ -600,6 +623,8 @@ struct ShardedLP {
   lp_result *d_res = nullptr, *h_res = nullptr;
   int *d_flags = nullptr, *h_flags = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double *alog = nullptr, *clog = nullptr;   // decision log of the main solve (lp_set_decision_log)
+  int64_t acap = 0, ccap = 0;
   bool solved = false;
   bool sigma_ready = false;  // sigma_max(K~) computed into every shard's P.sigma
   int polish_mode = 0;       // the running solve is a polishing sub-solve (reading 36): 1 primal, 2 dual
@@ -1092,7 +1117,9 @@ int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const dou
       STRY(launch_cols(E, COLS_STEP));
       STRY(launch_rows(E, ROWS_STEP));
       STRY(reduce_rowsum(E, 3));
-      for (auto &S : E.sh) MPAX_LAUNCH(k_decide, 1, 1, 0, s, S.st, S.P.tab, F, LIM);
+      for (size_t g = 0; g < E.sh.size(); ++g)
+        MPAX_LAUNCH(k_decide, 1, 1, 0, s, E.sh[g].st, E.sh[g].P.tab, F, LIM, g == 0 ? E.alog : nullptr,
+                    (int64_t)E.acap);
     }
     MPAX_CHECK_LAUNCH();
     return LP_OK;
@@ -1195,7 +1222,8 @@ int sharded_solve(ShardedLP &E, const lp_options &o, const double *X0, const dou
     for (size_t g = 0; g < E.sh.size(); ++g)
       MPAX_LAUNCH(k_check_decide, 1, 1, 0, s, E.sh[g].st, o.eps_abs, o.eps_rel, o.eps_primal_infeasible,
                   o.eps_dual_infeasible, LIM, (g == 0 && E.rank == 0) ? o.verbose : 0, o.display_frequency,
-                  (int64_t)o.check_frequency, E.polish_mode, o.eps_feas_polish);
+                  (int64_t)o.check_frequency, E.polish_mode, o.eps_feas_polish, g == 0 ? E.clog : nullptr,
+                  (int64_t)E.ccap);
     for (auto &S : E.sh)
       MPAX_LAUNCH(k_restart, blocks_for(S.j1 - S.j0 > S.P.m ? S.j1 - S.j0 : S.P.m), kB, 0, s, S.st, S.j0, S.j1, S.P.m,
                   S.V);
@@ -1297,6 +1325,11 @@ int sharded_solve_polished(ShardedLP &E, const lp_options &o, const double *X0, 
   om.feasibility_polishing = 0;
   STRY(sharded_solve(E, om, X0, Y0, out));
   if (!o.feasibility_polishing || out->status != LP_OPTIMAL) return LP_OK;
+  struct LogOff {   // the polishing sub-solves are not logged (lp.h)
+    ShardedLP &E; double *a, *c;
+    explicit LogOff(ShardedLP &e) : E(e), a(e.alog), c(e.clog) { E.alog = nullptr; E.clog = nullptr; }
+    ~LogOff() { E.alog = a; E.clog = c; }
+  } log_off(E);
   cudaStream_t s = E.s;
   const int64_t n = E.n;
   int64_t mtot = 0;
@@ -1469,6 +1502,10 @@ int64_t sharded_m_local(const ShardedLP *E) {
 }
 
 // Create: `descs` are this process's row shards (one per GPU rank, p for virtual mode).
+void sharded_set_log(ShardedLP *E, double *alog, int64_t acap, double *clog, int64_t ccap) {
+  E->alog = alog; E->acap = acap; E->clog = clog; E->ccap = ccap;
+}
+
 int sharded_create(ShardedLP *E, const std::vector<lp_problem_desc> &descs, const std::vector<int64_t> &offsets,
                    int64_t n, int64_t m1g, int64_t m2g, void *comm, int rank, int nranks, bool virt, bool cols) {
   E->n = n; E->m1_global = m1g; E->m_global = m1g + m2g;

@@ -231,3 +231,42 @@ def test_step_factors_past_the_table():
     sel = (j >= 65520) & (j <= 65560)   # across the table's end
     assert sel.sum() >= 40
     np.testing.assert_allclose(att[1:, 2][sel], want[sel], rtol=1e-14)
+
+
+# ---- the sharded engines (row and column shards, reading 33) ----
+SHARDED_CASES = [("C1", lpgen.g_rand(50, 100, 10, seed=1)), ("mid", lpgen.g_rand(3000, 5000, 12, seed=3)),
+                 ("wide", lpgen.g_rand(700, 9000, 30, seed=8))]
+
+
+@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("axis,shards", [("rows", 1), ("rows", 3), ("cols", 2)])
+@pytest.mark.parametrize("name,lp", SHARDED_CASES)
+def test_sharded_decision_log_matches_oracle(alg, axis, shards, name, lp):
+    """The sharded engine's decisions (taken redundantly on every shard from the reduced partials)
+    against the oracle's log, by the same criteria as the grid path's."""
+    ro = oracle.solve(lp, alg, log_capacity=20000)
+    with mp.ShardedSolver(mp.Problem.from_lp(lp), virtual_shards=shards, axis=axis) as s:
+        s.set_decision_log(att_cap=20000, chk_cap=1000)
+        rg = s.solve(algorithm=alg)
+        att, chk = s.decision_log()
+        # a second solve rewrites the log from its first row (the counters restart per solve)
+        rg2 = s.solve(algorithm=alg)
+        att2, chk2 = s.decision_log()
+        assert rg2["attempts"] == rg["attempts"]
+        assert np.array_equal(att, att2) and np.array_equal(chk, chk2)
+    assert len(att) == rg["attempts"] and len(chk) >= 1
+    parity_log(f"decision_log_sharded[{name},{alg},{axis}{shards}]",
+               **compare_logs(lp, alg, rg, att, chk, ro, f"{name}/{axis}{shards}"))
+
+
+def test_sharded_decision_log_skips_polishing():
+    lp = lpgen.g_rand(50, 100, 10, seed=1)
+    with mp.ShardedSolver(mp.Problem.from_lp(lp), virtual_shards=2) as s:
+        s.set_decision_log(att_cap=20000, chk_cap=1000)
+        r = s.solve(algorithm="ra", eps_abs=1e-2, eps_rel=1e-2, feasibility_polishing=1)
+        att, chk = s.decision_log()
+        ro = s.solve(algorithm="ra", eps_abs=1e-2, eps_rel=1e-2)
+        att2, chk2 = s.decision_log()
+    # the logged rows are the main solve's only: the same as a solve without polishing
+    assert r["status"] == ro["status"] == mp.LP_OPTIMAL
+    assert np.array_equal(att, att2) and np.array_equal(chk, chk2)
