@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-spo", action="store_true", help="skip the SPO+ (Warcraft-shaped) leg")
     ap.add_argument("--c5-sharded", action="store_true",
                     help="run the C5 leg on the row-sharded NCCL engine even at one rank (it is used for N > 1)")
+    ap.add_argument("--no-c5-sharded", action="store_true",
+                    help="at one rank, skip the sharded-engine C5 run that follows the grid-path C5 leg")
     ap.add_argument("--c5-axis", default="auto", choices=["rows", "cols", "auto"],
                     help="sharding axis of the C5 sharded leg; auto = the axis whose exchanged vector is "
                          "shorter (lp_shard_axis, DESIGN reading 33): columns for C5 (m < n)")
@@ -412,6 +414,12 @@ def run_ours(args):
         log("large-LP leg (C5, 1e8 nnz)")
         line["c5"] = large_lp_leg(mp, torch, dev, stream, peaks, args, m=5_000_000, seed=5, label="C5", reps=1,
                                   cpu=not args.no_cpu_baseline)
+        if not args.no_c5_sharded:   # the multi-GPU engine on the same LP at one NCCL rank (context)
+            log(f"large-LP leg (C5) on the sharded engine, one rank (axis {args.c5_axis})")
+            try:
+                line["c5_sharded"] = c5_sharded_leg(mp, torch, dev, 1, 0, args)
+            except Exception as e:
+                line["c5_sharded"] = {"error": f"{type(e).__name__}: {e}"[:400]}
     if not args.no_dense:
         log("dense shared-K leg (C3)")
         line["dense_batch"] = dense_leg(mp, torch, dev, peaks, args.no_cpu_baseline or rank != 0)

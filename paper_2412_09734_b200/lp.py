@@ -362,7 +362,7 @@ class Solver:
         return x, y, lam
 
     def set_decision_log(self, att_cap=4096, chk_cap=256, device=None):
-        """Record the grid path's decisions (lp_set_decision_log) into device buffers of the given
+        """Record the grid path's or the sharded engine's decisions (lp_set_decision_log) into device buffers of the given
         capacities (NaN-filled before every solve); decision_log() returns the rows written.
         att_cap = 0 and chk_cap = 0 switch it off."""
         import torch
