@@ -304,6 +304,20 @@ __global__ void k_rows_left(const ShState *st, int64_t m, const DevProblem P, co
   }
 }
 
+// pass 2 in column mode: V.tmp += K~_R x' (the sum order of the rows step's pass 2: left + right)
+template <bool LR>
+__global__ void k_rows_right_add(const ShState *st, int64_t m, const DevProblem P, const double *x, double *tmp) {
+  if (st->halt) return;
+  __shared__ double s_tile[kB / 32][kTileBuf];
+  const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x, nthr = (int64_t)gridDim.x * kB;
+  for (int64_t base = gt - (threadIdx.x & 31); base < m; base += nthr) {
+    const int64_t r = base + (threadIdx.x & 31);
+    const double v = tile_row_dot<double, double, LR>((int)r, r < m, (int)m, P.rpR, P.ciR, P.kvR, x,
+                                                       s_tile[threadIdx.x >> 5]);
+    if (r < m) tmp[r] = tmp[r] + v;
+  }
+}
+
 template <int MODE, bool LR>
 __global__ void k_rows(ShState *st, int64_t m, int64_t m1, int G, const DevProblem P, const Vecs V) {
   constexpr int mode = MODE;
@@ -874,9 +888,10 @@ int sharded_setup(ShardedLP &E, const std::vector<lp_problem_desc> &descs, const
     MPAX_CUDA(cudaFreeAsync(gam[g], s));
   }
   MPAX_CUDA(cudaFreeAsync(noflag, s));
-  // column halves of each K~_g for the two-pass rows step (grid_solver.cu grid_split_prepare:
-  // x' is replicated, so its 8n bytes are the gather target at every p)
-  if (!E.cols) for (int g = 0; g < p; ++g) STRY(grid_split_prepare(E.sh[g].P, s));
+  // column halves of each K~_g for the two-pass rows-side SpMV (grid_solver.cu grid_split_prepare):
+  // the gather target is x' -- replicated in row mode (8n bytes at every p), this shard's
+  // columns in column mode (8 n_local bytes: past the L2 knee only at small p)
+  for (int g = 0; g < p; ++g) STRY(grid_split_prepare(E.sh[g].P, s));
   MPAX_CUDA(cudaStreamSynchronize(s));
   return LP_OK;
 }
@@ -943,8 +958,14 @@ int launch_rows(ShardedLP &E, int mode) {
     for (auto &S : E.sh) {
       const int G = group_of(S.P.avg_row, S.P.max_row);
       const double *src = mode == ROWS_AVG ? S.V.xa : (mode == ROWS_INIT2 ? S.V.x : S.V.xp);
-      SH_LR(k_cols_spmv, long_rows(S.P.max_row), blocks_for(S.P.m * G), kB, 0, E.s, S.st, S.P.m, G, S.P.rp,
-            S.P.ci, S.P.kv, src, S.V.tmp);
+      const bool lr = long_rows(S.P.max_row);
+      if (S.P.split_h > 0 && G == 1 && S.P.m > 0) {   // column halves (past the L2 knee): two passes
+        SH_LR(k_rows_left, lr, blocks_for(S.P.m), kB, 0, E.s, S.st, S.P.m, S.P, src, S.V.tmp);
+        SH_LR(k_rows_right_add, lr, blocks_for(S.P.m), kB, 0, E.s, S.st, S.P.m, S.P, src, S.V.tmp);
+      } else {
+        SH_LR(k_cols_spmv, lr, blocks_for(S.P.m * G), kB, 0, E.s, S.st, S.P.m, G, S.P.rp, S.P.ci, S.P.kv, src,
+              S.V.tmp);
+      }
       bufs.push_back(S.V.tmp);
     }
     MPAX_CHECK_LAUNCH();

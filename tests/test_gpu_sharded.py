@@ -145,6 +145,23 @@ def sharded_cols(lp, alg, shards, axis="cols", **kw):
 
 
 @pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("shards", [1, 2])
+@pytest.mark.parametrize("name,lp", COL_CASES[:2] + LONG)
+def test_sharded_two_pass_cols(alg, shards, name, lp, monkeypatch):
+    """Column mode's K~_g x'_g over the column halves of each shard (forced on; by default only
+    past the L2 gather knee) against the oracle at fixed K."""
+    monkeypatch.setenv("MPAX_GRID_SPLIT", "1")
+    ro, stable, drift = oracle_stability(lp, alg, eps_abs=0.0, eps_rel=0.0, iteration_limit=64)
+    rg = sharded_cols(lp, alg, shards, eps_abs=0.0, eps_rel=0.0, iteration_limit=64)
+    if not stable:
+        pytest.skip("ill-conditioned at this K")
+    tol = max(1e-9, 100 * drift)
+    for key in ("status", "iterations", "attempts", "restarts"):
+        assert rg[key] == ro[key], (key, rg[key], ro[key])
+    assert rel(rg["x"], ro["x"]) <= tol and rel(rg["y"], ro["y"]) <= tol
+
+
+@pytest.mark.parametrize("alg", ALGS)
 @pytest.mark.parametrize("K", [1, 2, 64])
 @pytest.mark.parametrize("shards", [1, 2, 3])
 @pytest.mark.parametrize("name,lp", COL_CASES)
