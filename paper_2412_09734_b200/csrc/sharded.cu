@@ -318,8 +318,15 @@ __global__ void k_rows_right_add(const ShState *st, int64_t m, const DevProblem 
   }
 }
 
+// four resident CTAs per SM (<= 64 registers; the gathers want the warps): C5 by rows at one
+// rank 1.419 -> 1.377 ms per attempt, by columns 1.403 -> 1.384 (3 CTAs: 1.394 / 1.404;
+// scripts/gpu_ab_sharded_rows.sh)
+#ifndef MPAX_SH_ROWS_MINB
+#define MPAX_SH_ROWS_MINB 4
+#endif
+#define SH_ROWS_BOUNDS __launch_bounds__(kB, MPAX_SH_ROWS_MINB)
 template <int MODE, bool LR>
-__global__ void k_rows(ShState *st, int64_t m, int64_t m1, int G, const DevProblem P, const Vecs V) {
+__global__ void SH_ROWS_BOUNDS k_rows(ShState *st, int64_t m, int64_t m1, int G, const DevProblem P, const Vecs V) {
   constexpr int mode = MODE;
   if (st->halt && mode != ROWS_OUT) return;
   const bool r2 = st->r2, pend = st->pending;
