@@ -175,8 +175,13 @@ inline int blocks_for(int64_t work) {
 
 // ------------------------------------------------------------------ kernels --
 
+#ifdef MPAX_SH_SPMV_MINB   // experiments: resident CTAs per SM for the K~'y SpMV
+#define SH_SPMV_BOUNDS __launch_bounds__(kB, MPAX_SH_SPMV_MINB)
+#else
+#define SH_SPMV_BOUNDS
+#endif
 template <bool LR>
-__global__ void k_cols_spmv(const ShState *st, int64_t n, int G, const int32_t *trp, const int32_t *tci,
+__global__ void SH_SPMV_BOUNDS k_cols_spmv(const ShState *st, int64_t n, int G, const int32_t *trp, const int32_t *tci,
                             const double *tkv, const double *ysrc, double *out) {
   if (st->halt) return;
   __shared__ double s_tile[kB / 32][kTileBuf];
