@@ -200,8 +200,13 @@ enum { ROWS_STEP = 0, ROWS_COMMIT_ONLY = 1, ROWS_AVG = 2, ROWS_INIT = 3, ROWS_IN
 
 // MODE is a template parameter: each instantiation keeps only its own branch (fewer registers,
 // no per-element mode tests), the per-element arithmetic is unchanged.
+#ifdef MPAX_SH_COLS_MINB   // experiments: resident CTAs per SM for the column-side step kernels
+#define SH_COLS_BOUNDS __launch_bounds__(kB, MPAX_SH_COLS_MINB)
+#else
+#define SH_COLS_BOUNDS
+#endif
 template <int MODE>
-__global__ void k_cols(ShState *st, int64_t j0, int64_t n, const DevProblem P, const Vecs V) {
+__global__ void SH_COLS_BOUNDS k_cols(ShState *st, int64_t j0, int64_t n, const DevProblem P, const Vecs V) {
   constexpr int mode = MODE;
   if (st->halt && mode != COLS_OUT) return;
   const bool r2 = st->r2, pend = st->pending;
@@ -296,8 +301,13 @@ __global__ void k_cols(ShState *st, int64_t j0, int64_t n, const DevProblem P, c
 }
 
 // pass 1 of the two-pass rows step: V.tmp = K~_L x' (warp-tile mapping, same order as the grid kernel)
+#ifdef MPAX_SH_LEFT_MINB   // experiments: resident CTAs per SM for pass 1 of the rows-side SpMV
+#define SH_LEFT_BOUNDS __launch_bounds__(kB, MPAX_SH_LEFT_MINB)
+#else
+#define SH_LEFT_BOUNDS
+#endif
 template <bool LR>
-__global__ void k_rows_left(const ShState *st, int64_t m, const DevProblem P, const double *x, double *tmp) {
+__global__ void SH_LEFT_BOUNDS k_rows_left(const ShState *st, int64_t m, const DevProblem P, const double *x, double *tmp) {
   if (st->halt) return;
   __shared__ double s_tile[kB / 32][kTileBuf];
   const int64_t gt = blockIdx.x * (int64_t)kB + threadIdx.x, nthr = (int64_t)gridDim.x * kB;
